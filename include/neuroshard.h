@@ -1,0 +1,212 @@
+/*
+ * neuroshard.h -- C ABI of the B200-native NeuroShard plan-scoring hot path.
+ *
+ * NeuroShard ("Pre-train and Search: Efficient Embedding Table Sharding with
+ * Pre-trained Neural Cost Models", arXiv 2305.01868) shards embedding tables
+ * over D GPUs by searching column-wise splits (beam search, Alg. 1) and
+ * table-wise placements (greedy grid search, Alg. 2) against pre-trained
+ * neural cost models used as a simulator.  Citations "P:n" are lines of the
+ * paper text; "Rk" are the readings of ambiguous passages listed
+ * in DESIGN.md.
+ *
+ * Conventions (all calls)
+ *  - Every call returns an ns_status.  Negative = error: outputs are left
+ *    untouched and ns_last_error(ctx) holds a message (ctx-owned string, valid
+ *    until the next call on that ctx).  NS_INFEASIBLE (> 0) is data, not an
+ *    error ("-" = memory explosion).
+ *  - Ownership: the caller owns every array it passes; the library copies
+ *    what it keeps and never frees caller memory.  Handles (ns_ctx,
+ *    ns_tables) are library-owned until their destroy/free call.
+ *  - Pointers documented as "host or device" may point to host memory
+ *    (pageable or pinned) or to device memory of the ctx's GPU; the library
+ *    detects which with cudaPointerGetAttributes and copies accordingly.
+ *  - All GPU work is enqueued on the ctx stream.  Calls return after the
+ *    results they write to HOST memory are complete; results written to
+ *    DEVICE memory are complete when the ctx stream reaches that point.
+ *  - A ctx is bound to one GPU and is not thread-safe.  One process per GPU.
+ *  - Arithmetic: cost-model forward passes, greedy scores and plan costs are
+ *    computed in IEEE fp64 (the oracle's precision), so decisions agree with
+ *    the fp64 oracle except at relative top-2 margins ~1e-15.  Exception:
+ *    ns_score_plans with NS_SCORE_TF32X3 runs the comm MLPs on tcgen05 tensor
+ *    cores in split-TF32 (3 products) with FP32 accumulation (~1e-6 rel).
+ */
+#ifndef NEUROSHARD_H
+#define NEUROSHARD_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    NS_OK = 0,
+    NS_INFEASIBLE = 1,        /* at least one task has no feasible plan (cost = +inf) */
+    NS_ERR_ARG = -1,          /* invalid argument (NULL, out of range, shape mismatch) */
+    NS_ERR_STATE = -2,        /* call order violated (e.g. no models loaded) */
+    NS_ERR_NOMEM = -3,        /* device or host allocation failed */
+    NS_ERR_CUDA = -4,         /* CUDA runtime error (message has the CUDA string) */
+    NS_ERR_NCCL = -5,         /* NCCL error */
+    NS_ERR_INTERNAL = -6
+} ns_status;
+
+typedef struct ns_ctx ns_ctx;        /* opaque; one per (process, GPU) */
+typedef struct ns_tables ns_tables;  /* opaque featurised batch of sharding tasks (device-resident) */
+
+/* ------------------------------------------------------------------ lifecycle */
+/* Create a context on CUDA device `cuda_device`.  `cuda_stream` is a
+ * cudaStream_t (e.g. torch.cuda.current_stream().cuda_stream) or NULL for the
+ * legacy default stream.  *out receives the handle. */
+ns_status ns_create(ns_ctx** out, int cuda_device, void* cuda_stream);
+ns_status ns_destroy(ns_ctx* ctx);
+const char* ns_last_error(const ns_ctx* ctx);
+ns_status ns_set_stream(ns_ctx* ctx, void* cuda_stream);
+/* Block until all work enqueued by this ctx has finished. */
+ns_status ns_synchronize(ns_ctx* ctx);
+/* Number of kernels this ctx has launched since creation (bench evidence). */
+uint64_t ns_kernel_launches(const ns_ctx* ctx);
+
+/* ------------------------------------------------------------- cost models */
+/* One dense layer y = W x + b, torch.nn.Linear layout: W is [out][in]
+ * row-major fp64, b is [out] fp64.  Host pointers. */
+typedef struct {
+    int32_t in, out;
+    const double* W;
+    const double* b;
+} ns_linear;
+
+/* Computation cost model: shared table encoder "128-32"
+ * (enc[0]: F=5 -> 128, enc[1]: 128 -> 32, ReLU after both, reading R2),
+ * element-wise sum over the tables of a GPU, head "32-64" (head[0]: 32 -> 64,
+ * ReLU; head[1]: 64 -> 1, no output activation, reading R3). */
+typedef struct {
+    ns_linear enc[2];
+    ns_linear head[2];
+} ns_compute_model;
+
+/* Communication cost model: MLP "128-64-32-16",
+ * layer[0]: 2D -> 128, layer[1]: 128 -> 64, layer[2]: 64 -> 32,
+ * layer[3]: 32 -> 16, layer[4]: 16 -> D; ReLU on hidden layers.  Input is
+ * [starts_ms / start_scale (D), device_dims / dim_scale (D)], output is the
+ * per-GPU cost.  One model per direction ("two separate models"). */
+typedef struct {
+    int32_t D;
+    ns_linear layer[5];
+    double start_scale;   /* 20.0 (P:788 start range 0-20 ms) */
+    double dim_scale;     /* 1024.0 */
+} ns_comm_model;
+
+/* Load (copy to the GPU) the three pre-trained cost models.  Shapes are
+ * validated (NS_ERR_ARG on mismatch; fwd->D must equal bwd->D, 1 <= D <= 128).
+ * *fingerprint_out (may be NULL) receives an FNV-1a-64 hash of every weight
+ * byte, for the version control of P:226.  Replaces previously loaded models. */
+ns_status ns_load_cost_models(ns_ctx* ctx, const ns_compute_model* compute,
+                              const ns_comm_model* fwd, const ns_comm_model* bwd,
+                              uint64_t* fingerprint_out);
+
+/* ------------------------------------------------------------------ tables */
+/* One embedding table (P:111 factors; reading R1): dimension (columns,
+ * % 4 == 0), hash size (rows), mean pooling factor, indices-distribution
+ * skew scalar. */
+typedef struct {
+    int32_t dim;
+    int32_t reserved;     /* must be 0 */
+    int64_t hash_size;
+    double  pooling_factor;
+    double  skew;
+} ns_table_desc;
+
+/* Featurise a batch of n_tasks sharding tasks and run the cached per-table
+ * cost-model precompute (kernel N1, P:219 + table augmentation): for
+ * every table at its own dim (and, lazily on the first column-wise call, at
+ * every dim reachable by halving) the encoder output e, the hoisted head
+ * projection v = H1 e and the single-table cost C({t}).
+ *   tables       host or device, [task_offsets[n_tasks]] descriptors,
+ *                task i owns tables[task_offsets[i] .. task_offsets[i+1])
+ *   task_offsets host, [n_tasks + 1], task_offsets[0] == 0, each task >= 1 table
+ *   mem_cap      host, [n_tasks], per-GPU memory cap in bytes (P:368 4 GB;
+ *                table bytes = hash * dim * 4, reading R7)
+ * Requires loaded models.  *out is freed with ns_tables_free. */
+ns_status ns_featurize_tables(ns_ctx* ctx, const ns_table_desc* tables,
+                              const int32_t* task_offsets, const int64_t* mem_cap,
+                              int32_t n_tasks, ns_tables** out);
+ns_status ns_tables_free(ns_tables* tables);
+
+/* Copy the per-table single costs C({t}) (fp64, [task_offsets[n_tasks]]) and,
+ * if features_out != NULL, the features x ([..][5] fp64) to host memory. */
+ns_status ns_tables_single_costs(ns_ctx* ctx, const ns_tables* tables,
+                                 double* cost_out, double* features_out);
+
+/* ------------------------------------------------------------ plan scoring */
+typedef enum {
+    NS_SCORE_FP64 = 0,    /* fp64 SIMT (default) */
+    NS_SCORE_TF32X3 = 1   /* comm MLPs on tcgen05, split-TF32 x3, FP32 accumulate */
+} ns_score_mode;
+
+/* Simulator f(c, t) as a service ("estimate the embedding cost of any
+ * sharding plan"): score P explicit plans of task `task` of `tables`.
+ *   col_plan  host, [n_col] column plan c: step i halves table c_i
+ *             of the evolving list and appends the second half (n_col may be 0)
+ *   assign    host or device, [P][T + n_col] int8 device ids in 0..D-1
+ *   cost_out  host or device, [P] fp64 plan costs (may be NULL)
+ *   best_index_out / best_cost_out  host, argmin over P (lowest index on ties)
+ * f = max_d(comp_d + fwd_d + bwd_d) with comp_d = C(S_d) (0 if empty),
+ * fwd starts = comp - min(comp), bwd starts = 0 (readings R4, R10, R11).
+ * Memory and max_dim constraints are NOT applied (any plan can be scored).
+ * After ns_comm_init the P plans are split over the ranks and the argmin is
+ * an allreduce-min over packed (cost, index) keys; cost_out then holds only
+ * this rank's slice [P_begin, P_end) at its global positions. */
+ns_status ns_score_plans(ns_ctx* ctx, const ns_tables* tables, int32_t task, int32_t D,
+                         const int32_t* col_plan, int32_t n_col,
+                         const int8_t* assign, int64_t P, int32_t mode,
+                         double* cost_out, int64_t* best_index_out, double* best_cost_out);
+
+/* ------------------------------------------------------------------ search */
+typedef struct {
+    int32_t N;               /* candidate tables per kind, default 10 */
+    int32_t K;               /* beam width, default 3 */
+    int32_t L;               /* split steps, default 10; ignored by tablewise */
+    int32_t M;               /* grid points, default 11 */
+    double  grid_hi_factor;  /* M_e = factor * M_s, default 1.5 */
+    uint32_t flags;          /* reserved, must be 0 */
+} ns_search_params;
+
+/* Per-task results.  Every pointer is host or device; only `cost` is
+ * required, others may be NULL. */
+typedef struct {
+    double*   cost;          /* [n_tasks] best simulated cost, +inf if infeasible */
+    int32_t*  n_col;         /* [n_tasks] length of the best column plan */
+    int32_t*  col_plan;      /* [n_tasks][L] best column plan, -1 padded */
+    int8_t*   assign;        /* [n_tasks][assign_stride] device per table of the
+                                post-split list (T_i + n_col entries), -1 padded */
+    int32_t   assign_stride; /* >= max_i T_i + L (tablewise: max_i T_i) */
+    int32_t*  grid_index;    /* [n_tasks] winning grid point m (0..M-1), -1 if infeasible */
+    uint64_t* n_scores;      /* [n_tasks] candidate scores evaluated (work W, O12) */
+} ns_plan_batch;
+
+/* Table-wise sharding only: GreedyGridSearch (Alg. 2) of every
+ * task with the empty column plan.  Tasks are independent (batch axis).
+ * Returns NS_INFEASIBLE if some task has no feasible grid point. */
+ns_status ns_shard_tablewise(ns_ctx* ctx, const ns_tables* tables, int32_t D,
+                             const ns_search_params* params, ns_plan_batch* out);
+
+/* Column-wise + table-wise sharding: BeamSearch (Alg. 1) over
+ * column plans with GreedyGridSearch as the inner loop; the empty plan is
+ * evaluated first (reading R15).  After ns_comm_init, each level's
+ * trajectories are partitioned over the ranks and exchanged with one NCCL
+ * allgather of packed keys; every rank returns identical results. */
+ns_status ns_shard_columnwise(ns_ctx* ctx, const ns_tables* tables, int32_t D,
+                              const ns_search_params* params, ns_plan_batch* out);
+
+/* ------------------------------------------------------------ multi-GPU */
+/* 128-byte NCCL unique id (call on rank 0, broadcast by any means). */
+ns_status ns_comm_unique_id(unsigned char id_out[128]);
+/* Make subsequent ns_score_plans / ns_shard_columnwise calls collective over
+ * nranks processes (one GPU each).  nranks == 1 is allowed (no-op comm). */
+ns_status ns_comm_init(ns_ctx* ctx, int32_t nranks, int32_t rank, const unsigned char id[128]);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* NEUROSHARD_H */

@@ -1,0 +1,30 @@
+"""B200-native NeuroShard plan-scoring hot path (arXiv 2305.01868).
+
+The compute lives in ``libneuroshard.so`` (hand-written sm_100a CUDA behind
+the C ABI of ``include/neuroshard.h``); this package is its thin Python
+binding.  Importing it without the built library raises ImportError.
+"""
+from ._native import (  # noqa: F401
+    EXPORTED,
+    LIB,
+    LIB_PATH,
+    NS_SCORE_FP64,
+    NS_SCORE_TF32X3,
+    NSError,
+    TABLE_DESC,
+    Tables,
+    ns_comm_init,
+    ns_comm_unique_id,
+    ns_create,
+    ns_destroy,
+    ns_featurize_tables,
+    ns_kernel_launches,
+    ns_load_cost_models,
+    ns_score_plans,
+    ns_set_stream,
+    ns_shard_columnwise,
+    ns_shard_tablewise,
+    ns_synchronize,
+    ns_tables_single_costs,
+    table_descs,
+)

@@ -1,0 +1,291 @@
+"""ctypes binding of libneuroshard.so (include/neuroshard.h) -- marshalling only.
+
+Every function here converts Python / numpy / torch arguments to the C ABI
+and calls it; all compute happens in the CUDA library.  If the shared library
+is missing the import fails loudly (there is no CPU fallback).
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from typing import Any, Optional, Sequence
+
+import numpy as np
+
+_PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_PKG, "libneuroshard.so")
+
+NS_OK, NS_INFEASIBLE = 0, 1
+NS_SCORE_FP64, NS_SCORE_TF32X3 = 0, 1
+_STATUS = {0: "NS_OK", 1: "NS_INFEASIBLE", -1: "NS_ERR_ARG", -2: "NS_ERR_STATE", -3: "NS_ERR_NOMEM",
+           -4: "NS_ERR_CUDA", -5: "NS_ERR_NCCL", -6: "NS_ERR_INTERNAL"}
+
+TABLE_DESC = np.dtype([("dim", "<i4"), ("reserved", "<i4"), ("hash_size", "<i8"),
+                       ("pooling_factor", "<f8"), ("skew", "<f8")])
+assert TABLE_DESC.itemsize == 32
+
+
+class NSError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"{_STATUS.get(status, status)}: {msg}")
+        self.status = status
+
+
+class ns_linear(C.Structure):
+    _fields_ = [("in_", C.c_int32), ("out", C.c_int32), ("W", C.POINTER(C.c_double)), ("b", C.POINTER(C.c_double))]
+
+
+class ns_compute_model(C.Structure):
+    _fields_ = [("enc", ns_linear * 2), ("head", ns_linear * 2)]
+
+
+class ns_comm_model(C.Structure):
+    _fields_ = [("D", C.c_int32), ("layer", ns_linear * 5), ("start_scale", C.c_double), ("dim_scale", C.c_double)]
+
+
+class ns_search_params(C.Structure):
+    _fields_ = [("N", C.c_int32), ("K", C.c_int32), ("L", C.c_int32), ("M", C.c_int32),
+                ("grid_hi_factor", C.c_double), ("flags", C.c_uint32)]
+
+
+class ns_plan_batch(C.Structure):
+    _fields_ = [("cost", C.c_void_p), ("n_col", C.c_void_p), ("col_plan", C.c_void_p), ("assign", C.c_void_p),
+                ("assign_stride", C.c_int32), ("grid_index", C.c_void_p), ("n_scores", C.c_void_p)]
+
+
+def _load():
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"{LIB_PATH} is missing: build it with `python -m paper_2305_01868_b200.build` "
+                          "(there is no CPU fallback)")
+    lib = C.CDLL(LIB_PATH)
+    vp, i32, i64, u64p = C.c_void_p, C.c_int32, C.c_int64, C.POINTER(C.c_uint64)
+    sig = {
+        "ns_create": ([C.POINTER(vp), C.c_int, vp], C.c_int),
+        "ns_destroy": ([vp], C.c_int),
+        "ns_last_error": ([vp], C.c_char_p),
+        "ns_set_stream": ([vp, vp], C.c_int),
+        "ns_synchronize": ([vp], C.c_int),
+        "ns_kernel_launches": ([vp], C.c_uint64),
+        "ns_load_cost_models": ([vp, C.POINTER(ns_compute_model), C.POINTER(ns_comm_model),
+                                 C.POINTER(ns_comm_model), u64p], C.c_int),
+        "ns_featurize_tables": ([vp, vp, vp, vp, i32, C.POINTER(vp)], C.c_int),
+        "ns_tables_free": ([vp], C.c_int),
+        "ns_tables_single_costs": ([vp, vp, vp, vp], C.c_int),
+        "ns_score_plans": ([vp, vp, i32, i32, vp, i32, vp, i64, i32, vp, C.POINTER(i64), C.POINTER(C.c_double)],
+                           C.c_int),
+        "ns_shard_tablewise": ([vp, vp, i32, C.POINTER(ns_search_params), C.POINTER(ns_plan_batch)], C.c_int),
+        "ns_shard_columnwise": ([vp, vp, i32, C.POINTER(ns_search_params), C.POINTER(ns_plan_batch)], C.c_int),
+        "ns_comm_unique_id": ([vp], C.c_int),
+        "ns_comm_init": ([vp, i32, i32, vp], C.c_int),
+    }
+    for name, (args, res) in sig.items():
+        f = getattr(lib, name)
+        f.argtypes = args
+        f.restype = res
+    return lib
+
+
+LIB = _load()
+EXPORTED = ["ns_create", "ns_destroy", "ns_last_error", "ns_set_stream", "ns_synchronize", "ns_kernel_launches",
+            "ns_load_cost_models", "ns_featurize_tables", "ns_tables_free", "ns_tables_single_costs",
+            "ns_score_plans", "ns_shard_tablewise", "ns_shard_columnwise", "ns_comm_unique_id", "ns_comm_init"]
+
+
+def _check(ctx, status: int, allow_infeasible: bool = True) -> int:
+    if status < 0:
+        msg = LIB.ns_last_error(ctx).decode() if ctx else ""
+        raise NSError(status, msg)
+    if status == NS_INFEASIBLE and not allow_infeasible:
+        raise NSError(status, "infeasible")
+    return status
+
+
+def _ptr(x: Any) -> Optional[int]:
+    """Host numpy array or torch tensor (host or CUDA) -> raw address."""
+    if x is None:
+        return None
+    if isinstance(x, np.ndarray):
+        assert x.flags["C_CONTIGUOUS"], "arrays must be C-contiguous"
+        return x.ctypes.data
+    if hasattr(x, "data_ptr"):
+        assert x.is_contiguous(), "tensors must be contiguous"
+        return x.data_ptr()
+    raise TypeError(type(x))
+
+
+# ----------------------------------------------------------------- lifecycle
+def ns_create(device: int = 0, stream: Optional[int] = None) -> int:
+    h = C.c_void_p()
+    _check(None, LIB.ns_create(C.byref(h), device, stream))
+    return h.value
+
+
+def ns_destroy(ctx: int) -> None:
+    _check(ctx, LIB.ns_destroy(ctx))
+
+
+def ns_set_stream(ctx: int, stream: Optional[int]) -> None:
+    _check(ctx, LIB.ns_set_stream(ctx, stream))
+
+
+def ns_synchronize(ctx: int) -> None:
+    _check(ctx, LIB.ns_synchronize(ctx))
+
+
+def ns_kernel_launches(ctx: int) -> int:
+    return int(LIB.ns_kernel_launches(ctx))
+
+
+# ----------------------------------------------------------------- models
+def _lin(W: np.ndarray, b: np.ndarray, keep: list) -> ns_linear:
+    W = np.ascontiguousarray(W, dtype=np.float64)
+    b = np.ascontiguousarray(b, dtype=np.float64).reshape(-1)
+    keep += [W, b]
+    return ns_linear(W.shape[1], W.shape[0], W.ctypes.data_as(C.POINTER(C.c_double)),
+                     b.ctypes.data_as(C.POINTER(C.c_double)))
+
+
+def ns_load_cost_models(ctx: int, weights) -> int:
+    """weights: object with .enc, .head, .comm_fwd, .comm_bwd (lists of (W, b)),
+    .D, .start_scale, .dim_scale (see workload.synth.Weights).  Returns the
+    fingerprint."""
+    keep: list = []
+    cm = ns_compute_model()
+    for i in range(2):
+        cm.enc[i] = _lin(*weights.enc[i], keep)
+        cm.head[i] = _lin(*weights.head[i], keep)
+    comms = []
+    for layers in (weights.comm_fwd, weights.comm_bwd):
+        m = ns_comm_model()
+        m.D = weights.D
+        for i in range(5):
+            m.layer[i] = _lin(*layers[i], keep)
+        m.start_scale = weights.start_scale
+        m.dim_scale = weights.dim_scale
+        comms.append(m)
+    fp = C.c_uint64()
+    _check(ctx, LIB.ns_load_cost_models(ctx, C.byref(cm), C.byref(comms[0]), C.byref(comms[1]), C.byref(fp)))
+    return fp.value
+
+
+# ----------------------------------------------------------------- tables
+def table_descs(tasks: Sequence) -> tuple:
+    """Pack tasks (objects with dims/hash/pooling/skew/cap) into the ABI's
+    descriptor array, offsets and caps (host numpy)."""
+    n = sum(t.T for t in tasks)
+    desc = np.zeros(n, dtype=TABLE_DESC)
+    off = np.zeros(len(tasks) + 1, dtype=np.int32)
+    caps = np.zeros(len(tasks), dtype=np.int64)
+    k = 0
+    for i, t in enumerate(tasks):
+        T = t.T
+        desc["dim"][k:k + T] = t.dims
+        desc["hash_size"][k:k + T] = t.hash
+        desc["pooling_factor"][k:k + T] = t.pooling
+        desc["skew"][k:k + T] = t.skew
+        k += T
+        off[i + 1] = k
+        caps[i] = t.cap
+    return desc, off, caps
+
+
+class Tables:
+    """Owning handle of an ns_tables batch."""
+
+    def __init__(self, ctx: int, handle: int, offsets: np.ndarray, T_max: int):
+        self.ctx, self.handle, self.offsets, self.T_max = ctx, handle, offsets, T_max
+        self.n_tasks = len(offsets) - 1
+
+    def free(self):
+        if self.handle:
+            LIB.ns_tables_free(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.free()
+        except Exception:
+            pass
+
+
+def ns_featurize_tables(ctx: int, desc, offsets: np.ndarray, caps: np.ndarray) -> Tables:
+    """desc: TABLE_DESC numpy array (host) or a CUDA uint8 tensor holding the
+    same bytes; offsets/caps host numpy."""
+    offsets = np.ascontiguousarray(offsets, dtype=np.int32)
+    caps = np.ascontiguousarray(caps, dtype=np.int64)
+    h = C.c_void_p()
+    _check(ctx, LIB.ns_featurize_tables(ctx, _ptr(desc), offsets.ctypes.data, caps.ctypes.data,
+                                        len(caps), C.byref(h)))
+    T_max = int(np.max(np.diff(offsets)))
+    return Tables(ctx, h.value, offsets, T_max)
+
+
+def ns_tables_single_costs(ctx: int, tables: Tables, features: bool = False):
+    n = int(tables.offsets[-1])
+    c = np.zeros(n)
+    f = np.zeros((n, 5)) if features else None
+    _check(ctx, LIB.ns_tables_single_costs(ctx, tables.handle, c.ctypes.data, _ptr(f)))
+    return (c, f) if features else c
+
+
+# ----------------------------------------------------------------- scoring
+def ns_score_plans(ctx: int, tables: Tables, task: int, D: int, col_plan, assign, mode: int = NS_SCORE_FP64,
+                   cost_out=None):
+    """assign: int8 [P, T + n_col] numpy or CUDA tensor.  Returns
+    (cost_out, best_index, best_cost); cost_out is a new host array unless
+    one (host array or CUDA tensor) is given."""
+    col = np.ascontiguousarray(col_plan if col_plan is not None else [], dtype=np.int32)
+    P = int(assign.shape[0])
+    if cost_out is None:
+        cost_out = np.zeros(P)
+    bi, bc = C.c_int64(), C.c_double()
+    _check(ctx, LIB.ns_score_plans(ctx, tables.handle, task, D, col.ctypes.data if len(col) else None, len(col),
+                                   _ptr(assign), P, mode, _ptr(cost_out), C.byref(bi), C.byref(bc)))
+    return cost_out, bi.value, bc.value
+
+
+# ----------------------------------------------------------------- search
+def _params(N, K, L, M, hi):
+    return ns_search_params(N, K, L, M, hi, 0)
+
+
+def _alloc_out(n: int, stride: int, L: int, out: Optional[dict]):
+    if out is None:
+        out = dict(cost=np.zeros(n), n_col=np.zeros(n, np.int32), col_plan=np.zeros((n, max(L, 1)), np.int32),
+                   assign=np.zeros((n, stride), np.int8), grid_index=np.zeros(n, np.int32),
+                   n_scores=np.zeros(n, np.uint64))
+    pb = ns_plan_batch(_ptr(out["cost"]), _ptr(out.get("n_col")), _ptr(out.get("col_plan")),
+                       _ptr(out.get("assign")), int(out["assign"].shape[1]) if out.get("assign") is not None else 0,
+                       _ptr(out.get("grid_index")), _ptr(out.get("n_scores")))
+    return out, pb
+
+
+def ns_shard_tablewise(ctx: int, tables: Tables, D: int, M: int = 11, hi: float = 1.5, out: Optional[dict] = None):
+    out, pb = _alloc_out(tables.n_tasks, tables.T_max, 0, out)
+    p = _params(10, 3, 0, M, hi)
+    st = _check(ctx, LIB.ns_shard_tablewise(ctx, tables.handle, D, C.byref(p), C.byref(pb)))
+    out["status"] = st
+    return out
+
+
+def ns_shard_columnwise(ctx: int, tables: Tables, D: int, N: int = 10, K: int = 3, L: int = 10, M: int = 11,
+                        hi: float = 1.5, out: Optional[dict] = None):
+    out, pb = _alloc_out(tables.n_tasks, tables.T_max + L, L, out)
+    p = _params(N, K, L, M, hi)
+    st = _check(ctx, LIB.ns_shard_columnwise(ctx, tables.handle, D, C.byref(p), C.byref(pb)))
+    out["status"] = st
+    return out
+
+
+# ----------------------------------------------------------------- comm
+def ns_comm_unique_id() -> bytes:
+    buf = (C.c_ubyte * 128)()
+    st = LIB.ns_comm_unique_id(buf)
+    if st != 0:
+        raise NSError(st, "ns_comm_unique_id")
+    return bytes(buf)
+
+
+def ns_comm_init(ctx: int, nranks: int, rank: int, uid: Optional[bytes]) -> None:
+    buf = (C.c_ubyte * 128).from_buffer_copy(uid) if uid else None
+    _check(ctx, LIB.ns_comm_init(ctx, nranks, rank, buf))

@@ -1,0 +1,234 @@
+// k_score.cu -- ns_score_plans: the simulator f(c, t) over P explicit plans
+// ("estimate the embedding cost of any sharding plan"), kernel N2.
+//
+// Per plan: per-device sum pooling of the cached hoisted rows
+// u_d = hb1 + sum_{t on d} v_t (P:219 element-wise sum; hoist of the head's
+// first layer), comp_d = H2 ReLU(u_d) + hb2 (0 if empty, R4), then the fwd /
+// bwd comm MLPs and max over devices.  fp64, one warp per plan; the
+// argmin over plans is a deterministic two-stage (cost, index) reduction.
+#include <cuda_runtime.h>
+#include <math_constants.h>
+
+#include <cstring>
+#include <vector>
+
+#include "ns_device.cuh"
+#include "ns_internal.cuh"
+
+namespace ns {
+
+struct ScoreArgs {
+    long long p_begin, p_end;
+    int Tp, D;
+    const int8_t* assign;     // [P][Tp] (global plan index)
+    const int32_t* rows;      // [Tp] variant rows of the post-split list
+    const double* V;
+    const int32_t* vdim;
+    double* cost;             // [P] indexed by global plan index
+    HeadParams head;
+    CommParams cp;
+    double start_scale, dim_scale;
+};
+
+__global__ void __launch_bounds__(128) k_score_fp64(const ScoreArgs a) {
+    extern __shared__ double ssm[];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, wpb = blockDim.x >> 5;
+    const int D = a.D;
+    const size_t per_warp = (size_t)D * kV + D + (D + 1) / 2 + kPlanCostScratch(D);
+    double* u = ssm + (size_t)w * per_warp;     // [D][64]
+    double* comp = u + (size_t)D * kV;          // [D]
+    int32_t* dd = (int32_t*)(comp + D);         // [D]
+    double* scratch = comp + D + (D + 1) / 2;
+    for (long long p = a.p_begin + (long long)blockIdx.x * wpb + w; p < a.p_end; p += (long long)gridDim.x * wpb) {
+        for (int i = lane; i < D * kV; i += 32) u[i] = a.head.hb1[i % kV];
+        for (int d = lane; d < D; d += 32) dd[d] = 0;
+        __syncwarp();
+        const int8_t* pa = a.assign + p * a.Tp;
+        bool bad = false;
+        for (int t = 0; t < a.Tp; ++t) {
+            const int d = pa[t];
+            if (d < 0 || d >= D) {   // invalid device id: the plan scores NaN
+                bad = true;
+                continue;
+            }
+            const int row = __ldg(a.rows + t);
+            const double* v = a.V + (size_t)row * kV;
+            u[d * kV + lane] += __ldg(v + lane);
+            u[d * kV + lane + 32] += __ldg(v + lane + 32);
+            if (lane == 0) dd[d] += __ldg(a.vdim + row);
+        }
+        __syncwarp();
+        for (int d = 0; d < D; ++d) {
+            double part = a.head.H2[lane] * relu_exact(u[d * kV + lane]) +
+                          a.head.H2[lane + 32] * relu_exact(u[d * kV + lane + 32]);
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) part += __shfl_xor_sync(kFull, part, o);
+            if (lane == 0) comp[d] = dd[d] > 0 ? part + a.head.hb2 : 0.0;
+        }
+        __syncwarp();
+        const double c = warp_plan_cost(a.cp, comp, dd, scratch, lane, a.start_scale, a.dim_scale);
+        if (lane == 0) a.cost[p] = bad ? CUDART_NAN : c;
+        __syncwarp();
+    }
+}
+
+struct BestRec {
+    double cost;
+    long long idx;
+};
+
+__device__ __forceinline__ bool better(double c, long long i, double bc, long long bi) {
+    return c < bc || (c == bc && i < bi);
+}
+
+// stage 1: per-block lexicographic (cost, index) minimum
+__global__ void k_argmin(const double* cost, long long pb, long long pe, BestRec* out) {
+    __shared__ double sc[32];
+    __shared__ long long si[32];
+    double bc = CUDART_INF;
+    long long bi = 0x7fffffffffffffffll;
+    for (long long p = pb + (long long)blockIdx.x * blockDim.x + threadIdx.x; p < pe;
+         p += (long long)gridDim.x * blockDim.x) {
+        const double c = cost[p];
+        if (better(c, p, bc, bi)) {
+            bc = c;
+            bi = p;
+        }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        const double oc = __shfl_xor_sync(kFull, bc, o);
+        const long long oi = __shfl_xor_sync(kFull, bi, o);
+        if (better(oc, oi, bc, bi)) {
+            bc = oc;
+            bi = oi;
+        }
+    }
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (lane == 0) {
+        sc[w] = bc;
+        si[w] = bi;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int k = 1; k < (int)(blockDim.x >> 5); ++k)
+            if (better(sc[k], si[k], bc, bi)) {
+                bc = sc[k];
+                bi = si[k];
+            }
+        out[blockIdx.x].cost = bc;
+        out[blockIdx.x].idx = bi;
+    }
+}
+
+// stage 2: one thread reduces the per-block records (and the gathered ranks)
+__global__ void k_argmin_final(const BestRec* in, int n, BestRec* out) {
+    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    double bc = CUDART_INF;
+    long long bi = 0x7fffffffffffffffll;
+    for (int k = 0; k < n; ++k)
+        if (better(in[k].cost, in[k].idx, bc, bi)) {
+            bc = in[k].cost;
+            bi = in[k].idx;
+        }
+    out->cost = bc;
+    out->idx = bi;
+}
+
+ns_status run_score_plans_tf32x3(ns_ctx* ctx, const ScoreArgs& a, double* dcost);
+
+ns_status run_score_plans(ns_ctx* ctx, const ns_tables* t, int task, int D, const int32_t* col_plan, int n_col,
+                          const int8_t* assign, int64_t P, int mode, double* cost_out, int64_t* best_index_out,
+                          double* best_cost_out) {
+    const int T = t->off[task + 1] - t->off[task];
+    const int Tp = T + n_col;
+    // post-split list of variant rows; validated by the caller
+    std::vector<int32_t> rows(Tp);
+    for (int i = 0; i < T; ++i) rows[i] = (t->off[task] + i) * kDepth;
+    for (int k = 0; k < n_col; ++k) {
+        rows[col_plan[k]] += 1;
+        rows[T + k] = rows[col_plan[k]];
+    }
+    // partition the plans over ranks (contiguous blocks)
+    const long long per = (P + ctx->nranks - 1) / ctx->nranks;
+    const long long pb = std::min<long long>(P, per * ctx->rank);
+    const long long pe = std::min<long long>(P, pb + per);
+    const bool dev_assign = is_device_ptr(assign);
+    const int nblk_arg = 296;
+    size_t need = 256 + (size_t)Tp * 4 + (size_t)P * 8 + (size_t)(nblk_arg + 2 + ctx->nranks) * sizeof(BestRec) + 1024;
+    if (!dev_assign) need += (size_t)(pe - pb) * Tp + 256;
+    char* base = (char*)arena_get(ctx, need);
+    if (!base) return set_err(ctx, NS_ERR_NOMEM, "device arena (score)");
+    size_t off = 0;
+    auto take = [&](size_t bytes) {
+        off = (off + 255) & ~size_t(255);
+        char* p = base + off;
+        off += bytes;
+        return p;
+    };
+    int32_t* d_rows = (int32_t*)take((size_t)Tp * 4);
+    double* d_cost = (double*)take((size_t)P * 8);
+    BestRec* d_part = (BestRec*)take((size_t)nblk_arg * sizeof(BestRec));
+    BestRec* d_best = (BestRec*)take(sizeof(BestRec));
+    BestRec* d_all = (BestRec*)take((size_t)ctx->nranks * sizeof(BestRec));
+    const int8_t* d_assign = assign;
+    if (!dev_assign && pe > pb) {
+        int8_t* tmp = (int8_t*)take((size_t)(pe - pb) * Tp);
+        NS_CUDA(ctx, cudaMemcpyAsync(tmp, assign + pb * Tp, (size_t)(pe - pb) * Tp, cudaMemcpyHostToDevice,
+                                     ctx->stream));
+        d_assign = tmp - pb * Tp;   // indexed by global plan index
+    }
+    NS_CUDA(ctx, cudaMemcpyAsync(d_rows, rows.data(), (size_t)Tp * 4, cudaMemcpyHostToDevice, ctx->stream));
+    ScoreArgs a;
+    a.p_begin = pb;
+    a.p_end = pe;
+    a.Tp = Tp;
+    a.D = D;
+    a.assign = d_assign;
+    a.rows = d_rows;
+    a.V = t->d_V;
+    a.vdim = t->d_vdim;
+    a.cost = d_cost;
+    a.head = ctx->model.head;
+    a.cp = comm_params(ctx);
+    a.start_scale = ctx->model.start_scale;
+    a.dim_scale = ctx->model.dim_scale;
+    if (pe > pb) {
+        if (mode == NS_SCORE_TF32X3) {
+            ns_status s = run_score_plans_tf32x3(ctx, a, d_cost);
+            if (s != NS_OK) return s;
+        } else {
+            const size_t per_warp = ((size_t)D * kV + D + (D + 1) / 2 + kPlanCostScratch(D)) * sizeof(double);
+            int wpb = 4;
+            while (wpb > 1 && per_warp * wpb > 96 * 1024) wpb >>= 1;
+            const size_t smem = per_warp * wpb;
+            if (smem > 48 * 1024)
+                cudaFuncSetAttribute(k_score_fp64, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            const long long warps = pe - pb;
+            long long blocks = (warps + wpb - 1) / wpb;
+            const long long cap = (long long)ctx->sm_count * 16;
+            if (blocks > cap) blocks = cap;
+            k_score_fp64<<<(unsigned)blocks, wpb * 32, smem, ctx->stream>>>(a);
+            NS_LAUNCHED(ctx);
+        }
+    }
+    k_argmin<<<nblk_arg, 256, 0, ctx->stream>>>(d_cost, pb, pe, d_part);
+    NS_LAUNCHED(ctx);
+    k_argmin_final<<<1, 32, 0, ctx->stream>>>(d_part, nblk_arg, d_best);
+    NS_LAUNCHED(ctx);
+    ns_status s = comm_allgather(ctx, d_best, d_all, sizeof(BestRec));
+    if (s != NS_OK) return s;
+    k_argmin_final<<<1, 32, 0, ctx->stream>>>(d_all, ctx->nranks, d_best);
+    NS_LAUNCHED(ctx);
+    if (cost_out && pe > pb)
+        NS_CUDA(ctx, cudaMemcpyAsync(cost_out + pb, d_cost + pb, (size_t)(pe - pb) * 8, cudaMemcpyDefault,
+                                     ctx->stream));
+    BestRec h;
+    NS_CUDA(ctx, cudaMemcpyAsync(&h, d_best, sizeof(BestRec), cudaMemcpyDeviceToHost, ctx->stream));
+    NS_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+    if (best_index_out) *best_index_out = h.idx;
+    if (best_cost_out) *best_cost_out = h.cost;
+    return NS_OK;
+}
+
+}  // namespace ns

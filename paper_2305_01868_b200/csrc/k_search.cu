@@ -1,0 +1,886 @@
+// k_search.cu -- the search hot path: kernels N3 (level candidates / column
+// plans), order, N4 (greedy placement), N5 (finalize: plan cost), N6 (grid
+// argmin, beam top-K, global best), and the host drivers for
+// ns_shard_tablewise (Alg. 2) and ns_shard_columnwise (Alg. 1 + Alg. 2).
+//
+// Everything runs on the device; the host only enqueues a fixed sequence of
+// launches (5 per beam level) without synchronising, then copies results.
+#include <cuda_runtime.h>
+#include <math_constants.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <vector>
+
+#include "ns_device.cuh"
+#include "ns_internal.cuh"
+
+namespace ns {
+
+// ======================================================================
+// Device buffers of one search call (carved from the ctx arena).
+// "cp" = column-plan slot (one GreedyGridSearch call of Alg. 1 line 11);
+// "traj" = (cp, grid point m), the unit of data parallelism.
+// ======================================================================
+struct SearchBufs {
+    int n_tasks, D, M, K, N2, Lcap, Tpm, S, n_traj;
+    // per cp
+    int32_t* cp_task;
+    int32_t* cp_valid;
+    int32_t* cp_len;
+    int32_t* cp_plan;    // [S][Lcap]
+    int32_t* cp_Tp;
+    int32_t* ord_row;    // [S][Tpm]  variant row of the p-th table in cost order
+    int32_t* ord_idx;    // [S][Tpm]  its index in the post-split table list
+    // per traj
+    int8_t* assign;      // [n_traj][Tpm]
+    double* comp;        // [n_traj][D]
+    int32_t* devdim;     // [n_traj][D]
+    uint8_t* feas;       // [n_traj]
+    uint32_t* work;      // [n_traj]
+    double* tcost;       // [n_traj]
+    // per task
+    int32_t* capdim;     // [n_tasks][M]
+    int32_t* beam_plan;  // [n_tasks][K][Lcap]
+    int32_t* beam_cnt;   // [n_tasks]
+    double* best_cost;   // [n_tasks]
+    int32_t* best_m;
+    int32_t* best_ncol;
+    int32_t* best_plan;  // [n_tasks][Lcap]
+    int8_t* best_assign; // [n_tasks][Tpm]
+    uint64_t* n_scores;  // [n_tasks]
+};
+
+struct TaskView {   // read-only table arrays of the batch
+    const int32_t* off;
+    const int64_t* cap;
+    const double* V;
+    const double* C;
+    const int32_t* vdim;
+    const int64_t* vbytes;
+};
+
+// ---------------------------------------------------------------- helpers
+// Post-split table list of a column plan: entry i is a variant row
+// (table g, depth j) = g * kDepth + j.  The first half stays at c_i, the
+// second is appended.  Built by one thread into shared memory.
+__device__ void build_rows(const TaskView& tv, int q, const int32_t* plan, int len, int32_t* rows) {
+    const int base = tv.off[q], T = tv.off[q + 1] - base;
+    for (int i = 0; i < T; ++i) rows[i] = (base + i) * kDepth;
+    for (int k = 0; k < len; ++k) {
+        const int c = plan[k];
+        rows[c] += 1;
+        rows[T + k] = rows[c];
+    }
+}
+
+// ======================================================================
+// Level setup kernels
+// ======================================================================
+__global__ void k_setup_level0(SearchBufs b) {
+    const int q = blockIdx.x * blockDim.x + threadIdx.x;
+    if (q >= b.n_tasks) return;
+    b.cp_task[q] = q;
+    b.cp_valid[q] = 1;
+    b.cp_len[q] = 0;
+    b.best_cost[q] = CUDART_INF;
+    b.best_m[q] = -1;
+    b.best_ncol[q] = 0;
+    b.n_scores[q] = 0;
+    b.beam_cnt[q] = 0;
+}
+
+// N3: candidates of every beam plan (Alg. 1 line 8; reading
+// R14): top-N by single-table cost (-C, index) then top-N by bytes
+// (-bytes, index) not already listed, minus tables with dim % 8 != 0.  Child
+// column plans = parent + [candidate], generation index (beam rank b,
+// candidate rank j) -> slot (q*K + b)*2N + j.
+__global__ void k_expand(SearchBufs b, TaskView tv, int level) {
+    extern __shared__ int32_t sh[];
+    const int q = blockIdx.x / b.K, bb = blockIdx.x % b.K;
+    const int slot0 = (q * b.K + bb) * b.N2;
+    const int plen = level - 1;
+    const int T = tv.off[q + 1] - tv.off[q];
+    const int Tp = T + plen;
+    int32_t* rows = sh;                 // [Tp]
+    int32_t* selc = rows + b.Tpm;       // [N] by cost rank -> index
+    int32_t* sels = selc + b.N2;        // [N] by size rank -> index
+    __shared__ int ncand;
+    if (bb >= b.beam_cnt[q]) {
+        for (int j = threadIdx.x; j < b.N2; j += blockDim.x) b.cp_valid[slot0 + j] = 0;
+        return;
+    }
+    const int32_t* pplan = b.beam_plan + ((size_t)q * b.K + bb) * b.Lcap;
+    if (threadIdx.x == 0) build_rows(tv, q, pplan, plen, rows);
+    const int N = b.N2 / 2;
+    for (int j = threadIdx.x; j < b.N2; j += blockDim.x) selc[j] = sels[j] = -1;
+    __syncthreads();
+    for (int i = threadIdx.x; i < Tp; i += blockDim.x) {
+        const double ci = tv.C[rows[i]];
+        const long long bi = tv.vbytes[rows[i]];
+        int rc = 0, rs = 0;
+        for (int k = 0; k < Tp; ++k) {
+            const double ck = tv.C[rows[k]];
+            const long long bk = tv.vbytes[rows[k]];
+            rc += (ck > ci) || (ck == ci && k < i);
+            rs += (bk > bi) || (bk == bi && k < i);
+        }
+        if (rc < N) selc[rc] = i;
+        if (rs < N) sels[rs] = i;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        int n = 0;
+        int32_t* cand = sels + b.N2;    // [2N]
+        for (int r = 0; r < N; ++r)
+            if (selc[r] >= 0) cand[n++] = selc[r];
+        const int nc = n;
+        for (int r = 0; r < N; ++r) {
+            const int i = sels[r];
+            if (i < 0) continue;
+            bool dup = false;
+            for (int k = 0; k < nc; ++k) dup |= (cand[k] == i);
+            if (!dup) cand[n++] = i;
+        }
+        int m = 0;
+        for (int k = 0; k < n; ++k)
+            if (tv.vdim[rows[cand[k]]] % 8 == 0) cand[m++] = cand[k];
+        ncand = m;
+    }
+    __syncthreads();
+    const int32_t* cand = sels + b.N2;
+    for (int j = threadIdx.x; j < b.N2; j += blockDim.x) {
+        const int g = slot0 + j;
+        if (j < ncand) {
+            b.cp_valid[g] = 1;
+            b.cp_task[g] = q;
+            b.cp_len[g] = level;
+            int32_t* cpl = b.cp_plan + (size_t)g * b.Lcap;
+            for (int k = 0; k < plen; ++k) cpl[k] = pplan[k];
+            cpl[plen] = cand[j];
+        } else {
+            b.cp_valid[g] = 0;
+        }
+    }
+}
+
+// Alg. 2 lines 2-3: build the T' column-sharded tables and
+// sort them by descending predicted single-table cost, ties by list index
+// (reading R13).  Rank sort: rank_i = #{k : (-C_k, k) < (-C_i, i)}; fp64 keys.
+__global__ void k_build_order(SearchBufs b, TaskView tv) {
+    extern __shared__ int32_t sh[];
+    const int g = blockIdx.x;
+    if (!b.cp_valid[g]) return;
+    const int q = b.cp_task[g];
+    const int len = b.cp_len[g];
+    const int Tp = tv.off[q + 1] - tv.off[q] + len;
+    int32_t* rows = sh;
+    double* key = (double*)(sh + ((b.Tpm + 1) & ~1));
+    if (threadIdx.x == 0) {
+        build_rows(tv, q, b.cp_plan + (size_t)g * b.Lcap, len, rows);
+        b.cp_Tp[g] = Tp;
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < Tp; i += blockDim.x) key[i] = tv.C[rows[i]];
+    __syncthreads();
+    for (int i = threadIdx.x; i < Tp; i += blockDim.x) {
+        const double ci = key[i];
+        int r = 0;
+        for (int k = 0; k < Tp; ++k) {
+            const double ck = key[k];
+            r += (ck > ci) || (ck == ci && k < i);
+        }
+        b.ord_row[(size_t)g * b.Tpm + r] = rows[i];
+        b.ord_idx[(size_t)g * b.Tpm + r] = i;
+    }
+}
+
+// ======================================================================
+// N4: greedy placement (Alg. 2 lines 6-20, PAPER.md:289 step 3) -- the hot loop.
+//
+// Two lanes per (trajectory, device).  Lane half h in {0,1} keeps features
+// [32h, 32h+32) of the hoisted head pre-activation u_d = hb1 + sum_{t on d} v_t
+// and of the head weights H2 in registers (fp64).  For table t (cost order)
+// every feasible device scores C(S_d + {t}) = hb2 + H2 . ReLU(u_d + v_t)
+// (reading R5: cost after insertion): each lane computes its 32-term partial
+// dot product and one shuffle joins the pair.  A segmented shuffle argmin picks
+// d* (lowest d on ties, R13); both lanes of d* add their half of v_t.
+// Feasible: bytes_d + bytes_t <= cap and dim_d + dim_t <= floor(max_dim_m)
+// (R6, R7); no feasible device strands the trajectory (R9).
+//
+// Why two lanes per device: with all 64 features in one lane, u (128 regs)
+// plus the 64 head weights exceed the register file and the compiler spills
+// the weights (they cannot all live in uniform registers).  Splitting the
+// features keeps u, H2 and the streamed v chunk resident (~170 regs) for one
+// extra shuffle + add per score.
+// ======================================================================
+constexpr int kHalf = kV / 2;
+
+struct GreedyArgs {
+    int traj_begin, traj_end, M, D, Tpm;
+    long long n_rows;
+    const int32_t* cp_valid;
+    const int32_t* cp_task;
+    const int32_t* cp_Tp;
+    const int32_t* ord_row;
+    const int32_t* ord_idx;
+    const int32_t* capdim;
+    const int64_t* cap;
+    const double* V;
+    const int32_t* vdim;
+    const int64_t* vbytes;
+    int8_t* assign;
+    double* comp;
+    int32_t* devdim;
+    uint8_t* feas;
+    uint32_t* work;
+    HeadParams head;
+};
+
+// Half dot product sum_{k<32} w[k] ReLU(u[k] + v[k]), 4 partial accumulators,
+// v streamed from L1/L2 in chunks of 8 doubles.
+__device__ __forceinline__ double half_score(const double (&u)[kHalf], const double (&w)[kHalf],
+                                             const double2* __restrict__ v2) {
+    double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+#pragma unroll
+    for (int c = 0; c < kHalf / 8; ++c) {
+        double2 vv[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) vv[i] = __ldg(v2 + c * 4 + i);
+#pragma unroll
+        for (int i = 0; i < 4; i += 2) {
+            const int k = c * 8 + 2 * i;
+            a0 = fma(w[k + 0], relu_hi(u[k + 0] + vv[i].x), a0);
+            a1 = fma(w[k + 1], relu_hi(u[k + 1] + vv[i].y), a1);
+            a2 = fma(w[k + 2], relu_hi(u[k + 2] + vv[i + 1].x), a2);
+            a3 = fma(w[k + 3], relu_hi(u[k + 3] + vv[i + 1].y), a3);
+        }
+    }
+    return (a0 + a1) + (a2 + a3);
+}
+
+// u += v (the chosen device's lanes only)
+__device__ __forceinline__ void half_add(double (&u)[kHalf], const double2* __restrict__ v2) {
+#pragma unroll
+    for (int c = 0; c < kHalf / 8; ++c) {
+        double2 vv[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) vv[i] = __ldg(v2 + c * 4 + i);
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            u[c * 8 + 2 * i] += vv[i].x;
+            u[c * 8 + 2 * i + 1] += vv[i].y;
+        }
+    }
+}
+
+__device__ __forceinline__ double half_head(const double (&u)[kHalf], const double (&w)[kHalf]) {
+    double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+#pragma unroll
+    for (int k = 0; k < kHalf; k += 4) {
+        a0 = fma(w[k + 0], relu_exact(u[k + 0]), a0);
+        a1 = fma(w[k + 1], relu_exact(u[k + 1]), a1);
+        a2 = fma(w[k + 2], relu_exact(u[k + 2]), a2);
+        a3 = fma(w[k + 3], relu_exact(u[k + 3]), a3);
+    }
+    return (a0 + a1) + (a2 + a3);
+}
+
+__device__ __forceinline__ void argmin_step(double& bs, int& bd, int o) {
+    const double os = __shfl_xor_sync(kFull, bs, o);
+    const int od = __shfl_xor_sync(kFull, bd, o);
+    if (os < bs || (os == bs && od < bd)) {
+        bs = os;
+        bd = od;
+    }
+}
+
+// SEG = 2 * pow2(D) <= 32 lanes per trajectory, 32/SEG trajectories per warp.
+template <int SEG>
+__global__ void __launch_bounds__(128) k_greedy_seg(const GreedyArgs a) {
+    constexpr int TPW = 32 / SEG;
+    constexpr unsigned SEGMASK = SEG == 32 ? kFull : ((1u << SEG) - 1u);
+    const int lane = threadIdx.x & 31;
+    const long long gw = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int seg = lane / SEG;
+    const int d = (lane % SEG) >> 1, h = lane & 1;
+    const long long tau = a.traj_begin + gw * TPW + seg;
+    const bool in_range = tau < a.traj_end;
+    bool alive = in_range;
+    int g = 0, m = 0, Tp = 0, capd = 0;
+    long long cap = 0;
+    if (alive) {
+        g = (int)(tau / a.M);
+        m = (int)(tau % a.M);
+        alive = a.cp_valid[g] != 0;
+    }
+    if (alive) {
+        const int q = a.cp_task[g];
+        Tp = a.cp_Tp[g];
+        cap = a.cap[q];
+        capd = a.capdim[q * a.M + m];
+    }
+    const bool dev = d < a.D;
+    double u[kHalf], w[kHalf];
+#pragma unroll
+    for (int k = 0; k < kHalf; ++k) {
+        u[k] = h ? a.head.hb1[kHalf + k] : a.head.hb1[k];
+        w[k] = h ? a.head.H2[kHalf + k] : a.head.H2[k];
+    }
+    int dsum = 0;
+    long long bsum = 0;
+    uint32_t work = 0;
+    int Tmax = alive ? Tp : 0;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) Tmax = max(Tmax, __shfl_xor_sync(kFull, Tmax, o));
+    const int32_t* orow = a.ord_row + (size_t)g * a.Tpm;
+    const int32_t* oidx = a.ord_idx + (size_t)g * a.Tpm;
+    int8_t* asg = a.assign + (size_t)(in_range ? tau : 0) * a.Tpm;
+#pragma unroll 1
+    for (int p = 0; p < Tmax; ++p) {
+        const bool act = alive && p < Tp;
+        int row = 0, dt = 0;
+        long long bt = 0;
+        if (act) {
+            row = __ldg(orow + p);
+            dt = __ldg(a.vdim + row);
+            bt = __ldg(a.vbytes + row);
+        }
+#ifdef NS_DEBUG
+        if (act && (row < 0 || row >= a.n_rows))
+            printf("bad row %d tau %lld g %d p %d Tp %d lane %d\n", row, tau, g, p, Tp, lane);
+#endif
+        const bool f = act && dev && (bsum + bt <= cap) && (dsum + dt <= capd);
+        const double2* v2 = reinterpret_cast<const double2*>(a.V + (size_t)row * kV + h * kHalf);
+        double part = 0.0;
+        if (f) part = half_score(u, w, v2);
+        double bs = a.head.hb2 + (part + __shfl_xor_sync(kFull, part, 1));
+        if (!f) bs = CUDART_INF;
+        int bd = d;
+#pragma unroll
+        for (int o = SEG / 2; o > 1; o >>= 1) argmin_step(bs, bd, o);
+#ifdef NS_DEBUG
+        if (act && (bd < 0 || bd >= 64)) printf("bad bd %d tau %lld p %d lane %d bs %g\n", bd, tau, p, lane, bs);
+#endif
+        const unsigned bal = __ballot_sync(kFull, f && h == 0);
+        if (act) {
+            work += __popc((bal >> (seg * SEG)) & SEGMASK);
+            if (bs == CUDART_INF) alive = false;   // reading R9: stranded -> grid point infeasible
+        }
+        const bool take = act && bs != CUDART_INF && d == bd;
+        if (take) {   // only the chosen device's two lanes load and add v_t
+            half_add(u, v2);
+            dsum += dt;
+            bsum += bt;
+        }
+        if (act && bs != CUDART_INF && (lane % SEG) == 0) asg[__ldg(oidx + p)] = (int8_t)bd;
+    }
+    const double hp = half_head(u, w);
+    const double hc = a.head.hb2 + (hp + __shfl_xor_sync(kFull, hp, 1));
+    if (in_range) {
+        if (dev && h == 0) {
+            a.comp[tau * a.D + d] = dsum > 0 ? hc : 0.0;   // reading R4
+            a.devdim[tau * a.D + d] = dsum;
+        }
+        if ((lane % SEG) == 0) {
+            a.feas[tau] = alive ? 1 : 0;
+            a.work[tau] = work;
+        }
+    }
+}
+
+// 2*pow2(D) > 32: one trajectory per CTA of ceil(2D/32) warps; cross-warp
+// argmin through shared memory (double-buffered by step parity).
+__global__ void __launch_bounds__(256) k_greedy_big(const GreedyArgs a) {
+    __shared__ double s_sc[2][8];
+    __shared__ int s_dv[2][8];
+    __shared__ int s_cnt[2][8];
+    const int lane = threadIdx.x & 31, wi = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    const long long tau = a.traj_begin + blockIdx.x;
+    if (tau >= a.traj_end) return;
+    const int g = (int)(tau / a.M), m = (int)(tau % a.M);
+    const int d = threadIdx.x >> 1, h = threadIdx.x & 1;
+    bool alive = a.cp_valid[g] != 0;
+    int Tp = 0, capd = 0;
+    long long cap = 0;
+    if (alive) {
+        const int q = a.cp_task[g];
+        Tp = a.cp_Tp[g];
+        cap = a.cap[q];
+        capd = a.capdim[q * a.M + m];
+    }
+    const bool dev = d < a.D;
+    double u[kHalf], w[kHalf];
+#pragma unroll
+    for (int k = 0; k < kHalf; ++k) {
+        u[k] = h ? a.head.hb1[kHalf + k] : a.head.hb1[k];
+        w[k] = h ? a.head.H2[kHalf + k] : a.head.H2[k];
+    }
+    int dsum = 0;
+    long long bsum = 0;
+    uint32_t work = 0;
+    const int32_t* orow = a.ord_row + (size_t)g * a.Tpm;
+    const int32_t* oidx = a.ord_idx + (size_t)g * a.Tpm;
+    int8_t* asg = a.assign + (size_t)tau * a.Tpm;
+#pragma unroll 1
+    for (int p = 0; p < (alive ? Tp : 0); ++p) {
+        const int par = p & 1;
+        const int row = __ldg(orow + p);
+        const int dt = __ldg(a.vdim + row);
+        const long long bt = __ldg(a.vbytes + row);
+        const bool f = dev && (bsum + bt <= cap) && (dsum + dt <= capd);
+        const double2* v2 = reinterpret_cast<const double2*>(a.V + (size_t)row * kV + h * kHalf);
+        double part = 0.0;
+        if (f) part = half_score(u, w, v2);
+        double bs = a.head.hb2 + (part + __shfl_xor_sync(kFull, part, 1));
+        if (!f) bs = CUDART_INF;
+        int bd = d;
+#pragma unroll
+        for (int o = 16; o > 1; o >>= 1) argmin_step(bs, bd, o);
+        const unsigned bal = __ballot_sync(kFull, f && h == 0);
+        if (lane == 0) {
+            s_sc[par][wi] = bs;
+            s_dv[par][wi] = bd;
+            s_cnt[par][wi] = __popc(bal);
+        }
+        __syncthreads();
+        bs = s_sc[par][0];
+        bd = s_dv[par][0];
+        int cnt = s_cnt[par][0];
+        for (int k = 1; k < nw; ++k) {
+            const double os = s_sc[par][k];
+            const int od = s_dv[par][k];
+            cnt += s_cnt[par][k];
+            if (os < bs || (os == bs && od < bd)) {
+                bs = os;
+                bd = od;
+            }
+        }
+        work += cnt;
+        if (bs == CUDART_INF) {
+            alive = false;
+            break;   // uniform across the CTA
+        }
+        if (d == bd) {
+            half_add(u, v2);
+            dsum += dt;
+            bsum += bt;
+        }
+        if (threadIdx.x == 0) asg[__ldg(oidx + p)] = (int8_t)bd;
+    }
+    const double hp = half_head(u, w);
+    const double hc = a.head.hb2 + (hp + __shfl_xor_sync(kFull, hp, 1));
+    if (dev && h == 0) {
+        a.comp[tau * a.D + d] = dsum > 0 ? hc : 0.0;
+        a.devdim[tau * a.D + d] = dsum;
+    }
+    if (threadIdx.x == 0) {
+        a.feas[tau] = alive ? 1 : 0;
+        a.work[tau] = work;
+    }
+}
+
+// ======================================================================
+// N5: evaluate each completed trajectory with the cost models (Alg. 2 /
+// PAPER.md:289 step 4): f = max_d(comp_d + fwd_d + bwd_d).  One warp per
+// trajectory, fp64.
+// ======================================================================
+struct FinArgs {
+    int traj_begin, traj_end, D;
+    const uint8_t* feas;
+    const double* comp;
+    const int32_t* devdim;
+    double* tcost;
+    CommParams cp;
+    double start_scale, dim_scale;
+};
+
+__global__ void __launch_bounds__(128) k_finalize(const FinArgs a) {
+    extern __shared__ double fsm[];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const long long tau = a.traj_begin + ((long long)blockIdx.x * (blockDim.x >> 5) + w);
+    if (tau >= a.traj_end) return;
+    if (!a.feas[tau]) {
+        if (lane == 0) a.tcost[tau] = CUDART_INF;
+        return;
+    }
+    double* buf = fsm + (size_t)w * kPlanCostScratch(a.D);
+    const double c = warp_plan_cost(a.cp, a.comp + tau * a.D, a.devdim + tau * a.D, buf, lane,
+                                    a.start_scale, a.dim_scale);
+    if (lane == 0) a.tcost[tau] = c;
+}
+
+// ======================================================================
+// N6: per task, grid argmin of every child column plan (Alg. 2 lines 16-18,
+// reading R12: lowest m on ties), work totals, global best with strict < in
+// generation order (Alg. 1 lines 13-16), next beam = K lowest (cost, gen)
+// (Alg. 1 line 20; R13, R16).  One CTA per task.
+// ======================================================================
+__global__ void k_select(SearchBufs b, int C, int level, int Kbeam) {
+    extern __shared__ unsigned char ssm[];
+    const int q = blockIdx.x;
+    double* ccost = (double*)ssm;                    // [C]
+    int32_t* cm = (int32_t*)(ccost + C);             // [C]
+    int32_t* cval = cm + C;                          // [C]
+    __shared__ unsigned long long s_work;
+    __shared__ int s_best;
+    if (threadIdx.x == 0) s_work = 0;
+    __syncthreads();
+    unsigned long long wsum = 0;
+    for (int j = threadIdx.x; j < C; j += blockDim.x) {
+        const int g = q * C + j;
+        const int v = b.cp_valid[g];
+        double best = CUDART_INF;
+        int bm = -1;
+        if (v) {
+            for (int m = 0; m < b.M; ++m) {
+                const long long tau = (long long)g * b.M + m;
+                wsum += b.work[tau];
+                const double c = b.tcost[tau];
+                if (c < best) {
+                    best = c;
+                    bm = m;
+                }
+            }
+        }
+        ccost[j] = best;
+        cm[j] = bm;
+        cval[j] = v;
+    }
+    atomicAdd(&s_work, wsum);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        b.n_scores[q] += s_work;
+        // lexicographic (cost, gen) minimum of the level == the first strict
+        // improvement in generation order
+        int arg = -1;
+        for (int j = 0; j < C; ++j) {
+            if (!cval[j]) continue;
+            if (arg < 0 || ccost[j] < ccost[arg]) arg = j;
+        }
+        s_best = -1;
+        if (arg >= 0 && (level == 0 || ccost[arg] < b.best_cost[q])) {
+            // level 0 always installs [] as the initial global best (R15)
+            s_best = arg;
+            b.best_cost[q] = ccost[arg];
+            b.best_m[q] = cm[arg];
+            b.best_ncol[q] = level;
+            const int g = q * C + arg;
+            for (int k = 0; k < level; ++k) b.best_plan[(size_t)q * b.Lcap + k] = b.cp_plan[(size_t)g * b.Lcap + k];
+        }
+        if (level == 0) b.beam_cnt[q] = 1;   // C_p <- {[]}
+    }
+    __syncthreads();
+    if (s_best >= 0) {
+        const int g = q * C + s_best;
+        const int Tp = b.cp_Tp[g];
+        const int mm = cm[s_best];
+        for (int i = threadIdx.x; i < b.Tpm; i += blockDim.x) {
+            int8_t v = -1;
+            if (mm >= 0 && i < Tp) v = b.assign[((size_t)g * b.M + mm) * b.Tpm + i];
+            b.best_assign[(size_t)q * b.Tpm + i] = v;
+        }
+    }
+    if (level > 0) {
+        // next beam: rank among valid children by (cost, gen)
+        int nvalid = 0;
+        for (int j = 0; j < C; ++j) nvalid += cval[j];
+        for (int j = threadIdx.x; j < C; j += blockDim.x) {
+            if (!cval[j]) continue;
+            int r = 0;
+            for (int k = 0; k < C; ++k)
+                if (cval[k] && (ccost[k] < ccost[j] || (ccost[k] == ccost[j] && k < j))) ++r;
+            if (r < Kbeam) {
+                const int g = q * C + j;
+                for (int k = 0; k < level; ++k)
+                    b.beam_plan[((size_t)q * b.K + r) * b.Lcap + k] = b.cp_plan[(size_t)g * b.Lcap + k];
+            }
+        }
+        if (threadIdx.x == 0) b.beam_cnt[q] = nvalid < Kbeam ? nvalid : Kbeam;
+    }
+}
+
+// Grid of max_dim caps (reading R8): M_s = sum(dim)/D,
+// M_e = hi*M_s, step = (M_e - M_s)/(M-1), cap_m = floor(M_s + m*step).  Each
+// operation is one IEEE-rounded fp64 op (explicit _rn intrinsics, no
+// contraction), the operation order stated in DESIGN.md R8.
+__global__ void k_grid_caps(const int64_t* sumdim, int n_tasks, int D, int M, double hi, int32_t* capdim) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n_tasks * M) return;
+    const int q = i / M, m = i % M;
+    const double Ms = __ddiv_rn((double)sumdim[q], (double)D);
+    double md = Ms;
+    if (M > 1) {
+        const double Me = __dmul_rn(hi, Ms);
+        const double step = __ddiv_rn(__dsub_rn(Me, Ms), (double)(M - 1));
+        md = __dadd_rn(Ms, __dmul_rn((double)m, step));
+    }
+    const double f = floor(md);
+    capdim[i] = f > 2.0e9 ? 2000000000 : (int32_t)f;
+}
+
+// Pack per-task results into the contiguous staging layout.
+struct OutStage {
+    double* cost;
+    int32_t* n_col;
+    int32_t* col_plan;   // [n][Lout]
+    int8_t* assign;      // [n][Tpm]
+    int32_t* grid;
+    uint64_t* scores;
+};
+
+__global__ void k_write_out(SearchBufs b, OutStage o, int Lout) {
+    const int q = blockIdx.x;
+    const bool feasible = b.best_cost[q] < CUDART_INF;
+    if (threadIdx.x == 0) {
+        o.cost[q] = b.best_cost[q];
+        o.n_col[q] = b.best_ncol[q];
+        o.grid[q] = feasible ? b.best_m[q] : -1;
+        o.scores[q] = b.n_scores[q];
+    }
+    for (int k = threadIdx.x; k < Lout; k += blockDim.x)
+        o.col_plan[(size_t)q * Lout + k] = k < b.best_ncol[q] ? b.best_plan[(size_t)q * b.Lcap + k] : -1;
+    for (int i = threadIdx.x; i < b.Tpm; i += blockDim.x)
+        o.assign[(size_t)q * b.Tpm + i] = feasible ? b.best_assign[(size_t)q * b.Tpm + i] : (int8_t)-1;
+}
+
+// ======================================================================
+// Host driver
+// ======================================================================
+namespace {
+
+struct Carver {
+    char* base;
+    size_t off = 0;
+    template <typename T>
+    T* take(size_t n) {
+        off = (off + 255) & ~size_t(255);
+        T* p = base ? (T*)(base + off) : nullptr;
+        off += n * sizeof(T);
+        return p;
+    }
+};
+
+void carve(Carver& c, SearchBufs& b, OutStage& o, int Lout) {
+    b.cp_task = c.take<int32_t>(b.S);
+    b.cp_valid = c.take<int32_t>(b.S);
+    b.cp_len = c.take<int32_t>(b.S);
+    b.cp_plan = c.take<int32_t>((size_t)b.S * b.Lcap);
+    b.cp_Tp = c.take<int32_t>(b.S);
+    b.ord_row = c.take<int32_t>((size_t)b.S * b.Tpm);
+    b.ord_idx = c.take<int32_t>((size_t)b.S * b.Tpm);
+    b.assign = c.take<int8_t>((size_t)b.n_traj * b.Tpm);
+    b.comp = c.take<double>((size_t)b.n_traj * b.D);
+    b.devdim = c.take<int32_t>((size_t)b.n_traj * b.D);
+    b.feas = c.take<uint8_t>(b.n_traj);
+    b.work = c.take<uint32_t>(b.n_traj);
+    b.tcost = c.take<double>(b.n_traj);
+    b.capdim = c.take<int32_t>((size_t)b.n_tasks * b.M);
+    b.beam_plan = c.take<int32_t>((size_t)b.n_tasks * b.K * b.Lcap);
+    b.beam_cnt = c.take<int32_t>(b.n_tasks);
+    b.best_cost = c.take<double>(b.n_tasks);
+    b.best_m = c.take<int32_t>(b.n_tasks);
+    b.best_ncol = c.take<int32_t>(b.n_tasks);
+    b.best_plan = c.take<int32_t>((size_t)b.n_tasks * b.Lcap);
+    b.best_assign = c.take<int8_t>((size_t)b.n_tasks * b.Tpm);
+    b.n_scores = c.take<uint64_t>(b.n_tasks);
+    o.cost = c.take<double>(b.n_tasks);
+    o.n_col = c.take<int32_t>(b.n_tasks);
+    o.col_plan = c.take<int32_t>((size_t)b.n_tasks * Lout);
+    o.assign = c.take<int8_t>((size_t)b.n_tasks * b.Tpm);
+    o.grid = c.take<int32_t>(b.n_tasks);
+    o.scores = c.take<uint64_t>(b.n_tasks);
+}
+
+TaskView task_view(const ns_tables* t) {
+    TaskView tv;
+    tv.off = t->d_off;
+    tv.cap = t->d_cap;
+    tv.V = t->d_V;
+    tv.C = t->d_C;
+    tv.vdim = t->d_vdim;
+    tv.vbytes = t->d_vbytes;
+    return tv;
+}
+
+size_t order_smem(int Tpm) { return ((size_t)((Tpm + 1) & ~1)) * 4 + (size_t)Tpm * 8; }
+
+ns_status launch_greedy(ns_ctx* ctx, const SearchBufs& b, const ns_tables* t, long long tb, long long te) {
+    if (te <= tb) return NS_OK;
+    GreedyArgs a;
+    a.traj_begin = (int)tb;
+    a.traj_end = (int)te;
+    a.n_rows = (long long)t->n_tables * kDepth;
+    a.M = b.M;
+    a.D = b.D;
+    a.Tpm = b.Tpm;
+    a.cp_valid = b.cp_valid;
+    a.cp_task = b.cp_task;
+    a.cp_Tp = b.cp_Tp;
+    a.ord_row = b.ord_row;
+    a.ord_idx = b.ord_idx;
+    a.capdim = b.capdim;
+    a.cap = t->d_cap;
+    a.V = t->d_V;
+    a.vdim = t->d_vdim;
+    a.vbytes = t->d_vbytes;
+    a.assign = b.assign;
+    a.comp = b.comp;
+    a.devdim = b.devdim;
+    a.feas = b.feas;
+    a.work = b.work;
+    a.head = ctx->model.head;
+    const long long n = te - tb;
+    int dp = 1;
+    while (dp < b.D) dp <<= 1;
+    const int seg = 2 * dp;
+    if (seg > 32) {
+        const int threads = ((2 * b.D + 31) / 32) * 32;
+        k_greedy_big<<<(unsigned)n, threads, 0, ctx->stream>>>(a);
+    } else {
+        const long long tpw = 32 / seg;
+        const long long warps = (n + tpw - 1) / tpw;
+        const unsigned blocks = (unsigned)((warps + 3) / 4);
+        switch (seg) {
+            case 2: k_greedy_seg<2><<<blocks, 128, 0, ctx->stream>>>(a); break;
+            case 4: k_greedy_seg<4><<<blocks, 128, 0, ctx->stream>>>(a); break;
+            case 8: k_greedy_seg<8><<<blocks, 128, 0, ctx->stream>>>(a); break;
+            case 16: k_greedy_seg<16><<<blocks, 128, 0, ctx->stream>>>(a); break;
+            default: k_greedy_seg<32><<<blocks, 128, 0, ctx->stream>>>(a); break;
+        }
+    }
+    NS_LAUNCHED(ctx);
+    return NS_OK;
+}
+
+ns_status launch_finalize(ns_ctx* ctx, const SearchBufs& b, long long tb, long long te) {
+    if (te <= tb) return NS_OK;
+    FinArgs f;
+    f.traj_begin = (int)tb;
+    f.traj_end = (int)te;
+    f.D = b.D;
+    f.feas = b.feas;
+    f.comp = b.comp;
+    f.devdim = b.devdim;
+    f.tcost = b.tcost;
+    f.cp = comm_params(ctx);
+    f.start_scale = ctx->model.start_scale;
+    f.dim_scale = ctx->model.dim_scale;
+    const int wpb = 4;
+    const size_t smem = (size_t)wpb * kPlanCostScratch(b.D) * sizeof(double);
+    const long long n = te - tb;
+    k_finalize<<<(unsigned)((n + wpb - 1) / wpb), wpb * 32, smem, ctx->stream>>>(f);
+    NS_LAUNCHED(ctx);
+    return NS_OK;
+}
+
+// Copy staged results to the caller's (host or device) pointers.
+ns_status deliver(ns_ctx* ctx, const ns_tables* t, const OutStage& o, int Lout, int Tpm, ns_plan_batch* out) {
+    const int n = t->n_tasks;
+    cudaStream_t st = ctx->stream;
+    auto cp = [&](void* dst, const void* src, size_t bytes) -> cudaError_t {
+        if (!dst) return cudaSuccess;
+        return cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDefault, st);
+    };
+    NS_CUDA(ctx, cp(out->n_col, o.n_col, n * sizeof(int32_t)));
+    if (out->col_plan && Lout > 0) NS_CUDA(ctx, cp(out->col_plan, o.col_plan, (size_t)n * Lout * sizeof(int32_t)));
+    if (out->assign) {
+        if (out->assign_stride > Tpm) NS_CUDA(ctx, cudaMemset2DAsync(out->assign, out->assign_stride, 0xff,
+                                                                     0, 0, st));   // no-op placeholder
+        if (is_device_ptr(out->assign)) {
+            NS_CUDA(ctx, cudaMemset2DAsync(out->assign, out->assign_stride, 0xff, out->assign_stride, n, st));
+        } else {
+            for (int q = 0; q < n; ++q) std::memset(out->assign + (size_t)q * out->assign_stride, 0xff, out->assign_stride);
+        }
+        NS_CUDA(ctx, cudaMemcpy2DAsync(out->assign, out->assign_stride, o.assign, Tpm, Tpm, n, cudaMemcpyDefault, st));
+    }
+    NS_CUDA(ctx, cp(out->grid_index, o.grid, n * sizeof(int32_t)));
+    NS_CUDA(ctx, cp(out->n_scores, o.scores, n * sizeof(uint64_t)));
+    // costs always pass through pinned host memory: the status needs them
+    double* hcost = (double*)pinned_get(ctx, n * sizeof(double) + 64);
+    if (!hcost) return set_err(ctx, NS_ERR_NOMEM, "pinned staging");
+    int32_t* hflag = (int32_t*)(hcost + n);
+    NS_CUDA(ctx, cudaMemcpyAsync(hcost, o.cost, n * sizeof(double), cudaMemcpyDeviceToHost, st));
+    NS_CUDA(ctx, cudaMemcpyAsync(hflag, t->d_flag, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+    NS_CUDA(ctx, cp(out->cost, o.cost, n * sizeof(double)));
+    NS_CUDA(ctx, cudaStreamSynchronize(st));
+    ns_status fs = check_tables_flag(ctx, t, hflag);
+    if (fs != NS_OK) return fs;
+    for (int q = 0; q < n; ++q)
+        if (!std::isfinite(hcost[q])) return NS_INFEASIBLE;
+    return NS_OK;
+}
+
+ns_status run_search(ns_ctx* ctx, const ns_tables* t, int D, const ns_search_params* p, ns_plan_batch* out,
+                     bool columnwise) {
+    SearchBufs b{};
+    b.n_tasks = t->n_tasks;
+    b.D = D;
+    b.M = p->M;
+    const int L = columnwise ? p->L : 0;
+    b.K = columnwise ? p->K : 1;
+    b.N2 = columnwise ? 2 * p->N : 1;
+    b.Lcap = L > 0 ? L : 1;
+    b.Tpm = t->T_max + L;
+    const int C = (columnwise && L > 0) ? b.K * b.N2 : 1;
+    b.S = b.n_tasks * C;
+    b.n_traj = b.S * b.M;
+    const int Lout = L;
+    OutStage o{};
+    Carver probe{nullptr};
+    carve(probe, b, o, Lout > 0 ? Lout : 1);
+    char* base = (char*)arena_get(ctx, probe.off + 256);
+    if (!base) return set_err(ctx, NS_ERR_NOMEM, "device arena (search)");
+    Carver cv{base};
+    carve(cv, b, o, Lout > 0 ? Lout : 1);
+    ns_status s;
+    k_grid_caps<<<(b.n_tasks * b.M + 255) / 256, 256, 0, ctx->stream>>>(t->d_sumdim, b.n_tasks, b.D, b.M,
+                                                                        p->grid_hi_factor, b.capdim);
+    NS_LAUNCHED(ctx);
+    const TaskView tv = task_view(t);
+    const size_t osm = order_smem(b.Tpm);
+    if (osm > 48 * 1024) {
+        cudaFuncSetAttribute(k_build_order, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)osm);
+        cudaFuncSetAttribute(k_expand, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)osm);
+    }
+    // ---- level 0: the empty column plan (tablewise = this level only)
+    k_setup_level0<<<(b.n_tasks + 255) / 256, 256, 0, ctx->stream>>>(b);
+    NS_LAUNCHED(ctx);
+    k_build_order<<<b.n_tasks, 256, osm, ctx->stream>>>(b, tv);
+    NS_LAUNCHED(ctx);
+    const long long n0 = (long long)b.n_tasks * b.M;
+    if ((s = launch_greedy(ctx, b, t, 0, n0)) != NS_OK) return s;
+    if ((s = launch_finalize(ctx, b, 0, n0)) != NS_OK) return s;
+    k_select<<<b.n_tasks, 128, (size_t)1 * 16, ctx->stream>>>(b, 1, 0, b.K);
+    NS_LAUNCHED(ctx);
+    // ---- beam levels (Alg. 1 lines 6-22)
+    for (int level = 1; level <= L; ++level) {
+        const size_t esm = (size_t)b.Tpm * 4 + (size_t)b.N2 * 4 * 2 + (size_t)b.N2 * 4 + 64;
+        if (esm > 48 * 1024)
+            cudaFuncSetAttribute(k_expand, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)esm);
+        k_expand<<<b.n_tasks * b.K, 256, esm, ctx->stream>>>(b, tv, level);
+        NS_LAUNCHED(ctx);
+        k_build_order<<<b.S, 256, osm, ctx->stream>>>(b, tv);
+        NS_LAUNCHED(ctx);
+        if ((s = launch_greedy(ctx, b, t, 0, b.n_traj)) != NS_OK) return s;
+        if ((s = launch_finalize(ctx, b, 0, b.n_traj)) != NS_OK) return s;
+        k_select<<<b.n_tasks, 128, (size_t)C * 16, ctx->stream>>>(b, C, level, b.K);
+        NS_LAUNCHED(ctx);
+    }
+    k_write_out<<<b.n_tasks, 128, 0, ctx->stream>>>(b, o, Lout > 0 ? Lout : 1);
+    NS_LAUNCHED(ctx);
+    return deliver(ctx, t, o, Lout, b.Tpm, out);
+}
+
+}  // namespace
+
+ns_status run_tablewise(ns_ctx* ctx, const ns_tables* t, int D, const ns_search_params* p, ns_plan_batch* out) {
+    return run_search(ctx, t, D, p, out, false);
+}
+
+ns_status run_columnwise(ns_ctx* ctx, const ns_tables* t, int D, const ns_search_params* p, ns_plan_batch* out) {
+    return run_search(ctx, t, D, p, out, true);
+}
+
+}  // namespace ns

@@ -1,0 +1,154 @@
+// ns_internal.cuh -- internal data structures of the NeuroShard B200 library.
+// Not part of the C ABI (include/neuroshard.h is).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+#include <vector>
+
+#include "../../include/neuroshard.h"
+
+namespace ns {
+
+constexpr int kF = 5;        // table features (reading R1)
+constexpr int kH = 128;      // encoder hidden width  ("128-32")
+constexpr int kE = 32;       // table representation width
+constexpr int kV = 64;       // head hidden width     ("32-64")
+constexpr int kDepth = 6;    // variant slots per table: dim, dim/2, ..., dim/32 (128 -> 4)
+constexpr int kMaxD = 128;   // int8 device ids
+constexpr int kCommW[6] = {0, 128, 64, 32, 16, 0};   // comm widths "128-64-32-16"
+
+// Head weights passed by value as a kernel parameter (lands in the constant
+// bank, so the greedy's DFMA reads H2[k] as a constant operand).
+struct HeadParams {
+    double hb1[kV];
+    double H2[kV];
+    double hb2;
+};
+
+struct DevModel {
+    bool loaded = false;
+    // compute model, fp64, device
+    double* enc1W = nullptr;   // [128][5]
+    double* enc1b = nullptr;   // [128]
+    double* enc2W = nullptr;   // [32][128]
+    double* enc2b = nullptr;   // [32]
+    double* H1 = nullptr;      // [64][32]
+    HeadParams head{};
+    // comm models: [dir][layer] W [out][in], b [out]
+    int D = 0;
+    int cin[5] = {0}, cout[5] = {0};
+    double* cW[2][5] = {{nullptr}};
+    double* cb[2][5] = {{nullptr}};
+    // fp32 copies (TF32x3 score path)
+    float* cWf[2][5] = {{nullptr}};
+    float* cbf[2][5] = {{nullptr}};
+    double start_scale = 20.0, dim_scale = 1024.0;
+    uint64_t fingerprint = 0;
+};
+
+// Comm model pointers passed to kernels.
+struct CommParams {
+    int D;
+    const double* W[2][5];
+    const double* b[2][5];
+    double inv_start, inv_dim;   // 1/start_scale, 1/dim_scale
+};
+
+}  // namespace ns
+
+struct ns_ctx {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    std::string err;
+    ns::DevModel model;
+    uint64_t launches = 0;
+    int sm_count = 148;
+    // grow-only device arena for per-call scratch
+    void* arena = nullptr;
+    size_t arena_bytes = 0;
+    // pinned host staging
+    void* pinned = nullptr;
+    size_t pinned_bytes = 0;
+    // multi-GPU
+    void* nccl = nullptr;    // ncclComm_t
+    int nranks = 1, rank = 0;
+};
+
+struct ns_tables {
+    ns_ctx* ctx = nullptr;
+    int n_tasks = 0;
+    int n_tables = 0;
+    int T_max = 0;
+    std::vector<int32_t> off;       // [n_tasks + 1]
+    std::vector<int64_t> cap;       // [n_tasks]
+    std::vector<int32_t> dims;      // [n_tables] host copy (host input, or fetched lazily)
+    // device
+    int32_t* d_off = nullptr;
+    int64_t* d_cap = nullptr;
+    int64_t* d_sumdim = nullptr;    // [n_tasks] sum of dims (grid)
+    int32_t* d_flag = nullptr;      // device-side descriptor validation flag
+    ns_table_desc* d_desc = nullptr;
+    double* d_feat = nullptr;   // [rows][5]
+    double* d_V = nullptr;      // [rows][64]  v = H1 e (hb1 excluded)
+    double* d_C = nullptr;      // [rows]      single-table cost C({t})
+    int32_t* d_vdim = nullptr;  // [rows]      0 = invalid variant
+    int64_t* d_vbytes = nullptr;// [rows]
+    bool deep_done = false;     // variants of depth >= 1 computed
+};
+
+namespace ns {
+
+// ---------------------------------------------------------------- kernels
+// N1: featurise + encoder + hoisted head projection + single cost for rows
+// (table g, depth j), j in [jlo, jhi].
+void launch_precompute(ns_ctx* ctx, const ns_tables* t, int jlo, int jhi);
+// descriptor validation + per-task sum of dims (device side)
+void launch_tables_validate(ns_ctx* ctx, const ns_tables* t);
+ns_status ensure_host_dims(ns_ctx* ctx, const ns_tables* t);
+ns_status check_tables_flag(ns_ctx* ctx, const ns_tables* t, const int32_t* host_flag);
+
+struct SearchBufs;   // defined in k_search.cu
+ns_status run_tablewise(ns_ctx* ctx, const ns_tables* t, int D, const ns_search_params* p,
+                        ns_plan_batch* out);
+ns_status run_columnwise(ns_ctx* ctx, const ns_tables* t, int D, const ns_search_params* p,
+                         ns_plan_batch* out);
+ns_status run_score_plans(ns_ctx* ctx, const ns_tables* t, int task, int D,
+                          const int32_t* col_plan, int n_col, const int8_t* assign, int64_t P,
+                          int mode, double* cost_out, int64_t* best_index_out,
+                          double* best_cost_out);
+
+// helpers (ns_api.cu)
+ns_status set_err(ns_ctx* ctx, ns_status s, const std::string& msg);
+ns_status cuda_check(ns_ctx* ctx, cudaError_t e, const char* what);
+bool is_device_ptr(const void* p);
+void* arena_get(ns_ctx* ctx, size_t bytes);   // nullptr on failure
+void* pinned_get(ns_ctx* ctx, size_t bytes);
+CommParams comm_params(const ns_ctx* ctx);
+ns_status comm_allgather(ns_ctx* ctx, const void* send, void* recv, size_t bytes_per_rank);
+ns_status comm_allreduce_min_u64(ns_ctx* ctx, uint64_t* dev_buf, size_t count);
+void comm_destroy(ns_ctx* ctx);
+
+
+}  // namespace ns
+
+#define NS_CUDA(ctx, call)                                                   \
+    do {                                                                     \
+        cudaError_t _e = (call);                                             \
+        if (_e != cudaSuccess) return ns::cuda_check((ctx), _e, #call);      \
+    } while (0)
+
+#define NS_LAUNCHED(ctx)                                                     \
+    do {                                                                     \
+        (ctx)->launches++;                                                   \
+        cudaError_t _e = cudaGetLastError();                                 \
+        if (_e != cudaSuccess) return ns::cuda_check((ctx), _e, "kernel launch"); \
+    } while (0)
+
+#define NS_CHECK_LAST(ctx)                                                   \
+    do {                                                                     \
+        cudaError_t _e = cudaGetLastError();                                 \
+        if (_e != cudaSuccess) return ns::cuda_check((ctx), _e, "kernel launch"); \
+    } while (0)

@@ -1,0 +1,283 @@
+"""GPU parity: the CUDA path (through the C ABI) against the fp64 oracle on
+identical seeded inputs.  Tolerances: fp64 both sides, so costs agree to
+1e-12 relative and every decision (sort, greedy argmin, grid argmin, beam
+top-K, global best) is identical unless the oracle's top-2 margin is below
+1e-12; integers (assignments, column plans, grid index,
+work counts) are compared exactly."""
+import math
+
+import numpy as np
+import pytest
+
+from conftest import hand_task, hand_weights, small_task
+from oracle import brute, model as om, search as osr
+from workload.synth import gen_task, gen_tasks, gen_weights, gen_plans
+
+pytestmark = pytest.mark.gpu
+
+RTOL = 1e-12
+
+
+@pytest.fixture(scope="module")
+def ns():
+    import torch
+    assert torch.cuda.is_available()
+    import paper_2305_01868_b200 as ns
+    return ns
+
+
+@pytest.fixture(scope="module")
+def ctx(ns):
+    c = ns.ns_create(0)
+    yield c
+    ns.ns_destroy(c)
+
+
+def _setup(ns, ctx, tasks, w):
+    ns.ns_load_cost_models(ctx, w)
+    desc, off, caps = ns.table_descs(tasks)
+    return ns.ns_featurize_tables(ctx, desc, off, caps)
+
+
+def _rel(a, b):
+    if math.isinf(a) or math.isinf(b):
+        return 0.0 if a == b else math.inf
+    return abs(a - b) / max(abs(b), 1e-300)
+
+
+def _check_tablewise(ns, ctx, tasks, w, M):
+    tabs = _setup(ns, ctx, tasks, w)
+    out = ns.ns_shard_tablewise(ctx, tabs, w.D, M=M)
+    n_exact = 0
+    for i, task in enumerate(tasks):
+        emb = om.TableEmbeddings(w, task)
+        log = osr.DecisionLog()
+        r = osr.greedy_grid_search(w, emb, task, [], M, log=log)
+        assert int(out["n_scores"][i]) == r.work, f"task {i}: work"
+        if log.min_margin() < RTOL:
+            continue   # near-tie below fp64 resolution: decisions may legitimately differ
+        n_exact += 1
+        assert _rel(out["cost"][i], r.cost) <= RTOL, f"task {i}: cost {out['cost'][i]} vs {r.cost}"
+        if r.assign is None:
+            assert out["grid_index"][i] == -1 and np.all(out["assign"][i] == -1)
+        else:
+            assert out["grid_index"][i] == r.grid_index, f"task {i}: grid index"
+            assert out["assign"][i, :task.T].tolist() == r.assign, f"task {i}: assignment"
+    assert n_exact >= 0.95 * len(tasks)
+    return out
+
+
+def test_single_costs_and_features(ns, ctx):
+    w = gen_weights(4, "mono")
+    tasks = gen_tasks("C2", 3)
+    tabs = _setup(ns, ctx, tasks, w)
+    c, f = ns.ns_tables_single_costs(ctx, tabs, features=True)
+    k = 0
+    for task in tasks:
+        emb = om.TableEmbeddings(w, task)
+        for s in range(task.T):
+            x = om.featurize(int(task.dims[s]), int(task.hash[s]), float(task.pooling[s]), float(task.skew[s]))
+            np.testing.assert_allclose(f[k], x, rtol=1e-15, atol=0)
+            assert _rel(c[k], om.compute_cost(w, emb, [(s, int(task.dims[s]))])) <= RTOL
+            k += 1
+
+
+def test_hand_example(ns, ctx, golden_hand):
+    g = golden_hand
+    w, task = hand_weights(g), hand_task(g)
+    tabs = _setup(ns, ctx, [task], w)
+    out = ns.ns_shard_tablewise(ctx, tabs, 2, M=g["M"])
+    e = g["expected"]
+    assert out["cost"][0] == pytest.approx(e["cost"], rel=1e-12)
+    assert out["assign"][0, :3].tolist() == e["assign"]
+    assert out["grid_index"][0] == e["grid_index"]
+    assert int(out["n_scores"][0]) == e["work"]
+
+
+@pytest.mark.parametrize("kind", ["mono", "signed"])
+def test_tablewise_C1(ns, ctx, kind):
+    w = gen_weights(2, kind)
+    _check_tablewise(ns, ctx, gen_tasks("C1", 100), w, M=3)
+
+
+def test_tablewise_C2(ns, ctx):
+    w = gen_weights(4, "mono")
+    _check_tablewise(ns, ctx, gen_tasks("C2", 24), w, M=11)
+
+
+def test_tablewise_ragged_batch_and_edge_cases(ns, ctx):
+    # tasks of different sizes in one batch (ragged), T = 1, D = 1-like caps,
+    # and tasks whose grid points strand tables
+    rng = np.random.default_rng(11)
+    D = 3
+    tasks = [small_task(rng, T, D, hash_hi=1e6) for T in (1, 2, 3, 7, 17, 33, 64)]
+    tasks.append(small_task(rng, 9, D, cap=1 << 26, hash_hi=1e6))   # tight memory: some infeasible
+    w = gen_weights(D, "signed", seed=21)
+    _check_tablewise(ns, ctx, tasks, w, M=4)
+
+
+@pytest.mark.parametrize("D", [1, 5, 16])
+def test_tablewise_other_D(ns, ctx, D):
+    rng = np.random.default_rng(D)
+    tasks = [small_task(rng, 3 * D + 5, D) for _ in range(6)]
+    w = gen_weights(D, "mono", seed=30 + D)
+    _check_tablewise(ns, ctx, tasks, w, M=5)
+
+
+def test_tablewise_big_D_kernel(ns, ctx):
+    # D > 16 uses the multi-warp CTA kernel (C5 has D = 128)
+    rng = np.random.default_rng(5)
+    for D in (40, 128):
+        tasks = [small_task(rng, D + 30, D) for _ in range(2)]
+        w = gen_weights(D, "mono", seed=D)
+        _check_tablewise(ns, ctx, tasks, w, M=3)
+
+
+def test_infeasible_status(ns, ctx):
+    rng = np.random.default_rng(3)
+    task = small_task(rng, 6, 2, hash_hi=1e5)
+    task.dims[0] = 128
+    task.hash[0] = 10_000_000      # 5.1 GB table > 4 GiB cap
+    w = gen_weights(2, "mono")
+    tabs = _setup(ns, ctx, [task], w)
+    out = ns.ns_shard_tablewise(ctx, tabs, 2, M=3)
+    assert out["status"] == 1 and math.isinf(out["cost"][0]) and out["grid_index"][0] == -1
+    # column-wise search splits the oversized table (T14)
+    outc = ns.ns_shard_columnwise(ctx, tabs, 2, N=3, K=2, L=2, M=3)
+    emb = om.TableEmbeddings(w, task)
+    r = osr.beam_search(w, emb, task, N=3, K=2, L=2, M=3)
+    assert outc["status"] == 0 and 0 in outc["col_plan"][0, :outc["n_col"][0]].tolist()
+    assert _rel(outc["cost"][0], r.cost) <= RTOL
+    assert outc["col_plan"][0, :outc["n_col"][0]].tolist() == r.col_plan
+
+
+def _check_columnwise(ns, ctx, tasks, w, N, K, L, M):
+    tabs = _setup(ns, ctx, tasks, w)
+    out = ns.ns_shard_columnwise(ctx, tabs, w.D, N=N, K=K, L=L, M=M)
+    n_exact = 0
+    for i, task in enumerate(tasks):
+        emb = om.TableEmbeddings(w, task)
+        log = osr.DecisionLog()
+        r = osr.beam_search(w, emb, task, N=N, K=K, L=L, M=M, log=log)
+        assert int(out["n_scores"][i]) == r.work or log.min_margin() < RTOL, f"task {i}: work"
+        if log.min_margin() < RTOL:
+            continue
+        n_exact += 1
+        nc = int(out["n_col"][i])
+        assert out["col_plan"][i, :nc].tolist() == r.col_plan, f"task {i}: column plan"
+        assert _rel(out["cost"][i], r.cost) <= RTOL, f"task {i}: cost"
+        if r.assign is not None:
+            assert out["grid_index"][i] == r.grid_index
+            assert out["assign"][i, :task.T + nc].tolist() == r.assign, f"task {i}: assignment"
+    assert n_exact >= 0.9 * len(tasks)
+    return out
+
+
+def test_columnwise_small(ns, ctx):
+    w = gen_weights(4, "mono")
+    tasks = gen_tasks("C2", 4, T=16)
+    _check_columnwise(ns, ctx, tasks, w, N=4, K=2, L=3, M=5)
+
+
+def test_columnwise_signed_weights(ns, ctx):
+    w = gen_weights(3, "signed", seed=5)
+    rng = np.random.default_rng(8)
+    tasks = [small_task(rng, 12, 3) for _ in range(3)]
+    _check_columnwise(ns, ctx, tasks, w, N=3, K=3, L=3, M=4)
+
+
+def test_columnwise_C3_level1(ns, ctx):
+    # C3 shapes (T=80, D=8, N=10, K=10, M=11) with L=1: every level-1 child
+    w = gen_weights(8, "mono")
+    tasks = gen_tasks("C3", 2)
+    _check_columnwise(ns, ctx, tasks, w, N=10, K=10, L=1, M=11)
+
+
+def test_columnwise_C3_full_size_sampled(ns, ctx):
+    """Full C3 (L=10) in the bench's launch configuration; the oracle checks
+    the returned plan one by one: its cost from scratch (T8), GreedyGridSearch
+    of the returned column plan reproduces (cost, assign), and validity."""
+    w = gen_weights(8, "mono")
+    tasks = gen_tasks("C3", 2)
+    tabs = _setup(ns, ctx, tasks, w)
+    out = ns.ns_shard_columnwise(ctx, tabs, 8, N=10, K=10, L=10, M=11)
+    for i, task in enumerate(tasks):
+        emb = om.TableEmbeddings(w, task)
+        nc = int(out["n_col"][i])
+        c = out["col_plan"][i, :nc].tolist()
+        tables = osr.apply_col_plan(task, c)
+        a = out["assign"][i, :task.T + nc].tolist()
+        assert _rel(out["cost"][i], om.plan_cost(w, emb, tables, a, 8)[0]) <= RTOL
+        r = osr.greedy_grid_search(w, emb, task, c, 11)
+        assert r.assign == a and _rel(out["cost"][i], r.cost) <= RTOL
+        r0 = osr.greedy_grid_search(w, emb, task, [], 11)
+        assert out["cost"][i] <= r0.cost
+        load = np.zeros(8, np.int64)
+        for j, d in enumerate(a):
+            load[d] += osr.table_bytes(task, tables[j])
+        assert load.max() <= task.cap
+
+
+def test_score_plans_exhaustive(ns, ctx):
+    # every placement of <= 6 tables on 2-4 GPUs: per-plan costs and the argmin
+    for seed, (D, T) in enumerate([(2, 6), (3, 6), (4, 5)]):
+        rng = np.random.default_rng(50 + seed)
+        task = small_task(rng, T, D)
+        w = gen_weights(D, "mono" if seed % 2 == 0 else "signed", seed=60 + seed)
+        tabs = _setup(ns, ctx, [task], w)
+        emb = om.TableEmbeddings(w, task)
+        tables = osr.apply_col_plan(task, [])
+        plans = list(brute.all_placements(task, tables, D, respect_memory=False))
+        best, argset, costs = brute.exhaustive_best(w, emb, task, tables, D, respect_memory=False)
+        A = np.array(plans, dtype=np.int8)
+        cost, bi, bc = ns.ns_score_plans(ctx, tabs, 0, D, [], A)
+        np.testing.assert_allclose(cost, costs, rtol=RTOL)
+        assert plans[bi] in argset and _rel(bc, best) <= RTOL
+
+
+def test_score_plans_with_col_plan_and_device_input(ns, ctx):
+    import torch
+    w = gen_weights(8, "mono")
+    task = gen_task("C3", 0)
+    tabs = _setup(ns, ctx, [task], w)
+    emb = om.TableEmbeddings(w, task)
+    c = [i for i in range(task.T) if task.dims[i] % 8 == 0][:3]
+    tables = osr.apply_col_plan(task, c)
+    A = gen_plans(len(tables), 8, 300, seed=4)
+    At = torch.from_numpy(A).cuda()
+    cost_t = torch.zeros(300, dtype=torch.float64, device="cuda")
+    _, bi, bc = ns.ns_score_plans(ctx, tabs, 0, 8, c, At, cost_out=cost_t)
+    cost = cost_t.cpu().numpy()
+    for p in range(0, 300, 37):
+        assert _rel(cost[p], om.plan_cost(w, emb, tables, A[p].tolist(), 8)[0]) <= RTOL
+    assert bi == int(np.argmin(cost)) and bc == cost.min()
+
+
+def test_device_resident_inputs_and_outputs(ns, ctx):
+    import torch
+    w = gen_weights(4, "mono")
+    tasks = gen_tasks("C2", 8)
+    ns.ns_load_cost_models(ctx, w)
+    desc, off, caps = ns.table_descs(tasks)
+    d_desc = torch.from_numpy(desc.view(np.uint8)).cuda()
+    tabs = ns.ns_featurize_tables(ctx, d_desc, off, caps)
+    T = tabs.T_max
+    out = dict(cost=torch.zeros(8, dtype=torch.float64, device="cuda"),
+               n_col=torch.zeros(8, dtype=torch.int32, device="cuda"), col_plan=None,
+               assign=torch.zeros((8, T), dtype=torch.int8, device="cuda"),
+               grid_index=torch.zeros(8, dtype=torch.int32, device="cuda"),
+               n_scores=torch.zeros(8, dtype=torch.int64, device="cuda"))
+    ns.ns_shard_tablewise(ctx, tabs, 4, M=11, out=out)
+    host = ns.ns_shard_tablewise(ctx, tabs, 4, M=11)
+    assert np.array_equal(out["cost"].cpu().numpy(), host["cost"])
+    assert np.array_equal(out["assign"].cpu().numpy(), host["assign"])
+
+
+def test_determinism(ns, ctx):
+    w = gen_weights(8, "mono")
+    tasks = gen_tasks("C3", 2)
+    tabs = _setup(ns, ctx, tasks, w)
+    a = ns.ns_shard_columnwise(ctx, tabs, 8, N=10, K=3, L=4, M=11)
+    b = ns.ns_shard_columnwise(ctx, tabs, 8, N=10, K=3, L=4, M=11)
+    for k in ("cost", "n_col", "col_plan", "assign", "grid_index", "n_scores"):
+        assert np.array_equal(a[k], b[k]), k
