@@ -66,6 +66,14 @@ ns_status ns_set_stream(ns_ctx* ctx, void* cuda_stream);
 ns_status ns_synchronize(ns_ctx* ctx);
 /* Number of kernels this ctx has launched since creation (bench evidence). */
 uint64_t ns_kernel_launches(const ns_ctx* ctx);
+/* Kernel timers: with enable != 0 every launch is bracketed by CUDA events on
+ * the ctx stream; ns_profile resets the accumulators.  ns_profile_query
+ * returns the summed device time (ms) and launch count of one kernel class:
+ * "precompute" (N1), "validate", "order", "expand" (N3), "greedy" (N4),
+ * "finalize" (N5), "select" (N6), "score" (N2), "other".  Both synchronise
+ * the ctx stream. */
+ns_status ns_profile(ns_ctx* ctx, int32_t enable);
+ns_status ns_profile_query(ns_ctx* ctx, const char* kernel, double* total_ms, uint64_t* launches);
 
 /* ------------------------------------------------------------- cost models */
 /* One dense layer y = W x + b, torch.nn.Linear layout: W is [out][in]

@@ -20,6 +20,9 @@ from ._native import (  # noqa: F401
     ns_featurize_tables,
     ns_kernel_launches,
     ns_load_cost_models,
+    ns_profile,
+    ns_profile_query,
+    PROFILE_KINDS,
     ns_score_plans,
     ns_set_stream,
     ns_shard_columnwise,

@@ -66,6 +66,8 @@ def _load():
         "ns_set_stream": ([vp, vp], C.c_int),
         "ns_synchronize": ([vp], C.c_int),
         "ns_kernel_launches": ([vp], C.c_uint64),
+        "ns_profile": ([vp, i32], C.c_int),
+        "ns_profile_query": ([vp, C.c_char_p, C.POINTER(C.c_double), u64p], C.c_int),
         "ns_load_cost_models": ([vp, C.POINTER(ns_compute_model), C.POINTER(ns_comm_model),
                                  C.POINTER(ns_comm_model), u64p], C.c_int),
         "ns_featurize_tables": ([vp, vp, vp, vp, i32, C.POINTER(vp)], C.c_int),
@@ -87,6 +89,7 @@ def _load():
 
 LIB = _load()
 EXPORTED = ["ns_create", "ns_destroy", "ns_last_error", "ns_set_stream", "ns_synchronize", "ns_kernel_launches",
+            "ns_profile", "ns_profile_query",
             "ns_load_cost_models", "ns_featurize_tables", "ns_tables_free", "ns_tables_single_costs",
             "ns_score_plans", "ns_shard_tablewise", "ns_shard_columnwise", "ns_comm_unique_id", "ns_comm_init"]
 
@@ -134,6 +137,20 @@ def ns_synchronize(ctx: int) -> None:
 
 def ns_kernel_launches(ctx: int) -> int:
     return int(LIB.ns_kernel_launches(ctx))
+
+
+def ns_profile(ctx: int, enable: bool) -> None:
+    _check(ctx, LIB.ns_profile(ctx, 1 if enable else 0))
+
+
+PROFILE_KINDS = ("precompute", "validate", "order", "expand", "greedy", "finalize", "select", "score", "other")
+
+
+def ns_profile_query(ctx: int, kernel: str):
+    """(total device ms, launches) of one kernel class since ns_profile."""
+    ms, n = C.c_double(), C.c_uint64()
+    _check(ctx, LIB.ns_profile_query(ctx, kernel.encode(), C.byref(ms), C.byref(n)))
+    return ms.value, n.value
 
 
 # ----------------------------------------------------------------- models

@@ -1,0 +1,184 @@
+// k_mlp.cu -- kernel N5: plan cost f = max_d(comp_d + fwd_d + bwd_d) for a
+// batch of rows (trajectories of the search, or explicit plans of
+// ns_score_plans), with the two communication-cost MLPs
+// (2D -> 128 -> 64 -> 32 -> 16 -> D, "128-64-32-16"; "two
+// separate models") evaluated on the FP64 tensor cores.
+//
+// The MLP over a batch of rows is a chain of dense GEMMs
+// [rows x K] . W^T [K x N]; it runs as DMMA (mma.sync m8n8k4 .f64): fp64
+// products and fp64 accumulation, so plan costs keep the oracle's precision
+// (tcgen05 has no fp64 kind).  One warp owns 16 rows (two m8 tiles); the
+// activations of its rows stay in shared memory between layers (ping-pong
+// buffers padded so the A-fragment loads are bank-conflict free); weights
+// are read as B fragments through L1 (the whole comm model is <= 0.6 MB and
+// shared by every warp); bias + ReLU are fused into the accumulator epilogue.
+// Forward starts are comp - min(comp) (reading R10), backward starts 0,
+// inputs scaled by division exactly like the oracle (R10).
+#include <cuda_runtime.h>
+#include <math_constants.h>
+
+#include "ns_internal.cuh"
+
+namespace ns {
+
+struct PlanCostArgs {
+    long long row_begin, row_end;   // rows [row_begin, row_end) of the arrays below
+    int D;
+    const uint8_t* feas;            // [rows] or nullptr (all feasible)
+    const double* comp;             // [rows][D]
+    const int32_t* devdim;          // [rows][D]
+    double* cost;                   // [rows]
+    CommParams cp;
+    double start_scale, dim_scale;
+    int ldx, ldy;                   // smem row strides (doubles)
+};
+
+__device__ __forceinline__ void dmma(double (&c)[2], double a, double b) {
+    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+                 : "+d"(c[0]), "+d"(c[1])
+                 : "d"(a), "d"(b));
+}
+
+// Y[16 x N] = act(X[16 x K] . W^T + b) for the warp's 16 rows.
+// W is [N][K] row-major (torch Linear), K % 4 == 0 except the first layer
+// (guarded), N arbitrary (guarded).  RELU selects the hidden-layer epilogue.
+template <bool RELU>
+__device__ __forceinline__ void warp_layer(const double* __restrict__ W, const double* __restrict__ bias, int K,
+                                           int N, const double* X, int ldx, double* Y, int ldy, int lane) {
+    const int g = lane >> 2, t = lane & 3;
+    const int K4 = (K + 3) >> 2, N8 = (N + 7) >> 3;
+    for (int nc = 0; nc < N8; nc += 4) {
+        double acc[2][4][2];
+#pragma unroll
+        for (int m = 0; m < 2; ++m)
+#pragma unroll
+            for (int j = 0; j < 4; ++j) acc[m][j][0] = acc[m][j][1] = 0.0;
+        for (int kt = 0; kt < K4; ++kt) {
+            const int k = 4 * kt + t;
+            const double a0 = X[g * ldx + k];
+            const double a1 = X[(8 + g) * ldx + k];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                const int nt = nc + j;
+                if (nt < N8) {   // warp-uniform
+                    const int n = 8 * nt + g;
+                    const double b = (n < N && k < K) ? __ldg(W + (size_t)n * K + k) : 0.0;
+                    dmma(acc[0][j], a0, b);
+                    dmma(acc[1][j], a1, b);
+                }
+            }
+        }
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const int nt = nc + j;
+            if (nt >= N8) continue;
+            const int col = 8 * nt + 2 * t;
+#pragma unroll
+            for (int m = 0; m < 2; ++m) {
+                const int r = 8 * m + g;
+#pragma unroll
+                for (int e = 0; e < 2; ++e) {
+                    const int cc = col + e;
+                    if (cc < N) {
+                        double v = acc[m][j][e] + __ldg(bias + cc);
+                        if (RELU) v = v > 0.0 ? v : 0.0;
+                        Y[r * ldy + cc] = v;
+                    }
+                }
+            }
+        }
+    }
+    __syncwarp();
+}
+
+__global__ void __launch_bounds__(128) k_plan_cost_dmma(const PlanCostArgs a) {
+    extern __shared__ double psm[];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+    const int D = a.D, K0 = 2 * D;
+    const int per_warp = 16 * (a.ldx + a.ldy + 2 * D) + 16;
+    double* X = psm + (size_t)w * per_warp;
+    double* Y = X + 16 * a.ldx;
+    double* O = Y + 16 * a.ldy;          // [16][2D]: fwd, then bwd
+    double* mn = O + 16 * 2 * D;         // [16] min comp per row
+    const long long base = a.row_begin + ((long long)blockIdx.x * nwarps + w) * 16;
+    if (base >= a.row_end) return;
+    // per-row min comp (lane r < 16 owns row r)
+    if (lane < 16) {
+        const long long r = base + lane;
+        double m = 0.0;
+        if (r < a.row_end) {
+            m = CUDART_INF;
+            for (int d = 0; d < D; ++d) m = fmin(m, a.comp[r * D + d]);
+        }
+        mn[lane] = m;
+    }
+    __syncwarp();
+    for (int dir = 0; dir < 2; ++dir) {
+        // input rows [starts / start_scale (D), devdim / dim_scale (D)], zero padded
+        const int K0p = (K0 + 3) & ~3;
+        for (int i = lane; i < 16 * K0p; i += 32) {
+            const int r = i / K0p, c = i % K0p;
+            const long long row = base + r;
+            double v = 0.0;
+            if (row < a.row_end && c < K0) {
+                if (c < D)
+                    v = dir == 0 ? (a.comp[row * D + c] - mn[r]) / a.start_scale : 0.0;
+                else
+                    v = (double)a.devdim[row * D + (c - D)] / a.dim_scale;
+            }
+            X[r * a.ldx + c] = v;
+        }
+        __syncwarp();
+        warp_layer<true>(a.cp.W[dir][0], a.cp.b[dir][0], K0, 128, X, a.ldx, Y, a.ldy, lane);
+        warp_layer<true>(a.cp.W[dir][1], a.cp.b[dir][1], 128, 64, Y, a.ldy, X, a.ldx, lane);
+        warp_layer<true>(a.cp.W[dir][2], a.cp.b[dir][2], 64, 32, X, a.ldx, Y, a.ldy, lane);
+        warp_layer<true>(a.cp.W[dir][3], a.cp.b[dir][3], 32, 16, Y, a.ldy, X, a.ldx, lane);
+        warp_layer<false>(a.cp.W[dir][4], a.cp.b[dir][4], 16, D, X, a.ldx, O + dir * D, 2 * D, lane);
+    }
+    if (lane < 16) {
+        const long long row = base + lane;
+        if (row < a.row_end) {
+            double c = CUDART_INF;
+            if (!a.feas || a.feas[row]) {
+                c = -CUDART_INF;
+                for (int d = 0; d < D; ++d) c = fmax(c, (a.comp[row * D + d] + O[lane * 2 * D + d]) + O[lane * 2 * D + D + d]);
+            }
+            a.cost[row] = c;
+        }
+    }
+}
+
+static int ld_pad(int width) { return ((width + 15) / 16) * 16 + 4; }   // == 4 (mod 16): conflict-free A frags
+
+ns_status launch_plan_cost(ns_ctx* ctx, long long rb, long long re, const uint8_t* feas, const double* comp,
+                           const int32_t* devdim, double* cost) {
+    if (re <= rb) return NS_OK;
+    PlanCostArgs a;
+    a.row_begin = rb;
+    a.row_end = re;
+    a.D = ctx->model.D;
+    a.feas = feas;
+    a.comp = comp;
+    a.devdim = devdim;
+    a.cost = cost;
+    a.cp = comm_params(ctx);
+    a.start_scale = ctx->model.start_scale;
+    a.dim_scale = ctx->model.dim_scale;
+    const int K0p = (2 * a.D + 3) & ~3;
+    a.ldx = ld_pad(K0p > 64 ? K0p : 64);
+    a.ldy = ld_pad(128);
+    const size_t per_warp = (size_t)(16 * (a.ldx + a.ldy + 2 * a.D) + 16) * sizeof(double);
+    int wpb = 4;
+    while (wpb > 1 && per_warp * wpb > 110 * 1024) wpb >>= 1;
+    const size_t smem = per_warp * wpb;
+    cudaFuncSetAttribute(k_plan_cost_dmma, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    const long long rows = re - rb;
+    const long long blocks = (rows + 16LL * wpb - 1) / (16LL * wpb);
+    prof_begin(ctx, PK_FINALIZE);
+    k_plan_cost_dmma<<<(unsigned)blocks, wpb * 32, smem, ctx->stream>>>(a);
+    prof_end(ctx);
+    NS_LAUNCHED(ctx);
+    return NS_OK;
+}
+
+}  // namespace ns

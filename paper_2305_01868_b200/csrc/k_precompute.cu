@@ -155,7 +155,9 @@ __global__ void k_tables_validate(const ns_table_desc* desc, const int32_t* off,
 }  // namespace
 
 void launch_tables_validate(ns_ctx* ctx, const ns_tables* t) {
+    prof_begin(ctx, PK_VALIDATE);
     k_tables_validate<<<t->n_tasks, 128, 0, ctx->stream>>>(t->d_desc, t->d_off, t->d_sumdim, t->d_flag);
+    prof_end(ctx);
     ctx->launches++;
 }
 
@@ -187,7 +189,9 @@ void launch_precompute(ns_ctx* ctx, const ns_tables* t, int jlo, int jhi) {
     long long cap = (long long)ctx->sm_count * 3;
     int grid = (int)(blocks < cap ? blocks : cap);
     if (grid < 1) grid = 1;
+    prof_begin(ctx, PK_PRECOMPUTE);
     k_precompute<<<grid, kWarps * 32, smem, ctx->stream>>>(a);
+    prof_end(ctx);
     ctx->launches++;
 }
 

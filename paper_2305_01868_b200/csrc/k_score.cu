@@ -24,21 +24,22 @@ struct ScoreArgs {
     const int32_t* rows;      // [Tp] variant rows of the post-split list
     const double* V;
     const int32_t* vdim;
-    double* cost;             // [P] indexed by global plan index
+    double* comp;             // [P][D] (global plan index)
+    int32_t* devdim;          // [P][D]
+    uint8_t* ok;              // [P] 0 if the plan holds an invalid device id
     HeadParams head;
-    CommParams cp;
-    double start_scale, dim_scale;
 };
 
-__global__ void __launch_bounds__(128) k_score_fp64(const ScoreArgs a) {
+// Per plan (one warp): u_d = hb1 + sum_{t: a_t = d} v_t in shared memory
+// (lane = features k, k+32; tables in list order), comp_d = H2 ReLU(u_d) + hb2
+// for non-empty devices, 0 otherwise (R4), device dims.
+__global__ void __launch_bounds__(128) k_pool(const ScoreArgs a) {
     extern __shared__ double ssm[];
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, wpb = blockDim.x >> 5;
     const int D = a.D;
-    const size_t per_warp = (size_t)D * kV + D + (D + 1) / 2 + kPlanCostScratch(D);
+    const size_t per_warp = (size_t)D * kV + (D + 1) / 2;
     double* u = ssm + (size_t)w * per_warp;     // [D][64]
-    double* comp = u + (size_t)D * kV;          // [D]
-    int32_t* dd = (int32_t*)(comp + D);         // [D]
-    double* scratch = comp + D + (D + 1) / 2;
+    int32_t* dd = (int32_t*)(u + (size_t)D * kV);
     for (long long p = a.p_begin + (long long)blockIdx.x * wpb + w; p < a.p_end; p += (long long)gridDim.x * wpb) {
         for (int i = lane; i < D * kV; i += 32) u[i] = a.head.hb1[i % kV];
         for (int d = lane; d < D; d += 32) dd[d] = 0;
@@ -63,13 +64,19 @@ __global__ void __launch_bounds__(128) k_score_fp64(const ScoreArgs a) {
                           a.head.H2[lane + 32] * relu_exact(u[d * kV + lane + 32]);
 #pragma unroll
             for (int o = 16; o > 0; o >>= 1) part += __shfl_xor_sync(kFull, part, o);
-            if (lane == 0) comp[d] = dd[d] > 0 ? part + a.head.hb2 : 0.0;
+            if (lane == 0) {
+                a.comp[p * D + d] = dd[d] > 0 ? part + a.head.hb2 : 0.0;
+                a.devdim[p * D + d] = dd[d];
+            }
         }
-        __syncwarp();
-        const double c = warp_plan_cost(a.cp, comp, dd, scratch, lane, a.start_scale, a.dim_scale);
-        if (lane == 0) a.cost[p] = bad ? CUDART_NAN : c;
+        if (lane == 0) a.ok[p] = bad ? 0 : 1;
         __syncwarp();
     }
+}
+
+__global__ void k_mark_bad(const uint8_t* ok, double* cost, long long pb, long long pe) {
+    for (long long p = pb + (long long)blockIdx.x * blockDim.x + threadIdx.x; p < pe; p += (long long)gridDim.x * blockDim.x)
+        if (!ok[p]) cost[p] = CUDART_NAN;
 }
 
 struct BestRec {
@@ -155,8 +162,10 @@ ns_status run_score_plans(ns_ctx* ctx, const ns_tables* t, int task, int D, cons
     const long long pe = std::min<long long>(P, pb + per);
     const bool dev_assign = is_device_ptr(assign);
     const int nblk_arg = 296;
-    size_t need = 256 + (size_t)Tp * 4 + (size_t)P * 8 + (size_t)(nblk_arg + 2 + ctx->nranks) * sizeof(BestRec) + 1024;
-    if (!dev_assign) need += (size_t)(pe - pb) * Tp + 256;
+    const long long np_ = pe - pb;
+    size_t need = 256 + (size_t)Tp * 4 + (size_t)P * 8 + (size_t)(nblk_arg + 2 + ctx->nranks) * sizeof(BestRec) +
+                  (size_t)np_ * D * 12 + (size_t)np_ + 4096;
+    if (!dev_assign) need += (size_t)np_ * Tp + 256;
     char* base = (char*)arena_get(ctx, need);
     if (!base) return set_err(ctx, NS_ERR_NOMEM, "device arena (score)");
     size_t off = 0;
@@ -171,11 +180,13 @@ ns_status run_score_plans(ns_ctx* ctx, const ns_tables* t, int task, int D, cons
     BestRec* d_part = (BestRec*)take((size_t)nblk_arg * sizeof(BestRec));
     BestRec* d_best = (BestRec*)take(sizeof(BestRec));
     BestRec* d_all = (BestRec*)take((size_t)ctx->nranks * sizeof(BestRec));
+    double* d_comp = (double*)take((size_t)np_ * D * 8) - pb * D;        // global plan indexing
+    int32_t* d_dd = (int32_t*)take((size_t)np_ * D * 4) - pb * D;
+    uint8_t* d_ok = (uint8_t*)take((size_t)np_) - pb;
     const int8_t* d_assign = assign;
     if (!dev_assign && pe > pb) {
-        int8_t* tmp = (int8_t*)take((size_t)(pe - pb) * Tp);
-        NS_CUDA(ctx, cudaMemcpyAsync(tmp, assign + pb * Tp, (size_t)(pe - pb) * Tp, cudaMemcpyHostToDevice,
-                                     ctx->stream));
+        int8_t* tmp = (int8_t*)take((size_t)np_ * Tp);
+        NS_CUDA(ctx, cudaMemcpyAsync(tmp, assign + pb * Tp, (size_t)np_ * Tp, cudaMemcpyHostToDevice, ctx->stream));
         d_assign = tmp - pb * Tp;   // indexed by global plan index
     }
     NS_CUDA(ctx, cudaMemcpyAsync(d_rows, rows.data(), (size_t)Tp * 4, cudaMemcpyHostToDevice, ctx->stream));
@@ -188,37 +199,46 @@ ns_status run_score_plans(ns_ctx* ctx, const ns_tables* t, int task, int D, cons
     a.rows = d_rows;
     a.V = t->d_V;
     a.vdim = t->d_vdim;
-    a.cost = d_cost;
+    a.comp = d_comp;
+    a.devdim = d_dd;
+    a.ok = d_ok;
     a.head = ctx->model.head;
-    a.cp = comm_params(ctx);
-    a.start_scale = ctx->model.start_scale;
-    a.dim_scale = ctx->model.dim_scale;
     if (pe > pb) {
         if (mode == NS_SCORE_TF32X3) {
             ns_status s = run_score_plans_tf32x3(ctx, a, d_cost);
             if (s != NS_OK) return s;
         } else {
-            const size_t per_warp = ((size_t)D * kV + D + (D + 1) / 2 + kPlanCostScratch(D)) * sizeof(double);
+            const size_t per_warp = ((size_t)D * kV + (D + 1) / 2) * sizeof(double);
             int wpb = 4;
             while (wpb > 1 && per_warp * wpb > 96 * 1024) wpb >>= 1;
             const size_t smem = per_warp * wpb;
             if (smem > 48 * 1024)
-                cudaFuncSetAttribute(k_score_fp64, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-            const long long warps = pe - pb;
-            long long blocks = (warps + wpb - 1) / wpb;
+                cudaFuncSetAttribute(k_pool, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            long long blocks = (np_ + wpb - 1) / wpb;
             const long long cap = (long long)ctx->sm_count * 16;
             if (blocks > cap) blocks = cap;
-            k_score_fp64<<<(unsigned)blocks, wpb * 32, smem, ctx->stream>>>(a);
+            prof_begin(ctx, PK_SCORE);
+            k_pool<<<(unsigned)blocks, wpb * 32, smem, ctx->stream>>>(a);
+            prof_end(ctx);
+            NS_LAUNCHED(ctx);
+            ns_status s = launch_plan_cost(ctx, pb, pe, nullptr, d_comp, d_dd, d_cost);
+            if (s != NS_OK) return s;
+            k_mark_bad<<<(unsigned)std::min<long long>((np_ + 255) / 256, 4096), 256, 0, ctx->stream>>>(d_ok, d_cost, pb, pe);
             NS_LAUNCHED(ctx);
         }
     }
     k_argmin<<<nblk_arg, 256, 0, ctx->stream>>>(d_cost, pb, pe, d_part);
+    prof_end(ctx);
     NS_LAUNCHED(ctx);
+    prof_begin(ctx, PK_OTHER);
     k_argmin_final<<<1, 32, 0, ctx->stream>>>(d_part, nblk_arg, d_best);
+    prof_end(ctx);
     NS_LAUNCHED(ctx);
     ns_status s = comm_allgather(ctx, d_best, d_all, sizeof(BestRec));
     if (s != NS_OK) return s;
+    prof_begin(ctx, PK_OTHER);
     k_argmin_final<<<1, 32, 0, ctx->stream>>>(d_all, ctx->nranks, d_best);
+    prof_end(ctx);
     NS_LAUNCHED(ctx);
     if (cost_out && pe > pb)
         NS_CUDA(ctx, cudaMemcpyAsync(cost_out + pb, d_cost + pb, (size_t)(pe - pb) * 8, cudaMemcpyDefault,
@@ -226,6 +246,7 @@ ns_status run_score_plans(ns_ctx* ctx, const ns_tables* t, int task, int D, cons
     BestRec h;
     NS_CUDA(ctx, cudaMemcpyAsync(&h, d_best, sizeof(BestRec), cudaMemcpyDeviceToHost, ctx->stream));
     NS_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+    prof_collect(ctx);
     if (best_index_out) *best_index_out = h.idx;
     if (best_cost_out) *best_cost_out = h.cost;
     return NS_OK;

@@ -482,36 +482,6 @@ __global__ void __launch_bounds__(256) k_greedy_big(const GreedyArgs a) {
 }
 
 // ======================================================================
-// N5: evaluate each completed trajectory with the cost models (Alg. 2 /
-// PAPER.md:289 step 4): f = max_d(comp_d + fwd_d + bwd_d).  One warp per
-// trajectory, fp64.
-// ======================================================================
-struct FinArgs {
-    int traj_begin, traj_end, D;
-    const uint8_t* feas;
-    const double* comp;
-    const int32_t* devdim;
-    double* tcost;
-    CommParams cp;
-    double start_scale, dim_scale;
-};
-
-__global__ void __launch_bounds__(128) k_finalize(const FinArgs a) {
-    extern __shared__ double fsm[];
-    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-    const long long tau = a.traj_begin + ((long long)blockIdx.x * (blockDim.x >> 5) + w);
-    if (tau >= a.traj_end) return;
-    if (!a.feas[tau]) {
-        if (lane == 0) a.tcost[tau] = CUDART_INF;
-        return;
-    }
-    double* buf = fsm + (size_t)w * kPlanCostScratch(a.D);
-    const double c = warp_plan_cost(a.cp, a.comp + tau * a.D, a.devdim + tau * a.D, buf, lane,
-                                    a.start_scale, a.dim_scale);
-    if (lane == 0) a.tcost[tau] = c;
-}
-
-// ======================================================================
 // N6: per task, grid argmin of every child column plan (Alg. 2 lines 16-18,
 // reading R12: lowest m on ties), work totals, global best with strict < in
 // generation order (Alg. 1 lines 13-16), next beam = K lowest (cost, gen)
@@ -737,11 +707,14 @@ ns_status launch_greedy(ns_ctx* ctx, const SearchBufs& b, const ns_tables* t, lo
     const int seg = 2 * dp;
     if (seg > 32) {
         const int threads = ((2 * b.D + 31) / 32) * 32;
+        prof_begin(ctx, PK_GREEDY);
         k_greedy_big<<<(unsigned)n, threads, 0, ctx->stream>>>(a);
+        prof_end(ctx);
     } else {
         const long long tpw = 32 / seg;
         const long long warps = (n + tpw - 1) / tpw;
         const unsigned blocks = (unsigned)((warps + 3) / 4);
+        prof_begin(ctx, PK_GREEDY);
         switch (seg) {
             case 2: k_greedy_seg<2><<<blocks, 128, 0, ctx->stream>>>(a); break;
             case 4: k_greedy_seg<4><<<blocks, 128, 0, ctx->stream>>>(a); break;
@@ -749,30 +722,14 @@ ns_status launch_greedy(ns_ctx* ctx, const SearchBufs& b, const ns_tables* t, lo
             case 16: k_greedy_seg<16><<<blocks, 128, 0, ctx->stream>>>(a); break;
             default: k_greedy_seg<32><<<blocks, 128, 0, ctx->stream>>>(a); break;
         }
+        prof_end(ctx);
     }
     NS_LAUNCHED(ctx);
     return NS_OK;
 }
 
 ns_status launch_finalize(ns_ctx* ctx, const SearchBufs& b, long long tb, long long te) {
-    if (te <= tb) return NS_OK;
-    FinArgs f;
-    f.traj_begin = (int)tb;
-    f.traj_end = (int)te;
-    f.D = b.D;
-    f.feas = b.feas;
-    f.comp = b.comp;
-    f.devdim = b.devdim;
-    f.tcost = b.tcost;
-    f.cp = comm_params(ctx);
-    f.start_scale = ctx->model.start_scale;
-    f.dim_scale = ctx->model.dim_scale;
-    const int wpb = 4;
-    const size_t smem = (size_t)wpb * kPlanCostScratch(b.D) * sizeof(double);
-    const long long n = te - tb;
-    k_finalize<<<(unsigned)((n + wpb - 1) / wpb), wpb * 32, smem, ctx->stream>>>(f);
-    NS_LAUNCHED(ctx);
-    return NS_OK;
+    return launch_plan_cost(ctx, tb, te, b.feas, b.comp, b.devdim, b.tcost);
 }
 
 // Copy staged results to the caller's (host or device) pointers.
@@ -805,6 +762,7 @@ ns_status deliver(ns_ctx* ctx, const ns_tables* t, const OutStage& o, int Lout, 
     NS_CUDA(ctx, cudaMemcpyAsync(hflag, t->d_flag, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
     NS_CUDA(ctx, cp(out->cost, o.cost, n * sizeof(double)));
     NS_CUDA(ctx, cudaStreamSynchronize(st));
+    prof_collect(ctx);
     ns_status fs = check_tables_flag(ctx, t, hflag);
     if (fs != NS_OK) return fs;
     for (int q = 0; q < n; ++q)
@@ -835,8 +793,10 @@ ns_status run_search(ns_ctx* ctx, const ns_tables* t, int D, const ns_search_par
     Carver cv{base};
     carve(cv, b, o, Lout > 0 ? Lout : 1);
     ns_status s;
+    prof_begin(ctx, PK_OTHER);
     k_grid_caps<<<(b.n_tasks * b.M + 255) / 256, 256, 0, ctx->stream>>>(t->d_sumdim, b.n_tasks, b.D, b.M,
                                                                         p->grid_hi_factor, b.capdim);
+    prof_end(ctx);
     NS_LAUNCHED(ctx);
     const TaskView tv = task_view(t);
     const size_t osm = order_smem(b.Tpm);
@@ -845,30 +805,44 @@ ns_status run_search(ns_ctx* ctx, const ns_tables* t, int D, const ns_search_par
         cudaFuncSetAttribute(k_expand, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)osm);
     }
     // ---- level 0: the empty column plan (tablewise = this level only)
+    prof_begin(ctx, PK_OTHER);
     k_setup_level0<<<(b.n_tasks + 255) / 256, 256, 0, ctx->stream>>>(b);
+    prof_end(ctx);
     NS_LAUNCHED(ctx);
+    prof_begin(ctx, PK_ORDER);
     k_build_order<<<b.n_tasks, 256, osm, ctx->stream>>>(b, tv);
+    prof_end(ctx);
     NS_LAUNCHED(ctx);
     const long long n0 = (long long)b.n_tasks * b.M;
     if ((s = launch_greedy(ctx, b, t, 0, n0)) != NS_OK) return s;
     if ((s = launch_finalize(ctx, b, 0, n0)) != NS_OK) return s;
+    prof_begin(ctx, PK_SELECT);
     k_select<<<b.n_tasks, 128, (size_t)1 * 16, ctx->stream>>>(b, 1, 0, b.K);
+    prof_end(ctx);
     NS_LAUNCHED(ctx);
     // ---- beam levels (Alg. 1 lines 6-22)
     for (int level = 1; level <= L; ++level) {
         const size_t esm = (size_t)b.Tpm * 4 + (size_t)b.N2 * 4 * 2 + (size_t)b.N2 * 4 + 64;
         if (esm > 48 * 1024)
             cudaFuncSetAttribute(k_expand, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)esm);
+        prof_begin(ctx, PK_EXPAND);
         k_expand<<<b.n_tasks * b.K, 256, esm, ctx->stream>>>(b, tv, level);
+        prof_end(ctx);
         NS_LAUNCHED(ctx);
+        prof_begin(ctx, PK_ORDER);
         k_build_order<<<b.S, 256, osm, ctx->stream>>>(b, tv);
+        prof_end(ctx);
         NS_LAUNCHED(ctx);
         if ((s = launch_greedy(ctx, b, t, 0, b.n_traj)) != NS_OK) return s;
         if ((s = launch_finalize(ctx, b, 0, b.n_traj)) != NS_OK) return s;
+        prof_begin(ctx, PK_SELECT);
         k_select<<<b.n_tasks, 128, (size_t)C * 16, ctx->stream>>>(b, C, level, b.K);
+        prof_end(ctx);
         NS_LAUNCHED(ctx);
     }
+    prof_begin(ctx, PK_OTHER);
     k_write_out<<<b.n_tasks, 128, 0, ctx->stream>>>(b, o, Lout > 0 ? Lout : 1);
+    prof_end(ctx);
     NS_LAUNCHED(ctx);
     return deliver(ctx, t, o, Lout, b.Tpm, out);
 }

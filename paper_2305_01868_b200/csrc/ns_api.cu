@@ -84,6 +84,51 @@ CommParams comm_params(const ns_ctx* ctx) {
     return c;
 }
 
+static cudaEvent_t prof_event(ns_ctx* ctx) {
+    if (!ctx->prof_free.empty()) {
+        cudaEvent_t e = ctx->prof_free.back();
+        ctx->prof_free.pop_back();
+        return e;
+    }
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    return e;
+}
+
+void prof_begin(ns_ctx* ctx, int kind) {
+    if (!ctx->prof) return;
+    ProfPending p;
+    p.kind = kind;
+    p.a = prof_event(ctx);
+    p.b = nullptr;
+    cudaEventRecord(p.a, ctx->stream);
+    ctx->prof_pending.push_back(p);
+}
+
+void prof_end(ns_ctx* ctx) {
+    if (!ctx->prof || ctx->prof_pending.empty()) return;
+    ProfPending& p = ctx->prof_pending.back();
+    p.b = prof_event(ctx);
+    cudaEventRecord(p.b, ctx->stream);
+}
+
+void prof_collect(ns_ctx* ctx) {
+    for (ProfPending& p : ctx->prof_pending) {
+        if (p.b) {
+            float ms = 0.f;
+            if (cudaEventElapsedTime(&ms, p.a, p.b) == cudaSuccess) {
+                ctx->prof_acc[p.kind].total_ms += ms;
+                ctx->prof_acc[p.kind].launches += 1;
+            } else {
+                cudaGetLastError();
+            }
+            ctx->prof_free.push_back(p.b);
+        }
+        ctx->prof_free.push_back(p.a);
+    }
+    ctx->prof_pending.clear();
+}
+
 static void free_model(ns::DevModel& m) {
     double* ps[] = {m.enc1W, m.enc1b, m.enc2W, m.enc2b, m.H1};
     for (double* p : ps)
@@ -148,6 +193,8 @@ ns_status ns_destroy(ns_ctx* ctx) {
     free_model(ctx->model);
     if (ctx->arena) cudaFree(ctx->arena);
     if (ctx->pinned) cudaFreeHost(ctx->pinned);
+    prof_collect(ctx);
+    for (cudaEvent_t e : ctx->prof_free) cudaEventDestroy(e);
     comm_destroy(ctx);
     delete ctx;
     return NS_OK;
@@ -169,6 +216,33 @@ ns_status ns_synchronize(ns_ctx* ctx) {
 }
 
 uint64_t ns_kernel_launches(const ns_ctx* ctx) { return ctx ? ctx->launches : 0; }
+
+static const char* kProfNames[PK_COUNT] = {"precompute", "validate", "order", "expand", "greedy",
+                                            "finalize", "select", "score", "other"};
+
+ns_status ns_profile(ns_ctx* ctx, int32_t enable) {
+    if (!ctx) return NS_ERR_ARG;
+    cudaSetDevice(ctx->device);
+    NS_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+    prof_collect(ctx);
+    for (int k = 0; k < PK_COUNT; ++k) ctx->prof_acc[k] = ProfEntry();
+    ctx->prof = enable != 0;
+    return NS_OK;
+}
+
+ns_status ns_profile_query(ns_ctx* ctx, const char* kernel, double* total_ms, uint64_t* launches) {
+    if (!ctx || !kernel) return NS_ERR_ARG;
+    cudaSetDevice(ctx->device);
+    NS_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+    prof_collect(ctx);
+    for (int k = 0; k < PK_COUNT; ++k)
+        if (std::strcmp(kernel, kProfNames[k]) == 0) {
+            if (total_ms) *total_ms = ctx->prof_acc[k].total_ms;
+            if (launches) *launches = ctx->prof_acc[k].launches;
+            return NS_OK;
+        }
+    return set_err(ctx, NS_ERR_ARG, std::string("unknown kernel class ") + kernel);
+}
 
 static ns_status check_linear(ns_ctx* ctx, const ns_linear& l, int in, int out, const char* name) {
     if (l.in != in || l.out != out || !l.W || !l.b)

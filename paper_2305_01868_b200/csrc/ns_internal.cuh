@@ -59,6 +59,21 @@ struct CommParams {
 
 }  // namespace ns
 
+namespace ns {
+// Per-kernel-class timers (ns_profile): CUDA events around each launch on the
+// ctx stream, resolved at the next synchronising call.
+struct ProfEntry {
+    double total_ms = 0.0;
+    uint64_t launches = 0;
+};
+struct ProfPending {
+    int kind;
+    cudaEvent_t a, b;
+};
+enum ProfKind { PK_PRECOMPUTE = 0, PK_VALIDATE, PK_ORDER, PK_EXPAND, PK_GREEDY, PK_FINALIZE, PK_SELECT, PK_SCORE,
+                PK_OTHER, PK_COUNT };
+}  // namespace ns
+
 struct ns_ctx {
     int device = 0;
     cudaStream_t stream = nullptr;
@@ -72,6 +87,11 @@ struct ns_ctx {
     // pinned host staging
     void* pinned = nullptr;
     size_t pinned_bytes = 0;
+    // kernel timers
+    bool prof = false;
+    ns::ProfEntry prof_acc[ns::PK_COUNT];
+    std::vector<ns::ProfPending> prof_pending;
+    std::vector<cudaEvent_t> prof_free;
     // multi-GPU
     void* nccl = nullptr;    // ncclComm_t
     int nranks = 1, rank = 0;
@@ -119,6 +139,17 @@ ns_status run_score_plans(ns_ctx* ctx, const ns_tables* t, int task, int D,
                           const int32_t* col_plan, int n_col, const int8_t* assign, int64_t P,
                           int mode, double* cost_out, int64_t* best_index_out,
                           double* best_cost_out);
+
+// kernel timers (ns_api.cu): prof_begin before a launch, prof_end after it;
+// prof_collect after a stream synchronisation.
+void prof_begin(ns_ctx* ctx, int kind);
+void prof_end(ns_ctx* ctx);
+void prof_collect(ns_ctx* ctx);
+
+// N5 (k_mlp.cu): cost[r] = max_d(comp + fwd + bwd) for rows [rb, re) with the
+// comm MLPs on the FP64 tensor cores; rows with feas[r] == 0 get +inf.
+ns_status launch_plan_cost(ns_ctx* ctx, long long rb, long long re, const uint8_t* feas, const double* comp,
+                           const int32_t* devdim, double* cost);
 
 // helpers (ns_api.cu)
 ns_status set_err(ns_ctx* ctx, ns_status s, const std::string& msg);
