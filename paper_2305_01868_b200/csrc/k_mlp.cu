@@ -17,6 +17,7 @@
 #include <cuda_runtime.h>
 #include <math_constants.h>
 
+#include "ns_device.cuh"
 #include "ns_internal.cuh"
 
 namespace ns {
@@ -80,7 +81,7 @@ __device__ __forceinline__ void warp_layer(const double* __restrict__ W, const d
                 for (int e = 0; e < 2; ++e) {
                     const int cc = col + e;
                     if (cc < N) {
-                        double v = acc[m][j][e] + __ldg(bias + cc);
+                        double v = bias ? acc[m][j][e] + __ldg(bias + cc) : acc[m][j][e];
                         if (RELU) v = v > 0.0 ? v : 0.0;
                         Y[r * ldy + cc] = v;
                     }
@@ -148,6 +149,103 @@ __global__ void __launch_bounds__(128) k_plan_cost_dmma(const PlanCostArgs a) {
     }
 }
 
+// ---------------------------------------------------------------------------
+// N1 on the FP64 tensor cores: per-table cached cost-model precompute.
+// For every row (table g, split depth j): x = featurise(table, dim >> j)
+// (R1), e = ReLU(W2 ReLU(W1 x + b1) + b2) (encoder "128-32",
+// P:688; R2), v = H1 e (hoisted first head layer: H1 sum_t e_t + hb1 =
+// hb1 + sum_t v_t), C({t}) = H2 ReLU(v + hb1) + hb2.  The encoder and the
+// projection are a GEMM chain over rows; one warp owns 16 rows.
+struct PreDmmaArgs {
+    const ns_table_desc* desc;
+    long long n_rows;        // n_tables * nj
+    int jlo, nj;
+    const double* enc1W;
+    const double* enc1b;
+    const double* enc2W;
+    const double* enc2b;
+    const double* H1;
+    HeadParams head;
+    double* feat;
+    double* V;
+    double* C;
+    int32_t* vdim;
+    int64_t* vbytes;
+    int ldx, ldy;
+};
+
+__global__ void __launch_bounds__(128) k_precompute_dmma(const PreDmmaArgs a) {
+    extern __shared__ double qsm[];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+    const int per_warp = 16 * (a.ldx + a.ldy);
+    double* X = qsm + (size_t)w * per_warp;
+    double* Y = X + 16 * a.ldx;
+    for (long long base = ((long long)blockIdx.x * nwarps + w) * 16; base < a.n_rows;
+         base += (long long)gridDim.x * nwarps * 16) {
+        // features of the 16 rows (lane r < 16 owns row r); invalid variants -> zeros
+        if (lane < 16) {
+            const long long r = base + lane;
+            double x[kF] = {0, 0, 0, 0, 0};
+            if (r < a.n_rows) {
+                const long long gtab = r / a.nj;
+                const int j = a.jlo + (int)(r % a.nj);
+                const ns_table_desc td = a.desc[gtab];
+                bool ok = true;
+                int dim = td.dim;
+                for (int k = 0; k < j; ++k) {
+                    if (dim % 8 != 0) ok = false;
+                    dim >>= 1;
+                }
+                const long long row = gtab * kDepth + j;
+                if (ok) {
+                    x[0] = (double)dim / 128.0;
+                    x[1] = log10((double)td.hash_size) / 8.0;
+                    x[2] = td.pooling_factor / 50.0;
+                    x[3] = td.skew / 2.0;
+                    x[4] = (double)td.hash_size * (double)dim * 4.0 / 1073741824.0;
+                    for (int f = 0; f < kF; ++f) a.feat[row * kF + f] = x[f];
+                    a.vdim[row] = dim;
+                    a.vbytes[row] = td.hash_size * (long long)dim * 4;
+                } else {
+                    a.vdim[row] = 0;
+                }
+            }
+#pragma unroll
+            for (int f = 0; f < kF; ++f) X[lane * a.ldx + f] = x[f];
+            for (int f = kF; f < 8; ++f) X[lane * a.ldx + f] = 0.0;
+        }
+        __syncwarp();
+        warp_layer<true>(a.enc1W, a.enc1b, kF, kH, X, a.ldx, Y, a.ldy, lane);     // 5 -> 128
+        warp_layer<true>(a.enc2W, a.enc2b, kH, kE, Y, a.ldy, X, a.ldx, lane);     // 128 -> 32 (e)
+        warp_layer<false>(a.H1, nullptr, kE, kV, X, a.ldx, Y, a.ldy, lane);       // v = H1 e
+        // write v (coalesced) and the single-table cost
+        for (int i = lane; i < 16 * kV; i += 32) {
+            const int r = i / kV, k = i % kV;
+            const long long rr = base + r;
+            if (rr < a.n_rows) {
+                const long long row = (rr / a.nj) * kDepth + a.jlo + (int)(rr % a.nj);
+                a.V[row * kV + k] = Y[r * a.ldy + k];
+            }
+        }
+        if (lane < 16) {
+            const long long rr = base + lane;
+            if (rr < a.n_rows) {
+                const long long row = (rr / a.nj) * kDepth + a.jlo + (int)(rr % a.nj);
+                double c0 = 0.0, c1 = 0.0, c2 = 0.0, c3 = 0.0;
+                for (int k = 0; k < kV; k += 4) {
+                    const double* y = Y + lane * a.ldy + k;
+                    c0 = fma(a.head.H2[k], relu_exact(y[0] + a.head.hb1[k]), c0);
+                    c1 = fma(a.head.H2[k + 1], relu_exact(y[1] + a.head.hb1[k + 1]), c1);
+                    c2 = fma(a.head.H2[k + 2], relu_exact(y[2] + a.head.hb1[k + 2]), c2);
+                    c3 = fma(a.head.H2[k + 3], relu_exact(y[3] + a.head.hb1[k + 3]), c3);
+                }
+                a.C[row] = a.head.hb2 + ((c0 + c1) + (c2 + c3));
+            }
+        }
+        __syncwarp();
+    }
+}
+
 static int ld_pad(int width) { return ((width + 15) / 16) * 16 + 4; }   // == 4 (mod 16): conflict-free A frags
 
 ns_status launch_plan_cost(ns_ctx* ctx, long long rb, long long re, const uint8_t* feas, const double* comp,
@@ -179,6 +277,38 @@ ns_status launch_plan_cost(ns_ctx* ctx, long long rb, long long re, const uint8_
     prof_end(ctx);
     NS_LAUNCHED(ctx);
     return NS_OK;
+}
+
+void launch_precompute(ns_ctx* ctx, const ns_tables* t, int jlo, int jhi) {
+    PreDmmaArgs a;
+    a.desc = t->d_desc;
+    a.nj = jhi - jlo + 1;
+    a.jlo = jlo;
+    a.n_rows = (long long)t->n_tables * a.nj;
+    a.enc1W = ctx->model.enc1W;
+    a.enc1b = ctx->model.enc1b;
+    a.enc2W = ctx->model.enc2W;
+    a.enc2b = ctx->model.enc2b;
+    a.H1 = ctx->model.H1;
+    a.head = ctx->model.head;
+    a.feat = t->d_feat;
+    a.V = t->d_V;
+    a.C = t->d_C;
+    a.vdim = t->d_vdim;
+    a.vbytes = t->d_vbytes;
+    a.ldx = ld_pad(kE > 8 ? kE : 8);   // holds x (8) and e (32)
+    a.ldy = ld_pad(kH);                // holds h (128) and v (64)
+    const int wpb = 4;
+    const size_t smem = (size_t)wpb * 16 * (a.ldx + a.ldy) * sizeof(double);
+    cudaFuncSetAttribute(k_precompute_dmma, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    long long blocks = (a.n_rows + 16LL * wpb - 1) / (16LL * wpb);
+    const long long cap = (long long)ctx->sm_count * 8;
+    if (blocks > cap) blocks = cap;
+    if (blocks < 1) blocks = 1;
+    prof_begin(ctx, PK_PRECOMPUTE);
+    k_precompute_dmma<<<(unsigned)blocks, wpb * 32, smem, ctx->stream>>>(a);
+    prof_end(ctx);
+    ctx->launches++;
 }
 
 }  // namespace ns

@@ -215,8 +215,6 @@ __global__ void k_build_order(SearchBufs b, TaskView tv) {
 // features keeps u, H2 and the streamed v chunk resident (~170 regs) for one
 // extra shuffle + add per score.
 // ======================================================================
-constexpr int kHalf = kV / 2;
-
 struct GreedyArgs {
     int traj_begin, traj_end, M, D, Tpm;
     long long n_rows;
@@ -238,16 +236,24 @@ struct GreedyArgs {
     HeadParams head;
 };
 
-// Half dot product sum_{k<32} w[k] ReLU(u[k] + v[k]), 4 partial accumulators,
-// v streamed from L1/L2 in chunks of 8 doubles.
-__device__ __forceinline__ double half_score(const double (&u)[kHalf], const double (&w)[kHalf],
+// Features per lane FPL = 64 / LPD (LPD = lanes per device).
+template <bool SMEM>
+__device__ __forceinline__ double2 ld_v2(const double2* p) {
+    if constexpr (SMEM) return *p;
+    else return __ldg(p);
+}
+
+// Partial dot product sum_{k<FPL} w[k] ReLU(u[k] + v[k]) with 4 accumulators,
+// v streamed in chunks of 8 doubles.
+template <int FPL, bool SMEM>
+__device__ __forceinline__ double part_score(const double (&u)[FPL], const double (&w)[FPL],
                                              const double2* __restrict__ v2) {
     double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
 #pragma unroll
-    for (int c = 0; c < kHalf / 8; ++c) {
+    for (int c = 0; c < FPL / 8; ++c) {
         double2 vv[4];
 #pragma unroll
-        for (int i = 0; i < 4; ++i) vv[i] = __ldg(v2 + c * 4 + i);
+        for (int i = 0; i < 4; ++i) vv[i] = ld_v2<SMEM>(v2 + c * 4 + i);
 #pragma unroll
         for (int i = 0; i < 4; i += 2) {
             const int k = c * 8 + 2 * i;
@@ -260,13 +266,14 @@ __device__ __forceinline__ double half_score(const double (&u)[kHalf], const dou
     return (a0 + a1) + (a2 + a3);
 }
 
-// u += v (the chosen device's lanes only)
-__device__ __forceinline__ void half_add(double (&u)[kHalf], const double2* __restrict__ v2) {
+// u += v (only the chosen device's lanes execute it)
+template <int FPL, bool SMEM>
+__device__ __forceinline__ void part_add(double (&u)[FPL], const double2* __restrict__ v2) {
 #pragma unroll
-    for (int c = 0; c < kHalf / 8; ++c) {
+    for (int c = 0; c < FPL / 8; ++c) {
         double2 vv[4];
 #pragma unroll
-        for (int i = 0; i < 4; ++i) vv[i] = __ldg(v2 + c * 4 + i);
+        for (int i = 0; i < 4; ++i) vv[i] = ld_v2<SMEM>(v2 + c * 4 + i);
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
             u[c * 8 + 2 * i] += vv[i].x;
@@ -275,16 +282,26 @@ __device__ __forceinline__ void half_add(double (&u)[kHalf], const double2* __re
     }
 }
 
-__device__ __forceinline__ double half_head(const double (&u)[kHalf], const double (&w)[kHalf]) {
+template <int FPL>
+__device__ __forceinline__ double part_head(const double (&u)[FPL], const double (&w)[FPL]) {
     double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
 #pragma unroll
-    for (int k = 0; k < kHalf; k += 4) {
+    for (int k = 0; k < FPL; k += 4) {
         a0 = fma(w[k + 0], relu_exact(u[k + 0]), a0);
         a1 = fma(w[k + 1], relu_exact(u[k + 1]), a1);
         a2 = fma(w[k + 2], relu_exact(u[k + 2]), a2);
         a3 = fma(w[k + 3], relu_exact(u[k + 3]), a3);
     }
     return (a0 + a1) + (a2 + a3);
+}
+
+// Sum of the LPD partials of one device (xor butterfly; IEEE addition is
+// commutative so every lane of the device holds the identical value).
+template <int LPD>
+__device__ __forceinline__ double lane_group_sum(double x) {
+#pragma unroll
+    for (int o = LPD / 2; o > 0; o >>= 1) x += __shfl_xor_sync(kFull, x, o);
+    return x;
 }
 
 __device__ __forceinline__ void argmin_step(double& bs, int& bd, int o) {
@@ -296,111 +313,148 @@ __device__ __forceinline__ void argmin_step(double& bs, int& bd, int o) {
     }
 }
 
-// SEG = 2 * pow2(D) <= 32 lanes per trajectory, 32/SEG trajectories per warp.
-template <int SEG>
-__global__ void __launch_bounds__(128) k_greedy_seg(const GreedyArgs a) {
-    constexpr int TPW = 32 / SEG;
-    constexpr unsigned SEGMASK = SEG == 32 ? kFull : ((1u << SEG) - 1u);
-    const int lane = threadIdx.x & 31;
-    const long long gw = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    const int seg = lane / SEG;
-    const int d = (lane % SEG) >> 1, h = lane & 1;
-    const long long tau = a.traj_begin + gw * TPW + seg;
-    const bool in_range = tau < a.traj_end;
-    bool alive = in_range;
-    int g = 0, m = 0, Tp = 0, capd = 0;
-    long long cap = 0;
-    if (alive) {
-        g = (int)(tau / a.M);
-        m = (int)(tau % a.M);
-        alive = a.cp_valid[g] != 0;
+// Per-lane slice of hb1 (initial u) and H2 (head weights); the weights are
+// made opaque so the compiler keeps them in registers instead of
+// re-loading them from the constant bank with a lane-dependent address.
+template <int FPL>
+__device__ __forceinline__ void load_lane_head(const HeadParams& hp, int part, double (&u)[FPL], double (&w)[FPL]) {
+#pragma unroll
+    for (int k = 0; k < FPL; ++k) {
+        double hu = hp.hb1[k], hw = hp.H2[k];
+#pragma unroll
+        for (int q = 1; q < kV / FPL; ++q)
+            if (part == q) {
+                hu = hp.hb1[q * FPL + k];
+                hw = hp.H2[q * FPL + k];
+            }
+        u[k] = hu;
+        w[k] = hw;
+        asm volatile("" : "+d"(w[k]));
     }
-    if (alive) {
+}
+
+// Staged greedy: one CTA per (column plan, chunk of grid points).  All
+// trajectories of a column plan consume the same cost-ordered table stream,
+// so the CTA stages the v rows (and dim / bytes / list index) of the next
+// kRing tables into shared memory once and every lane reads its slice from
+// there (broadcast within a segment; the LPD slices of a row are padded
+// 16 B apart so they fall on different banks) instead of each warp walking
+// the order and the rows through L1/L2.
+constexpr int kRing = 40;   // tables staged per chunk (C2: the whole task)
+
+template <int SEG, int LPD>
+__global__ void __launch_bounds__(256) k_greedy_cta(const GreedyArgs a, int mchunk, int nchunk) {
+    constexpr int FPL = kV / LPD;
+    constexpr int PSTR = FPL + 2;            // slice stride (doubles)
+    constexpr int RSTR = LPD * PSTR;         // row stride (doubles)
+    __shared__ __align__(16) double s_v[kRing * RSTR];
+    __shared__ int s_dim[kRing];
+    __shared__ long long s_bytes[kRing];
+    __shared__ int s_idx[kRing];
+    constexpr unsigned SEGMASK = SEG == 32 ? kFull : ((1u << SEG) - 1u);
+    const int g = blockIdx.x / nchunk, chunk = blockIdx.x % nchunk;
+    const int lane = threadIdx.x & 31;
+    const int j = threadIdx.x / SEG;                      // local trajectory
+    const int seg = lane / SEG;
+    const int ls = threadIdx.x % SEG;
+    const int d = ls / LPD, part = ls % LPD;
+    const int m = chunk * mchunk + j;
+    const long long tau = (long long)g * a.M + m;
+    const bool in_range = j < mchunk && m < a.M && tau >= a.traj_begin && tau < a.traj_end;
+    const bool valid = a.cp_valid[g] != 0;
+    bool alive = in_range && valid;
+    int Tp = 0, capd = 0;
+    long long cap = 0;
+    if (valid) {
         const int q = a.cp_task[g];
         Tp = a.cp_Tp[g];
         cap = a.cap[q];
-        capd = a.capdim[q * a.M + m];
+        if (in_range) capd = a.capdim[q * a.M + m];
     }
     const bool dev = d < a.D;
-    double u[kHalf], w[kHalf];
-#pragma unroll
-    for (int k = 0; k < kHalf; ++k) {
-        u[k] = h ? a.head.hb1[kHalf + k] : a.head.hb1[k];
-        w[k] = h ? a.head.H2[kHalf + k] : a.head.H2[k];
-    }
+    double u[FPL], w[FPL];
+    load_lane_head<FPL>(a.head, part, u, w);
     int dsum = 0;
     long long bsum = 0;
     uint32_t work = 0;
-    int Tmax = alive ? Tp : 0;
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) Tmax = max(Tmax, __shfl_xor_sync(kFull, Tmax, o));
     const int32_t* orow = a.ord_row + (size_t)g * a.Tpm;
     const int32_t* oidx = a.ord_idx + (size_t)g * a.Tpm;
     int8_t* asg = a.assign + (size_t)(in_range ? tau : 0) * a.Tpm;
+    const int Tmax = valid ? Tp : 0;   // uniform over the CTA
+    for (int p0 = 0; p0 < Tmax; p0 += kRing) {
+        const int np = min(kRing, Tmax - p0);
+        __syncthreads();   // previous chunk fully consumed
+        for (int i = threadIdx.x; i < np * (kV / 2); i += blockDim.x) {
+            const int r = i / (kV / 2), c2 = i % (kV / 2);
+            const int row = __ldg(orow + p0 + r);
+            const double2 v = __ldg(reinterpret_cast<const double2*>(a.V + (size_t)row * kV) + c2);
+            const int k = 2 * c2;
+            *reinterpret_cast<double2*>(s_v + r * RSTR + (k / FPL) * PSTR + (k % FPL)) = v;
+        }
+        for (int r = threadIdx.x; r < np; r += blockDim.x) {
+            const int row = __ldg(orow + p0 + r);
+            s_dim[r] = __ldg(a.vdim + row);
+            s_bytes[r] = __ldg(a.vbytes + row);
+            s_idx[r] = __ldg(oidx + p0 + r);
+        }
+        __syncthreads();
 #pragma unroll 1
-    for (int p = 0; p < Tmax; ++p) {
-        const bool act = alive && p < Tp;
-        int row = 0, dt = 0;
-        long long bt = 0;
-        if (act) {
-            row = __ldg(orow + p);
-            dt = __ldg(a.vdim + row);
-            bt = __ldg(a.vbytes + row);
-        }
-#ifdef NS_DEBUG
-        if (act && (row < 0 || row >= a.n_rows))
-            printf("bad row %d tau %lld g %d p %d Tp %d lane %d\n", row, tau, g, p, Tp, lane);
-#endif
-        const bool f = act && dev && (bsum + bt <= cap) && (dsum + dt <= capd);
-        const double2* v2 = reinterpret_cast<const double2*>(a.V + (size_t)row * kV + h * kHalf);
-        double part = 0.0;
-        if (f) part = half_score(u, w, v2);
-        double bs = a.head.hb2 + (part + __shfl_xor_sync(kFull, part, 1));
-        if (!f) bs = CUDART_INF;
-        int bd = d;
+        for (int r = 0; r < np; ++r) {
+            const bool act = alive;   // p0 + r < Tp == Tmax
+            const int dt = s_dim[r];
+            const long long bt = s_bytes[r];
+            const bool f = act && dev && (bsum + bt <= cap) && (dsum + dt <= capd);
+            const double2* v2 = reinterpret_cast<const double2*>(s_v + r * RSTR + part * PSTR);
+            double ps = 0.0;
+            if (f) ps = part_score<FPL, true>(u, w, v2);
+            double bs = a.head.hb2 + lane_group_sum<LPD>(ps);
+            if (!f) bs = CUDART_INF;
+            int bd = d;
 #pragma unroll
-        for (int o = SEG / 2; o > 1; o >>= 1) argmin_step(bs, bd, o);
-#ifdef NS_DEBUG
-        if (act && (bd < 0 || bd >= 64)) printf("bad bd %d tau %lld p %d lane %d bs %g\n", bd, tau, p, lane, bs);
-#endif
-        const unsigned bal = __ballot_sync(kFull, f && h == 0);
-        if (act) {
-            work += __popc((bal >> (seg * SEG)) & SEGMASK);
-            if (bs == CUDART_INF) alive = false;   // reading R9: stranded -> grid point infeasible
+            for (int o = SEG / 2; o >= LPD; o >>= 1) argmin_step(bs, bd, o);
+            const unsigned bal = __ballot_sync(kFull, f && part == 0);
+            if (act) {
+                work += __popc((bal >> (seg * SEG)) & SEGMASK);
+                if (bs == CUDART_INF) alive = false;   // R9: stranded -> grid point infeasible
+            }
+            if (act && bs != CUDART_INF) {
+                if (d == bd) {
+                    part_add<FPL, true>(u, v2);
+                    dsum += dt;
+                    bsum += bt;
+                }
+                if (ls == 0) asg[s_idx[r]] = (int8_t)bd;
+            }
         }
-        const bool take = act && bs != CUDART_INF && d == bd;
-        if (take) {   // only the chosen device's two lanes load and add v_t
-            half_add(u, v2);
-            dsum += dt;
-            bsum += bt;
-        }
-        if (act && bs != CUDART_INF && (lane % SEG) == 0) asg[__ldg(oidx + p)] = (int8_t)bd;
     }
-    const double hp = half_head(u, w);
-    const double hc = a.head.hb2 + (hp + __shfl_xor_sync(kFull, hp, 1));
+    const double hc = a.head.hb2 + lane_group_sum<LPD>(part_head<FPL>(u, w));
     if (in_range) {
-        if (dev && h == 0) {
+        if (dev && part == 0) {
             a.comp[tau * a.D + d] = dsum > 0 ? hc : 0.0;   // reading R4
             a.devdim[tau * a.D + d] = dsum;
         }
-        if ((lane % SEG) == 0) {
+        if (ls == 0) {
             a.feas[tau] = alive ? 1 : 0;
             a.work[tau] = work;
         }
     }
 }
 
-// 2*pow2(D) > 32: one trajectory per CTA of ceil(2D/32) warps; cross-warp
-// argmin through shared memory (double-buffered by step parity).
-__global__ void __launch_bounds__(256) k_greedy_big(const GreedyArgs a) {
-    __shared__ double s_sc[2][8];
-    __shared__ int s_dv[2][8];
-    __shared__ int s_cnt[2][8];
+// Large D (LPD * pow2(D) > 32, e.g. C5's 128 simulated GPUs): one trajectory
+// per CTA of LPD * D threads; cross-warp argmin through shared memory
+// (double-buffered by step parity); v rows read through L1/L2 (no other
+// trajectory of the CTA would share a staged row).
+template <int LPD>
+__global__ void __launch_bounds__(512) k_greedy_big(const GreedyArgs a) {
+    constexpr int FPL = kV / LPD;
+    __shared__ double s_sc[2][16];
+    __shared__ int s_dv[2][16];
+    __shared__ int s_cnt[2][16];
     const int lane = threadIdx.x & 31, wi = threadIdx.x >> 5, nw = blockDim.x >> 5;
     const long long tau = a.traj_begin + blockIdx.x;
     if (tau >= a.traj_end) return;
     const int g = (int)(tau / a.M), m = (int)(tau % a.M);
-    const int d = threadIdx.x >> 1, h = threadIdx.x & 1;
+    const int d = threadIdx.x / LPD, part = threadIdx.x % LPD;
     bool alive = a.cp_valid[g] != 0;
     int Tp = 0, capd = 0;
     long long cap = 0;
@@ -411,12 +465,8 @@ __global__ void __launch_bounds__(256) k_greedy_big(const GreedyArgs a) {
         capd = a.capdim[q * a.M + m];
     }
     const bool dev = d < a.D;
-    double u[kHalf], w[kHalf];
-#pragma unroll
-    for (int k = 0; k < kHalf; ++k) {
-        u[k] = h ? a.head.hb1[kHalf + k] : a.head.hb1[k];
-        w[k] = h ? a.head.H2[kHalf + k] : a.head.H2[k];
-    }
+    double u[FPL], w[FPL];
+    load_lane_head<FPL>(a.head, part, u, w);
     int dsum = 0;
     long long bsum = 0;
     uint32_t work = 0;
@@ -430,15 +480,15 @@ __global__ void __launch_bounds__(256) k_greedy_big(const GreedyArgs a) {
         const int dt = __ldg(a.vdim + row);
         const long long bt = __ldg(a.vbytes + row);
         const bool f = dev && (bsum + bt <= cap) && (dsum + dt <= capd);
-        const double2* v2 = reinterpret_cast<const double2*>(a.V + (size_t)row * kV + h * kHalf);
-        double part = 0.0;
-        if (f) part = half_score(u, w, v2);
-        double bs = a.head.hb2 + (part + __shfl_xor_sync(kFull, part, 1));
+        const double2* v2 = reinterpret_cast<const double2*>(a.V + (size_t)row * kV + part * FPL);
+        double ps = 0.0;
+        if (f) ps = part_score<FPL, false>(u, w, v2);
+        double bs = a.head.hb2 + lane_group_sum<LPD>(ps);
         if (!f) bs = CUDART_INF;
         int bd = d;
 #pragma unroll
-        for (int o = 16; o > 1; o >>= 1) argmin_step(bs, bd, o);
-        const unsigned bal = __ballot_sync(kFull, f && h == 0);
+        for (int o = 16; o >= LPD; o >>= 1) argmin_step(bs, bd, o);
+        const unsigned bal = __ballot_sync(kFull, f && part == 0);
         if (lane == 0) {
             s_sc[par][wi] = bs;
             s_dv[par][wi] = bd;
@@ -463,15 +513,14 @@ __global__ void __launch_bounds__(256) k_greedy_big(const GreedyArgs a) {
             break;   // uniform across the CTA
         }
         if (d == bd) {
-            half_add(u, v2);
+            part_add<FPL, false>(u, v2);
             dsum += dt;
             bsum += bt;
         }
         if (threadIdx.x == 0) asg[__ldg(oidx + p)] = (int8_t)bd;
     }
-    const double hp = half_head(u, w);
-    const double hc = a.head.hb2 + (hp + __shfl_xor_sync(kFull, hp, 1));
-    if (dev && h == 0) {
+    const double hc = a.head.hb2 + lane_group_sum<LPD>(part_head<FPL>(u, w));
+    if (dev && part == 0) {
         a.comp[tau * a.D + d] = dsum > 0 ? hc : 0.0;
         a.devdim[tau * a.D + d] = dsum;
     }
@@ -704,23 +753,46 @@ ns_status launch_greedy(ns_ctx* ctx, const SearchBufs& b, const ns_tables* t, lo
     const long long n = te - tb;
     int dp = 1;
     while (dp < b.D) dp <<= 1;
-    const int seg = 2 * dp;
+    // lanes per device: 4 (16 features/lane) when a trajectory fits a warp,
+    // else 2, else the one-trajectory-per-CTA kernel
+    const int lpd = (4 * dp <= 32) ? 4 : 2;
+    const int seg = lpd * dp;
     if (seg > 32) {
-        const int threads = ((2 * b.D + 31) / 32) * 32;
+        const int threads = ((4 * b.D + 31) / 32) * 32;
         prof_begin(ctx, PK_GREEDY);
-        k_greedy_big<<<(unsigned)n, threads, 0, ctx->stream>>>(a);
+        k_greedy_big<4><<<(unsigned)n, threads, 0, ctx->stream>>>(a);
         prof_end(ctx);
     } else {
-        const long long tpw = 32 / seg;
-        const long long warps = (n + tpw - 1) / tpw;
-        const unsigned blocks = (unsigned)((warps + 3) / 4);
+        // CTA per (column plan, chunk of grid points); trajectories of a
+        // column plan are contiguous: tau = g * M + m
+        const int mchunk = std::min(b.M, 256 / seg);
+        const int nchunk = (b.M + mchunk - 1) / mchunk;
+        const int threads = ((mchunk * seg + 31) / 32) * 32;
+        const long long g0 = tb / b.M, g1 = (te - 1) / b.M + 1;
+        GreedyArgs a2 = a;
+        a2.ord_row = b.ord_row + (size_t)g0 * b.Tpm;
+        a2.ord_idx = b.ord_idx + (size_t)g0 * b.Tpm;
+        a2.cp_valid = b.cp_valid + g0;
+        a2.cp_task = b.cp_task + g0;
+        a2.cp_Tp = b.cp_Tp + g0;
+        a2.traj_begin = (int)(tb - g0 * b.M);
+        a2.traj_end = (int)(te - g0 * b.M);
+        a2.assign = b.assign + (size_t)g0 * b.M * b.Tpm;
+        a2.comp = b.comp + (size_t)g0 * b.M * b.D;
+        a2.devdim = b.devdim + (size_t)g0 * b.M * b.D;
+        a2.feas = b.feas + (size_t)g0 * b.M;
+        a2.work = b.work + (size_t)g0 * b.M;
+        const unsigned blocks = (unsigned)((g1 - g0) * nchunk);
         prof_begin(ctx, PK_GREEDY);
         switch (seg) {
-            case 2: k_greedy_seg<2><<<blocks, 128, 0, ctx->stream>>>(a); break;
-            case 4: k_greedy_seg<4><<<blocks, 128, 0, ctx->stream>>>(a); break;
-            case 8: k_greedy_seg<8><<<blocks, 128, 0, ctx->stream>>>(a); break;
-            case 16: k_greedy_seg<16><<<blocks, 128, 0, ctx->stream>>>(a); break;
-            default: k_greedy_seg<32><<<blocks, 128, 0, ctx->stream>>>(a); break;
+            case 4: k_greedy_cta<4, 4><<<blocks, threads, 0, ctx->stream>>>(a2, mchunk, nchunk); break;
+            case 8: k_greedy_cta<8, 4><<<blocks, threads, 0, ctx->stream>>>(a2, mchunk, nchunk); break;
+            case 16: k_greedy_cta<16, 4><<<blocks, threads, 0, ctx->stream>>>(a2, mchunk, nchunk); break;
+            case 32:
+                if (lpd == 4) k_greedy_cta<32, 4><<<blocks, threads, 0, ctx->stream>>>(a2, mchunk, nchunk);
+                else k_greedy_cta<32, 2><<<blocks, threads, 0, ctx->stream>>>(a2, mchunk, nchunk);
+                break;
+            default: return set_err(ctx, NS_ERR_INTERNAL, "bad greedy segment");
         }
         prof_end(ctx);
     }
