@@ -32,6 +32,8 @@ struct PlanCostArgs {
     CommParams cp;
     double start_scale, dim_scale;
     int ldx, ldy;                   // smem row strides (doubles)
+    const int32_t* list;            // optional: rows = list[i], i < *list_n (then row_begin = 0, row_end = capacity)
+    const int32_t* list_n;
 };
 
 __device__ __forceinline__ void dmma(double (&c)[2], double a, double b) {
@@ -96,18 +98,23 @@ __global__ void __launch_bounds__(128) k_plan_cost_dmma(const PlanCostArgs a) {
     extern __shared__ double psm[];
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
     const int D = a.D, K0 = 2 * D;
-    const int per_warp = 16 * (a.ldx + a.ldy + 2 * D) + 16;
+    const int per_warp = 16 * (a.ldx + a.ldy + 2 * D) + 32;
     double* X = psm + (size_t)w * per_warp;
     double* Y = X + 16 * a.ldx;
     double* O = Y + 16 * a.ldy;          // [16][2D]: fwd, then bwd
     double* mn = O + 16 * 2 * D;         // [16] min comp per row
+    long long* rid = (long long*)(mn + 16);
     const long long base = a.row_begin + ((long long)blockIdx.x * nwarps + w) * 16;
-    if (base >= a.row_end) return;
-    // per-row min comp (lane r < 16 owns row r)
+    const long long end = a.list ? a.row_begin + *a.list_n : a.row_end;
+    if (base >= end) return;
+    // row ids and per-row min comp (lane r < 16 owns row r)
     if (lane < 16) {
-        const long long r = base + lane;
+        const long long i = base + lane;
+        long long r = -1;
+        if (i < end) r = a.list ? (long long)a.list[i] : i;
+        rid[lane] = r;
         double m = 0.0;
-        if (r < a.row_end) {
+        if (r >= 0) {
             m = CUDART_INF;
             for (int d = 0; d < D; ++d) m = fmin(m, a.comp[r * D + d]);
         }
@@ -119,9 +126,9 @@ __global__ void __launch_bounds__(128) k_plan_cost_dmma(const PlanCostArgs a) {
         const int K0p = (K0 + 3) & ~3;
         for (int i = lane; i < 16 * K0p; i += 32) {
             const int r = i / K0p, c = i % K0p;
-            const long long row = base + r;
+            const long long row = rid[r];
             double v = 0.0;
-            if (row < a.row_end && c < K0) {
+            if (row >= 0 && c < K0) {
                 if (c < D)
                     v = dir == 0 ? (a.comp[row * D + c] - mn[r]) / a.start_scale : 0.0;
                 else
@@ -137,8 +144,8 @@ __global__ void __launch_bounds__(128) k_plan_cost_dmma(const PlanCostArgs a) {
         warp_layer<false>(a.cp.W[dir][4], a.cp.b[dir][4], 16, D, X, a.ldx, O + dir * D, 2 * D, lane);
     }
     if (lane < 16) {
-        const long long row = base + lane;
-        if (row < a.row_end) {
+        const long long row = rid[lane];
+        if (row >= 0) {
             double c = CUDART_INF;
             if (!a.feas || a.feas[row]) {
                 c = -CUDART_INF;
@@ -249,9 +256,11 @@ __global__ void __launch_bounds__(128) k_precompute_dmma(const PreDmmaArgs a) {
 static int ld_pad(int width) { return ((width + 15) / 16) * 16 + 4; }   // == 4 (mod 16): conflict-free A frags
 
 ns_status launch_plan_cost(ns_ctx* ctx, long long rb, long long re, const uint8_t* feas, const double* comp,
-                           const int32_t* devdim, double* cost) {
+                           const int32_t* devdim, double* cost, const int32_t* list, const int32_t* list_n) {
     if (re <= rb) return NS_OK;
     PlanCostArgs a;
+    a.list = list;
+    a.list_n = list_n;
     a.row_begin = rb;
     a.row_end = re;
     a.D = ctx->model.D;
@@ -265,7 +274,7 @@ ns_status launch_plan_cost(ns_ctx* ctx, long long rb, long long re, const uint8_
     const int K0p = (2 * a.D + 3) & ~3;
     a.ldx = ld_pad(K0p > 64 ? K0p : 64);
     a.ldy = ld_pad(128);
-    const size_t per_warp = (size_t)(16 * (a.ldx + a.ldy + 2 * a.D) + 16) * sizeof(double);
+    const size_t per_warp = (size_t)(16 * (a.ldx + a.ldy + 2 * a.D) + 32) * sizeof(double);
     int wpb = 4;
     while (wpb > 1 && per_warp * wpb > 110 * 1024) wpb >>= 1;
     const size_t smem = per_warp * wpb;

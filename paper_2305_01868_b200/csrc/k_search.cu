@@ -40,6 +40,11 @@ struct SearchBufs {
     uint8_t* feas;       // [n_traj]
     uint32_t* work;      // [n_traj]
     double* tcost;       // [n_traj]
+    int32_t* dup_of;     // [n_traj] grouped greedy: tau whose plan this one duplicates, or -1
+    int32_t* uniq;       // [n_traj] compacted list of trajectories carrying a distinct feasible plan
+    int32_t* n_uniq;     // [1]
+    double* gscratch;    // grouped greedy group states
+    int gscratch_warps;
     // per task
     int32_t* capdim;     // [n_tasks][M]
     int32_t* beam_plan;  // [n_tasks][K][Lcap]
@@ -243,56 +248,45 @@ __device__ __forceinline__ double2 ld_v2(const double2* p) {
     else return __ldg(p);
 }
 
-// Partial dot product sum_{k<FPL} w[k] ReLU(u[k] + v[k]) with 4 accumulators,
-// v streamed in chunks of 8 doubles.
+// Partial dot product sum_{k<FPL} w[k] ReLU(u[k] + v[k]) with (up to) 4
+// accumulators, v streamed in chunks of (up to) 8 doubles.
 template <int FPL, bool SMEM>
 __device__ __forceinline__ double part_score(const double (&u)[FPL], const double (&w)[FPL],
                                              const double2* __restrict__ v2) {
-    double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+    constexpr int CH = FPL < 8 ? FPL : 8;   // doubles per chunk
+    double acc[4] = {0.0, 0.0, 0.0, 0.0};
 #pragma unroll
-    for (int c = 0; c < FPL / 8; ++c) {
-        double2 vv[4];
+    for (int c = 0; c < FPL / CH; ++c) {
+        double2 vv[CH / 2];
 #pragma unroll
-        for (int i = 0; i < 4; ++i) vv[i] = ld_v2<SMEM>(v2 + c * 4 + i);
+        for (int i = 0; i < CH / 2; ++i) vv[i] = ld_v2<SMEM>(v2 + c * (CH / 2) + i);
 #pragma unroll
-        for (int i = 0; i < 4; i += 2) {
-            const int k = c * 8 + 2 * i;
-            a0 = fma(w[k + 0], relu_hi(u[k + 0] + vv[i].x), a0);
-            a1 = fma(w[k + 1], relu_hi(u[k + 1] + vv[i].y), a1);
-            a2 = fma(w[k + 2], relu_hi(u[k + 2] + vv[i + 1].x), a2);
-            a3 = fma(w[k + 3], relu_hi(u[k + 3] + vv[i + 1].y), a3);
+        for (int i = 0; i < CH / 2; ++i) {
+            const int k = c * CH + 2 * i;
+            acc[(2 * i) & 3] = fma(w[k], relu_hi(u[k] + vv[i].x), acc[(2 * i) & 3]);
+            acc[(2 * i + 1) & 3] = fma(w[k + 1], relu_hi(u[k + 1] + vv[i].y), acc[(2 * i + 1) & 3]);
         }
     }
-    return (a0 + a1) + (a2 + a3);
+    return (acc[0] + acc[1]) + (acc[2] + acc[3]);
 }
 
 // u += v (only the chosen device's lanes execute it)
 template <int FPL, bool SMEM>
 __device__ __forceinline__ void part_add(double (&u)[FPL], const double2* __restrict__ v2) {
 #pragma unroll
-    for (int c = 0; c < FPL / 8; ++c) {
-        double2 vv[4];
-#pragma unroll
-        for (int i = 0; i < 4; ++i) vv[i] = ld_v2<SMEM>(v2 + c * 4 + i);
-#pragma unroll
-        for (int i = 0; i < 4; ++i) {
-            u[c * 8 + 2 * i] += vv[i].x;
-            u[c * 8 + 2 * i + 1] += vv[i].y;
-        }
+    for (int i = 0; i < FPL / 2; ++i) {
+        const double2 vv = ld_v2<SMEM>(v2 + i);
+        u[2 * i] += vv.x;
+        u[2 * i + 1] += vv.y;
     }
 }
 
 template <int FPL>
 __device__ __forceinline__ double part_head(const double (&u)[FPL], const double (&w)[FPL]) {
-    double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+    double acc[4] = {0.0, 0.0, 0.0, 0.0};
 #pragma unroll
-    for (int k = 0; k < FPL; k += 4) {
-        a0 = fma(w[k + 0], relu_exact(u[k + 0]), a0);
-        a1 = fma(w[k + 1], relu_exact(u[k + 1]), a1);
-        a2 = fma(w[k + 2], relu_exact(u[k + 2]), a2);
-        a3 = fma(w[k + 3], relu_exact(u[k + 3]), a3);
-    }
-    return (a0 + a1) + (a2 + a3);
+    for (int k = 0; k < FPL; ++k) acc[k & 3] = fma(w[k], relu_exact(u[k]), acc[k & 3]);
+    return (acc[0] + acc[1]) + (acc[2] + acc[3]);
 }
 
 // Sum of the LPD partials of one device (xor butterfly; IEEE addition is
@@ -440,6 +434,313 @@ __global__ void __launch_bounds__(256) k_greedy_cta(const GreedyArgs a, int mchu
     }
 }
 
+// ---------------------------------------------------------------------------
+// Grouped greedy (used for D <= 16): one WARP per column plan, all M grid
+// trajectories of that column plan handled together.
+//
+// The M grid points differ only in the max_dim cap, so their greedy
+// runs coincide until a cap binds: trajectories with the same assignment
+// history have the same device states and therefore the same candidate
+// scores C(S_d + {t}); only their feasible sets differ (by the dim cap).  The
+// kernel keeps one device state per GROUP of identical trajectories, scores
+// the D devices once per group, and lets every member take its own argmin
+// over its own feasible set; members that choose a different device than the
+// group's lowest member split off into a new group (state copied before the
+// update).  This is the data-parallel form of the paper's life-long cache
+// ("if we only make small changes to ... max_dim, the cost model will be
+// very likely to be asked to predict the cost for the same set of tables",
+// PAPER.md:291): every score the algorithm asks for is answered -- the work
+// count W (O12) counts each member's feasible devices -- but each distinct
+// (state, table) score is computed once.  Results are identical to running
+// the M trajectories separately (same arithmetic on the same state).
+//
+// Lane layout: lane = (device d, part) with LPD = 32 / pow2(D) lanes per
+// device and FPL = 64 / LPD features per lane.  Group 0 (which holds the
+// loosest caps and lives the longest) keeps its state in registers; later
+// groups live in a per-warp global scratch (L1/L2).  Member and group
+// bookkeeping lives in shared memory.
+// ---------------------------------------------------------------------------
+struct DedupArgs {
+    int n_cp;              // column plans of this launch: [0, n_cp) relative to the GreedyArgs pointers
+    int mmax;              // M
+    double* scratch;       // [total_warps][M][D][64] group states (groups >= 1)
+    int total_warps;
+    int32_t* dup_of;       // [n_traj] tau of the member whose plan this one duplicates, or -1
+};
+
+template <int LPD>
+__global__ void __launch_bounds__(128, (LPD >= 8 ? 4 : (LPD == 4 ? 2 : 1))) k_greedy_dedup(const GreedyArgs a, const DedupArgs x) {
+    constexpr int FPL = kV / LPD;
+    constexpr int DPW = 32 / LPD;   // device slots per warp
+    extern __shared__ unsigned char dsm[];
+    const int lane = threadIdx.x & 31, wl = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    const int M = x.mmax, D = a.D;
+    const int d = lane / LPD, part = lane % LPD;
+    const bool dev = d < D;
+    // per-warp shared bookkeeping
+    const size_t per_warp = (size_t)M * (4 + 4 + 4 + 4 + DPW * 4 + DPW * 8 + 4) + DPW * (8 + 4 + 4) + 64;
+    unsigned char* base = dsm + (size_t)wl * ((per_warp + 15) & ~size_t(15));
+    long long* gb = (long long*)base;                 // [M][DPW] group bytes per device
+    double* sc = (double*)(gb + (size_t)M * DPW);     // [DPW] scores of the current group
+    int* gd = (int*)(sc + DPW);                       // [M][DPW] group dims per device
+    int* mgroup = gd + (size_t)M * DPW;               // [M] member -> group (-1 dead)
+    int* mcap = mgroup + M;                           // [M] member dim cap
+    uint32_t* mwork = (uint32_t*)(mcap + M);          // [M]
+    int* mpick = (int*)(mwork + M);                   // [M]
+    int* gcap = mpick + M;                            // [M] loosest cap among a group's members
+    int* sdv = gcap + M;                              // [DPW] dim after insertion
+    int* sok = sdv + DPW;                             // [DPW] device scored
+    double w[FPL], u0[FPL], uinit[FPL];
+    load_lane_head<FPL>(a.head, part, uinit, w);
+#pragma unroll
+    for (int k = 0; k < FPL; ++k) asm volatile("" : "+d"(uinit[k]));
+    const long long gw = (long long)blockIdx.x * nw + wl;
+    double* scr = x.scratch + (size_t)gw * M * D * kV;   // this warp's group states
+    for (long long g = gw; g < x.n_cp; g += x.total_warps) {
+        const bool valid = a.cp_valid[g] != 0;
+        const long long tau0 = g * M;
+        if (!valid) {
+            for (int m = lane; m < M; m += 32) {
+                a.feas[tau0 + m] = 0;
+                a.work[tau0 + m] = 0;
+                x.dup_of[tau0 + m] = -1;
+            }
+            continue;
+        }
+        const int q = a.cp_task[g];
+        const int Tp = a.cp_Tp[g];
+        const long long cap = a.cap[q];
+        int cmax = 0;
+        for (int m = lane; m < M; m += 32) {
+            mgroup[m] = 0;
+            mcap[m] = a.capdim[q * M + m];
+            mwork[m] = 0;
+            cmax = max(cmax, mcap[m]);
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) cmax = max(cmax, __shfl_xor_sync(kFull, cmax, o));
+        for (int i = lane; i < DPW; i += 32) {
+            gd[i] = 0;
+            gb[i] = 0;
+        }
+        if (lane == 0) gcap[0] = cmax;
+#pragma unroll
+        for (int k = 0; k < FPL; ++k) u0[k] = uinit[k];
+        int ng = 1;
+        __syncwarp();
+        const int32_t* orow = a.ord_row + (size_t)g * a.Tpm;
+        const int32_t* oidx = a.ord_idx + (size_t)g * a.Tpm;
+        // two-deep software pipeline over the cost-ordered table stream:
+        // row index two steps ahead, (v slice, dim, bytes, list index) one ahead
+        int row_nn = Tp > 1 ? __ldg(orow + 1) : 0;
+        int row_n = __ldg(orow);
+        double2 vn[FPL / 2];
+#pragma unroll
+        for (int i2 = 0; i2 < FPL / 2; ++i2)
+            vn[i2] = __ldg(reinterpret_cast<const double2*>(a.V + (size_t)row_n * kV + part * FPL) + i2);
+        int dt_n = __ldg(a.vdim + row_n), idx_n = __ldg(oidx);
+        long long bt_n = __ldg(a.vbytes + row_n);
+#pragma unroll 1
+        for (int p = 0; p < Tp; ++p) {
+            double vcd[FPL];
+#pragma unroll
+            for (int i2 = 0; i2 < FPL / 2; ++i2) {
+                vcd[2 * i2] = vn[i2].x;
+                vcd[2 * i2 + 1] = vn[i2].y;
+            }
+            const int dt = dt_n, idx = idx_n;
+            const long long bt = bt_n;
+            if (p + 1 < Tp) {
+                const int r1 = row_nn;
+#pragma unroll
+                for (int i2 = 0; i2 < FPL / 2; ++i2)
+                    vn[i2] = __ldg(reinterpret_cast<const double2*>(a.V + (size_t)r1 * kV + part * FPL) + i2);
+                dt_n = __ldg(a.vdim + r1);
+                bt_n = __ldg(a.vbytes + r1);
+                idx_n = __ldg(oidx + p + 1);
+                if (p + 2 < Tp) row_nn = __ldg(orow + p + 2);
+            }
+            const int ng0 = ng;
+#pragma unroll 1
+            for (int gr = 0; gr < ng0; ++gr) {
+                // ---- score the D devices once for the whole group (R5: after insertion)
+                const int gcap_gr = gcap[gr];
+                if (gcap_gr < 0) continue;   // group without live members
+                const int dsum = dev ? gd[gr * DPW + d] : 0;
+                const long long bsum = dev ? gb[gr * DPW + d] : 0;
+                const bool f = dev && (bsum + bt <= cap) && (dsum + dt <= gcap_gr);
+                double* ug = scr + ((size_t)gr * D + (dev ? d : 0)) * kV + part * FPL;   // valid for gr >= 1
+                double ps = 0.0;
+                if (f) {
+                    double acc[4] = {0.0, 0.0, 0.0, 0.0};
+                    if (gr == 0) {
+#pragma unroll
+                        for (int k = 0; k < FPL; ++k) acc[k & 3] = fma(w[k], relu_hi(u0[k] + vcd[k]), acc[k & 3]);
+                    } else {
+#pragma unroll
+                        for (int k = 0; k < FPL; ++k) acc[k & 3] = fma(w[k], relu_hi(ug[k] + vcd[k]), acc[k & 3]);
+                    }
+                    ps = (acc[0] + acc[1]) + (acc[2] + acc[3]);
+                }
+                const double s = a.head.hb2 + lane_group_sum<LPD>(ps);
+                if (part == 0 && d < DPW) {
+                    sc[d] = s;
+                    sdv[d] = dsum + dt;
+                    sok[d] = f ? 1 : 0;
+                }
+                __syncwarp();
+                // ---- every member takes its own argmin over its own feasible set
+                //      (dim cap of its grid point; lowest device on ties, R13)
+                int first = M;
+                bool split = false, left = false;
+                for (int m0 = 0; m0 < M; m0 += 32) {
+                    const int m = m0 + lane;
+                    int pick = -2;
+                    if (m < M && mgroup[m] == gr) {
+                        double best = CUDART_INF;
+                        int bd = -1;
+                        uint32_t cnt = 0;
+                        const int cm = mcap[m];
+                        for (int dd = 0; dd < D; ++dd) {
+                            if (sok[dd] && sdv[dd] <= cm) {
+                                ++cnt;
+                                const double sv = sc[dd];
+                                if (sv < best) {
+                                    best = sv;
+                                    bd = dd;
+                                }
+                            }
+                        }
+                        mwork[m] += cnt;
+                        if (bd < 0) {
+                            mgroup[m] = -1;   // R9: stranded -> grid point infeasible
+                            pick = -1;
+                        } else {
+                            pick = bd;
+                            a.assign[(size_t)(tau0 + m) * a.Tpm + idx] = (int8_t)bd;
+                        }
+                    }
+                    if (m < M) mpick[m] = pick;
+                    const unsigned live = __ballot_sync(kFull, pick >= 0);
+                    left |= __any_sync(kFull, pick == -1);
+                    if (first == M && live) first = m0 + __ffs(live) - 1;
+                }
+                __syncwarp();
+                if (first == M) {   // every member stranded
+                    if (lane == 0) gcap[gr] = -1;
+                    __syncwarp();
+                    continue;
+                }
+                const int main_pick = mpick[first];
+                for (int m0 = 0; m0 < M; m0 += 32) {
+                    const int m = m0 + lane;
+                    split |= __any_sync(kFull, m < M && mpick[m] >= 0 && mpick[m] != main_pick);
+                }
+                // ---- members choosing another device split off (state before the update)
+                if (split) {
+                    for (int dd = 0; dd < D; ++dd) {
+                        if (dd == main_pick) continue;
+                        int any = 0, c2 = -1;
+                        for (int m0 = 0; m0 < M; m0 += 32) {
+                            const int m = m0 + lane;
+                            const bool mine = m < M && mpick[m] == dd;
+                            if (mine) {
+                                mgroup[m] = ng;
+                                c2 = max(c2, mcap[m]);
+                            }
+                            any |= __any_sync(kFull, mine);
+                        }
+                        if (!any) continue;
+#pragma unroll
+                        for (int o = 16; o > 0; o >>= 1) c2 = max(c2, __shfl_xor_sync(kFull, c2, o));
+                        // new group ng = state(gr) + v_t on device dd
+                        if (dev) {
+                            double* un = scr + ((size_t)ng * D + d) * kV + part * FPL;
+                            const double* us = scr + ((size_t)gr * D + d) * kV + part * FPL;
+#pragma unroll
+                            for (int k = 0; k < FPL; ++k) {
+                                double val = gr == 0 ? u0[k] : us[k];
+                                if (d == dd) val += vcd[k];
+                                un[k] = val;
+                            }
+                        }
+                        for (int i3 = lane; i3 < DPW; i3 += 32) {
+                            gd[ng * DPW + i3] = gd[gr * DPW + i3] + (i3 == dd ? dt : 0);
+                            gb[ng * DPW + i3] = gb[gr * DPW + i3] + (i3 == dd ? bt : 0);
+                        }
+                        if (lane == 0) gcap[ng] = c2;
+                        ++ng;
+                        __syncwarp();
+                    }
+                }
+                // ---- the group itself takes main_pick
+                if (d == main_pick) {
+                    if (gr == 0) {
+#pragma unroll
+                        for (int k = 0; k < FPL; ++k) u0[k] += vcd[k];
+                    } else {
+#pragma unroll
+                        for (int k = 0; k < FPL; ++k) ug[k] += vcd[k];
+                    }
+                }
+                int c3 = gcap_gr;
+                if (split || left) {   // members left: tighten the group's loosest cap
+                    c3 = -1;
+                    for (int m = lane; m < M; m += 32)
+                        if (mgroup[m] == gr) c3 = max(c3, mcap[m]);
+#pragma unroll
+                    for (int o = 16; o > 0; o >>= 1) c3 = max(c3, __shfl_xor_sync(kFull, c3, o));
+                }
+                __syncwarp();
+                if (lane == 0) {
+                    gd[gr * DPW + main_pick] += dt;
+                    gb[gr * DPW + main_pick] += bt;
+                    gcap[gr] = c3;
+                }
+                __syncwarp();
+            }
+        }
+        // ---- outputs: per member feasibility, work, and its group's device costs
+        for (int gr = 0; gr < ng; ++gr) {
+            double hp;
+            if (gr == 0) {
+                hp = part_head<FPL>(u0, w);
+            } else {
+                double tu[FPL];
+                const double* ug = scr + ((size_t)gr * D + (dev ? d : 0)) * kV + part * FPL;
+#pragma unroll
+                for (int k = 0; k < FPL; ++k) tu[k] = ug[k];
+                hp = part_head<FPL>(tu, w);
+            }
+            const double hc = a.head.hb2 + lane_group_sum<LPD>(hp);
+            if (part == 0 && dev) sc[d] = hc;
+            __syncwarp();
+            // members of this group: the first one carries the plan, others duplicate it
+            int rep = -1;
+            for (int m0 = 0; m0 < M; m0 += 32) {
+                const unsigned mem = __ballot_sync(kFull, m0 + lane < M && mgroup[m0 + lane] == gr);
+                if (rep < 0 && mem) rep = m0 + __ffs(mem) - 1;
+            }
+            for (int i = lane; i < M * D; i += 32) {
+                const int m = i / D, dd = i % D;
+                if (mgroup[m] != gr) continue;
+                const int dsum = gd[gr * DPW + dd];
+                a.comp[(tau0 + m) * D + dd] = dsum > 0 ? sc[dd] : 0.0;   // reading R4
+                a.devdim[(tau0 + m) * D + dd] = dsum;
+            }
+            for (int m = lane; m < M; m += 32)
+                if (mgroup[m] == gr) x.dup_of[tau0 + m] = (m == rep) ? -1 : (int32_t)(tau0 + rep);
+            __syncwarp();
+        }
+        for (int m = lane; m < M; m += 32) {
+            a.feas[tau0 + m] = mgroup[m] >= 0 ? 1 : 0;
+            a.work[tau0 + m] = mwork[m];
+            if (mgroup[m] < 0) x.dup_of[tau0 + m] = -1;
+        }
+        __syncwarp();
+    }
+}
+
 // Large D (LPD * pow2(D) > 32, e.g. C5's 128 simulated GPUs): one trajectory
 // per CTA of LPD * D threads; cross-warp argmin through shared memory
 // (double-buffered by step parity); v rows read through L1/L2 (no other
@@ -556,7 +857,8 @@ __global__ void k_select(SearchBufs b, int C, int level, int Kbeam) {
             for (int m = 0; m < b.M; ++m) {
                 const long long tau = (long long)g * b.M + m;
                 wsum += b.work[tau];
-                const double c = b.tcost[tau];
+                const long long src = b.dup_of[tau] >= 0 ? (long long)b.dup_of[tau] : tau;
+                const double c = b.feas[tau] ? b.tcost[src] : CUDART_INF;
                 if (c < best) {
                     best = c;
                     bm = m;
@@ -695,6 +997,10 @@ void carve(Carver& c, SearchBufs& b, OutStage& o, int Lout) {
     b.feas = c.take<uint8_t>(b.n_traj);
     b.work = c.take<uint32_t>(b.n_traj);
     b.tcost = c.take<double>(b.n_traj);
+    b.dup_of = c.take<int32_t>(b.n_traj);
+    b.uniq = c.take<int32_t>(b.n_traj);
+    b.n_uniq = c.take<int32_t>(1);
+    b.gscratch = c.take<double>((size_t)b.gscratch_warps * b.M * b.D * kV);
     b.capdim = c.take<int32_t>((size_t)b.n_tasks * b.M);
     b.beam_plan = c.take<int32_t>((size_t)b.n_tasks * b.K * b.Lcap);
     b.beam_cnt = c.take<int32_t>(b.n_tasks);
@@ -753,55 +1059,84 @@ ns_status launch_greedy(ns_ctx* ctx, const SearchBufs& b, const ns_tables* t, lo
     const long long n = te - tb;
     int dp = 1;
     while (dp < b.D) dp <<= 1;
-    // lanes per device: 4 (16 features/lane) when a trajectory fits a warp,
-    // else 2, else the one-trajectory-per-CTA kernel
-    const int lpd = (4 * dp <= 32) ? 4 : 2;
-    const int seg = lpd * dp;
-    if (seg > 32) {
-        const int threads = ((4 * b.D + 31) / 32) * 32;
-        prof_begin(ctx, PK_GREEDY);
-        k_greedy_big<4><<<(unsigned)n, threads, 0, ctx->stream>>>(a);
-        prof_end(ctx);
-    } else {
-        // CTA per (column plan, chunk of grid points); trajectories of a
-        // column plan are contiguous: tau = g * M + m
-        const int mchunk = std::min(b.M, 256 / seg);
-        const int nchunk = (b.M + mchunk - 1) / mchunk;
-        const int threads = ((mchunk * seg + 31) / 32) * 32;
-        const long long g0 = tb / b.M, g1 = (te - 1) / b.M + 1;
+    if (dp <= 16) {
+        // grouped greedy: one warp per column plan (trajectories [tb, te) are
+        // whole column plans: tb, te multiples of M)
+        const long long g0 = tb / b.M, g1 = te / b.M;
         GreedyArgs a2 = a;
         a2.ord_row = b.ord_row + (size_t)g0 * b.Tpm;
         a2.ord_idx = b.ord_idx + (size_t)g0 * b.Tpm;
         a2.cp_valid = b.cp_valid + g0;
         a2.cp_task = b.cp_task + g0;
         a2.cp_Tp = b.cp_Tp + g0;
-        a2.traj_begin = (int)(tb - g0 * b.M);
-        a2.traj_end = (int)(te - g0 * b.M);
         a2.assign = b.assign + (size_t)g0 * b.M * b.Tpm;
         a2.comp = b.comp + (size_t)g0 * b.M * b.D;
         a2.devdim = b.devdim + (size_t)g0 * b.M * b.D;
         a2.feas = b.feas + (size_t)g0 * b.M;
         a2.work = b.work + (size_t)g0 * b.M;
-        const unsigned blocks = (unsigned)((g1 - g0) * nchunk);
+        DedupArgs x;
+        x.n_cp = (int)(g1 - g0);
+        x.mmax = b.M;
+        x.scratch = b.gscratch;
+        x.total_warps = (int)std::min<long long>(x.n_cp, (long long)b.gscratch_warps);
+        x.dup_of = b.dup_of + (size_t)g0 * b.M;
+        const int lpd = 32 / dp;
+        const int DPW = dp;
+        const size_t per_warp = (((size_t)b.M * (20 + DPW * 12) + DPW * 16 + 64) + 15) & ~size_t(15);
+        const int wpb = 4;
+        const size_t smem = per_warp * wpb;
+        const unsigned blocks = (unsigned)((x.total_warps + wpb - 1) / wpb);
+        x.total_warps = (int)blocks * wpb;   // every launched warp strides the column plans
         prof_begin(ctx, PK_GREEDY);
-        switch (seg) {
-            case 4: k_greedy_cta<4, 4><<<blocks, threads, 0, ctx->stream>>>(a2, mchunk, nchunk); break;
-            case 8: k_greedy_cta<8, 4><<<blocks, threads, 0, ctx->stream>>>(a2, mchunk, nchunk); break;
-            case 16: k_greedy_cta<16, 4><<<blocks, threads, 0, ctx->stream>>>(a2, mchunk, nchunk); break;
-            case 32:
-                if (lpd == 4) k_greedy_cta<32, 4><<<blocks, threads, 0, ctx->stream>>>(a2, mchunk, nchunk);
-                else k_greedy_cta<32, 2><<<blocks, threads, 0, ctx->stream>>>(a2, mchunk, nchunk);
-                break;
-            default: return set_err(ctx, NS_ERR_INTERNAL, "bad greedy segment");
+        switch (lpd) {
+#define NS_DEDUP(L)                                                                                  \
+    case L:                                                                                          \
+        if (smem > 48 * 1024)                                                                        \
+            cudaFuncSetAttribute(k_greedy_dedup<L>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
+        k_greedy_dedup<L><<<blocks, wpb * 32, smem, ctx->stream>>>(a2, x);                           \
+        break;
+            NS_DEDUP(2)
+            NS_DEDUP(4)
+            NS_DEDUP(8)
+            NS_DEDUP(16)
+            NS_DEDUP(32)
+#undef NS_DEDUP
+            default: return set_err(ctx, NS_ERR_INTERNAL, "bad greedy lane split");
         }
         prof_end(ctx);
+    } else {
+        const int threads = ((4 * b.D + 31) / 32) * 32;
+        prof_begin(ctx, PK_GREEDY);
+        k_greedy_big<4><<<(unsigned)n, threads, 0, ctx->stream>>>(a);
+        prof_end(ctx);
+        // no grouping: every trajectory carries its own plan
+        NS_CUDA(ctx, cudaMemsetAsync(b.dup_of + tb, 0xff, (size_t)n * sizeof(int32_t), ctx->stream));
     }
     NS_LAUNCHED(ctx);
     return NS_OK;
 }
 
+// Distinct feasible plans of [tb, te): duplicates (grouped greedy members
+// that ended with the plan of an earlier member) read the representative's
+// cost in k_select, infeasible trajectories are +inf there.
+__global__ void k_compact(const uint8_t* feas, const int32_t* dup_of, long long tb, long long te, int32_t* list,
+                          int32_t* n) {
+    for (long long t = tb + (long long)blockIdx.x * blockDim.x + threadIdx.x; t < te;
+         t += (long long)gridDim.x * blockDim.x) {
+        if (feas[t] && dup_of[t] < 0) list[atomicAdd(n, 1)] = (int32_t)t;
+    }
+}
+
 ns_status launch_finalize(ns_ctx* ctx, const SearchBufs& b, long long tb, long long te) {
-    return launch_plan_cost(ctx, tb, te, b.feas, b.comp, b.devdim, b.tcost);
+    if (te <= tb) return NS_OK;
+    NS_CUDA(ctx, cudaMemsetAsync(b.n_uniq, 0, sizeof(int32_t), ctx->stream));
+    const long long n = te - tb;
+    prof_begin(ctx, PK_OTHER);
+    k_compact<<<(unsigned)std::min<long long>((n + 255) / 256, 2048), 256, 0, ctx->stream>>>(b.feas, b.dup_of, tb, te,
+                                                                                           b.uniq, b.n_uniq);
+    prof_end(ctx);
+    NS_LAUNCHED(ctx);
+    return launch_plan_cost(ctx, 0, n, nullptr, b.comp, b.devdim, b.tcost, b.uniq, b.n_uniq);
 }
 
 // Copy staged results to the caller's (host or device) pointers.
@@ -857,6 +1192,15 @@ ns_status run_search(ns_ctx* ctx, const ns_tables* t, int D, const ns_search_par
     b.S = b.n_tasks * C;
     b.n_traj = b.S * b.M;
     const int Lout = L;
+    {
+        int dp = 1;
+        while (dp < D) dp <<= 1;
+        const long long max_cp = (long long)b.S;
+        const size_t per = (size_t)b.M * D * kV * sizeof(double);
+        long long warps = std::min<long long>(max_cp, (long long)ctx->sm_count * 16);
+        warps = std::max<long long>(4, std::min<long long>(warps, (long long)((512ull << 20) / per)));
+        b.gscratch_warps = dp <= 16 ? (int)(((warps + 3) / 4) * 4) : 0;
+    }
     OutStage o{};
     Carver probe{nullptr};
     carve(probe, b, o, Lout > 0 ? Lout : 1);

@@ -147,9 +147,12 @@ void prof_end(ns_ctx* ctx);
 void prof_collect(ns_ctx* ctx);
 
 // N5 (k_mlp.cu): cost[r] = max_d(comp + fwd + bwd) for rows [rb, re) with the
-// comm MLPs on the FP64 tensor cores; rows with feas[r] == 0 get +inf.
+// comm MLPs on the FP64 tensor cores; rows with feas[r] == 0 get +inf.  With a
+// row list, the rows are list[rb .. rb + *list_n) (device count), re - rb is
+// the list capacity (grid size).
 ns_status launch_plan_cost(ns_ctx* ctx, long long rb, long long re, const uint8_t* feas, const double* comp,
-                           const int32_t* devdim, double* cost);
+                           const int32_t* devdim, double* cost, const int32_t* list = nullptr,
+                           const int32_t* list_n = nullptr);
 
 // helpers (ns_api.cu)
 ns_status set_err(ns_ctx* ctx, ns_status s, const std::string& msg);
