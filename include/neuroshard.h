@@ -171,13 +171,22 @@ ns_status ns_score_plans(ns_ctx* ctx, const ns_tables* tables, int32_t task, int
                          double* cost_out, int64_t* best_index_out, double* best_cost_out);
 
 /* ------------------------------------------------------------------ search */
+/* ns_search_params.flags: which greedy kernel (N4) runs.  All variants give
+ * identical results; they differ in how the M grid trajectories of a column
+ * plan are mapped to lanes. */
+#define NS_GREEDY_AUTO 0u     /* grouped when there are many column plans, else per-lane */
+#define NS_GREEDY_GROUPED 1u  /* one warp per column plan; trajectories with identical
+                                 assignment history share their scores (the paper's
+                                 life-long cache, as data parallelism) */
+#define NS_GREEDY_LANES 2u    /* every trajectory in its own lane segment (latency mode) */
+
 typedef struct {
     int32_t N;               /* candidate tables per kind, default 10 */
     int32_t K;               /* beam width, default 3 */
     int32_t L;               /* split steps, default 10; ignored by tablewise */
     int32_t M;               /* grid points, default 11 */
     double  grid_hi_factor;  /* M_e = factor * M_s, default 1.5 */
-    uint32_t flags;          /* reserved, must be 0 */
+    uint32_t flags;          /* NS_GREEDY_* (0 = auto); other bits must be 0 */
 } ns_search_params;
 
 /* Per-task results.  Every pointer is host or device; only `cost` is

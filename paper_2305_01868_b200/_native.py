@@ -262,8 +262,11 @@ def ns_score_plans(ctx: int, tables: Tables, task: int, D: int, col_plan, assign
 
 
 # ----------------------------------------------------------------- search
-def _params(N, K, L, M, hi):
-    return ns_search_params(N, K, L, M, hi, 0)
+NS_GREEDY_AUTO, NS_GREEDY_GROUPED, NS_GREEDY_LANES = 0, 1, 2
+
+
+def _params(N, K, L, M, hi, greedy=NS_GREEDY_AUTO):
+    return ns_search_params(N, K, L, M, hi, greedy)
 
 
 def _alloc_out(n: int, stride: int, L: int, out: Optional[dict]):
@@ -277,18 +280,19 @@ def _alloc_out(n: int, stride: int, L: int, out: Optional[dict]):
     return out, pb
 
 
-def ns_shard_tablewise(ctx: int, tables: Tables, D: int, M: int = 11, hi: float = 1.5, out: Optional[dict] = None):
+def ns_shard_tablewise(ctx: int, tables: Tables, D: int, M: int = 11, hi: float = 1.5, out: Optional[dict] = None,
+                       greedy: int = NS_GREEDY_AUTO):
     out, pb = _alloc_out(tables.n_tasks, tables.T_max, 0, out)
-    p = _params(10, 3, 0, M, hi)
+    p = _params(10, 3, 0, M, hi, greedy)
     st = _check(ctx, LIB.ns_shard_tablewise(ctx, tables.handle, D, C.byref(p), C.byref(pb)))
     out["status"] = st
     return out
 
 
 def ns_shard_columnwise(ctx: int, tables: Tables, D: int, N: int = 10, K: int = 3, L: int = 10, M: int = 11,
-                        hi: float = 1.5, out: Optional[dict] = None):
+                        hi: float = 1.5, out: Optional[dict] = None, greedy: int = NS_GREEDY_AUTO):
     out, pb = _alloc_out(tables.n_tasks, tables.T_max + L, L, out)
-    p = _params(N, K, L, M, hi)
+    p = _params(N, K, L, M, hi, greedy)
     st = _check(ctx, LIB.ns_shard_columnwise(ctx, tables.handle, D, C.byref(p), C.byref(pb)))
     out["status"] = st
     return out

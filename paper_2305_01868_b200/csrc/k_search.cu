@@ -9,6 +9,7 @@
 #include <math_constants.h>
 
 #include <algorithm>
+#include <climits>
 #include <cmath>
 #include <cstring>
 #include <vector>
@@ -25,6 +26,7 @@ namespace ns {
 // ======================================================================
 struct SearchBufs {
     int n_tasks, D, M, K, N2, Lcap, Tpm, S, n_traj;
+    uint32_t greedy_mode;   // NS_GREEDY_*
     // per cp
     int32_t* cp_task;
     int32_t* cp_valid;
@@ -478,7 +480,7 @@ __global__ void __launch_bounds__(128, (LPD >= 8 ? 4 : (LPD == 4 ? 2 : 1))) k_gr
     const int d = lane / LPD, part = lane % LPD;
     const bool dev = d < D;
     // per-warp shared bookkeeping
-    const size_t per_warp = (size_t)M * (4 + 4 + 4 + 4 + DPW * 4 + DPW * 8 + 4) + DPW * (8 + 4 + 4) + 64;
+    const size_t per_warp = (size_t)M * (4 + 4 + 4 + 4 + DPW * 4 + DPW * 8 + 4 + 8) + DPW * (8 + 4 + 4) + 64;
     unsigned char* base = dsm + (size_t)wl * ((per_warp + 15) & ~size_t(15));
     long long* gb = (long long*)base;                 // [M][DPW] group bytes per device
     double* sc = (double*)(gb + (size_t)M * DPW);     // [DPW] scores of the current group
@@ -490,6 +492,8 @@ __global__ void __launch_bounds__(128, (LPD >= 8 ? 4 : (LPD == 4 ? 2 : 1))) k_gr
     int* gcap = mpick + M;                            // [M] loosest cap among a group's members
     int* sdv = gcap + M;                              // [DPW] dim after insertion
     int* sok = sdv + DPW;                             // [DPW] device scored
+    int* gmin = sok + DPW;                            // [M] tightest cap among a group's live members
+    uint32_t* gwork = (uint32_t*)(gmin + M);          // [M] work of the group's uniform steps
     double w[FPL], u0[FPL], uinit[FPL];
     load_lane_head<FPL>(a.head, part, uinit, w);
 #pragma unroll
@@ -510,15 +514,23 @@ __global__ void __launch_bounds__(128, (LPD >= 8 ? 4 : (LPD == 4 ? 2 : 1))) k_gr
         const int q = a.cp_task[g];
         const int Tp = a.cp_Tp[g];
         const long long cap = a.cap[q];
-        int cmax = 0;
+        int cmax = 0, cmin = INT_MAX;
         for (int m = lane; m < M; m += 32) {
             mgroup[m] = 0;
             mcap[m] = a.capdim[q * M + m];
             mwork[m] = 0;
             cmax = max(cmax, mcap[m]);
+            cmin = min(cmin, mcap[m]);
         }
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1) cmax = max(cmax, __shfl_xor_sync(kFull, cmax, o));
+        for (int o = 16; o > 0; o >>= 1) {
+            cmax = max(cmax, __shfl_xor_sync(kFull, cmax, o));
+            cmin = min(cmin, __shfl_xor_sync(kFull, cmin, o));
+        }
+        if (lane == 0) {
+            gmin[0] = cmin;
+            gwork[0] = 0;
+        }
         for (int i = lane; i < DPW; i += 32) {
             gd[i] = 0;
             gb[i] = 0;
@@ -530,36 +542,24 @@ __global__ void __launch_bounds__(128, (LPD >= 8 ? 4 : (LPD == 4 ? 2 : 1))) k_gr
         __syncwarp();
         const int32_t* orow = a.ord_row + (size_t)g * a.Tpm;
         const int32_t* oidx = a.ord_idx + (size_t)g * a.Tpm;
-        // two-deep software pipeline over the cost-ordered table stream:
-        // row index two steps ahead, (v slice, dim, bytes, list index) one ahead
-        int row_nn = Tp > 1 ? __ldg(orow + 1) : 0;
-        int row_n = __ldg(orow);
-        double2 vn[FPL / 2];
-#pragma unroll
-        for (int i2 = 0; i2 < FPL / 2; ++i2)
-            vn[i2] = __ldg(reinterpret_cast<const double2*>(a.V + (size_t)row_n * kV + part * FPL) + i2);
-        int dt_n = __ldg(a.vdim + row_n), idx_n = __ldg(oidx);
-        long long bt_n = __ldg(a.vbytes + row_n);
-#pragma unroll 1
-        for (int p = 0; p < Tp; ++p) {
-            double vcd[FPL];
+        // software pipeline over the cost-ordered table stream: the next
+        // table's (v slice, dim, bytes, list index) is fetched while the
+        // current one is processed (two register buffers, loop unrolled by 2)
+        int8_t* asg_lane = a.assign + (size_t)(tau0 + lane) * a.Tpm;   // member m = lane (+32k)
+        auto fetch = [&](int pp, double (&vb)[FPL], int& dtb, long long& btb, int& idxb) {
+            const int r = __ldg(orow + pp);
+            const double2* src = reinterpret_cast<const double2*>(a.V + (size_t)r * kV + part * FPL);
 #pragma unroll
             for (int i2 = 0; i2 < FPL / 2; ++i2) {
-                vcd[2 * i2] = vn[i2].x;
-                vcd[2 * i2 + 1] = vn[i2].y;
+                const double2 xv = __ldg(src + i2);
+                vb[2 * i2] = xv.x;
+                vb[2 * i2 + 1] = xv.y;
             }
-            const int dt = dt_n, idx = idx_n;
-            const long long bt = bt_n;
-            if (p + 1 < Tp) {
-                const int r1 = row_nn;
-#pragma unroll
-                for (int i2 = 0; i2 < FPL / 2; ++i2)
-                    vn[i2] = __ldg(reinterpret_cast<const double2*>(a.V + (size_t)r1 * kV + part * FPL) + i2);
-                dt_n = __ldg(a.vdim + r1);
-                bt_n = __ldg(a.vbytes + r1);
-                idx_n = __ldg(oidx + p + 1);
-                if (p + 2 < Tp) row_nn = __ldg(orow + p + 2);
-            }
+            dtb = __ldg(a.vdim + r);
+            btb = __ldg(a.vbytes + r);
+            idxb = __ldg(oidx + pp);
+        };
+        auto process = [&](const double (&vcd)[FPL], const int dt, const long long bt, const int idx) {
             const int ng0 = ng;
 #pragma unroll 1
             for (int gr = 0; gr < ng0; ++gr) {
@@ -583,6 +583,54 @@ __global__ void __launch_bounds__(128, (LPD >= 8 ? 4 : (LPD == 4 ? 2 : 1))) k_gr
                     ps = (acc[0] + acc[1]) + (acc[2] + acc[3]);
                 }
                 const double s = a.head.hb2 + lane_group_sum<LPD>(ps);
+                // ---- fast path: every live member's cap admits every scored
+                //      device -> all members see the same feasible set and take
+                //      the group argmin (no split, uniform work)
+                {
+                    int smax = f ? dsum + dt : 0;
+#pragma unroll
+                    for (int o = 16; o >= LPD; o >>= 1) smax = max(smax, __shfl_xor_sync(kFull, smax, o));
+                    if (smax <= gmin[gr]) {
+                        double bs = f ? s : CUDART_INF;
+                        int bd = d;
+#pragma unroll
+                        for (int o = 16; o >= LPD; o >>= 1) argmin_step(bs, bd, o);
+                        const unsigned nf = __popc(__ballot_sync(kFull, f && part == 0));
+                        if (bs == CUDART_INF) {   // nothing feasible: the whole group strands (R9)
+                            for (int m = lane; m < M; m += 32)
+                                if (mgroup[m] == gr) {
+                                    mwork[m] += gwork[gr];
+                                    mgroup[m] = -1;
+                                }
+                            __syncwarp();
+                            if (lane == 0) gcap[gr] = -1;
+                            __syncwarp();
+                            continue;
+                        }
+                        if (d == bd) {
+                            if (gr == 0) {
+#pragma unroll
+                                for (int k = 0; k < FPL; ++k) u0[k] += vcd[k];
+                            } else {
+#pragma unroll
+                                for (int k = 0; k < FPL; ++k) ug[k] += vcd[k];
+                            }
+                        }
+                        {
+                            int8_t* ap = asg_lane;
+                            for (int m = lane; m < M; m += 32, ap += 32 * (size_t)a.Tpm)
+                                if (mgroup[m] == gr) ap[idx] = (int8_t)bd;
+                        }
+                        __syncwarp();
+                        if (lane == 0) {
+                            gd[gr * DPW + bd] += dt;
+                            gb[gr * DPW + bd] += bt;
+                            gwork[gr] += nf;
+                        }
+                        __syncwarp();
+                        continue;
+                    }
+                }
                 if (part == 0 && d < DPW) {
                     sc[d] = s;
                     sdv[d] = dsum + dt;
@@ -613,11 +661,12 @@ __global__ void __launch_bounds__(128, (LPD >= 8 ? 4 : (LPD == 4 ? 2 : 1))) k_gr
                         }
                         mwork[m] += cnt;
                         if (bd < 0) {
+                            mwork[m] += gwork[gr];
                             mgroup[m] = -1;   // R9: stranded -> grid point infeasible
                             pick = -1;
                         } else {
                             pick = bd;
-                            a.assign[(size_t)(tau0 + m) * a.Tpm + idx] = (int8_t)bd;
+                            asg_lane[(size_t)m0 * a.Tpm + idx] = (int8_t)bd;
                         }
                     }
                     if (m < M) mpick[m] = pick;
@@ -640,19 +689,24 @@ __global__ void __launch_bounds__(128, (LPD >= 8 ? 4 : (LPD == 4 ? 2 : 1))) k_gr
                 if (split) {
                     for (int dd = 0; dd < D; ++dd) {
                         if (dd == main_pick) continue;
-                        int any = 0, c2 = -1;
+                        int any = 0, c2 = -1, c2min = INT_MAX;
                         for (int m0 = 0; m0 < M; m0 += 32) {
                             const int m = m0 + lane;
                             const bool mine = m < M && mpick[m] == dd;
                             if (mine) {
                                 mgroup[m] = ng;
+                                mwork[m] += gwork[gr];   // bank the old group's uniform work
                                 c2 = max(c2, mcap[m]);
+                                c2min = min(c2min, mcap[m]);
                             }
                             any |= __any_sync(kFull, mine);
                         }
                         if (!any) continue;
 #pragma unroll
-                        for (int o = 16; o > 0; o >>= 1) c2 = max(c2, __shfl_xor_sync(kFull, c2, o));
+                        for (int o = 16; o > 0; o >>= 1) {
+                            c2 = max(c2, __shfl_xor_sync(kFull, c2, o));
+                            c2min = min(c2min, __shfl_xor_sync(kFull, c2min, o));
+                        }
                         // new group ng = state(gr) + v_t on device dd
                         if (dev) {
                             double* un = scr + ((size_t)ng * D + d) * kV + part * FPL;
@@ -668,7 +722,11 @@ __global__ void __launch_bounds__(128, (LPD >= 8 ? 4 : (LPD == 4 ? 2 : 1))) k_gr
                             gd[ng * DPW + i3] = gd[gr * DPW + i3] + (i3 == dd ? dt : 0);
                             gb[ng * DPW + i3] = gb[gr * DPW + i3] + (i3 == dd ? bt : 0);
                         }
-                        if (lane == 0) gcap[ng] = c2;
+                        if (lane == 0) {
+                            gcap[ng] = c2;
+                            gmin[ng] = c2min;
+                            gwork[ng] = 0;
+                        }
                         ++ng;
                         __syncwarp();
                     }
@@ -683,22 +741,44 @@ __global__ void __launch_bounds__(128, (LPD >= 8 ? 4 : (LPD == 4 ? 2 : 1))) k_gr
                         for (int k = 0; k < FPL; ++k) ug[k] += vcd[k];
                     }
                 }
-                int c3 = gcap_gr;
-                if (split || left) {   // members left: tighten the group's loosest cap
+                int c3 = gcap_gr, c3min = gmin[gr];
+                if (split || left) {   // members left: tighten the group's cap range
                     c3 = -1;
+                    c3min = INT_MAX;
                     for (int m = lane; m < M; m += 32)
-                        if (mgroup[m] == gr) c3 = max(c3, mcap[m]);
+                        if (mgroup[m] == gr) {
+                            c3 = max(c3, mcap[m]);
+                            c3min = min(c3min, mcap[m]);
+                        }
 #pragma unroll
-                    for (int o = 16; o > 0; o >>= 1) c3 = max(c3, __shfl_xor_sync(kFull, c3, o));
+                    for (int o = 16; o > 0; o >>= 1) {
+                        c3 = max(c3, __shfl_xor_sync(kFull, c3, o));
+                        c3min = min(c3min, __shfl_xor_sync(kFull, c3min, o));
+                    }
                 }
                 __syncwarp();
                 if (lane == 0) {
                     gd[gr * DPW + main_pick] += dt;
                     gb[gr * DPW + main_pick] += bt;
                     gcap[gr] = c3;
+                    gmin[gr] = c3min;
                 }
                 __syncwarp();
             }
+        };
+        double vn[FPL];
+        int dt_n = 0, idx_n = 0;
+        long long bt_n = 0;
+        fetch(0, vn, dt_n, bt_n, idx_n);
+#pragma unroll 1
+        for (int p = 0; p < Tp; ++p) {
+            double vcd[FPL];
+#pragma unroll
+            for (int k = 0; k < FPL; ++k) vcd[k] = vn[k];
+            const int dt = dt_n, idx = idx_n;
+            const long long bt = bt_n;
+            if (p + 1 < Tp) fetch(p + 1, vn, dt_n, bt_n, idx_n);
+            process(vcd, dt, bt, idx);
         }
         // ---- outputs: per member feasibility, work, and its group's device costs
         for (int gr = 0; gr < ng; ++gr) {
@@ -734,7 +814,7 @@ __global__ void __launch_bounds__(128, (LPD >= 8 ? 4 : (LPD == 4 ? 2 : 1))) k_gr
         }
         for (int m = lane; m < M; m += 32) {
             a.feas[tau0 + m] = mgroup[m] >= 0 ? 1 : 0;
-            a.work[tau0 + m] = mwork[m];
+            a.work[tau0 + m] = mwork[m] + (mgroup[m] >= 0 ? gwork[mgroup[m]] : 0);
             if (mgroup[m] < 0) x.dup_of[tau0 + m] = -1;
         }
         __syncwarp();
@@ -1059,7 +1139,44 @@ ns_status launch_greedy(ns_ctx* ctx, const SearchBufs& b, const ns_tables* t, lo
     const long long n = te - tb;
     int dp = 1;
     while (dp < b.D) dp <<= 1;
-    if (dp <= 16) {
+    const long long n_cp_launch = (te - tb) / b.M;
+    // Latency mode: with few column plans (a single-task column-wise search)
+    // one warp per column plan leaves most SMs idle and the step chain is the
+    // critical path, so every trajectory runs in its own lane segment
+    // (k_greedy_cta).  Throughput mode (many column plans): grouped greedy.
+    const bool latency_mode =
+        4 * dp <= 32 && (b.greedy_mode == NS_GREEDY_LANES ||
+                         (b.greedy_mode == NS_GREEDY_AUTO && n_cp_launch * 4 < (long long)ctx->sm_count * 16));
+    if (latency_mode) {
+        const int seg = 4 * dp;
+        const int mchunk = std::min(b.M, 256 / seg);
+        const int nchunk = (b.M + mchunk - 1) / mchunk;
+        const int threads = ((mchunk * seg + 31) / 32) * 32;
+        const long long g0 = tb / b.M, g1 = (te - 1) / b.M + 1;
+        GreedyArgs a2 = a;
+        a2.ord_row = b.ord_row + (size_t)g0 * b.Tpm;
+        a2.ord_idx = b.ord_idx + (size_t)g0 * b.Tpm;
+        a2.cp_valid = b.cp_valid + g0;
+        a2.cp_task = b.cp_task + g0;
+        a2.cp_Tp = b.cp_Tp + g0;
+        a2.traj_begin = (int)(tb - g0 * b.M);
+        a2.traj_end = (int)(te - g0 * b.M);
+        a2.assign = b.assign + (size_t)g0 * b.M * b.Tpm;
+        a2.comp = b.comp + (size_t)g0 * b.M * b.D;
+        a2.devdim = b.devdim + (size_t)g0 * b.M * b.D;
+        a2.feas = b.feas + (size_t)g0 * b.M;
+        a2.work = b.work + (size_t)g0 * b.M;
+        const unsigned blocks = (unsigned)((g1 - g0) * nchunk);
+        prof_begin(ctx, PK_GREEDY);
+        switch (seg) {
+            case 4: k_greedy_cta<4, 4><<<blocks, threads, 0, ctx->stream>>>(a2, mchunk, nchunk); break;
+            case 8: k_greedy_cta<8, 4><<<blocks, threads, 0, ctx->stream>>>(a2, mchunk, nchunk); break;
+            case 16: k_greedy_cta<16, 4><<<blocks, threads, 0, ctx->stream>>>(a2, mchunk, nchunk); break;
+            default: k_greedy_cta<32, 4><<<blocks, threads, 0, ctx->stream>>>(a2, mchunk, nchunk); break;
+        }
+        prof_end(ctx);
+        NS_CUDA(ctx, cudaMemsetAsync(b.dup_of + tb, 0xff, (size_t)n * sizeof(int32_t), ctx->stream));
+    } else if (dp <= 16) {
         // grouped greedy: one warp per column plan (trajectories [tb, te) are
         // whole column plans: tb, te multiples of M)
         const long long g0 = tb / b.M, g1 = te / b.M;
@@ -1082,7 +1199,7 @@ ns_status launch_greedy(ns_ctx* ctx, const SearchBufs& b, const ns_tables* t, lo
         x.dup_of = b.dup_of + (size_t)g0 * b.M;
         const int lpd = 32 / dp;
         const int DPW = dp;
-        const size_t per_warp = (((size_t)b.M * (20 + DPW * 12) + DPW * 16 + 64) + 15) & ~size_t(15);
+        const size_t per_warp = (((size_t)b.M * (28 + DPW * 12) + DPW * 16 + 64) + 15) & ~size_t(15);
         const int wpb = 4;
         const size_t smem = per_warp * wpb;
         const unsigned blocks = (unsigned)((x.total_warps + wpb - 1) / wpb);
@@ -1181,6 +1298,7 @@ ns_status run_search(ns_ctx* ctx, const ns_tables* t, int D, const ns_search_par
                      bool columnwise) {
     SearchBufs b{};
     b.n_tasks = t->n_tasks;
+    b.greedy_mode = p->flags & 3u;
     b.D = D;
     b.M = p->M;
     const int L = columnwise ? p->L : 0;

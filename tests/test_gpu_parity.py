@@ -45,9 +45,12 @@ def _rel(a, b):
     return abs(a - b) / max(abs(b), 1e-300)
 
 
-def _check_tablewise(ns, ctx, tasks, w, M):
+GREEDY = [1, 2]   # NS_GREEDY_GROUPED, NS_GREEDY_LANES: both kernels must reproduce the oracle
+
+
+def _check_tablewise(ns, ctx, tasks, w, M, greedy=0):
     tabs = _setup(ns, ctx, tasks, w)
-    out = ns.ns_shard_tablewise(ctx, tabs, w.D, M=M)
+    out = ns.ns_shard_tablewise(ctx, tabs, w.D, M=M, greedy=greedy)
     n_exact = 0
     for i, task in enumerate(tasks):
         emb = om.TableEmbeddings(w, task)
@@ -94,18 +97,38 @@ def test_hand_example(ns, ctx, golden_hand):
     assert int(out["n_scores"][0]) == e["work"]
 
 
+@pytest.mark.parametrize("greedy", GREEDY)
 @pytest.mark.parametrize("kind", ["mono", "signed"])
-def test_tablewise_C1(ns, ctx, kind):
+def test_tablewise_C1(ns, ctx, kind, greedy):
     w = gen_weights(2, kind)
-    _check_tablewise(ns, ctx, gen_tasks("C1", 100), w, M=3)
+    _check_tablewise(ns, ctx, gen_tasks("C1", 100), w, M=3, greedy=greedy)
 
 
-def test_tablewise_C2(ns, ctx):
+@pytest.mark.parametrize("greedy", GREEDY)
+def test_tablewise_C2(ns, ctx, greedy):
     w = gen_weights(4, "mono")
-    _check_tablewise(ns, ctx, gen_tasks("C2", 24), w, M=11)
+    _check_tablewise(ns, ctx, gen_tasks("C2", 24), w, M=11, greedy=greedy)
 
 
-def test_tablewise_ragged_batch_and_edge_cases(ns, ctx):
+def test_tablewise_C2_bench_launch(ns, ctx):
+    # the bench's launch configuration (many tasks -> grouped greedy, auto
+    # mode); the oracle checks a sample of tasks one by one
+    w = gen_weights(4, "mono")
+    tasks = gen_tasks("C2", 4096)
+    tabs = _setup(ns, ctx, tasks, w)
+    out = ns.ns_shard_tablewise(ctx, tabs, 4, M=11)
+    for i in range(0, 4096, 97):
+        task = tasks[i]
+        emb = om.TableEmbeddings(w, task)
+        r = osr.greedy_grid_search(w, emb, task, [], 11)
+        assert int(out["n_scores"][i]) == r.work
+        assert _rel(out["cost"][i], r.cost) <= RTOL
+        if r.assign is not None:
+            assert out["assign"][i, :task.T].tolist() == r.assign
+
+
+@pytest.mark.parametrize("greedy", GREEDY)
+def test_tablewise_ragged_batch_and_edge_cases(ns, ctx, greedy):
     # tasks of different sizes in one batch (ragged), T = 1, D = 1-like caps,
     # and tasks whose grid points strand tables
     rng = np.random.default_rng(11)
@@ -113,15 +136,16 @@ def test_tablewise_ragged_batch_and_edge_cases(ns, ctx):
     tasks = [small_task(rng, T, D, hash_hi=1e6) for T in (1, 2, 3, 7, 17, 33, 64)]
     tasks.append(small_task(rng, 9, D, cap=1 << 26, hash_hi=1e6))   # tight memory: some infeasible
     w = gen_weights(D, "signed", seed=21)
-    _check_tablewise(ns, ctx, tasks, w, M=4)
+    _check_tablewise(ns, ctx, tasks, w, M=4, greedy=greedy)
 
 
+@pytest.mark.parametrize("greedy", GREEDY)
 @pytest.mark.parametrize("D", [1, 5, 16])
-def test_tablewise_other_D(ns, ctx, D):
+def test_tablewise_other_D(ns, ctx, D, greedy):
     rng = np.random.default_rng(D)
     tasks = [small_task(rng, 3 * D + 5, D) for _ in range(6)]
     w = gen_weights(D, "mono", seed=30 + D)
-    _check_tablewise(ns, ctx, tasks, w, M=5)
+    _check_tablewise(ns, ctx, tasks, w, M=5, greedy=greedy)
 
 
 def test_tablewise_big_D_kernel(ns, ctx):
@@ -151,9 +175,9 @@ def test_infeasible_status(ns, ctx):
     assert outc["col_plan"][0, :outc["n_col"][0]].tolist() == r.col_plan
 
 
-def _check_columnwise(ns, ctx, tasks, w, N, K, L, M):
+def _check_columnwise(ns, ctx, tasks, w, N, K, L, M, greedy=0):
     tabs = _setup(ns, ctx, tasks, w)
-    out = ns.ns_shard_columnwise(ctx, tabs, w.D, N=N, K=K, L=L, M=M)
+    out = ns.ns_shard_columnwise(ctx, tabs, w.D, N=N, K=K, L=L, M=M, greedy=greedy)
     n_exact = 0
     for i, task in enumerate(tasks):
         emb = om.TableEmbeddings(w, task)
@@ -173,24 +197,34 @@ def _check_columnwise(ns, ctx, tasks, w, N, K, L, M):
     return out
 
 
-def test_columnwise_small(ns, ctx):
+@pytest.mark.parametrize("greedy", GREEDY)
+def test_columnwise_small(ns, ctx, greedy):
     w = gen_weights(4, "mono")
     tasks = gen_tasks("C2", 4, T=16)
-    _check_columnwise(ns, ctx, tasks, w, N=4, K=2, L=3, M=5)
+    _check_columnwise(ns, ctx, tasks, w, N=4, K=2, L=3, M=5, greedy=greedy)
 
 
-def test_columnwise_signed_weights(ns, ctx):
+@pytest.mark.parametrize("greedy", GREEDY)
+def test_columnwise_signed_weights(ns, ctx, greedy):
     w = gen_weights(3, "signed", seed=5)
     rng = np.random.default_rng(8)
     tasks = [small_task(rng, 12, 3) for _ in range(3)]
-    _check_columnwise(ns, ctx, tasks, w, N=3, K=3, L=3, M=4)
+    _check_columnwise(ns, ctx, tasks, w, N=3, K=3, L=3, M=4, greedy=greedy)
 
 
-def test_columnwise_C3_level1(ns, ctx):
+@pytest.mark.parametrize("greedy", GREEDY)
+def test_columnwise_C3_level1(ns, ctx, greedy):
     # C3 shapes (T=80, D=8, N=10, K=10, M=11) with L=1: every level-1 child
     w = gen_weights(8, "mono")
     tasks = gen_tasks("C3", 2)
-    _check_columnwise(ns, ctx, tasks, w, N=10, K=10, L=1, M=11)
+    _check_columnwise(ns, ctx, tasks, w, N=10, K=10, L=1, M=11, greedy=greedy)
+
+
+def test_columnwise_C4_wide_grid_level1(ns, ctx):
+    # C4 shapes: T=200, D=8, M=51 (wide grid), 8 GiB cap; level 1 of the beam
+    w = gen_weights(8, "mono")
+    tasks = gen_tasks("C4", 1)
+    _check_columnwise(ns, ctx, tasks, w, N=10, K=3, L=1, M=51, greedy=1)
 
 
 def test_columnwise_C3_full_size_sampled(ns, ctx):
