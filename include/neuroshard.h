@@ -59,6 +59,7 @@ typedef struct ns_tables ns_tables;  /* opaque featurised batch of sharding task
  * cudaStream_t (e.g. torch.cuda.current_stream().cuda_stream) or NULL for the
  * legacy default stream.  *out receives the handle. */
 ns_status ns_create(ns_ctx** out, int cuda_device, void* cuda_stream);
+/* Frees the ctx and every ns_tables it still owns (their handles become invalid). */
 ns_status ns_destroy(ns_ctx* ctx);
 const char* ns_last_error(const ns_ctx* ctx);
 ns_status ns_set_stream(ns_ctx* ctx, void* cuda_stream);
@@ -219,8 +220,13 @@ ns_status ns_shard_columnwise(ns_ctx* ctx, const ns_tables* tables, int32_t D,
 /* ------------------------------------------------------------ multi-GPU */
 /* 128-byte NCCL unique id (call on rank 0, broadcast by any means). */
 ns_status ns_comm_unique_id(unsigned char id_out[128]);
-/* Make subsequent ns_score_plans / ns_shard_columnwise calls collective over
- * nranks processes (one GPU each).  nranks == 1 is allowed (no-op comm). */
+/* Make subsequent ns_score_plans / ns_shard_* calls collective over nranks
+ * processes (one GPU each): each level's column plans are split into equal
+ * contiguous blocks per rank and the per-trajectory results are allgathered
+ * (NCCL) so every rank selects identically.  nranks == 1 is allowed (no-op).
+ * id == NULL with nranks > 1 is a test hook ("emulated ranks"): this process
+ * computes every rank's block itself, exercising the partitioning without
+ * NCCL. */
 ns_status ns_comm_init(ns_ctx* ctx, int32_t nranks, int32_t rank, const unsigned char id[128]);
 
 #ifdef __cplusplus

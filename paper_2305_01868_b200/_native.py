@@ -120,10 +120,16 @@ def _ptr(x: Any) -> Optional[int]:
 def ns_create(device: int = 0, stream: Optional[int] = None) -> int:
     h = C.c_void_p()
     _check(None, LIB.ns_create(C.byref(h), device, stream))
+    _LIVE_CTX.add(h.value)
     return h.value
 
 
+_LIVE_CTX: set = set()
+
+
 def ns_destroy(ctx: int) -> None:
+    """Destroys the ctx and every ns_tables still owned by it."""
+    _LIVE_CTX.discard(ctx)
     _check(ctx, LIB.ns_destroy(ctx))
 
 
@@ -214,9 +220,9 @@ class Tables:
         self.n_tasks = len(offsets) - 1
 
     def free(self):
-        if self.handle:
+        if self.handle and self.ctx in _LIVE_CTX:   # ns_destroy already freed it otherwise
             LIB.ns_tables_free(self.handle)
-            self.handle = None
+        self.handle = None
 
     def __del__(self):
         try:
@@ -308,5 +314,6 @@ def ns_comm_unique_id() -> bytes:
 
 
 def ns_comm_init(ctx: int, nranks: int, rank: int, uid: Optional[bytes]) -> None:
+    """uid None with nranks > 1: emulated ranks (test hook, no NCCL)."""
     buf = (C.c_ubyte * 128).from_buffer_copy(uid) if uid else None
     _check(ctx, LIB.ns_comm_init(ctx, nranks, rank, buf))

@@ -66,11 +66,12 @@ void comm_destroy(ns_ctx* ctx) {
         ctx->nccl = nullptr;
         ctx->nranks = 1;
         ctx->rank = 0;
+        ctx->emulated = false;
     }
 }
 
 ns_status comm_allgather(ns_ctx* ctx, const void* send, void* recv, size_t bytes_per_rank) {
-    if (ctx->nranks == 1) {
+    if (ctx->nranks == 1 || ctx->emulated) {
         if (send != recv)
             NS_CUDA(ctx, cudaMemcpyAsync(recv, send, bytes_per_rank, cudaMemcpyDeviceToDevice, ctx->stream));
         return NS_OK;
@@ -81,7 +82,7 @@ ns_status comm_allgather(ns_ctx* ctx, const void* send, void* recv, size_t bytes
 }
 
 ns_status comm_allreduce_min_u64(ns_ctx* ctx, uint64_t* buf, size_t count) {
-    if (ctx->nranks == 1) return NS_OK;
+    if (ctx->nranks == 1 || ctx->emulated) return NS_OK;
     ncclResult_t r = api().AllReduce(buf, buf, count, ncclUint64, ncclMin, (ncclComm_t)ctx->nccl, ctx->stream);
     if (r != ncclSuccess) return nccl_err(ctx, r, "ncclAllReduce(min)");
     return NS_OK;
@@ -103,10 +104,15 @@ ns_status ns_comm_unique_id(unsigned char id_out[128]) {
 
 ns_status ns_comm_init(ns_ctx* ctx, int32_t nranks, int32_t rank, const unsigned char id[128]) {
     if (!ctx) return NS_ERR_ARG;
-    if (nranks < 1 || rank < 0 || rank >= nranks || (nranks > 1 && !id))
-        return ns::set_err(ctx, NS_ERR_ARG, "ns_comm_init: bad nranks/rank/id");
+    if (nranks < 1 || rank < 0 || rank >= nranks) return ns::set_err(ctx, NS_ERR_ARG, "ns_comm_init: bad nranks/rank");
     ns::comm_destroy(ctx);
     if (nranks == 1) return NS_OK;
+    if (!id) {   // emulated ranks: partitioning exercised in one process, no NCCL
+        ctx->nranks = nranks;
+        ctx->rank = 0;
+        ctx->emulated = true;
+        return NS_OK;
+    }
     if (!api().ok) return ns::set_err(ctx, NS_ERR_NCCL, api().why);
     cudaSetDevice(ctx->device);
     ncclUniqueId uid;

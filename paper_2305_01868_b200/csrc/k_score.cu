@@ -157,8 +157,9 @@ ns_status run_score_plans(ns_ctx* ctx, const ns_tables* t, int task, int D, cons
         rows[T + k] = rows[col_plan[k]];
     }
     // partition the plans over ranks (contiguous blocks)
-    const long long per = (P + ctx->nranks - 1) / ctx->nranks;
-    const long long pb = std::min<long long>(P, per * ctx->rank);
+    const int R = ctx->emulated ? 1 : ctx->nranks;   // emulated ranks: one process scores every slice
+    const long long per = (P + R - 1) / R;
+    const long long pb = std::min<long long>(P, per * (ctx->emulated ? 0 : ctx->rank));
     const long long pe = std::min<long long>(P, pb + per);
     const bool dev_assign = is_device_ptr(assign);
     const int nblk_arg = 296;
@@ -237,7 +238,7 @@ ns_status run_score_plans(ns_ctx* ctx, const ns_tables* t, int task, int D, cons
     ns_status s = comm_allgather(ctx, d_best, d_all, sizeof(BestRec));
     if (s != NS_OK) return s;
     prof_begin(ctx, PK_OTHER);
-    k_argmin_final<<<1, 32, 0, ctx->stream>>>(d_all, ctx->nranks, d_best);
+    k_argmin_final<<<1, 32, 0, ctx->stream>>>(d_all, R, d_best);
     prof_end(ctx);
     NS_LAUNCHED(ctx);
     if (cost_out && pe > pb)

@@ -463,6 +463,7 @@ __global__ void __launch_bounds__(256) k_greedy_cta(const GreedyArgs a, int mchu
 // bookkeeping lives in shared memory.
 // ---------------------------------------------------------------------------
 struct DedupArgs {
+    long long tau_base;    // absolute trajectory index of the first column plan (dup_of holds absolute taus)
     int n_cp;              // column plans of this launch: [0, n_cp) relative to the GreedyArgs pointers
     int mmax;              // M
     double* scratch;       // [total_warps][M][D][64] group states (groups >= 1)
@@ -809,7 +810,7 @@ __global__ void __launch_bounds__(128, (LPD >= 8 ? 4 : (LPD == 4 ? 2 : 1))) k_gr
                 a.devdim[(tau0 + m) * D + dd] = dsum;
             }
             for (int m = lane; m < M; m += 32)
-                if (mgroup[m] == gr) x.dup_of[tau0 + m] = (m == rep) ? -1 : (int32_t)(tau0 + rep);
+                if (mgroup[m] == gr) x.dup_of[tau0 + m] = (m == rep) ? -1 : (int32_t)(x.tau_base + tau0 + rep);
             __syncwarp();
         }
         for (int m = lane; m < M; m += 32) {
@@ -1197,6 +1198,7 @@ ns_status launch_greedy(ns_ctx* ctx, const SearchBufs& b, const ns_tables* t, lo
         x.scratch = b.gscratch;
         x.total_warps = (int)std::min<long long>(x.n_cp, (long long)b.gscratch_warps);
         x.dup_of = b.dup_of + (size_t)g0 * b.M;
+        x.tau_base = g0 * b.M;
         const int lpd = 32 / dp;
         const int DPW = dp;
         const size_t per_warp = (((size_t)b.M * (28 + DPW * 12) + DPW * 16 + 64) + 15) & ~size_t(15);
@@ -1256,6 +1258,43 @@ ns_status launch_finalize(ns_ctx* ctx, const SearchBufs& b, long long tb, long l
     return launch_plan_cost(ctx, 0, n, nullptr, b.comp, b.devdim, b.tcost, b.uniq, b.n_uniq);
 }
 
+// One level's trajectories: the n_cp column plans are split into equal
+// contiguous blocks over the ranks (whole column plans, so grouped
+// trajectories stay together); each rank runs N4 + N5 on its block, then the
+// per-trajectory results (cost, feasibility, work, duplicate link, assignment)
+// are allgathered in place so every rank runs the identical N6 selection
+// (SURVEY §8(e)).  Single rank: plain launches.
+ns_status run_level_trajectories(ns_ctx* ctx, const SearchBufs& b, const ns_tables* t, long long n_cp) {
+    const long long R = ctx->nranks;
+    const long long per = (n_cp + R - 1) / R;
+    ns_status s;
+    // emulated ranks (test hook, ns_comm_init with id == NULL): this process
+    // computes every rank's block into the shared buffers, the allgather is
+    // the identity
+    const long long r0 = ctx->emulated ? 0 : ctx->rank, r1 = ctx->emulated ? R : ctx->rank + 1;
+    for (long long rk = r0; rk < r1; ++rk) {
+        const long long cb = std::min(n_cp, rk * per), ce = std::min(n_cp, cb + per);
+        if (ce > cb) {
+            if ((s = launch_greedy(ctx, b, t, cb * b.M, ce * b.M)) != NS_OK) return s;
+            if ((s = launch_finalize(ctx, b, cb * b.M, ce * b.M)) != NS_OK) return s;
+        }
+    }
+    if (R == 1 || ctx->emulated) return NS_OK;
+    const long long rk = ctx->rank;
+    const size_t blk = (size_t)per * b.M;   // trajectories per rank block
+    struct {
+        void* base;
+        size_t elem;
+    } arrs[] = {{b.tcost, sizeof(double)}, {b.feas, 1}, {b.work, sizeof(uint32_t)}, {b.dup_of, sizeof(int32_t)},
+                {b.assign, (size_t)b.Tpm}};
+    for (auto& ar : arrs) {
+        char* recv = (char*)ar.base;
+        const size_t bytes = blk * ar.elem;
+        if ((s = comm_allgather(ctx, recv + (size_t)rk * bytes, recv, bytes)) != NS_OK) return s;
+    }
+    return NS_OK;
+}
+
 // Copy staged results to the caller's (host or device) pointers.
 ns_status deliver(ns_ctx* ctx, const ns_tables* t, const OutStage& o, int Lout, int Tpm, ns_plan_batch* out) {
     const int n = t->n_tasks;
@@ -1308,7 +1347,13 @@ ns_status run_search(ns_ctx* ctx, const ns_tables* t, int D, const ns_search_par
     b.Tpm = t->T_max + L;
     const int C = (columnwise && L > 0) ? b.K * b.N2 : 1;
     b.S = b.n_tasks * C;
-    b.n_traj = b.S * b.M;
+    {
+        // trajectory capacity: rank blocks of whole column plans (allgather needs
+        // equal blocks), level 0 has n_tasks column plans, beam levels S
+        const long long R = ctx->nranks;
+        const long long per0 = (b.n_tasks + R - 1) / R, per = ((long long)b.S + R - 1) / R;
+        b.n_traj = (int)(std::max(per0, per) * R * b.M);
+    }
     const int Lout = L;
     {
         int dp = 1;
@@ -1348,8 +1393,8 @@ ns_status run_search(ns_ctx* ctx, const ns_tables* t, int D, const ns_search_par
     prof_end(ctx);
     NS_LAUNCHED(ctx);
     const long long n0 = (long long)b.n_tasks * b.M;
-    if ((s = launch_greedy(ctx, b, t, 0, n0)) != NS_OK) return s;
-    if ((s = launch_finalize(ctx, b, 0, n0)) != NS_OK) return s;
+    (void)n0;
+    if ((s = run_level_trajectories(ctx, b, t, b.n_tasks)) != NS_OK) return s;
     prof_begin(ctx, PK_SELECT);
     k_select<<<b.n_tasks, 128, (size_t)1 * 16, ctx->stream>>>(b, 1, 0, b.K);
     prof_end(ctx);
@@ -1367,8 +1412,7 @@ ns_status run_search(ns_ctx* ctx, const ns_tables* t, int D, const ns_search_par
         k_build_order<<<b.S, 256, osm, ctx->stream>>>(b, tv);
         prof_end(ctx);
         NS_LAUNCHED(ctx);
-        if ((s = launch_greedy(ctx, b, t, 0, b.n_traj)) != NS_OK) return s;
-        if ((s = launch_finalize(ctx, b, 0, b.n_traj)) != NS_OK) return s;
+        if ((s = run_level_trajectories(ctx, b, t, b.S)) != NS_OK) return s;
         prof_begin(ctx, PK_SELECT);
         k_select<<<b.n_tasks, 128, (size_t)C * 16, ctx->stream>>>(b, C, level, b.K);
         prof_end(ctx);

@@ -190,6 +190,8 @@ ns_status ns_destroy(ns_ctx* ctx) {
     if (!ctx) return NS_ERR_ARG;
     cudaSetDevice(ctx->device);
     cudaStreamSynchronize(ctx->stream);
+    while (!ctx->tables.empty()) ns_tables_free(*ctx->tables.begin());
+    cudaStreamSynchronize(ctx->stream);
     free_model(ctx->model);
     if (ctx->arena) cudaFree(ctx->arena);
     if (ctx->pinned) cudaFreeHost(ctx->pinned);
@@ -415,12 +417,14 @@ ns_status ns_featurize_tables(ns_ctx* ctx, const ns_table_desc* tables, const in
     launch_tables_validate(ctx, t);
     launch_precompute(ctx, t, 0, 0);
     if ((e = cudaGetLastError()) != cudaSuccess) return fail(e);
+    ctx->tables.insert(t);
     *out = t;
     return NS_OK;
 }
 
 ns_status ns_tables_free(ns_tables* t) {
     if (!t) return NS_ERR_ARG;
+    if (t->ctx) t->ctx->tables.erase(t);
     cudaStream_t st = t->ctx ? t->ctx->stream : nullptr;
     if (t->ctx) cudaSetDevice(t->ctx->device);
     void* ps[] = {t->d_off, t->d_cap, t->d_sumdim, t->d_desc, t->d_feat, t->d_V, t->d_C, t->d_vdim, t->d_vbytes,

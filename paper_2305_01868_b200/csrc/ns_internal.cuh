@@ -5,6 +5,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <set>
 #include <string>
 #include <vector>
 
@@ -95,6 +96,8 @@ struct ns_ctx {
     // multi-GPU
     void* nccl = nullptr;    // ncclComm_t
     int nranks = 1, rank = 0;
+    bool emulated = false;   // ns_comm_init(id == NULL): all ranks' blocks computed in-process (test hook)
+    std::set<ns_tables*> tables;   // live ns_tables of this ctx (freed by ns_destroy)
 };
 
 struct ns_tables {

@@ -315,3 +315,33 @@ def test_determinism(ns, ctx):
     b = ns.ns_shard_columnwise(ctx, tabs, 8, N=10, K=3, L=4, M=11)
     for k in ("cost", "n_col", "col_plan", "assign", "grid_index", "n_scores"):
         assert np.array_equal(a[k], b[k]), k
+
+
+@pytest.mark.parametrize("nranks", [2, 3])
+def test_rank_partition_emulated(ns, ctx, nranks):
+    """Trajectory partitioning over ranks: with emulated ranks
+    every rank's block of column plans is computed separately; the results
+    must equal the single-rank run bit for bit (table-wise and column-wise)."""
+    w = gen_weights(4, "mono")
+    tasks = gen_tasks("C2", 7, T=18)
+    tabs = _setup(ns, ctx, tasks, w)
+    # each greedy kernel against its own single-rank run (the two kernels split
+    # the 64 features differently over lanes, so their last bits may differ)
+    ref = {g: (ns.ns_shard_tablewise(ctx, tabs, 4, M=11, greedy=g),
+               ns.ns_shard_columnwise(ctx, tabs, 4, N=4, K=3, L=3, M=5, greedy=g)) for g in (1, 2)}
+    ns.ns_comm_init(ctx, nranks, 0, None)
+    try:
+        for greedy in (1, 2):
+            ref_t, ref_c = ref[greedy]
+            got_t = ns.ns_shard_tablewise(ctx, tabs, 4, M=11, greedy=greedy)
+            got_c = ns.ns_shard_columnwise(ctx, tabs, 4, N=4, K=3, L=3, M=5, greedy=greedy)
+            for k in ("cost", "assign", "grid_index", "n_scores"):
+                assert np.array_equal(got_t[k], ref_t[k]), k
+            for k in ("cost", "n_col", "col_plan", "assign", "grid_index", "n_scores"):
+                assert np.array_equal(got_c[k], ref_c[k]), k
+        A = gen_plans(18, 4, 1000, seed=2)
+        c1, b1, v1 = ns.ns_score_plans(ctx, tabs, 0, 4, [], A)
+    finally:
+        ns.ns_comm_init(ctx, 1, 0, None)
+    c0, b0, v0 = ns.ns_score_plans(ctx, tabs, 0, 4, [], A)
+    assert np.array_equal(c0, c1) and b0 == b1 and v0 == v1
