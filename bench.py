@@ -362,7 +362,8 @@ def search_latency(ns, ctx, torch):
     """Wall time of one ns_shard_* call for ONE task (featurise included,
     model load excluded), C2 table-wise and C3 column-wise."""
     res = {}
-    for cfg, mode in (("C2", "tablewise"), ("C3", "columnwise")):
+    for cfg, mode in (("C1", "tablewise"), ("C2", "tablewise"), ("C3", "columnwise"), ("C4", "columnwise"),
+                      ("C5", "columnwise")):
         c = CONFIGS[cfg]
         w = gen_weights(c["D"], "mono")
         ns.ns_load_cost_models(ctx, w)

@@ -45,6 +45,7 @@ struct SearchBufs {
     int32_t* dup_of;     // [n_traj] grouped greedy: tau whose plan this one duplicates, or -1
     int32_t* uniq;       // [n_traj] compacted list of trajectories carrying a distinct feasible plan
     int32_t* n_uniq;     // [1]
+    unsigned int* next_cp;   // [1] grouped-greedy work queue
     double* gscratch;    // grouped greedy group states
     int gscratch_warps;
     // per task
@@ -469,6 +470,7 @@ struct DedupArgs {
     double* scratch;       // [total_warps][M][D][64] group states (groups >= 1)
     int total_warps;
     int32_t* dup_of;       // [n_traj] tau of the member whose plan this one duplicates, or -1
+    unsigned int* next_cp; // dynamic queue counter (zeroed before the launch)
 };
 
 template <int LPD>
@@ -501,7 +503,10 @@ __global__ void __launch_bounds__(128, (LPD >= 8 ? 4 : (LPD == 4 ? 2 : 1))) k_gr
     for (int k = 0; k < FPL; ++k) asm volatile("" : "+d"(uinit[k]));
     const long long gw = (long long)blockIdx.x * nw + wl;
     double* scr = x.scratch + (size_t)gw * M * D * kV;   // this warp's group states
-    for (long long g = gw; g < x.n_cp; g += x.total_warps) {
+    // dynamic column-plan queue (column plans differ in length and in how many
+    // groups they split into; a static stride leaves a long tail)
+    long long g = gw;
+    for (; g < x.n_cp;) {
         const bool valid = a.cp_valid[g] != 0;
         const long long tau0 = g * M;
         if (!valid) {
@@ -510,6 +515,9 @@ __global__ void __launch_bounds__(128, (LPD >= 8 ? 4 : (LPD == 4 ? 2 : 1))) k_gr
                 a.work[tau0 + m] = 0;
                 x.dup_of[tau0 + m] = -1;
             }
+            long long nx = 0;
+            if (lane == 0) nx = x.total_warps + (long long)atomicAdd(x.next_cp, 1u);
+            g = __shfl_sync(kFull, nx, 0);
             continue;
         }
         const int q = a.cp_task[g];
@@ -819,6 +827,9 @@ __global__ void __launch_bounds__(128, (LPD >= 8 ? 4 : (LPD == 4 ? 2 : 1))) k_gr
             if (mgroup[m] < 0) x.dup_of[tau0 + m] = -1;
         }
         __syncwarp();
+        long long nx = 0;
+        if (lane == 0) nx = x.total_warps + (long long)atomicAdd(x.next_cp, 1u);
+        g = __shfl_sync(kFull, nx, 0);
     }
 }
 
@@ -1081,6 +1092,7 @@ void carve(Carver& c, SearchBufs& b, OutStage& o, int Lout) {
     b.dup_of = c.take<int32_t>(b.n_traj);
     b.uniq = c.take<int32_t>(b.n_traj);
     b.n_uniq = c.take<int32_t>(1);
+    b.next_cp = c.take<unsigned int>(1);
     b.gscratch = c.take<double>((size_t)b.gscratch_warps * b.M * b.D * kV);
     b.capdim = c.take<int32_t>((size_t)b.n_tasks * b.M);
     b.beam_plan = c.take<int32_t>((size_t)b.n_tasks * b.K * b.Lcap);
@@ -1199,6 +1211,8 @@ ns_status launch_greedy(ns_ctx* ctx, const SearchBufs& b, const ns_tables* t, lo
         x.total_warps = (int)std::min<long long>(x.n_cp, (long long)b.gscratch_warps);
         x.dup_of = b.dup_of + (size_t)g0 * b.M;
         x.tau_base = g0 * b.M;
+        x.next_cp = b.next_cp;
+        NS_CUDA(ctx, cudaMemsetAsync(b.next_cp, 0, sizeof(unsigned int), ctx->stream));
         const int lpd = 32 / dp;
         const int DPW = dp;
         const size_t per_warp = (((size_t)b.M * (28 + DPW * 12) + DPW * 16 + 64) + 15) & ~size_t(15);
