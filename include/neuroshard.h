@@ -25,10 +25,9 @@
  *    DEVICE memory are complete when the ctx stream reaches that point.
  *  - A ctx is bound to one GPU and is not thread-safe.  One process per GPU.
  *  - Arithmetic: cost-model forward passes, greedy scores and plan costs are
- *    computed in IEEE fp64 (the oracle's precision), so decisions agree with
- *    the fp64 oracle except at relative top-2 margins ~1e-15.  Exception:
- *    ns_score_plans with NS_SCORE_TF32X3 runs the comm MLPs on tcgen05 tensor
- *    cores in split-TF32 (3 products) with FP32 accumulation (~1e-6 rel).
+ *    computed in IEEE fp64 (the oracle's precision; dense MLP layers on the
+ *    FP64 tensor cores), so decisions agree with the fp64 oracle except at
+ *    relative top-2 margins ~1e-15.
  */
 #ifndef NEUROSHARD_H
 #define NEUROSHARD_H
@@ -149,8 +148,7 @@ ns_status ns_tables_single_costs(ns_ctx* ctx, const ns_tables* tables,
 
 /* ------------------------------------------------------------ plan scoring */
 typedef enum {
-    NS_SCORE_FP64 = 0,    /* fp64 SIMT (default) */
-    NS_SCORE_TF32X3 = 1   /* comm MLPs on tcgen05, split-TF32 x3, FP32 accumulate */
+    NS_SCORE_FP64 = 0     /* fp64: pooling on the FP64 pipe, comm MLPs on the FP64 tensor cores */
 } ns_score_mode;
 
 /* Simulator f(c, t) as a service ("estimate the embedding cost of any

@@ -142,8 +142,6 @@ __global__ void k_argmin_final(const BestRec* in, int n, BestRec* out) {
     out->idx = bi;
 }
 
-ns_status run_score_plans_tf32x3(ns_ctx* ctx, const ScoreArgs& a, double* dcost);
-
 ns_status run_score_plans(ns_ctx* ctx, const ns_tables* t, int task, int D, const int32_t* col_plan, int n_col,
                           const int8_t* assign, int64_t P, int mode, double* cost_out, int64_t* best_index_out,
                           double* best_cost_out) {
@@ -205,10 +203,8 @@ ns_status run_score_plans(ns_ctx* ctx, const ns_tables* t, int task, int D, cons
     a.ok = d_ok;
     a.head = ctx->model.head;
     if (pe > pb) {
-        if (mode == NS_SCORE_TF32X3) {
-            ns_status s = run_score_plans_tf32x3(ctx, a, d_cost);
-            if (s != NS_OK) return s;
-        } else {
+        (void)mode;
+        {
             const size_t per_warp = ((size_t)D * kV + (D + 1) / 2) * sizeof(double);
             int wpb = 4;
             while (wpb > 1 && per_warp * wpb > 96 * 1024) wpb >>= 1;

@@ -137,8 +137,6 @@ static void free_model(ns::DevModel& m) {
         for (int l = 0; l < 5; ++l) {
             if (m.cW[r][l]) cudaFree(m.cW[r][l]);
             if (m.cb[r][l]) cudaFree(m.cb[r][l]);
-            if (m.cWf[r][l]) cudaFree(m.cWf[r][l]);
-            if (m.cbf[r][l]) cudaFree(m.cbf[r][l]);
         }
     m = ns::DevModel();
 }
@@ -311,13 +309,6 @@ ns_status ns_load_cost_models(ns_ctx* ctx, const ns_compute_model* cm, const ns_
             size_t nw = (size_t)widths[l] * widths[l + 1];
             if ((s = upload(ctx, &m.cW[r][l], cms[r]->layer[l].W, nw, &fp)) != NS_OK) return s;
             if ((s = upload(ctx, &m.cb[r][l], cms[r]->layer[l].b, widths[l + 1], &fp)) != NS_OK) return s;
-            std::vector<float> wf(nw), bf(widths[l + 1]);
-            for (size_t i = 0; i < nw; ++i) wf[i] = (float)cms[r]->layer[l].W[i];
-            for (int i = 0; i < widths[l + 1]; ++i) bf[i] = (float)cms[r]->layer[l].b[i];
-            NS_CUDA(ctx, cudaMalloc(&m.cWf[r][l], nw * sizeof(float)));
-            NS_CUDA(ctx, cudaMemcpy(m.cWf[r][l], wf.data(), nw * sizeof(float), cudaMemcpyHostToDevice));
-            NS_CUDA(ctx, cudaMalloc(&m.cbf[r][l], bf.size() * sizeof(float)));
-            NS_CUDA(ctx, cudaMemcpy(m.cbf[r][l], bf.data(), bf.size() * sizeof(float), cudaMemcpyHostToDevice));
         }
     m.start_scale = fwd->start_scale;
     m.dim_scale = fwd->dim_scale;
@@ -530,7 +521,7 @@ ns_status ns_score_plans(ns_ctx* ctx, const ns_tables* t, int32_t task, int32_t 
     if (!ctx->model.loaded) return set_err(ctx, NS_ERR_STATE, "no cost models loaded");
     if (D != ctx->model.D) return set_err(ctx, NS_ERR_ARG, "D differs from the loaded comm models' D");
     if (task < 0 || task >= t->n_tasks) return set_err(ctx, NS_ERR_ARG, "task out of range");
-    if (mode != NS_SCORE_FP64 && mode != NS_SCORE_TF32X3) return set_err(ctx, NS_ERR_ARG, "bad mode");
+    if (mode != NS_SCORE_FP64) return set_err(ctx, NS_ERR_ARG, "bad mode");
     // validate the column plan against the evolving dims
     if (n_col > 0) {
         ns_status ds = ensure_host_dims(ctx, t);

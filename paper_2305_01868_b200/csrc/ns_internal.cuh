@@ -43,9 +43,6 @@ struct DevModel {
     int cin[5] = {0}, cout[5] = {0};
     double* cW[2][5] = {{nullptr}};
     double* cb[2][5] = {{nullptr}};
-    // fp32 copies (TF32x3 score path)
-    float* cWf[2][5] = {{nullptr}};
-    float* cbf[2][5] = {{nullptr}};
     double start_scale = 20.0, dim_scale = 1024.0;
     uint64_t fingerprint = 0;
 };
