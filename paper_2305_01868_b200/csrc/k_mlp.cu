@@ -181,18 +181,29 @@ struct PreDmmaArgs {
     int ldx, ldy;
 };
 
+// One warp owns 16 rows.  The 128-wide hidden layer is produced in four
+// 32-column chunks and folded into the layer-2 accumulators (kept in
+// registers) immediately, so only a 16x32 chunk is ever staged in shared
+// memory (11 KB per warp instead of 21 KB -> 2.5x the resident warps).  v
+// leaves the accumulator fragments straight to HBM; the single-table cost is
+// reduced from the same fragments.
 __global__ void __launch_bounds__(128) k_precompute_dmma(const PreDmmaArgs a) {
     extern __shared__ double qsm[];
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
-    const int per_warp = 16 * (a.ldx + a.ldy);
-    double* X = qsm + (size_t)w * per_warp;
-    double* Y = X + 16 * a.ldx;
+    const int g = lane >> 2, t = lane & 3;
+    const int ldx = a.ldx, ldh = a.ldy;             // x and e stride / h-chunk stride
+    const int per_warp = 16 * (ldx + ldh + ldh) + 16;
+    double* X = qsm + (size_t)w * per_warp;         // [16][8]  features (zero padded)
+    double* Hc = X + 16 * ldx;                      // [16][32] hidden chunk
+    double* E = Hc + 16 * ldh;                      // [16][32] table representation e
+    long long* rowid = (long long*)(E + 16 * ldh);  // [16] variant row (or -1)
     for (long long base = ((long long)blockIdx.x * nwarps + w) * 16; base < a.n_rows;
          base += (long long)gridDim.x * nwarps * 16) {
-        // features of the 16 rows (lane r < 16 owns row r); invalid variants -> zeros
+        // ---- features of the 16 rows (lane r < 16 owns row r); invalid variants -> zeros
         if (lane < 16) {
             const long long r = base + lane;
             double x[kF] = {0, 0, 0, 0, 0};
+            long long row = -1;
             if (r < a.n_rows) {
                 const long long gtab = r / a.nj;
                 const int j = a.jlo + (int)(r % a.nj);
@@ -203,7 +214,7 @@ __global__ void __launch_bounds__(128) k_precompute_dmma(const PreDmmaArgs a) {
                     if (dim % 8 != 0) ok = false;
                     dim >>= 1;
                 }
-                const long long row = gtab * kDepth + j;
+                row = gtab * kDepth + j;
                 if (ok) {
                     x[0] = (double)dim / 128.0;
                     x[1] = log10((double)td.hash_size) / 8.0;
@@ -215,39 +226,128 @@ __global__ void __launch_bounds__(128) k_precompute_dmma(const PreDmmaArgs a) {
                     a.vbytes[row] = td.hash_size * (long long)dim * 4;
                 } else {
                     a.vdim[row] = 0;
+                    row = -1;   // no v / cost for a variant that cannot exist
+                }
+            }
+            rowid[lane] = row;
+#pragma unroll
+            for (int f = 0; f < kF; ++f) X[lane * ldx + f] = x[f];
+            for (int f = kF; f < 8; ++f) X[lane * ldx + f] = 0.0;
+        }
+        __syncwarp();
+        // ---- layers 1+2 fused over 4 chunks of 32 hidden units
+        double e_acc[2][4][2];
+#pragma unroll
+        for (int m = 0; m < 2; ++m)
+#pragma unroll
+            for (int q = 0; q < 4; ++q) e_acc[m][q][0] = e_acc[m][q][1] = 0.0;
+#pragma unroll 1
+        for (int hc = 0; hc < kH / 32; ++hc) {
+            // h chunk = ReLU(x W1[hc*32 .. +32]^T + b1)   (K = 5, padded to 8)
+            double hacc[2][4][2];
+#pragma unroll
+            for (int m = 0; m < 2; ++m)
+#pragma unroll
+                for (int q = 0; q < 4; ++q) hacc[m][q][0] = hacc[m][q][1] = 0.0;
+#pragma unroll
+            for (int kt = 0; kt < 2; ++kt) {
+                const int k = 4 * kt + t;
+                const double a0 = X[g * ldx + k], a1 = X[(8 + g) * ldx + k];
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    const int n = hc * 32 + 8 * q + g;
+                    const double bv = k < kF ? __ldg(a.enc1W + n * kF + k) : 0.0;
+                    dmma(hacc[0][q], a0, bv);
+                    dmma(hacc[1][q], a1, bv);
                 }
             }
 #pragma unroll
-            for (int f = 0; f < kF; ++f) X[lane * a.ldx + f] = x[f];
-            for (int f = kF; f < 8; ++f) X[lane * a.ldx + f] = 0.0;
+            for (int q = 0; q < 4; ++q) {
+                const int col = 8 * q + 2 * t;
+                const double b0 = __ldg(a.enc1b + hc * 32 + col), b1 = __ldg(a.enc1b + hc * 32 + col + 1);
+#pragma unroll
+                for (int m = 0; m < 2; ++m) {
+                    double2 hv;
+                    hv.x = relu_exact(hacc[m][q][0] + b0);
+                    hv.y = relu_exact(hacc[m][q][1] + b1);
+                    *reinterpret_cast<double2*>(Hc + (8 * m + g) * ldh + col) = hv;
+                }
+            }
+            __syncwarp();
+            // e_acc += h_chunk W2[:, hc*32 .. +32]^T    (K = 32 per chunk)
+#pragma unroll
+            for (int kt = 0; kt < 8; ++kt) {
+                const int k = 4 * kt + t;
+                const double a0 = Hc[g * ldh + k], a1 = Hc[(8 + g) * ldh + k];
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    const int n = 8 * q + g;
+                    const double bv = __ldg(a.enc2W + n * kH + hc * 32 + k);
+                    dmma(e_acc[0][q], a0, bv);
+                    dmma(e_acc[1][q], a1, bv);
+                }
+            }
+            __syncwarp();
+        }
+        // ---- e = ReLU(e_acc + b2) -> smem
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const int col = 8 * q + 2 * t;
+            const double b0 = __ldg(a.enc2b + col), b1 = __ldg(a.enc2b + col + 1);
+#pragma unroll
+            for (int m = 0; m < 2; ++m) {
+                double2 ev;
+                ev.x = relu_exact(e_acc[m][q][0] + b0);
+                ev.y = relu_exact(e_acc[m][q][1] + b1);
+                *reinterpret_cast<double2*>(E + (8 * m + g) * ldh + col) = ev;
+            }
         }
         __syncwarp();
-        warp_layer<true>(a.enc1W, a.enc1b, kF, kH, X, a.ldx, Y, a.ldy, lane);     // 5 -> 128
-        warp_layer<true>(a.enc2W, a.enc2b, kH, kE, Y, a.ldy, X, a.ldx, lane);     // 128 -> 32 (e)
-        warp_layer<false>(a.H1, nullptr, kE, kV, X, a.ldx, Y, a.ldy, lane);       // v = H1 e
-        // write v (coalesced) and the single-table cost
-        for (int i = lane; i < 16 * kV; i += 32) {
-            const int r = i / kV, k = i % kV;
-            const long long rr = base + r;
-            if (rr < a.n_rows) {
-                const long long row = (rr / a.nj) * kDepth + a.jlo + (int)(rr % a.nj);
-                a.V[row * kV + k] = Y[r * a.ldy + k];
+        // ---- v = H1 e (64 outputs, K = 32), straight from the fragments to HBM,
+        //      and the single-table cost C({t}) = hb2 + sum_k H2_k ReLU(v_k + hb1_k)
+        double cpart[2] = {0.0, 0.0};
+        const long long row0 = rowid[g], row1 = rowid[8 + g];
+#pragma unroll
+        for (int nc = 0; nc < 2; ++nc) {
+            double vacc[2][4][2];
+#pragma unroll
+            for (int m = 0; m < 2; ++m)
+#pragma unroll
+                for (int q = 0; q < 4; ++q) vacc[m][q][0] = vacc[m][q][1] = 0.0;
+#pragma unroll
+            for (int kt = 0; kt < 8; ++kt) {
+                const int k = 4 * kt + t;
+                const double a0 = E[g * ldh + k], a1 = E[(8 + g) * ldh + k];
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    const int n = nc * 32 + 8 * q + g;
+                    const double bv = __ldg(a.H1 + n * kE + k);
+                    dmma(vacc[0][q], a0, bv);
+                    dmma(vacc[1][q], a1, bv);
+                }
+            }
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const int col = nc * 32 + 8 * q + 2 * t;
+#pragma unroll
+                for (int m = 0; m < 2; ++m) {
+                    const long long row = m ? row1 : row0;
+                    const double v0 = vacc[m][q][0], v1 = vacc[m][q][1];
+                    if (row >= 0) *reinterpret_cast<double2*>(a.V + row * kV + col) = make_double2(v0, v1);
+                    cpart[m] = fma(a.head.H2[col], relu_exact(v0 + a.head.hb1[col]), cpart[m]);
+                    cpart[m] = fma(a.head.H2[col + 1], relu_exact(v1 + a.head.hb1[col + 1]), cpart[m]);
+                }
             }
         }
-        if (lane < 16) {
-            const long long rr = base + lane;
-            if (rr < a.n_rows) {
-                const long long row = (rr / a.nj) * kDepth + a.jlo + (int)(rr % a.nj);
-                double c0 = 0.0, c1 = 0.0, c2 = 0.0, c3 = 0.0;
-                for (int k = 0; k < kV; k += 4) {
-                    const double* y = Y + lane * a.ldy + k;
-                    c0 = fma(a.head.H2[k], relu_exact(y[0] + a.head.hb1[k]), c0);
-                    c1 = fma(a.head.H2[k + 1], relu_exact(y[1] + a.head.hb1[k + 1]), c1);
-                    c2 = fma(a.head.H2[k + 2], relu_exact(y[2] + a.head.hb1[k + 2]), c2);
-                    c3 = fma(a.head.H2[k + 3], relu_exact(y[3] + a.head.hb1[k + 3]), c3);
-                }
-                a.C[row] = a.head.hb2 + ((c0 + c1) + (c2 + c3));
-            }
+        // reduce the 4 lanes of each row (fixed xor order -> deterministic)
+#pragma unroll
+        for (int m = 0; m < 2; ++m) {
+            cpart[m] += __shfl_xor_sync(kFull, cpart[m], 1);
+            cpart[m] += __shfl_xor_sync(kFull, cpart[m], 2);
+        }
+        if (t == 0) {
+            if (row0 >= 0) a.C[row0] = a.head.hb2 + cpart[0];
+            if (row1 >= 0) a.C[row1] = a.head.hb2 + cpart[1];
         }
         __syncwarp();
     }
@@ -305,13 +405,13 @@ void launch_precompute(ns_ctx* ctx, const ns_tables* t, int jlo, int jhi) {
     a.C = t->d_C;
     a.vdim = t->d_vdim;
     a.vbytes = t->d_vbytes;
-    a.ldx = ld_pad(kE > 8 ? kE : 8);   // holds x (8) and e (32)
-    a.ldy = ld_pad(kH);                // holds h (128) and v (64)
+    a.ldx = ld_pad(8);    // x (8 features, zero padded)
+    a.ldy = ld_pad(32);   // hidden chunk and e (32)
     const int wpb = 4;
-    const size_t smem = (size_t)wpb * 16 * (a.ldx + a.ldy) * sizeof(double);
+    const size_t smem = (size_t)wpb * (16 * (a.ldx + 2 * a.ldy) + 16) * sizeof(double);
     cudaFuncSetAttribute(k_precompute_dmma, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     long long blocks = (a.n_rows + 16LL * wpb - 1) / (16LL * wpb);
-    const long long cap = (long long)ctx->sm_count * 8;
+    const long long cap = (long long)ctx->sm_count * 16;
     if (blocks > cap) blocks = cap;
     if (blocks < 1) blocks = 1;
     prof_begin(ctx, PK_PRECOMPUTE);
