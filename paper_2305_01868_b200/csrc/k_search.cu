@@ -437,6 +437,27 @@ __global__ void __launch_bounds__(256) k_greedy_cta(const GreedyArgs a, int mchu
     }
 }
 
+// cp.async (LDGSTS) helpers: the grouped greedy streams the next kStages
+// tables' v rows into a per-warp shared-memory ring so the HBM/L2 latency of
+// the row fetch is hidden behind kStages - 1 steps of work.
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+    const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sa), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
+    const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(sa), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async4(void* smem, const void* gmem) {
+    const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(sa), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
+constexpr int kStages = 8;   // row-stream ring depth of the grouped greedy
+
 // ---------------------------------------------------------------------------
 // Grouped greedy (used for D <= 16): one WARP per column plan, all M grid
 // trajectories of that column plan handled together.
@@ -474,7 +495,7 @@ struct DedupArgs {
 };
 
 template <int LPD>
-__global__ void __launch_bounds__(128, (LPD >= 8 ? 4 : (LPD == 4 ? 2 : 1))) k_greedy_dedup(const GreedyArgs a, const DedupArgs x) {
+__global__ void __launch_bounds__(128, (LPD >= 8 ? 5 : (LPD == 4 ? 2 : 1))) k_greedy_dedup(const GreedyArgs a, const DedupArgs x) {
     constexpr int FPL = kV / LPD;
     constexpr int DPW = 32 / LPD;   // device slots per warp
     extern __shared__ unsigned char dsm[];
@@ -483,7 +504,8 @@ __global__ void __launch_bounds__(128, (LPD >= 8 ? 4 : (LPD == 4 ? 2 : 1))) k_gr
     const int d = lane / LPD, part = lane % LPD;
     const bool dev = d < D;
     // per-warp shared bookkeeping
-    const size_t per_warp = (size_t)M * (4 + 4 + 4 + 4 + DPW * 4 + DPW * 8 + 4 + 8) + DPW * (8 + 4 + 4) + 64;
+    const size_t per_warp = (size_t)M * (4 + 4 + 4 + 4 + DPW * 4 + DPW * 8 + 4 + 8) + DPW * (8 + 4 + 4) + 64 +
+                            kStages * (LPD * (FPL * 8 + 16) + 16) + 16;
     unsigned char* base = dsm + (size_t)wl * ((per_warp + 15) & ~size_t(15));
     long long* gb = (long long*)base;                 // [M][DPW] group bytes per device
     double* sc = (double*)(gb + (size_t)M * DPW);     // [DPW] scores of the current group
@@ -497,10 +519,19 @@ __global__ void __launch_bounds__(128, (LPD >= 8 ? 4 : (LPD == 4 ? 2 : 1))) k_gr
     int* sok = sdv + DPW;                             // [DPW] device scored
     int* gmin = sok + DPW;                            // [M] tightest cap among a group's live members
     uint32_t* gwork = (uint32_t*)(gmin + M);          // [M] work of the group's uniform steps
-    double w[FPL], u0[FPL], uinit[FPL];
-    load_lane_head<FPL>(a.head, part, uinit, w);
-#pragma unroll
-    for (int k = 0; k < FPL; ++k) asm volatile("" : "+d"(uinit[k]));
+    constexpr int SS = FPL * 8 + 16;                  // ring slice stride (bytes): +16 B keeps the LPD
+    constexpr int RS = LPD * SS;                      //   slices of a row on distinct banks
+    unsigned char* ring = (unsigned char*)(((uintptr_t)(gwork + M) + 15) & ~uintptr_t(15));   // [kStages][RS]
+    int* sdt = (int*)(ring + kStages * RS);           // [kStages] dim of the staged table
+    int* sidx = sdt + kStages;                        // [kStages] its list index
+    long long* sbt = (long long*)(sidx + kStages);    // [kStages] its bytes
+    // hb1 (the empty-device pre-activation) is re-read from shared memory at
+    // every column plan instead of occupying FPL registers for the whole kernel
+    __shared__ double s_hb1[kV];
+    for (int k = threadIdx.x; k < kV; k += blockDim.x) s_hb1[k] = a.head.hb1[k];
+    __syncthreads();
+    double w[FPL], u0[FPL];
+    load_lane_head<FPL>(a.head, part, u0, w);
     const long long gw = (long long)blockIdx.x * nw + wl;
     double* scr = x.scratch + (size_t)gw * M * D * kV;   // this warp's group states
     // dynamic column-plan queue (column plans differ in length and in how many
@@ -546,7 +577,7 @@ __global__ void __launch_bounds__(128, (LPD >= 8 ? 4 : (LPD == 4 ? 2 : 1))) k_gr
         }
         if (lane == 0) gcap[0] = cmax;
 #pragma unroll
-        for (int k = 0; k < FPL; ++k) u0[k] = uinit[k];
+        for (int k = 0; k < FPL; ++k) u0[k] = s_hb1[part * FPL + k];
         int ng = 1;
         __syncwarp();
         const int32_t* orow = a.ord_row + (size_t)g * a.Tpm;
@@ -555,18 +586,24 @@ __global__ void __launch_bounds__(128, (LPD >= 8 ? 4 : (LPD == 4 ? 2 : 1))) k_gr
         // table's (v slice, dim, bytes, list index) is fetched while the
         // current one is processed (two register buffers, loop unrolled by 2)
         int8_t* asg_lane = a.assign + (size_t)(tau0 + lane) * a.Tpm;   // member m = lane (+32k)
-        auto fetch = [&](int pp, double (&vb)[FPL], int& dtb, long long& btb, int& idxb) {
-            const int r = __ldg(orow + pp);
-            const double2* src = reinterpret_cast<const double2*>(a.V + (size_t)r * kV + part * FPL);
-#pragma unroll
-            for (int i2 = 0; i2 < FPL / 2; ++i2) {
-                const double2 xv = __ldg(src + i2);
-                vb[2 * i2] = xv.x;
-                vb[2 * i2 + 1] = xv.y;
+        // row-index window: the next 32 entries of the cost order in one register per lane
+        int oc_cur = lane < Tp ? __ldg(orow + lane) : 0;
+        int oc_nxt = 32 + lane < Tp ? __ldg(orow + 32 + lane) : 0;
+        auto issue = [&](int pp) {   // stage table pp of the cost order into ring slot pp % kStages
+            if (pp < Tp) {
+                if (pp > 0 && (pp & 31) == 0) {
+                    oc_cur = oc_nxt;
+                    oc_nxt = pp + 32 + lane < Tp ? __ldg(orow + pp + 32 + lane) : 0;
+                }
+                const int r = __shfl_sync(kFull, oc_cur, pp & 31);
+                unsigned char* st = ring + (pp % kStages) * RS;
+                constexpr int CPS = FPL / 2;   // 16-byte chunks per slice
+                cp_async16(st + (lane / CPS) * SS + (lane % CPS) * 16, a.V + (size_t)r * kV + 2 * lane);
+                if (lane == 0) cp_async4(sdt + pp % kStages, a.vdim + r);
+                if (lane == 1) cp_async4(sidx + pp % kStages, oidx + pp);
+                if (lane == 2) cp_async8(sbt + pp % kStages, a.vbytes + r);
             }
-            dtb = __ldg(a.vdim + r);
-            btb = __ldg(a.vbytes + r);
-            idxb = __ldg(oidx + pp);
+            cp_async_commit();   // one group per step, empty past the end
         };
         auto process = [&](const double (&vcd)[FPL], const int dt, const long long bt, const int idx) {
             const int ng0 = ng;
@@ -775,20 +812,26 @@ __global__ void __launch_bounds__(128, (LPD >= 8 ? 4 : (LPD == 4 ? 2 : 1))) k_gr
                 __syncwarp();
             }
         };
-        double vn[FPL];
-        int dt_n = 0, idx_n = 0;
-        long long bt_n = 0;
-        fetch(0, vn, dt_n, bt_n, idx_n);
+#pragma unroll 1
+        for (int pp = 0; pp < kStages - 1; ++pp) issue(pp);
 #pragma unroll 1
         for (int p = 0; p < Tp; ++p) {
+            __syncwarp();                  // slot (p - 1) % kStages fully consumed
+            issue(p + kStages - 1);
+            cp_async_wait<kStages - 1>();  // table p has landed (this lane's copies)
+            __syncwarp();                  // ... and every lane's
+            const int sl = p % kStages;
             double vcd[FPL];
+            const double2* src = reinterpret_cast<const double2*>(ring + sl * RS + part * SS);
 #pragma unroll
-            for (int k = 0; k < FPL; ++k) vcd[k] = vn[k];
-            const int dt = dt_n, idx = idx_n;
-            const long long bt = bt_n;
-            if (p + 1 < Tp) fetch(p + 1, vn, dt_n, bt_n, idx_n);
-            process(vcd, dt, bt, idx);
+            for (int i2 = 0; i2 < FPL / 2; ++i2) {
+                const double2 xv = src[i2];
+                vcd[2 * i2] = xv.x;
+                vcd[2 * i2 + 1] = xv.y;
+            }
+            process(vcd, sdt[sl], sbt[sl], sidx[sl]);
         }
+        cp_async_wait<0>();
         // ---- outputs: per member feasibility, work, and its group's device costs
         for (int gr = 0; gr < ng; ++gr) {
             double hp;
@@ -1215,7 +1258,8 @@ ns_status launch_greedy(ns_ctx* ctx, const SearchBufs& b, const ns_tables* t, lo
         NS_CUDA(ctx, cudaMemsetAsync(b.next_cp, 0, sizeof(unsigned int), ctx->stream));
         const int lpd = 32 / dp;
         const int DPW = dp;
-        const size_t per_warp = (((size_t)b.M * (28 + DPW * 12) + DPW * 16 + 64) + 15) & ~size_t(15);
+        const size_t per_warp = (((size_t)b.M * (28 + DPW * 12) + DPW * 16 + 64 +
+                                  kStages * ((size_t)lpd * ((64 / lpd) * 8 + 16) + 16) + 16) + 15) & ~size_t(15);
         const int wpb = 4;
         const size_t smem = per_warp * wpb;
         const unsigned blocks = (unsigned)((x.total_warps + wpb - 1) / wpb);
@@ -1374,7 +1418,7 @@ ns_status run_search(ns_ctx* ctx, const ns_tables* t, int D, const ns_search_par
         while (dp < D) dp <<= 1;
         const long long max_cp = (long long)b.S;
         const size_t per = (size_t)b.M * D * kV * sizeof(double);
-        long long warps = std::min<long long>(max_cp, (long long)ctx->sm_count * 16);
+        long long warps = std::min<long long>(max_cp, (long long)ctx->sm_count * 20);
         warps = std::max<long long>(4, std::min<long long>(warps, (long long)((512ull << 20) / per)));
         b.gscratch_warps = dp <= 16 ? (int)(((warps + 3) / 4) * 4) : 0;
     }
