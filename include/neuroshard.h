@@ -135,6 +135,10 @@ typedef struct {
  *   task_offsets host, [n_tasks + 1], task_offsets[0] == 0, each task >= 1 table
  *   mem_cap      host, [n_tasks], per-GPU memory cap in bytes (P:368 4 GB;
  *                table bytes = hash * dim * 4, reading R7)
+ * Descriptors in pageable host memory are validated before the call returns
+ * (NS_ERR_ARG); device-resident or pinned descriptors are copied directly and
+ * validated on the GPU, an invalid one making the next synchronising call
+ * (ns_shard_*, ns_score_plans) return NS_ERR_ARG.
  * Requires loaded models.  *out is freed with ns_tables_free. */
 ns_status ns_featurize_tables(ns_ctx* ctx, const ns_table_desc* tables,
                               const int32_t* task_offsets, const int64_t* mem_cap,

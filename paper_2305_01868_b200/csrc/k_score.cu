@@ -241,9 +241,13 @@ ns_status run_score_plans(ns_ctx* ctx, const ns_tables* t, int task, int D, cons
         NS_CUDA(ctx, cudaMemcpyAsync(cost_out + pb, d_cost + pb, (size_t)(pe - pb) * 8, cudaMemcpyDefault,
                                      ctx->stream));
     BestRec h;
+    int32_t hflag = 0;
     NS_CUDA(ctx, cudaMemcpyAsync(&h, d_best, sizeof(BestRec), cudaMemcpyDeviceToHost, ctx->stream));
+    NS_CUDA(ctx, cudaMemcpyAsync(&hflag, t->d_flag, sizeof(int32_t), cudaMemcpyDeviceToHost, ctx->stream));
     NS_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
     prof_collect(ctx);
+    ns_status fs = check_tables_flag(ctx, t, &hflag);
+    if (fs != NS_OK) return fs;
     if (best_index_out) *best_index_out = h.idx;
     if (best_cost_out) *best_cost_out = h.cost;
     return NS_OK;

@@ -35,6 +35,17 @@ bool is_device_ptr(const void* p) {
     return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
 }
 
+bool is_pinned_host_ptr(const void* p) {
+    if (!p) return false;
+    cudaPointerAttributes a;
+    cudaError_t e = cudaPointerGetAttributes(&a, p);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return a.type == cudaMemoryTypeHost;
+}
+
 void* arena_get(ns_ctx* ctx, size_t bytes) {
     if (bytes <= ctx->arena_bytes) return ctx->arena;
     if (ctx->arena) {
@@ -338,6 +349,10 @@ ns_status ns_featurize_tables(ns_ctx* ctx, const ns_table_desc* tables, const in
     const int n = task_offsets[n_tasks];
     cudaSetDevice(ctx->device);
     const bool dev_in = is_device_ptr(tables);
+    // pinned host descriptors are DMA'd directly and validated on the device
+    // like device-resident ones (no host pass over the batch)
+    const bool pinned_in = !dev_in && is_pinned_host_ptr(tables);
+    const bool direct = dev_in || pinned_in;
     ns_tables* t = new (std::nothrow) ns_tables();
     if (!t) return set_err(ctx, NS_ERR_NOMEM, "host alloc");
     t->ctx = ctx;
@@ -346,9 +361,10 @@ ns_status ns_featurize_tables(ns_ctx* ctx, const ns_table_desc* tables, const in
     t->T_max = T_max;
     t->off.assign(task_offsets, task_offsets + n_tasks + 1);
     t->cap.assign(mem_cap, mem_cap + n_tasks);
-    if (!dev_in) {
-        // host descriptors: validate here; device descriptors are validated by
-        // the k_tables_validate kernel and reported at the next synchronising call
+    if (!direct) {
+        // pageable host descriptors: validate here; device / pinned descriptors
+        // are validated by the k_tables_validate kernel and reported at the next
+        // synchronising call
         t->dims.resize(n);
         for (int g = 0; g < n; ++g) {
             const ns_table_desc& d = tables[g];
@@ -383,7 +399,7 @@ ns_status ns_featurize_tables(ns_ctx* ctx, const ns_table_desc* tables, const in
 #undef NS_TALLOC
     // small host arrays go through pinned staging so the copies stay async
     const size_t meta = (n_tasks + 1) * sizeof(int32_t) + n_tasks * sizeof(int64_t);
-    const size_t hbytes = meta + (dev_in ? 0 : (size_t)n * sizeof(ns_table_desc));
+    const size_t hbytes = meta + (direct ? 0 : (size_t)n * sizeof(ns_table_desc));
     char* pin = (char*)pinned_get(ctx, hbytes + 64);
     if (!pin) {
         ns_tables_free(t);
@@ -392,18 +408,18 @@ ns_status ns_featurize_tables(ns_ctx* ctx, const ns_table_desc* tables, const in
     if ((e = cudaStreamSynchronize(st)) != cudaSuccess) return fail(e);   // pinned buffer reuse
     std::memcpy(pin, task_offsets, (n_tasks + 1) * sizeof(int32_t));
     std::memcpy(pin + (n_tasks + 1) * sizeof(int32_t), mem_cap, n_tasks * sizeof(int64_t));
-    if (!dev_in) std::memcpy(pin + meta, tables, (size_t)n * sizeof(ns_table_desc));
+    if (!direct) std::memcpy(pin + meta, tables, (size_t)n * sizeof(ns_table_desc));
     if ((e = cudaMemcpyAsync(t->d_off, pin, (n_tasks + 1) * sizeof(int32_t), cudaMemcpyHostToDevice, st)) !=
         cudaSuccess)
         return fail(e);
     if ((e = cudaMemcpyAsync(t->d_cap, pin + (n_tasks + 1) * sizeof(int32_t), n_tasks * sizeof(int64_t),
                              cudaMemcpyHostToDevice, st)) != cudaSuccess)
         return fail(e);
-    if ((e = cudaMemcpyAsync(t->d_desc, dev_in ? (const void*)tables : (const void*)(pin + meta),
+    if ((e = cudaMemcpyAsync(t->d_desc, direct ? (const void*)tables : (const void*)(pin + meta),
                              n * sizeof(ns_table_desc), dev_in ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice,
                              st)) != cudaSuccess)
         return fail(e);
-    if ((e = cudaMemsetAsync(t->d_vdim, 0, rows * sizeof(int32_t), st)) != cudaSuccess) return fail(e);
+    // (vdim of every row is written by the precompute of its depth before any read)
     if ((e = cudaMemsetAsync(t->d_flag, 0, sizeof(int32_t), st)) != cudaSuccess) return fail(e);
     launch_tables_validate(ctx, t);
     launch_precompute(ctx, t, 0, 0);

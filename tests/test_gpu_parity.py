@@ -345,3 +345,53 @@ def test_rank_partition_emulated(ns, ctx, nranks):
         ns.ns_comm_init(ctx, 1, 0, None)
     c0, b0, v0 = ns.ns_score_plans(ctx, tabs, 0, 4, [], A)
     assert np.array_equal(c0, c1) and b0 == b1 and v0 == v1
+
+
+def test_columnwise_C5_full_size_sampled(ns, ctx):
+    """C5 (1000 tables, 128 simulated GPUs, beam N=10 K=3 L=10 M=11) through the
+    multi-warp greedy kernel; the oracle recomputes the returned plan's cost
+    from scratch and checks validity (memory cap, the winning grid cap)."""
+    from workload.synth import CONFIGS
+    c = CONFIGS["C5"]
+    w = gen_weights(128, "mono")
+    task = gen_task("C5", 0)
+    tabs = _setup(ns, ctx, [task], w)
+    out = ns.ns_shard_columnwise(ctx, tabs, 128, N=c["N"], K=c["K"], L=c["L"], M=c["M"])
+    assert out["status"] == 0
+    nc = int(out["n_col"][0])
+    col = out["col_plan"][0, :nc].tolist()
+    tables = osr.apply_col_plan(task, col)
+    a = out["assign"][0, :len(tables)].tolist()
+    emb = om.TableEmbeddings(w, task)
+    assert _rel(out["cost"][0], om.plan_cost(w, emb, tables, a, 128)[0]) <= RTOL
+    load = np.zeros(128, np.int64)
+    dd = np.zeros(128, np.int64)
+    for j, d in enumerate(a):
+        load[d] += osr.table_bytes(task, tables[j])
+        dd[d] += tables[j][1]
+    assert load.max() <= task.cap
+    md = osr.grid_max_dims(int(task.dims.sum()), 128, c["M"])[int(out["grid_index"][0])]
+    assert dd.max() <= math.floor(md)
+    # the search never returns something worse than the empty column plan
+    r0 = ns.ns_shard_tablewise(ctx, tabs, 128, M=c["M"])
+    assert out["cost"][0] <= r0["cost"][0]
+
+
+def test_invalid_descriptor_device_and_pinned(ns, ctx):
+    """Pageable host descriptors are validated at ns_featurize_tables; device
+    and pinned ones on the GPU, reported by the next synchronising call."""
+    import torch
+    w = gen_weights(4, "mono")
+    ns.ns_load_cost_models(ctx, w)
+    tasks = gen_tasks("C2", 2)
+    desc, off, caps = ns.table_descs(tasks)
+    desc["dim"][5] = 6     # not a multiple of 4 (P:237)
+    with pytest.raises(ns.NSError):
+        ns.ns_featurize_tables(ctx, desc, off, caps)
+    for buf in (torch.from_numpy(desc.view(np.uint8)).cuda(), torch.from_numpy(desc.view(np.uint8)).pin_memory()):
+        tabs = ns.ns_featurize_tables(ctx, buf, off, caps)
+        with pytest.raises(ns.NSError):
+            ns.ns_shard_tablewise(ctx, tabs, 4, M=11)
+        with pytest.raises(ns.NSError):
+            ns.ns_score_plans(ctx, tabs, 0, 4, [], gen_plans(40, 4, 8, seed=1))
+        tabs.free()
