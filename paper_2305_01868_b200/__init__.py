@@ -9,6 +9,7 @@ from ._native import (  # noqa: F401
     LIB,
     LIB_PATH,
     NS_SCORE_FP64,
+    NS_SCORE_TF32X3,
     NS_GREEDY_AUTO,
     NS_GREEDY_GROUPED,
     NS_GREEDY_LANES,

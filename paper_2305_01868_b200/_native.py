@@ -16,7 +16,7 @@ _PKG = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_PKG, "libneuroshard.so")
 
 NS_OK, NS_INFEASIBLE = 0, 1
-NS_SCORE_FP64 = 0
+NS_SCORE_FP64, NS_SCORE_TF32X3 = 0, 1
 _STATUS = {0: "NS_OK", 1: "NS_INFEASIBLE", -1: "NS_ERR_ARG", -2: "NS_ERR_STATE", -3: "NS_ERR_NOMEM",
            -4: "NS_ERR_CUDA", -5: "NS_ERR_NCCL", -6: "NS_ERR_INTERNAL"}
 

@@ -9,6 +9,7 @@
 #include <cuda_runtime.h>
 #include <math_constants.h>
 
+#include <algorithm>
 #include <cstring>
 #include <vector>
 
@@ -77,6 +78,75 @@ __global__ void __launch_bounds__(128) k_pool(const ScoreArgs a) {
 __global__ void k_mark_bad(const uint8_t* ok, double* cost, long long pb, long long pe) {
     for (long long p = pb + (long long)blockIdx.x * blockDim.x + threadIdx.x; p < pe; p += (long long)gridDim.x * blockDim.x)
         if (!ok[p]) cost[p] = CUDART_NAN;
+}
+
+// Staged pooling (T' * 512 B fits in shared memory): every plan of a call
+// scores the same task, so each CTA stages the task's v rows and dims once
+// (coalesced).  A warp scores a plan: it reads the assignment 32 tables at a
+// time (one coalesced byte load), splits the chunk by device with one ballot
+// per device, and lane k accumulates features (2k, 2k+1) of every device in
+// registers over that device's tables in list order -- warp-level segmented
+// adds over staged rows, no read-modify-write through memory.
+template <int DM>
+__global__ void __launch_bounds__(256) k_pool_staged(const ScoreArgs a) {
+    extern __shared__ double ssm[];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, wpb = blockDim.x >> 5;
+    const int D = a.D, Tp = a.Tp;
+    double* sv = ssm;                                            // [Tp][64]
+    int* sdim = (int*)(sv + (size_t)Tp * kV);                    // [Tp]
+    for (int i = threadIdx.x; i < Tp * (kV / 2); i += blockDim.x) {
+        const int t = i / (kV / 2), c = i % (kV / 2);
+        const int row = __ldg(a.rows + t);
+        reinterpret_cast<double2*>(sv + (size_t)t * kV)[c] = __ldg(reinterpret_cast<const double2*>(a.V + (size_t)row * kV) + c);
+    }
+    for (int t = threadIdx.x; t < Tp; t += blockDim.x) sdim[t] = __ldg(a.vdim + __ldg(a.rows + t));
+    __syncthreads();
+    const double hb0 = a.head.hb1[2 * lane], hb1 = a.head.hb1[2 * lane + 1];
+    const double w0 = a.head.H2[2 * lane], w1 = a.head.H2[2 * lane + 1];
+    for (long long p = a.p_begin + (long long)blockIdx.x * wpb + w; p < a.p_end; p += (long long)gridDim.x * wpb) {
+        double acc[DM][2];
+#pragma unroll
+        for (int d = 0; d < DM; ++d) {
+            acc[d][0] = hb0;
+            acc[d][1] = hb1;
+        }
+        int dd_local = 0;   // lane d < D: dims of device d
+        bool bad = false;
+        const int8_t* pa = a.assign + p * Tp;
+        for (int c0 = 0; c0 < Tp; c0 += 32) {
+            const int t0 = c0 + lane;
+            const int my_a = t0 < Tp ? (int)pa[t0] : 0;
+            const int my_dim = t0 < Tp ? sdim[t0] : 0;
+            bad |= __any_sync(kFull, t0 < Tp && (my_a < 0 || my_a >= D));
+#pragma unroll
+            for (int d = 0; d < DM; ++d) {
+                if (d >= D) break;
+                unsigned m = __ballot_sync(kFull, t0 < Tp && my_a == d);
+                const int s = __reduce_add_sync(kFull, (m >> lane) & 1 ? my_dim : 0);
+                if (lane == d) dd_local += s;
+                while (m) {   // this device's tables of the chunk, in list order
+                    const int j = __ffs(m) - 1;
+                    m &= m - 1;
+                    const double2 vv = reinterpret_cast<const double2*>(sv + (size_t)(c0 + j) * kV)[lane];
+                    acc[d][0] += vv.x;
+                    acc[d][1] += vv.y;
+                }
+            }
+        }
+#pragma unroll
+        for (int d = 0; d < DM; ++d) {
+            if (d >= D) break;
+            double part = w0 * relu_exact(acc[d][0]) + w1 * relu_exact(acc[d][1]);
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) part += __shfl_xor_sync(kFull, part, o);
+            const int ddim = __shfl_sync(kFull, dd_local, d);
+            if (lane == 0) {
+                a.comp[p * D + d] = ddim > 0 ? part + a.head.hb2 : 0.0;
+                a.devdim[p * D + d] = ddim;
+            }
+        }
+        if (lane == 0) a.ok[p] = bad ? 0 : 1;
+    }
 }
 
 struct BestRec {
@@ -163,7 +233,7 @@ ns_status run_score_plans(ns_ctx* ctx, const ns_tables* t, int task, int D, cons
     const int nblk_arg = 296;
     const long long np_ = pe - pb;
     size_t need = 256 + (size_t)Tp * 4 + (size_t)P * 8 + (size_t)(nblk_arg + 2 + ctx->nranks) * sizeof(BestRec) +
-                  (size_t)np_ * D * 12 + (size_t)np_ + 4096;
+                  (size_t)np_ * D * 20 + (size_t)np_ + 4096;
     if (!dev_assign) need += (size_t)np_ * Tp + 256;
     char* base = (char*)arena_get(ctx, need);
     if (!base) return set_err(ctx, NS_ERR_NOMEM, "device arena (score)");
@@ -182,6 +252,8 @@ ns_status run_score_plans(ns_ctx* ctx, const ns_tables* t, int task, int D, cons
     double* d_comp = (double*)take((size_t)np_ * D * 8) - pb * D;        // global plan indexing
     int32_t* d_dd = (int32_t*)take((size_t)np_ * D * 4) - pb * D;
     uint8_t* d_ok = (uint8_t*)take((size_t)np_) - pb;
+    float* d_fwd = mode == NS_SCORE_TF32X3 ? (float*)take((size_t)np_ * D * 4) : nullptr;
+    float* d_bwd = mode == NS_SCORE_TF32X3 ? (float*)take((size_t)np_ * D * 4) : nullptr;
     const int8_t* d_assign = assign;
     if (!dev_assign && pe > pb) {
         int8_t* tmp = (int8_t*)take((size_t)np_ * Tp);
@@ -203,25 +275,50 @@ ns_status run_score_plans(ns_ctx* ctx, const ns_tables* t, int task, int D, cons
     a.ok = d_ok;
     a.head = ctx->model.head;
     if (pe > pb) {
-        (void)mode;
         {
-            const size_t per_warp = ((size_t)D * kV + (D + 1) / 2) * sizeof(double);
-            int wpb = 4;
-            while (wpb > 1 && per_warp * wpb > 96 * 1024) wpb >>= 1;
-            const size_t smem = per_warp * wpb;
-            if (smem > 48 * 1024)
-                cudaFuncSetAttribute(k_pool, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-            long long blocks = (np_ + wpb - 1) / wpb;
-            const long long cap = (long long)ctx->sm_count * 16;
-            if (blocks > cap) blocks = cap;
-            prof_begin(ctx, PK_SCORE);
-            k_pool<<<(unsigned)blocks, wpb * 32, smem, ctx->stream>>>(a);
-            prof_end(ctx);
-            NS_LAUNCHED(ctx);
-            ns_status s = launch_plan_cost(ctx, pb, pe, nullptr, d_comp, d_dd, d_cost);
-            if (s != NS_OK) return s;
-            k_mark_bad<<<(unsigned)std::min<long long>((np_ + 255) / 256, 4096), 256, 0, ctx->stream>>>(d_ok, d_cost, pb, pe);
-            NS_LAUNCHED(ctx);
+            const size_t stage = (size_t)Tp * kV * sizeof(double) + (size_t)Tp * sizeof(int) + 16;
+            const size_t uw = (size_t)D * kV * sizeof(double);
+            (void)uw;
+            if (D <= 16 && stage <= 160 * 1024) {
+                // staged task rows, registers per device: 8 warps per CTA
+                const int wpb = 8;
+                const size_t smem = stage;
+                long long blocks = (np_ + wpb - 1) / wpb;
+                const long long cap = (long long)ctx->sm_count * std::max<long long>(1, (long long)((200 * 1024) / smem));
+                if (blocks > cap) blocks = cap;
+                prof_begin(ctx, PK_SCORE);
+#define NS_POOL(DM)                                                                                       \
+    cudaFuncSetAttribute(k_pool_staged<DM>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);      \
+    k_pool_staged<DM><<<(unsigned)blocks, wpb * 32, smem, ctx->stream>>>(a);
+                if (D <= 2) { NS_POOL(2) } else if (D <= 4) { NS_POOL(4) } else if (D <= 8) { NS_POOL(8) } else { NS_POOL(16) }
+#undef NS_POOL
+                prof_end(ctx);
+                NS_LAUNCHED(ctx);
+            } else {
+                const size_t per_warp = ((size_t)D * kV + (D + 1) / 2) * sizeof(double);
+                int wpb = 4;
+                while (wpb > 1 && per_warp * wpb > 96 * 1024) wpb >>= 1;
+                const size_t smem = per_warp * wpb;
+                if (smem > 48 * 1024)
+                    cudaFuncSetAttribute(k_pool, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+                long long blocks = (np_ + wpb - 1) / wpb;
+                const long long cap = (long long)ctx->sm_count * 16;
+                if (blocks > cap) blocks = cap;
+                prof_begin(ctx, PK_SCORE);
+                k_pool<<<(unsigned)blocks, wpb * 32, smem, ctx->stream>>>(a);
+                prof_end(ctx);
+                NS_LAUNCHED(ctx);
+            }
+            if (mode == NS_SCORE_TF32X3) {
+                ns_status s = launch_plan_cost_tc(ctx, pb, pe, d_comp, d_dd, d_ok, d_fwd - pb * D, d_bwd - pb * D, d_cost);
+                if (s != NS_OK) return s;
+            } else {
+                ns_status s = launch_plan_cost(ctx, pb, pe, nullptr, d_comp, d_dd, d_cost);
+                if (s != NS_OK) return s;
+                k_mark_bad<<<(unsigned)std::min<long long>((np_ + 255) / 256, 4096), 256, 0, ctx->stream>>>(d_ok, d_cost,
+                                                                                                           pb, pe);
+                NS_LAUNCHED(ctx);
+            }
         }
     }
     k_argmin<<<nblk_arg, 256, 0, ctx->stream>>>(d_cost, pb, pe, d_part);

@@ -1,0 +1,380 @@
+// k_score_tc.cu -- ns_score_plans bulk mode (NS_SCORE_TF32X3): the two
+// communication-cost MLPs (2D -> 128 -> 64 -> 32 -> 16 -> D) as a
+// chain of tcgen05 GEMMs on the 5th-generation tensor cores.
+//
+// Precision: every operand is split x = hi + lo with hi = x rounded to TF32
+// (10-bit mantissa) and lo = x - hi (exact in fp32), and each layer computes
+// A_hi B_hi + A_hi B_lo + A_lo B_hi with FP32 accumulation in TMEM ("3xTF32"):
+// ~1e-6 relative, FP32-grade, within the north star's 1e-3 plan-cost
+// tolerance.  The greedy search keeps the fp64 DMMA path (its decisions are
+// compared at far smaller margins).
+//
+// Structure (one CTA of 128 threads per SM, persistent over 128-row tiles,
+// one launch per model direction): the model's weights (hi/lo, K-major
+// canonical no-swizzle layout) stay resident in shared memory; thread i owns
+// plan row i = TMEM lane i.  Per tile: build the input rows, then for each
+// layer one elected thread issues tcgen05.mma (A, B from shared-memory
+// descriptors, D in TMEM), tcgen05.commit arrives on an mbarrier, and the
+// 4 warps read their 32 TMEM lanes back (tcgen05.ld), apply bias + ReLU,
+// re-split and write the next layer's A operand.  The 128-wide hidden layer is
+// consumed by layer 2 in four 32-column K chunks through a double-buffered
+// operand ring so the activations never need more than 64 KB of smem.
+#include <cuda_runtime.h>
+#include <math_constants.h>
+
+#include <algorithm>
+
+#include "ns_device.cuh"
+#include "ns_internal.cuh"
+
+namespace ns {
+namespace {
+
+constexpr int kTile = 128;     // rows (plans) per tile = TMEM lanes = UMMA M
+
+__device__ __forceinline__ uint32_t su32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+// UMMA shared-memory descriptor, K-major, SWIZZLE_NONE (canonical layout
+// ((8,m),2):((16B,SBO),LBO)), version 1.
+__device__ __forceinline__ uint64_t umma_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+    uint64_t d = (uint64_t)((saddr >> 4) & 0x3FFF);
+    d |= (uint64_t)((lbo >> 4) & 0x3FFF) << 16;
+    d |= (uint64_t)((sbo >> 4) & 0x3FFF) << 32;
+    d |= (uint64_t)1 << 46;
+    return d;
+}
+
+// Instruction descriptor: kind::tf32, D f32, A/B tf32 K-major, M x N.
+__device__ __forceinline__ uint32_t idesc_tf32(int M, int N) {
+    return (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
+}
+
+// element (r, k) of a K-major [rows x K] operand, in floats
+__device__ __forceinline__ int kmaj(int r, int k, int rows) {
+    return (k >> 2) * (rows * 4) + (r >> 3) * 32 + (r & 7) * 4 + (k & 3);
+}
+
+__device__ __forceinline__ float tf32_rn(float x) {   // round to nearest TF32 (10-bit mantissa)
+    uint32_t u = __float_as_uint(x);
+    u += 0x1000u;
+    return __uint_as_float(u & 0xFFFFE000u);
+}
+
+__device__ __forceinline__ void mma_tf32(uint32_t tmem, uint64_t ad, uint64_t bd, uint32_t idesc, uint32_t acc) {
+    asm volatile("{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
+                 " tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n}" ::"r"(tmem),
+                 "l"(ad), "l"(bd), "r"(idesc), "r"(acc));
+}
+
+__device__ __forceinline__ void commit(uint64_t* bar) {
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(su32(bar)));
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
+    uint32_t done = 0;
+    while (!done) {
+        asm volatile("{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}"
+                     : "=r"(done)
+                     : "r"(su32(bar)), "r"(phase));
+    }
+}
+
+// 16 consecutive fp32 columns of this thread's TMEM lane
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, float (&v)[16]) {
+    uint32_t r[16];
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+                   "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+                 : "r"(taddr));
+    asm volatile("tcgen05.wait::ld.sync.aligned;");
+#pragma unroll
+    for (int j = 0; j < 16; ++j) v[j] = __uint_as_float(r[j]);
+}
+
+struct TcArgs {
+    long long row_begin, row_end;   // plan rows
+    int D, K0p, N5p;                // 2D padded to 8, D padded to 16
+    int dir;                        // 0 fwd (starts = comp - min comp), 1 bwd (starts = 0)
+    const double* comp;             // [P][D]
+    const int32_t* devdim;          // [P][D]
+    float* out;                     // [P][D] MLP output of this direction
+    const double* W[5];
+    const double* b[5];
+    double start_scale, dim_scale;
+    int n_tiles;
+};
+
+// weight smem layout: per layer hi block then lo block, each K-major [Np x Kp]
+struct WLayout {
+    int Kp[5], Np[5], K[5], N[5];
+    int off[5];      // float offset of the hi block; lo block follows
+    int total;       // floats
+};
+
+__device__ __forceinline__ WLayout wlayout(int D, int K0p, int N5p) {
+    WLayout L;
+    const int K[5] = {2 * D, 128, 64, 32, 16};
+    const int N[5] = {128, 64, 32, 16, D};
+    const int Kp[5] = {K0p, 128, 64, 32, 16};
+    const int Np[5] = {128, 64, 32, 16, N5p};
+    int o = 0;
+    for (int l = 0; l < 5; ++l) {
+        L.K[l] = K[l];
+        L.N[l] = N[l];
+        L.Kp[l] = Kp[l];
+        L.Np[l] = Np[l];
+        L.off[l] = o;
+        o += 2 * Kp[l] * Np[l];
+    }
+    L.total = o;
+    return L;
+}
+
+__global__ void __launch_bounds__(128, 1) k_plan_mlp_tc(const TcArgs a) {
+    extern __shared__ __align__(128) float tsm[];
+    __shared__ uint32_t s_tmem;
+    __shared__ __align__(8) uint64_t s_bar[3];   // 0: layer done, 1/2: layer-2 chunk buffers free
+    __shared__ float s_bias[128 + 64 + 32 + 16 + 64];
+    const int tid = threadIdx.x, warp = tid >> 5;
+    const WLayout L = wlayout(a.D, a.K0p, a.N5p);
+    float* sW = tsm;                       // weights (resident)
+    float* sA = tsm + L.total;             // activation operand: 2 buffers x [128 x 32] x (hi, lo)
+    constexpr int kChunk = 32;
+    const int abuf = kTile * kChunk * 2;   // floats per chunk buffer (hi + lo)
+    // ---- resident weights: hi/lo split, K-major, zero padded
+    for (int l = 0; l < 5; ++l) {
+        const int Kp = L.Kp[l], Np = L.Np[l], K = L.K[l], N = L.N[l];
+        float* hi = sW + L.off[l];
+        float* lo = hi + Kp * Np;
+        for (int i = tid; i < Kp * Np; i += blockDim.x) {
+            const int n = i / Kp, k = i % Kp;
+            const float x = (n < N && k < K) ? (float)a.W[l][(size_t)n * K + k] : 0.0f;
+            const float h = tf32_rn(x);
+            hi[kmaj(n, k, Np)] = h;
+            lo[kmaj(n, k, Np)] = x - h;
+        }
+    }
+    {
+        const int N[5] = {128, 64, 32, 16, a.D};
+        const int off[5] = {0, 128, 192, 224, 240};
+        for (int l = 0; l < 5; ++l)
+            for (int i = tid; i < N[l]; i += blockDim.x) s_bias[off[l] + i] = (float)a.b[l][i];
+    }
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 256;" ::"r"(su32(&s_tmem)));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    if (tid == 0) {
+        for (int i = 0; i < 3; ++i) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(su32(&s_bar[i])));
+        asm volatile("fence.mbarrier_init.release.cluster;");
+    }
+    asm volatile("fence.proxy.async.shared::cta;");
+    asm volatile("tcgen05.fence::before_thread_sync;");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;");
+    const uint32_t tmem = s_tmem;
+    const uint32_t lane_base = tmem + ((uint32_t)(warp * 32) << 16);
+    uint32_t ph0 = 0, ph1 = 0, ph2 = 0;   // mbarrier phases
+    const float* bias1 = s_bias;
+    const float* bias2 = s_bias + 128;
+    const float* bias3 = s_bias + 192;
+    const float* bias4 = s_bias + 224;
+    const float* bias5 = s_bias + 240;
+
+    // issue one layer: D[cols d0..) (+)= A . B^T over k-steps [ks0, ks1) of the A/B blocks
+    auto issue = [&](const float* Ahi, const float* Alo, int arows_k4stride, const float* Bhi, const float* Blo,
+                     int Np, int ks0, int ks1, int kb_off, uint32_t dcol, bool acc_first) {
+        const uint32_t idesc = idesc_tf32(kTile, Np);
+        for (int s = ks0; s < ks1; ++s) {
+            const uint64_t ahd = umma_desc(su32(Ahi + 2 * (s - ks0) * kTile * 4), kTile * 16, 128);
+            const uint64_t ald = umma_desc(su32(Alo + 2 * (s - ks0) * kTile * 4), kTile * 16, 128);
+            const uint64_t bhd = umma_desc(su32(Bhi + 2 * (s + kb_off) * Np * 4), Np * 16, 128);
+            const uint64_t bld = umma_desc(su32(Blo + 2 * (s + kb_off) * Np * 4), Np * 16, 128);
+            const uint32_t acc0 = (s > ks0 || acc_first) ? 1u : 0u;
+            mma_tf32(tmem + dcol, ahd, bhd, idesc, acc0);
+            mma_tf32(tmem + dcol, ahd, bld, idesc, 1u);
+            mma_tf32(tmem + dcol, ald, bhd, idesc, 1u);
+        }
+        (void)arows_k4stride;
+    };
+    // write this thread's row values v[0..n) (columns c0..) into an A operand
+    // block [128 x Kblk] (hi, lo) as TF32 splits
+    auto put_row = [&](float* Ahi, float* Alo, int c0, const float* v, int n) {
+        for (int j = 0; j < n; ++j) {
+            const float x = v[j], h = tf32_rn(x);
+            Ahi[kmaj(tid, c0 + j, kTile)] = h;
+            Alo[kmaj(tid, c0 + j, kTile)] = x - h;
+        }
+    };
+    auto sync_for_mma = [&]() {
+        asm volatile("fence.proxy.async.shared::cta;");
+        asm volatile("tcgen05.fence::before_thread_sync;");
+        __syncthreads();
+        asm volatile("tcgen05.fence::after_thread_sync;");
+    };
+
+    // TMEM columns: [0,128) layer-1 output, [128,192) layer-2 accumulator,
+    // [192,224) layer 3, [224,240) layer 4, [240,256) layer 5
+    for (int tile = blockIdx.x; tile < a.n_tiles; tile += gridDim.x) {
+        const long long row = a.row_begin + (long long)tile * kTile + tid;
+        const bool rv = row < a.row_end;
+        // ---- layer-1 input row: [starts / start_scale, devdim / dim_scale]
+        {
+            float* Ahi = sA;
+            float* Alo = sA + kTile * a.K0p;
+            double mn = CUDART_INF;
+            if (rv && a.dir == 0)
+                for (int d = 0; d < a.D; ++d) mn = fmin(mn, a.comp[row * a.D + d]);
+            for (int k = 0; k < a.K0p; ++k) {
+                float x = 0.0f;
+                if (rv && k < 2 * a.D) {
+                    if (k < a.D)
+                        x = a.dir == 0 ? (float)((a.comp[row * a.D + k] - mn) / a.start_scale) : 0.0f;
+                    else
+                        x = (float)((double)a.devdim[row * a.D + k - a.D] / a.dim_scale);
+                }
+                const float h = tf32_rn(x);
+                Ahi[kmaj(tid, k, kTile)] = h;
+                Alo[kmaj(tid, k, kTile)] = x - h;
+            }
+        }
+        sync_for_mma();
+        if (tid == 0) {
+            issue(sA, sA + kTile * a.K0p, 0, sW + L.off[0], sW + L.off[0] + L.Kp[0] * L.Np[0], 128, 0, a.K0p / 8, 0, 0,
+                  false);
+            commit(&s_bar[0]);
+        }
+        mbar_wait(&s_bar[0], ph0);
+        ph0 ^= 1;
+        asm volatile("tcgen05.fence::after_thread_sync;");
+        // ---- layer 2 (K = 128) in four 32-column chunks through two operand buffers
+        for (int c = 0; c < 4; ++c) {
+            float* Ahi = sA + (c & 1) * abuf;
+            float* Alo = Ahi + kTile * kChunk;
+            if (c >= 2) {   // the MMAs of chunk c-2 must have consumed this buffer
+                if (c & 1) {
+                    mbar_wait(&s_bar[2], ph2);
+                    ph2 ^= 1;
+                } else {
+                    mbar_wait(&s_bar[1], ph1);
+                    ph1 ^= 1;
+                }
+            }
+            for (int h = 0; h < 2; ++h) {
+                float v[16];
+                tmem_ld16(lane_base + 32 * c + 16 * h, v);
+#pragma unroll
+                for (int j = 0; j < 16; ++j) v[j] = fmaxf(v[j] + bias1[32 * c + 16 * h + j], 0.0f);
+                put_row(Ahi, Alo, 16 * h, v, 16);
+            }
+            sync_for_mma();
+            if (tid == 0) {
+                issue(Ahi, Alo, 0, sW + L.off[1], sW + L.off[1] + L.Kp[1] * L.Np[1], 64, 0, kChunk / 8, c * (kChunk / 8),
+                      128, c > 0);
+                commit(&s_bar[1 + (c & 1)]);
+            }
+        }
+        // wait for chunks 2 and 3 (the last commits on both buffers)
+        mbar_wait(&s_bar[1], ph1);
+        ph1 ^= 1;
+        mbar_wait(&s_bar[2], ph2);
+        ph2 ^= 1;
+        asm volatile("tcgen05.fence::after_thread_sync;");
+        // ---- layers 3, 4, 5 (K = 64, 32, 16), operand in buffer 0/1 region (64 KB)
+        const int lin[3] = {128, 192, 224};     // TMEM column of the layer input
+        const int lout[3] = {192, 224, 240};    // TMEM column of the layer output
+        const int Kin[3] = {64, 32, 16};
+        const float* bin[3] = {bias2, bias3, bias4};
+        for (int l = 2; l < 5; ++l) {
+            const int i = l - 2;
+            const int K = Kin[i];
+            float* Ahi = sA;
+            float* Alo = sA + kTile * K;
+            for (int c0 = 0; c0 < K; c0 += 16) {
+                float v[16];
+                tmem_ld16(lane_base + lin[i] + c0, v);
+#pragma unroll
+                for (int j = 0; j < 16; ++j) v[j] = fmaxf(v[j] + bin[i][c0 + j], 0.0f);
+                put_row(Ahi, Alo, c0, v, 16);
+            }
+            sync_for_mma();
+            if (tid == 0) {
+                issue(Ahi, Alo, 0, sW + L.off[l], sW + L.off[l] + L.Kp[l] * L.Np[l], L.Np[l], 0, K / 8, 0, lout[i],
+                      false);
+                commit(&s_bar[0]);
+            }
+            mbar_wait(&s_bar[0], ph0);
+            ph0 ^= 1;
+            asm volatile("tcgen05.fence::after_thread_sync;");
+        }
+        // ---- output layer (no activation)
+        {
+            float v[16];
+            tmem_ld16(lane_base + 240, v);
+            if (rv)
+                for (int d = 0; d < a.D; ++d) a.out[row * a.D + d] = v[d] + bias5[d];
+        }
+        asm volatile("tcgen05.fence::before_thread_sync;");
+        __syncthreads();   // TMEM and operand buffers reused by the next tile
+        asm volatile("tcgen05.fence::after_thread_sync;");
+    }
+    __syncthreads();
+    if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 256;" ::"r"(tmem));
+}
+
+__global__ void k_plan_cost_combine(const double* comp, const float* fwd, const float* bwd, const uint8_t* ok,
+                                    long long pb, long long pe, int D, double* cost) {
+    for (long long p = pb + (long long)blockIdx.x * blockDim.x + threadIdx.x; p < pe;
+         p += (long long)gridDim.x * blockDim.x) {
+        double c = -CUDART_INF;
+        for (int d = 0; d < D; ++d)
+            c = fmax(c, (comp[p * D + d] + (double)fwd[p * D + d]) + (double)bwd[p * D + d]);
+        cost[p] = ok[p] ? c : CUDART_NAN;
+    }
+}
+
+}  // namespace
+
+// Plan costs of rows [pb, pe) with the comm MLPs on tcgen05 (3xTF32).
+// comp/devdim/ok/cost indexed by global plan index; fbuf/bbuf scratch [P][D].
+ns_status launch_plan_cost_tc(ns_ctx* ctx, long long pb, long long pe, const double* comp, const int32_t* devdim,
+                              const uint8_t* ok, float* fbuf, float* bbuf, double* cost) {
+    const int D = ctx->model.D;
+    if (D > 16) return set_err(ctx, NS_ERR_ARG, "NS_SCORE_TF32X3 supports D <= 16");
+    if (pe <= pb) return NS_OK;
+    TcArgs a;
+    a.row_begin = pb;
+    a.row_end = pe;
+    a.D = D;
+    a.K0p = ((2 * D + 7) / 8) * 8;
+    a.N5p = 16;
+    a.comp = comp;
+    a.devdim = devdim;
+    a.start_scale = ctx->model.start_scale;
+    a.dim_scale = ctx->model.dim_scale;
+    a.n_tiles = (int)((pe - pb + kTile - 1) / kTile);
+    // weight floats: 2 * sum(Kp * Np)
+    const int wfl = 2 * (a.K0p * 128 + 128 * 64 + 64 * 32 + 32 * 16 + 16 * 16);
+    const size_t smem = (size_t)(wfl + 2 * kTile * 32 * 2) * sizeof(float) + 128;
+    cudaFuncSetAttribute(k_plan_mlp_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    const int grid = std::min(a.n_tiles, ctx->sm_count);
+    for (int dir = 0; dir < 2; ++dir) {
+        a.dir = dir;
+        a.out = dir == 0 ? fbuf : bbuf;
+        for (int l = 0; l < 5; ++l) {
+            a.W[l] = ctx->model.cW[dir][l];
+            a.b[l] = ctx->model.cb[dir][l];
+        }
+        prof_begin(ctx, PK_FINALIZE);
+        k_plan_mlp_tc<<<grid, 128, smem, ctx->stream>>>(a);
+        prof_end(ctx);
+        NS_LAUNCHED(ctx);
+    }
+    const long long n = pe - pb;
+    k_plan_cost_combine<<<(unsigned)std::min<long long>((n + 255) / 256, 4096), 256, 0, ctx->stream>>>(
+        comp, fbuf, bbuf, ok, pb, pe, D, cost);
+    NS_LAUNCHED(ctx);
+    return NS_OK;
+}
+
+}  // namespace ns

@@ -537,7 +537,8 @@ ns_status ns_score_plans(ns_ctx* ctx, const ns_tables* t, int32_t task, int32_t 
     if (!ctx->model.loaded) return set_err(ctx, NS_ERR_STATE, "no cost models loaded");
     if (D != ctx->model.D) return set_err(ctx, NS_ERR_ARG, "D differs from the loaded comm models' D");
     if (task < 0 || task >= t->n_tasks) return set_err(ctx, NS_ERR_ARG, "task out of range");
-    if (mode != NS_SCORE_FP64) return set_err(ctx, NS_ERR_ARG, "bad mode");
+    if (mode != NS_SCORE_FP64 && mode != NS_SCORE_TF32X3) return set_err(ctx, NS_ERR_ARG, "bad mode");
+    if (mode == NS_SCORE_TF32X3 && D > 16) return set_err(ctx, NS_ERR_ARG, "NS_SCORE_TF32X3 needs D <= 16");
     // validate the column plan against the evolving dims
     if (n_col > 0) {
         ns_status ds = ensure_host_dims(ctx, t);

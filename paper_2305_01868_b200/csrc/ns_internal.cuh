@@ -154,6 +154,11 @@ ns_status launch_plan_cost(ns_ctx* ctx, long long rb, long long re, const uint8_
                            const int32_t* devdim, double* cost, const int32_t* list = nullptr,
                            const int32_t* list_n = nullptr);
 
+// N5 on tcgen05 (k_score_tc.cu, NS_SCORE_TF32X3): comm MLPs in split-TF32 x3
+// with FP32 accumulation in TMEM; cost[p] = max_d(comp + fwd + bwd), NaN if !ok[p].
+ns_status launch_plan_cost_tc(ns_ctx* ctx, long long pb, long long pe, const double* comp, const int32_t* devdim,
+                              const uint8_t* ok, float* fbuf, float* bbuf, double* cost);
+
 // helpers (ns_api.cu)
 ns_status set_err(ns_ctx* ctx, ns_status s, const std::string& msg);
 ns_status cuda_check(ns_ctx* ctx, cudaError_t e, const char* what);

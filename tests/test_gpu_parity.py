@@ -395,3 +395,27 @@ def test_invalid_descriptor_device_and_pinned(ns, ctx):
         with pytest.raises(ns.NSError):
             ns.ns_score_plans(ctx, tabs, 0, 4, [], gen_plans(40, 4, 8, seed=1))
         tabs.free()
+
+
+@pytest.mark.parametrize("D", [2, 4, 8, 16])
+def test_score_plans_tf32x3_tcgen05(ns, ctx, D):
+    """Bulk mode: comm MLPs on tcgen05 in split-TF32 x3 (FP32 accumulation).
+    Plan costs within 1e-5 relative of the fp64 path and of the oracle
+    (north star tolerance 1e-3); the argmin agrees unless its margin is below
+    that tolerance."""
+    rng = np.random.default_rng(70 + D)
+    task = small_task(rng, 3 * D + 10, D)
+    w = gen_weights(D, "mono", seed=80 + D)
+    tabs = _setup(ns, ctx, [task], w)
+    A = gen_plans(task.T, D, 3000, seed=D)       # > 16 tiles of 128 rows, ragged tail
+    c64, b64, v64 = ns.ns_score_plans(ctx, tabs, 0, D, [], A, mode=ns.NS_SCORE_FP64)
+    c32, b32, v32 = ns.ns_score_plans(ctx, tabs, 0, D, [], A, mode=ns.NS_SCORE_TF32X3)
+    rel = np.abs(c32 - c64) / np.abs(c64)
+    assert rel.max() < 1e-5, rel.max()
+    emb = om.TableEmbeddings(w, task)
+    tables = osr.apply_col_plan(task, [])
+    for p in range(0, 3000, 331):
+        assert _rel(c32[p], om.plan_cost(w, emb, tables, A[p].tolist(), D)[0]) < 1e-5
+    srt = np.sort(c64)
+    if (srt[1] - srt[0]) / abs(srt[0]) > 1e-5:
+        assert b32 == b64
