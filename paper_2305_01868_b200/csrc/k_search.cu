@@ -718,7 +718,10 @@ __global__ void __launch_bounds__(128, (LPD >= 8 ? 5 : (LPD == 4 ? 2 : 1))) k_gr
                     if (m < M) mpick[m] = pick;
                     const unsigned live = __ballot_sync(kFull, pick >= 0);
                     left |= __any_sync(kFull, pick == -1);
-                    if (first == M && live) first = m0 + __ffs(live) - 1;
+                    // the group keeps the pick of its LOOSEST-cap live member (highest m):
+                    // tight caps bind first, so the splitting members are the few
+                    // tight ones and the majority stays in the register-resident group
+                    if (live) first = m0 + 31 - __clz(live);
                 }
                 __syncwarp();
                 if (first == M) {   // every member stranded
