@@ -886,9 +886,15 @@ __global__ void __launch_bounds__(128, (LPD >= 8 ? 5 : (LPD == 4 ? 2 : 1))) k_gr
 template <int LPD>
 __global__ void __launch_bounds__(512) k_greedy_big(const GreedyArgs a) {
     constexpr int FPL = kV / LPD;
+    constexpr int SS = FPL * 8 + 16;   // ring slice stride (bytes)
+    constexpr int RS = LPD * SS;
+    constexpr int kLook = kStages - 2; // lookahead: the slot being overwritten was last read two steps ago
     __shared__ double s_sc[2][16];
     __shared__ int s_dv[2][16];
     __shared__ int s_cnt[2][16];
+    __shared__ __align__(16) unsigned char ring[kStages * RS];
+    __shared__ int sdt[kStages], sidx[kStages];
+    __shared__ long long sbt[kStages];
     const int lane = threadIdx.x & 31, wi = threadIdx.x >> 5, nw = blockDim.x >> 5;
     const long long tau = a.traj_begin + blockIdx.x;
     if (tau >= a.traj_end) return;
@@ -912,16 +918,37 @@ __global__ void __launch_bounds__(512) k_greedy_big(const GreedyArgs a) {
     const int32_t* orow = a.ord_row + (size_t)g * a.Tpm;
     const int32_t* oidx = a.ord_idx + (size_t)g * a.Tpm;
     int8_t* asg = a.assign + (size_t)tau * a.Tpm;
+    const int T = alive ? Tp : 0;
+    // warp 0 streams the cost-ordered v rows through a cp.async ring
+    auto issue = [&](int pp) {
+        if (pp < T) {
+            const int r = __ldg(orow + pp);
+            unsigned char* st = ring + (pp % kStages) * RS;
+            constexpr int CPS = FPL / 2;
+            cp_async16(st + (lane / CPS) * SS + (lane % CPS) * 16, a.V + (size_t)r * kV + 2 * lane);
+            if (lane == 0) cp_async4(sdt + pp % kStages, a.vdim + r);
+            if (lane == 1) cp_async4(sidx + pp % kStages, oidx + pp);
+            if (lane == 2) cp_async8(sbt + pp % kStages, a.vbytes + r);
+        }
+        cp_async_commit();
+    };
+    if (wi == 0)
+        for (int pp = 0; pp < kLook; ++pp) issue(pp);
 #pragma unroll 1
-    for (int p = 0; p < (alive ? Tp : 0); ++p) {
+    for (int p = 0; p < T; ++p) {
         const int par = p & 1;
-        const int row = __ldg(orow + p);
-        const int dt = __ldg(a.vdim + row);
-        const long long bt = __ldg(a.vbytes + row);
+        if (wi == 0) {
+            issue(p + kLook);
+            cp_async_wait<kLook>();   // table p landed
+        }
+        __syncthreads();              // ... visible to every warp
+        const int sl = p % kStages;
+        const int dt = sdt[sl];
+        const long long bt = sbt[sl];
         const bool f = dev && (bsum + bt <= cap) && (dsum + dt <= capd);
-        const double2* v2 = reinterpret_cast<const double2*>(a.V + (size_t)row * kV + part * FPL);
+        const double2* v2 = reinterpret_cast<const double2*>(ring + sl * RS + part * SS);
         double ps = 0.0;
-        if (f) ps = part_score<FPL, false>(u, w, v2);
+        if (f) ps = part_score<FPL, true>(u, w, v2);
         double bs = a.head.hb2 + lane_group_sum<LPD>(ps);
         if (!f) bs = CUDART_INF;
         int bd = d;
@@ -952,12 +979,13 @@ __global__ void __launch_bounds__(512) k_greedy_big(const GreedyArgs a) {
             break;   // uniform across the CTA
         }
         if (d == bd) {
-            part_add<FPL, false>(u, v2);
+            part_add<FPL, true>(u, v2);
             dsum += dt;
             bsum += bt;
         }
-        if (threadIdx.x == 0) asg[__ldg(oidx + p)] = (int8_t)bd;
+        if (threadIdx.x == 0) asg[sidx[sl]] = (int8_t)bd;
     }
+    if (wi == 0) cp_async_wait<0>();
     const double hc = a.head.hb2 + lane_group_sum<LPD>(part_head<FPL>(u, w));
     if (dev && part == 0) {
         a.comp[tau * a.D + d] = dsum > 0 ? hc : 0.0;
