@@ -82,6 +82,27 @@ void* pinned_get(ns_ctx* ctx, size_t bytes) {
     return ctx->pinned;
 }
 
+void* pinned_in_get(ns_ctx* ctx, size_t bytes) {
+    if (ctx->pinned_in_done) cudaEventSynchronize(ctx->pinned_in_done);   // previous copy out of the buffer
+    if (bytes <= ctx->pinned_in_bytes) return ctx->pinned_in;
+    if (ctx->pinned_in) cudaFreeHost(ctx->pinned_in);
+    ctx->pinned_in = nullptr;
+    ctx->pinned_in_bytes = 0;
+    const size_t want = bytes + bytes / 4 + 4096;
+    if (cudaMallocHost(&ctx->pinned_in, want) != cudaSuccess) {
+        cudaGetLastError();
+        ctx->pinned_in = nullptr;
+        return nullptr;
+    }
+    ctx->pinned_in_bytes = want;
+    return ctx->pinned_in;
+}
+
+void pinned_in_release(ns_ctx* ctx) {
+    if (!ctx->pinned_in_done) cudaEventCreateWithFlags(&ctx->pinned_in_done, cudaEventDisableTiming);
+    cudaEventRecord(ctx->pinned_in_done, ctx->stream);
+}
+
 CommParams comm_params(const ns_ctx* ctx) {
     CommParams c{};
     c.D = ctx->model.D;
@@ -204,6 +225,8 @@ ns_status ns_destroy(ns_ctx* ctx) {
     free_model(ctx->model);
     if (ctx->arena) cudaFree(ctx->arena);
     if (ctx->pinned) cudaFreeHost(ctx->pinned);
+    if (ctx->pinned_in) cudaFreeHost(ctx->pinned_in);
+    if (ctx->pinned_in_done) cudaEventDestroy(ctx->pinned_in_done);
     prof_collect(ctx);
     for (cudaEvent_t e : ctx->prof_free) cudaEventDestroy(e);
     comm_destroy(ctx);
@@ -400,12 +423,11 @@ ns_status ns_featurize_tables(ns_ctx* ctx, const ns_table_desc* tables, const in
     // small host arrays go through pinned staging so the copies stay async
     const size_t meta = (n_tasks + 1) * sizeof(int32_t) + n_tasks * sizeof(int64_t);
     const size_t hbytes = meta + (direct ? 0 : (size_t)n * sizeof(ns_table_desc));
-    char* pin = (char*)pinned_get(ctx, hbytes + 64);
+    char* pin = (char*)pinned_in_get(ctx, hbytes + 64);
     if (!pin) {
         ns_tables_free(t);
         return set_err(ctx, NS_ERR_NOMEM, "pinned staging");
     }
-    if ((e = cudaStreamSynchronize(st)) != cudaSuccess) return fail(e);   // pinned buffer reuse
     std::memcpy(pin, task_offsets, (n_tasks + 1) * sizeof(int32_t));
     std::memcpy(pin + (n_tasks + 1) * sizeof(int32_t), mem_cap, n_tasks * sizeof(int64_t));
     if (!direct) std::memcpy(pin + meta, tables, (size_t)n * sizeof(ns_table_desc));
@@ -419,6 +441,7 @@ ns_status ns_featurize_tables(ns_ctx* ctx, const ns_table_desc* tables, const in
                              n * sizeof(ns_table_desc), dev_in ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice,
                              st)) != cudaSuccess)
         return fail(e);
+    pinned_in_release(ctx);   // the staging buffer may be reused once these copies ran
     // (vdim of every row is written by the precompute of its depth before any read)
     if ((e = cudaMemsetAsync(t->d_flag, 0, sizeof(int32_t), st)) != cudaSuccess) return fail(e);
     launch_tables_validate(ctx, t);

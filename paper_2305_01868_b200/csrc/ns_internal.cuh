@@ -82,9 +82,13 @@ struct ns_ctx {
     // grow-only device arena for per-call scratch
     void* arena = nullptr;
     size_t arena_bytes = 0;
-    // pinned host staging
+    // pinned host staging (results), and a second buffer for featurise inputs
+    // guarded by an event so a new featurise call never waits for the stream
     void* pinned = nullptr;
     size_t pinned_bytes = 0;
+    void* pinned_in = nullptr;
+    size_t pinned_in_bytes = 0;
+    cudaEvent_t pinned_in_done = nullptr;
     // kernel timers
     bool prof = false;
     ns::ProfEntry prof_acc[ns::PK_COUNT];
@@ -165,6 +169,8 @@ ns_status cuda_check(ns_ctx* ctx, cudaError_t e, const char* what);
 bool is_device_ptr(const void* p);
 void* arena_get(ns_ctx* ctx, size_t bytes);   // nullptr on failure
 void* pinned_get(ns_ctx* ctx, size_t bytes);
+void* pinned_in_get(ns_ctx* ctx, size_t bytes);      // waits only for the previous input copy
+void pinned_in_release(ns_ctx* ctx);                  // record: copies out of it are enqueued
 CommParams comm_params(const ns_ctx* ctx);
 ns_status comm_allgather(ns_ctx* ctx, const void* send, void* recv, size_t bytes_per_rank);
 ns_status comm_allreduce_min_u64(ns_ctx* ctx, uint64_t* dev_buf, size_t count);
