@@ -43,7 +43,8 @@ def _nccl_include() -> str:
 
 def flags():
     return ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler", "-ffp-contract=off",
-                   "-Xptxas", "-v", "--expt-relaxed-constexpr", "-I", CSRC,] + (["-DNS_DEBUG"] if os.environ.get("NS_DEBUG") else []) + [
+                   "-Xptxas", "-v", "--expt-relaxed-constexpr", "-I", CSRC,] + (["-DNS_DEBUG"] if os.environ.get("NS_DEBUG") else []) + \
+        os.environ.get("NS_NVCC_EXTRA", "").split() + [
                    "-I", os.path.join(os.path.dirname(PKG), "include"), "-I", _nccl_include()]
 
 

@@ -47,6 +47,7 @@ struct SearchBufs {
     int32_t* n_uniq;     // [1]
     unsigned int* next_cp;   // [1] grouped-greedy work queue
     double* gscratch;    // grouped greedy group states
+    int8_t* ghist;       // grouped greedy group histories [gscratch_warps][M][Tpm]
     int gscratch_warps;
     // per task
     int32_t* capdim;     // [n_tasks][M]
@@ -480,51 +481,70 @@ constexpr int kStages = 8;   // row-stream ring depth of the grouped greedy
 //
 // Lane layout: lane = (device d, part) with LPD = 32 / pow2(D) lanes per
 // device and FPL = 64 / LPD features per lane.  Group 0 (which holds the
-// loosest caps and lives the longest) keeps its state in registers; later
+// loosest caps and lives the longest) keeps its whole state in registers
+// (pre-activations, per-device dim/bytes, cap range, uniform work); later
 // groups live in a per-warp global scratch (L1/L2).  Member and group
-// bookkeeping lives in shared memory.
+// bookkeeping lives in shared memory with compile-time extents (MC >= M).
+// Device choices are recorded once per GROUP and step (a per-group history
+// by list index, plus the parent and step of each split); at the end the
+// histories are completed in creation order and only each group's
+// representative (its lowest live member) gets an assignment row, comp /
+// devdim row and dup_of = -1 -- the other members point at it through dup_of
+// (plan cost and selection read representatives only).
 // ---------------------------------------------------------------------------
 struct DedupArgs {
     long long tau_base;    // absolute trajectory index of the first column plan (dup_of holds absolute taus)
     int n_cp;              // column plans of this launch: [0, n_cp) relative to the GreedyArgs pointers
-    int mmax;              // M
+    int mmax;              // M (<= the kernel's MC)
     double* scratch;       // [total_warps][M][D][64] group states (groups >= 1)
+    int8_t* hist;          // [total_warps][M][Tpm] per-group device choices by list index
     int total_warps;
     int32_t* dup_of;       // [n_traj] tau of the member whose plan this one duplicates, or -1
     unsigned int* next_cp; // dynamic queue counter (zeroed before the launch)
 };
 
-template <int LPD>
-__global__ void __launch_bounds__(128, (LPD >= 8 ? 5 : (LPD == 4 ? 2 : 1))) k_greedy_dedup(const GreedyArgs a, const DedupArgs x) {
-    constexpr int FPL = kV / LPD;
-    constexpr int DPW = 32 / LPD;   // device slots per warp
-    extern __shared__ unsigned char dsm[];
+// Per-warp shared-memory bookkeeping of the grouped greedy.  Every array has
+// a compile-time extent (MC >= M grid points), so each field is a constant
+// offset from one base register.
+template <int LPD, int MC>
+struct __align__(16) DedupSmem {
+    static constexpr int FPL = kV / LPD;
+    static constexpr int DPW = 32 / LPD;      // device slots per warp
+    static constexpr int SS = FPL * 8 + 16;   // ring slice stride (bytes): +16 B keeps the LPD
+    static constexpr int RS = LPD * SS;       //   slices of a row on distinct banks
+    unsigned char ring[kStages][RS];          // staged v rows of the next tables
+    long long gb[MC][DPW];                    // group bytes per device (groups >= 1)
+    long long sbt[kStages];                   // bytes of the staged table
+    double sc[DPW];                           // scores of the current group
+    int gd[MC][DPW];                          // group dims per device (groups >= 1)
+    int mgroup[MC];                           // member -> group (-1 stranded)
+    int mcap[MC];                             // member dim cap
+    int mpick[MC];
+    int gcap[MC];                             // loosest cap among a group's live members
+    int gmin[MC];                             // tightest cap among a group's live members
+    int gpar[MC];                             // group it split from
+    int gstep[MC];                            // step (cost-order position) of the split
+    uint32_t mwork[MC];
+    uint32_t gwork[MC];                       // work of the group's uniform steps
+    int sdv[DPW];                             // dim after insertion
+    int sok[DPW];                             // device scored
+    int sdt[kStages];                         // dim of the staged table
+    int sidx[kStages];                        // its list index
+};
+
+template <int LPD, int MC>
+#ifndef NS_DEDUP_BLOCKS8
+#define NS_DEDUP_BLOCKS8 4   // CTAs per SM for LPD >= 8 (D <= 4): 126 registers, no spills
+#endif
+__global__ void __launch_bounds__(128, (LPD >= 8 ? NS_DEDUP_BLOCKS8 : (LPD == 4 ? 2 : 1))) k_greedy_dedup(const GreedyArgs a, const DedupArgs x) {
+    using SM = DedupSmem<LPD, MC>;
+    constexpr int FPL = SM::FPL, DPW = SM::DPW, SS = SM::SS;
+    extern __shared__ __align__(16) unsigned char dsm[];
     const int lane = threadIdx.x & 31, wl = threadIdx.x >> 5, nw = blockDim.x >> 5;
     const int M = x.mmax, D = a.D;
     const int d = lane / LPD, part = lane % LPD;
     const bool dev = d < D;
-    // per-warp shared bookkeeping
-    const size_t per_warp = (size_t)M * (4 + 4 + 4 + 4 + DPW * 4 + DPW * 8 + 4 + 8) + DPW * (8 + 4 + 4) + 64 +
-                            kStages * (LPD * (FPL * 8 + 16) + 16) + 16;
-    unsigned char* base = dsm + (size_t)wl * ((per_warp + 15) & ~size_t(15));
-    long long* gb = (long long*)base;                 // [M][DPW] group bytes per device
-    double* sc = (double*)(gb + (size_t)M * DPW);     // [DPW] scores of the current group
-    int* gd = (int*)(sc + DPW);                       // [M][DPW] group dims per device
-    int* mgroup = gd + (size_t)M * DPW;               // [M] member -> group (-1 dead)
-    int* mcap = mgroup + M;                           // [M] member dim cap
-    uint32_t* mwork = (uint32_t*)(mcap + M);          // [M]
-    int* mpick = (int*)(mwork + M);                   // [M]
-    int* gcap = mpick + M;                            // [M] loosest cap among a group's members
-    int* sdv = gcap + M;                              // [DPW] dim after insertion
-    int* sok = sdv + DPW;                             // [DPW] device scored
-    int* gmin = sok + DPW;                            // [M] tightest cap among a group's live members
-    uint32_t* gwork = (uint32_t*)(gmin + M);          // [M] work of the group's uniform steps
-    constexpr int SS = FPL * 8 + 16;                  // ring slice stride (bytes): +16 B keeps the LPD
-    constexpr int RS = LPD * SS;                      //   slices of a row on distinct banks
-    unsigned char* ring = (unsigned char*)(((uintptr_t)(gwork + M) + 15) & ~uintptr_t(15));   // [kStages][RS]
-    int* sdt = (int*)(ring + kStages * RS);           // [kStages] dim of the staged table
-    int* sidx = sdt + kStages;                        // [kStages] its list index
-    long long* sbt = (long long*)(sidx + kStages);    // [kStages] its bytes
+    SM& s = reinterpret_cast<SM*>(dsm)[wl];
     // hb1 (the empty-device pre-activation) is re-read from shared memory at
     // every column plan instead of occupying FPL registers for the whole kernel
     __shared__ double s_hb1[kV];
@@ -534,6 +554,7 @@ __global__ void __launch_bounds__(128, (LPD >= 8 ? 5 : (LPD == 4 ? 2 : 1))) k_gr
     load_lane_head<FPL>(a.head, part, u0, w);
     const long long gw = (long long)blockIdx.x * nw + wl;
     double* scr = x.scratch + (size_t)gw * M * D * kV;   // this warp's group states
+    int8_t* hist = x.hist + (size_t)gw * M * a.Tpm;       // this warp's group histories
     // dynamic column-plan queue (column plans differ in length and in how many
     // groups they split into; a static stride leaves a long tail)
     long long g = gw;
@@ -541,10 +562,14 @@ __global__ void __launch_bounds__(128, (LPD >= 8 ? 5 : (LPD == 4 ? 2 : 1))) k_gr
         const bool valid = a.cp_valid[g] != 0;
         const long long tau0 = g * M;
         if (!valid) {
-            for (int m = lane; m < M; m += 32) {
-                a.feas[tau0 + m] = 0;
-                a.work[tau0 + m] = 0;
-                x.dup_of[tau0 + m] = -1;
+#pragma unroll
+            for (int m0 = 0; m0 < MC; m0 += 32) {
+                const int m = m0 + lane;
+                if (m < M) {
+                    a.feas[tau0 + m] = 0;
+                    a.work[tau0 + m] = 0;
+                    x.dup_of[tau0 + m] = -1;
+                }
             }
             long long nx = 0;
             if (lane == 0) nx = x.total_warps + (long long)atomicAdd(x.next_cp, 1u);
@@ -554,38 +579,36 @@ __global__ void __launch_bounds__(128, (LPD >= 8 ? 5 : (LPD == 4 ? 2 : 1))) k_gr
         const int q = a.cp_task[g];
         const int Tp = a.cp_Tp[g];
         const long long cap = a.cap[q];
+        // group 0 (all members at the start; keeps the loosest-cap members)
+        // lives in registers: per-device dim / bytes in the device's lanes,
+        // cap range and uniform work warp-uniform
         int cmax = 0, cmin = INT_MAX;
-        for (int m = lane; m < M; m += 32) {
-            mgroup[m] = 0;
-            mcap[m] = a.capdim[q * M + m];
-            mwork[m] = 0;
-            cmax = max(cmax, mcap[m]);
-            cmin = min(cmin, mcap[m]);
+#pragma unroll
+        for (int m0 = 0; m0 < MC; m0 += 32) {
+            const int m = m0 + lane;
+            if (m < M) {
+                const int c = a.capdim[q * M + m];
+                s.mgroup[m] = 0;
+                s.mcap[m] = c;
+                s.mwork[m] = 0;
+                cmax = max(cmax, c);
+                cmin = min(cmin, c);
+            }
         }
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) {
             cmax = max(cmax, __shfl_xor_sync(kFull, cmax, o));
             cmin = min(cmin, __shfl_xor_sync(kFull, cmin, o));
         }
-        if (lane == 0) {
-            gmin[0] = cmin;
-            gwork[0] = 0;
-        }
-        for (int i = lane; i < DPW; i += 32) {
-            gd[i] = 0;
-            gb[i] = 0;
-        }
-        if (lane == 0) gcap[0] = cmax;
+        int r_dsum = 0, r_gcap = cmax, r_gmin = cmin;
+        long long r_bsum = 0;
+        uint32_t r_gwork = 0;
 #pragma unroll
         for (int k = 0; k < FPL; ++k) u0[k] = s_hb1[part * FPL + k];
         int ng = 1;
         __syncwarp();
         const int32_t* orow = a.ord_row + (size_t)g * a.Tpm;
         const int32_t* oidx = a.ord_idx + (size_t)g * a.Tpm;
-        // software pipeline over the cost-ordered table stream: the next
-        // table's (v slice, dim, bytes, list index) is fetched while the
-        // current one is processed (two register buffers, loop unrolled by 2)
-        int8_t* asg_lane = a.assign + (size_t)(tau0 + lane) * a.Tpm;   // member m = lane (+32k)
         // row-index window: the next 32 entries of the cost order in one register per lane
         int oc_cur = lane < Tp ? __ldg(orow + lane) : 0;
         int oc_nxt = 32 + lane < Tp ? __ldg(orow + 32 + lane) : 0;
@@ -596,24 +619,24 @@ __global__ void __launch_bounds__(128, (LPD >= 8 ? 5 : (LPD == 4 ? 2 : 1))) k_gr
                     oc_nxt = pp + 32 + lane < Tp ? __ldg(orow + pp + 32 + lane) : 0;
                 }
                 const int r = __shfl_sync(kFull, oc_cur, pp & 31);
-                unsigned char* st = ring + (pp % kStages) * RS;
+                const int sl = pp % kStages;
                 constexpr int CPS = FPL / 2;   // 16-byte chunks per slice
-                cp_async16(st + (lane / CPS) * SS + (lane % CPS) * 16, a.V + (size_t)r * kV + 2 * lane);
-                if (lane == 0) cp_async4(sdt + pp % kStages, a.vdim + r);
-                if (lane == 1) cp_async4(sidx + pp % kStages, oidx + pp);
-                if (lane == 2) cp_async8(sbt + pp % kStages, a.vbytes + r);
+                cp_async16(&s.ring[sl][(lane / CPS) * SS + (lane % CPS) * 16], a.V + (size_t)r * kV + 2 * lane);
+                if (lane == 0) cp_async4(&s.sdt[sl], a.vdim + r);
+                if (lane == 1) cp_async4(&s.sidx[sl], oidx + pp);
+                if (lane == 2) cp_async8(&s.sbt[sl], a.vbytes + r);
             }
             cp_async_commit();   // one group per step, empty past the end
         };
-        auto process = [&](const double (&vcd)[FPL], const int dt, const long long bt, const int idx) {
+        auto process = [&](const double (&vcd)[FPL], const int dt, const long long bt, const int idx, const int p) {
             const int ng0 = ng;
 #pragma unroll 1
             for (int gr = 0; gr < ng0; ++gr) {
                 // ---- score the D devices once for the whole group (R5: after insertion)
-                const int gcap_gr = gcap[gr];
+                const int gcap_gr = gr == 0 ? r_gcap : s.gcap[gr];
                 if (gcap_gr < 0) continue;   // group without live members
-                const int dsum = dev ? gd[gr * DPW + d] : 0;
-                const long long bsum = dev ? gb[gr * DPW + d] : 0;
+                const int dsum = gr == 0 ? r_dsum : (dev ? s.gd[gr][d] : 0);
+                const long long bsum = gr == 0 ? r_bsum : (dev ? s.gb[gr][d] : 0);
                 const bool f = dev && (bsum + bt <= cap) && (dsum + dt <= gcap_gr);
                 double* ug = scr + ((size_t)gr * D + (dev ? d : 0)) * kV + part * FPL;   // valid for gr >= 1
                 double ps = 0.0;
@@ -628,7 +651,8 @@ __global__ void __launch_bounds__(128, (LPD >= 8 ? 5 : (LPD == 4 ? 2 : 1))) k_gr
                     }
                     ps = (acc[0] + acc[1]) + (acc[2] + acc[3]);
                 }
-                const double s = a.head.hb2 + lane_group_sum<LPD>(ps);
+                const double sco = a.head.hb2 + lane_group_sum<LPD>(ps);
+                const int gmin_gr = gr == 0 ? r_gmin : s.gmin[gr];
                 // ---- fast path: every live member's cap admits every scored
                 //      device -> all members see the same feasible set and take
                 //      the group argmin (no split, uniform work)
@@ -636,20 +660,29 @@ __global__ void __launch_bounds__(128, (LPD >= 8 ? 5 : (LPD == 4 ? 2 : 1))) k_gr
                     int smax = f ? dsum + dt : 0;
 #pragma unroll
                     for (int o = 16; o >= LPD; o >>= 1) smax = max(smax, __shfl_xor_sync(kFull, smax, o));
-                    if (smax <= gmin[gr]) {
-                        double bs = f ? s : CUDART_INF;
-                        int bd = d;
+                    if (smax <= gmin_gr) {
+                        // device argmin: butterfly minimum, then the lowest device
+                        // attaining it (R13) from one ballot
+                        const double own = f ? sco : CUDART_INF;
+                        double bs = own;
 #pragma unroll
-                        for (int o = 16; o >= LPD; o >>= 1) argmin_step(bs, bd, o);
+                        for (int o = 16; o >= LPD; o >>= 1) bs = fmin(bs, __shfl_xor_sync(kFull, bs, o));
                         const unsigned nf = __popc(__ballot_sync(kFull, f && part == 0));
+                        const unsigned hit = __ballot_sync(kFull, f && part == 0 && own == bs);
+                        const int bd = (__ffs(hit) - 1) / LPD;
                         if (bs == CUDART_INF) {   // nothing feasible: the whole group strands (R9)
-                            for (int m = lane; m < M; m += 32)
-                                if (mgroup[m] == gr) {
-                                    mwork[m] += gwork[gr];
-                                    mgroup[m] = -1;
+                            const uint32_t gwk = gr == 0 ? r_gwork : s.gwork[gr];
+#pragma unroll
+                            for (int m0 = 0; m0 < MC; m0 += 32) {
+                                const int m = m0 + lane;
+                                if (m < M && s.mgroup[m] == gr) {
+                                    s.mwork[m] += gwk;
+                                    s.mgroup[m] = -1;
                                 }
+                            }
+                            if (gr == 0) r_gcap = -1;
                             __syncwarp();
-                            if (lane == 0) gcap[gr] = -1;
+                            if (gr != 0 && lane == 0) s.gcap[gr] = -1;
                             __syncwarp();
                             continue;
                         }
@@ -662,60 +695,64 @@ __global__ void __launch_bounds__(128, (LPD >= 8 ? 5 : (LPD == 4 ? 2 : 1))) k_gr
                                 for (int k = 0; k < FPL; ++k) ug[k] += vcd[k];
                             }
                         }
-                        {
-                            int8_t* ap = asg_lane;
-                            for (int m = lane; m < M; m += 32, ap += 32 * (size_t)a.Tpm)
-                                if (mgroup[m] == gr) ap[idx] = (int8_t)bd;
+                        if (lane == 0) hist[(size_t)gr * a.Tpm + idx] = (int8_t)bd;
+                        if (gr == 0) {
+                            if (d == bd) {
+                                r_dsum += dt;
+                                r_bsum += bt;
+                            }
+                            r_gwork += nf;
+                        } else {
+                            if (lane == 0) {
+                                s.gd[gr][bd] += dt;
+                                s.gb[gr][bd] += bt;
+                                s.gwork[gr] += nf;
+                            }
+                            __syncwarp();
                         }
-                        __syncwarp();
-                        if (lane == 0) {
-                            gd[gr * DPW + bd] += dt;
-                            gb[gr * DPW + bd] += bt;
-                            gwork[gr] += nf;
-                        }
-                        __syncwarp();
                         continue;
                     }
                 }
                 if (part == 0 && d < DPW) {
-                    sc[d] = s;
-                    sdv[d] = dsum + dt;
-                    sok[d] = f ? 1 : 0;
+                    s.sc[d] = sco;
+                    s.sdv[d] = dsum + dt;
+                    s.sok[d] = f ? 1 : 0;
                 }
                 __syncwarp();
                 // ---- every member takes its own argmin over its own feasible set
                 //      (dim cap of its grid point; lowest device on ties, R13)
+                const uint32_t gwk = gr == 0 ? r_gwork : s.gwork[gr];
                 int first = M;
-                bool split = false, left = false;
-                for (int m0 = 0; m0 < M; m0 += 32) {
+                bool left = false;
+#pragma unroll
+                for (int m0 = 0; m0 < MC; m0 += 32) {
                     const int m = m0 + lane;
                     int pick = -2;
-                    if (m < M && mgroup[m] == gr) {
+                    if (m < M && s.mgroup[m] == gr) {
                         double best = CUDART_INF;
                         int bd = -1;
                         uint32_t cnt = 0;
-                        const int cm = mcap[m];
+                        const int cm = s.mcap[m];
                         for (int dd = 0; dd < D; ++dd) {
-                            if (sok[dd] && sdv[dd] <= cm) {
+                            if (s.sok[dd] && s.sdv[dd] <= cm) {
                                 ++cnt;
-                                const double sv = sc[dd];
+                                const double sv = s.sc[dd];
                                 if (sv < best) {
                                     best = sv;
                                     bd = dd;
                                 }
                             }
                         }
-                        mwork[m] += cnt;
+                        s.mwork[m] += cnt;
                         if (bd < 0) {
-                            mwork[m] += gwork[gr];
-                            mgroup[m] = -1;   // R9: stranded -> grid point infeasible
+                            s.mwork[m] += gwk;
+                            s.mgroup[m] = -1;   // R9: stranded -> grid point infeasible
                             pick = -1;
                         } else {
                             pick = bd;
-                            asg_lane[(size_t)m0 * a.Tpm + idx] = (int8_t)bd;
                         }
                     }
-                    if (m < M) mpick[m] = pick;
+                    if (m < M) s.mpick[m] = pick;
                     const unsigned live = __ballot_sync(kFull, pick >= 0);
                     left |= __any_sync(kFull, pick == -1);
                     // the group keeps the pick of its LOOSEST-cap live member (highest m):
@@ -725,28 +762,32 @@ __global__ void __launch_bounds__(128, (LPD >= 8 ? 5 : (LPD == 4 ? 2 : 1))) k_gr
                 }
                 __syncwarp();
                 if (first == M) {   // every member stranded
-                    if (lane == 0) gcap[gr] = -1;
+                    if (gr == 0) r_gcap = -1;
+                    else if (lane == 0) s.gcap[gr] = -1;
                     __syncwarp();
                     continue;
                 }
-                const int main_pick = mpick[first];
-                for (int m0 = 0; m0 < M; m0 += 32) {
+                const int main_pick = s.mpick[first];
+                bool split = false;
+#pragma unroll
+                for (int m0 = 0; m0 < MC; m0 += 32) {
                     const int m = m0 + lane;
-                    split |= __any_sync(kFull, m < M && mpick[m] >= 0 && mpick[m] != main_pick);
+                    split |= __any_sync(kFull, m < M && s.mpick[m] >= 0 && s.mpick[m] != main_pick);
                 }
                 // ---- members choosing another device split off (state before the update)
                 if (split) {
                     for (int dd = 0; dd < D; ++dd) {
                         if (dd == main_pick) continue;
                         int any = 0, c2 = -1, c2min = INT_MAX;
-                        for (int m0 = 0; m0 < M; m0 += 32) {
+#pragma unroll
+                        for (int m0 = 0; m0 < MC; m0 += 32) {
                             const int m = m0 + lane;
-                            const bool mine = m < M && mpick[m] == dd;
+                            const bool mine = m < M && s.mpick[m] == dd;
                             if (mine) {
-                                mgroup[m] = ng;
-                                mwork[m] += gwork[gr];   // bank the old group's uniform work
-                                c2 = max(c2, mcap[m]);
-                                c2min = min(c2min, mcap[m]);
+                                s.mgroup[m] = ng;
+                                s.mwork[m] += gwk;   // bank the old group's uniform work
+                                c2 = max(c2, s.mcap[m]);
+                                c2min = min(c2min, s.mcap[m]);
                             }
                             any |= __any_sync(kFull, mine);
                         }
@@ -759,22 +800,24 @@ __global__ void __launch_bounds__(128, (LPD >= 8 ? 5 : (LPD == 4 ? 2 : 1))) k_gr
                         // new group ng = state(gr) + v_t on device dd
                         if (dev) {
                             double* un = scr + ((size_t)ng * D + d) * kV + part * FPL;
-                            const double* us = scr + ((size_t)gr * D + d) * kV + part * FPL;
 #pragma unroll
                             for (int k = 0; k < FPL; ++k) {
-                                double val = gr == 0 ? u0[k] : us[k];
+                                double val = gr == 0 ? u0[k] : ug[k];
                                 if (d == dd) val += vcd[k];
                                 un[k] = val;
                             }
-                        }
-                        for (int i3 = lane; i3 < DPW; i3 += 32) {
-                            gd[ng * DPW + i3] = gd[gr * DPW + i3] + (i3 == dd ? dt : 0);
-                            gb[ng * DPW + i3] = gb[gr * DPW + i3] + (i3 == dd ? bt : 0);
+                            if (part == 0) {
+                                s.gd[ng][d] = dsum + (d == dd ? dt : 0);
+                                s.gb[ng][d] = bsum + (d == dd ? bt : 0);
+                            }
                         }
                         if (lane == 0) {
-                            gcap[ng] = c2;
-                            gmin[ng] = c2min;
-                            gwork[ng] = 0;
+                            s.gcap[ng] = c2;
+                            s.gmin[ng] = c2min;
+                            s.gwork[ng] = 0;
+                            s.gpar[ng] = gr;
+                            s.gstep[ng] = p;
+                            hist[(size_t)ng * a.Tpm + idx] = (int8_t)dd;
                         }
                         ++ng;
                         __syncwarp();
@@ -790,29 +833,43 @@ __global__ void __launch_bounds__(128, (LPD >= 8 ? 5 : (LPD == 4 ? 2 : 1))) k_gr
                         for (int k = 0; k < FPL; ++k) ug[k] += vcd[k];
                     }
                 }
-                int c3 = gcap_gr, c3min = gmin[gr];
+                int c3 = gcap_gr, c3min = gmin_gr;
                 if (split || left) {   // members left: tighten the group's cap range
                     c3 = -1;
                     c3min = INT_MAX;
-                    for (int m = lane; m < M; m += 32)
-                        if (mgroup[m] == gr) {
-                            c3 = max(c3, mcap[m]);
-                            c3min = min(c3min, mcap[m]);
+#pragma unroll
+                    for (int m0 = 0; m0 < MC; m0 += 32) {
+                        const int m = m0 + lane;
+                        if (m < M && s.mgroup[m] == gr) {
+                            c3 = max(c3, s.mcap[m]);
+                            c3min = min(c3min, s.mcap[m]);
                         }
+                    }
 #pragma unroll
                     for (int o = 16; o > 0; o >>= 1) {
                         c3 = max(c3, __shfl_xor_sync(kFull, c3, o));
                         c3min = min(c3min, __shfl_xor_sync(kFull, c3min, o));
                     }
                 }
-                __syncwarp();
-                if (lane == 0) {
-                    gd[gr * DPW + main_pick] += dt;
-                    gb[gr * DPW + main_pick] += bt;
-                    gcap[gr] = c3;
-                    gmin[gr] = c3min;
+                if (lane == 0) hist[(size_t)gr * a.Tpm + idx] = (int8_t)main_pick;
+                if (gr == 0) {
+                    if (d == main_pick) {
+                        r_dsum += dt;
+                        r_bsum += bt;
+                    }
+                    r_gcap = c3;
+                    r_gmin = c3min;
+                    __syncwarp();
+                } else {
+                    __syncwarp();
+                    if (lane == 0) {
+                        s.gd[gr][main_pick] += dt;
+                        s.gb[gr][main_pick] += bt;
+                        s.gcap[gr] = c3;
+                        s.gmin[gr] = c3min;
+                    }
+                    __syncwarp();
                 }
-                __syncwarp();
             }
         };
 #pragma unroll 1
@@ -825,16 +882,30 @@ __global__ void __launch_bounds__(128, (LPD >= 8 ? 5 : (LPD == 4 ? 2 : 1))) k_gr
             __syncwarp();                  // ... and every lane's
             const int sl = p % kStages;
             double vcd[FPL];
-            const double2* src = reinterpret_cast<const double2*>(ring + sl * RS + part * SS);
+            const double2* src = reinterpret_cast<const double2*>(&s.ring[sl][part * SS]);
 #pragma unroll
             for (int i2 = 0; i2 < FPL / 2; ++i2) {
                 const double2 xv = src[i2];
                 vcd[2 * i2] = xv.x;
                 vcd[2 * i2 + 1] = xv.y;
             }
-            process(vcd, sdt[sl], sbt[sl], sidx[sl]);
+            process(vcd, s.sdt[sl], s.sbt[sl], s.sidx[sl], p);
         }
         cp_async_wait<0>();
+        // ---- group 0's register state to shared memory for the epilogue
+        if (part == 0 && dev) s.gd[0][d] = r_dsum;
+        if (lane == 0) s.gwork[0] = r_gwork;
+        __syncwarp();
+        // ---- complete the group histories in creation order: a group shares
+        //      its parent's choices before the step it split off
+        for (int gg = 1; gg < ng; ++gg) {
+            const int par = s.gpar[gg], st = s.gstep[gg];
+            for (int p2 = lane; p2 < st; p2 += 32) {
+                const int i = __ldg(oidx + p2);
+                hist[(size_t)gg * a.Tpm + i] = hist[(size_t)par * a.Tpm + i];
+            }
+            __syncwarp();
+        }
         // ---- outputs: per member feasibility, work, and its group's device costs
         for (int gr = 0; gr < ng; ++gr) {
             double hp;
@@ -848,29 +919,42 @@ __global__ void __launch_bounds__(128, (LPD >= 8 ? 5 : (LPD == 4 ? 2 : 1))) k_gr
                 hp = part_head<FPL>(tu, w);
             }
             const double hc = a.head.hb2 + lane_group_sum<LPD>(hp);
-            if (part == 0 && dev) sc[d] = hc;
+            if (part == 0 && dev) s.sc[d] = hc;
             __syncwarp();
             // members of this group: the first one carries the plan, others duplicate it
             int rep = -1;
-            for (int m0 = 0; m0 < M; m0 += 32) {
-                const unsigned mem = __ballot_sync(kFull, m0 + lane < M && mgroup[m0 + lane] == gr);
+#pragma unroll
+            for (int m0 = 0; m0 < MC; m0 += 32) {
+                const unsigned mem = __ballot_sync(kFull, m0 + lane < M && s.mgroup[m0 + lane] == gr);
                 if (rep < 0 && mem) rep = m0 + __ffs(mem) - 1;
             }
-            for (int i = lane; i < M * D; i += 32) {
-                const int m = i / D, dd = i % D;
-                if (mgroup[m] != gr) continue;
-                const int dsum = gd[gr * DPW + dd];
-                a.comp[(tau0 + m) * D + dd] = dsum > 0 ? sc[dd] : 0.0;   // reading R4
-                a.devdim[(tau0 + m) * D + dd] = dsum;
+            if (rep < 0) continue;   // group without live members (uniform)
+            // plan cost (N5) and selection read the representative's row only
+            for (int dd = lane; dd < D; dd += 32) {
+                const int dsum = s.gd[gr][dd];
+                a.comp[(tau0 + rep) * D + dd] = dsum > 0 ? s.sc[dd] : 0.0;   // reading R4
+                a.devdim[(tau0 + rep) * D + dd] = dsum;
             }
-            for (int m = lane; m < M; m += 32)
-                if (mgroup[m] == gr) x.dup_of[tau0 + m] = (m == rep) ? -1 : (int32_t)(x.tau_base + tau0 + rep);
+#pragma unroll
+            for (int m0 = 0; m0 < MC; m0 += 32) {
+                const int m = m0 + lane;
+                if (m < M && s.mgroup[m] == gr) x.dup_of[tau0 + m] = (m == rep) ? -1 : (int32_t)(x.tau_base + tau0 + rep);
+            }
+            // the representative carries the plan (duplicates are read through dup_of)
+            int8_t* arow = a.assign + (size_t)(tau0 + rep) * a.Tpm;
+            const int8_t* hrow = hist + (size_t)gr * a.Tpm;
+            for (int i = lane; i < Tp; i += 32) arow[i] = hrow[i];
             __syncwarp();
         }
-        for (int m = lane; m < M; m += 32) {
-            a.feas[tau0 + m] = mgroup[m] >= 0 ? 1 : 0;
-            a.work[tau0 + m] = mwork[m] + (mgroup[m] >= 0 ? gwork[mgroup[m]] : 0);
-            if (mgroup[m] < 0) x.dup_of[tau0 + m] = -1;
+#pragma unroll
+        for (int m0 = 0; m0 < MC; m0 += 32) {
+            const int m = m0 + lane;
+            if (m < M) {
+                const int mg = s.mgroup[m];
+                a.feas[tau0 + m] = mg >= 0 ? 1 : 0;
+                a.work[tau0 + m] = s.mwork[m] + (mg >= 0 ? s.gwork[mg] : 0);
+                if (mg < 0) x.dup_of[tau0 + m] = -1;
+            }
         }
         __syncwarp();
         long long nx = 0;
@@ -1168,6 +1252,7 @@ void carve(Carver& c, SearchBufs& b, OutStage& o, int Lout) {
     b.n_uniq = c.take<int32_t>(1);
     b.next_cp = c.take<unsigned int>(1);
     b.gscratch = c.take<double>((size_t)b.gscratch_warps * b.M * b.D * kV);
+    b.ghist = c.take<int8_t>((size_t)b.gscratch_warps * b.M * b.Tpm);
     b.capdim = c.take<int32_t>((size_t)b.n_tasks * b.M);
     b.beam_plan = c.take<int32_t>((size_t)b.n_tasks * b.K * b.Lcap);
     b.beam_cnt = c.take<int32_t>(b.n_tasks);
@@ -1232,7 +1317,7 @@ ns_status launch_greedy(ns_ctx* ctx, const SearchBufs& b, const ns_tables* t, lo
     // critical path, so every trajectory runs in its own lane segment
     // (k_greedy_cta).  Throughput mode (many column plans): grouped greedy.
     const bool latency_mode =
-        4 * dp <= 32 && (b.greedy_mode == NS_GREEDY_LANES ||
+        4 * dp <= 32 && (b.greedy_mode == NS_GREEDY_LANES || b.M > 64 ||   // grouped kernel: M <= 64
                          (b.greedy_mode == NS_GREEDY_AUTO && n_cp_launch * 4 < (long long)ctx->sm_count * 16));
     if (latency_mode) {
         const int seg = 4 * dp;
@@ -1263,7 +1348,7 @@ ns_status launch_greedy(ns_ctx* ctx, const SearchBufs& b, const ns_tables* t, lo
         }
         prof_end(ctx);
         NS_CUDA(ctx, cudaMemsetAsync(b.dup_of + tb, 0xff, (size_t)n * sizeof(int32_t), ctx->stream));
-    } else if (dp <= 16) {
+    } else if (dp <= 16 && b.M <= 64) {
         // grouped greedy: one warp per column plan (trajectories [tb, te) are
         // whole column plans: tb, te multiples of M)
         const long long g0 = tb / b.M, g1 = te / b.M;
@@ -1282,32 +1367,38 @@ ns_status launch_greedy(ns_ctx* ctx, const SearchBufs& b, const ns_tables* t, lo
         x.n_cp = (int)(g1 - g0);
         x.mmax = b.M;
         x.scratch = b.gscratch;
+        x.hist = b.ghist;
         x.total_warps = (int)std::min<long long>(x.n_cp, (long long)b.gscratch_warps);
         x.dup_of = b.dup_of + (size_t)g0 * b.M;
         x.tau_base = g0 * b.M;
         x.next_cp = b.next_cp;
         NS_CUDA(ctx, cudaMemsetAsync(b.next_cp, 0, sizeof(unsigned int), ctx->stream));
         const int lpd = 32 / dp;
-        const int DPW = dp;
-        const size_t per_warp = (((size_t)b.M * (28 + DPW * 12) + DPW * 16 + 64 +
-                                  kStages * ((size_t)lpd * ((64 / lpd) * 8 + 16) + 16) + 16) + 15) & ~size_t(15);
+        const int mc = b.M <= 16 ? 16 : 64;
         const int wpb = 4;
-        const size_t smem = per_warp * wpb;
-        const unsigned blocks = (unsigned)((x.total_warps + wpb - 1) / wpb);
-        x.total_warps = (int)blocks * wpb;   // every launched warp strides the column plans
+        unsigned blocks = 0;
         prof_begin(ctx, PK_GREEDY);
-        switch (lpd) {
-#define NS_DEDUP(L)                                                                                  \
-    case L:                                                                                          \
-        if (smem > 48 * 1024)                                                                        \
-            cudaFuncSetAttribute(k_greedy_dedup<L>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
-        k_greedy_dedup<L><<<blocks, wpb * 32, smem, ctx->stream>>>(a2, x);                           \
-        break;
-            NS_DEDUP(2)
-            NS_DEDUP(4)
-            NS_DEDUP(8)
-            NS_DEDUP(16)
-            NS_DEDUP(32)
+        switch (lpd * 1000 + mc) {
+#define NS_DEDUP(L, MC)                                                                                  \
+    case L * 1000 + MC: {                                                                                \
+        const size_t smem = sizeof(DedupSmem<L, MC>) * wpb;                                              \
+        blocks = (unsigned)((x.total_warps + wpb - 1) / wpb);                                            \
+        x.total_warps = (int)blocks * wpb; /* every launched warp strides the column plans */            \
+        if (smem > 48 * 1024)                                                                            \
+            cudaFuncSetAttribute(k_greedy_dedup<L, MC>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
+        k_greedy_dedup<L, MC><<<blocks, wpb * 32, smem, ctx->stream>>>(a2, x);                           \
+        break;                                                                                           \
+    }
+            NS_DEDUP(2, 16)
+            NS_DEDUP(4, 16)
+            NS_DEDUP(8, 16)
+            NS_DEDUP(16, 16)
+            NS_DEDUP(32, 16)
+            NS_DEDUP(2, 64)
+            NS_DEDUP(4, 64)
+            NS_DEDUP(8, 64)
+            NS_DEDUP(16, 64)
+            NS_DEDUP(32, 64)
 #undef NS_DEDUP
             default: return set_err(ctx, NS_ERR_INTERNAL, "bad greedy lane split");
         }
