@@ -62,7 +62,8 @@ ns_status ns_create(ns_ctx** out, int cuda_device, void* cuda_stream);
 ns_status ns_destroy(ns_ctx* ctx);
 const char* ns_last_error(const ns_ctx* ctx);
 ns_status ns_set_stream(ns_ctx* ctx, void* cuda_stream);
-/* Block until all work enqueued by this ctx has finished. */
+/* Block until all work enqueued by this ctx has finished; reports a pending
+ * descriptor-validation error of an NS_SEARCH_ASYNC search (NS_ERR_ARG). */
 ns_status ns_synchronize(ns_ctx* ctx);
 /* Number of kernels this ctx has launched since creation (bench evidence). */
 uint64_t ns_kernel_launches(const ns_ctx* ctx);
@@ -185,6 +186,15 @@ ns_status ns_score_plans(ns_ctx* ctx, const ns_tables* tables, int32_t task, int
                                  assignment history share their scores (the paper's
                                  life-long cache, as data parallelism) */
 #define NS_GREEDY_LANES 2u    /* every trajectory in its own lane segment (latency mode) */
+/* May be OR-ed with the greedy selector: enqueue the search on the ctx stream
+ * and return without waiting (NS_OK unless an argument/launch error).  The
+ * outputs land in stream order; the caller synchronises (ns_synchronize, or
+ * any later stream sync) before reading them.  Infeasible tasks are visible
+ * as +inf costs (there is no NS_INFEASIBLE status); a descriptor-validation
+ * error of device-resident featurise input is returned by the next
+ * ns_synchronize.  Output pointers should be device or pinned host memory
+ * (pageable host outputs make the copy, and so the call, blocking). */
+#define NS_SEARCH_ASYNC 4u
 
 typedef struct {
     int32_t N;               /* candidate tables per kind, default 10 */
@@ -192,7 +202,7 @@ typedef struct {
     int32_t L;               /* split steps, default 10; ignored by tablewise */
     int32_t M;               /* grid points, default 11 */
     double  grid_hi_factor;  /* M_e = factor * M_s, default 1.5 */
-    uint32_t flags;          /* NS_GREEDY_* (0 = auto); other bits must be 0 */
+    uint32_t flags;          /* NS_GREEDY_* (0 = auto) | NS_SEARCH_ASYNC; other bits must be 0 */
 } ns_search_params;
 
 /* Per-task results.  Every pointer is host or device; only `cost` is

@@ -269,10 +269,11 @@ def ns_score_plans(ctx: int, tables: Tables, task: int, D: int, col_plan, assign
 
 # ----------------------------------------------------------------- search
 NS_GREEDY_AUTO, NS_GREEDY_GROUPED, NS_GREEDY_LANES = 0, 1, 2
+NS_SEARCH_ASYNC = 4
 
 
-def _params(N, K, L, M, hi, greedy=NS_GREEDY_AUTO):
-    return ns_search_params(N, K, L, M, hi, greedy)
+def _params(N, K, L, M, hi, greedy=NS_GREEDY_AUTO, async_=False):
+    return ns_search_params(N, K, L, M, hi, greedy | (NS_SEARCH_ASYNC if async_ else 0))
 
 
 def _alloc_out(n: int, stride: int, L: int, out: Optional[dict]):
@@ -287,18 +288,20 @@ def _alloc_out(n: int, stride: int, L: int, out: Optional[dict]):
 
 
 def ns_shard_tablewise(ctx: int, tables: Tables, D: int, M: int = 11, hi: float = 1.5, out: Optional[dict] = None,
-                       greedy: int = NS_GREEDY_AUTO):
+                       greedy: int = NS_GREEDY_AUTO, async_: bool = False):
+    """async_=True: NS_SEARCH_ASYNC (returns after enqueueing; sync before reading out)."""
     out, pb = _alloc_out(tables.n_tasks, tables.T_max, 0, out)
-    p = _params(10, 3, 0, M, hi, greedy)
+    p = _params(10, 3, 0, M, hi, greedy, async_)
     st = _check(ctx, LIB.ns_shard_tablewise(ctx, tables.handle, D, C.byref(p), C.byref(pb)))
     out["status"] = st
     return out
 
 
 def ns_shard_columnwise(ctx: int, tables: Tables, D: int, N: int = 10, K: int = 3, L: int = 10, M: int = 11,
-                        hi: float = 1.5, out: Optional[dict] = None, greedy: int = NS_GREEDY_AUTO):
+                        hi: float = 1.5, out: Optional[dict] = None, greedy: int = NS_GREEDY_AUTO,
+                        async_: bool = False):
     out, pb = _alloc_out(tables.n_tasks, tables.T_max + L, L, out)
-    p = _params(N, K, L, M, hi, greedy)
+    p = _params(N, K, L, M, hi, greedy, async_)
     st = _check(ctx, LIB.ns_shard_columnwise(ctx, tables.handle, D, C.byref(p), C.byref(pb)))
     out["status"] = st
     return out

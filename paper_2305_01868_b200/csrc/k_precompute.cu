@@ -11,10 +11,12 @@
 // device with 64-wide adds on cached v rows instead of re-running the MLP
 // (SURVEY.md TL;DR 2).  All arithmetic is fp64.
 //
-// Work per row: 5*128 + 128*32 + 32*64 + 64 MAC = 6.8k DFMA.  Mapping: one
-// warp per row, weights staged once per CTA in shared memory (transposed so
-// lanes read consecutive addresses), persistent grid-stride loop.
+// Work per row: 5*128 + 128*32 + 32*64 + 64 MAC = 6.8k DFMA, run as a GEMM
+// chain on the FP64 tensor cores (k_precompute_dmma in k_mlp.cu).  This file
+// holds the descriptor validation that precedes it.
 #include <cuda_runtime.h>
+
+#include <algorithm>
 
 #include "ns_internal.cuh"
 
@@ -23,31 +25,34 @@ namespace {
 
 // Per task: validate the descriptors (device-resident input) and sum the
 // dims (sum(dim) is invariant under column splits, so the grid of
-// P:289 is fixed per task).
-__global__ void k_tables_validate(const ns_table_desc* desc, const int32_t* off, int64_t* sumdim, int32_t* flag) {
-    __shared__ long long s_sum;
-    const int q = blockIdx.x;
-    if (threadIdx.x == 0) s_sum = 0;
-    __syncthreads();
-    long long sum = 0;
+// P:289 is fixed per task).  One warp per task (grid-stride), shuffle sum.
+__global__ void __launch_bounds__(256) k_tables_validate(const ns_table_desc* desc, const int32_t* off, int n_tasks,
+                                                         int64_t* sumdim, int32_t* flag) {
+    const int lane = threadIdx.x & 31;
     int bad = 0;
-    for (int g = off[q] + threadIdx.x; g < off[q + 1]; g += blockDim.x) {
-        const ns_table_desc d = desc[g];
-        bad |= (d.dim < 4 || d.dim % 4 != 0 || d.dim > (1 << 20) || d.hash_size < 1 || !(d.pooling_factor > 0) ||
-                !(d.skew >= 0) || d.reserved != 0);
-        sum += d.dim;
+    for (int q = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; q < n_tasks; q += (gridDim.x * blockDim.x) >> 5) {
+        long long sum = 0;
+        const int e = off[q + 1];
+        for (int g = off[q] + lane; g < e; g += 32) {
+            const ns_table_desc d = desc[g];
+            bad |= (d.dim < 4 || d.dim % 4 != 0 || d.dim > (1 << 20) || d.hash_size < 1 || !(d.pooling_factor > 0) ||
+                    !(d.skew >= 0) || d.reserved != 0);
+            sum += d.dim;
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+        if (lane == 0) sumdim[q] = sum;
     }
-    atomicAdd((unsigned long long*)&s_sum, (unsigned long long)sum);
-    if (bad) atomicOr(flag, 1);
-    __syncthreads();
-    if (threadIdx.x == 0) sumdim[q] = s_sum;
+    if (__any_sync(0xffffffffu, bad) && lane == 0) atomicOr(flag, 1);
 }
 
 }  // namespace
 
 void launch_tables_validate(ns_ctx* ctx, const ns_tables* t) {
     prof_begin(ctx, PK_VALIDATE);
-    k_tables_validate<<<t->n_tasks, 128, 0, ctx->stream>>>(t->d_desc, t->d_off, t->d_sumdim, t->d_flag);
+    const long long warps = t->n_tasks > 0 ? t->n_tasks : 1;
+    const unsigned blocks = (unsigned)std::min<long long>((warps + 7) / 8, (long long)ctx->sm_count * 8);
+    k_tables_validate<<<blocks, 256, 0, ctx->stream>>>(t->d_desc, t->d_off, t->n_tasks, t->d_sumdim, t->d_flag);
     prof_end(ctx);
     ctx->launches++;
 }

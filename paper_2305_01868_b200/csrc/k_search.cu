@@ -205,6 +205,77 @@ __global__ void k_build_order(SearchBufs b, TaskView tv) {
     }
 }
 
+// Warp-per-column-plan form of k_build_order for short lists (Tpm <= 256):
+// same rank sort, no CTA-wide barriers.  At level 0 it also initialises the
+// per-task search state (column plan [] of task q in slot q) and the task's
+// M grid caps floor(max_dim_m) (Alg. 2 line 4; operation order of
+// reading R8 with explicit IEEE roundings).
+__device__ __forceinline__ int32_t grid_cap(long long sumdim, int D, int M, int m, double hi) {
+    const double Ms = __ddiv_rn((double)sumdim, (double)D);
+    double md = Ms;
+    if (M > 1) {
+        const double Me = __dmul_rn(hi, Ms);
+        const double step = __ddiv_rn(__dsub_rn(Me, Ms), (double)(M - 1));
+        md = __dadd_rn(Ms, __dmul_rn((double)m, step));
+    }
+    const double f = floor(md);
+    return f > 2.0e9 ? 2000000000 : (int32_t)f;
+}
+
+__global__ void __launch_bounds__(256) k_order_warp(SearchBufs b, TaskView tv, int n_cp, int level0,
+                                                    const int64_t* sumdim, double hi) {
+    extern __shared__ __align__(16) unsigned char wsm[];
+    const int lane = threadIdx.x & 31, wl = threadIdx.x >> 5;
+    const int ri = (b.Tpm + 1) & ~1;
+    int32_t* rows = (int32_t*)(wsm + (size_t)wl * (ri * 4 + b.Tpm * 8));
+    double* key = (double*)(rows + ri);
+    for (int g = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; g < n_cp; g += (gridDim.x * blockDim.x) >> 5) {
+        if (level0) {
+            if (lane == 0) {
+                b.cp_task[g] = g;
+                b.cp_valid[g] = 1;
+                b.cp_len[g] = 0;
+                b.best_cost[g] = CUDART_INF;
+                b.best_m[g] = -1;
+                b.best_ncol[g] = 0;
+                b.n_scores[g] = 0;
+                b.beam_cnt[g] = 0;
+            }
+            for (int m = lane; m < b.M; m += 32) b.capdim[g * b.M + m] = grid_cap(sumdim[g], b.D, b.M, m, hi);
+        } else if (!b.cp_valid[g]) {
+            continue;
+        }
+        const int q = level0 ? g : b.cp_task[g];
+        const int len = level0 ? 0 : b.cp_len[g];
+        const int base = tv.off[q], T = tv.off[q + 1] - base, Tp = T + len;
+        for (int i = lane; i < T; i += 32) rows[i] = (base + i) * kDepth;
+        __syncwarp();
+        if (lane == 0) {
+            const int32_t* plan = b.cp_plan + (size_t)g * b.Lcap;
+            for (int k = 0; k < len; ++k) {   // halve c_k in place, append the other half
+                const int c = plan[k];
+                rows[c] += 1;
+                rows[T + k] = rows[c];
+            }
+            b.cp_Tp[g] = Tp;
+        }
+        __syncwarp();
+        for (int i = lane; i < Tp; i += 32) key[i] = tv.C[rows[i]];
+        __syncwarp();
+        for (int i = lane; i < Tp; i += 32) {
+            const double ci = key[i];
+            int r = 0;
+            for (int k = 0; k < Tp; ++k) {
+                const double ck = key[k];
+                r += (ck > ci) || (ck == ci && k < i);
+            }
+            b.ord_row[(size_t)g * b.Tpm + r] = rows[i];
+            b.ord_idx[(size_t)g * b.Tpm + r] = i;
+        }
+        __syncwarp();
+    }
+}
+
 // ======================================================================
 // N4: greedy placement (Alg. 2 lines 6-20, PAPER.md:289 step 3) -- the hot loop.
 //
@@ -1087,6 +1158,54 @@ __global__ void __launch_bounds__(512) k_greedy_big(const GreedyArgs a) {
 // generation order (Alg. 1 lines 13-16), next beam = K lowest (cost, gen)
 // (Alg. 1 line 20; R13, R16).  One CTA per task.
 // ======================================================================
+// Level 0 (one column plan per task, C = 1): one warp per task.  The grid
+// argmin (lowest m on ties, R12) is reduced with shuffles; level 0 always
+// installs [] as the initial global best (R15).
+__global__ void __launch_bounds__(256) k_select0(SearchBufs b) {
+    const int lane = threadIdx.x & 31;
+    for (int q = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; q < b.n_tasks; q += (gridDim.x * blockDim.x) >> 5) {
+        unsigned long long wsum = 0;
+        double best = CUDART_INF;
+        int bm = INT_MAX;
+        for (int m = lane; m < b.M; m += 32) {
+            const long long tau = (long long)q * b.M + m;
+            wsum += b.work[tau];
+            const long long src = b.dup_of[tau] >= 0 ? (long long)b.dup_of[tau] : tau;
+            const double c = b.feas[tau] ? b.tcost[src] : CUDART_INF;
+            if (c < best) {   // m increases per lane: strict < keeps the lowest m
+                best = c;
+                bm = m;
+            }
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            wsum += __shfl_xor_sync(kFull, wsum, o);
+            const double ob = __shfl_xor_sync(kFull, best, o);
+            const int om = __shfl_xor_sync(kFull, bm, o);
+            if (ob < best || (ob == best && om < bm)) {
+                best = ob;
+                bm = om;
+            }
+        }
+        if (best == CUDART_INF) bm = -1;
+        if (lane == 0) {
+            b.n_scores[q] += wsum;
+            b.best_cost[q] = best;
+            b.best_m[q] = bm;
+            b.best_ncol[q] = 0;
+            b.beam_cnt[q] = 1;   // C_p <- {[]}
+        }
+        const int Tp = b.cp_Tp[q];
+        long long src = -1;
+        if (bm >= 0) {
+            const long long tau = (long long)q * b.M + bm;
+            src = b.dup_of[tau] >= 0 ? (long long)b.dup_of[tau] : tau;
+        }
+        for (int i = lane; i < b.Tpm; i += 32)
+            b.best_assign[(size_t)q * b.Tpm + i] = (src >= 0 && i < Tp) ? b.assign[src * b.Tpm + i] : (int8_t)-1;
+    }
+}
+
 __global__ void k_select(SearchBufs b, int C, int level, int Kbeam) {
     extern __shared__ unsigned char ssm[];
     const int q = blockIdx.x;
@@ -1149,7 +1268,11 @@ __global__ void k_select(SearchBufs b, int C, int level, int Kbeam) {
         const int mm = cm[s_best];
         for (int i = threadIdx.x; i < b.Tpm; i += blockDim.x) {
             int8_t v = -1;
-            if (mm >= 0 && i < Tp) v = b.assign[((size_t)g * b.M + mm) * b.Tpm + i];
+            if (mm >= 0 && i < Tp) {
+                const long long tau = (long long)g * b.M + mm;
+                const long long src = b.dup_of[tau] >= 0 ? (long long)b.dup_of[tau] : tau;
+                v = b.assign[src * b.Tpm + i];
+            }
             b.best_assign[(size_t)q * b.Tpm + i] = v;
         }
     }
@@ -1196,24 +1319,31 @@ struct OutStage {
     double* cost;
     int32_t* n_col;
     int32_t* col_plan;   // [n][Lout]
-    int8_t* assign;      // [n][Tpm]
+    int8_t* assign;      // [n][astride]: columns >= Tpm are -1
+    int astride;
     int32_t* grid;
     uint64_t* scores;
+    // which fields point straight at the caller's device buffers (no copy in deliver)
+    bool d_cost, d_ncol, d_plan, d_assign, d_grid, d_scores;
 };
 
-__global__ void k_write_out(SearchBufs b, OutStage o, int Lout) {
-    const int q = blockIdx.x;
-    const bool feasible = b.best_cost[q] < CUDART_INF;
-    if (threadIdx.x == 0) {
-        o.cost[q] = b.best_cost[q];
-        o.n_col[q] = b.best_ncol[q];
-        o.grid[q] = feasible ? b.best_m[q] : -1;
-        o.scores[q] = b.n_scores[q];
+__global__ void __launch_bounds__(256) k_write_out(SearchBufs b, OutStage o, int Lout) {
+    const int lane = threadIdx.x & 31;
+    for (int q = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; q < b.n_tasks; q += (gridDim.x * blockDim.x) >> 5) {
+        const bool feasible = b.best_cost[q] < CUDART_INF;
+        const int ncol = b.best_ncol[q];
+        if (lane == 0) {
+            o.cost[q] = b.best_cost[q];
+            o.n_col[q] = ncol;
+            o.grid[q] = feasible ? b.best_m[q] : -1;
+            o.scores[q] = b.n_scores[q];
+        }
+        for (int k = lane; k < Lout; k += 32)
+            o.col_plan[(size_t)q * Lout + k] = k < ncol ? b.best_plan[(size_t)q * b.Lcap + k] : -1;
+        for (int i = lane; i < o.astride; i += 32)
+            o.assign[(size_t)q * o.astride + i] =
+                (feasible && i < b.Tpm) ? b.best_assign[(size_t)q * b.Tpm + i] : (int8_t)-1;
     }
-    for (int k = threadIdx.x; k < Lout; k += blockDim.x)
-        o.col_plan[(size_t)q * Lout + k] = k < b.best_ncol[q] ? b.best_plan[(size_t)q * b.Lcap + k] : -1;
-    for (int i = threadIdx.x; i < b.Tpm; i += blockDim.x)
-        o.assign[(size_t)q * b.Tpm + i] = feasible ? b.best_assign[(size_t)q * b.Tpm + i] : (int8_t)-1;
 }
 
 // ======================================================================
@@ -1266,6 +1396,7 @@ void carve(Carver& c, SearchBufs& b, OutStage& o, int Lout) {
     o.n_col = c.take<int32_t>(b.n_tasks);
     o.col_plan = c.take<int32_t>((size_t)b.n_tasks * Lout);
     o.assign = c.take<int8_t>((size_t)b.n_tasks * b.Tpm);
+    o.astride = b.Tpm;
     o.grid = c.take<int32_t>(b.n_tasks);
     o.scores = c.take<uint64_t>(b.n_tasks);
 }
@@ -1475,35 +1606,61 @@ ns_status run_level_trajectories(ns_ctx* ctx, const SearchBufs& b, const ns_tabl
     return NS_OK;
 }
 
-// Copy staged results to the caller's (host or device) pointers.
-ns_status deliver(ns_ctx* ctx, const ns_tables* t, const OutStage& o, int Lout, int Tpm, ns_plan_batch* out) {
+// Outputs the caller passed as device pointers are written by k_write_out
+// directly (assign with the caller's stride, -1 padded); the others go
+// through the staging buffers and are copied by deliver.
+void bind_outputs(OutStage& o, const ns_plan_batch* out, int n, int Lout) {
+    o.d_cost = out->cost && is_device_ptr(out->cost);
+    o.d_ncol = out->n_col && is_device_ptr(out->n_col);
+    o.d_plan = out->col_plan && Lout > 0 && is_device_ptr(out->col_plan);
+    o.d_assign = out->assign && is_device_ptr(out->assign);
+    o.d_grid = out->grid_index && is_device_ptr(out->grid_index);
+    o.d_scores = out->n_scores && is_device_ptr(out->n_scores);
+    (void)n;
+    if (o.d_cost) o.cost = out->cost;
+    if (o.d_ncol) o.n_col = out->n_col;
+    if (o.d_plan) o.col_plan = out->col_plan;
+    if (o.d_assign) {
+        o.assign = out->assign;
+        o.astride = out->assign_stride;
+    }
+    if (o.d_grid) o.grid = out->grid_index;
+    if (o.d_scores) o.scores = (uint64_t*)out->n_scores;
+}
+
+// Copy staged results to the caller's (host) pointers.
+ns_status deliver(ns_ctx* ctx, const ns_tables* t, const OutStage& o, int Lout, int Tpm, ns_plan_batch* out,
+                  bool async) {
     const int n = t->n_tasks;
     cudaStream_t st = ctx->stream;
     auto cp = [&](void* dst, const void* src, size_t bytes) -> cudaError_t {
         if (!dst) return cudaSuccess;
         return cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDefault, st);
     };
-    NS_CUDA(ctx, cp(out->n_col, o.n_col, n * sizeof(int32_t)));
-    if (out->col_plan && Lout > 0) NS_CUDA(ctx, cp(out->col_plan, o.col_plan, (size_t)n * Lout * sizeof(int32_t)));
-    if (out->assign) {
-        if (out->assign_stride > Tpm) NS_CUDA(ctx, cudaMemset2DAsync(out->assign, out->assign_stride, 0xff,
-                                                                     0, 0, st));   // no-op placeholder
-        if (is_device_ptr(out->assign)) {
-            NS_CUDA(ctx, cudaMemset2DAsync(out->assign, out->assign_stride, 0xff, out->assign_stride, n, st));
-        } else {
-            for (int q = 0; q < n; ++q) std::memset(out->assign + (size_t)q * out->assign_stride, 0xff, out->assign_stride);
+    if (!o.d_ncol) NS_CUDA(ctx, cp(out->n_col, o.n_col, n * sizeof(int32_t)));
+    if (out->col_plan && Lout > 0 && !o.d_plan)
+        NS_CUDA(ctx, cp(out->col_plan, o.col_plan, (size_t)n * Lout * sizeof(int32_t)));
+    if (out->assign && !o.d_assign) {
+        // columns [Tpm, stride) are -1 (the copy below fills [0, Tpm))
+        if (out->assign_stride > Tpm) {
+            for (int q = 0; q < n; ++q)
+                std::memset(out->assign + (size_t)q * out->assign_stride + Tpm, 0xff, out->assign_stride - Tpm);
         }
         NS_CUDA(ctx, cudaMemcpy2DAsync(out->assign, out->assign_stride, o.assign, Tpm, Tpm, n, cudaMemcpyDefault, st));
     }
-    NS_CUDA(ctx, cp(out->grid_index, o.grid, n * sizeof(int32_t)));
-    NS_CUDA(ctx, cp(out->n_scores, o.scores, n * sizeof(uint64_t)));
+    if (!o.d_grid) NS_CUDA(ctx, cp(out->grid_index, o.grid, n * sizeof(int32_t)));
+    if (!o.d_scores) NS_CUDA(ctx, cp(out->n_scores, o.scores, n * sizeof(uint64_t)));
+    if (async) {   // NS_SEARCH_ASYNC: no wait; the validation flag is checked by ns_synchronize
+        if (!o.d_cost) NS_CUDA(ctx, cp(out->cost, o.cost, n * sizeof(double)));
+        return record_async_flag(ctx, t->d_flag);
+    }
     // costs always pass through pinned host memory: the status needs them
     double* hcost = (double*)pinned_get(ctx, n * sizeof(double) + 64);
     if (!hcost) return set_err(ctx, NS_ERR_NOMEM, "pinned staging");
     int32_t* hflag = (int32_t*)(hcost + n);
     NS_CUDA(ctx, cudaMemcpyAsync(hcost, o.cost, n * sizeof(double), cudaMemcpyDeviceToHost, st));
     NS_CUDA(ctx, cudaMemcpyAsync(hflag, t->d_flag, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
-    NS_CUDA(ctx, cp(out->cost, o.cost, n * sizeof(double)));
+    if (!o.d_cost) NS_CUDA(ctx, cp(out->cost, o.cost, n * sizeof(double)));
     NS_CUDA(ctx, cudaStreamSynchronize(st));
     prof_collect(ctx);
     ns_status fs = check_tables_flag(ctx, t, hflag);
@@ -1552,31 +1709,40 @@ ns_status run_search(ns_ctx* ctx, const ns_tables* t, int D, const ns_search_par
     Carver cv{base};
     carve(cv, b, o, Lout > 0 ? Lout : 1);
     ns_status s;
-    prof_begin(ctx, PK_OTHER);
-    k_grid_caps<<<(b.n_tasks * b.M + 255) / 256, 256, 0, ctx->stream>>>(t->d_sumdim, b.n_tasks, b.D, b.M,
-                                                                        p->grid_hi_factor, b.capdim);
-    prof_end(ctx);
-    NS_LAUNCHED(ctx);
     const TaskView tv = task_view(t);
     const size_t osm = order_smem(b.Tpm);
     if (osm > 48 * 1024) {
         cudaFuncSetAttribute(k_build_order, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)osm);
         cudaFuncSetAttribute(k_expand, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)osm);
     }
+    // short lists: one warp per column plan (8 per CTA); long lists: one CTA
+    const bool warp_order = b.Tpm <= 256;
+    const size_t wsm = 8 * osm;
+    auto launch_order = [&](int n_cp, int level0) {
+        prof_begin(ctx, PK_ORDER);
+        if (warp_order) {
+            const unsigned blocks = (unsigned)std::max(1, std::min((n_cp + 7) / 8, ctx->sm_count * 8));
+            k_order_warp<<<blocks, 256, wsm, ctx->stream>>>(b, tv, n_cp, level0, t->d_sumdim, p->grid_hi_factor);
+        } else {
+            k_build_order<<<n_cp, 256, osm, ctx->stream>>>(b, tv);
+        }
+        prof_end(ctx);
+        NS_LAUNCHED(ctx);
+    };
     // ---- level 0: the empty column plan (tablewise = this level only)
-    prof_begin(ctx, PK_OTHER);
-    k_setup_level0<<<(b.n_tasks + 255) / 256, 256, 0, ctx->stream>>>(b);
-    prof_end(ctx);
-    NS_LAUNCHED(ctx);
-    prof_begin(ctx, PK_ORDER);
-    k_build_order<<<b.n_tasks, 256, osm, ctx->stream>>>(b, tv);
-    prof_end(ctx);
-    NS_LAUNCHED(ctx);
-    const long long n0 = (long long)b.n_tasks * b.M;
-    (void)n0;
+    if (!warp_order) {
+        prof_begin(ctx, PK_OTHER);
+        k_grid_caps<<<(b.n_tasks * b.M + 255) / 256, 256, 0, ctx->stream>>>(t->d_sumdim, b.n_tasks, b.D, b.M,
+                                                                            p->grid_hi_factor, b.capdim);
+        k_setup_level0<<<(b.n_tasks + 255) / 256, 256, 0, ctx->stream>>>(b);
+        prof_end(ctx);
+        NS_LAUNCHED(ctx);
+        NS_LAUNCHED(ctx);
+    }
+    launch_order(b.n_tasks, warp_order ? 1 : 0);
     if ((s = run_level_trajectories(ctx, b, t, b.n_tasks)) != NS_OK) return s;
     prof_begin(ctx, PK_SELECT);
-    k_select<<<b.n_tasks, 128, (size_t)1 * 16, ctx->stream>>>(b, 1, 0, b.K);
+    k_select0<<<(unsigned)std::max(1, std::min((b.n_tasks + 7) / 8, ctx->sm_count * 8)), 256, 0, ctx->stream>>>(b);
     prof_end(ctx);
     NS_LAUNCHED(ctx);
     // ---- beam levels (Alg. 1 lines 6-22)
@@ -1588,21 +1754,20 @@ ns_status run_search(ns_ctx* ctx, const ns_tables* t, int D, const ns_search_par
         k_expand<<<b.n_tasks * b.K, 256, esm, ctx->stream>>>(b, tv, level);
         prof_end(ctx);
         NS_LAUNCHED(ctx);
-        prof_begin(ctx, PK_ORDER);
-        k_build_order<<<b.S, 256, osm, ctx->stream>>>(b, tv);
-        prof_end(ctx);
-        NS_LAUNCHED(ctx);
+        launch_order(b.S, 0);
         if ((s = run_level_trajectories(ctx, b, t, b.S)) != NS_OK) return s;
         prof_begin(ctx, PK_SELECT);
         k_select<<<b.n_tasks, 128, (size_t)C * 16, ctx->stream>>>(b, C, level, b.K);
         prof_end(ctx);
         NS_LAUNCHED(ctx);
     }
+    bind_outputs(o, out, b.n_tasks, Lout);
     prof_begin(ctx, PK_OTHER);
-    k_write_out<<<b.n_tasks, 128, 0, ctx->stream>>>(b, o, Lout > 0 ? Lout : 1);
+    k_write_out<<<(unsigned)std::max(1, std::min((b.n_tasks + 7) / 8, ctx->sm_count * 8)), 256, 0, ctx->stream>>>(
+        b, o, Lout > 0 ? Lout : 1);
     prof_end(ctx);
     NS_LAUNCHED(ctx);
-    return deliver(ctx, t, o, Lout, b.Tpm, out);
+    return deliver(ctx, t, o, Lout, b.Tpm, out, (p->flags & NS_SEARCH_ASYNC) != 0);
 }
 
 }  // namespace

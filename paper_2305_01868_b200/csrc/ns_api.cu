@@ -227,6 +227,8 @@ ns_status ns_destroy(ns_ctx* ctx) {
     if (ctx->pinned) cudaFreeHost(ctx->pinned);
     if (ctx->pinned_in) cudaFreeHost(ctx->pinned_in);
     if (ctx->pinned_in_done) cudaEventDestroy(ctx->pinned_in_done);
+    if (ctx->d_async_flags) cudaFree(ctx->d_async_flags);
+    if (ctx->h_async_flags) cudaFreeHost(ctx->h_async_flags);
     prof_collect(ctx);
     for (cudaEvent_t e : ctx->prof_free) cudaEventDestroy(e);
     comm_destroy(ctx);
@@ -246,7 +248,8 @@ ns_status ns_synchronize(ns_ctx* ctx) {
     if (!ctx) return NS_ERR_ARG;
     cudaSetDevice(ctx->device);
     NS_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
-    return NS_OK;
+    prof_collect(ctx);
+    return check_async_flags(ctx);
 }
 
 uint64_t ns_kernel_launches(const ns_ctx* ctx) { return ctx ? ctx->launches : 0; }
@@ -482,6 +485,36 @@ ns_status ensure_host_dims(ns_ctx* ctx, const ns_tables* t) {
     return NS_OK;
 }
 
+// NS_SEARCH_ASYNC: the tables' validation flag is copied (stream-ordered) into
+// a ctx slot; ns_synchronize checks every recorded slot.
+ns_status record_async_flag(ns_ctx* ctx, const int32_t* d_flag) {
+    if (!ctx->d_async_flags) {
+        NS_CUDA(ctx, cudaMalloc(&ctx->d_async_flags, ns_ctx::kAsyncFlags * sizeof(int32_t)));
+        NS_CUDA(ctx, cudaMallocHost(&ctx->h_async_flags, ns_ctx::kAsyncFlags * sizeof(int32_t)));
+    }
+    if (ctx->n_async_flags == ns_ctx::kAsyncFlags) {   // full: check (and empty) now
+        ns_status s = check_async_flags(ctx);
+        if (s != NS_OK) return s;
+    }
+    NS_CUDA(ctx, cudaMemcpyAsync(ctx->d_async_flags + ctx->n_async_flags++, d_flag, sizeof(int32_t),
+                                 cudaMemcpyDeviceToDevice, ctx->stream));
+    return NS_OK;
+}
+
+ns_status check_async_flags(ns_ctx* ctx) {
+    const int n = ctx->n_async_flags;
+    if (n == 0) return NS_OK;
+    ctx->n_async_flags = 0;
+    NS_CUDA(ctx, cudaMemcpyAsync(ctx->h_async_flags, ctx->d_async_flags, n * sizeof(int32_t), cudaMemcpyDeviceToHost,
+                                 ctx->stream));
+    NS_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+    for (int i = 0; i < n; ++i) {
+        ns_status s = check_tables_flag(ctx, nullptr, ctx->h_async_flags + i);
+        if (s != NS_OK) return s;
+    }
+    return NS_OK;
+}
+
 // Device-side validation flag of the descriptors (set by k_tables_validate).
 ns_status check_tables_flag(ns_ctx* ctx, const ns_tables* t, const int32_t* host_flag) {
     (void)t;
@@ -516,7 +549,7 @@ static ns_status check_search(ns_ctx* ctx, const ns_tables* t, int D, const ns_s
     if (!ctx->model.loaded) return set_err(ctx, NS_ERR_STATE, "no cost models loaded");
     if (D != ctx->model.D) return set_err(ctx, NS_ERR_ARG, "D differs from the loaded comm models' D");
     if (p->M < 1 || p->M > 4096) return set_err(ctx, NS_ERR_ARG, "need 1 <= M <= 4096");
-    if (!(p->grid_hi_factor >= 1.0) || p->flags > NS_GREEDY_LANES)
+    if (!(p->grid_hi_factor >= 1.0) || (p->flags & ~NS_SEARCH_ASYNC) > NS_GREEDY_LANES)
         return set_err(ctx, NS_ERR_ARG, "bad grid_hi_factor/flags");
     if (columnwise) {
         if (p->N < 1 || p->K < 1 || p->L < 0 || p->L > 64 || p->N > 512 || p->K > 512)

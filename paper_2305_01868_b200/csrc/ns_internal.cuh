@@ -99,6 +99,11 @@ struct ns_ctx {
     int nranks = 1, rank = 0;
     bool emulated = false;   // ns_comm_init(id == NULL): all ranks' blocks computed in-process (test hook)
     std::set<ns_tables*> tables;   // live ns_tables of this ctx (freed by ns_destroy)
+    // validation flags of NS_SEARCH_ASYNC searches, checked by ns_synchronize
+    static constexpr int kAsyncFlags = 256;
+    int32_t* d_async_flags = nullptr;   // [kAsyncFlags] device copies of the tables' flags
+    int32_t* h_async_flags = nullptr;   // pinned
+    int n_async_flags = 0;
 };
 
 struct ns_tables {
@@ -132,6 +137,8 @@ void launch_precompute(ns_ctx* ctx, const ns_tables* t, int jlo, int jhi);
 // descriptor validation + per-task sum of dims (device side)
 void launch_tables_validate(ns_ctx* ctx, const ns_tables* t);
 ns_status ensure_host_dims(ns_ctx* ctx, const ns_tables* t);
+ns_status check_async_flags(ns_ctx* ctx);   // syncs the stream
+ns_status record_async_flag(ns_ctx* ctx, const int32_t* d_flag);
 ns_status check_tables_flag(ns_ctx* ctx, const ns_tables* t, const int32_t* host_flag);
 
 struct SearchBufs;   // defined in k_search.cu

@@ -307,6 +307,66 @@ def test_device_resident_inputs_and_outputs(ns, ctx):
     assert np.array_equal(out["assign"].cpu().numpy(), host["assign"])
 
 
+def test_async_search_matches_sync(ns, ctx):
+    """NS_SEARCH_ASYNC: several searches enqueued back to back into device
+    outputs, one ns_synchronize, results equal the synchronous calls."""
+    import torch
+    w = gen_weights(4, "mono")
+    ns.ns_load_cost_models(ctx, w)
+    batches = [gen_tasks("C2", 6, start=6 * i) for i in range(3)]
+    outs, refs = [], []
+    for tasks in batches:
+        desc, off, caps = ns.table_descs(tasks)
+        tabs = ns.ns_featurize_tables(ctx, torch.from_numpy(desc.view(np.uint8)).cuda(), off, caps)
+        n, T = len(tasks), tabs.T_max
+        out = dict(cost=torch.zeros(n, dtype=torch.float64, device="cuda"),
+                   n_col=torch.zeros(n, dtype=torch.int32, device="cuda"), col_plan=None,
+                   assign=torch.zeros((n, T + 2), dtype=torch.int8, device="cuda"),
+                   grid_index=torch.zeros(n, dtype=torch.int32, device="cuda"),
+                   n_scores=torch.zeros(n, dtype=torch.int64, device="cuda"))
+        ns.ns_shard_tablewise(ctx, tabs, 4, M=11, out=out, async_=True)
+        outc = ns.ns_shard_columnwise(ctx, tabs, 4, N=4, K=2, L=2, M=5, async_=True)   # pageable outputs
+        outs.append((out, outc))
+        tabs.free()   # stream-ordered: safe while the searches are in flight
+    ns.ns_synchronize(ctx)
+    for tasks, (out, outc) in zip(batches, outs):
+        tabs = _setup(ns, ctx, tasks, w)
+        ref = ns.ns_shard_tablewise(ctx, tabs, 4, M=11)
+        refc = ns.ns_shard_columnwise(ctx, tabs, 4, N=4, K=2, L=2, M=5)
+        T = tabs.T_max
+        assert np.array_equal(out["cost"].cpu().numpy(), ref["cost"])
+        a = out["assign"].cpu().numpy()
+        assert np.array_equal(a[:, :T], ref["assign"]) and (a[:, T:] == -1).all()
+        assert np.array_equal(out["grid_index"].cpu().numpy(), ref["grid_index"])
+        assert np.array_equal(out["n_scores"].cpu().numpy().astype(np.uint64), ref["n_scores"])
+        for k in ("cost", "n_col", "col_plan", "assign", "grid_index", "n_scores"):
+            assert np.array_equal(outc[k], refc[k]), k
+        tabs.free()
+
+
+def test_async_search_defers_validation_error(ns, ctx):
+    """An invalid device-resident descriptor under NS_SEARCH_ASYNC: the search
+    call returns, the next ns_synchronize reports NS_ERR_ARG, and the ctx keeps
+    working afterwards."""
+    import torch
+    w = gen_weights(4, "mono")
+    ns.ns_load_cost_models(ctx, w)
+    tasks = gen_tasks("C2", 2)
+    desc, off, caps = ns.table_descs(tasks)
+    bad = desc.copy()
+    bad["dim"][3] = 6
+    tabs = ns.ns_featurize_tables(ctx, torch.from_numpy(bad.view(np.uint8)).cuda(), off, caps)
+    ns.ns_shard_tablewise(ctx, tabs, 4, M=11, async_=True)
+    tabs.free()
+    with pytest.raises(ns.NSError):
+        ns.ns_synchronize(ctx)
+    ns.ns_synchronize(ctx)   # reported once
+    tabs = ns.ns_featurize_tables(ctx, torch.from_numpy(desc.view(np.uint8)).cuda(), off, caps)
+    ns.ns_shard_tablewise(ctx, tabs, 4, M=11, async_=True)
+    ns.ns_synchronize(ctx)
+    tabs.free()
+
+
 def test_determinism(ns, ctx):
     w = gen_weights(8, "mono")
     tasks = gen_tasks("C3", 2)
