@@ -1,9 +1,9 @@
-"""Per-source-line instructions per (column plan, table) step and stall share of one greedy ncu report."""
-import csv, subprocess, sys
+"""Per-source-line instructions per unit and stall share of one kernel in an ncu report (KREGEX, default greedy)."""
+import csv, os, subprocess, sys
 from collections import defaultdict
 rep = sys.argv[1]
 steps = float(sys.argv[2]) if len(sys.argv) > 2 else 16384 * 40
-out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "cuda,sass", "-k", "regex:greedy"],
+out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "cuda,sass", "-k", "regex:" + os.environ.get("KREGEX", "greedy")],
                      capture_output=True, text=True).stdout
 r = list(csv.reader(out.splitlines()))
 h = next(x for x in r if x and x[0] == "Line No")
