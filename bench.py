@@ -62,8 +62,16 @@ def dist_setup(n_gpus):
     if world > 1:
         import torch.distributed as dist
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        n_dev = torch.cuda.device_count()
+        if n_dev >= world:
+            torch.cuda.set_device(local)
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            # more ranks than GPUs (functional check of the N > 1 path on a
+            # 1-GPU box): ranks share devices, NCCL refuses duplicates -> gloo
+            local = local % max(n_dev, 1)
+            torch.cuda.set_device(local)
+            dist.init_process_group("gloo")
     return world, rank, local
 
 
