@@ -279,21 +279,22 @@ __global__ void __launch_bounds__(256) k_order_warp(SearchBufs b, TaskView tv, i
 // ======================================================================
 // N4: greedy placement (Alg. 2 lines 6-20, PAPER.md:289 step 3) -- the hot loop.
 //
-// Two lanes per (trajectory, device).  Lane half h in {0,1} keeps features
-// [32h, 32h+32) of the hoisted head pre-activation u_d = hb1 + sum_{t on d} v_t
-// and of the head weights H2 in registers (fp64).  For table t (cost order)
-// every feasible device scores C(S_d + {t}) = hb2 + H2 . ReLU(u_d + v_t)
-// (reading R5: cost after insertion): each lane computes its 32-term partial
-// dot product and one shuffle joins the pair.  A segmented shuffle argmin picks
-// d* (lowest d on ties, R13); both lanes of d* add their half of v_t.
-// Feasible: bytes_d + bytes_t <= cap and dim_d + dim_t <= floor(max_dim_m)
-// (R6, R7); no feasible device strands the trajectory (R9).
+// LPD lanes per (trajectory or group, device); each lane keeps FPL = 64/LPD
+// features of the hoisted head pre-activation u_d = hb1 + sum_{t on d} v_t and
+// of the head weights H2 in registers (fp64).  For table t (cost order) every
+// feasible device scores C(S_d + {t}) = hb2 + H2 . ReLU(u_d + v_t) (reading
+// R5: cost after insertion): each lane computes its partial dot product and a
+// butterfly over the LPD lanes joins them.  A shuffle argmin picks d* (lowest
+// d on ties, R13); the lanes of d* add their slice of v_t.  Feasible:
+// bytes_d + bytes_t <= cap and dim_d + dim_t <= floor(max_dim_m) (R6, R7); no
+// feasible device strands the trajectory (R9).
 //
-// Why two lanes per device: with all 64 features in one lane, u (128 regs)
-// plus the 64 head weights exceed the register file and the compiler spills
-// the weights (they cannot all live in uniform registers).  Splitting the
-// features keeps u, H2 and the streamed v chunk resident (~170 regs) for one
-// extra shuffle + add per score.
+// Why several lanes per device: with all 64 features in one lane, u plus the
+// 64 head weights exceed the register budget and the compiler spills the
+// weights.  Three kernels share this scheme: k_greedy_cta (latency mode,
+// every trajectory in its own lane segment), k_greedy_dedup (throughput mode,
+// one warp per column plan, identical trajectories grouped) and k_greedy_big
+// (D > 16: one trajectory per CTA).
 // ======================================================================
 struct GreedyArgs {
     int traj_begin, traj_end, M, D, Tpm;
