@@ -1516,7 +1516,7 @@ ns_status launch_greedy(ns_ctx* ctx, const SearchBufs& b, const ns_tables* t, lo
         const size_t smem = sizeof(DedupSmem<L, MC>) * wpb;                                              \
         blocks = (unsigned)((x.total_warps + wpb - 1) / wpb);                                            \
         x.total_warps = (int)blocks * wpb; /* every launched warp strides the column plans */            \
-        if (smem > 48 * 1024)                                                                            \
+        if (smem + 1024 > 48 * 1024) /* + the static s_hb1 */                                           \
             cudaFuncSetAttribute(k_greedy_dedup<L, MC>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
         k_greedy_dedup<L, MC><<<blocks, wpb * 32, smem, ctx->stream>>>(a2, x);                           \
         break;                                                                                           \
