@@ -139,7 +139,10 @@ typedef struct {
  * Descriptors in pageable host memory are validated before the call returns
  * (NS_ERR_ARG); device-resident or pinned descriptors are copied directly and
  * validated on the GPU, an invalid one making the next synchronising call
- * (ns_shard_*, ns_score_plans) return NS_ERR_ARG.
+ * (ns_shard_*, ns_score_plans, ns_synchronize) return NS_ERR_ARG.  Device and
+ * pinned descriptors are read asynchronously (pinned ones on a copy stream
+ * that overlaps work already queued on the ctx stream): they must stay
+ * unchanged until the ctx stream has passed this call (ns_synchronize).
  * Requires loaded models.  *out is freed with ns_tables_free. */
 ns_status ns_featurize_tables(ns_ctx* ctx, const ns_table_desc* tables,
                               const int32_t* task_offsets, const int64_t* mem_cap,

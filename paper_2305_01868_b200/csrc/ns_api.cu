@@ -98,6 +98,41 @@ void* pinned_in_get(ns_ctx* ctx, size_t bytes) {
     return ctx->pinned_in;
 }
 
+// Pinned host -> device copy that overlaps work already queued on the ctx
+// stream: H2D on the ctx's copy stream into staging buffer i (double
+// buffered), the ctx stream waits for it and copies D2D into dst.
+static cudaError_t stage_pinned_h2d(ns_ctx* ctx, void* dst, const void* host, size_t bytes) {
+    cudaError_t e;
+    if (!ctx->copy_stream) {
+        if ((e = cudaStreamCreateWithFlags(&ctx->copy_stream, cudaStreamNonBlocking)) != cudaSuccess) return e;
+        for (int k = 0; k < 2; ++k) {
+            if ((e = cudaEventCreateWithFlags(&ctx->dstage_ready[k], cudaEventDisableTiming)) != cudaSuccess) return e;
+            if ((e = cudaEventCreateWithFlags(&ctx->dstage_free[k], cudaEventDisableTiming)) != cudaSuccess) return e;
+        }
+    }
+    const int i = ctx->dstage_i;
+    ctx->dstage_i ^= 1;
+    if (ctx->dstage_bytes[i] < bytes) {
+        if (ctx->dstage[i]) {
+            cudaEventSynchronize(ctx->dstage_free[i]);
+            cudaFree(ctx->dstage[i]);
+            ctx->dstage[i] = nullptr;
+            ctx->dstage_bytes[i] = 0;
+        }
+        const size_t want = bytes + bytes / 4 + 4096;
+        if ((e = cudaMalloc(&ctx->dstage[i], want)) != cudaSuccess) return e;
+        ctx->dstage_bytes[i] = want;
+    }
+    if ((e = cudaStreamWaitEvent(ctx->copy_stream, ctx->dstage_free[i], 0)) != cudaSuccess) return e;
+    if ((e = cudaMemcpyAsync(ctx->dstage[i], host, bytes, cudaMemcpyHostToDevice, ctx->copy_stream)) != cudaSuccess)
+        return e;
+    if ((e = cudaEventRecord(ctx->dstage_ready[i], ctx->copy_stream)) != cudaSuccess) return e;
+    if ((e = cudaStreamWaitEvent(ctx->stream, ctx->dstage_ready[i], 0)) != cudaSuccess) return e;
+    if ((e = cudaMemcpyAsync(dst, ctx->dstage[i], bytes, cudaMemcpyDeviceToDevice, ctx->stream)) != cudaSuccess)
+        return e;
+    return cudaEventRecord(ctx->dstage_free[i], ctx->stream);
+}
+
 void pinned_in_release(ns_ctx* ctx) {
     if (!ctx->pinned_in_done) cudaEventCreateWithFlags(&ctx->pinned_in_done, cudaEventDisableTiming);
     cudaEventRecord(ctx->pinned_in_done, ctx->stream);
@@ -228,6 +263,15 @@ ns_status ns_destroy(ns_ctx* ctx) {
     if (ctx->pinned_in) cudaFreeHost(ctx->pinned_in);
     if (ctx->pinned_in_done) cudaEventDestroy(ctx->pinned_in_done);
     if (ctx->d_async_flags) cudaFree(ctx->d_async_flags);
+    if (ctx->copy_stream) {
+        cudaStreamSynchronize(ctx->copy_stream);
+        cudaStreamDestroy(ctx->copy_stream);
+    }
+    for (int k = 0; k < 2; ++k) {
+        if (ctx->dstage[k]) cudaFree(ctx->dstage[k]);
+        if (ctx->dstage_ready[k]) cudaEventDestroy(ctx->dstage_ready[k]);
+        if (ctx->dstage_free[k]) cudaEventDestroy(ctx->dstage_free[k]);
+    }
     if (ctx->h_async_flags) cudaFreeHost(ctx->h_async_flags);
     prof_collect(ctx);
     for (cudaEvent_t e : ctx->prof_free) cudaEventDestroy(e);
@@ -440,10 +484,13 @@ ns_status ns_featurize_tables(ns_ctx* ctx, const ns_table_desc* tables, const in
     if ((e = cudaMemcpyAsync(t->d_cap, pin + (n_tasks + 1) * sizeof(int32_t), n_tasks * sizeof(int64_t),
                              cudaMemcpyHostToDevice, st)) != cudaSuccess)
         return fail(e);
-    if ((e = cudaMemcpyAsync(t->d_desc, direct ? (const void*)tables : (const void*)(pin + meta),
-                             n * sizeof(ns_table_desc), dev_in ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice,
-                             st)) != cudaSuccess)
+    if (pinned_in) {
+        if ((e = stage_pinned_h2d(ctx, t->d_desc, tables, n * sizeof(ns_table_desc))) != cudaSuccess) return fail(e);
+    } else if ((e = cudaMemcpyAsync(t->d_desc, dev_in ? (const void*)tables : (const void*)(pin + meta),
+                                    n * sizeof(ns_table_desc),
+                                    dev_in ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, st)) != cudaSuccess) {
         return fail(e);
+    }
     pinned_in_release(ctx);   // the staging buffer may be reused once these copies ran
     // (vdim of every row is written by the precompute of its depth before any read)
     if ((e = cudaMemsetAsync(t->d_flag, 0, sizeof(int32_t), st)) != cudaSuccess) return fail(e);

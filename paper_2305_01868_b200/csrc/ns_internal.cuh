@@ -89,6 +89,15 @@ struct ns_ctx {
     void* pinned_in = nullptr;
     size_t pinned_in_bytes = 0;
     cudaEvent_t pinned_in_done = nullptr;
+    // pinned host descriptors: H2D on a copy stream into one of two device
+    // staging buffers (overlaps the previous batch's kernels), then a D2D
+    // copy on the ctx stream
+    cudaStream_t copy_stream = nullptr;
+    void* dstage[2] = {nullptr, nullptr};
+    size_t dstage_bytes[2] = {0, 0};
+    cudaEvent_t dstage_ready[2] = {nullptr, nullptr};
+    cudaEvent_t dstage_free[2] = {nullptr, nullptr};
+    int dstage_i = 0;
     // kernel timers
     bool prof = false;
     ns::ProfEntry prof_acc[ns::PK_COUNT];

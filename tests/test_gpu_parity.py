@@ -344,6 +344,31 @@ def test_async_search_matches_sync(ns, ctx):
         tabs.free()
 
 
+def test_pinned_descriptors_overlapped_copies(ns, ctx):
+    """Pinned host descriptors go through the copy stream and two staging
+    buffers: four batches enqueued back to back (async searches, no sync in
+    between) give the same results as synchronous pageable-input runs."""
+    import torch
+    w = gen_weights(4, "mono")
+    ns.ns_load_cost_models(ctx, w)
+    batches = [gen_tasks("C2", 5 + i, start=40 + 10 * i) for i in range(4)]
+    pins, outs = [], []
+    for tasks in batches:
+        desc, off, caps = ns.table_descs(tasks)
+        pin = torch.from_numpy(desc.view(np.uint8)).pin_memory()
+        pins.append(pin)   # must outlive the asynchronous copy
+        tabs = ns.ns_featurize_tables(ctx, pin, off, caps)
+        outs.append(ns.ns_shard_tablewise(ctx, tabs, 4, M=11, async_=True))
+        tabs.free()
+    ns.ns_synchronize(ctx)
+    for tasks, out in zip(batches, outs):
+        tabs = _setup(ns, ctx, tasks, w)
+        ref = ns.ns_shard_tablewise(ctx, tabs, 4, M=11)
+        for k in ("cost", "assign", "grid_index", "n_scores"):
+            assert np.array_equal(out[k], ref[k]), k
+        tabs.free()
+
+
 def test_async_search_defers_validation_error(ns, ctx):
     """An invalid device-resident descriptor under NS_SEARCH_ASYNC: the search
     call returns, the next ns_synchronize reports NS_ERR_ARG, and the ctx keeps
