@@ -293,8 +293,8 @@ __global__ void __launch_bounds__(256) k_order_warp(SearchBufs b, TaskView tv, i
 // 64 head weights exceed the register budget and the compiler spills the
 // weights.  Three kernels share this scheme: k_greedy_cta (latency mode,
 // every trajectory in its own lane segment), k_greedy_dedup (throughput mode,
-// one warp per column plan, identical trajectories grouped) and k_greedy_big
-// (D > 16: one trajectory per CTA).
+// one warp per column plan, identical trajectories grouped) and k_greedy_wide
+// (D > 16: one trajectory per CTA, one thread per device).
 // ======================================================================
 struct GreedyArgs {
     int traj_begin, traj_end, M, D, Tpm;
@@ -1035,27 +1035,34 @@ __global__ void __launch_bounds__(128, (LPD >= 8 ? NS_DEDUP_BLOCKS8 : (LPD == 4 
     }
 }
 
-// Large D (LPD * pow2(D) > 32, e.g. C5's 128 simulated GPUs): one trajectory
-// per CTA of LPD * D threads; cross-warp argmin through shared memory
-// (double-buffered by step parity); v rows read through L1/L2 (no other
-// trajectory of the CTA would share a staged row).
-template <int LPD>
-__global__ void __launch_bounds__(512) k_greedy_big(const GreedyArgs a) {
-    constexpr int FPL = kV / LPD;
-    constexpr int SS = FPL * 8 + 16;   // ring slice stride (bytes)
-    constexpr int RS = LPD * SS;
-    constexpr int kLook = kStages - 2; // lookahead: the slot being overwritten was last read two steps ago
-    __shared__ double s_sc[2][16];
-    __shared__ int s_dv[2][16];
-    __shared__ int s_cnt[2][16];
-    __shared__ __align__(16) unsigned char ring[kStages * RS];
+// Large D (D > 16, e.g. C5's 128 simulated GPUs): one trajectory per CTA and
+// ONE thread per device holding all 64 features of u_d in registers; the head
+// weights and the staged v row are read from shared memory as broadcasts
+// (every thread of the CTA reads the same address).  A CTA is at most 4 warps
+// (D <= 128) and ~165 registers per thread, so 3 CTAs fit per SM -- the 660
+// trajectories of a C5 level run in 1.5 waves instead of 4.5 with 4 lanes per
+// device.  Cross-warp argmin: shuffle argmin per warp, the <= 4 candidates
+// through shared memory (double-buffered by step parity), reduced by every
+// thread in warp order (lowest device on ties, R13).
+__global__ void __launch_bounds__(128, 3) k_greedy_wide(const GreedyArgs a) {
+    constexpr int kLook = kStages - 2;   // the slot being overwritten was last read two steps ago
+    __shared__ __align__(16) double s_w[kV];
+    __shared__ __align__(16) double s_hb1[kV];
+    __shared__ __align__(16) double ring[kStages][kV];
+    __shared__ double s_sc[2][4];
+    __shared__ int s_dv[2][4];
+    __shared__ int s_cnt[2][4];
     __shared__ int sdt[kStages], sidx[kStages];
     __shared__ long long sbt[kStages];
     const int lane = threadIdx.x & 31, wi = threadIdx.x >> 5, nw = blockDim.x >> 5;
     const long long tau = a.traj_begin + blockIdx.x;
     if (tau >= a.traj_end) return;
+    for (int k = threadIdx.x; k < kV; k += blockDim.x) {
+        s_w[k] = a.head.H2[k];
+        s_hb1[k] = a.head.hb1[k];
+    }
     const int g = (int)(tau / a.M), m = (int)(tau % a.M);
-    const int d = threadIdx.x / LPD, part = threadIdx.x % LPD;
+    const int d = threadIdx.x;
     bool alive = a.cp_valid[g] != 0;
     int Tp = 0, capd = 0;
     long long cap = 0;
@@ -1066,8 +1073,10 @@ __global__ void __launch_bounds__(512) k_greedy_big(const GreedyArgs a) {
         capd = a.capdim[q * a.M + m];
     }
     const bool dev = d < a.D;
-    double u[FPL], w[FPL];
-    load_lane_head<FPL>(a.head, part, u, w);
+    __syncthreads();
+    double u[kV];
+#pragma unroll
+    for (int k = 0; k < kV; ++k) u[k] = s_hb1[k];
     int dsum = 0;
     long long bsum = 0;
     uint32_t work = 0;
@@ -1079,12 +1088,11 @@ __global__ void __launch_bounds__(512) k_greedy_big(const GreedyArgs a) {
     auto issue = [&](int pp) {
         if (pp < T) {
             const int r = __ldg(orow + pp);
-            unsigned char* st = ring + (pp % kStages) * RS;
-            constexpr int CPS = FPL / 2;
-            cp_async16(st + (lane / CPS) * SS + (lane % CPS) * 16, a.V + (size_t)r * kV + 2 * lane);
-            if (lane == 0) cp_async4(sdt + pp % kStages, a.vdim + r);
-            if (lane == 1) cp_async4(sidx + pp % kStages, oidx + pp);
-            if (lane == 2) cp_async8(sbt + pp % kStages, a.vbytes + r);
+            const int slot = pp % kStages;
+            cp_async16(&ring[slot][2 * lane], a.V + (size_t)r * kV + 2 * lane);
+            if (lane == 0) cp_async4(sdt + slot, a.vdim + r);
+            if (lane == 1) cp_async4(sidx + slot, oidx + pp);
+            if (lane == 2) cp_async8(sbt + slot, a.vbytes + r);
         }
         cp_async_commit();
     };
@@ -1102,15 +1110,23 @@ __global__ void __launch_bounds__(512) k_greedy_big(const GreedyArgs a) {
         const int dt = sdt[sl];
         const long long bt = sbt[sl];
         const bool f = dev && (bsum + bt <= cap) && (dsum + dt <= capd);
-        const double2* v2 = reinterpret_cast<const double2*>(ring + sl * RS + part * SS);
-        double ps = 0.0;
-        if (f) ps = part_score<FPL, true>(u, w, v2);
-        double bs = a.head.hb2 + lane_group_sum<LPD>(ps);
-        if (!f) bs = CUDART_INF;
+        const double2* v2 = reinterpret_cast<const double2*>(ring[sl]);
+        const double2* w2 = reinterpret_cast<const double2*>(s_w);
+        double bs = CUDART_INF;
+        if (f) {
+            double acc[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+            for (int k2 = 0; k2 < kV / 2; ++k2) {
+                const double2 vv = v2[k2], ww = w2[k2];
+                acc[(2 * k2) & 3] = fma(ww.x, relu_hi(u[2 * k2] + vv.x), acc[(2 * k2) & 3]);
+                acc[(2 * k2 + 1) & 3] = fma(ww.y, relu_hi(u[2 * k2 + 1] + vv.y), acc[(2 * k2 + 1) & 3]);
+            }
+            bs = a.head.hb2 + ((acc[0] + acc[1]) + (acc[2] + acc[3]));
+        }
         int bd = d;
 #pragma unroll
-        for (int o = 16; o >= LPD; o >>= 1) argmin_step(bs, bd, o);
-        const unsigned bal = __ballot_sync(kFull, f && part == 0);
+        for (int o = 16; o > 0; o >>= 1) argmin_step(bs, bd, o);
+        const unsigned bal = __ballot_sync(kFull, f);
         if (lane == 0) {
             s_sc[par][wi] = bs;
             s_dv[par][wi] = bd;
@@ -1135,16 +1151,24 @@ __global__ void __launch_bounds__(512) k_greedy_big(const GreedyArgs a) {
             break;   // uniform across the CTA
         }
         if (d == bd) {
-            part_add<FPL, true>(u, v2);
+#pragma unroll
+            for (int k2 = 0; k2 < kV / 2; ++k2) {
+                const double2 vv = v2[k2];
+                u[2 * k2] += vv.x;
+                u[2 * k2 + 1] += vv.y;
+            }
             dsum += dt;
             bsum += bt;
         }
         if (threadIdx.x == 0) asg[sidx[sl]] = (int8_t)bd;
     }
     if (wi == 0) cp_async_wait<0>();
-    const double hc = a.head.hb2 + lane_group_sum<LPD>(part_head<FPL>(u, w));
-    if (dev && part == 0) {
-        a.comp[tau * a.D + d] = dsum > 0 ? hc : 0.0;
+    if (dev) {
+        double acc[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+        for (int k = 0; k < kV; ++k) acc[k & 3] = fma(s_w[k], relu_exact(u[k]), acc[k & 3]);
+        const double hc = a.head.hb2 + ((acc[0] + acc[1]) + (acc[2] + acc[3]));
+        a.comp[tau * a.D + d] = dsum > 0 ? hc : 0.0;   // reading R4
         a.devdim[tau * a.D + d] = dsum;
     }
     if (threadIdx.x == 0) {
@@ -1536,9 +1560,9 @@ ns_status launch_greedy(ns_ctx* ctx, const SearchBufs& b, const ns_tables* t, lo
         }
         prof_end(ctx);
     } else {
-        const int threads = ((4 * b.D + 31) / 32) * 32;
+        const int threads = ((b.D + 31) / 32) * 32;
         prof_begin(ctx, PK_GREEDY);
-        k_greedy_big<4><<<(unsigned)n, threads, 0, ctx->stream>>>(a);
+        k_greedy_wide<<<(unsigned)n, threads, 0, ctx->stream>>>(a);
         prof_end(ctx);
         // no grouping: every trajectory carries its own plan
         NS_CUDA(ctx, cudaMemsetAsync(b.dup_of + tb, 0xff, (size_t)n * sizeof(int32_t), ctx->stream));
