@@ -94,7 +94,9 @@ __device__ __forceinline__ void warp_layer(const double* __restrict__ W, const d
     __syncwarp();
 }
 
-// One warp owns 16 rows.  Layers 1 and 2 (2D -> 128 -> 64) are fused over
+// Two warps own 16 rows, one per model direction (fwd / bwd run
+// concurrently: half the dependent DMMA chain per row block, which is what
+// bounds a single-task search's few hundred rows).  Layers 1 and 2 (2D -> 128 -> 64) are fused over
 // four 32-unit chunks of the 128-wide hidden layer: each chunk is staged in
 // shared memory and folded into the layer-2 accumulators (registers) at once,
 // so no 16 x 128 activation buffer is needed (15 KB per warp instead of 27 KB
@@ -105,17 +107,20 @@ __global__ void __launch_bounds__(128, 3) k_plan_cost_dmma(const PlanCostArgs a)
     const int g = lane >> 2, t = lane & 3;
     const int D = a.D, K0 = 2 * D, K0p = (K0 + 3) & ~3;
     const int ldx = a.ldx, ldh = a.ldy;
-    const int per_warp = 16 * (ldx + ldh + 2 * D) + 32;
+    const int rb = w >> 1, dir = w & 1;   // row block of the CTA, model direction
+    const int nrb = nwarps >> 1;
+    const int per_warp = 16 * (ldx + ldh);
+    const int per_rb = 16 * 2 * D + 32;
     double* X = psm + (size_t)w * per_warp;  // [16][ldx]: input, layer-2 out (64), layer-4 out (16)
     double* Hc = X + 16 * ldx;               // [16][ldh]: layer-1 chunk (32), layer-3 out (32)
-    double* O = Hc + 16 * ldh;               // [16][2D]: fwd, then bwd
+    double* O = psm + (size_t)nwarps * per_warp + (size_t)rb * per_rb;   // [16][2D]: fwd, bwd
     double* mn = O + 16 * 2 * D;             // [16] min comp per row
     long long* rid = (long long*)(mn + 16);
-    const long long base = a.row_begin + ((long long)blockIdx.x * nwarps + w) * 16;
+    const long long base = a.row_begin + ((long long)blockIdx.x * nrb + rb) * 16;
     const long long end = a.list ? a.row_begin + *a.list_n : a.row_end;
-    if (base >= end) return;
-    // row ids and per-row min comp (lane r < 16 owns row r)
-    if (lane < 16) {
+    const bool rows = base < end;
+    // row ids and per-row min comp (lane r < 16 of the fwd warp owns row r)
+    if (rows && dir == 0 && lane < 16) {
         const long long i = base + lane;
         long long r = -1;
         if (i < end) r = a.list ? (long long)a.list[i] : i;
@@ -127,8 +132,8 @@ __global__ void __launch_bounds__(128, 3) k_plan_cost_dmma(const PlanCostArgs a)
         }
         mn[lane] = m;
     }
-    __syncwarp();
-    for (int dir = 0; dir < 2; ++dir) {
+    __syncthreads();
+    if (rows) {
         // input rows [starts / start_scale (D), devdim / dim_scale (D)], zero padded
         for (int i = lane; i < 16 * K0p; i += 32) {
             const int r = i / K0p, c = i % K0p;
@@ -216,7 +221,8 @@ __global__ void __launch_bounds__(128, 3) k_plan_cost_dmma(const PlanCostArgs a)
         warp_layer<true>(a.cp.W[dir][3], a.cp.b[dir][3], 32, 16, Hc, ldh, X, ldx, lane);
         warp_layer<false>(a.cp.W[dir][4], a.cp.b[dir][4], 16, D, X, ldx, O + dir * D, 2 * D, lane);
     }
-    if (lane < 16) {
+    __syncthreads();
+    if (rows && dir == 0 && lane < 16) {
         const long long row = rid[lane];
         if (row >= 0) {
             double c = CUDART_INF;
@@ -447,13 +453,14 @@ ns_status launch_plan_cost(ns_ctx* ctx, long long rb, long long re, const uint8_
     const int K0p = (2 * a.D + 3) & ~3;
     a.ldx = ld_pad(K0p > 64 ? K0p : 64);
     a.ldy = ld_pad(32);
-    const size_t per_warp = (size_t)(16 * (a.ldx + a.ldy + 2 * a.D) + 32) * sizeof(double);
-    int wpb = 4;
-    while (wpb > 1 && per_warp * wpb > 72 * 1024) wpb >>= 1;
-    const size_t smem = per_warp * wpb;
+    const size_t per_warp = (size_t)16 * (a.ldx + a.ldy) * sizeof(double);
+    const size_t per_rb = (size_t)(16 * 2 * a.D + 32) * sizeof(double);
+    int wpb = 4;   // warps per CTA: two per 16-row block (fwd, bwd)
+    while (wpb > 2 && per_warp * wpb + per_rb * (wpb / 2) > 72 * 1024) wpb >>= 1;
+    const size_t smem = per_warp * wpb + per_rb * (wpb / 2);
     cudaFuncSetAttribute(k_plan_cost_dmma, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     const long long rows = re - rb;
-    const long long blocks = (rows + 16LL * wpb - 1) / (16LL * wpb);
+    const long long blocks = (rows + 8LL * wpb - 1) / (8LL * wpb);   // 16 rows per warp pair
     prof_begin(ctx, PK_FINALIZE);
     k_plan_cost_dmma<<<(unsigned)blocks, wpb * 32, smem, ctx->stream>>>(a);
     prof_end(ctx);
