@@ -73,16 +73,8 @@ struct TaskView {   // read-only table arrays of the batch
 // ---------------------------------------------------------------- helpers
 // Post-split table list of a column plan: entry i is a variant row
 // (table g, depth j) = g * kDepth + j.  The first half stays at c_i, the
-// second is appended.  Built by one thread into shared memory.
-__device__ void build_rows(const TaskView& tv, int q, const int32_t* plan, int len, int32_t* rows) {
-    const int base = tv.off[q], T = tv.off[q + 1] - base;
-    for (int i = 0; i < T; ++i) rows[i] = (base + i) * kDepth;
-    for (int k = 0; k < len; ++k) {
-        const int c = plan[k];
-        rows[c] += 1;
-        rows[T + k] = rows[c];
-    }
-}
+// second is appended.  Every kernel that needs the list builds it in shared
+// memory: rows in parallel, then the splits in plan order by one thread.
 
 // ======================================================================
 // Level setup kernels
@@ -112,7 +104,9 @@ __global__ void k_expand(SearchBufs b, TaskView tv, int level) {
     const int plen = level - 1;
     const int T = tv.off[q + 1] - tv.off[q];
     const int Tp = T + plen;
-    int32_t* rows = sh;                 // [Tp]
+    double* keyc = (double*)sh;                         // [Tpm] single cost of entry i
+    long long* keyb = (long long*)(keyc + b.Tpm);       // [Tpm] bytes of entry i
+    int32_t* rows = (int32_t*)(keyb + b.Tpm);           // [Tpm]
     int32_t* selc = rows + b.Tpm;       // [N] by cost rank -> index
     int32_t* sels = selc + b.N2;        // [N] by size rank -> index
     __shared__ int ncand;
@@ -121,24 +115,124 @@ __global__ void k_expand(SearchBufs b, TaskView tv, int level) {
         return;
     }
     const int32_t* pplan = b.beam_plan + ((size_t)q * b.K + bb) * b.Lcap;
-    if (threadIdx.x == 0) build_rows(tv, q, pplan, plen, rows);
+    {   // post-split table list, built in parallel then split in order
+        const int base = tv.off[q];
+        for (int i = threadIdx.x; i < T; i += blockDim.x) rows[i] = (base + i) * kDepth;
+        __syncthreads();
+        if (threadIdx.x == 0)
+            for (int k = 0; k < plen; ++k) {
+                const int c = pplan[k];
+                rows[c] += 1;
+                rows[T + k] = rows[c];
+            }
+    }
     const int N = b.N2 / 2;
     for (int j = threadIdx.x; j < b.N2; j += blockDim.x) selc[j] = sels[j] = -1;
     __syncthreads();
     for (int i = threadIdx.x; i < Tp; i += blockDim.x) {
-        const double ci = tv.C[rows[i]];
-        const long long bi = tv.vbytes[rows[i]];
-        int rc = 0, rs = 0;
-        for (int k = 0; k < Tp; ++k) {
-            const double ck = tv.C[rows[k]];
-            const long long bk = tv.vbytes[rows[k]];
-            rc += (ck > ci) || (ck == ci && k < i);
-            rs += (bk > bi) || (bk == bi && k < i);
-        }
-        if (rc < N) selc[rc] = i;
-        if (rs < N) sels[rs] = i;
+        keyc[i] = tv.C[rows[i]];
+        keyb[i] = tv.vbytes[rows[i]];
     }
     __syncthreads();
+    if (Tp <= 256) {
+        // short lists: ranks by counting, stopped once both reach N
+        for (int i = threadIdx.x; i < Tp; i += blockDim.x) {
+            const double ci = keyc[i];
+            const long long bi = keyb[i];
+            int rc = 0, rs = 0;
+            for (int k = 0; k < Tp && (rc < N || rs < N); ++k) {
+                const double ck = keyc[k];
+                const long long bk = keyb[k];
+                rc += (ck > ci) || (ck == ci && k < i);
+                rs += (bk > bi) || (bk == bi && k < i);
+            }
+            if (rc < N) selc[rc] = i;
+            if (rs < N) sels[rs] = i;
+        }
+        __syncthreads();
+    }
+    // long lists -- top-N by cost and top-N by bytes: N rounds of a block-wide
+    // argmax; round r takes the largest entry below round r-1's pick in the
+    // total order (key descending, list index ascending), nothing is marked
+    __shared__ double s_kc[32];
+    __shared__ long long s_kb[32];
+    __shared__ int s_ic[32], s_ib[32];
+    double pc = CUDART_INF;   // previous picks (+inf / INT_MIN: nothing picked yet)
+    long long pb = LLONG_MAX;
+    int pic = -1, pib = -1;
+    const int lane = threadIdx.x & 31, wi = threadIdx.x >> 5, nwarp = blockDim.x >> 5;
+    for (int r = 0; r < (Tp > 256 ? N : 0); ++r) {
+        double bc = -CUDART_INF;
+        long long bbv = LLONG_MIN;
+        int ic = -1, ib = -1;
+        for (int i = threadIdx.x; i < Tp; i += blockDim.x) {
+            const double ci = keyc[i];
+            const long long bi = keyb[i];
+            // eligible: strictly after the previous pick in (key desc, index asc)
+            const bool ec = ci < pc || (ci == pc && i > pic);
+            const bool eb = bi < pb || (bi == pb && i > pib);
+            if (ec && (ic < 0 || ci > bc || (ci == bc && i < ic))) {
+                bc = ci;
+                ic = i;
+            }
+            if (eb && (ib < 0 || bi > bbv || (bi == bbv && i < ib))) {
+                bbv = bi;
+                ib = i;
+            }
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            const double oc = __shfl_xor_sync(kFull, bc, o);
+            const int oic = __shfl_xor_sync(kFull, ic, o);
+            const long long ob = __shfl_xor_sync(kFull, bbv, o);
+            const int oib = __shfl_xor_sync(kFull, ib, o);
+            if (oic >= 0 && (ic < 0 || oc > bc || (oc == bc && oic < ic))) {
+                bc = oc;
+                ic = oic;
+            }
+            if (oib >= 0 && (ib < 0 || ob > bbv || (ob == bbv && oib < ib))) {
+                bbv = ob;
+                ib = oib;
+            }
+        }
+        if (lane == 0) {
+            s_kc[wi] = bc;
+            s_ic[wi] = ic;
+            s_kb[wi] = bbv;
+            s_ib[wi] = ib;
+        }
+        __syncthreads();
+        bc = -CUDART_INF;
+        bbv = LLONG_MIN;
+        ic = ib = -1;
+        for (int k = 0; k < nwarp; ++k) {   // every thread reduces the warp winners (same order)
+            if (s_ic[k] >= 0 && (ic < 0 || s_kc[k] > bc || (s_kc[k] == bc && s_ic[k] < ic))) {
+                bc = s_kc[k];
+                ic = s_ic[k];
+            }
+            if (s_ib[k] >= 0 && (ib < 0 || s_kb[k] > bbv || (s_kb[k] == bbv && s_ib[k] < ib))) {
+                bbv = s_kb[k];
+                ib = s_ib[k];
+            }
+        }
+        if (threadIdx.x == 0) {
+            selc[r] = ic;
+            sels[r] = ib;
+        }
+        pc = bc;
+        pic = ic;
+        pb = bbv;
+        pib = ib;
+        if (ic < 0) {   // fewer than N entries: later rounds select nothing
+            pc = -CUDART_INF;
+            pic = INT_MAX;
+        }
+        if (ib < 0) {
+            pb = LLONG_MIN;
+            pib = INT_MAX;
+        }
+        __syncthreads();
+    }
     if (threadIdx.x == 0) {
         int n = 0;
         int32_t* cand = sels + b.N2;    // [2N]
@@ -176,30 +270,65 @@ __global__ void k_expand(SearchBufs b, TaskView tv, int level) {
 
 // Alg. 2 lines 2-3: build the T' column-sharded tables and
 // sort them by descending predicted single-table cost, ties by list index
-// (reading R13).  Rank sort: rank_i = #{k : (-C_k, k) < (-C_i, i)}; fp64 keys.
+// (reading R13): ascending order of the distinct keys (-C_i, i), fp64.  Long
+// lists (T' > 256): one CTA per column plan, bitonic sort in shared memory
+// over the next power of two (padding keys (+inf, INT_MAX) sort last).
+__host__ __device__ inline int pow2_ceil(int x) {
+    int n = 1;
+    while (n < x) n <<= 1;
+    return n;
+}
+
 __global__ void k_build_order(SearchBufs b, TaskView tv) {
-    extern __shared__ int32_t sh[];
+    extern __shared__ __align__(16) unsigned char bsm[];
     const int g = blockIdx.x;
     if (!b.cp_valid[g]) return;
     const int q = b.cp_task[g];
     const int len = b.cp_len[g];
-    const int Tp = tv.off[q + 1] - tv.off[q] + len;
-    int32_t* rows = sh;
-    double* key = (double*)(sh + ((b.Tpm + 1) & ~1));
+    const int base = tv.off[q], T = tv.off[q + 1] - base;
+    const int Tp = T + len;
+    const int n = pow2_ceil(b.Tpm);
+    double* key = (double*)bsm;              // [n]  -C
+    int32_t* id = (int32_t*)(key + n);       // [n]  list index
+    int32_t* rows = id + n;                  // [Tpm]
+    for (int i = threadIdx.x; i < T; i += blockDim.x) rows[i] = (base + i) * kDepth;
+    __syncthreads();
     if (threadIdx.x == 0) {
-        build_rows(tv, q, b.cp_plan + (size_t)g * b.Lcap, len, rows);
+        const int32_t* plan = b.cp_plan + (size_t)g * b.Lcap;
+        for (int k = 0; k < len; ++k) {   // halve c_k in place, append the other half
+            const int c = plan[k];
+            rows[c] += 1;
+            rows[T + k] = rows[c];
+        }
         b.cp_Tp[g] = Tp;
     }
     __syncthreads();
-    for (int i = threadIdx.x; i < Tp; i += blockDim.x) key[i] = tv.C[rows[i]];
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+        key[i] = i < Tp ? -tv.C[rows[i]] : CUDART_INF;
+        id[i] = i < Tp ? i : INT_MAX;
+    }
     __syncthreads();
-    for (int i = threadIdx.x; i < Tp; i += blockDim.x) {
-        const double ci = key[i];
-        int r = 0;
-        for (int k = 0; k < Tp; ++k) {
-            const double ck = key[k];
-            r += (ck > ci) || (ck == ci && k < i);
+    for (int k = 2; k <= n; k <<= 1) {
+        for (int j = k >> 1; j > 0; j >>= 1) {
+            for (int i = threadIdx.x; i < n; i += blockDim.x) {
+                const int ixj = i ^ j;
+                if (ixj > i) {
+                    const double ka = key[i], kb = key[ixj];
+                    const int ia = id[i], ib = id[ixj];
+                    const bool a_gt_b = ka > kb || (ka == kb && ia > ib);
+                    if (((i & k) == 0) == a_gt_b) {   // ascending block: out of order if a > b
+                        key[i] = kb;
+                        key[ixj] = ka;
+                        id[i] = ib;
+                        id[ixj] = ia;
+                    }
+                }
+            }
+            __syncthreads();
         }
+    }
+    for (int r = threadIdx.x; r < Tp; r += blockDim.x) {
+        const int i = id[r];
         b.ord_row[(size_t)g * b.Tpm + r] = rows[i];
         b.ord_idx[(size_t)g * b.Tpm + r] = i;
     }
@@ -1231,51 +1360,110 @@ __global__ void __launch_bounds__(256) k_select0(SearchBufs b) {
     }
 }
 
-__global__ void k_select(SearchBufs b, int C, int level, int Kbeam) {
+__global__ void __launch_bounds__(256) k_select(SearchBufs b, int C, int level, int Kbeam, int staged) {
     extern __shared__ unsigned char ssm[];
     const int q = blockIdx.x;
+    const int lane = threadIdx.x & 31, wi = threadIdx.x >> 5, nw = blockDim.x >> 5;
     double* ccost = (double*)ssm;                    // [C]
     int32_t* cm = (int32_t*)(ccost + C);             // [C]
     int32_t* cval = cm + C;                          // [C]
-    __shared__ unsigned long long s_work;
-    __shared__ int s_best;
-    if (threadIdx.x == 0) s_work = 0;
-    __syncthreads();
+    double* tc = (double*)(cval + C + (C & 1));      // [C][M] trajectory costs (staged mode)
+    __shared__ unsigned long long s_work[32];
+    __shared__ double s_bc[32];
+    __shared__ int s_bj[32], s_nv[32];
+    __shared__ int s_best, s_nvalid;
+    // ---- grid argmin of every child column plan: one warp per child, lanes over m
     unsigned long long wsum = 0;
-    for (int j = threadIdx.x; j < C; j += blockDim.x) {
+    if (staged) {
+        // every (child, m) cost gathered in parallel first (the dependent
+        // dup_of -> tcost loads of all trajectories in flight at once)
+        const long long t0 = (long long)q * C * b.M;
+        for (int e = threadIdx.x; e < C * b.M; e += blockDim.x) {
+            const long long tau = t0 + e;
+            double c = CUDART_INF;
+            if (b.cp_valid[q * C + e / b.M]) {
+                wsum += b.work[tau];
+                const long long src = b.dup_of[tau] >= 0 ? (long long)b.dup_of[tau] : tau;
+                if (b.feas[tau]) c = b.tcost[src];
+            }
+            tc[e] = c;
+        }
+        __syncthreads();
+    }
+    double wbc = CUDART_INF;   // this warp's lexicographic (cost, generation) minimum over valid children
+    int wbj = INT_MAX, wnv = 0;
+    for (int j = wi; j < C; j += nw) {
         const int g = q * C + j;
         const int v = b.cp_valid[g];
         double best = CUDART_INF;
-        int bm = -1;
+        int bm = INT_MAX;
         if (v) {
-            for (int m = 0; m < b.M; ++m) {
-                const long long tau = (long long)g * b.M + m;
-                wsum += b.work[tau];
-                const long long src = b.dup_of[tau] >= 0 ? (long long)b.dup_of[tau] : tau;
-                const double c = b.feas[tau] ? b.tcost[src] : CUDART_INF;
-                if (c < best) {
+            for (int m = lane; m < b.M; m += 32) {
+                double c;
+                if (staged) {
+                    c = tc[j * b.M + m];
+                } else {
+                    const long long tau = (long long)g * b.M + m;
+                    wsum += b.work[tau];
+                    const long long src = b.dup_of[tau] >= 0 ? (long long)b.dup_of[tau] : tau;
+                    c = b.feas[tau] ? b.tcost[src] : CUDART_INF;
+                }
+                if (c < best) {   // m increases per lane: strict < keeps the lowest m
                     best = c;
                     bm = m;
                 }
             }
         }
-        ccost[j] = best;
-        cm[j] = bm;
-        cval[j] = v;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            const double ob = __shfl_xor_sync(kFull, best, o);
+            const int om = __shfl_xor_sync(kFull, bm, o);
+            if (ob < best || (ob == best && om < bm)) {
+                best = ob;
+                bm = om;
+            }
+        }
+        if (best == CUDART_INF) bm = -1;
+        if (lane == 0) {
+            ccost[j] = best;
+            cm[j] = bm;
+            cval[j] = v;
+        }
+        if (v) {
+            ++wnv;
+            if (best < wbc || (best == wbc && j < wbj)) {
+                wbc = best;
+                wbj = j;
+            }
+        }
     }
-    atomicAdd(&s_work, wsum);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) wsum += __shfl_xor_sync(kFull, wsum, o);
+    if (lane == 0) {
+        s_work[wi] = wsum;
+        s_bc[wi] = wbc;
+        s_bj[wi] = wbj;
+        s_nv[wi] = wnv;
+    }
     __syncthreads();
     if (threadIdx.x == 0) {
-        b.n_scores[q] += s_work;
+        unsigned long long work = 0;
+        int arg = INT_MAX, nvalid = 0;
+        double ac = CUDART_INF;
+        for (int k = 0; k < nw; ++k) {
+            work += s_work[k];
+            nvalid += s_nv[k];
+            if (s_bj[k] != INT_MAX && (s_bc[k] < ac || (s_bc[k] == ac && s_bj[k] < arg))) {
+                ac = s_bc[k];
+                arg = s_bj[k];
+            }
+        }
+        b.n_scores[q] += work;
+        s_nvalid = nvalid;
         // lexicographic (cost, gen) minimum of the level == the first strict
         // improvement in generation order
-        int arg = -1;
-        for (int j = 0; j < C; ++j) {
-            if (!cval[j]) continue;
-            if (arg < 0 || ccost[j] < ccost[arg]) arg = j;
-        }
         s_best = -1;
-        if (arg >= 0 && (level == 0 || ccost[arg] < b.best_cost[q])) {
+        if (arg != INT_MAX && (level == 0 || ccost[arg] < b.best_cost[q])) {
             // level 0 always installs [] as the initial global best (R15)
             s_best = arg;
             b.best_cost[q] = ccost[arg];
@@ -1291,32 +1479,32 @@ __global__ void k_select(SearchBufs b, int C, int level, int Kbeam) {
         const int g = q * C + s_best;
         const int Tp = b.cp_Tp[g];
         const int mm = cm[s_best];
-        for (int i = threadIdx.x; i < b.Tpm; i += blockDim.x) {
-            int8_t v = -1;
-            if (mm >= 0 && i < Tp) {
-                const long long tau = (long long)g * b.M + mm;
-                const long long src = b.dup_of[tau] >= 0 ? (long long)b.dup_of[tau] : tau;
-                v = b.assign[src * b.Tpm + i];
-            }
-            b.best_assign[(size_t)q * b.Tpm + i] = v;
+        long long src = -1;
+        if (mm >= 0) {
+            const long long tau = (long long)g * b.M + mm;
+            src = b.dup_of[tau] >= 0 ? (long long)b.dup_of[tau] : tau;
         }
+        for (int i = threadIdx.x; i < b.Tpm; i += blockDim.x)
+            b.best_assign[(size_t)q * b.Tpm + i] = (src >= 0 && i < Tp) ? b.assign[src * b.Tpm + i] : (int8_t)-1;
     }
     if (level > 0) {
-        // next beam: rank among valid children by (cost, gen)
-        int nvalid = 0;
-        for (int j = 0; j < C; ++j) nvalid += cval[j];
-        for (int j = threadIdx.x; j < C; j += blockDim.x) {
+        // next beam: rank among valid children by (cost, gen); one warp per child
+        for (int j = wi; j < C; j += nw) {
             if (!cval[j]) continue;
+            const double cj = ccost[j];
             int r = 0;
-            for (int k = 0; k < C; ++k)
-                if (cval[k] && (ccost[k] < ccost[j] || (ccost[k] == ccost[j] && k < j))) ++r;
+            for (int k0 = 0; k0 < C; k0 += 32) {
+                const int k = k0 + lane;
+                const bool less = k < C && cval[k] && (ccost[k] < cj || (ccost[k] == cj && k < j));
+                r += __popc(__ballot_sync(kFull, less));
+            }
             if (r < Kbeam) {
                 const int g = q * C + j;
-                for (int k = 0; k < level; ++k)
+                for (int k = lane; k < level; k += 32)
                     b.beam_plan[((size_t)q * b.K + r) * b.Lcap + k] = b.cp_plan[(size_t)g * b.Lcap + k];
             }
         }
-        if (threadIdx.x == 0) b.beam_cnt[q] = nvalid < Kbeam ? nvalid : Kbeam;
+        if (threadIdx.x == 0) b.beam_cnt[q] = s_nvalid < Kbeam ? s_nvalid : Kbeam;
     }
 }
 
@@ -1735,11 +1923,9 @@ ns_status run_search(ns_ctx* ctx, const ns_tables* t, int D, const ns_search_par
     carve(cv, b, o, Lout > 0 ? Lout : 1);
     ns_status s;
     const TaskView tv = task_view(t);
-    const size_t osm = order_smem(b.Tpm);
-    if (osm > 48 * 1024) {
-        cudaFuncSetAttribute(k_build_order, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)osm);
-        cudaFuncSetAttribute(k_expand, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)osm);
-    }
+    const size_t osm = order_smem(b.Tpm);                                        // per warp (k_order_warp)
+    const size_t bsm = (size_t)pow2_ceil(b.Tpm) * 12 + (size_t)b.Tpm * 4 + 16;   // k_build_order
+    if (bsm > 48 * 1024) cudaFuncSetAttribute(k_build_order, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bsm);
     // short lists: one warp per column plan (8 per CTA); long lists: one CTA
     const bool warp_order = b.Tpm <= 256;
     const size_t wsm = 8 * osm;
@@ -1749,7 +1935,7 @@ ns_status run_search(ns_ctx* ctx, const ns_tables* t, int D, const ns_search_par
             const unsigned blocks = (unsigned)std::max(1, std::min((n_cp + 7) / 8, ctx->sm_count * 8));
             k_order_warp<<<blocks, 256, wsm, ctx->stream>>>(b, tv, n_cp, level0, t->d_sumdim, p->grid_hi_factor);
         } else {
-            k_build_order<<<n_cp, 256, osm, ctx->stream>>>(b, tv);
+            k_build_order<<<n_cp, 512, bsm, ctx->stream>>>(b, tv);
         }
         prof_end(ctx);
         NS_LAUNCHED(ctx);
@@ -1772,7 +1958,7 @@ ns_status run_search(ns_ctx* ctx, const ns_tables* t, int D, const ns_search_par
     NS_LAUNCHED(ctx);
     // ---- beam levels (Alg. 1 lines 6-22)
     for (int level = 1; level <= L; ++level) {
-        const size_t esm = (size_t)b.Tpm * 4 + (size_t)b.N2 * 4 * 2 + (size_t)b.N2 * 4 + 64;
+        const size_t esm = (size_t)b.Tpm * 20 + (size_t)b.N2 * 4 * 2 + (size_t)b.N2 * 4 + 64;
         if (esm > 48 * 1024)
             cudaFuncSetAttribute(k_expand, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)esm);
         prof_begin(ctx, PK_EXPAND);
@@ -1782,7 +1968,11 @@ ns_status run_search(ns_ctx* ctx, const ns_tables* t, int D, const ns_search_par
         launch_order(b.S, 0);
         if ((s = run_level_trajectories(ctx, b, t, b.S)) != NS_OK) return s;
         prof_begin(ctx, PK_SELECT);
-        k_select<<<b.n_tasks, 128, (size_t)C * 16, ctx->stream>>>(b, C, level, b.K);
+        size_t ssel = (size_t)C * 16 + 8;
+        const int staged = ssel + (size_t)C * b.M * 8 <= 160 * 1024 ? 1 : 0;
+        if (staged) ssel += (size_t)C * b.M * 8;
+        if (ssel > 40 * 1024) cudaFuncSetAttribute(k_select, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ssel);
+        k_select<<<b.n_tasks, 256, ssel, ctx->stream>>>(b, C, level, b.K, staged);
         prof_end(ctx);
         NS_LAUNCHED(ctx);
     }
