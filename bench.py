@@ -356,6 +356,7 @@ def main():
     secondary = None
     if rank == 0 and not args.no_secondary and not args.profile_run:
         secondary = search_latency(ns, ctx, torch)
+        secondary["score_plans"] = score_plans_rate(ns, ctx, torch)
 
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": "scores/s", "n_gpus": world, "steps": args.steps,
@@ -400,6 +401,63 @@ def search_latency(ns, ctx, torch):
             scores = int(out["n_scores"][0])
         t = float(np.median(times[1:]))
         res[cfg] = {"mode": mode, "search_ms_per_task": 1e3 * t, "scores": scores, "scores_per_s": scores / t}
+    return res
+
+
+def score_plans_rate(ns, ctx, torch):
+    """ns_score_plans (the simulator as a service) on 2^20 explicit
+    random plans of one C3 task (T = 80, D = 8), device-resident assignments,
+    in both modes, with each stage against its own ceiling: pooling (N2) =
+    T x 64 DADD + D x 64 (head) per plan on the FP64 pipe; comm MLPs (N5) =
+    2 x 25856 MAC per plan on the FP64 tensor cores (DMMA, measured 37.1
+    TFLOP/s, tools/fp64_peak.cu) or, split-TF32x3 on tcgen05, 3 x that on the
+    TF32 tensor peak (MEASURED_PEAKS bf16 / 2)."""
+    from workload.synth import gen_plans, gen_task
+    c = CONFIGS["C3"]
+    D = c["D"]
+    w = gen_weights(D, "mono")
+    ns.ns_load_cost_models(ctx, w)
+    task = gen_task("C3", 0)
+    desc, off, caps = ns.table_descs([task])
+    tabs = ns.ns_featurize_tables(ctx, desc, off, caps)
+    P = 1 << 20
+    T = task.T
+    A = torch.from_numpy(gen_plans(T, D, P, seed=1)).cuda()
+    cost = torch.zeros(P, dtype=torch.float64, device="cuda")
+    mlp_flop = 2.0 * 2 * (2 * D * 128 + 128 * 64 + 64 * 32 + 32 * 16 + 16 * D)
+    pool_flop = T * 64 + D * 64 * 3
+    clock = 1965e6
+    fp64_pipe = 148 * 64 * clock          # DADD/s
+    peaks = {}
+    try:
+        peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        pass
+    tf32_peak = peaks.get("bf16_tflops", 2250.0) / 2 * 1e12
+    res = {"workload": f"C3 task, T={T}, D={D}, {P} random plans (device-resident int8 assignments)"}
+    for mode, name in ((ns.NS_SCORE_FP64, "fp64"), (ns.NS_SCORE_TF32X3, "tf32x3")):
+        ns.ns_score_plans(ctx, tabs, 0, D, [], A, mode=mode, cost_out=cost)
+        torch.cuda.synchronize()
+        reps = 5
+        ns.ns_profile(ctx, True)
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        for _ in range(reps):
+            ns.ns_score_plans(ctx, tabs, 0, D, [], A, mode=mode, cost_out=cost)
+        b.record()
+        torch.cuda.synchronize()
+        ms = a.elapsed_time(b) / reps
+        pool_ms = ns.ns_profile_query(ctx, "score")[0] / reps
+        mlp_ms = ns.ns_profile_query(ctx, "finalize")[0] / reps
+        ns.ns_profile(ctx, False)
+        mlp_peak = 37.1e12 if name == "fp64" else tf32_peak
+        mlp_work = mlp_flop if name == "fp64" else 3 * mlp_flop
+        res[name] = {"plans_per_s": P / (ms * 1e-3), "ms_per_call": ms, "pool_ms": pool_ms, "mlp_ms": mlp_ms,
+                     "pool_frac_fp64_pipe": P * pool_flop / (pool_ms * 1e-3) / fp64_pipe,
+                     "mlp_tflops": P * mlp_work / (mlp_ms * 1e-3) / 1e12,
+                     "mlp_frac": P * mlp_work / (mlp_ms * 1e-3) / mlp_peak,
+                     "hbm_gbs": (P * T + P * 8) / (ms * 1e-3) / 1e9}
+    tabs.free()
     return res
 
 
