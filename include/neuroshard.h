@@ -230,8 +230,9 @@ ns_status ns_shard_tablewise(ns_ctx* ctx, const ns_tables* tables, int32_t D,
 /* Column-wise + table-wise sharding: BeamSearch (Alg. 1) over
  * column plans with GreedyGridSearch as the inner loop; the empty plan is
  * evaluated first (reading R15).  After ns_comm_init, each level's
- * trajectories are partitioned over the ranks and exchanged with one NCCL
- * allgather of packed keys; every rank returns identical results. */
+ * trajectories are partitioned over the ranks and the per-trajectory results
+ * (cost, feasibility, work, duplicate link, assignment) are exchanged with
+ * in-place NCCL allgathers; every rank returns identical results. */
 ns_status ns_shard_columnwise(ns_ctx* ctx, const ns_tables* tables, int32_t D,
                               const ns_search_params* params, ns_plan_batch* out);
 

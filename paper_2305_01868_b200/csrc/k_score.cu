@@ -212,6 +212,26 @@ __global__ void k_argmin_final(const BestRec* in, int n, BestRec* out) {
     out->idx = bi;
 }
 
+// Packed keys of the cross-rank argmin (stage 0: cost key, stage 1: index
+// key, stage 2: unpack the global winner into *best).
+__device__ __forceinline__ uint64_t order_key(double c) {   // monotone map double -> u64
+    const uint64_t u = (uint64_t)__double_as_longlong(c);
+    return (u >> 63) ? ~u : (u | 0x8000000000000000ull);
+}
+__global__ void k_rank_key(BestRec* best, uint64_t* key, int stage) {
+    if (threadIdx.x != 0) return;
+    if (stage == 0) {
+        key[0] = order_key(best->cost);
+    } else if (stage == 1) {
+        key[1] = order_key(best->cost) == key[0] ? (uint64_t)best->idx : ~0ull;
+    } else {
+        const uint64_t k = key[0];
+        const uint64_t u = (k >> 63) ? (k & 0x7fffffffffffffffull) : ~k;
+        best->cost = __longlong_as_double((long long)u);
+        best->idx = (long long)key[1];
+    }
+}
+
 ns_status run_score_plans(ns_ctx* ctx, const ns_tables* t, int task, int D, const int32_t* col_plan, int n_col,
                           const int8_t* assign, int64_t P, int mode, double* cost_out, int64_t* best_index_out,
                           double* best_cost_out) {
@@ -328,12 +348,21 @@ ns_status run_score_plans(ns_ctx* ctx, const ns_tables* t, int task, int D, cons
     k_argmin_final<<<1, 32, 0, ctx->stream>>>(d_part, nblk_arg, d_best);
     prof_end(ctx);
     NS_LAUNCHED(ctx);
-    ns_status s = comm_allgather(ctx, d_best, d_all, sizeof(BestRec));
-    if (s != NS_OK) return s;
-    prof_begin(ctx, PK_OTHER);
-    k_argmin_final<<<1, 32, 0, ctx->stream>>>(d_all, R, d_best);
-    prof_end(ctx);
-    NS_LAUNCHED(ctx);
+    if (ctx->nranks > 1) {   // (emulated ranks run the key stages with a no-op reduction)
+        // global argmin over ranks: exact two-key NCCL allreduce-min -- first
+        // the order-preserving 64-bit image of the best cost, then the lowest
+        // plan index among the ranks holding that cost (lowest index on ties)
+        uint64_t* d_key = reinterpret_cast<uint64_t*>(d_all);
+        k_rank_key<<<1, 32, 0, ctx->stream>>>(d_best, d_key, 0);
+        NS_LAUNCHED(ctx);
+        ns_status s = comm_allreduce_min_u64(ctx, d_key, 1);
+        if (s != NS_OK) return s;
+        k_rank_key<<<1, 32, 0, ctx->stream>>>(d_best, d_key, 1);
+        NS_LAUNCHED(ctx);
+        if ((s = comm_allreduce_min_u64(ctx, d_key + 1, 1)) != NS_OK) return s;
+        k_rank_key<<<1, 32, 0, ctx->stream>>>(d_best, d_key, 2);
+        NS_LAUNCHED(ctx);
+    }
     if (cost_out && pe > pb)
         NS_CUDA(ctx, cudaMemcpyAsync(cost_out + pb, d_cost + pb, (size_t)(pe - pb) * 8, cudaMemcpyDefault,
                                      ctx->stream));
