@@ -34,7 +34,7 @@ struct SearchBufs {
     int32_t* cp_plan;    // [S][Lcap]
     int32_t* cp_Tp;
     int32_t* ord_row;    // [S][Tpm]  variant row of the p-th table in cost order
-    int32_t* ord_idx;    // [S][Tpm]  its index in the post-split table list
+    int4* ord_meta;      // [S][Tpm]  {dim, list index, bytes lo, bytes hi} of the p-th table (grouped greedy stream)
     // per traj
     int8_t* assign;      // [n_traj][Tpm]
     double* comp;        // [n_traj][D]
@@ -279,6 +279,13 @@ __host__ __device__ inline int pow2_ceil(int x) {
     return n;
 }
 
+// One 16-byte record per cost-order position: the grouped greedy stages it
+// with a single copy instead of three gathers (dim, list index, bytes).
+__device__ __forceinline__ int4 pack_meta(const TaskView& tv, int row, int i) {
+    const unsigned long long by = (unsigned long long)tv.vbytes[row];
+    return make_int4(tv.vdim[row], i, (int)(unsigned)(by & 0xffffffffull), (int)(unsigned)(by >> 32));
+}
+
 __global__ void k_build_order(SearchBufs b, TaskView tv) {
     extern __shared__ __align__(16) unsigned char bsm[];
     const int g = blockIdx.x;
@@ -330,7 +337,7 @@ __global__ void k_build_order(SearchBufs b, TaskView tv) {
     for (int r = threadIdx.x; r < Tp; r += blockDim.x) {
         const int i = id[r];
         b.ord_row[(size_t)g * b.Tpm + r] = rows[i];
-        b.ord_idx[(size_t)g * b.Tpm + r] = i;
+        b.ord_meta[(size_t)g * b.Tpm + r] = pack_meta(tv, rows[i], i);
     }
 }
 
@@ -399,7 +406,7 @@ __global__ void __launch_bounds__(256) k_order_warp(SearchBufs b, TaskView tv, i
                 r += (ck > ci) || (ck == ci && k < i);
             }
             b.ord_row[(size_t)g * b.Tpm + r] = rows[i];
-            b.ord_idx[(size_t)g * b.Tpm + r] = i;
+            b.ord_meta[(size_t)g * b.Tpm + r] = pack_meta(tv, rows[i], i);
         }
         __syncwarp();
     }
@@ -432,7 +439,7 @@ struct GreedyArgs {
     const int32_t* cp_task;
     const int32_t* cp_Tp;
     const int32_t* ord_row;
-    const int32_t* ord_idx;
+    const int4* ord_meta;
     const int32_t* capdim;
     const int64_t* cap;
     const double* V;
@@ -577,7 +584,7 @@ __global__ void __launch_bounds__(256) k_greedy_cta(const GreedyArgs a, int mchu
     long long bsum = 0;
     uint32_t work = 0;
     const int32_t* orow = a.ord_row + (size_t)g * a.Tpm;
-    const int32_t* oidx = a.ord_idx + (size_t)g * a.Tpm;
+    const int4* ometa = a.ord_meta + (size_t)g * a.Tpm;
     int8_t* asg = a.assign + (size_t)(in_range ? tau : 0) * a.Tpm;
     const int Tmax = valid ? Tp : 0;   // uniform over the CTA
     for (int p0 = 0; p0 < Tmax; p0 += kRing) {
@@ -591,10 +598,10 @@ __global__ void __launch_bounds__(256) k_greedy_cta(const GreedyArgs a, int mchu
             *reinterpret_cast<double2*>(s_v + r * RSTR + (k / FPL) * PSTR + (k % FPL)) = v;
         }
         for (int r = threadIdx.x; r < np; r += blockDim.x) {
-            const int row = __ldg(orow + p0 + r);
-            s_dim[r] = __ldg(a.vdim + row);
-            s_bytes[r] = __ldg(a.vbytes + row);
-            s_idx[r] = __ldg(oidx + p0 + r);
+            const int4 mt = __ldg(ometa + p0 + r);
+            s_dim[r] = mt.x;
+            s_bytes[r] = (long long)(((unsigned long long)(unsigned)mt.w << 32) | (unsigned)mt.z);
+            s_idx[r] = mt.y;
         }
         __syncthreads();
 #pragma unroll 1
@@ -658,7 +665,11 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 
-constexpr int kStages = 8;   // row-stream ring depth of the grouped greedy
+constexpr int kStages = 8;   // row-stream ring depth (large-D greedy)
+#ifndef NS_DSTAGES
+#define NS_DSTAGES 6
+#endif
+constexpr int kDStages = NS_DSTAGES;   // row-stream ring depth of the grouped greedy
 
 // ---------------------------------------------------------------------------
 // Grouped greedy (used for D <= 16): one WARP per column plan, all M grid
@@ -713,9 +724,9 @@ struct __align__(16) DedupSmem {
     static constexpr int DPW = 32 / LPD;      // device slots per warp
     static constexpr int SS = FPL * 8 + 16;   // ring slice stride (bytes): +16 B keeps the LPD
     static constexpr int RS = LPD * SS;       //   slices of a row on distinct banks
-    unsigned char ring[kStages][RS];          // staged v rows of the next tables
+    unsigned char ring[kDStages][RS];          // staged v rows of the next tables
     long long gb[MC][DPW];                    // group bytes per device (groups >= 1)
-    long long sbt[kStages];                   // bytes of the staged table
+    int4 meta[kDStages];                       // staged {dim, list index, bytes lo, bytes hi}
     double sc[DPW];                           // scores of the current group
     int gd[MC][DPW];                          // group dims per device (groups >= 1)
     int mgroup[MC];                           // member -> group (-1 stranded)
@@ -729,13 +740,11 @@ struct __align__(16) DedupSmem {
     uint32_t gwork[MC];                       // work of the group's uniform steps
     int sdv[DPW];                             // dim after insertion
     int sok[DPW];                             // device scored
-    int sdt[kStages];                         // dim of the staged table
-    int sidx[kStages];                        // its list index
 };
 
 template <int LPD, int MC>
 #ifndef NS_DEDUP_BLOCKS8
-#define NS_DEDUP_BLOCKS8 4   // CTAs per SM for LPD >= 8 (D <= 4): 126 registers, no spills
+#define NS_DEDUP_BLOCKS8 5   // CTAs per SM for LPD >= 8 (D <= 4): 96 registers, no spills
 #endif
 __global__ void __launch_bounds__(128, (LPD >= 8 ? NS_DEDUP_BLOCKS8 : (LPD == 4 ? 2 : 1))) k_greedy_dedup(const GreedyArgs a, const DedupArgs x) {
     using SM = DedupSmem<LPD, MC>;
@@ -750,11 +759,25 @@ __global__ void __launch_bounds__(128, (LPD >= 8 ? NS_DEDUP_BLOCKS8 : (LPD == 4 
     // every column plan instead of occupying FPL registers for the whole kernel
     __shared__ double s_hb1[kV];
     for (int k = threadIdx.x; k < kV; k += blockDim.x) s_hb1[k] = a.head.hb1[k];
+#ifndef NS_GW_REGS
+    // head weights as per-part slices padded 16 B apart (the LPD slices of one
+    // load fall on distinct banks): FPL fewer register pairs per lane
+    __shared__ __align__(16) double s_wp[LPD][FPL + 2];
+    for (int k = threadIdx.x; k < kV; k += blockDim.x) s_wp[k / FPL][k % FPL] = a.head.H2[k];
+#define GW(k) s_wp[part][k]
+#else
+#define GW(k) w[k]
+#endif
     __syncthreads();
-    double w[FPL], u0[FPL];
+    double u0[FPL];
+#ifdef NS_GW_REGS
+    double w[FPL];
     load_lane_head<FPL>(a.head, part, u0, w);
+#endif
     const long long gw = (long long)blockIdx.x * nw + wl;
     double* scr = x.scratch + (size_t)gw * M * D * kV;   // this warp's group states
+    // state slice of group gr >= 1 owned by this lane (device dd, part)
+    auto gptr = [&](int gr, int dd) -> double* { return scr + ((size_t)gr * D + dd) * kV + part * FPL; };
     int8_t* hist = x.hist + (size_t)gw * M * a.Tpm;       // this warp's group histories
     // dynamic column-plan queue (column plans differ in length and in how many
     // groups they split into; a static stride leaves a long tail)
@@ -809,27 +832,25 @@ __global__ void __launch_bounds__(128, (LPD >= 8 ? NS_DEDUP_BLOCKS8 : (LPD == 4 
         int ng = 1;
         __syncwarp();
         const int32_t* orow = a.ord_row + (size_t)g * a.Tpm;
-        const int32_t* oidx = a.ord_idx + (size_t)g * a.Tpm;
+        const int4* ometa = a.ord_meta + (size_t)g * a.Tpm;
         // row-index window: the next 32 entries of the cost order in one register per lane
         int oc_cur = lane < Tp ? __ldg(orow + lane) : 0;
         int oc_nxt = 32 + lane < Tp ? __ldg(orow + 32 + lane) : 0;
-        auto issue = [&](int pp) {   // stage table pp of the cost order into ring slot pp % kStages
+        auto issue = [&](int pp) {   // stage table pp of the cost order into ring slot pp % kDStages
             if (pp < Tp) {
                 if (pp > 0 && (pp & 31) == 0) {
                     oc_cur = oc_nxt;
                     oc_nxt = pp + 32 + lane < Tp ? __ldg(orow + pp + 32 + lane) : 0;
                 }
                 const int r = __shfl_sync(kFull, oc_cur, pp & 31);
-                const int sl = pp % kStages;
+                const int sl = pp % kDStages;
                 constexpr int CPS = FPL / 2;   // 16-byte chunks per slice
                 cp_async16(&s.ring[sl][(lane / CPS) * SS + (lane % CPS) * 16], a.V + (size_t)r * kV + 2 * lane);
-                if (lane == 0) cp_async4(&s.sdt[sl], a.vdim + r);
-                if (lane == 1) cp_async4(&s.sidx[sl], oidx + pp);
-                if (lane == 2) cp_async8(&s.sbt[sl], a.vbytes + r);
+                if (lane == 0) cp_async16(&s.meta[sl], ometa + pp);
             }
             cp_async_commit();   // one group per step, empty past the end
         };
-        auto process = [&](const double (&vcd)[FPL], const int dt, const long long bt, const int idx, const int p) {
+        auto process = [&](const auto& vcd, const int dt, const long long bt, const int idx, const int p) {
             const int ng0 = ng;
 #pragma unroll 1
             for (int gr = 0; gr < ng0; ++gr) {
@@ -839,16 +860,16 @@ __global__ void __launch_bounds__(128, (LPD >= 8 ? NS_DEDUP_BLOCKS8 : (LPD == 4 
                 const int dsum = gr == 0 ? r_dsum : (dev ? s.gd[gr][d] : 0);
                 const long long bsum = gr == 0 ? r_bsum : (dev ? s.gb[gr][d] : 0);
                 const bool f = dev && (bsum + bt <= cap) && (dsum + dt <= gcap_gr);
-                double* ug = scr + ((size_t)gr * D + (dev ? d : 0)) * kV + part * FPL;   // valid for gr >= 1
+                double* ug = gptr(gr, dev ? d : 0);   // valid for gr >= 1
                 double ps = 0.0;
                 if (f) {
                     double acc[4] = {0.0, 0.0, 0.0, 0.0};
                     if (gr == 0) {
 #pragma unroll
-                        for (int k = 0; k < FPL; ++k) acc[k & 3] = fma(w[k], relu_hi(u0[k] + vcd[k]), acc[k & 3]);
+                        for (int k = 0; k < FPL; ++k) acc[k & 3] = fma(GW(k), relu_hi(u0[k] + vcd[k]), acc[k & 3]);
                     } else {
 #pragma unroll
-                        for (int k = 0; k < FPL; ++k) acc[k & 3] = fma(w[k], relu_hi(ug[k] + vcd[k]), acc[k & 3]);
+                        for (int k = 0; k < FPL; ++k) acc[k & 3] = fma(GW(k), relu_hi(ug[k] + vcd[k]), acc[k & 3]);
                     }
                     ps = (acc[0] + acc[1]) + (acc[2] + acc[3]);
                 }
@@ -867,7 +888,11 @@ __global__ void __launch_bounds__(128, (LPD >= 8 ? NS_DEDUP_BLOCKS8 : (LPD == 4 
                         const double own = f ? sco : CUDART_INF;
                         double bs = own;
 #pragma unroll
-                        for (int o = 16; o >= LPD; o >>= 1) bs = fmin(bs, __shfl_xor_sync(kFull, bs, o));
+                        for (int o = 16; o >= LPD; o >>= 1) {
+                            // plain select (scores are never NaN): no fmin NaN fix-ups
+                            const double ob = __shfl_xor_sync(kFull, bs, o);
+                            bs = ob < bs ? ob : bs;
+                        }
                         const unsigned nf = __popc(__ballot_sync(kFull, f && part == 0));
                         const unsigned hit = __ballot_sync(kFull, f && part == 0 && own == bs);
                         const int bd = (__ffs(hit) - 1) / LPD;
@@ -1000,7 +1025,7 @@ __global__ void __launch_bounds__(128, (LPD >= 8 ? NS_DEDUP_BLOCKS8 : (LPD == 4 
                         }
                         // new group ng = state(gr) + v_t on device dd
                         if (dev) {
-                            double* un = scr + ((size_t)ng * D + d) * kV + part * FPL;
+                            double* un = gptr(ng, d);
 #pragma unroll
                             for (int k = 0; k < FPL; ++k) {
                                 double val = gr == 0 ? u0[k] : ug[k];
@@ -1074,14 +1099,18 @@ __global__ void __launch_bounds__(128, (LPD >= 8 ? NS_DEDUP_BLOCKS8 : (LPD == 4 
             }
         };
 #pragma unroll 1
-        for (int pp = 0; pp < kStages - 1; ++pp) issue(pp);
+        for (int pp = 0; pp < kDStages - 1; ++pp) issue(pp);
 #pragma unroll 1
         for (int p = 0; p < Tp; ++p) {
-            __syncwarp();                  // slot (p - 1) % kStages fully consumed
-            issue(p + kStages - 1);
-            cp_async_wait<kStages - 1>();  // table p has landed (this lane's copies)
+            __syncwarp();                  // slot (p - 1) % kDStages fully consumed
+            issue(p + kDStages - 1);
+            cp_async_wait<kDStages - 1>();  // table p has landed (this lane's copies)
             __syncwarp();                  // ... and every lane's
-            const int sl = p % kStages;
+            const int sl = p % kDStages;
+#ifdef NS_GV_SMEM
+            // v_t read from the ring slice at each use (not held in registers)
+            const double* vcd = reinterpret_cast<const double*>(&s.ring[sl][part * SS]);
+#else
             double vcd[FPL];
             const double2* src = reinterpret_cast<const double2*>(&s.ring[sl][part * SS]);
 #pragma unroll
@@ -1090,7 +1119,9 @@ __global__ void __launch_bounds__(128, (LPD >= 8 ? NS_DEDUP_BLOCKS8 : (LPD == 4 
                 vcd[2 * i2] = xv.x;
                 vcd[2 * i2 + 1] = xv.y;
             }
-            process(vcd, s.sdt[sl], s.sbt[sl], s.sidx[sl], p);
+#endif
+            const int4 mt = s.meta[sl];
+            process(vcd, mt.x, (long long)(((unsigned long long)(unsigned)mt.w << 32) | (unsigned)mt.z), mt.y, p);
         }
         cp_async_wait<0>();
         // ---- group 0's register state to shared memory for the epilogue
@@ -1102,7 +1133,7 @@ __global__ void __launch_bounds__(128, (LPD >= 8 ? NS_DEDUP_BLOCKS8 : (LPD == 4 
         for (int gg = 1; gg < ng; ++gg) {
             const int par = s.gpar[gg], st = s.gstep[gg];
             for (int p2 = lane; p2 < st; p2 += 32) {
-                const int i = __ldg(oidx + p2);
+                const int i = __ldg(&ometa[p2].y);
                 hist[(size_t)gg * a.Tpm + i] = hist[(size_t)par * a.Tpm + i];
             }
             __syncwarp();
@@ -1110,11 +1141,16 @@ __global__ void __launch_bounds__(128, (LPD >= 8 ? NS_DEDUP_BLOCKS8 : (LPD == 4 
         // ---- outputs: per member feasibility, work, and its group's device costs
         for (int gr = 0; gr < ng; ++gr) {
             double hp;
+#ifndef NS_GW_REGS
+            double w[FPL];
+#pragma unroll
+            for (int k = 0; k < FPL; ++k) w[k] = GW(k);
+#endif
             if (gr == 0) {
                 hp = part_head<FPL>(u0, w);
             } else {
                 double tu[FPL];
-                const double* ug = scr + ((size_t)gr * D + (dev ? d : 0)) * kV + part * FPL;
+                const double* ug = gptr(gr, dev ? d : 0);
 #pragma unroll
                 for (int k = 0; k < FPL; ++k) tu[k] = ug[k];
                 hp = part_head<FPL>(tu, w);
@@ -1164,6 +1200,8 @@ __global__ void __launch_bounds__(128, (LPD >= 8 ? NS_DEDUP_BLOCKS8 : (LPD == 4 
     }
 }
 
+#undef GW
+
 // Large D (D > 16, e.g. C5's 128 simulated GPUs): one trajectory per CTA and
 // ONE thread per device holding all 64 features of u_d in registers; the head
 // weights and the staged v row are read from shared memory as broadcasts
@@ -1181,8 +1219,7 @@ __global__ void __launch_bounds__(128, 3) k_greedy_wide(const GreedyArgs a) {
     __shared__ double s_sc[2][4];
     __shared__ int s_dv[2][4];
     __shared__ int s_cnt[2][4];
-    __shared__ int sdt[kStages], sidx[kStages];
-    __shared__ long long sbt[kStages];
+    __shared__ int4 smeta[kStages];   // {dim, list index, bytes lo, bytes hi}
     const int lane = threadIdx.x & 31, wi = threadIdx.x >> 5, nw = blockDim.x >> 5;
     const long long tau = a.traj_begin + blockIdx.x;
     if (tau >= a.traj_end) return;
@@ -1210,7 +1247,7 @@ __global__ void __launch_bounds__(128, 3) k_greedy_wide(const GreedyArgs a) {
     long long bsum = 0;
     uint32_t work = 0;
     const int32_t* orow = a.ord_row + (size_t)g * a.Tpm;
-    const int32_t* oidx = a.ord_idx + (size_t)g * a.Tpm;
+    const int4* ometa = a.ord_meta + (size_t)g * a.Tpm;
     int8_t* asg = a.assign + (size_t)tau * a.Tpm;
     const int T = alive ? Tp : 0;
     // warp 0 streams the cost-ordered v rows through a cp.async ring
@@ -1219,9 +1256,7 @@ __global__ void __launch_bounds__(128, 3) k_greedy_wide(const GreedyArgs a) {
             const int r = __ldg(orow + pp);
             const int slot = pp % kStages;
             cp_async16(&ring[slot][2 * lane], a.V + (size_t)r * kV + 2 * lane);
-            if (lane == 0) cp_async4(sdt + slot, a.vdim + r);
-            if (lane == 1) cp_async4(sidx + slot, oidx + pp);
-            if (lane == 2) cp_async8(sbt + slot, a.vbytes + r);
+            if (lane == 0) cp_async16(smeta + slot, ometa + pp);
         }
         cp_async_commit();
     };
@@ -1236,8 +1271,9 @@ __global__ void __launch_bounds__(128, 3) k_greedy_wide(const GreedyArgs a) {
         }
         __syncthreads();              // ... visible to every warp
         const int sl = p % kStages;
-        const int dt = sdt[sl];
-        const long long bt = sbt[sl];
+        const int4 mt = smeta[sl];
+        const int dt = mt.x;
+        const long long bt = (long long)(((unsigned long long)(unsigned)mt.w << 32) | (unsigned)mt.z);
         const bool f = dev && (bsum + bt <= cap) && (dsum + dt <= capd);
         const double2* v2 = reinterpret_cast<const double2*>(ring[sl]);
         const double2* w2 = reinterpret_cast<const double2*>(s_w);
@@ -1289,7 +1325,7 @@ __global__ void __launch_bounds__(128, 3) k_greedy_wide(const GreedyArgs a) {
             dsum += dt;
             bsum += bt;
         }
-        if (threadIdx.x == 0) asg[sidx[sl]] = (int8_t)bd;
+        if (threadIdx.x == 0) asg[mt.y] = (int8_t)bd;
     }
     if (wi == 0) cp_async_wait<0>();
     if (dev) {
@@ -1583,7 +1619,7 @@ void carve(Carver& c, SearchBufs& b, OutStage& o, int Lout) {
     b.cp_plan = c.take<int32_t>((size_t)b.S * b.Lcap);
     b.cp_Tp = c.take<int32_t>(b.S);
     b.ord_row = c.take<int32_t>((size_t)b.S * b.Tpm);
-    b.ord_idx = c.take<int32_t>((size_t)b.S * b.Tpm);
+    b.ord_meta = c.take<int4>((size_t)b.S * b.Tpm);
     b.assign = c.take<int8_t>((size_t)b.n_traj * b.Tpm);
     b.comp = c.take<double>((size_t)b.n_traj * b.D);
     b.devdim = c.take<int32_t>((size_t)b.n_traj * b.D);
@@ -1640,7 +1676,7 @@ ns_status launch_greedy(ns_ctx* ctx, const SearchBufs& b, const ns_tables* t, lo
     a.cp_task = b.cp_task;
     a.cp_Tp = b.cp_Tp;
     a.ord_row = b.ord_row;
-    a.ord_idx = b.ord_idx;
+    a.ord_meta = b.ord_meta;
     a.capdim = b.capdim;
     a.cap = t->d_cap;
     a.V = t->d_V;
@@ -1671,7 +1707,7 @@ ns_status launch_greedy(ns_ctx* ctx, const SearchBufs& b, const ns_tables* t, lo
         const long long g0 = tb / b.M, g1 = (te - 1) / b.M + 1;
         GreedyArgs a2 = a;
         a2.ord_row = b.ord_row + (size_t)g0 * b.Tpm;
-        a2.ord_idx = b.ord_idx + (size_t)g0 * b.Tpm;
+        a2.ord_meta = b.ord_meta + (size_t)g0 * b.Tpm;
         a2.cp_valid = b.cp_valid + g0;
         a2.cp_task = b.cp_task + g0;
         a2.cp_Tp = b.cp_Tp + g0;
@@ -1698,7 +1734,7 @@ ns_status launch_greedy(ns_ctx* ctx, const SearchBufs& b, const ns_tables* t, lo
         const long long g0 = tb / b.M, g1 = te / b.M;
         GreedyArgs a2 = a;
         a2.ord_row = b.ord_row + (size_t)g0 * b.Tpm;
-        a2.ord_idx = b.ord_idx + (size_t)g0 * b.Tpm;
+        a2.ord_meta = b.ord_meta + (size_t)g0 * b.Tpm;
         a2.cp_valid = b.cp_valid + g0;
         a2.cp_task = b.cp_task + g0;
         a2.cp_Tp = b.cp_Tp + g0;
@@ -1728,7 +1764,7 @@ ns_status launch_greedy(ns_ctx* ctx, const SearchBufs& b, const ns_tables* t, lo
         const size_t smem = sizeof(DedupSmem<L, MC>) * wpb;                                              \
         blocks = (unsigned)((x.total_warps + wpb - 1) / wpb);                                            \
         x.total_warps = (int)blocks * wpb; /* every launched warp strides the column plans */            \
-        if (smem + 1024 > 48 * 1024) /* + the static s_hb1 */                                           \
+        if (smem + 2048 > 48 * 1024) /* + the static s_hb1, s_wp */                                     \
             cudaFuncSetAttribute(k_greedy_dedup<L, MC>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
         k_greedy_dedup<L, MC><<<blocks, wpb * 32, smem, ctx->stream>>>(a2, x);                           \
         break;                                                                                           \
