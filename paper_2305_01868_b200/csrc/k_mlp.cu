@@ -101,7 +101,10 @@ __device__ __forceinline__ void warp_layer(const double* __restrict__ W, const d
 // shared memory and folded into the layer-2 accumulators (registers) at once,
 // so no 16 x 128 activation buffer is needed (15 KB per warp instead of 27 KB
 // -> 1.5x the resident warps).  Layers 3-5 use warp_layer.
-__global__ void __launch_bounds__(128, 3) k_plan_cost_dmma(const PlanCostArgs a) {
+#ifndef NS_PC_BLOCKS
+#define NS_PC_BLOCKS 3
+#endif
+__global__ void __launch_bounds__(128, NS_PC_BLOCKS) k_plan_cost_dmma(const PlanCostArgs a) {
     extern __shared__ double psm[];
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
     const int g = lane >> 2, t = lane & 3;
@@ -266,7 +269,11 @@ struct PreDmmaArgs {
 // memory (11 KB per warp instead of 21 KB -> 2.5x the resident warps).  v
 // leaves the accumulator fragments straight to HBM; the single-table cost is
 // reduced from the same fragments.
-__global__ void __launch_bounds__(128) k_precompute_dmma(const PreDmmaArgs a) {
+#define PRE_RELU relu_int
+#ifndef NS_PRE_BLOCKS
+#define NS_PRE_BLOCKS 5
+#endif
+__global__ void __launch_bounds__(128, NS_PRE_BLOCKS) k_precompute_dmma(const PreDmmaArgs a) {
     extern __shared__ double qsm[];
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
     const int g = lane >> 2, t = lane & 3;
@@ -347,8 +354,8 @@ __global__ void __launch_bounds__(128) k_precompute_dmma(const PreDmmaArgs a) {
 #pragma unroll
                 for (int m = 0; m < 2; ++m) {
                     double2 hv;
-                    hv.x = relu_exact(hacc[m][q][0] + b0);
-                    hv.y = relu_exact(hacc[m][q][1] + b1);
+                    hv.x = PRE_RELU(hacc[m][q][0] + b0);
+                    hv.y = PRE_RELU(hacc[m][q][1] + b1);
                     *reinterpret_cast<double2*>(Hc + (8 * m + g) * ldh + col) = hv;
                 }
             }
@@ -376,8 +383,8 @@ __global__ void __launch_bounds__(128) k_precompute_dmma(const PreDmmaArgs a) {
 #pragma unroll
             for (int m = 0; m < 2; ++m) {
                 double2 ev;
-                ev.x = relu_exact(e_acc[m][q][0] + b0);
-                ev.y = relu_exact(e_acc[m][q][1] + b1);
+                ev.x = PRE_RELU(e_acc[m][q][0] + b0);
+                ev.y = PRE_RELU(e_acc[m][q][1] + b1);
                 *reinterpret_cast<double2*>(E + (8 * m + g) * ldh + col) = ev;
             }
         }
@@ -413,8 +420,8 @@ __global__ void __launch_bounds__(128) k_precompute_dmma(const PreDmmaArgs a) {
                     const long long row = m ? row1 : row0;
                     const double v0 = vacc[m][q][0], v1 = vacc[m][q][1];
                     if (row >= 0) *reinterpret_cast<double2*>(a.V + row * kV + col) = make_double2(v0, v1);
-                    cpart[m] = fma(a.head.H2[col], relu_exact(v0 + a.head.hb1[col]), cpart[m]);
-                    cpart[m] = fma(a.head.H2[col + 1], relu_exact(v1 + a.head.hb1[col + 1]), cpart[m]);
+                    cpart[m] = fma(a.head.H2[col], PRE_RELU(v0 + a.head.hb1[col]), cpart[m]);
+                    cpart[m] = fma(a.head.H2[col + 1], PRE_RELU(v1 + a.head.hb1[col + 1]), cpart[m]);
                 }
             }
         }

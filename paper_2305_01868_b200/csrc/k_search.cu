@@ -746,7 +746,10 @@ template <int LPD, int MC>
 #ifndef NS_DEDUP_BLOCKS8
 #define NS_DEDUP_BLOCKS8 5   // CTAs per SM for LPD >= 8 (D <= 4): 96 registers, no spills
 #endif
-__global__ void __launch_bounds__(128, (LPD >= 8 ? NS_DEDUP_BLOCKS8 : (LPD == 4 ? 2 : 1))) k_greedy_dedup(const GreedyArgs a, const DedupArgs x) {
+#ifndef NS_DEDUP_WPB
+#define NS_DEDUP_WPB 4   // warps (column plans in flight) per CTA
+#endif
+__global__ void __launch_bounds__(NS_DEDUP_WPB * 32, (LPD >= 8 ? NS_DEDUP_BLOCKS8 : (LPD == 4 ? 2 : 1))) k_greedy_dedup(const GreedyArgs a, const DedupArgs x) {
     using SM = DedupSmem<LPD, MC>;
     constexpr int FPL = SM::FPL, DPW = SM::DPW, SS = SM::SS;
     extern __shared__ __align__(16) unsigned char dsm[];
@@ -1755,7 +1758,7 @@ ns_status launch_greedy(ns_ctx* ctx, const SearchBufs& b, const ns_tables* t, lo
         NS_CUDA(ctx, cudaMemsetAsync(b.next_cp, 0, sizeof(unsigned int), ctx->stream));
         const int lpd = 32 / dp;
         const int mc = b.M <= 16 ? 16 : 64;
-        const int wpb = 4;
+        const int wpb = NS_DEDUP_WPB;
         unsigned blocks = 0;
         prof_begin(ctx, PK_GREEDY);
         switch (lpd * 1000 + mc) {
@@ -1946,9 +1949,11 @@ ns_status run_search(ns_ctx* ctx, const ns_tables* t, int D, const ns_search_par
         while (dp < D) dp <<= 1;
         const long long max_cp = (long long)b.S;
         const size_t per = (size_t)b.M * D * kV * sizeof(double);
-        long long warps = std::min<long long>(max_cp, (long long)ctx->sm_count * 20);
-        warps = std::max<long long>(4, std::min<long long>(warps, (long long)((512ull << 20) / per)));
-        b.gscratch_warps = dp <= 16 ? (int)(((warps + 3) / 4) * 4) : 0;
+        // one resident wave of grouped-greedy warps (they pull column plans from a queue)
+        constexpr int W = NS_DEDUP_WPB;
+        long long warps = std::min<long long>(max_cp, (long long)ctx->sm_count * W * NS_DEDUP_BLOCKS8);
+        warps = std::max<long long>(W, std::min<long long>(warps, (long long)((512ull << 20) / per)));
+        b.gscratch_warps = dp <= 16 ? (int)(((warps + W - 1) / W) * W) : 0;
     }
     OutStage o{};
     Carver probe{nullptr};

@@ -11,7 +11,16 @@ namespace ns {
 
 constexpr unsigned kFull = 0xffffffffu;
 
-__device__ __forceinline__ double relu_exact(double x) { return x > 0.0 ? x : 0.0; }
+// Exact max(x, 0) on the integer pipe (no FP64-pipe compare): the sign mask
+// clears both words of a negative input (-0.0 -> +0.0), same value as
+// x > 0 ? x : 0 for every non-NaN x.
+__device__ __forceinline__ double relu_int(double x) {
+    const int hi = __double2hiint(x), lo = __double2loint(x);
+    const int m = hi >> 31;
+    return __hiloint2double(hi & ~m, lo & ~m);
+}
+__device__ __forceinline__ double relu_exact(double x) { return relu_int(x); }
+
 
 // max(x, 0) for the greedy's hot loop in ONE integer op: clamp the high word
 // of the IEEE double at 0 (IMNMX).  For x >= 0 the result is x bit-for-bit;
@@ -24,6 +33,7 @@ __device__ __forceinline__ double relu_hi(double x) {
     int hi = __double2hiint(x);
     return __hiloint2double(max(hi, 0), lo);
 }
+
 
 // One dense fp64 layer computed by a warp: y[o] = act(b[o] + sum_i W[o][i] x[i])
 // with x and y in shared memory.  Deterministic sequential order over i.
