@@ -91,6 +91,22 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, float (&v)[16]) {
     for (int j = 0; j < 16; ++j) v[j] = __uint_as_float(r[j]);
 }
 
+// 32 consecutive fp32 columns of this thread's TMEM lane (one load, one wait)
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v)[32]) {
+    uint32_t r[32];
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+                 "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+                   "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
+                   "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]),
+                   "=r"(r[23]), "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]),
+                   "=r"(r[30]), "=r"(r[31])
+                 : "r"(taddr));
+    asm volatile("tcgen05.wait::ld.sync.aligned;");
+#pragma unroll
+    for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
+}
+
 struct TcArgs {
     long long row_begin, row_end;   // plan rows
     int D, K0p, N5p;                // 2D padded to 8, D padded to 16
@@ -199,11 +215,22 @@ __global__ void __launch_bounds__(128, 1) k_plan_mlp_tc(const TcArgs a) {
     };
     // write this thread's row values v[0..n) (columns c0..) into an A operand
     // block [128 x Kblk] (hi, lo) as TF32 splits
+    // (c0 and n multiples of 4: the 4 k-values of a core-matrix row are 16
+    // contiguous bytes, so each group is one conflict-free 128-bit store --
+    // eight threads fill one 128-byte wavefront)
     auto put_row = [&](float* Ahi, float* Alo, int c0, const float* v, int n) {
-        for (int j = 0; j < n; ++j) {
-            const float x = v[j], h = tf32_rn(x);
-            Ahi[kmaj(tid, c0 + j, kTile)] = h;
-            Alo[kmaj(tid, c0 + j, kTile)] = x - h;
+        for (int j = 0; j < n; j += 4) {
+            float4 h4, l4;
+            h4.x = tf32_rn(v[j]);
+            h4.y = tf32_rn(v[j + 1]);
+            h4.z = tf32_rn(v[j + 2]);
+            h4.w = tf32_rn(v[j + 3]);
+            l4.x = v[j] - h4.x;
+            l4.y = v[j + 1] - h4.y;
+            l4.z = v[j + 2] - h4.z;
+            l4.w = v[j + 3] - h4.w;
+            *reinterpret_cast<float4*>(&Ahi[kmaj(tid, c0 + j, kTile)]) = h4;
+            *reinterpret_cast<float4*>(&Alo[kmaj(tid, c0 + j, kTile)]) = l4;
         }
     };
     auto sync_for_mma = [&]() {
@@ -225,17 +252,21 @@ __global__ void __launch_bounds__(128, 1) k_plan_mlp_tc(const TcArgs a) {
             double mn = CUDART_INF;
             if (rv && a.dir == 0)
                 for (int d = 0; d < a.D; ++d) mn = fmin(mn, a.comp[row * a.D + d]);
-            for (int k = 0; k < a.K0p; ++k) {
-                float x = 0.0f;
-                if (rv && k < 2 * a.D) {
-                    if (k < a.D)
-                        x = a.dir == 0 ? (float)((a.comp[row * a.D + k] - mn) / a.start_scale) : 0.0f;
-                    else
-                        x = (float)((double)a.devdim[row * a.D + k - a.D] / a.dim_scale);
+            for (int k0 = 0; k0 < a.K0p; k0 += 4) {
+                float xs[4];
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    const int k = k0 + j;
+                    float x = 0.0f;
+                    if (rv && k < 2 * a.D) {
+                        if (k < a.D)
+                            x = a.dir == 0 ? (float)((a.comp[row * a.D + k] - mn) / a.start_scale) : 0.0f;
+                        else
+                            x = (float)((double)a.devdim[row * a.D + k - a.D] / a.dim_scale);
+                    }
+                    xs[j] = x;
                 }
-                const float h = tf32_rn(x);
-                Ahi[kmaj(tid, k, kTile)] = h;
-                Alo[kmaj(tid, k, kTile)] = x - h;
+                put_row(Ahi, Alo, k0, xs, 4);
             }
         }
         sync_for_mma();
@@ -260,12 +291,12 @@ __global__ void __launch_bounds__(128, 1) k_plan_mlp_tc(const TcArgs a) {
                     ph1 ^= 1;
                 }
             }
-            for (int h = 0; h < 2; ++h) {
-                float v[16];
-                tmem_ld16(lane_base + 32 * c + 16 * h, v);
+            {
+                float v[32];
+                tmem_ld32(lane_base + 32 * c, v);
 #pragma unroll
-                for (int j = 0; j < 16; ++j) v[j] = fmaxf(v[j] + bias1[32 * c + 16 * h + j], 0.0f);
-                put_row(Ahi, Alo, 16 * h, v, 16);
+                for (int j = 0; j < 32; ++j) v[j] = fmaxf(v[j] + bias1[32 * c + j], 0.0f);
+                put_row(Ahi, Alo, 0, v, 32);
             }
             sync_for_mma();
             if (tid == 0) {
