@@ -146,17 +146,26 @@ __device__ __forceinline__ WLayout wlayout(int D, int K0p, int N5p) {
     return L;
 }
 
-__global__ void __launch_bounds__(128, 1) k_plan_mlp_tc(const TcArgs a) {
+// Two tile groups per CTA (warps 0-3 and 4-7, 128 rows each, own 256 TMEM
+// columns, own operand ring and mbarriers, named barriers): while one group
+// runs its TMEM -> register -> smem epilogue, the other's MMAs keep the
+// tensor core busy.  Every layer's A operand streams through a per-group
+// ring of two 16-column K chunks (hi, lo): the epilogue of chunk c overlaps
+// the MMAs of chunk c - 1.
+constexpr int kGroups = 2;
+constexpr int kKc = 16;                       // K columns per operand chunk
+constexpr int kABuf = kTile * kKc * 2;        // floats per operand buffer (hi + lo)
+
+__global__ void __launch_bounds__(128 * kGroups, 1) k_plan_mlp_tc(const TcArgs a) {
     extern __shared__ __align__(128) float tsm[];
     __shared__ uint32_t s_tmem;
-    __shared__ __align__(8) uint64_t s_bar[3];   // 0: layer done, 1/2: layer-2 chunk buffers free
+    __shared__ __align__(8) uint64_t s_bar[kGroups][2];   // per group: operand buffer 0 / 1 consumed
     __shared__ float s_bias[128 + 64 + 32 + 16 + 64];
     const int tid = threadIdx.x, warp = tid >> 5;
+    const int grp = tid >> 7, gtid = tid & 127, gwarp = warp & 3;
     const WLayout L = wlayout(a.D, a.K0p, a.N5p);
-    float* sW = tsm;                       // weights (resident)
-    float* sA = tsm + L.total;             // activation operand: 2 buffers x [128 x 32] x (hi, lo)
-    constexpr int kChunk = 32;
-    const int abuf = kTile * kChunk * 2;   // floats per chunk buffer (hi + lo)
+    float* sW = tsm;                                   // weights (resident, shared by both groups)
+    float* sA = tsm + L.total + grp * 2 * kABuf;       // this group's two operand buffers
     // ---- resident weights: hi/lo split, K-major, zero padded
     for (int l = 0; l < 5; ++l) {
         const int Kp = L.Kp[l], Np = L.Np[l], K = L.K[l], N = L.N[l];
@@ -177,48 +186,35 @@ __global__ void __launch_bounds__(128, 1) k_plan_mlp_tc(const TcArgs a) {
             for (int i = tid; i < N[l]; i += blockDim.x) s_bias[off[l] + i] = (float)a.b[l][i];
     }
     if (warp == 0) {
-        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 256;" ::"r"(su32(&s_tmem)));
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(su32(&s_tmem)),
+                     "r"(256 * kGroups));
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
     }
     if (tid == 0) {
-        for (int i = 0; i < 3; ++i) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(su32(&s_bar[i])));
+        for (int g = 0; g < kGroups; ++g)
+            for (int i = 0; i < 2; ++i) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(su32(&s_bar[g][i])));
         asm volatile("fence.mbarrier_init.release.cluster;");
     }
     asm volatile("fence.proxy.async.shared::cta;");
     asm volatile("tcgen05.fence::before_thread_sync;");
     __syncthreads();
     asm volatile("tcgen05.fence::after_thread_sync;");
-    const uint32_t tmem = s_tmem;
-    const uint32_t lane_base = tmem + ((uint32_t)(warp * 32) << 16);
-    uint32_t ph0 = 0, ph1 = 0, ph2 = 0;   // mbarrier phases
-    const float* bias1 = s_bias;
-    const float* bias2 = s_bias + 128;
-    const float* bias3 = s_bias + 192;
-    const float* bias4 = s_bias + 224;
-    const float* bias5 = s_bias + 240;
+    const uint32_t tmem = s_tmem + (uint32_t)(grp * 256);               // this group's columns
+    const uint32_t lane_base = tmem + ((uint32_t)(gwarp * 32) << 16);   // this warp's 32 TMEM lanes
+    uint64_t* bar = s_bar[grp];
+    uint32_t ph[2] = {0, 0};   // mbarrier phases (every thread waits on every commit, in order)
 
-    // issue one layer: D[cols d0..) (+)= A . B^T over k-steps [ks0, ks1) of the A/B blocks
-    auto issue = [&](const float* Ahi, const float* Alo, int arows_k4stride, const float* Bhi, const float* Blo,
-                     int Np, int ks0, int ks1, int kb_off, uint32_t dcol, bool acc_first) {
-        const uint32_t idesc = idesc_tf32(kTile, Np);
-        for (int s = ks0; s < ks1; ++s) {
-            const uint64_t ahd = umma_desc(su32(Ahi + 2 * (s - ks0) * kTile * 4), kTile * 16, 128);
-            const uint64_t ald = umma_desc(su32(Alo + 2 * (s - ks0) * kTile * 4), kTile * 16, 128);
-            const uint64_t bhd = umma_desc(su32(Bhi + 2 * (s + kb_off) * Np * 4), Np * 16, 128);
-            const uint64_t bld = umma_desc(su32(Blo + 2 * (s + kb_off) * Np * 4), Np * 16, 128);
-            const uint32_t acc0 = (s > ks0 || acc_first) ? 1u : 0u;
-            mma_tf32(tmem + dcol, ahd, bhd, idesc, acc0);
-            mma_tf32(tmem + dcol, ahd, bld, idesc, 1u);
-            mma_tf32(tmem + dcol, ald, bhd, idesc, 1u);
-        }
-        (void)arows_k4stride;
+    // the group's operand writes -> visible to the async proxy, then the MMA issue
+    auto gsync = [&]() {
+        asm volatile("fence.proxy.async.shared::cta;");
+        asm volatile("tcgen05.fence::before_thread_sync;");
+        asm volatile("bar.sync %0, 128;" ::"r"(1 + grp));
+        asm volatile("tcgen05.fence::after_thread_sync;");
     };
-    // write this thread's row values v[0..n) (columns c0..) into an A operand
-    // block [128 x Kblk] (hi, lo) as TF32 splits
-    // (c0 and n multiples of 4: the 4 k-values of a core-matrix row are 16
-    // contiguous bytes, so each group is one conflict-free 128-bit store --
-    // eight threads fill one 128-byte wavefront)
-    auto put_row = [&](float* Ahi, float* Alo, int c0, const float* v, int n) {
+    // this thread's row values v[0..n) (n multiple of 4) at chunk columns 0..n
+    // as TF32 hi / lo splits: 128-bit stores of whole core-matrix rows
+    // (eight threads fill one 128-byte wavefront, no bank conflicts)
+    auto put_row = [&](float* Ahi, float* Alo, int n, const float* v) {
         for (int j = 0; j < n; j += 4) {
             float4 h4, l4;
             h4.x = tf32_rn(v[j]);
@@ -229,128 +225,101 @@ __global__ void __launch_bounds__(128, 1) k_plan_mlp_tc(const TcArgs a) {
             l4.y = v[j + 1] - h4.y;
             l4.z = v[j + 2] - h4.z;
             l4.w = v[j + 3] - h4.w;
-            *reinterpret_cast<float4*>(&Ahi[kmaj(tid, c0 + j, kTile)]) = h4;
-            *reinterpret_cast<float4*>(&Alo[kmaj(tid, c0 + j, kTile)]) = l4;
+            *reinterpret_cast<float4*>(&Ahi[kmaj(gtid, j, kTile)]) = h4;
+            *reinterpret_cast<float4*>(&Alo[kmaj(gtid, j, kTile)]) = l4;
         }
     };
-    auto sync_for_mma = [&]() {
-        asm volatile("fence.proxy.async.shared::cta;");
-        asm volatile("tcgen05.fence::before_thread_sync;");
-        __syncthreads();
+    // one layer: D[dcol..] = A . W_l^T over K input columns, A produced chunk
+    // by chunk by make(c0, v) (Kc values of input columns c0..c0+Kc)
+    auto layer = [&](int l, int K, uint32_t dcol, auto&& make) {
+        const int Kc = K < kKc ? K : kKc;
+        const int nch = K / Kc;
+        const int Np = L.Np[l];
+        const float* Bhi = sW + L.off[l];
+        const float* Blo = Bhi + L.Kp[l] * Np;
+        const uint32_t idesc = idesc_tf32(kTile, Np);
+        for (int c = 0; c < nch; ++c) {
+            const int b = c & 1;
+            if (c >= 2) {   // chunk c - 2's MMAs have consumed buffer b
+                mbar_wait(&bar[b], ph[b]);
+                ph[b] ^= 1;
+            }
+            float* Ahi = sA + b * kABuf;
+            float* Alo = Ahi + kTile * Kc;
+            float v[kKc];
+            make(c * Kc, v);
+            put_row(Ahi, Alo, Kc, v);
+            gsync();
+            if (gtid == 0) {
+                for (int s = 0; s < Kc / 8; ++s) {
+                    const int kb = c * (Kc / 8) + s;   // k-step of the weight block
+                    const uint64_t ahd = umma_desc(su32(Ahi + s * 8 * kTile), kTile * 16, 128);
+                    const uint64_t ald = umma_desc(su32(Alo + s * 8 * kTile), kTile * 16, 128);
+                    const uint64_t bhd = umma_desc(su32(Bhi + kb * 8 * Np), Np * 16, 128);
+                    const uint64_t bld = umma_desc(su32(Blo + kb * 8 * Np), Np * 16, 128);
+                    const uint32_t acc0 = (kb > 0) ? 1u : 0u;
+                    mma_tf32(tmem + dcol, ahd, bhd, idesc, acc0);
+                    mma_tf32(tmem + dcol, ahd, bld, idesc, 1u);
+                    mma_tf32(tmem + dcol, ald, bhd, idesc, 1u);
+                }
+                commit(&bar[b]);
+            }
+        }
+        // drain the last (up to) two chunks: every MMA of the layer has landed
+        for (int c = nch >= 2 ? nch - 2 : 0; c < nch; ++c) {
+            const int b = c & 1;
+            mbar_wait(&bar[b], ph[b]);
+            ph[b] ^= 1;
+        }
         asm volatile("tcgen05.fence::after_thread_sync;");
+    };
+    // hidden-layer input: the previous layer's TMEM columns + bias, ReLU
+    auto from_tmem = [&](int col0, const float* bias) {
+        return [=](int c0, float (&v)[kKc]) {
+            tmem_ld16(lane_base + col0 + c0, v);
+#pragma unroll
+            for (int j = 0; j < kKc; ++j) v[j] = fmaxf(v[j] + bias[c0 + j], 0.0f);
+        };
     };
 
-    // TMEM columns: [0,128) layer-1 output, [128,192) layer-2 accumulator,
+    // TMEM columns of a group: [0,128) layer-1 output, [128,192) layer 2,
     // [192,224) layer 3, [224,240) layer 4, [240,256) layer 5
-    for (int tile = blockIdx.x; tile < a.n_tiles; tile += gridDim.x) {
-        const long long row = a.row_begin + (long long)tile * kTile + tid;
+    for (int tile = blockIdx.x * kGroups + grp; tile < a.n_tiles; tile += gridDim.x * kGroups) {
+        const long long row = a.row_begin + (long long)tile * kTile + gtid;
         const bool rv = row < a.row_end;
         // ---- layer-1 input row: [starts / start_scale, devdim / dim_scale]
-        {
-            float* Ahi = sA;
-            float* Alo = sA + kTile * a.K0p;
-            double mn = CUDART_INF;
-            if (rv && a.dir == 0)
-                for (int d = 0; d < a.D; ++d) mn = fmin(mn, a.comp[row * a.D + d]);
-            for (int k0 = 0; k0 < a.K0p; k0 += 4) {
-                float xs[4];
-#pragma unroll
-                for (int j = 0; j < 4; ++j) {
-                    const int k = k0 + j;
-                    float x = 0.0f;
-                    if (rv && k < 2 * a.D) {
-                        if (k < a.D)
-                            x = a.dir == 0 ? (float)((a.comp[row * a.D + k] - mn) / a.start_scale) : 0.0f;
-                        else
-                            x = (float)((double)a.devdim[row * a.D + k - a.D] / a.dim_scale);
-                    }
-                    xs[j] = x;
+        double mn = CUDART_INF;
+        if (rv && a.dir == 0)
+            for (int d = 0; d < a.D; ++d) mn = fmin(mn, a.comp[row * a.D + d]);
+        layer(0, a.K0p, 0, [&](int c0, float (&v)[kKc]) {
+            for (int j = 0; j < kKc; ++j) {
+                const int k = c0 + j;
+                float x = 0.0f;
+                if (rv && k < 2 * a.D) {
+                    if (k < a.D)
+                        x = a.dir == 0 ? (float)((a.comp[row * a.D + k] - mn) / a.start_scale) : 0.0f;
+                    else
+                        x = (float)((double)a.devdim[row * a.D + k - a.D] / a.dim_scale);
                 }
-                put_row(Ahi, Alo, k0, xs, 4);
+                v[j] = x;
             }
-        }
-        sync_for_mma();
-        if (tid == 0) {
-            issue(sA, sA + kTile * a.K0p, 0, sW + L.off[0], sW + L.off[0] + L.Kp[0] * L.Np[0], 128, 0, a.K0p / 8, 0, 0,
-                  false);
-            commit(&s_bar[0]);
-        }
-        mbar_wait(&s_bar[0], ph0);
-        ph0 ^= 1;
-        asm volatile("tcgen05.fence::after_thread_sync;");
-        // ---- layer 2 (K = 128) in four 32-column chunks through two operand buffers
-        for (int c = 0; c < 4; ++c) {
-            float* Ahi = sA + (c & 1) * abuf;
-            float* Alo = Ahi + kTile * kChunk;
-            if (c >= 2) {   // the MMAs of chunk c-2 must have consumed this buffer
-                if (c & 1) {
-                    mbar_wait(&s_bar[2], ph2);
-                    ph2 ^= 1;
-                } else {
-                    mbar_wait(&s_bar[1], ph1);
-                    ph1 ^= 1;
-                }
-            }
-            {
-                float v[32];
-                tmem_ld32(lane_base + 32 * c, v);
-#pragma unroll
-                for (int j = 0; j < 32; ++j) v[j] = fmaxf(v[j] + bias1[32 * c + j], 0.0f);
-                put_row(Ahi, Alo, 0, v, 32);
-            }
-            sync_for_mma();
-            if (tid == 0) {
-                issue(Ahi, Alo, 0, sW + L.off[1], sW + L.off[1] + L.Kp[1] * L.Np[1], 64, 0, kChunk / 8, c * (kChunk / 8),
-                      128, c > 0);
-                commit(&s_bar[1 + (c & 1)]);
-            }
-        }
-        // wait for chunks 2 and 3 (the last commits on both buffers)
-        mbar_wait(&s_bar[1], ph1);
-        ph1 ^= 1;
-        mbar_wait(&s_bar[2], ph2);
-        ph2 ^= 1;
-        asm volatile("tcgen05.fence::after_thread_sync;");
-        // ---- layers 3, 4, 5 (K = 64, 32, 16), operand in buffer 0/1 region (64 KB)
-        const int lin[3] = {128, 192, 224};     // TMEM column of the layer input
-        const int lout[3] = {192, 224, 240};    // TMEM column of the layer output
-        const int Kin[3] = {64, 32, 16};
-        const float* bin[3] = {bias2, bias3, bias4};
-        for (int l = 2; l < 5; ++l) {
-            const int i = l - 2;
-            const int K = Kin[i];
-            float* Ahi = sA;
-            float* Alo = sA + kTile * K;
-            for (int c0 = 0; c0 < K; c0 += 16) {
-                float v[16];
-                tmem_ld16(lane_base + lin[i] + c0, v);
-#pragma unroll
-                for (int j = 0; j < 16; ++j) v[j] = fmaxf(v[j] + bin[i][c0 + j], 0.0f);
-                put_row(Ahi, Alo, c0, v, 16);
-            }
-            sync_for_mma();
-            if (tid == 0) {
-                issue(Ahi, Alo, 0, sW + L.off[l], sW + L.off[l] + L.Kp[l] * L.Np[l], L.Np[l], 0, K / 8, 0, lout[i],
-                      false);
-                commit(&s_bar[0]);
-            }
-            mbar_wait(&s_bar[0], ph0);
-            ph0 ^= 1;
-            asm volatile("tcgen05.fence::after_thread_sync;");
-        }
+        });
+        layer(1, 128, 128, from_tmem(0, s_bias));
+        layer(2, 64, 192, from_tmem(128, s_bias + 128));
+        layer(3, 32, 224, from_tmem(192, s_bias + 192));
+        layer(4, 16, 240, from_tmem(224, s_bias + 224));
         // ---- output layer (no activation)
         {
             float v[16];
             tmem_ld16(lane_base + 240, v);
             if (rv)
-                for (int d = 0; d < a.D; ++d) a.out[row * a.D + d] = v[d] + bias5[d];
+                for (int d = 0; d < a.D; ++d) a.out[row * a.D + d] = v[d] + s_bias[240 + d];
         }
-        asm volatile("tcgen05.fence::before_thread_sync;");
-        __syncthreads();   // TMEM and operand buffers reused by the next tile
-        asm volatile("tcgen05.fence::after_thread_sync;");
     }
+    asm volatile("tcgen05.fence::before_thread_sync;");
     __syncthreads();
-    if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 256;" ::"r"(tmem));
+    if (warp == 0)
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(s_tmem), "r"(256 * kGroups));
 }
 
 __global__ void k_plan_cost_combine(const double* comp, const float* fwd, const float* bwd, const uint8_t* ok,
@@ -386,9 +355,9 @@ ns_status launch_plan_cost_tc(ns_ctx* ctx, long long pb, long long pe, const dou
     a.n_tiles = (int)((pe - pb + kTile - 1) / kTile);
     // weight floats: 2 * sum(Kp * Np)
     const int wfl = 2 * (a.K0p * 128 + 128 * 64 + 64 * 32 + 32 * 16 + 16 * 16);
-    const size_t smem = (size_t)(wfl + 2 * kTile * 32 * 2) * sizeof(float) + 128;
+    const size_t smem = (size_t)(wfl + kGroups * 2 * kABuf) * sizeof(float) + 128;
     cudaFuncSetAttribute(k_plan_mlp_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    const int grid = std::min(a.n_tiles, ctx->sm_count);
+    const int grid = std::min((a.n_tiles + kGroups - 1) / kGroups, ctx->sm_count);
     for (int dir = 0; dir < 2; ++dir) {
         a.dir = dir;
         a.out = dir == 0 ? fbuf : bbuf;
@@ -397,7 +366,7 @@ ns_status launch_plan_cost_tc(ns_ctx* ctx, long long pb, long long pe, const dou
             a.b[l] = ctx->model.cb[dir][l];
         }
         prof_begin(ctx, PK_FINALIZE);
-        k_plan_mlp_tc<<<grid, 128, smem, ctx->stream>>>(a);
+        k_plan_mlp_tc<<<grid, 128 * kGroups, smem, ctx->stream>>>(a);
         prof_end(ctx);
         NS_LAUNCHED(ctx);
     }
