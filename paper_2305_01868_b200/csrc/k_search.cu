@@ -779,8 +779,9 @@ __global__ void __launch_bounds__(NS_DEDUP_WPB * 32, (LPD >= 8 ? NS_DEDUP_BLOCKS
 #endif
     const long long gw = (long long)blockIdx.x * nw + wl;
     double* scr = x.scratch + (size_t)gw * M * D * kV;   // this warp's group states
-    // state slice of group gr >= 1 owned by this lane (device dd, part)
-    auto gptr = [&](int gr, int dd) -> double* { return scr + ((size_t)gr * D + dd) * kV + part * FPL; };
+    // state slice of group gr >= 1 owned by this lane (its device, part)
+    double* const scr_l = scr + (size_t)(dev ? d : 0) * kV + part * FPL;
+    auto gptr = [&](int gr) -> double* { return scr_l + (size_t)gr * D * kV; };
     int8_t* hist = x.hist + (size_t)gw * M * a.Tpm;       // this warp's group histories
     // dynamic column-plan queue (column plans differ in length and in how many
     // groups they split into; a static stride leaves a long tail)
@@ -853,253 +854,258 @@ __global__ void __launch_bounds__(NS_DEDUP_WPB * 32, (LPD >= 8 ? NS_DEDUP_BLOCKS
             }
             cp_async_commit();   // one group per step, empty past the end
         };
-        auto process = [&](const auto& vcd, const int dt, const long long bt, const int idx, const int p) {
-            const int ng0 = ng;
-#pragma unroll 1
-            for (int gr = 0; gr < ng0; ++gr) {
-                // ---- score the D devices once for the whole group (R5: after insertion)
-                const int gcap_gr = gr == 0 ? r_gcap : s.gcap[gr];
-                if (gcap_gr < 0) continue;   // group without live members
-                const int dsum = gr == 0 ? r_dsum : (dev ? s.gd[gr][d] : 0);
-                const long long bsum = gr == 0 ? r_bsum : (dev ? s.gb[gr][d] : 0);
-                const bool f = dev && (bsum + bt <= cap) && (dsum + dt <= gcap_gr);
-                double* ug = gptr(gr, dev ? d : 0);   // valid for gr >= 1
-                double ps = 0.0;
-                if (f) {
-                    double acc[4] = {0.0, 0.0, 0.0, 0.0};
-                    if (gr == 0) {
+        // one group's pass over table t (G0: group 0, register-resident state)
+        auto pass = [&](auto g0tag, const int gr, const auto& vcd, const int dt, const long long bt, const int idx,
+                        const int p) {
+            constexpr bool G0 = decltype(g0tag)::value;
+            // ---- score the D devices once for the whole group (R5: after insertion)
+            const int gcap_gr = G0 ? r_gcap : s.gcap[gr];
+            if (gcap_gr < 0) return;   // group without live members
+            const int dsum = G0 ? r_dsum : (dev ? s.gd[gr][d] : 0);
+            const long long bsum = G0 ? r_bsum : (dev ? s.gb[gr][d] : 0);
+            const bool f = dev && (bsum + bt <= cap) && (dsum + dt <= gcap_gr);
+            double* ug = gptr(gr);   // valid for gr >= 1
+            double ps = 0.0;
+            if (f) {
+                double acc[4] = {0.0, 0.0, 0.0, 0.0};
+                if (G0) {
 #pragma unroll
-                        for (int k = 0; k < FPL; ++k) acc[k & 3] = fma(GW(k), relu_hi(u0[k] + vcd[k]), acc[k & 3]);
-                    } else {
+                    for (int k = 0; k < FPL; ++k) acc[k & 3] = fma(GW(k), relu_hi(u0[k] + vcd[k]), acc[k & 3]);
+                } else {
 #pragma unroll
-                        for (int k = 0; k < FPL; ++k) acc[k & 3] = fma(GW(k), relu_hi(ug[k] + vcd[k]), acc[k & 3]);
+                    for (int k = 0; k < FPL; ++k) acc[k & 3] = fma(GW(k), relu_hi(ug[k] + vcd[k]), acc[k & 3]);
+                }
+                ps = (acc[0] + acc[1]) + (acc[2] + acc[3]);
+            }
+            const double sco = a.head.hb2 + lane_group_sum<LPD>(ps);
+            const int gmin_gr = G0 ? r_gmin : s.gmin[gr];
+            // ---- fast path: every live member's cap admits every scored
+            //      device -> all members see the same feasible set and take
+            //      the group argmin (no split, uniform work)
+            {
+                int smax = f ? dsum + dt : 0;
+#pragma unroll
+                for (int o = 16; o >= LPD; o >>= 1) smax = max(smax, __shfl_xor_sync(kFull, smax, o));
+                if (smax <= gmin_gr) {
+                    // device argmin: butterfly minimum, then the lowest device
+                    // attaining it (R13) from one ballot
+                    const double own = f ? sco : CUDART_INF;
+                    double bs = own;
+#pragma unroll
+                    for (int o = 16; o >= LPD; o >>= 1) {
+                        // plain select (scores are never NaN): no fmin NaN fix-ups
+                        const double ob = __shfl_xor_sync(kFull, bs, o);
+                        bs = ob < bs ? ob : bs;
                     }
-                    ps = (acc[0] + acc[1]) + (acc[2] + acc[3]);
-                }
-                const double sco = a.head.hb2 + lane_group_sum<LPD>(ps);
-                const int gmin_gr = gr == 0 ? r_gmin : s.gmin[gr];
-                // ---- fast path: every live member's cap admits every scored
-                //      device -> all members see the same feasible set and take
-                //      the group argmin (no split, uniform work)
-                {
-                    int smax = f ? dsum + dt : 0;
-#pragma unroll
-                    for (int o = 16; o >= LPD; o >>= 1) smax = max(smax, __shfl_xor_sync(kFull, smax, o));
-                    if (smax <= gmin_gr) {
-                        // device argmin: butterfly minimum, then the lowest device
-                        // attaining it (R13) from one ballot
-                        const double own = f ? sco : CUDART_INF;
-                        double bs = own;
-#pragma unroll
-                        for (int o = 16; o >= LPD; o >>= 1) {
-                            // plain select (scores are never NaN): no fmin NaN fix-ups
-                            const double ob = __shfl_xor_sync(kFull, bs, o);
-                            bs = ob < bs ? ob : bs;
-                        }
-                        const unsigned nf = __popc(__ballot_sync(kFull, f && part == 0));
-                        const unsigned hit = __ballot_sync(kFull, f && part == 0 && own == bs);
-                        const int bd = (__ffs(hit) - 1) / LPD;
-                        if (bs == CUDART_INF) {   // nothing feasible: the whole group strands (R9)
-                            const uint32_t gwk = gr == 0 ? r_gwork : s.gwork[gr];
-#pragma unroll
-                            for (int m0 = 0; m0 < MC; m0 += 32) {
-                                const int m = m0 + lane;
-                                if (m < M && s.mgroup[m] == gr) {
-                                    s.mwork[m] += gwk;
-                                    s.mgroup[m] = -1;
-                                }
-                            }
-                            if (gr == 0) r_gcap = -1;
-                            __syncwarp();
-                            if (gr != 0 && lane == 0) s.gcap[gr] = -1;
-                            __syncwarp();
-                            continue;
-                        }
-                        if (d == bd) {
-                            if (gr == 0) {
-#pragma unroll
-                                for (int k = 0; k < FPL; ++k) u0[k] += vcd[k];
-                            } else {
-#pragma unroll
-                                for (int k = 0; k < FPL; ++k) ug[k] += vcd[k];
-                            }
-                        }
-                        if (lane == 0) hist[(size_t)gr * a.Tpm + idx] = (int8_t)bd;
-                        if (gr == 0) {
-                            if (d == bd) {
-                                r_dsum += dt;
-                                r_bsum += bt;
-                            }
-                            r_gwork += nf;
-                        } else {
-                            if (lane == 0) {
-                                s.gd[gr][bd] += dt;
-                                s.gb[gr][bd] += bt;
-                                s.gwork[gr] += nf;
-                            }
-                            __syncwarp();
-                        }
-                        continue;
-                    }
-                }
-                if (part == 0 && d < DPW) {
-                    s.sc[d] = sco;
-                    s.sdv[d] = dsum + dt;
-                    s.sok[d] = f ? 1 : 0;
-                }
-                __syncwarp();
-                // ---- every member takes its own argmin over its own feasible set
-                //      (dim cap of its grid point; lowest device on ties, R13)
-                const uint32_t gwk = gr == 0 ? r_gwork : s.gwork[gr];
-                int first = M;
-                bool left = false;
-#pragma unroll
-                for (int m0 = 0; m0 < MC; m0 += 32) {
-                    const int m = m0 + lane;
-                    int pick = -2;
-                    if (m < M && s.mgroup[m] == gr) {
-                        double best = CUDART_INF;
-                        int bd = -1;
-                        uint32_t cnt = 0;
-                        const int cm = s.mcap[m];
-                        for (int dd = 0; dd < D; ++dd) {
-                            if (s.sok[dd] && s.sdv[dd] <= cm) {
-                                ++cnt;
-                                const double sv = s.sc[dd];
-                                if (sv < best) {
-                                    best = sv;
-                                    bd = dd;
-                                }
-                            }
-                        }
-                        s.mwork[m] += cnt;
-                        if (bd < 0) {
-                            s.mwork[m] += gwk;
-                            s.mgroup[m] = -1;   // R9: stranded -> grid point infeasible
-                            pick = -1;
-                        } else {
-                            pick = bd;
-                        }
-                    }
-                    if (m < M) s.mpick[m] = pick;
-                    const unsigned live = __ballot_sync(kFull, pick >= 0);
-                    left |= __any_sync(kFull, pick == -1);
-                    // the group keeps the pick of its LOOSEST-cap live member (highest m):
-                    // tight caps bind first, so the splitting members are the few
-                    // tight ones and the majority stays in the register-resident group
-                    if (live) first = m0 + 31 - __clz(live);
-                }
-                __syncwarp();
-                if (first == M) {   // every member stranded
-                    if (gr == 0) r_gcap = -1;
-                    else if (lane == 0) s.gcap[gr] = -1;
-                    __syncwarp();
-                    continue;
-                }
-                const int main_pick = s.mpick[first];
-                bool split = false;
-#pragma unroll
-                for (int m0 = 0; m0 < MC; m0 += 32) {
-                    const int m = m0 + lane;
-                    split |= __any_sync(kFull, m < M && s.mpick[m] >= 0 && s.mpick[m] != main_pick);
-                }
-                // ---- members choosing another device split off (state before the update)
-                if (split) {
-                    for (int dd = 0; dd < D; ++dd) {
-                        if (dd == main_pick) continue;
-                        int any = 0, c2 = -1, c2min = INT_MAX;
+                    const unsigned nf = __popc(__ballot_sync(kFull, f && part == 0));
+                    const unsigned hit = __ballot_sync(kFull, f && part == 0 && own == bs);
+                    const int bd = (__ffs(hit) - 1) / LPD;
+                    if (bs == CUDART_INF) {   // nothing feasible: the whole group strands (R9)
+                        const uint32_t gwk = G0 ? r_gwork : s.gwork[gr];
 #pragma unroll
                         for (int m0 = 0; m0 < MC; m0 += 32) {
                             const int m = m0 + lane;
-                            const bool mine = m < M && s.mpick[m] == dd;
-                            if (mine) {
-                                s.mgroup[m] = ng;
-                                s.mwork[m] += gwk;   // bank the old group's uniform work
-                                c2 = max(c2, s.mcap[m]);
-                                c2min = min(c2min, s.mcap[m]);
+                            if (m < M && s.mgroup[m] == gr) {
+                                s.mwork[m] += gwk;
+                                s.mgroup[m] = -1;
                             }
-                            any |= __any_sync(kFull, mine);
                         }
-                        if (!any) continue;
+                        if (G0) r_gcap = -1;
+                        __syncwarp();
+                        if (!G0 && lane == 0) s.gcap[gr] = -1;
+                        __syncwarp();
+                        return;
+                    }
+                    if (d == bd) {
+                        if (G0) {
 #pragma unroll
-                        for (int o = 16; o > 0; o >>= 1) {
-                            c2 = max(c2, __shfl_xor_sync(kFull, c2, o));
-                            c2min = min(c2min, __shfl_xor_sync(kFull, c2min, o));
-                        }
-                        // new group ng = state(gr) + v_t on device dd
-                        if (dev) {
-                            double* un = gptr(ng, d);
+                            for (int k = 0; k < FPL; ++k) u0[k] += vcd[k];
+                        } else {
 #pragma unroll
-                            for (int k = 0; k < FPL; ++k) {
-                                double val = gr == 0 ? u0[k] : ug[k];
-                                if (d == dd) val += vcd[k];
-                                un[k] = val;
-                            }
-                            if (part == 0) {
-                                s.gd[ng][d] = dsum + (d == dd ? dt : 0);
-                                s.gb[ng][d] = bsum + (d == dd ? bt : 0);
-                            }
+                            for (int k = 0; k < FPL; ++k) ug[k] += vcd[k];
                         }
+                    }
+                    if (lane == 0) hist[(size_t)gr * a.Tpm + idx] = (int8_t)bd;
+                    if (G0) {
+                        if (d == bd) {
+                            r_dsum += dt;
+                            r_bsum += bt;
+                        }
+                        r_gwork += nf;
+                    } else {
                         if (lane == 0) {
-                            s.gcap[ng] = c2;
-                            s.gmin[ng] = c2min;
-                            s.gwork[ng] = 0;
-                            s.gpar[ng] = gr;
-                            s.gstep[ng] = p;
-                            hist[(size_t)ng * a.Tpm + idx] = (int8_t)dd;
+                            s.gd[gr][bd] += dt;
+                            s.gb[gr][bd] += bt;
+                            s.gwork[gr] += nf;
                         }
-                        ++ng;
                         __syncwarp();
                     }
+                    return;
                 }
-                // ---- the group itself takes main_pick
-                if (d == main_pick) {
-                    if (gr == 0) {
+            }
+            if (part == 0 && d < DPW) {
+                s.sc[d] = sco;
+                s.sdv[d] = dsum + dt;
+                s.sok[d] = f ? 1 : 0;
+            }
+            __syncwarp();
+            // ---- every member takes its own argmin over its own feasible set
+            //      (dim cap of its grid point; lowest device on ties, R13)
+            const uint32_t gwk = G0 ? r_gwork : s.gwork[gr];
+            int first = M;
+            bool left = false;
 #pragma unroll
-                        for (int k = 0; k < FPL; ++k) u0[k] += vcd[k];
+            for (int m0 = 0; m0 < MC; m0 += 32) {
+                const int m = m0 + lane;
+                int pick = -2;
+                if (m < M && s.mgroup[m] == gr) {
+                    double best = CUDART_INF;
+                    int bd = -1;
+                    uint32_t cnt = 0;
+                    const int cm = s.mcap[m];
+                    for (int dd = 0; dd < D; ++dd) {
+                        if (s.sok[dd] && s.sdv[dd] <= cm) {
+                            ++cnt;
+                            const double sv = s.sc[dd];
+                            if (sv < best) {
+                                best = sv;
+                                bd = dd;
+                            }
+                        }
+                    }
+                    s.mwork[m] += cnt;
+                    if (bd < 0) {
+                        s.mwork[m] += gwk;
+                        s.mgroup[m] = -1;   // R9: stranded -> grid point infeasible
+                        pick = -1;
                     } else {
-#pragma unroll
-                        for (int k = 0; k < FPL; ++k) ug[k] += vcd[k];
+                        pick = bd;
                     }
                 }
-                int c3 = gcap_gr, c3min = gmin_gr;
-                if (split || left) {   // members left: tighten the group's cap range
-                    c3 = -1;
-                    c3min = INT_MAX;
+                if (m < M) s.mpick[m] = pick;
+                const unsigned live = __ballot_sync(kFull, pick >= 0);
+                left |= __any_sync(kFull, pick == -1);
+                // the group keeps the pick of its LOOSEST-cap live member (highest m):
+                // tight caps bind first, so the splitting members are the few
+                // tight ones and the majority stays in the register-resident group
+                if (live) first = m0 + 31 - __clz(live);
+            }
+            __syncwarp();
+            if (first == M) {   // every member stranded
+                if (G0) r_gcap = -1;
+                else if (lane == 0) s.gcap[gr] = -1;
+                __syncwarp();
+                return;
+            }
+            const int main_pick = s.mpick[first];
+            bool split = false;
+#pragma unroll
+            for (int m0 = 0; m0 < MC; m0 += 32) {
+                const int m = m0 + lane;
+                split |= __any_sync(kFull, m < M && s.mpick[m] >= 0 && s.mpick[m] != main_pick);
+            }
+            // ---- members choosing another device split off (state before the update)
+            if (split) {
+                for (int dd = 0; dd < D; ++dd) {
+                    if (dd == main_pick) continue;
+                    int any = 0, c2 = -1, c2min = INT_MAX;
 #pragma unroll
                     for (int m0 = 0; m0 < MC; m0 += 32) {
                         const int m = m0 + lane;
-                        if (m < M && s.mgroup[m] == gr) {
-                            c3 = max(c3, s.mcap[m]);
-                            c3min = min(c3min, s.mcap[m]);
+                        const bool mine = m < M && s.mpick[m] == dd;
+                        if (mine) {
+                            s.mgroup[m] = ng;
+                            s.mwork[m] += gwk;   // bank the old group's uniform work
+                            c2 = max(c2, s.mcap[m]);
+                            c2min = min(c2min, s.mcap[m]);
                         }
+                        any |= __any_sync(kFull, mine);
                     }
+                    if (!any) continue;
 #pragma unroll
                     for (int o = 16; o > 0; o >>= 1) {
-                        c3 = max(c3, __shfl_xor_sync(kFull, c3, o));
-                        c3min = min(c3min, __shfl_xor_sync(kFull, c3min, o));
+                        c2 = max(c2, __shfl_xor_sync(kFull, c2, o));
+                        c2min = min(c2min, __shfl_xor_sync(kFull, c2min, o));
                     }
-                }
-                if (lane == 0) hist[(size_t)gr * a.Tpm + idx] = (int8_t)main_pick;
-                if (gr == 0) {
-                    if (d == main_pick) {
-                        r_dsum += dt;
-                        r_bsum += bt;
+                    // new group ng = state(gr) + v_t on device dd
+                    if (dev) {
+                        double* un = gptr(ng);
+#pragma unroll
+                        for (int k = 0; k < FPL; ++k) {
+                            double val = G0 ? u0[k] : ug[k];
+                            if (d == dd) val += vcd[k];
+                            un[k] = val;
+                        }
+                        if (part == 0) {
+                            s.gd[ng][d] = dsum + (d == dd ? dt : 0);
+                            s.gb[ng][d] = bsum + (d == dd ? bt : 0);
+                        }
                     }
-                    r_gcap = c3;
-                    r_gmin = c3min;
-                    __syncwarp();
-                } else {
-                    __syncwarp();
                     if (lane == 0) {
-                        s.gd[gr][main_pick] += dt;
-                        s.gb[gr][main_pick] += bt;
-                        s.gcap[gr] = c3;
-                        s.gmin[gr] = c3min;
+                        s.gcap[ng] = c2;
+                        s.gmin[ng] = c2min;
+                        s.gwork[ng] = 0;
+                        s.gpar[ng] = gr;
+                        s.gstep[ng] = p;
+                        hist[(size_t)ng * a.Tpm + idx] = (int8_t)dd;
                     }
+                    ++ng;
                     __syncwarp();
                 }
             }
+            // ---- the group itself takes main_pick
+            if (d == main_pick) {
+                if (G0) {
+#pragma unroll
+                    for (int k = 0; k < FPL; ++k) u0[k] += vcd[k];
+                } else {
+#pragma unroll
+                    for (int k = 0; k < FPL; ++k) ug[k] += vcd[k];
+                }
+            }
+            int c3 = gcap_gr, c3min = gmin_gr;
+            if (split || left) {   // members left: tighten the group's cap range
+                c3 = -1;
+                c3min = INT_MAX;
+#pragma unroll
+                for (int m0 = 0; m0 < MC; m0 += 32) {
+                    const int m = m0 + lane;
+                    if (m < M && s.mgroup[m] == gr) {
+                        c3 = max(c3, s.mcap[m]);
+                        c3min = min(c3min, s.mcap[m]);
+                    }
+                }
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) {
+                    c3 = max(c3, __shfl_xor_sync(kFull, c3, o));
+                    c3min = min(c3min, __shfl_xor_sync(kFull, c3min, o));
+                }
+            }
+            if (lane == 0) hist[(size_t)gr * a.Tpm + idx] = (int8_t)main_pick;
+            if (G0) {
+                if (d == main_pick) {
+                    r_dsum += dt;
+                    r_bsum += bt;
+                }
+                r_gcap = c3;
+                r_gmin = c3min;
+                __syncwarp();
+            } else {
+                __syncwarp();
+                if (lane == 0) {
+                    s.gd[gr][main_pick] += dt;
+                    s.gb[gr][main_pick] += bt;
+                    s.gcap[gr] = c3;
+                    s.gmin[gr] = c3min;
+                }
+                __syncwarp();
+            }
+                };
+        auto process = [&](const auto& vcd, const int dt, const long long bt, const int idx, const int p) {
+            const int ng0 = ng;
+            pass(std::true_type{}, 0, vcd, dt, bt, idx, p);
+#pragma unroll 1
+            for (int gr = 1; gr < ng0; ++gr) pass(std::false_type{}, gr, vcd, dt, bt, idx, p);
         };
 #pragma unroll 1
         for (int pp = 0; pp < kDStages - 1; ++pp) issue(pp);
@@ -1153,7 +1159,7 @@ __global__ void __launch_bounds__(NS_DEDUP_WPB * 32, (LPD >= 8 ? NS_DEDUP_BLOCKS
                 hp = part_head<FPL>(u0, w);
             } else {
                 double tu[FPL];
-                const double* ug = gptr(gr, dev ? d : 0);
+                const double* ug = gptr(gr);
 #pragma unroll
                 for (int k = 0; k < FPL; ++k) tu[k] = ug[k];
                 hp = part_head<FPL>(tu, w);
