@@ -725,7 +725,7 @@ struct __align__(16) DedupSmem {
     static constexpr int SS = FPL * 8 + 16;   // ring slice stride (bytes): +16 B keeps the LPD
     static constexpr int RS = LPD * SS;       //   slices of a row on distinct banks
     unsigned char ring[kDStages][RS];          // staged v rows of the next tables
-    long long gb[MC][DPW];                    // group bytes per device (groups >= 1)
+    long long gb[MC][DPW];                    // group memory headroom cap - bytes per device (groups >= 1)
     int4 meta[kDStages];                       // staged {dim, list index, bytes lo, bytes hi}
     double sc[DPW];                           // scores of the current group
     int gd[MC][DPW];                          // group dims per device (groups >= 1)
@@ -758,6 +758,8 @@ __global__ void __launch_bounds__(NS_DEDUP_WPB * 32, (LPD >= 8 ? NS_DEDUP_BLOCKS
     const int d = lane / LPD, part = lane % LPD;
     const bool dev = d < D;
     SM& s = reinterpret_cast<SM*>(dsm)[wl];
+    // this lane's 16-byte chunk of a staged v row (slot 0; + slot * RS)
+    unsigned char* const ring_lane = &s.ring[0][(lane / (FPL / 2)) * SS + (lane % (FPL / 2)) * 16];
     // hb1 (the empty-device pre-activation) is re-read from shared memory at
     // every column plan instead of occupying FPL registers for the whole kernel
     __shared__ double s_hb1[kV];
@@ -829,7 +831,7 @@ __global__ void __launch_bounds__(NS_DEDUP_WPB * 32, (LPD >= 8 ? NS_DEDUP_BLOCKS
             cmin = min(cmin, __shfl_xor_sync(kFull, cmin, o));
         }
         int r_dsum = 0, r_gcap = cmax, r_gmin = cmin;
-        long long r_bsum = 0;
+        long long r_bhr = cap;   // group 0: per-device memory headroom cap - bytes_d (this lane's device)
         uint32_t r_gwork = 0;
 #pragma unroll
         for (int k = 0; k < FPL; ++k) u0[k] = s_hb1[part * FPL + k];
@@ -840,19 +842,21 @@ __global__ void __launch_bounds__(NS_DEDUP_WPB * 32, (LPD >= 8 ? NS_DEDUP_BLOCKS
         // row-index window: the next 32 entries of the cost order in one register per lane
         int oc_cur = lane < Tp ? __ldg(orow + lane) : 0;
         int oc_nxt = 32 + lane < Tp ? __ldg(orow + 32 + lane) : 0;
-        auto issue = [&](int pp) {   // stage table pp of the cost order into ring slot pp % kDStages
+        // ring slots rotate with counters (no modulo): table pp goes to slot
+        // pp % kDStages == sl_w at its issue
+        int sl_w = 0;
+        auto issue = [&](int pp) {   // stage table pp of the cost order into ring slot sl_w
             if (pp < Tp) {
                 if (pp > 0 && (pp & 31) == 0) {
                     oc_cur = oc_nxt;
                     oc_nxt = pp + 32 + lane < Tp ? __ldg(orow + pp + 32 + lane) : 0;
                 }
                 const int r = __shfl_sync(kFull, oc_cur, pp & 31);
-                const int sl = pp % kDStages;
-                constexpr int CPS = FPL / 2;   // 16-byte chunks per slice
-                cp_async16(&s.ring[sl][(lane / CPS) * SS + (lane % CPS) * 16], a.V + (size_t)r * kV + 2 * lane);
-                if (lane == 0) cp_async16(&s.meta[sl], ometa + pp);
+                cp_async16(ring_lane + sl_w * SM::RS, a.V + (size_t)r * kV + 2 * lane);
+                if (lane == 0) cp_async16(&s.meta[sl_w], ometa + pp);
             }
             cp_async_commit();   // one group per step, empty past the end
+            sl_w = sl_w + 1 == kDStages ? 0 : sl_w + 1;
         };
         // one group's pass over table t (G0: group 0, register-resident state)
         auto pass = [&](auto g0tag, const int gr, const auto& vcd, const int dt, const long long bt, const int idx,
@@ -862,8 +866,8 @@ __global__ void __launch_bounds__(NS_DEDUP_WPB * 32, (LPD >= 8 ? NS_DEDUP_BLOCKS
             const int gcap_gr = G0 ? r_gcap : s.gcap[gr];
             if (gcap_gr < 0) return;   // group without live members
             const int dsum = G0 ? r_dsum : (dev ? s.gd[gr][d] : 0);
-            const long long bsum = G0 ? r_bsum : (dev ? s.gb[gr][d] : 0);
-            const bool f = dev && (bsum + bt <= cap) && (dsum + dt <= gcap_gr);
+            const long long bhr = G0 ? r_bhr : (dev ? s.gb[gr][d] : 0);   // memory headroom
+            const bool f = dev && (bt <= bhr) && (dsum + dt <= gcap_gr);
             double* ug = gptr(gr);   // valid for gr >= 1
             double ps = 0.0;
             if (f) {
@@ -929,13 +933,13 @@ __global__ void __launch_bounds__(NS_DEDUP_WPB * 32, (LPD >= 8 ? NS_DEDUP_BLOCKS
                     if (G0) {
                         if (d == bd) {
                             r_dsum += dt;
-                            r_bsum += bt;
+                            r_bhr -= bt;
                         }
                         r_gwork += nf;
                     } else {
                         if (lane == 0) {
                             s.gd[gr][bd] += dt;
-                            s.gb[gr][bd] += bt;
+                            s.gb[gr][bd] -= bt;
                             s.gwork[gr] += nf;
                         }
                         __syncwarp();
@@ -1038,7 +1042,7 @@ __global__ void __launch_bounds__(NS_DEDUP_WPB * 32, (LPD >= 8 ? NS_DEDUP_BLOCKS
                         }
                         if (part == 0) {
                             s.gd[ng][d] = dsum + (d == dd ? dt : 0);
-                            s.gb[ng][d] = bsum + (d == dd ? bt : 0);
+                            s.gb[ng][d] = bhr - (d == dd ? bt : 0);
                         }
                     }
                     if (lane == 0) {
@@ -1085,7 +1089,7 @@ __global__ void __launch_bounds__(NS_DEDUP_WPB * 32, (LPD >= 8 ? NS_DEDUP_BLOCKS
             if (G0) {
                 if (d == main_pick) {
                     r_dsum += dt;
-                    r_bsum += bt;
+                    r_bhr -= bt;
                 }
                 r_gcap = c3;
                 r_gmin = c3min;
@@ -1094,7 +1098,7 @@ __global__ void __launch_bounds__(NS_DEDUP_WPB * 32, (LPD >= 8 ? NS_DEDUP_BLOCKS
                 __syncwarp();
                 if (lane == 0) {
                     s.gd[gr][main_pick] += dt;
-                    s.gb[gr][main_pick] += bt;
+                    s.gb[gr][main_pick] -= bt;
                     s.gcap[gr] = c3;
                     s.gmin[gr] = c3min;
                 }
@@ -1109,13 +1113,13 @@ __global__ void __launch_bounds__(NS_DEDUP_WPB * 32, (LPD >= 8 ? NS_DEDUP_BLOCKS
         };
 #pragma unroll 1
         for (int pp = 0; pp < kDStages - 1; ++pp) issue(pp);
+        int sl = 0;   // slot of table p
 #pragma unroll 1
-        for (int p = 0; p < Tp; ++p) {
+        for (int p = 0; p < Tp; ++p, sl = sl + 1 == kDStages ? 0 : sl + 1) {
             __syncwarp();                  // slot (p - 1) % kDStages fully consumed
             issue(p + kDStages - 1);
             cp_async_wait<kDStages - 1>();  // table p has landed (this lane's copies)
             __syncwarp();                  // ... and every lane's
-            const int sl = p % kDStages;
 #ifdef NS_GV_SMEM
             // v_t read from the ring slice at each use (not held in registers)
             const double* vcd = reinterpret_cast<const double*>(&s.ring[sl][part * SS]);
