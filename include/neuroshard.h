@@ -67,8 +67,10 @@ ns_status ns_set_stream(ns_ctx* ctx, void* cuda_stream);
 ns_status ns_synchronize(ns_ctx* ctx);
 /* Number of kernels this ctx has launched since creation (bench evidence). */
 uint64_t ns_kernel_launches(const ns_ctx* ctx);
-/* Kernel timers: with enable != 0 every launch is bracketed by CUDA events on
- * the ctx stream; ns_profile resets the accumulators.  ns_profile_query
+/* Kernel timers: with enable == 1 every launch is bracketed by CUDA events on
+ * the ctx stream; enable > 1 is a class mask (bit k + 1 times kernel class k
+ * of the list below, in order, e.g. 1 << 5 = "greedy" only); 0 turns them
+ * off.  ns_profile resets the accumulators.  ns_profile_query
  * returns the summed device time (ms) and launch count of one kernel class:
  * "precompute" (N1), "validate", "order", "expand" (N3), "greedy" (N4),
  * "finalize" (N5), "select" (N6), "score" (N2), "other".  Both synchronise

@@ -145,8 +145,15 @@ def ns_kernel_launches(ctx: int) -> int:
     return int(LIB.ns_kernel_launches(ctx))
 
 
-def ns_profile(ctx: int, enable: bool) -> None:
-    _check(ctx, LIB.ns_profile(ctx, 1 if enable else 0))
+def ns_profile(ctx: int, enable: bool, kinds=None) -> None:
+    """Kernel timers on/off; kinds = iterable of PROFILE_KINDS names to time
+    only those classes (fewer events inside a timed region)."""
+    mode = 1 if enable else 0
+    if enable and kinds is not None:
+        mode = 0
+        for k in kinds:
+            mode |= 1 << (PROFILE_KINDS.index(k) + 1)
+    _check(ctx, LIB.ns_profile(ctx, mode))
 
 
 PROFILE_KINDS = ("precompute", "validate", "order", "expand", "greedy", "finalize", "select", "score", "other")

@@ -670,6 +670,9 @@ constexpr int kStages = 8;   // row-stream ring depth (large-D greedy)
 #define NS_DSTAGES 6
 #endif
 constexpr int kDStages = NS_DSTAGES;   // row-stream ring depth of the grouped greedy
+#ifndef NS_G1SM
+#define NS_G1SM 1   // group 1 of the grouped greedy in shared memory (typed pass)
+#endif
 
 // ---------------------------------------------------------------------------
 // Grouped greedy (used for D <= 16): one WARP per column plan, all M grid
@@ -725,6 +728,9 @@ struct __align__(16) DedupSmem {
     static constexpr int SS = FPL * 8 + 16;   // ring slice stride (bytes): +16 B keeps the LPD
     static constexpr int RS = LPD * SS;       //   slices of a row on distinct banks
     unsigned char ring[kDStages][RS];          // staged v rows of the next tables
+#if NS_G1SM
+    double g1[32][FPL + 2];                   // group 1's state (per-lane slices, 16 B pad)
+#endif
     long long gb[MC][DPW];                    // group memory headroom cap - bytes per device (groups >= 1)
     int4 meta[kDStages];                       // staged {dim, list index, bytes lo, bytes hi}
     double sc[DPW];                           // scores of the current group
@@ -784,6 +790,10 @@ __global__ void __launch_bounds__(NS_DEDUP_WPB * 32, (LPD >= 8 ? NS_DEDUP_BLOCKS
     // state slice of group gr >= 1 owned by this lane (its device, part)
     double* const scr_l = scr + (size_t)(dev ? d : 0) * kV + part * FPL;
     auto gptr = [&](int gr) -> double* { return scr_l + (size_t)gr * D * kV; };
+#if NS_G1SM
+    // group 1's state in shared memory (this lane's slice, padded 16 B apart)
+    double* const g1_l = &s.g1[(dev ? d : 0) * LPD + part][0];
+#endif
     int8_t* hist = x.hist + (size_t)gw * M * a.Tpm;       // this warp's group histories
     // dynamic column-plan queue (column plans differ in length and in how many
     // groups they split into; a static stride leaves a long tail)
@@ -861,14 +871,19 @@ __global__ void __launch_bounds__(NS_DEDUP_WPB * 32, (LPD >= 8 ? NS_DEDUP_BLOCKS
         // one group's pass over table t (G0: group 0, register-resident state)
         auto pass = [&](auto g0tag, const int gr, const auto& vcd, const int dt, const long long bt, const int idx,
                         const int p) {
-            constexpr bool G0 = decltype(g0tag)::value;
+            constexpr int KIND = decltype(g0tag)::value;   // 0: group 0, 1: group 1 (smem), 2: others
+            constexpr bool G0 = KIND == 0;
             // ---- score the D devices once for the whole group (R5: after insertion)
             const int gcap_gr = G0 ? r_gcap : s.gcap[gr];
             if (gcap_gr < 0) return;   // group without live members
             const int dsum = G0 ? r_dsum : (dev ? s.gd[gr][d] : 0);
             const long long bhr = G0 ? r_bhr : (dev ? s.gb[gr][d] : 0);   // memory headroom
             const bool f = dev && (bt <= bhr) && (dsum + dt <= gcap_gr);
+#if NS_G1SM
+            double* ug = KIND == 1 ? g1_l : gptr(gr);   // valid for gr >= 1
+#else
             double* ug = gptr(gr);   // valid for gr >= 1
+#endif
             double ps = 0.0;
             if (f) {
                 double acc[4] = {0.0, 0.0, 0.0, 0.0};
@@ -1033,12 +1048,24 @@ __global__ void __launch_bounds__(NS_DEDUP_WPB * 32, (LPD >= 8 ? NS_DEDUP_BLOCKS
                     }
                     // new group ng = state(gr) + v_t on device dd
                     if (dev) {
-                        double* un = gptr(ng);
+#if NS_G1SM
+                        if (ng == 1) {
 #pragma unroll
-                        for (int k = 0; k < FPL; ++k) {
-                            double val = G0 ? u0[k] : ug[k];
-                            if (d == dd) val += vcd[k];
-                            un[k] = val;
+                            for (int k = 0; k < FPL; ++k) {
+                                double val = G0 ? u0[k] : ug[k];
+                                if (d == dd) val += vcd[k];
+                                g1_l[k] = val;
+                            }
+                        } else
+#endif
+                        {
+                            double* un = gptr(ng);
+#pragma unroll
+                            for (int k = 0; k < FPL; ++k) {
+                                double val = G0 ? u0[k] : ug[k];
+                                if (d == dd) val += vcd[k];
+                                un[k] = val;
+                            }
                         }
                         if (part == 0) {
                             s.gd[ng][d] = dsum + (d == dd ? dt : 0);
@@ -1107,9 +1134,15 @@ __global__ void __launch_bounds__(NS_DEDUP_WPB * 32, (LPD >= 8 ? NS_DEDUP_BLOCKS
                 };
         auto process = [&](const auto& vcd, const int dt, const long long bt, const int idx, const int p) {
             const int ng0 = ng;
-            pass(std::true_type{}, 0, vcd, dt, bt, idx, p);
+            pass(std::integral_constant<int, 0>{}, 0, vcd, dt, bt, idx, p);
+#if NS_G1SM
+            if (ng0 > 1) pass(std::integral_constant<int, 1>{}, 1, vcd, dt, bt, idx, p);
 #pragma unroll 1
-            for (int gr = 1; gr < ng0; ++gr) pass(std::false_type{}, gr, vcd, dt, bt, idx, p);
+            for (int gr = 2; gr < ng0; ++gr) pass(std::integral_constant<int, 2>{}, gr, vcd, dt, bt, idx, p);
+#else
+#pragma unroll 1
+            for (int gr = 1; gr < ng0; ++gr) pass(std::integral_constant<int, 2>{}, gr, vcd, dt, bt, idx, p);
+#endif
         };
 #pragma unroll 1
         for (int pp = 0; pp < kDStages - 1; ++pp) issue(pp);
@@ -1163,7 +1196,11 @@ __global__ void __launch_bounds__(NS_DEDUP_WPB * 32, (LPD >= 8 ? NS_DEDUP_BLOCKS
                 hp = part_head<FPL>(u0, w);
             } else {
                 double tu[FPL];
+#if NS_G1SM
+                const double* ug = gr == 1 ? g1_l : gptr(gr);
+#else
                 const double* ug = gptr(gr);
+#endif
 #pragma unroll
                 for (int k = 0; k < FPL; ++k) tu[k] = ug[k];
                 hp = part_head<FPL>(tu, w);

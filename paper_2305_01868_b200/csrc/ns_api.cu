@@ -163,7 +163,9 @@ static cudaEvent_t prof_event(ns_ctx* ctx) {
 }
 
 void prof_begin(ns_ctx* ctx, int kind) {
-    if (!ctx->prof) return;
+    ctx->prof_open = false;
+    if (!ctx->prof || !((ctx->prof_mask >> kind) & 1u)) return;
+    ctx->prof_open = true;
     ProfPending p;
     p.kind = kind;
     p.a = prof_event(ctx);
@@ -173,7 +175,8 @@ void prof_begin(ns_ctx* ctx, int kind) {
 }
 
 void prof_end(ns_ctx* ctx) {
-    if (!ctx->prof || ctx->prof_pending.empty()) return;
+    if (!ctx->prof || !ctx->prof_open || ctx->prof_pending.empty()) return;
+    ctx->prof_open = false;
     ProfPending& p = ctx->prof_pending.back();
     p.b = prof_event(ctx);
     cudaEventRecord(p.b, ctx->stream);
@@ -307,7 +310,10 @@ ns_status ns_profile(ns_ctx* ctx, int32_t enable) {
     NS_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
     prof_collect(ctx);
     for (int k = 0; k < PK_COUNT; ++k) ctx->prof_acc[k] = ProfEntry();
+    // 1: every kernel class; > 1: bit (k + 1) times class k only (fewer
+    // events inside a timed region)
     ctx->prof = enable != 0;
+    ctx->prof_mask = enable == 1 ? 0xffffffffu : ((uint32_t)enable >> 1);
     return NS_OK;
 }
 

@@ -100,6 +100,8 @@ struct ns_ctx {
     int dstage_i = 0;
     // kernel timers
     bool prof = false;
+    uint32_t prof_mask = 0;   // kernel classes timed (bit k = class k)
+    bool prof_open = false;   // the last prof_begin recorded an event
     ns::ProfEntry prof_acc[ns::PK_COUNT];
     std::vector<ns::ProfPending> prof_pending;
     std::vector<cudaEvent_t> prof_free;
