@@ -770,21 +770,13 @@ __global__ void __launch_bounds__(NS_DEDUP_WPB * 32, (LPD >= 8 ? NS_DEDUP_BLOCKS
     // every column plan instead of occupying FPL registers for the whole kernel
     __shared__ double s_hb1[kV];
     for (int k = threadIdx.x; k < kV; k += blockDim.x) s_hb1[k] = a.head.hb1[k];
-#ifndef NS_GW_REGS
     // head weights as per-part slices padded 16 B apart (the LPD slices of one
     // load fall on distinct banks): FPL fewer register pairs per lane
     __shared__ __align__(16) double s_wp[LPD][FPL + 2];
     for (int k = threadIdx.x; k < kV; k += blockDim.x) s_wp[k / FPL][k % FPL] = a.head.H2[k];
 #define GW(k) s_wp[part][k]
-#else
-#define GW(k) w[k]
-#endif
     __syncthreads();
     double u0[FPL];
-#ifdef NS_GW_REGS
-    double w[FPL];
-    load_lane_head<FPL>(a.head, part, u0, w);
-#endif
     const long long gw = (long long)blockIdx.x * nw + wl;
     double* scr = x.scratch + (size_t)gw * M * D * kV;   // this warp's group states
     // state slice of group gr >= 1 owned by this lane (its device, part)
@@ -1153,10 +1145,6 @@ __global__ void __launch_bounds__(NS_DEDUP_WPB * 32, (LPD >= 8 ? NS_DEDUP_BLOCKS
             issue(p + kDStages - 1);
             cp_async_wait<kDStages - 1>();  // table p has landed (this lane's copies)
             __syncwarp();                  // ... and every lane's
-#ifdef NS_GV_SMEM
-            // v_t read from the ring slice at each use (not held in registers)
-            const double* vcd = reinterpret_cast<const double*>(&s.ring[sl][part * SS]);
-#else
             double vcd[FPL];
             const double2* src = reinterpret_cast<const double2*>(&s.ring[sl][part * SS]);
 #pragma unroll
@@ -1165,7 +1153,6 @@ __global__ void __launch_bounds__(NS_DEDUP_WPB * 32, (LPD >= 8 ? NS_DEDUP_BLOCKS
                 vcd[2 * i2] = xv.x;
                 vcd[2 * i2 + 1] = xv.y;
             }
-#endif
             const int4 mt = s.meta[sl];
             process(vcd, mt.x, (long long)(((unsigned long long)(unsigned)mt.w << 32) | (unsigned)mt.z), mt.y, p);
         }
@@ -1187,11 +1174,9 @@ __global__ void __launch_bounds__(NS_DEDUP_WPB * 32, (LPD >= 8 ? NS_DEDUP_BLOCKS
         // ---- outputs: per member feasibility, work, and its group's device costs
         for (int gr = 0; gr < ng; ++gr) {
             double hp;
-#ifndef NS_GW_REGS
             double w[FPL];
 #pragma unroll
             for (int k = 0; k < FPL; ++k) w[k] = GW(k);
-#endif
             if (gr == 0) {
                 hp = part_head<FPL>(u0, w);
             } else {

@@ -504,3 +504,27 @@ def test_score_plans_tf32x3_tcgen05(ns, ctx, D):
     srt = np.sort(c64)
     if (srt[1] - srt[0]) / abs(srt[0]) > 1e-5:
         assert b32 == b64
+
+
+def test_profile_class_mask(ns, ctx):
+    """ns_profile with a class list times only those kernel classes (the bench
+    brackets just the roofline kernel inside its timed region); the search
+    result is unchanged by the timers."""
+    w = gen_weights(4, "mono")
+    tasks = gen_tasks("C2", 64)
+    tabs = _setup(ns, ctx, tasks, w)
+    ref = ns.ns_shard_tablewise(ctx, tabs, 4, M=11)
+    ns.ns_profile(ctx, True, kinds=("greedy",))
+    out = ns.ns_shard_tablewise(ctx, tabs, 4, M=11)
+    q = {k: ns.ns_profile_query(ctx, k) for k in ns.PROFILE_KINDS}
+    ns.ns_profile(ctx, False)
+    assert q["greedy"][1] == 1 and q["greedy"][0] > 0.0
+    assert all(v[1] == 0 for k, v in q.items() if k != "greedy")
+    ns.ns_profile(ctx, True)
+    ns.ns_shard_tablewise(ctx, tabs, 4, M=11)
+    q_all = {k: ns.ns_profile_query(ctx, k) for k in ns.PROFILE_KINDS}
+    ns.ns_profile(ctx, False)
+    assert q_all["greedy"][1] == 1 and q_all["order"][1] >= 1 and q_all["finalize"][1] >= 1
+    np.testing.assert_array_equal(out["cost"], ref["cost"])
+    np.testing.assert_array_equal(out["assign"], ref["assign"])
+    tabs.free()
