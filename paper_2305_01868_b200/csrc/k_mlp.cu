@@ -273,16 +273,58 @@ struct PreDmmaArgs {
 #ifndef NS_PRE_BLOCKS
 #define NS_PRE_BLOCKS 5
 #endif
-__global__ void __launch_bounds__(128, NS_PRE_BLOCKS) k_precompute_dmma(const PreDmmaArgs a) {
+// shared-memory weight layout (NS_PRE_WSM): padded rows, stride == 4 mod 16
+// doubles so a warp's B fragments fall on distinct banks
+constexpr int kPW1 = 20, kPW2 = 132, kPW3 = 36;              // row strides of W1 [128][5], W2 [32][128], H1 [64][32]
+constexpr int kPO1 = 0, kPO2 = kPO1 + 128 * kPW1, kPO3 = kPO2 + 32 * kPW2;
+constexpr int kPOb1 = kPO3 + 64 * kPW3, kPOb2 = kPOb1 + 128, kPOhb1 = kPOb2 + 32, kPOH2 = kPOhb1 + 64;
+constexpr int kPWTotal = kPOH2 + 64;                          // doubles
+// WSM: encoder / projection weights resident in shared memory, one 16-warp CTA
+// per SM (batches: the weights are staged once per SM and every B fragment is
+// a conflict-free shared-memory load); otherwise B fragments through L1 with
+// 4-warp CTAs (a few hundred rows: no staging latency).
+template <bool WSM>
+__global__ void __launch_bounds__(WSM ? 512 : 128, WSM ? 1 : NS_PRE_BLOCKS) k_precompute_dmma(const PreDmmaArgs a) {
     extern __shared__ double qsm[];
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
     const int g = lane >> 2, t = lane & 3;
     const int ldx = a.ldx, ldh = a.ldy;             // x and e stride / h-chunk stride
-    const int per_warp = 16 * (ldx + ldh + ldh) + 16;
-    double* X = qsm + (size_t)w * per_warp;         // [16][8]  features (zero padded)
-    double* Hc = X + 16 * ldx;                      // [16][32] hidden chunk
-    double* E = Hc + 16 * ldh;                      // [16][32] table representation e
-    long long* rowid = (long long*)(E + 16 * ldh);  // [16] variant row (or -1)
+    double* const sw = qsm;   // WSM: weights (kPWTotal doubles) then the per-warp buffers
+    if constexpr (WSM) {
+        for (int i = threadIdx.x; i < 128 * kPW1; i += blockDim.x) {
+            const int n = i / kPW1, k = i % kPW1;
+            sw[kPO1 + i] = k < kF ? a.enc1W[n * kF + k] : 0.0;
+        }
+        for (int i = threadIdx.x; i < 32 * kPW2; i += blockDim.x) {
+            const int n = i / kPW2, k = i % kPW2;
+            sw[kPO2 + i] = k < kH ? a.enc2W[n * kH + k] : 0.0;
+        }
+        for (int i = threadIdx.x; i < 64 * kPW3; i += blockDim.x) {
+            const int n = i / kPW3, k = i % kPW3;
+            sw[kPO3 + i] = k < kE ? a.H1[n * kE + k] : 0.0;
+        }
+        for (int i = threadIdx.x; i < 128; i += blockDim.x) sw[kPOb1 + i] = a.enc1b[i];
+        for (int i = threadIdx.x; i < 32; i += blockDim.x) sw[kPOb2 + i] = a.enc2b[i];
+        for (int i = threadIdx.x; i < 64; i += blockDim.x) {
+            sw[kPOhb1 + i] = a.head.hb1[i];
+            sw[kPOH2 + i] = a.head.H2[i];
+        }
+        __syncthreads();
+    }
+#define PW1(n, k) (WSM ? sw[kPO1 + (n) * kPW1 + (k)] : ((k) < kF ? __ldg(a.enc1W + (n) * kF + (k)) : 0.0))
+#define PB1(i) (WSM ? sw[kPOb1 + (i)] : __ldg(a.enc1b + (i)))
+#define PW2(n, k) (WSM ? sw[kPO2 + (n) * kPW2 + (k)] : __ldg(a.enc2W + (n) * kH + (k)))
+#define PB2(i) (WSM ? sw[kPOb2 + (i)] : __ldg(a.enc2b + (i)))
+#define PH1(n, k) (WSM ? sw[kPO3 + (n) * kPW3 + (k)] : __ldg(a.H1 + (n) * kE + (k)))
+#define PHB1(i) (WSM ? sw[kPOhb1 + (i)] : a.head.hb1[i])
+#define PH2(i) (WSM ? sw[kPOH2 + (i)] : a.head.H2[i])
+    // per warp: X [16][ldx] features (zero padded), Hc [16][ldh] hidden chunk,
+    // E [16][ldh] table representation e (WSM: reuses the chunk buffer), row ids
+    const int per_warp = WSM ? 16 * (ldx + ldh) + 16 : 16 * (ldx + ldh + ldh) + 16;
+    double* X = qsm + (WSM ? kPWTotal : 0) + (size_t)w * per_warp;
+    double* Hc = X + 16 * ldx;
+    double* E = WSM ? Hc : Hc + 16 * ldh;
+    long long* rowid = (long long*)(E + 16 * ldh);
     for (long long base = ((long long)blockIdx.x * nwarps + w) * 16; base < a.n_rows;
          base += (long long)gridDim.x * nwarps * 16) {
         // ---- features of the 16 rows (lane r < 16 owns row r); invalid variants -> zeros
@@ -342,7 +384,7 @@ __global__ void __launch_bounds__(128, NS_PRE_BLOCKS) k_precompute_dmma(const Pr
 #pragma unroll
                 for (int q = 0; q < 4; ++q) {
                     const int n = hc * 32 + 8 * q + g;
-                    const double bv = k < kF ? __ldg(a.enc1W + n * kF + k) : 0.0;
+                    const double bv = PW1(n, k);
                     dmma(hacc[0][q], a0, bv);
                     dmma(hacc[1][q], a1, bv);
                 }
@@ -350,7 +392,7 @@ __global__ void __launch_bounds__(128, NS_PRE_BLOCKS) k_precompute_dmma(const Pr
 #pragma unroll
             for (int q = 0; q < 4; ++q) {
                 const int col = 8 * q + 2 * t;
-                const double b0 = __ldg(a.enc1b + hc * 32 + col), b1 = __ldg(a.enc1b + hc * 32 + col + 1);
+                const double b0 = PB1(hc * 32 + col), b1 = PB1(hc * 32 + col + 1);
 #pragma unroll
                 for (int m = 0; m < 2; ++m) {
                     double2 hv;
@@ -368,7 +410,7 @@ __global__ void __launch_bounds__(128, NS_PRE_BLOCKS) k_precompute_dmma(const Pr
 #pragma unroll
                 for (int q = 0; q < 4; ++q) {
                     const int n = 8 * q + g;
-                    const double bv = __ldg(a.enc2W + n * kH + hc * 32 + k);
+                    const double bv = PW2(n, hc * 32 + k);
                     dmma(e_acc[0][q], a0, bv);
                     dmma(e_acc[1][q], a1, bv);
                 }
@@ -379,7 +421,7 @@ __global__ void __launch_bounds__(128, NS_PRE_BLOCKS) k_precompute_dmma(const Pr
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
             const int col = 8 * q + 2 * t;
-            const double b0 = __ldg(a.enc2b + col), b1 = __ldg(a.enc2b + col + 1);
+            const double b0 = PB2(col), b1 = PB2(col + 1);
 #pragma unroll
             for (int m = 0; m < 2; ++m) {
                 double2 ev;
@@ -407,7 +449,7 @@ __global__ void __launch_bounds__(128, NS_PRE_BLOCKS) k_precompute_dmma(const Pr
 #pragma unroll
                 for (int q = 0; q < 4; ++q) {
                     const int n = nc * 32 + 8 * q + g;
-                    const double bv = __ldg(a.H1 + n * kE + k);
+                    const double bv = PH1(n, k);
                     dmma(vacc[0][q], a0, bv);
                     dmma(vacc[1][q], a1, bv);
                 }
@@ -420,8 +462,8 @@ __global__ void __launch_bounds__(128, NS_PRE_BLOCKS) k_precompute_dmma(const Pr
                     const long long row = m ? row1 : row0;
                     const double v0 = vacc[m][q][0], v1 = vacc[m][q][1];
                     if (row >= 0) *reinterpret_cast<double2*>(a.V + row * kV + col) = make_double2(v0, v1);
-                    cpart[m] = fma(a.head.H2[col], PRE_RELU(v0 + a.head.hb1[col]), cpart[m]);
-                    cpart[m] = fma(a.head.H2[col + 1], PRE_RELU(v1 + a.head.hb1[col + 1]), cpart[m]);
+                    cpart[m] = fma(PH2(col), PRE_RELU(v0 + PHB1(col)), cpart[m]);
+                    cpart[m] = fma(PH2(col + 1), PRE_RELU(v1 + PHB1(col + 1)), cpart[m]);
                 }
             }
         }
@@ -438,6 +480,13 @@ __global__ void __launch_bounds__(128, NS_PRE_BLOCKS) k_precompute_dmma(const Pr
         __syncwarp();
     }
 }
+#undef PW1
+#undef PB1
+#undef PW2
+#undef PB2
+#undef PH1
+#undef PHB1
+#undef PH2
 
 static int ld_pad(int width) { return ((width + 15) / 16) * 16 + 4; }   // == 4 (mod 16): conflict-free A frags
 
@@ -494,15 +543,25 @@ void launch_precompute(ns_ctx* ctx, const ns_tables* t, int jlo, int jhi) {
     a.vbytes = t->d_vbytes;
     a.ldx = ld_pad(8);    // x (8 features, zero padded)
     a.ldy = ld_pad(32);   // hidden chunk and e (32)
-    const int wpb = 4;
-    const size_t smem = (size_t)wpb * (16 * (a.ldx + 2 * a.ldy) + 16) * sizeof(double);
-    cudaFuncSetAttribute(k_precompute_dmma, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    // batches stage the weights once per SM; a few hundred rows (a single
+    // task) read them through L1 instead of paying the staging latency
+    const bool wsm = a.n_rows >= 16LL * 16 * ctx->sm_count;
+    const int wpb = wsm ? 16 : 4;
+    const size_t smem = wsm ? ((size_t)kPWTotal + (size_t)wpb * (16 * (a.ldx + a.ldy) + 16)) * sizeof(double)
+                            : (size_t)wpb * (16 * (a.ldx + 2 * a.ldy) + 16) * sizeof(double);
+    if (wsm)
+        cudaFuncSetAttribute(k_precompute_dmma<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    else
+        cudaFuncSetAttribute(k_precompute_dmma<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     long long blocks = (a.n_rows + 16LL * wpb - 1) / (16LL * wpb);
-    const long long cap = (long long)ctx->sm_count * 16;
+    const long long cap = (long long)ctx->sm_count * (wsm ? 1 : 16);
     if (blocks > cap) blocks = cap;
     if (blocks < 1) blocks = 1;
     prof_begin(ctx, PK_PRECOMPUTE);
-    k_precompute_dmma<<<(unsigned)blocks, wpb * 32, smem, ctx->stream>>>(a);
+    if (wsm)
+        k_precompute_dmma<true><<<(unsigned)blocks, wpb * 32, smem, ctx->stream>>>(a);
+    else
+        k_precompute_dmma<false><<<(unsigned)blocks, wpb * 32, smem, ctx->stream>>>(a);
     prof_end(ctx);
     ctx->launches++;
 }
