@@ -379,6 +379,9 @@ def main():
                            "l2": "flushed between steps (256 MiB write)"},
                 "gpu_launches": int(launches), "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
                 "clocks": clocks, "kernels_ms_per_step": {k: v[0] / args.steps for k, v in prof_all.items() if v[1]},
+                "kernels_ms_note": "kernels_ms_per_step: a separate pass of the same K steps with CUDA events "
+                                   "around every launch; roofline.greedy_ms_per_launch: events around the "
+                                   "greedy only, inside the timed region",
                 "secondary": secondary}
         print(json.dumps(line), flush=True)
     ns.ns_destroy(ctx)
