@@ -87,6 +87,35 @@ __global__ void k_mark_bad(const uint8_t* ok, double* cost, long long pb, long l
 // per device, and lane k accumulates features (2k, 2k+1) of every device in
 // registers over that device's tables in list order -- warp-level segmented
 // adds over staged rows, no read-modify-write through memory.
+// Transposed butterfly over the warp for DM values per lane (all devices at
+// once): at each of the first log2(DM) levels a lane keeps half of its values
+// and adds the partner's copy of them, so 2*DM - 1 + (5 - log2(DM)) shuffles
+// of doubles replace DM full 5-level butterflies.  Afterwards lane L holds the
+// warp sum of value dev(L) = bits (4, 3, ...) of L.
+template <int DM>
+__device__ __forceinline__ double warp_sum_multi(double (&v)[DM], int lane) {
+    constexpr int LG = DM == 1 ? 0 : DM == 2 ? 1 : DM == 4 ? 2 : DM == 8 ? 3 : 4;
+    int n = DM;
+#pragma unroll
+    for (int l = 0; l < LG; ++l) {
+        const int o = 16 >> l;
+        const bool hi = (lane & o) != 0;
+        n >>= 1;
+#pragma unroll
+        for (int i = 0; i < DM / 2; ++i) {
+            if (i < n) {
+                const double send = hi ? v[i] : v[i + n];
+                const double keep = hi ? v[i + n] : v[i];
+                v[i] = keep + __shfl_xor_sync(kFull, send, o);
+            }
+        }
+    }
+    double x = v[0];
+#pragma unroll
+    for (int o = 16 >> LG; o > 0; o >>= 1) x += __shfl_xor_sync(kFull, x, o);
+    return x;
+}
+
 template <int DM>
 __global__ void __launch_bounds__(256) k_pool_staged(const ScoreArgs a) {
     extern __shared__ double ssm[];
@@ -94,6 +123,7 @@ __global__ void __launch_bounds__(256) k_pool_staged(const ScoreArgs a) {
     const int D = a.D, Tp = a.Tp;
     double* sv = ssm;                                            // [Tp][64]
     int* sdim = (int*)(sv + (size_t)Tp * kV);                    // [Tp]
+    int* sdd = sdim + Tp + 16 * w;                               // [16] this warp's per-device dims
     for (int i = threadIdx.x; i < Tp * (kV / 2); i += blockDim.x) {
         const int t = i / (kV / 2), c = i % (kV / 2);
         const int row = __ldg(a.rows + t);
@@ -103,6 +133,8 @@ __global__ void __launch_bounds__(256) k_pool_staged(const ScoreArgs a) {
     __syncthreads();
     const double hb0 = a.head.hb1[2 * lane], hb1 = a.head.hb1[2 * lane + 1];
     const double w0 = a.head.H2[2 * lane], w1 = a.head.H2[2 * lane + 1];
+    constexpr int LG = DM == 1 ? 0 : DM == 2 ? 1 : DM == 4 ? 2 : DM == 8 ? 3 : 4;
+    const int my_dev = (lane >> (5 - LG)) & (DM - 1);   // device whose sum lane holds after warp_sum_multi
     for (long long p = a.p_begin + (long long)blockIdx.x * wpb + w; p < a.p_end; p += (long long)gridDim.x * wpb) {
         double acc[DM][2];
 #pragma unroll
@@ -110,42 +142,43 @@ __global__ void __launch_bounds__(256) k_pool_staged(const ScoreArgs a) {
             acc[d][0] = hb0;
             acc[d][1] = hb1;
         }
-        int dd_local = 0;   // lane d < D: dims of device d
+        if (lane < 16) sdd[lane] = 0;
+        __syncwarp();
         bool bad = false;
         const int8_t* pa = a.assign + p * Tp;
         for (int c0 = 0; c0 < Tp; c0 += 32) {
             const int t0 = c0 + lane;
             const int my_a = t0 < Tp ? (int)pa[t0] : 0;
-            const int my_dim = t0 < Tp ? sdim[t0] : 0;
-            bad |= __any_sync(kFull, t0 < Tp && (my_a < 0 || my_a >= D));
+            const bool ok = t0 < Tp && (unsigned)my_a < (unsigned)D;
+            bad |= __any_sync(kFull, t0 < Tp && !ok);
+            if (ok) atomicAdd(&sdd[my_a], sdim[t0]);   // device dims (integer: order-free)
+            const double2* svc = reinterpret_cast<const double2*>(sv + (size_t)c0 * kV) + lane;
 #pragma unroll
             for (int d = 0; d < DM; ++d) {
                 if (d >= D) break;
-                unsigned m = __ballot_sync(kFull, t0 < Tp && my_a == d);
-                const int s = __reduce_add_sync(kFull, (m >> lane) & 1 ? my_dim : 0);
-                if (lane == d) dd_local += s;
-                while (m) {   // this device's tables of the chunk, in list order
-                    const int j = __ffs(m) - 1;
-                    m &= m - 1;
-                    const double2 vv = reinterpret_cast<const double2*>(sv + (size_t)(c0 + j) * kV)[lane];
+                unsigned m = __ballot_sync(kFull, ok && my_a == d);
+                while (m) {   // this device's tables of the chunk
+                    const int j = 31 - __clz(m);
+                    m ^= 1u << j;
+                    const double2 vv = svc[j * (kV / 2)];
                     acc[d][0] += vv.x;
                     acc[d][1] += vv.y;
                 }
             }
         }
+        __syncwarp();
+        double part[DM];
 #pragma unroll
-        for (int d = 0; d < DM; ++d) {
-            if (d >= D) break;
-            double part = w0 * relu_exact(acc[d][0]) + w1 * relu_exact(acc[d][1]);
-#pragma unroll
-            for (int o = 16; o > 0; o >>= 1) part += __shfl_xor_sync(kFull, part, o);
-            const int ddim = __shfl_sync(kFull, dd_local, d);
-            if (lane == 0) {
-                a.comp[p * D + d] = ddim > 0 ? part + a.head.hb2 : 0.0;
-                a.devdim[p * D + d] = ddim;
-            }
+        for (int d = 0; d < DM; ++d) part[d] = w0 * relu_exact(acc[d][0]) + w1 * relu_exact(acc[d][1]);
+        const double sum = warp_sum_multi<DM>(part, lane);
+        // one lane per device writes (the lowest lane holding it)
+        if ((lane & ((32 >> LG) - 1)) == 0 && my_dev < D) {
+            const int ddim = sdd[my_dev];
+            a.comp[p * D + my_dev] = ddim > 0 ? sum + a.head.hb2 : 0.0;
+            a.devdim[p * D + my_dev] = ddim;
         }
         if (lane == 0) a.ok[p] = bad ? 0 : 1;
+        __syncwarp();
     }
 }
 
@@ -296,7 +329,7 @@ ns_status run_score_plans(ns_ctx* ctx, const ns_tables* t, int task, int D, cons
     a.head = ctx->model.head;
     if (pe > pb) {
         {
-            const size_t stage = (size_t)Tp * kV * sizeof(double) + (size_t)Tp * sizeof(int) + 16;
+            const size_t stage = (size_t)Tp * kV * sizeof(double) + (size_t)Tp * sizeof(int) + 8 * 16 * sizeof(int) + 16;
             const size_t uw = (size_t)D * kV * sizeof(double);
             (void)uw;
             if (D <= 16 && stage <= 160 * 1024) {
