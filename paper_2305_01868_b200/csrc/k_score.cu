@@ -11,6 +11,7 @@
 
 #include <algorithm>
 #include <cstring>
+#include <type_traits>
 #include <vector>
 
 #include "ns_device.cuh"
@@ -116,18 +117,28 @@ __device__ __forceinline__ double warp_sum_multi(double (&v)[DM], int lane) {
     return x;
 }
 
-template <int DM>
+// F32 (NS_SCORE_TF32X3 only, whose comm MLPs are FP32-grade anyway): the
+// staged rows and the per-device sums are fp32 -- half the shared-memory
+// bytes per (plan, table) visit and FP32-pipe adds; the head epilogue runs in
+// fp64 on the fp32 sums (~1e-7 relative).
+template <int DM, bool F32>
 __global__ void __launch_bounds__(256) k_pool_staged(const ScoreArgs a) {
+    using S = std::conditional_t<F32, float, double>;
+    using S2 = std::conditional_t<F32, float2, double2>;
     extern __shared__ double ssm[];
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, wpb = blockDim.x >> 5;
     const int D = a.D, Tp = a.Tp;
-    double* sv = ssm;                                            // [Tp][64]
+    S* sv = reinterpret_cast<S*>(ssm);                           // [Tp][64]
     int* sdim = (int*)(sv + (size_t)Tp * kV);                    // [Tp]
     int* sdd = sdim + Tp + 16 * w;                               // [16] this warp's per-device dims
     for (int i = threadIdx.x; i < Tp * (kV / 2); i += blockDim.x) {
         const int t = i / (kV / 2), c = i % (kV / 2);
         const int row = __ldg(a.rows + t);
-        reinterpret_cast<double2*>(sv + (size_t)t * kV)[c] = __ldg(reinterpret_cast<const double2*>(a.V + (size_t)row * kV) + c);
+        const double2 x = __ldg(reinterpret_cast<const double2*>(a.V + (size_t)row * kV) + c);
+        S2 y;
+        y.x = (S)x.x;
+        y.y = (S)x.y;
+        reinterpret_cast<S2*>(sv + (size_t)t * kV)[c] = y;
     }
     for (int t = threadIdx.x; t < Tp; t += blockDim.x) sdim[t] = __ldg(a.vdim + __ldg(a.rows + t));
     __syncthreads();
@@ -136,11 +147,11 @@ __global__ void __launch_bounds__(256) k_pool_staged(const ScoreArgs a) {
     constexpr int LG = DM == 1 ? 0 : DM == 2 ? 1 : DM == 4 ? 2 : DM == 8 ? 3 : 4;
     const int my_dev = (lane >> (5 - LG)) & (DM - 1);   // device whose sum lane holds after warp_sum_multi
     for (long long p = a.p_begin + (long long)blockIdx.x * wpb + w; p < a.p_end; p += (long long)gridDim.x * wpb) {
-        double acc[DM][2];
+        S acc[DM][2];
 #pragma unroll
         for (int d = 0; d < DM; ++d) {
-            acc[d][0] = hb0;
-            acc[d][1] = hb1;
+            acc[d][0] = (S)hb0;
+            acc[d][1] = (S)hb1;
         }
         if (lane < 16) sdd[lane] = 0;
         __syncwarp();
@@ -152,7 +163,7 @@ __global__ void __launch_bounds__(256) k_pool_staged(const ScoreArgs a) {
             const bool ok = t0 < Tp && (unsigned)my_a < (unsigned)D;
             bad |= __any_sync(kFull, t0 < Tp && !ok);
             if (ok) atomicAdd(&sdd[my_a], sdim[t0]);   // device dims (integer: order-free)
-            const double2* svc = reinterpret_cast<const double2*>(sv + (size_t)c0 * kV) + lane;
+            const S2* svc = reinterpret_cast<const S2*>(sv + (size_t)c0 * kV) + lane;
 #pragma unroll
             for (int d = 0; d < DM; ++d) {
                 if (d >= D) break;
@@ -160,7 +171,7 @@ __global__ void __launch_bounds__(256) k_pool_staged(const ScoreArgs a) {
                 while (m) {   // this device's tables of the chunk
                     const int j = 31 - __clz(m);
                     m ^= 1u << j;
-                    const double2 vv = svc[j * (kV / 2)];
+                    const S2 vv = svc[j * (kV / 2)];
                     acc[d][0] += vv.x;
                     acc[d][1] += vv.y;
                 }
@@ -169,7 +180,8 @@ __global__ void __launch_bounds__(256) k_pool_staged(const ScoreArgs a) {
         __syncwarp();
         double part[DM];
 #pragma unroll
-        for (int d = 0; d < DM; ++d) part[d] = w0 * relu_exact(acc[d][0]) + w1 * relu_exact(acc[d][1]);
+        for (int d = 0; d < DM; ++d)
+            part[d] = w0 * relu_exact((double)acc[d][0]) + w1 * relu_exact((double)acc[d][1]);
         const double sum = warp_sum_multi<DM>(part, lane);
         // one lane per device writes (the lowest lane holding it)
         if ((lane & ((32 >> LG) - 1)) == 0 && my_dev < D) {
@@ -329,7 +341,9 @@ ns_status run_score_plans(ns_ctx* ctx, const ns_tables* t, int task, int D, cons
     a.head = ctx->model.head;
     if (pe > pb) {
         {
-            const size_t stage = (size_t)Tp * kV * sizeof(double) + (size_t)Tp * sizeof(int) + 8 * 16 * sizeof(int) + 16;
+            const bool f32 = mode == NS_SCORE_TF32X3;   // fp32 pooling in the FP32-grade mode
+            const size_t stage = (size_t)Tp * kV * (f32 ? sizeof(float) : sizeof(double)) + (size_t)Tp * sizeof(int) +
+                                 8 * 16 * sizeof(int) + 16;
             const size_t uw = (size_t)D * kV * sizeof(double);
             (void)uw;
             if (D <= 16 && stage <= 160 * 1024) {
@@ -340,11 +354,18 @@ ns_status run_score_plans(ns_ctx* ctx, const ns_tables* t, int task, int D, cons
                 const long long cap = (long long)ctx->sm_count * std::max<long long>(1, (long long)((200 * 1024) / smem));
                 if (blocks > cap) blocks = cap;
                 prof_begin(ctx, PK_SCORE);
-#define NS_POOL(DM)                                                                                       \
-    cudaFuncSetAttribute(k_pool_staged<DM>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);      \
-    k_pool_staged<DM><<<(unsigned)blocks, wpb * 32, smem, ctx->stream>>>(a);
+#define NS_POOL2(DM, F)                                                                                   \
+    cudaFuncSetAttribute(k_pool_staged<DM, F>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);   \
+    k_pool_staged<DM, F><<<(unsigned)blocks, wpb * 32, smem, ctx->stream>>>(a);
+#define NS_POOL(DM)             \
+    if (f32) {                  \
+        NS_POOL2(DM, true)      \
+    } else {                    \
+        NS_POOL2(DM, false)     \
+    }
                 if (D <= 2) { NS_POOL(2) } else if (D <= 4) { NS_POOL(4) } else if (D <= 8) { NS_POOL(8) } else { NS_POOL(16) }
 #undef NS_POOL
+#undef NS_POOL2
                 prof_end(ctx);
                 NS_LAUNCHED(ctx);
             } else {
