@@ -528,3 +528,25 @@ def test_profile_class_mask(ns, ctx):
     np.testing.assert_array_equal(out["cost"], ref["cost"])
     np.testing.assert_array_equal(out["assign"], ref["assign"])
     tabs.free()
+
+
+def test_ablation_invariants(ns, ctx):
+    """SURVEY §8(f) F1 ablations on the GPU path (tools/ablation.py): the
+    column-wise search with L = 0 is exactly the table-wise search ("w/o beam
+    search", reading R15); the full beam search is never worse than L = 0 (the
+    global best only improves over levels); for the table-wise search the M = 11
+    grid contains M = 1's single cap (m = 0 is M_s), so it is never worse."""
+    D = 4
+    tasks = [gen_task("C3", i, T=24, D=D) for i in range(32)]
+    w = gen_weights(D, "mono")
+    tabs = _setup(ns, ctx, tasks, w)
+    tw11 = ns.ns_shard_tablewise(ctx, tabs, D, M=11)
+    tw1 = ns.ns_shard_tablewise(ctx, tabs, D, M=1)
+    cw0 = ns.ns_shard_columnwise(ctx, tabs, D, N=4, K=2, L=0, M=11)
+    cw = ns.ns_shard_columnwise(ctx, tabs, D, N=4, K=2, L=3, M=11)
+    np.testing.assert_array_equal(cw0["cost"], tw11["cost"])
+    np.testing.assert_array_equal(cw0["assign"][:, :24], tw11["assign"][:, :24])
+    assert np.all(cw["cost"] <= tw11["cost"])
+    assert np.all(tw11["cost"] <= tw1["cost"])
+    assert np.isfinite(cw["cost"]).sum() >= np.isfinite(tw11["cost"]).sum()
+    tabs.free()
