@@ -415,6 +415,26 @@ def search_latency(ns, ctx, torch):
             scores = int(out["n_scores"][0])
         t = float(np.median(times[1:]))
         res[cfg] = {"mode": mode, "search_ms_per_task": 1e3 * t, "scores": scores, "scores_per_s": scores / t}
+    # batched column-wise search (multi-task batching): 64 C3
+    # tasks and 4 C5 tasks per call, device time per task and scores/s
+    for cfg, n in (("C3", 64), ("C5", 4)):
+        c = CONFIGS[cfg]
+        w = gen_weights(c["D"], "mono")
+        ns.ns_load_cost_models(ctx, w)
+        tasks = gen_tasks(cfg, n)
+        desc, off, caps = ns.table_descs(tasks)
+        times, scores = [], 0
+        for it in range(3):
+            t0 = time.perf_counter()
+            tabs = ns.ns_featurize_tables(ctx, desc, off, caps)
+            out = ns.ns_shard_columnwise(ctx, tabs, c["D"], N=c["N"], K=c["K"], L=c["L"], M=c["M"])
+            tabs.free()
+            torch.cuda.synchronize()
+            times.append(time.perf_counter() - t0)
+            scores = int(np.sum(out["n_scores"]))
+        t = float(np.median(times[1:]))
+        res[f"{cfg}x{n}"] = {"mode": "columnwise, batched", "tasks": n, "ms_per_task": 1e3 * t / n,
+                             "scores": scores, "scores_per_s": scores / t}
     return res
 
 
