@@ -1237,33 +1237,39 @@ __global__ void __launch_bounds__(NS_DEDUP_WPB * 32, (LPD >= 8 ? NS_DEDUP_BLOCKS
 
 #undef GW
 
-// Large D (D > 16, e.g. C5's 128 simulated GPUs): one trajectory per CTA and
-// ONE thread per device holding all 64 features of u_d in registers; the head
-// weights and the staged v row are read from shared memory as broadcasts
-// (every thread of the CTA reads the same address).  A CTA is at most 4 warps
-// (D <= 128) and ~165 registers per thread, so 3 CTAs fit per SM -- the 660
-// trajectories of a C5 level run in 1.5 waves instead of 4.5 with 4 lanes per
-// device.  Cross-warp argmin: shuffle argmin per warp, the <= 4 candidates
-// through shared memory (double-buffered by step parity), reduced by every
-// thread in warp order (lowest device on ties, R13).
-__global__ void __launch_bounds__(128, 3) k_greedy_wide(const GreedyArgs a) {
-    constexpr int kLook = kStages - 2;   // the slot being overwritten was last read two steps ago
-    __shared__ __align__(16) double s_w[kV];
+// Large D (D > 16, e.g. C5's 128 simulated GPUs): one trajectory per CTA,
+// TPD threads per device, each holding FPL = 64 / TPD features of u_d in
+// registers; the head weights and the staged v row are read from shared memory
+// (per-slice rows padded 16 B apart: the TPD slices of one load fall on
+// distinct banks).  A single-task search is latency-bound -- its longest
+// trajectories (~T' steps) run nearly alone once the short ones have
+// stranded -- so the per-step chain matters most: TPD = 4 cuts the per-thread
+// score to 16 features plus a 2-level lane butterfly.  Cross-warp argmin: each
+// warp's (score, device) goes through shared memory (double-buffered by step
+// parity); lane k of every warp loads warp k's entry and one warp butterfly
+// picks the lowest (score, device) (R13).
+template <int TPD>
+__global__ void __launch_bounds__(128 * TPD, TPD >= 4 ? 1 : (TPD == 2 ? 2 : 3)) k_greedy_wide(const GreedyArgs a) {
+    constexpr int FPL = kV / TPD;            // features per thread
+    constexpr int SS = FPL + 2;              // padded slice stride (doubles)
+    constexpr int kLook = kStages - 2;       // the slot being overwritten was last read two steps ago
+    constexpr int NWM = 4 * TPD;             // warps of a D = 128 CTA
+    __shared__ __align__(16) double s_w[TPD][SS];
     __shared__ __align__(16) double s_hb1[kV];
-    __shared__ __align__(16) double ring[kStages][kV];
-    __shared__ double s_sc[2][4];
-    __shared__ int s_dv[2][4];
-    __shared__ int s_cnt[2][4];
+    __shared__ __align__(16) double ring[kStages][TPD * SS];
+    __shared__ double s_sc[2][NWM];
+    __shared__ int s_dv[2][NWM];
+    __shared__ int s_cnt[2][NWM];
     __shared__ int4 smeta[kStages];   // {dim, list index, bytes lo, bytes hi}
     const int lane = threadIdx.x & 31, wi = threadIdx.x >> 5, nw = blockDim.x >> 5;
     const long long tau = a.traj_begin + blockIdx.x;
     if (tau >= a.traj_end) return;
     for (int k = threadIdx.x; k < kV; k += blockDim.x) {
-        s_w[k] = a.head.H2[k];
+        s_w[k / FPL][k % FPL] = a.head.H2[k];
         s_hb1[k] = a.head.hb1[k];
     }
     const int g = (int)(tau / a.M), m = (int)(tau % a.M);
-    const int d = threadIdx.x;
+    const int d = threadIdx.x / TPD, part = threadIdx.x % TPD;
     bool alive = a.cp_valid[g] != 0;
     int Tp = 0, capd = 0;
     long long cap = 0;
@@ -1275,9 +1281,9 @@ __global__ void __launch_bounds__(128, 3) k_greedy_wide(const GreedyArgs a) {
     }
     const bool dev = d < a.D;
     __syncthreads();
-    double u[kV];
+    double u[FPL];
 #pragma unroll
-    for (int k = 0; k < kV; ++k) u[k] = s_hb1[k];
+    for (int k = 0; k < FPL; ++k) u[k] = s_hb1[part * FPL + k];
     int dsum = 0;
     long long bsum = 0;
     uint32_t work = 0;
@@ -1285,18 +1291,21 @@ __global__ void __launch_bounds__(128, 3) k_greedy_wide(const GreedyArgs a) {
     const int4* ometa = a.ord_meta + (size_t)g * a.Tpm;
     int8_t* asg = a.assign + (size_t)tau * a.Tpm;
     const int T = alive ? Tp : 0;
-    // warp 0 streams the cost-ordered v rows through a cp.async ring
+    // warp 0 streams the cost-ordered v rows through a cp.async ring; lane l
+    // copies features (2l, 2l + 1) into slice 2l / FPL
+    const int my_slice = (2 * lane) / FPL, my_off = (2 * lane) % FPL;
     auto issue = [&](int pp) {
         if (pp < T) {
             const int r = __ldg(orow + pp);
             const int slot = pp % kStages;
-            cp_async16(&ring[slot][2 * lane], a.V + (size_t)r * kV + 2 * lane);
+            cp_async16(&ring[slot][my_slice * SS + my_off], a.V + (size_t)r * kV + 2 * lane);
             if (lane == 0) cp_async16(smeta + slot, ometa + pp);
         }
         cp_async_commit();
     };
     if (wi == 0)
         for (int pp = 0; pp < kLook; ++pp) issue(pp);
+    const double2* w2 = reinterpret_cast<const double2*>(&s_w[part][0]);
 #pragma unroll 1
     for (int p = 0; p < T; ++p) {
         const int par = p & 1;
@@ -1310,41 +1319,37 @@ __global__ void __launch_bounds__(128, 3) k_greedy_wide(const GreedyArgs a) {
         const int dt = mt.x;
         const long long bt = (long long)(((unsigned long long)(unsigned)mt.w << 32) | (unsigned)mt.z);
         const bool f = dev && (bsum + bt <= cap) && (dsum + dt <= capd);
-        const double2* v2 = reinterpret_cast<const double2*>(ring[sl]);
-        const double2* w2 = reinterpret_cast<const double2*>(s_w);
-        double bs = CUDART_INF;
+        const double2* v2 = reinterpret_cast<const double2*>(&ring[sl][part * SS]);
+        double ps = 0.0;
         if (f) {
             double acc[4] = {0.0, 0.0, 0.0, 0.0};
 #pragma unroll
-            for (int k2 = 0; k2 < kV / 2; ++k2) {
+            for (int k2 = 0; k2 < FPL / 2; ++k2) {
                 const double2 vv = v2[k2], ww = w2[k2];
                 acc[(2 * k2) & 3] = fma(ww.x, relu_hi(u[2 * k2] + vv.x), acc[(2 * k2) & 3]);
                 acc[(2 * k2 + 1) & 3] = fma(ww.y, relu_hi(u[2 * k2 + 1] + vv.y), acc[(2 * k2 + 1) & 3]);
             }
-            bs = a.head.hb2 + ((acc[0] + acc[1]) + (acc[2] + acc[3]));
+            ps = (acc[0] + acc[1]) + (acc[2] + acc[3]);
         }
+        const double sco = a.head.hb2 + lane_group_sum<TPD>(ps);
+        double bs = f ? sco : CUDART_INF;
         int bd = d;
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1) argmin_step(bs, bd, o);
-        const unsigned bal = __ballot_sync(kFull, f);
+        for (int o = 16; o >= TPD; o >>= 1) argmin_step(bs, bd, o);
+        const unsigned bal = __ballot_sync(kFull, f && part == 0);
         if (lane == 0) {
             s_sc[par][wi] = bs;
             s_dv[par][wi] = bd;
             s_cnt[par][wi] = __popc(bal);
         }
         __syncthreads();
-        bs = s_sc[par][0];
-        bd = s_dv[par][0];
-        int cnt = s_cnt[par][0];
-        for (int k = 1; k < nw; ++k) {
-            const double os = s_sc[par][k];
-            const int od = s_dv[par][k];
-            cnt += s_cnt[par][k];
-            if (os < bs || (os == bs && od < bd)) {
-                bs = os;
-                bd = od;
-            }
-        }
+        // lane k holds warp k's candidate; one butterfly gives every lane the
+        // lowest (score, device) of the CTA
+        bs = lane < nw ? s_sc[par][lane] : CUDART_INF;
+        bd = lane < nw ? s_dv[par][lane] : INT_MAX;
+        const int cnt = __reduce_add_sync(kFull, lane < nw ? s_cnt[par][lane] : 0);
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) argmin_step(bs, bd, o);
         work += cnt;
         if (bs == CUDART_INF) {
             alive = false;
@@ -1352,7 +1357,7 @@ __global__ void __launch_bounds__(128, 3) k_greedy_wide(const GreedyArgs a) {
         }
         if (d == bd) {
 #pragma unroll
-            for (int k2 = 0; k2 < kV / 2; ++k2) {
+            for (int k2 = 0; k2 < FPL / 2; ++k2) {
                 const double2 vv = v2[k2];
                 u[2 * k2] += vv.x;
                 u[2 * k2 + 1] += vv.y;
@@ -1363,11 +1368,12 @@ __global__ void __launch_bounds__(128, 3) k_greedy_wide(const GreedyArgs a) {
         if (threadIdx.x == 0) asg[mt.y] = (int8_t)bd;
     }
     if (wi == 0) cp_async_wait<0>();
-    if (dev) {
-        double acc[4] = {0.0, 0.0, 0.0, 0.0};
+    // final per-device cost (every lane takes part in the lane-group sum)
+    double acc[4] = {0.0, 0.0, 0.0, 0.0};
 #pragma unroll
-        for (int k = 0; k < kV; ++k) acc[k & 3] = fma(s_w[k], relu_exact(u[k]), acc[k & 3]);
-        const double hc = a.head.hb2 + ((acc[0] + acc[1]) + (acc[2] + acc[3]));
+    for (int k = 0; k < FPL; ++k) acc[k & 3] = fma(s_w[part][k], relu_exact(u[k]), acc[k & 3]);
+    const double hc = a.head.hb2 + lane_group_sum<TPD>((acc[0] + acc[1]) + (acc[2] + acc[3]));
+    if (dev && part == 0) {
         a.comp[tau * a.D + d] = dsum > 0 ? hc : 0.0;   // reading R4
         a.devdim[tau * a.D + d] = dsum;
     }
@@ -1819,9 +1825,13 @@ ns_status launch_greedy(ns_ctx* ctx, const SearchBufs& b, const ns_tables* t, lo
         }
         prof_end(ctx);
     } else {
-        const int threads = ((b.D + 31) / 32) * 32;
+#ifndef NS_WIDE_TPD
+#define NS_WIDE_TPD 2
+#endif
+        constexpr int TPD = NS_WIDE_TPD;
+        const int threads = ((b.D * TPD + 31) / 32) * 32;
         prof_begin(ctx, PK_GREEDY);
-        k_greedy_wide<<<(unsigned)n, threads, 0, ctx->stream>>>(a);
+        k_greedy_wide<TPD><<<(unsigned)n, threads, 0, ctx->stream>>>(a);
         prof_end(ctx);
         // no grouping: every trajectory carries its own plan
         NS_CUDA(ctx, cudaMemsetAsync(b.dup_of + tb, 0xff, (size_t)n * sizeof(int32_t), ctx->stream));
