@@ -45,7 +45,7 @@ __device__ __forceinline__ void dmma(double (&c)[2], double a, double b) {
 // Y[16 x N] = act(X[16 x K] . W^T + b) for the warp's 16 rows.
 // W is [N][K] row-major (torch Linear), K % 4 == 0 except the first layer
 // (guarded), N arbitrary (guarded).  RELU selects the hidden-layer epilogue.
-template <bool RELU>
+template <bool RELU, bool UNROLL = false>
 __device__ __forceinline__ void warp_layer(const double* __restrict__ W, const double* __restrict__ bias, int K,
                                            int N, const double* X, int ldx, double* Y, int ldy, int lane) {
     const int g = lane >> 2, t = lane & 3;
@@ -56,7 +56,7 @@ __device__ __forceinline__ void warp_layer(const double* __restrict__ W, const d
         for (int m = 0; m < 2; ++m)
 #pragma unroll
             for (int j = 0; j < 4; ++j) acc[m][j][0] = acc[m][j][1] = 0.0;
-        for (int kt = 0; kt < K4; ++kt) {
+        auto kstep = [&](int kt) {
             const int k = 4 * kt + t;
             const double a0 = X[g * ldx + k];
             const double a1 = X[(8 + g) * ldx + k];
@@ -70,6 +70,12 @@ __device__ __forceinline__ void warp_layer(const double* __restrict__ W, const d
                     dmma(acc[1][j], a1, b);
                 }
             }
+        };
+        if constexpr (UNROLL) {
+#pragma unroll 4
+            for (int kt = 0; kt < K4; ++kt) kstep(kt);
+        } else {
+            for (int kt = 0; kt < K4; ++kt) kstep(kt);
         }
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
@@ -104,6 +110,9 @@ __device__ __forceinline__ void warp_layer(const double* __restrict__ W, const d
 #ifndef NS_PC_BLOCKS
 #define NS_PC_BLOCKS 3
 #endif
+// BIG (D > 16, e.g. C5's 128 devices): the wide layers' weights stream from L2;
+// their k-loops are unrolled so several B-fragment loads are in flight
+template <bool BIG>
 __global__ void __launch_bounds__(128, NS_PC_BLOCKS) k_plan_cost_dmma(const PlanCostArgs a) {
     extern __shared__ double psm[];
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
@@ -167,7 +176,10 @@ __global__ void __launch_bounds__(128, NS_PC_BLOCKS) k_plan_cost_dmma(const Plan
             for (int m = 0; m < 2; ++m)
 #pragma unroll
                 for (int q = 0; q < 4; ++q) acc1[m][q][0] = acc1[m][q][1] = 0.0;
-            for (int kt = 0; kt < K0p / 4; ++kt) {
+            // (unrolled: the B-fragment loads of several k-steps are in
+            // flight together -- for large D the 2D x 128 layer-1 weights
+            // stream from L2 and a one-step loop exposes its latency per step)
+            auto l1_step = [&](int kt) {
                 const int k = 4 * kt + t;
                 const double a0 = X[g * ldx + k], a1 = X[(8 + g) * ldx + k];
 #pragma unroll
@@ -177,6 +189,12 @@ __global__ void __launch_bounds__(128, NS_PC_BLOCKS) k_plan_cost_dmma(const Plan
                     dmma(acc1[0][q], a0, bv);
                     dmma(acc1[1][q], a1, bv);
                 }
+            };
+            if constexpr (BIG) {
+#pragma unroll 4
+                for (int kt = 0; kt < K0p / 4; ++kt) l1_step(kt);
+            } else {
+                for (int kt = 0; kt < K0p / 4; ++kt) l1_step(kt);
             }
 #pragma unroll
             for (int q = 0; q < 4; ++q) {
@@ -220,9 +238,9 @@ __global__ void __launch_bounds__(128, NS_PC_BLOCKS) k_plan_cost_dmma(const Plan
             }
         }
         __syncwarp();
-        warp_layer<true>(a.cp.W[dir][2], a.cp.b[dir][2], 64, 32, X, ldx, Hc, ldh, lane);
-        warp_layer<true>(a.cp.W[dir][3], a.cp.b[dir][3], 32, 16, Hc, ldh, X, ldx, lane);
-        warp_layer<false>(a.cp.W[dir][4], a.cp.b[dir][4], 16, D, X, ldx, O + dir * D, 2 * D, lane);
+        warp_layer<true, BIG>(a.cp.W[dir][2], a.cp.b[dir][2], 64, 32, X, ldx, Hc, ldh, lane);
+        warp_layer<true, BIG>(a.cp.W[dir][3], a.cp.b[dir][3], 32, 16, Hc, ldh, X, ldx, lane);
+        warp_layer<false, BIG>(a.cp.W[dir][4], a.cp.b[dir][4], 16, D, X, ldx, O + dir * D, 2 * D, lane);
     }
     __syncthreads();
     if (rows && dir == 0 && lane < 16) {
@@ -514,11 +532,17 @@ ns_status launch_plan_cost(ns_ctx* ctx, long long rb, long long re, const uint8_
     int wpb = 4;   // warps per CTA: two per 16-row block (fwd, bwd)
     while (wpb > 2 && per_warp * wpb + per_rb * (wpb / 2) > 72 * 1024) wpb >>= 1;
     const size_t smem = per_warp * wpb + per_rb * (wpb / 2);
-    cudaFuncSetAttribute(k_plan_cost_dmma, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (a.D > 16)
+        cudaFuncSetAttribute(k_plan_cost_dmma<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    else
+        cudaFuncSetAttribute(k_plan_cost_dmma<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     const long long rows = re - rb;
     const long long blocks = (rows + 8LL * wpb - 1) / (8LL * wpb);   // 16 rows per warp pair
     prof_begin(ctx, PK_FINALIZE);
-    k_plan_cost_dmma<<<(unsigned)blocks, wpb * 32, smem, ctx->stream>>>(a);
+    if (a.D > 16)
+        k_plan_cost_dmma<true><<<(unsigned)blocks, wpb * 32, smem, ctx->stream>>>(a);
+    else
+        k_plan_cost_dmma<false><<<(unsigned)blocks, wpb * 32, smem, ctx->stream>>>(a);
     prof_end(ctx);
     NS_LAUNCHED(ctx);
     return NS_OK;

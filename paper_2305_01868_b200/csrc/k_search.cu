@@ -666,6 +666,9 @@ template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 
 constexpr int kStages = 8;   // row-stream ring depth (large-D greedy)
+#ifndef NS_WIDE_WARPRING
+#define NS_WIDE_WARPRING 0   // large-D greedy: per-warp row rings instead of one ring + CTA barrier
+#endif
 #ifndef NS_DSTAGES
 #define NS_DSTAGES 6
 #endif
@@ -1256,12 +1259,25 @@ __global__ void __launch_bounds__(128 * TPD, TPD >= 4 ? 1 : (TPD == 2 ? 2 : 3)) 
     constexpr int NWM = 4 * TPD;             // warps of a D = 128 CTA
     __shared__ __align__(16) double s_w[TPD][SS];
     __shared__ __align__(16) double s_hb1[kV];
+#if NS_WIDE_WARPRING
+    // every warp stages its own copy of the row stream (no CTA barrier per step
+    // for the ring; only the argmin exchange synchronises the CTA)
+    __shared__ __align__(16) double ringw[NWM][kStages][TPD * SS];
+    __shared__ int4 smetaw[NWM][kStages];
+#else
     __shared__ __align__(16) double ring[kStages][TPD * SS];
+#endif
     __shared__ double s_sc[2][NWM];
     __shared__ int s_dv[2][NWM];
     __shared__ int s_cnt[2][NWM];
+#if !NS_WIDE_WARPRING
     __shared__ int4 smeta[kStages];   // {dim, list index, bytes lo, bytes hi}
+#endif
     const int lane = threadIdx.x & 31, wi = threadIdx.x >> 5, nw = blockDim.x >> 5;
+#if NS_WIDE_WARPRING
+    double (*ring)[TPD * SS] = ringw[wi];
+    int4* smeta = smetaw[wi];
+#endif
     const long long tau = a.traj_begin + blockIdx.x;
     if (tau >= a.traj_end) return;
     for (int k = threadIdx.x; k < kV; k += blockDim.x) {
@@ -1303,17 +1319,28 @@ __global__ void __launch_bounds__(128 * TPD, TPD >= 4 ? 1 : (TPD == 2 ? 2 : 3)) 
         }
         cp_async_commit();
     };
+#if NS_WIDE_WARPRING
+    for (int pp = 0; pp < kLook; ++pp) issue(pp);
+#else
     if (wi == 0)
         for (int pp = 0; pp < kLook; ++pp) issue(pp);
+#endif
     const double2* w2 = reinterpret_cast<const double2*>(&s_w[part][0]);
 #pragma unroll 1
     for (int p = 0; p < T; ++p) {
         const int par = p & 1;
+#if NS_WIDE_WARPRING
+        __syncwarp();                 // (the slot being refilled was read two steps ago)
+        issue(p + kLook);
+        cp_async_wait<kLook>();       // table p landed (this lane's copies)
+        __syncwarp();                 // ... and the warp's
+#else
         if (wi == 0) {
             issue(p + kLook);
             cp_async_wait<kLook>();   // table p landed
         }
         __syncthreads();              // ... visible to every warp
+#endif
         const int sl = p % kStages;
         const int4 mt = smeta[sl];
         const int dt = mt.x;
@@ -1367,7 +1394,11 @@ __global__ void __launch_bounds__(128 * TPD, TPD >= 4 ? 1 : (TPD == 2 ? 2 : 3)) 
         }
         if (threadIdx.x == 0) asg[mt.y] = (int8_t)bd;
     }
+#if NS_WIDE_WARPRING
+    cp_async_wait<0>();
+#else
     if (wi == 0) cp_async_wait<0>();
+#endif
     // final per-device cost (every lane takes part in the lane-group sum)
     double acc[4] = {0.0, 0.0, 0.0, 0.0};
 #pragma unroll
