@@ -160,7 +160,8 @@ ns_status ns_tables_single_costs(ns_ctx* ctx, const ns_tables* tables,
 typedef enum {
     NS_SCORE_FP64 = 0,    /* fp64: pooling on the FP64 pipe, comm MLPs on the FP64 tensor cores */
     NS_SCORE_TF32X3 = 1   /* bulk mode (D <= 16): comm MLPs on the tcgen05 tensor cores in
-                             split-TF32 (hi*hi + hi*lo + lo*hi), FP32 accumulation in TMEM;
+                             split-TF32 (hi*hi + hi*lo + lo*hi), FP32 accumulation in TMEM,
+                             and the per-device pooling in fp32 (head epilogue in fp64);
                              ~1e-6 relative plan costs (north star tolerance 1e-3) */
 } ns_score_mode;
 
