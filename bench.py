@@ -487,7 +487,10 @@ def score_plans_rate(ns, ctx, torch):
         mlp_peak = 37.1e12 if name == "fp64" else tf32_peak
         mlp_work = mlp_flop if name == "fp64" else 3 * mlp_flop
         res[name] = {"plans_per_s": P / (ms * 1e-3), "ms_per_call": ms, "pool_ms": pool_ms, "mlp_ms": mlp_ms,
-                     "pool_frac_fp64_pipe": P * pool_flop / (pool_ms * 1e-3) / fp64_pipe,
+                     # pooling runs in fp64 (FP64 pipe) in fp64 mode and in fp32 (FP32
+                     # pipe, 2x the lanes) in the FP32-grade TF32x3 mode
+                     ("pool_frac_fp64_pipe" if name == "fp64" else "pool_frac_fp32_pipe"):
+                         P * pool_flop / (pool_ms * 1e-3) / (fp64_pipe if name == "fp64" else 2 * fp64_pipe),
                      "mlp_tflops": P * mlp_work / (mlp_ms * 1e-3) / 1e12,
                      "mlp_frac": P * mlp_work / (mlp_ms * 1e-3) / mlp_peak,
                      "hbm_gbs": (P * T + P * 8) / (ms * 1e-3) / 1e9}
