@@ -670,7 +670,7 @@ constexpr int kStages = 8;   // row-stream ring depth (large-D greedy)
 #define NS_WIDE_WARPRING 0   // large-D greedy: per-warp row rings instead of one ring + CTA barrier
 #endif
 #ifndef NS_DSTAGES
-#define NS_DSTAGES 6
+#define NS_DSTAGES 3
 #endif
 constexpr int kDStages = NS_DSTAGES;   // row-stream ring depth of the grouped greedy
 #ifndef NS_G1SM
