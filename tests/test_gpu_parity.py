@@ -550,3 +550,32 @@ def test_ablation_invariants(ns, ctx):
     assert np.all(tw11["cost"] <= tw1["cost"])
     assert np.isfinite(cw["cost"]).sum() >= np.isfinite(tw11["cost"]).sum()
     tabs.free()
+
+
+def test_precompute_batched_path_bit_identical(ns, ctx):
+    """The precompute has two launch shapes: batches of >= 16*16*SMs rows keep
+    the encoder/projection weights in shared memory (one 16-warp CTA per SM),
+    small calls read them through L1.  Same fragment scheme and arithmetic
+    order, so the single costs (and every search decision) are bit-identical;
+    a table-wise search of the small batch equals the same tasks inside the
+    large batch."""
+    w = gen_weights(4, "mono")
+    tasks = gen_tasks("C2", 1200)               # 48000 rows: batched shape
+    ns.ns_load_cost_models(ctx, w)
+    desc, off, caps = ns.table_descs(tasks)
+    big = ns.ns_featurize_tables(ctx, desc, off, caps)
+    c_big = ns.ns_tables_single_costs(ctx, big)
+    small_tasks = tasks[:8]                      # 320 rows: L1 shape
+    d2, o2, k2 = ns.table_descs(small_tasks)
+    small = ns.ns_featurize_tables(ctx, d2, o2, k2)
+    c_small = ns.ns_tables_single_costs(ctx, small)
+    np.testing.assert_array_equal(c_small, c_big[:len(c_small)])
+    r_big = ns.ns_shard_tablewise(ctx, big, 4, M=11)
+    r_small = ns.ns_shard_tablewise(ctx, small, 4, M=11)
+    np.testing.assert_array_equal(r_small["cost"], r_big["cost"][:8])
+    np.testing.assert_array_equal(r_small["assign"], r_big["assign"][:8, :r_small["assign"].shape[1]])
+    emb = om.TableEmbeddings(w, tasks[0])
+    ref = [om.compute_cost(w, emb, [(s, int(tasks[0].dims[s]))]) for s in range(tasks[0].T)]
+    assert max(_rel(a, b) for a, b in zip(c_big[:tasks[0].T], ref)) < RTOL
+    big.free()
+    small.free()
