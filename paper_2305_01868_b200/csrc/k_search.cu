@@ -1423,7 +1423,22 @@ __global__ void __launch_bounds__(128 * TPD, TPD >= 4 ? 1 : (TPD == 2 ? 2 : 3)) 
 // Level 0 (one column plan per task, C = 1): one warp per task.  The grid
 // argmin (lowest m on ties, R12) is reduced with shuffles; level 0 always
 // installs [] as the initial global best (R15).
-__global__ void __launch_bounds__(256) k_select0(SearchBufs b) {
+// Pack per-task results into the contiguous staging layout.
+struct OutStage {
+    double* cost;
+    int32_t* n_col;
+    int32_t* col_plan;   // [n][Lout]
+    int8_t* assign;      // [n][astride]: columns >= Tpm are -1
+    int astride;
+    int32_t* grid;
+    uint64_t* scores;
+    // which fields point straight at the caller's device buffers (no copy in deliver)
+    bool d_cost, d_ncol, d_plan, d_assign, d_grid, d_scores;
+};
+
+// final_out (table-wise search, L = 0): level 0 is the whole search, so the
+// warp also packs the task's outputs (k_write_out's job) -- one launch less.
+__global__ void __launch_bounds__(256) k_select0(SearchBufs b, OutStage o, int final_out) {
     const int lane = threadIdx.x & 31;
     for (int q = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; q < b.n_tasks; q += (gridDim.x * blockDim.x) >> 5) {
         unsigned long long wsum = 0;
@@ -1451,11 +1466,19 @@ __global__ void __launch_bounds__(256) k_select0(SearchBufs b) {
         }
         if (best == CUDART_INF) bm = -1;
         if (lane == 0) {
-            b.n_scores[q] += wsum;
+            const unsigned long long sc = b.n_scores[q] + wsum;
+            b.n_scores[q] = sc;
             b.best_cost[q] = best;
             b.best_m[q] = bm;
             b.best_ncol[q] = 0;
             b.beam_cnt[q] = 1;   // C_p <- {[]}
+            if (final_out) {
+                o.cost[q] = best;
+                o.n_col[q] = 0;
+                o.grid[q] = bm;
+                o.scores[q] = sc;
+                o.col_plan[q] = -1;   // Lout = 1 slot, no split
+            }
         }
         const int Tp = b.cp_Tp[q];
         long long src = -1;
@@ -1463,8 +1486,14 @@ __global__ void __launch_bounds__(256) k_select0(SearchBufs b) {
             const long long tau = (long long)q * b.M + bm;
             src = b.dup_of[tau] >= 0 ? (long long)b.dup_of[tau] : tau;
         }
-        for (int i = lane; i < b.Tpm; i += 32)
-            b.best_assign[(size_t)q * b.Tpm + i] = (src >= 0 && i < Tp) ? b.assign[src * b.Tpm + i] : (int8_t)-1;
+        if (final_out) {
+            for (int i = lane; i < o.astride; i += 32)
+                o.assign[(size_t)q * o.astride + i] =
+                    (src >= 0 && i < Tp && i < b.Tpm) ? b.assign[src * b.Tpm + i] : (int8_t)-1;
+        } else {
+            for (int i = lane; i < b.Tpm; i += 32)
+                b.best_assign[(size_t)q * b.Tpm + i] = (src >= 0 && i < Tp) ? b.assign[src * b.Tpm + i] : (int8_t)-1;
+        }
     }
 }
 
@@ -1635,18 +1664,6 @@ __global__ void k_grid_caps(const int64_t* sumdim, int n_tasks, int D, int M, do
     capdim[i] = f > 2.0e9 ? 2000000000 : (int32_t)f;
 }
 
-// Pack per-task results into the contiguous staging layout.
-struct OutStage {
-    double* cost;
-    int32_t* n_col;
-    int32_t* col_plan;   // [n][Lout]
-    int8_t* assign;      // [n][astride]: columns >= Tpm are -1
-    int astride;
-    int32_t* grid;
-    uint64_t* scores;
-    // which fields point straight at the caller's device buffers (no copy in deliver)
-    bool d_cost, d_ncol, d_plan, d_assign, d_grid, d_scores;
-};
 
 __global__ void __launch_bounds__(256) k_write_out(SearchBufs b, OutStage o, int Lout) {
     const int lane = threadIdx.x & 31;
@@ -2066,8 +2083,12 @@ ns_status run_search(ns_ctx* ctx, const ns_tables* t, int D, const ns_search_par
     }
     launch_order(b.n_tasks, warp_order ? 1 : 0);
     if ((s = run_level_trajectories(ctx, b, t, b.n_tasks)) != NS_OK) return s;
+    // table-wise (L = 0): the level-0 selection also packs the outputs
+    const bool final0 = L == 0;
+    if (final0) bind_outputs(o, out, b.n_tasks, Lout);
     prof_begin(ctx, PK_SELECT);
-    k_select0<<<(unsigned)std::max(1, std::min((b.n_tasks + 7) / 8, ctx->sm_count * 8)), 256, 0, ctx->stream>>>(b);
+    k_select0<<<(unsigned)std::max(1, std::min((b.n_tasks + 7) / 8, ctx->sm_count * 8)), 256, 0, ctx->stream>>>(
+        b, o, final0 ? 1 : 0);
     prof_end(ctx);
     NS_LAUNCHED(ctx);
     // ---- beam levels (Alg. 1 lines 6-22)
@@ -2090,12 +2111,14 @@ ns_status run_search(ns_ctx* ctx, const ns_tables* t, int D, const ns_search_par
         prof_end(ctx);
         NS_LAUNCHED(ctx);
     }
-    bind_outputs(o, out, b.n_tasks, Lout);
-    prof_begin(ctx, PK_OTHER);
-    k_write_out<<<(unsigned)std::max(1, std::min((b.n_tasks + 7) / 8, ctx->sm_count * 8)), 256, 0, ctx->stream>>>(
-        b, o, Lout > 0 ? Lout : 1);
-    prof_end(ctx);
-    NS_LAUNCHED(ctx);
+    if (!final0) {
+        bind_outputs(o, out, b.n_tasks, Lout);
+        prof_begin(ctx, PK_OTHER);
+        k_write_out<<<(unsigned)std::max(1, std::min((b.n_tasks + 7) / 8, ctx->sm_count * 8)), 256, 0, ctx->stream>>>(
+            b, o, Lout > 0 ? Lout : 1);
+        prof_end(ctx);
+        NS_LAUNCHED(ctx);
+    }
     return deliver(ctx, t, o, Lout, b.Tpm, out, (p->flags & NS_SEARCH_ASYNC) != 0);
 }
 
