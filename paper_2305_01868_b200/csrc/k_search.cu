@@ -1701,6 +1701,8 @@ struct Carver {
     }
 };
 
+static unsigned int* base_counter(int32_t* pair) { return reinterpret_cast<unsigned int*>(pair + 1); }
+
 void carve(Carver& c, SearchBufs& b, OutStage& o, int Lout) {
     b.cp_task = c.take<int32_t>(b.S);
     b.cp_valid = c.take<int32_t>(b.S);
@@ -1717,8 +1719,11 @@ void carve(Carver& c, SearchBufs& b, OutStage& o, int Lout) {
     b.tcost = c.take<double>(b.n_traj);
     b.dup_of = c.take<int32_t>(b.n_traj);
     b.uniq = c.take<int32_t>(b.n_traj);
-    b.n_uniq = c.take<int32_t>(1);
-    b.next_cp = c.take<unsigned int>(1);
+    {   // the two per-launch counters are adjacent: one memset clears both
+        int32_t* ctr = c.take<int32_t>(2);
+        b.n_uniq = ctr;
+        b.next_cp = base_counter(ctr);
+    }
     b.gscratch = c.take<double>((size_t)b.gscratch_warps * b.M * b.D * kV);
     b.ghist = c.take<int8_t>((size_t)b.gscratch_warps * b.M * b.Tpm);
     b.capdim = c.take<int32_t>((size_t)b.n_tasks * b.M);
@@ -1753,6 +1758,9 @@ TaskView task_view(const ns_tables* t) {
 size_t order_smem(int Tpm) { return ((size_t)((Tpm + 1) & ~1)) * 4 + (size_t)Tpm * 8; }
 
 ns_status launch_greedy(ns_ctx* ctx, const SearchBufs& b, const ns_tables* t, long long tb, long long te) {
+    // one memset per (greedy, finalize) pair: the grouped greedy's queue
+    // counter and the compaction counter of the finalize that follows
+    NS_CUDA(ctx, cudaMemsetAsync(b.n_uniq, 0, 2 * sizeof(int32_t), ctx->stream));
     if (te <= tb) return NS_OK;
     GreedyArgs a;
     a.traj_begin = (int)tb;
@@ -1841,7 +1849,6 @@ ns_status launch_greedy(ns_ctx* ctx, const SearchBufs& b, const ns_tables* t, lo
         x.dup_of = b.dup_of + (size_t)g0 * b.M;
         x.tau_base = g0 * b.M;
         x.next_cp = b.next_cp;
-        NS_CUDA(ctx, cudaMemsetAsync(b.next_cp, 0, sizeof(unsigned int), ctx->stream));
         const int lpd = 32 / dp;
         const int mc = b.M <= 16 ? 16 : 64;
         const int wpb = NS_DEDUP_WPB;
@@ -1901,7 +1908,7 @@ __global__ void k_compact(const uint8_t* feas, const int32_t* dup_of, long long 
 
 ns_status launch_finalize(ns_ctx* ctx, const SearchBufs& b, long long tb, long long te) {
     if (te <= tb) return NS_OK;
-    NS_CUDA(ctx, cudaMemsetAsync(b.n_uniq, 0, sizeof(int32_t), ctx->stream));
+    // (n_uniq was cleared with the greedy queue counter by launch_greedy)
     const long long n = te - tb;
     prof_begin(ctx, PK_OTHER);
     k_compact<<<(unsigned)std::min<long long>((n + 255) / 256, 2048), 256, 0, ctx->stream>>>(b.feas, b.dup_of, tb, te,
