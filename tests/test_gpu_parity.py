@@ -110,14 +110,18 @@ def test_tablewise_C2(ns, ctx, greedy):
     _check_tablewise(ns, ctx, gen_tasks("C2", 24), w, M=11, greedy=greedy)
 
 
+BENCH_TASKS = 65536   # bench.py --tasks default (BASELINE configs[1] = C2)
+
+
 def test_tablewise_C2_bench_launch(ns, ctx):
-    # the bench's launch configuration (many tasks -> grouped greedy, auto
-    # mode); the oracle checks a sample of tasks one by one
+    # the bench's full size and launch configuration (65536 tasks -> batched
+    # precompute, grouped greedy, auto mode); the oracle checks a sample of
+    # tasks one by one
     w = gen_weights(4, "mono")
-    tasks = gen_tasks("C2", 4096)
+    tasks = gen_tasks("C2", BENCH_TASKS)
     tabs = _setup(ns, ctx, tasks, w)
     out = ns.ns_shard_tablewise(ctx, tabs, 4, M=11)
-    for i in range(0, 4096, 97):
+    for i in range(0, BENCH_TASKS, 257):
         task = tasks[i]
         emb = om.TableEmbeddings(w, task)
         r = osr.greedy_grid_search(w, emb, task, [], 11)

@@ -90,7 +90,7 @@ def main():
         if "k_greedy_dedup" in d["Kernel Name"]:
             json.dump({"kernel": d["Kernel Name"], "bytes_per_launch": dram,
                        "source": f"ncu --set full, profiles/{out_tag}_ncu_full_metrics.json "
-                                 "(dram__bytes_read.sum + dram__bytes_write.sum, 16384 C2 tasks)"},
+                                 "(dram__bytes_read.sum + dram__bytes_write.sum, bench default batch of C2 tasks)"},
                       open("profiles/greedy_traffic.json", "w"), indent=1)
 
 
