@@ -398,15 +398,36 @@ __global__ void __launch_bounds__(256) k_order_warp(SearchBufs b, TaskView tv, i
         __syncwarp();
         for (int i = lane; i < Tp; i += 32) key[i] = tv.C[rows[i]];
         __syncwarp();
-        for (int i = lane; i < Tp; i += 32) {
-            const double ci = key[i];
-            int r = 0;
+        if (Tp <= 64) {
+            // items lane and lane + 32 ranked in one pass over the keys (each
+            // key load serves both comparisons; no second, mostly idle pass)
+            const int i0 = lane, i1 = lane + 32;
+            const double c0 = i0 < Tp ? key[i0] : 0.0, c1 = i1 < Tp ? key[i1] : 0.0;
+            int r0 = 0, r1 = 0;
             for (int k = 0; k < Tp; ++k) {
                 const double ck = key[k];
-                r += (ck > ci) || (ck == ci && k < i);
+                r0 += (ck > c0) || (ck == c0 && k < i0);
+                r1 += (ck > c1) || (ck == c1 && k < i1);
             }
-            b.ord_row[(size_t)g * b.Tpm + r] = rows[i];
-            b.ord_meta[(size_t)g * b.Tpm + r] = pack_meta(tv, rows[i], i);
+            if (i0 < Tp) {
+                b.ord_row[(size_t)g * b.Tpm + r0] = rows[i0];
+                b.ord_meta[(size_t)g * b.Tpm + r0] = pack_meta(tv, rows[i0], i0);
+            }
+            if (i1 < Tp) {
+                b.ord_row[(size_t)g * b.Tpm + r1] = rows[i1];
+                b.ord_meta[(size_t)g * b.Tpm + r1] = pack_meta(tv, rows[i1], i1);
+            }
+        } else {
+            for (int i = lane; i < Tp; i += 32) {
+                const double ci = key[i];
+                int r = 0;
+                for (int k = 0; k < Tp; ++k) {
+                    const double ck = key[k];
+                    r += (ck > ci) || (ck == ci && k < i);
+                }
+                b.ord_row[(size_t)g * b.Tpm + r] = rows[i];
+                b.ord_meta[(size_t)g * b.Tpm + r] = pack_meta(tv, rows[i], i);
+            }
         }
         __syncwarp();
     }
