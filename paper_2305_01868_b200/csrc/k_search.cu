@@ -693,7 +693,10 @@ constexpr int kStages = 8;   // row-stream ring depth (large-D greedy)
 #ifndef NS_DSTAGES
 #define NS_DSTAGES 3
 #endif
-constexpr int kDStages = NS_DSTAGES;   // row-stream ring depth of the grouped greedy
+#ifndef NS_PAIR_STAGE
+#define NS_PAIR_STAGE 2   // tables staged per cp.async group in the grouped greedy (0: one per step)
+#endif
+constexpr int kDStages = NS_PAIR_STAGE ? 2 * NS_PAIR_STAGE : NS_DSTAGES;   // row-stream ring depth of the grouped greedy
 #ifndef NS_G1SM
 #define NS_G1SM 1   // group 1 of the grouped greedy in shared memory (typed pass)
 #endif
@@ -868,6 +871,7 @@ __global__ void __launch_bounds__(NS_DEDUP_WPB * 32, (LPD >= 8 ? NS_DEDUP_BLOCKS
         // row-index window: the next 32 entries of the cost order in one register per lane
         int oc_cur = lane < Tp ? __ldg(orow + lane) : 0;
         int oc_nxt = 32 + lane < Tp ? __ldg(orow + 32 + lane) : 0;
+#if !NS_PAIR_STAGE
         // ring slots rotate with counters (no modulo): table pp goes to slot
         // pp % kDStages == sl_w at its issue
         int sl_w = 0;
@@ -884,6 +888,24 @@ __global__ void __launch_bounds__(NS_DEDUP_WPB * 32, (LPD >= 8 ? NS_DEDUP_BLOCKS
             cp_async_commit();   // one group per step, empty past the end
             sl_w = sl_w + 1 == kDStages ? 0 : sl_w + 1;
         };
+#else
+        // group staging: G = NS_PAIR_STAGE consecutive tables of the cost order
+        // go into slots pp % 2G as ONE cp.async group, issued every G-th step
+        // (1/G of the issue / wait / warp-sync overhead per step); the ring
+        // holds the G tables in use and the G in flight
+        constexpr int G = NS_PAIR_STAGE;
+        auto stage1 = [&](int pp) {
+            if (pp < Tp) {
+                if (pp > 0 && (pp & 31) == 0) {
+                    oc_cur = oc_nxt;
+                    oc_nxt = pp + 32 + lane < Tp ? __ldg(orow + pp + 32 + lane) : 0;
+                }
+                const int r = __shfl_sync(kFull, oc_cur, pp & 31);
+                cp_async16(ring_lane + (pp % (2 * G)) * SM::RS, a.V + (size_t)r * kV + 2 * lane);
+                if (lane == 0) cp_async16(&s.meta[pp % (2 * G)], ometa + pp);
+            }
+        };
+#endif
         // one group's pass over table t (G0: group 0, register-resident state)
         auto pass = [&](auto g0tag, const int gr, const auto& vcd, const int dt, const long long bt, const int idx,
                         const int p) {
@@ -1161,6 +1183,22 @@ __global__ void __launch_bounds__(NS_DEDUP_WPB * 32, (LPD >= 8 ? NS_DEDUP_BLOCKS
 #endif
         };
 #pragma unroll 1
+#if NS_PAIR_STAGE
+#pragma unroll
+        for (int j = 0; j < G; ++j) stage1(j);
+        cp_async_commit();
+#pragma unroll 1
+        for (int p = 0; p < Tp; ++p) {
+            const int sl = p % (2 * G);
+            if (p % G == 0) {
+                __syncwarp();              // tables p - G .. p - 1 (slots being refilled) consumed
+#pragma unroll
+                for (int j = 0; j < G; ++j) stage1(p + G + j);
+                cp_async_commit();
+                cp_async_wait<1>();        // tables p .. p + G - 1 have landed (this lane's copies)
+                __syncwarp();              // ... and every lane's
+            }
+#else
         for (int pp = 0; pp < kDStages - 1; ++pp) issue(pp);
         int sl = 0;   // slot of table p
 #pragma unroll 1
@@ -1169,6 +1207,7 @@ __global__ void __launch_bounds__(NS_DEDUP_WPB * 32, (LPD >= 8 ? NS_DEDUP_BLOCKS
             issue(p + kDStages - 1);
             cp_async_wait<kDStages - 1>();  // table p has landed (this lane's copies)
             __syncwarp();                  // ... and every lane's
+#endif
             double vcd[FPL];
             const double2* src = reinterpret_cast<const double2*>(&s.ring[sl][part * SS]);
 #pragma unroll
