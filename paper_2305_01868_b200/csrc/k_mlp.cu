@@ -108,12 +108,12 @@ __device__ __forceinline__ void warp_layer(const double* __restrict__ W, const d
 // so no 16 x 128 activation buffer is needed (15 KB per warp instead of 27 KB
 // -> 1.5x the resident warps).  Layers 3-5 use warp_layer.
 #ifndef NS_PC_BLOCKS
-#define NS_PC_BLOCKS 3
+#define NS_PC_BLOCKS 4
 #endif
 // BIG (D > 16, e.g. C5's 128 devices): the wide layers' weights stream from L2;
 // their k-loops are unrolled so several B-fragment loads are in flight
 template <bool BIG>
-__global__ void __launch_bounds__(128, NS_PC_BLOCKS) k_plan_cost_dmma(const PlanCostArgs a) {
+__global__ void __launch_bounds__(128, BIG ? 3 : NS_PC_BLOCKS) k_plan_cost_dmma(const PlanCostArgs a) {
     extern __shared__ double psm[];
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
     const int g = lane >> 2, t = lane & 3;
