@@ -302,7 +302,10 @@ constexpr int kPWTotal = kPOH2 + 64;                          // doubles
 // a conflict-free shared-memory load); otherwise B fragments through L1 with
 // 4-warp CTAs (a few hundred rows: no staging latency).
 template <bool WSM>
-__global__ void __launch_bounds__(WSM ? 512 : 128, WSM ? 1 : NS_PRE_BLOCKS) k_precompute_dmma(const PreDmmaArgs a) {
+#ifndef NS_PRE_WSM_WARPS
+#define NS_PRE_WSM_WARPS 16   // warps of the batched (shared-memory weights) precompute CTA
+#endif
+__global__ void __launch_bounds__(WSM ? 32 * NS_PRE_WSM_WARPS : 128, WSM ? 1 : NS_PRE_BLOCKS) k_precompute_dmma(const PreDmmaArgs a) {
     extern __shared__ double qsm[];
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
     const int g = lane >> 2, t = lane & 3;
@@ -570,7 +573,7 @@ void launch_precompute(ns_ctx* ctx, const ns_tables* t, int jlo, int jhi) {
     // batches stage the weights once per SM; a few hundred rows (a single
     // task) read them through L1 instead of paying the staging latency
     const bool wsm = a.n_rows >= 16LL * 16 * ctx->sm_count;
-    const int wpb = wsm ? 16 : 4;
+    const int wpb = wsm ? NS_PRE_WSM_WARPS : 4;
     const size_t smem = wsm ? ((size_t)kPWTotal + (size_t)wpb * (16 * (a.ldx + a.ldy) + 16)) * sizeof(double)
                             : (size_t)wpb * (16 * (a.ldx + 2 * a.ldy) + 16) * sizeof(double);
     if (wsm)
