@@ -687,9 +687,6 @@ template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 
 constexpr int kStages = 8;   // row-stream ring depth (large-D greedy)
-#ifndef NS_WIDE_WARPRING
-#define NS_WIDE_WARPRING 0   // large-D greedy: per-warp row rings instead of one ring + CTA barrier
-#endif
 #ifndef NS_DSTAGES
 #define NS_DSTAGES 3
 #endif
@@ -1316,28 +1313,16 @@ __global__ void __launch_bounds__(128 * TPD, TPD >= 4 ? 1 : (TPD == 2 ? 2 : 3)) 
     constexpr int FPL = kV / TPD;            // features per thread
     constexpr int SS = FPL + 2;              // padded slice stride (doubles)
     constexpr int kLook = kStages - 2;       // the slot being overwritten was last read two steps ago
+    constexpr int kRingW = kStages;
     constexpr int NWM = 4 * TPD;             // warps of a D = 128 CTA
     __shared__ __align__(16) double s_w[TPD][SS];
     __shared__ __align__(16) double s_hb1[kV];
-#if NS_WIDE_WARPRING
-    // every warp stages its own copy of the row stream (no CTA barrier per step
-    // for the ring; only the argmin exchange synchronises the CTA)
-    __shared__ __align__(16) double ringw[NWM][kStages][TPD * SS];
-    __shared__ int4 smetaw[NWM][kStages];
-#else
-    __shared__ __align__(16) double ring[kStages][TPD * SS];
-#endif
+    __shared__ __align__(16) double ring[kRingW][TPD * SS];
     __shared__ double s_sc[2][NWM];
     __shared__ int s_dv[2][NWM];
     __shared__ int s_cnt[2][NWM];
-#if !NS_WIDE_WARPRING
-    __shared__ int4 smeta[kStages];   // {dim, list index, bytes lo, bytes hi}
-#endif
+    __shared__ int4 smeta[kRingW];    // {dim, list index, bytes lo, bytes hi}
     const int lane = threadIdx.x & 31, wi = threadIdx.x >> 5, nw = blockDim.x >> 5;
-#if NS_WIDE_WARPRING
-    double (*ring)[TPD * SS] = ringw[wi];
-    int4* smeta = smetaw[wi];
-#endif
     const long long tau = a.traj_begin + blockIdx.x;
     if (tau >= a.traj_end) return;
     for (int k = threadIdx.x; k < kV; k += blockDim.x) {
@@ -1370,38 +1355,30 @@ __global__ void __launch_bounds__(128 * TPD, TPD >= 4 ? 1 : (TPD == 2 ? 2 : 3)) 
     // warp 0 streams the cost-ordered v rows through a cp.async ring; lane l
     // copies features (2l, 2l + 1) into slice 2l / FPL
     const int my_slice = (2 * lane) / FPL, my_off = (2 * lane) % FPL;
-    auto issue = [&](int pp) {
+    auto stage = [&](int pp) {
         if (pp < T) {
             const int r = __ldg(orow + pp);
-            const int slot = pp % kStages;
+            const int slot = pp % kRingW;
             cp_async16(&ring[slot][my_slice * SS + my_off], a.V + (size_t)r * kV + 2 * lane);
             if (lane == 0) cp_async16(smeta + slot, ometa + pp);
         }
+    };
+    auto issue = [&](int pp) {
+        stage(pp);
         cp_async_commit();
     };
-#if NS_WIDE_WARPRING
-    for (int pp = 0; pp < kLook; ++pp) issue(pp);
-#else
     if (wi == 0)
         for (int pp = 0; pp < kLook; ++pp) issue(pp);
-#endif
     const double2* w2 = reinterpret_cast<const double2*>(&s_w[part][0]);
 #pragma unroll 1
     for (int p = 0; p < T; ++p) {
         const int par = p & 1;
-#if NS_WIDE_WARPRING
-        __syncwarp();                 // (the slot being refilled was read two steps ago)
-        issue(p + kLook);
-        cp_async_wait<kLook>();       // table p landed (this lane's copies)
-        __syncwarp();                 // ... and the warp's
-#else
         if (wi == 0) {
             issue(p + kLook);
             cp_async_wait<kLook>();   // table p landed
         }
         __syncthreads();              // ... visible to every warp
-#endif
-        const int sl = p % kStages;
+        const int sl = p % kRingW;
         const int4 mt = smeta[sl];
         const int dt = mt.x;
         const long long bt = (long long)(((unsigned long long)(unsigned)mt.w << 32) | (unsigned)mt.z);
@@ -1454,11 +1431,7 @@ __global__ void __launch_bounds__(128 * TPD, TPD >= 4 ? 1 : (TPD == 2 ? 2 : 3)) 
         }
         if (threadIdx.x == 0) asg[mt.y] = (int8_t)bd;
     }
-#if NS_WIDE_WARPRING
-    cp_async_wait<0>();
-#else
     if (wi == 0) cp_async_wait<0>();
-#endif
     // final per-device cost (every lane takes part in the lane-group sum)
     double acc[4] = {0.0, 0.0, 0.0, 0.0};
 #pragma unroll
