@@ -1017,8 +1017,9 @@ __global__ void __launch_bounds__(NS_DEDUP_WPB * 32, (LPD >= 8 ? NS_DEDUP_BLOCKS
                     int bd = -1;
                     uint32_t cnt = 0;
                     const int cm = s.mcap[m];
-                    for (int dd = 0; dd < D; ++dd) {
-                        if (s.sok[dd] && s.sdv[dd] <= cm) {
+#pragma unroll
+                    for (int dd = 0; dd < DPW; ++dd) {   // DPW >= D device slots, unrolled
+                        if (dd < D && s.sok[dd] && s.sdv[dd] <= cm) {
                             ++cnt;
                             const double sv = s.sc[dd];
                             if (sv < best) {
