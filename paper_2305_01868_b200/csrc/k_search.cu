@@ -937,10 +937,8 @@ __global__ void __launch_bounds__(NS_DEDUP_WPB * 32, (LPD >= 8 ? NS_DEDUP_BLOCKS
             //      device -> all members see the same feasible set and take
             //      the group argmin (no split, uniform work)
             {
-                int smax = f ? dsum + dt : 0;
-#pragma unroll
-                for (int o = 16; o >= LPD; o >>= 1) smax = max(smax, __shfl_xor_sync(kFull, smax, o));
-                if (smax <= gmin_gr) {
+                // (one warp vote: every scored device fits the tightest member cap)
+                if (__all_sync(kFull, !f || dsum + dt <= gmin_gr)) {
                     // device argmin: butterfly minimum, then the lowest device
                     // attaining it (R13) from one ballot
                     const double own = f ? sco : CUDART_INF;
