@@ -371,6 +371,7 @@ def main():
     if rank == 0 and not args.no_secondary and not args.profile_run:
         secondary = search_latency(ns, ctx, torch)
         secondary["score_plans"] = score_plans_rate(ns, ctx, torch)
+        secondary["service"] = service_rate(ns)
 
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": "scores/s", "n_gpus": world, "steps": args.steps,
@@ -439,6 +440,39 @@ def search_latency(ns, ctx, torch):
         res[f"{cfg}x{n}"] = {"mode": "columnwise, batched", "tasks": n, "ms_per_task": 1e3 * t / n,
                              "scores": scores, "scores_per_s": scores / t}
     return res
+
+
+def service_rate(ns):
+    """the batching front end (paper_2305_01868_b200.service)
+    fed by 8 submitter threads with 16384 host-side C2 tasks; wall time from
+    the first submit to the last result (host packing, featurise, search and
+    per-task result split included)."""
+    import threading
+    from paper_2305_01868_b200.service import ShardingService
+    c = CONFIGS[CFG]
+    w = gen_weights(c["D"], "mono")
+    tasks = gen_tasks(CFG, 16384, start=1 << 20)
+    with ShardingService(w, c["D"], M=c["M"], max_batch=8192, max_wait_ms=5.0) as svc:
+        svc.shard(tasks[:256])   # warm-up
+        b0, t0n = svc.batches, svc.tasks
+        res = [None] * len(tasks)
+
+        def sub(k):
+            fs = [(i, svc.submit(tasks[i])) for i in range(k, len(tasks), 8)]
+            for i, f in fs:
+                res[i] = f.result()
+
+        th = [threading.Thread(target=sub, args=(k,)) for k in range(8)]
+        t0 = time.perf_counter()
+        for t in th:
+            t.start()
+        for t in th:
+            t.join()
+        dt = time.perf_counter() - t0
+        batches = svc.batches - b0
+    scores = sum(r["n_scores"] for r in res)
+    return {"tasks": len(tasks), "submitters": 8, "batches": batches, "tasks_per_s": len(tasks) / dt,
+            "scores_per_s": scores / dt, "ms_total": 1e3 * dt}
 
 
 def score_plans_rate(ns, ctx, torch):

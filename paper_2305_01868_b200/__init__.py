@@ -34,3 +34,4 @@ from ._native import (  # noqa: F401
     ns_tables_single_costs,
     table_descs,
 )
+from .service import ShardingService  # noqa: F401,E402

@@ -70,3 +70,15 @@ def test_oracle_and_product_are_independent():
         if f.endswith(".py"):
             txt = open(os.path.join(ROOT, "oracle", f)).read()
             assert "paper_2305_01868_b200" not in re.findall(r"^\s*(?:from|import)\s+(\w+)", txt, re.M), f
+
+
+def test_batching_service_without_gpu_raises():
+    """The batching service's worker reports the ctx failure to the caller
+    (no silent CPU path)."""
+    import torch
+    from paper_2305_01868_b200 import NSError, ShardingService
+    from workload.synth import gen_weights
+    if torch.cuda.is_available():
+        pytest.skip("GPU present")
+    with pytest.raises(NSError):
+        ShardingService(gen_weights(4, "mono"), 4)

@@ -583,3 +583,42 @@ def test_precompute_batched_path_bit_identical(ns, ctx):
     assert max(_rel(a, b) for a, b in zip(c_big[:tasks[0].T], ref)) < RTOL
     big.free()
     small.free()
+
+
+def test_batching_service(ns, ctx):
+    """the batching front end (paper_2305_01868_b200.service)
+    -- tasks submitted one by one from four threads, batched by the worker --
+    returns exactly the plans of one direct batched call (table-wise), and the
+    column-wise service matches the direct column-wise search."""
+    import threading
+    from paper_2305_01868_b200.service import ShardingService
+    w = gen_weights(4, "mono")
+    tasks = gen_tasks("C2", 200)
+    tabs = _setup(ns, ctx, tasks, w)
+    ref = ns.ns_shard_tablewise(ctx, tabs, 4, M=11)
+    tabs.free()
+    res = [None] * len(tasks)
+    with ShardingService(w, 4, M=11, max_batch=64, max_wait_ms=2.0) as svc:
+        def worker(k):
+            fs = [(i, svc.submit(tasks[i])) for i in range(k, len(tasks), 4)]
+            for i, f in fs:
+                res[i] = f.result(timeout=120)
+        th = [threading.Thread(target=worker, args=(k,)) for k in range(4)]
+        for t in th:
+            t.start()
+        for t in th:
+            t.join()
+        assert svc.tasks == len(tasks) and svc.batches >= 4
+    for i, r in enumerate(res):
+        assert r["cost"] == ref["cost"][i]
+        assert r["n_scores"] == int(ref["n_scores"][i])
+        np.testing.assert_array_equal(r["assign"], ref["assign"][i, :tasks[i].T])
+    ctasks = [gen_task("C3", i, T=24, D=4) for i in range(12)]
+    tabs = _setup(ns, ctx, ctasks, w)
+    cref = ns.ns_shard_columnwise(ctx, tabs, 4, N=4, K=2, L=2, M=5)
+    tabs.free()
+    with ShardingService(w, 4, columnwise=True, N=4, K=2, L=2, M=5, max_batch=5) as svc:
+        cres = svc.shard(ctasks)
+    for i, r in enumerate(cres):
+        assert r["cost"] == cref["cost"][i]
+        assert r["col_plan"] == cref["col_plan"][i, :int(cref["n_col"][i])].tolist()
