@@ -202,20 +202,15 @@ def ns_load_cost_models(ctx: int, weights) -> int:
 def table_descs(tasks: Sequence) -> tuple:
     """Pack tasks (objects with dims/hash/pooling/skew/cap) into the ABI's
     descriptor array, offsets and caps (host numpy)."""
-    n = sum(t.T for t in tasks)
-    desc = np.zeros(n, dtype=TABLE_DESC)
     off = np.zeros(len(tasks) + 1, dtype=np.int32)
-    caps = np.zeros(len(tasks), dtype=np.int64)
-    k = 0
-    for i, t in enumerate(tasks):
-        T = t.T
-        desc["dim"][k:k + T] = t.dims
-        desc["hash_size"][k:k + T] = t.hash
-        desc["pooling_factor"][k:k + T] = t.pooling
-        desc["skew"][k:k + T] = t.skew
-        k += T
-        off[i + 1] = k
-        caps[i] = t.cap
+    np.cumsum([t.T for t in tasks], out=off[1:])
+    caps = np.fromiter((t.cap for t in tasks), dtype=np.int64, count=len(tasks))
+    desc = np.zeros(int(off[-1]), dtype=TABLE_DESC)
+    if len(tasks):
+        desc["dim"] = np.concatenate([t.dims for t in tasks])
+        desc["hash_size"] = np.concatenate([t.hash for t in tasks])
+        desc["pooling_factor"] = np.concatenate([t.pooling for t in tasks])
+        desc["skew"] = np.concatenate([t.skew for t in tasks])
     return desc, off, caps
 
 
