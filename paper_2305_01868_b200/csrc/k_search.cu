@@ -1825,11 +1825,15 @@ ns_status launch_greedy(ns_ctx* ctx, const SearchBufs& b, const ns_tables* t, lo
     // one warp per column plan leaves most SMs idle and the step chain is the
     // critical path, so every trajectory runs in its own lane segment
     // (k_greedy_cta).  Throughput mode (many column plans): grouped greedy.
+    // Both kernels split a device's 64 features over the same LPD = 32 / dp
+    // lanes and sum them in the same order, so their scores -- hence their
+    // decisions and plan costs -- are bit-identical: a task's result does not
+    // depend on the batch (kernel) it runs in.
     const bool latency_mode =
-        4 * dp <= 32 && (b.greedy_mode == NS_GREEDY_LANES || b.M > 64 ||   // grouped kernel: M <= 64
-                         (b.greedy_mode == NS_GREEDY_AUTO && n_cp_launch * 4 < (long long)ctx->sm_count * 16));
+        dp <= 16 && (b.greedy_mode == NS_GREEDY_LANES || b.M > 64 ||   // grouped kernel: M <= 64
+                     (b.greedy_mode == NS_GREEDY_AUTO && n_cp_launch * 4 < (long long)ctx->sm_count * 16));
     if (latency_mode) {
-        const int seg = 4 * dp;
+        const int seg = 32;   // one trajectory per warp, LPD = 32 / dp lanes per device
         const int mchunk = std::min(b.M, 256 / seg);
         const int nchunk = (b.M + mchunk - 1) / mchunk;
         const int threads = ((mchunk * seg + 31) / 32) * 32;
@@ -1849,11 +1853,12 @@ ns_status launch_greedy(ns_ctx* ctx, const SearchBufs& b, const ns_tables* t, lo
         a2.work = b.work + (size_t)g0 * b.M;
         const unsigned blocks = (unsigned)((g1 - g0) * nchunk);
         prof_begin(ctx, PK_GREEDY);
-        switch (seg) {
-            case 4: k_greedy_cta<4, 4><<<blocks, threads, 0, ctx->stream>>>(a2, mchunk, nchunk); break;
-            case 8: k_greedy_cta<8, 4><<<blocks, threads, 0, ctx->stream>>>(a2, mchunk, nchunk); break;
-            case 16: k_greedy_cta<16, 4><<<blocks, threads, 0, ctx->stream>>>(a2, mchunk, nchunk); break;
-            default: k_greedy_cta<32, 4><<<blocks, threads, 0, ctx->stream>>>(a2, mchunk, nchunk); break;
+        switch (dp) {
+            case 1: k_greedy_cta<32, 32><<<blocks, threads, 0, ctx->stream>>>(a2, mchunk, nchunk); break;
+            case 2: k_greedy_cta<32, 16><<<blocks, threads, 0, ctx->stream>>>(a2, mchunk, nchunk); break;
+            case 4: k_greedy_cta<32, 8><<<blocks, threads, 0, ctx->stream>>>(a2, mchunk, nchunk); break;
+            case 8: k_greedy_cta<32, 4><<<blocks, threads, 0, ctx->stream>>>(a2, mchunk, nchunk); break;
+            default: k_greedy_cta<32, 2><<<blocks, threads, 0, ctx->stream>>>(a2, mchunk, nchunk); break;
         }
         prof_end(ctx);
         NS_CUDA(ctx, cudaMemsetAsync(b.dup_of + tb, 0xff, (size_t)n * sizeof(int32_t), ctx->stream));

@@ -622,3 +622,21 @@ def test_batching_service(ns, ctx):
     for i, r in enumerate(cres):
         assert r["cost"] == cref["cost"][i]
         assert r["col_plan"] == cref["col_plan"][i, :int(cref["n_col"][i])].tolist()
+
+
+@pytest.mark.parametrize("D", [1, 2, 3, 4, 6, 8, 12, 16])
+def test_greedy_kernels_bit_identical(ns, ctx, D):
+    """The grouped greedy (throughput) and the per-lane greedy (latency) split
+    a device's 64 features over the same lanes and sum them in the same
+    order, so plan costs, assignments and score counts are bit-identical --
+    a task's result does not depend on the batch size that picks the kernel."""
+    w = gen_weights(D, "mono")
+    tasks = [gen_task("C2", i, T=12 + (i % 17), D=D) for i in range(96)]
+    tabs = _setup(ns, ctx, tasks, w)
+    g = ns.ns_shard_tablewise(ctx, tabs, D, M=11, greedy=1)
+    l = ns.ns_shard_tablewise(ctx, tabs, D, M=11, greedy=2)
+    np.testing.assert_array_equal(g["cost"], l["cost"])
+    np.testing.assert_array_equal(g["assign"], l["assign"])
+    np.testing.assert_array_equal(g["n_scores"], l["n_scores"])
+    np.testing.assert_array_equal(g["grid_index"], l["grid_index"])
+    tabs.free()
