@@ -330,8 +330,11 @@ def main():
         a.record(stream)
         for k in range(args.steps):
             step(pin_desc, hout)
-        b.record(stream)
+        # the last step's result copies run on the library's copy stream:
+        # close the timed region only after ns_synchronize has drained both
         ns.ns_synchronize(ctx)
+        b.record(stream)
+        torch.cuda.synchronize()
         barrier(world)
         e_total = allreduce_max(world, float(a.elapsed_time(b)))
         assert int(hout["n_scores"].sum()) == scores_per_step

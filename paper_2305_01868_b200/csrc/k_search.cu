@@ -2019,6 +2019,18 @@ ns_status deliver(ns_ctx* ctx, const ns_tables* t, const OutStage& o, int Lout, 
                   bool async) {
     const int n = t->n_tasks;
     cudaStream_t st = ctx->stream;
+    // NS_SEARCH_ASYNC with host outputs: the result copies go to the output
+    // stream once the search is done, so they overlap the caller's next batch
+    // (its search waits for them before rewriting the staging; run_search)
+    const bool host_out = (out->n_col && !o.d_ncol) || (out->col_plan && Lout > 0 && !o.d_plan) ||
+                          (out->assign && !o.d_assign) || (out->grid_index && !o.d_grid) ||
+                          (out->n_scores && !o.d_scores) || (out->cost && !o.d_cost);
+    if (async && host_out) {
+        NS_CUDA(ctx, ensure_copy_stream(ctx));
+        NS_CUDA(ctx, cudaEventRecord(ctx->out_ready, ctx->stream));
+        NS_CUDA(ctx, cudaStreamWaitEvent(ctx->out_stream, ctx->out_ready, 0));
+        st = ctx->out_stream;
+    }
     auto cp = [&](void* dst, const void* src, size_t bytes) -> cudaError_t {
         if (!dst) return cudaSuccess;
         return cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDefault, st);
@@ -2038,6 +2050,10 @@ ns_status deliver(ns_ctx* ctx, const ns_tables* t, const OutStage& o, int Lout, 
     if (!o.d_scores) NS_CUDA(ctx, cp(out->n_scores, o.scores, n * sizeof(uint64_t)));
     if (async) {   // NS_SEARCH_ASYNC: no wait; the validation flag is checked by ns_synchronize
         if (!o.d_cost) NS_CUDA(ctx, cp(out->cost, o.cost, n * sizeof(double)));
+        if (host_out) {
+            NS_CUDA(ctx, cudaEventRecord(ctx->out_done, ctx->out_stream));
+            ctx->out_pending = true;
+        }
         return record_async_flag(ctx, t->d_flag);
     }
     // costs always pass through pinned host memory: the status needs them

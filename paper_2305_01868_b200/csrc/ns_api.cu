@@ -47,9 +47,16 @@ bool is_pinned_host_ptr(const void* p) {
 }
 
 void* arena_get(ns_ctx* ctx, size_t bytes) {
+    // a previous async search's result copies (copy stream) still read the
+    // arena's output staging: work enqueued from here on waits for them
+    if (ctx->out_pending) {
+        cudaStreamWaitEvent(ctx->stream, ctx->out_done, 0);
+        ctx->out_pending = false;
+    }
     if (bytes <= ctx->arena_bytes) return ctx->arena;
     if (ctx->arena) {
         cudaStreamSynchronize(ctx->stream);
+        if (ctx->out_stream) cudaStreamSynchronize(ctx->out_stream);   // result copies read the arena
         cudaFree(ctx->arena);
         ctx->arena = nullptr;
         ctx->arena_bytes = 0;
@@ -101,7 +108,7 @@ void* pinned_in_get(ns_ctx* ctx, size_t bytes) {
 // Pinned host -> device copy that overlaps work already queued on the ctx
 // stream: H2D on the ctx's copy stream into staging buffer i (double
 // buffered), the ctx stream waits for it and copies D2D into dst.
-static cudaError_t stage_pinned_h2d(ns_ctx* ctx, void* dst, const void* host, size_t bytes) {
+cudaError_t ensure_copy_stream(ns_ctx* ctx) {
     cudaError_t e;
     if (!ctx->copy_stream) {
         if ((e = cudaStreamCreateWithFlags(&ctx->copy_stream, cudaStreamNonBlocking)) != cudaSuccess) return e;
@@ -109,7 +116,16 @@ static cudaError_t stage_pinned_h2d(ns_ctx* ctx, void* dst, const void* host, si
             if ((e = cudaEventCreateWithFlags(&ctx->dstage_ready[k], cudaEventDisableTiming)) != cudaSuccess) return e;
             if ((e = cudaEventCreateWithFlags(&ctx->dstage_free[k], cudaEventDisableTiming)) != cudaSuccess) return e;
         }
+        if ((e = cudaStreamCreateWithFlags(&ctx->out_stream, cudaStreamNonBlocking)) != cudaSuccess) return e;
+        if ((e = cudaEventCreateWithFlags(&ctx->out_ready, cudaEventDisableTiming)) != cudaSuccess) return e;
+        if ((e = cudaEventCreateWithFlags(&ctx->out_done, cudaEventDisableTiming)) != cudaSuccess) return e;
     }
+    return cudaSuccess;
+}
+
+static cudaError_t stage_pinned_h2d(ns_ctx* ctx, void* dst, const void* host, size_t bytes) {
+    cudaError_t e;
+    if ((e = ensure_copy_stream(ctx)) != cudaSuccess) return e;
     const int i = ctx->dstage_i;
     ctx->dstage_i ^= 1;
     if (ctx->dstage_bytes[i] < bytes) {
@@ -258,6 +274,7 @@ ns_status ns_destroy(ns_ctx* ctx) {
     if (!ctx) return NS_ERR_ARG;
     cudaSetDevice(ctx->device);
     cudaStreamSynchronize(ctx->stream);
+    if (ctx->out_stream) cudaStreamSynchronize(ctx->out_stream);   // result copies read the arena
     while (!ctx->tables.empty()) ns_tables_free(*ctx->tables.begin());
     cudaStreamSynchronize(ctx->stream);
     free_model(ctx->model);
@@ -274,6 +291,11 @@ ns_status ns_destroy(ns_ctx* ctx) {
         if (ctx->dstage[k]) cudaFree(ctx->dstage[k]);
         if (ctx->dstage_ready[k]) cudaEventDestroy(ctx->dstage_ready[k]);
         if (ctx->dstage_free[k]) cudaEventDestroy(ctx->dstage_free[k]);
+    }
+    {
+        if (ctx->out_stream) cudaStreamDestroy(ctx->out_stream);
+        if (ctx->out_ready) cudaEventDestroy(ctx->out_ready);
+        if (ctx->out_done) cudaEventDestroy(ctx->out_done);
     }
     if (ctx->h_async_flags) cudaFreeHost(ctx->h_async_flags);
     prof_collect(ctx);
@@ -295,6 +317,8 @@ ns_status ns_synchronize(ns_ctx* ctx) {
     if (!ctx) return NS_ERR_ARG;
     cudaSetDevice(ctx->device);
     NS_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+    if (ctx->out_stream) NS_CUDA(ctx, cudaStreamSynchronize(ctx->out_stream));   // result copies
+    ctx->out_pending = false;
     prof_collect(ctx);
     return check_async_flags(ctx);
 }

@@ -98,6 +98,13 @@ struct ns_ctx {
     cudaEvent_t dstage_ready[2] = {nullptr, nullptr};
     cudaEvent_t dstage_free[2] = {nullptr, nullptr};
     int dstage_i = 0;
+    // NS_SEARCH_ASYNC with host outputs: the result copies run on the copy
+    // stream after out_ready (search done) and record out_done; the next
+    // search waits for out_done before its kernels rewrite the staging
+    cudaStream_t out_stream = nullptr;   // device -> host result copies (separate from the H2D copies)
+    cudaEvent_t out_ready = nullptr;
+    cudaEvent_t out_done = nullptr;
+    bool out_pending = false;
     // kernel timers
     bool prof = false;
     uint32_t prof_mask = 0;   // kernel classes timed (bit k = class k)
@@ -189,6 +196,7 @@ void* arena_get(ns_ctx* ctx, size_t bytes);   // nullptr on failure
 void* pinned_get(ns_ctx* ctx, size_t bytes);
 void* pinned_in_get(ns_ctx* ctx, size_t bytes);      // waits only for the previous input copy
 void pinned_in_release(ns_ctx* ctx);                  // record: copies out of it are enqueued
+cudaError_t ensure_copy_stream(ns_ctx* ctx);          // lazily created copy stream + its events
 CommParams comm_params(const ns_ctx* ctx);
 ns_status comm_allgather(ns_ctx* ctx, const void* send, void* recv, size_t bytes_per_rank);
 ns_status comm_allreduce_min_u64(ns_ctx* ctx, uint64_t* dev_buf, size_t count);
