@@ -193,9 +193,12 @@ ns_status ns_score_plans(ns_ctx* ctx, const ns_tables* tables, int32_t task, int
                                  life-long cache, as data parallelism) */
 #define NS_GREEDY_LANES 2u    /* every trajectory in its own lane segment (latency mode) */
 /* May be OR-ed with the greedy selector: enqueue the search on the ctx stream
- * and return without waiting (NS_OK unless an argument/launch error).  The
- * outputs land in stream order; the caller synchronises (ns_synchronize, or
- * any later stream sync) before reading them.  Infeasible tasks are visible
+ * and return without waiting (NS_OK unless an argument/launch error).  Device
+ * outputs land in ctx-stream order; host outputs are copied by a library
+ * output stream once the search is done (overlapping the caller's next
+ * batch), so read them after ns_synchronize (or a device-wide sync).  The
+ * next call that reuses the library's staging waits for those copies on the
+ * device, never on the host.  Infeasible tasks are visible
  * as +inf costs (there is no NS_INFEASIBLE status); a descriptor-validation
  * error of device-resident featurise input is returned by the next
  * ns_synchronize.  Output pointers should be device or pinned host memory
