@@ -98,9 +98,9 @@ struct ns_ctx {
     cudaEvent_t dstage_ready[2] = {nullptr, nullptr};
     cudaEvent_t dstage_free[2] = {nullptr, nullptr};
     int dstage_i = 0;
-    // NS_SEARCH_ASYNC with host outputs: the result copies run on the copy
-    // stream after out_ready (search done) and record out_done; the next
-    // search waits for out_done before its kernels rewrite the staging
+    // NS_SEARCH_ASYNC with host outputs: the result copies run on out_stream
+    // after out_ready (search done) and record out_done; the next search
+    // waits for out_done before its kernels rewrite the staging
     cudaStream_t out_stream = nullptr;   // device -> host result copies (separate from the H2D copies)
     cudaEvent_t out_ready = nullptr;
     cudaEvent_t out_done = nullptr;
