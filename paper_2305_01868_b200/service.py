@@ -45,7 +45,9 @@ class ShardingService:
         self.device, self.max_batch, self.max_wait = device, max_batch, max_wait_ms * 1e-3
         self.batches = 0
         self.tasks = 0
-        self._q: "queue.Queue[Optional[Tuple[Any, Future]]]" = queue.Queue()
+        # SimpleQueue: C-implemented, one lock per put/get (submitters and the
+        # worker share the GIL; queue.Queue's Condition bookkeeping costs more)
+        self._q: "queue.SimpleQueue[Optional[Tuple[Any, Future]]]" = queue.SimpleQueue()
         self._ready = threading.Event()
         self._err: Optional[BaseException] = None
         self._worker = threading.Thread(target=self._run, args=(weights,), daemon=True)
@@ -141,13 +143,20 @@ class ShardingService:
             return
         self.batches += 1
         self.tasks += len(batch)
+        # one conversion per output array, then per-task views / list items
+        # (the per-task host work is what bounds the service: DESIGN.md §14)
+        cost = out["cost"].tolist()
+        gidx = out["grid_index"].tolist()
+        nsc = out["n_scores"].tolist()
+        assign = np.array(out["assign"], dtype=np.int8)
+        ncol = out["n_col"].tolist() if out.get("n_col") is not None else None
+        colp = np.array(out["col_plan"]) if ncol is not None else None
         for i, (t, f) in enumerate(batch):
-            ncol = int(out["n_col"][i]) if out.get("n_col") is not None else 0
-            col = [int(c) for c in out["col_plan"][i, :ncol]] if ncol else []
+            nc = ncol[i] if ncol is not None else 0
             f.set_result({
-                "cost": float(out["cost"][i]),
-                "assign": np.array(out["assign"][i, :t.T + ncol], dtype=np.int8),
-                "col_plan": col,
-                "grid_index": int(out["grid_index"][i]),
-                "n_scores": int(out["n_scores"][i]),
+                "cost": cost[i],
+                "assign": assign[i, :t.T + nc],
+                "col_plan": colp[i, :nc].tolist() if nc else [],
+                "grid_index": gidx[i],
+                "n_scores": nsc[i],
             })
