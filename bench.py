@@ -449,7 +449,11 @@ def service_rate(ns):
     """the batching front end (paper_2305_01868_b200.service)
     fed by 8 submitter threads with 16384 host-side C2 tasks; wall time from
     the first submit to the last result (host packing, featurise, search and
-    per-task result split included)."""
+    per-task result split included).  The bench's own long-lived objects
+    (the 65536-task batches) are frozen out of the cyclic GC first, as a
+    serving process would do after start-up: otherwise every gen-2
+    collection triggered by the service's per-task futures walks them."""
+    import gc
     import threading
     from paper_2305_01868_b200.service import ShardingService
     c = CONFIGS[CFG]
@@ -457,6 +461,8 @@ def service_rate(ns):
     tasks = gen_tasks(CFG, 16384, start=1 << 20)
     with ShardingService(w, c["D"], M=c["M"], max_batch=8192, max_wait_ms=5.0) as svc:
         svc.shard(tasks[:256])   # warm-up
+        gc.collect()
+        gc.freeze()
         b0, t0n = svc.batches, svc.tasks
         res = [None] * len(tasks)
 
@@ -472,6 +478,7 @@ def service_rate(ns):
         for t in th:
             t.join()
         dt = time.perf_counter() - t0
+        gc.unfreeze()
         batches = svc.batches - b0
     scores = sum(r["n_scores"] for r in res)
     return {"tasks": len(tasks), "submitters": 8, "batches": batches, "tasks_per_s": len(tasks) / dt,
