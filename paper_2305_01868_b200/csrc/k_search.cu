@@ -690,6 +690,9 @@ constexpr int kStages = 8;   // row-stream ring depth (large-D greedy)
 #ifndef NS_DSTAGES
 #define NS_DSTAGES 3
 #endif
+#ifndef NS_REDUX_ARGMIN
+#define NS_REDUX_ARGMIN 1   // grouped greedy fast path: device argmin by two 32-bit warp reductions of an order key
+#endif
 #ifndef NS_PAIR_STAGE
 #define NS_PAIR_STAGE 2   // tables staged per cp.async group in the grouped greedy (0: one per step)
 #endif
@@ -941,6 +944,23 @@ __global__ void __launch_bounds__(NS_DEDUP_WPB * 32, (LPD >= 8 ? NS_DEDUP_BLOCKS
                 if (__all_sync(kFull, !f || dsum + dt <= gmin_gr)) {
                     // device argmin: butterfly minimum, then the lowest device
                     // attaining it (R13) from one ballot
+#if NS_REDUX_ARGMIN
+                    // order key of the score (unsigned compare == double
+                    // compare for non-NaN values; + 0.0 folds -0.0 into +0.0
+                    // so equal scores keep equal keys); infeasible = all ones.
+                    // min over the warp = high-word min, then low-word min
+                    // among the lanes holding it (two REDUX, no 64-bit shuffles)
+                    const long long sb = __double_as_longlong(sco + 0.0);
+                    const unsigned long long key =
+                        f ? (unsigned long long)(sb ^ ((sb >> 63) | (long long)0x8000000000000000ULL)) : ~0ULL;
+                    const unsigned khi = (unsigned)(key >> 32), klo = (unsigned)key;
+                    const unsigned mhi = __reduce_min_sync(kFull, khi);
+                    const unsigned mlo = __reduce_min_sync(kFull, khi == mhi ? klo : 0xFFFFFFFFu);
+                    const unsigned nf = __popc(__ballot_sync(kFull, f && part == 0));
+                    const unsigned hit = __ballot_sync(kFull, f && part == 0 && khi == mhi && klo == mlo);
+                    const int bd = (__ffs(hit) - 1) / LPD;
+                    if (hit == 0u) {   // nothing feasible: the whole group strands (R9)
+#else
                     const double own = f ? sco : CUDART_INF;
                     double bs = own;
 #pragma unroll
@@ -953,6 +973,7 @@ __global__ void __launch_bounds__(NS_DEDUP_WPB * 32, (LPD >= 8 ? NS_DEDUP_BLOCKS
                     const unsigned hit = __ballot_sync(kFull, f && part == 0 && own == bs);
                     const int bd = (__ffs(hit) - 1) / LPD;
                     if (bs == CUDART_INF) {   // nothing feasible: the whole group strands (R9)
+#endif
                         const uint32_t gwk = G0 ? r_gwork : s.gwork[gr];
 #pragma unroll
                         for (int m0 = 0; m0 < MC; m0 += 32) {
