@@ -567,6 +567,9 @@ __device__ __forceinline__ void load_lane_head(const HeadParams& hp, int part, d
 // there (broadcast within a segment; the LPD slices of a row are padded
 // 16 B apart so they fall on different banks) instead of each warp walking
 // the order and the rows through L1/L2.
+#ifndef NS_REDUX_ARGMIN
+#define NS_REDUX_ARGMIN 1   // greedy kernels (grouped fast path, per-warp latency kernel): device argmin by two 32-bit warp reductions of an order key
+#endif
 constexpr int kRing = 40;   // tables staged per chunk (C2: the whole task)
 
 template <int SEG, int LPD>
@@ -635,10 +638,24 @@ __global__ void __launch_bounds__(256) k_greedy_cta(const GreedyArgs a, int mchu
             double ps = 0.0;
             if (f) ps = part_score<FPL, true>(u, w, v2);
             double bs = a.head.hb2 + lane_group_sum<LPD>(ps);
-            if (!f) bs = CUDART_INF;
             int bd = d;
+            if constexpr (SEG == 32 && NS_REDUX_ARGMIN) {
+                // one trajectory per warp: the grouped kernel's order-key
+                // argmin (two REDUX; lowest device among equal scores)
+                const long long sb = __double_as_longlong(bs + 0.0);
+                const unsigned long long key =
+                    f ? (unsigned long long)(sb ^ ((sb >> 63) | (long long)0x8000000000000000ULL)) : ~0ULL;
+                const unsigned khi = (unsigned)(key >> 32), klo = (unsigned)key;
+                const unsigned mhi = __reduce_min_sync(kFull, khi);
+                const unsigned mlo = __reduce_min_sync(kFull, khi == mhi ? klo : 0xFFFFFFFFu);
+                const unsigned hit = __ballot_sync(kFull, f && part == 0 && khi == mhi && klo == mlo);
+                if (hit == 0u) bs = CUDART_INF;
+                bd = (__ffs(hit) - 1) / LPD;
+            } else {
+                if (!f) bs = CUDART_INF;
 #pragma unroll
-            for (int o = SEG / 2; o >= LPD; o >>= 1) argmin_step(bs, bd, o);
+                for (int o = SEG / 2; o >= LPD; o >>= 1) argmin_step(bs, bd, o);
+            }
             const unsigned bal = __ballot_sync(kFull, f && part == 0);
             if (act) {
                 work += __popc((bal >> (seg * SEG)) & SEGMASK);
@@ -689,9 +706,6 @@ __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_gr
 constexpr int kStages = 8;   // row-stream ring depth (large-D greedy)
 #ifndef NS_DSTAGES
 #define NS_DSTAGES 3
-#endif
-#ifndef NS_REDUX_ARGMIN
-#define NS_REDUX_ARGMIN 1   // grouped greedy fast path: device argmin by two 32-bit warp reductions of an order key
 #endif
 #ifndef NS_PAIR_STAGE
 #define NS_PAIR_STAGE 2   // tables staged per cp.async group in the grouped greedy (0: one per step)
