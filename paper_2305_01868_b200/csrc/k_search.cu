@@ -1352,7 +1352,11 @@ __global__ void __launch_bounds__(128 * TPD, TPD >= 4 ? 1 : (TPD == 2 ? 2 : 3)) 
     __shared__ __align__(16) double s_w[TPD][SS];
     __shared__ __align__(16) double s_hb1[kV];
     __shared__ __align__(16) double ring[kRingW][TPD * SS];
+#if NS_REDUX_ARGMIN
+    __shared__ unsigned long long s_key[2][NWM];
+#else
     __shared__ double s_sc[2][NWM];
+#endif
     __shared__ int s_dv[2][NWM];
     __shared__ int s_cnt[2][NWM];
     __shared__ int4 smeta[kRingW];    // {dim, list index, bytes lo, bytes hi}
@@ -1430,6 +1434,34 @@ __global__ void __launch_bounds__(128 * TPD, TPD >= 4 ? 1 : (TPD == 2 ? 2 : 3)) 
             ps = (acc[0] + acc[1]) + (acc[2] + acc[3]);
         }
         const double sco = a.head.hb2 + lane_group_sum<TPD>(ps);
+#if NS_REDUX_ARGMIN
+        // order keys (see k_greedy_dedup): warp minimum by two REDUX, the
+        // lowest device holding it from one ballot; then lane k takes warp
+        // k's key and the same two REDUX + ballot give the CTA's lowest
+        // (score, device) -- warps hold increasing device ranges
+        const long long sb = __double_as_longlong(sco + 0.0);
+        unsigned long long key = f ? (unsigned long long)(sb ^ ((sb >> 63) | (long long)0x8000000000000000ULL)) : ~0ULL;
+        unsigned khi = (unsigned)(key >> 32), klo = (unsigned)key;
+        unsigned mhi = __reduce_min_sync(kFull, khi);
+        unsigned mlo = __reduce_min_sync(kFull, khi == mhi ? klo : 0xFFFFFFFFu);
+        unsigned hit = __ballot_sync(kFull, f && part == 0 && khi == mhi && klo == mlo);
+        const unsigned bal = __ballot_sync(kFull, f && part == 0);
+        if (lane == 0) {
+            s_key[par][wi] = ((unsigned long long)mhi << 32) | mlo;
+            s_dv[par][wi] = wi * (32 / TPD) + (hit ? (__ffs(hit) - 1) / TPD : 0);
+            s_cnt[par][wi] = __popc(bal);
+        }
+        __syncthreads();
+        key = lane < nw ? s_key[par][lane] : ~0ULL;
+        khi = (unsigned)(key >> 32);
+        klo = (unsigned)key;
+        mhi = __reduce_min_sync(kFull, khi);
+        mlo = __reduce_min_sync(kFull, khi == mhi ? klo : 0xFFFFFFFFu);
+        hit = __ballot_sync(kFull, lane < nw && khi == mhi && klo == mlo);
+        const int cnt = __reduce_add_sync(kFull, lane < nw ? s_cnt[par][lane] : 0);
+        const double bs = (mhi & mlo) == 0xFFFFFFFFu ? CUDART_INF : 0.0;   // INF: nothing feasible
+        const int bd = s_dv[par][hit ? __ffs(hit) - 1 : 0];
+#else
         double bs = f ? sco : CUDART_INF;
         int bd = d;
 #pragma unroll
@@ -1448,6 +1480,7 @@ __global__ void __launch_bounds__(128 * TPD, TPD >= 4 ? 1 : (TPD == 2 ? 2 : 3)) 
         const int cnt = __reduce_add_sync(kFull, lane < nw ? s_cnt[par][lane] : 0);
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) argmin_step(bs, bd, o);
+#endif
         work += cnt;
         if (bs == CUDART_INF) {
             alive = false;
