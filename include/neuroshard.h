@@ -118,8 +118,9 @@ ns_status ns_load_cost_models(ns_ctx* ctx, const ns_compute_model* compute,
 
 /* ------------------------------------------------------------------ tables */
 /* One embedding table (P:111 factors; reading R1): dimension (columns,
- * % 4 == 0), hash size (rows), mean pooling factor, indices-distribution
- * skew scalar. */
+ * % 4 == 0, P:237, and 4 <= dim <= 128, the paper's maximum table dim P:368:
+ * every dim reachable by halving then fits the library's 6 cached variants),
+ * hash size (rows), mean pooling factor, indices-distribution skew scalar. */
 typedef struct {
     int32_t dim;
     int32_t reserved;     /* must be 0 */

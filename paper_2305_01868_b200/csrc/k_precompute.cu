@@ -35,7 +35,7 @@ __global__ void __launch_bounds__(256) k_tables_validate(const ns_table_desc* de
         const int e = off[q + 1];
         for (int g = off[q] + lane; g < e; g += 32) {
             const ns_table_desc d = desc[g];
-            bad |= (d.dim < 4 || d.dim % 4 != 0 || d.dim > (1 << 20) || d.hash_size < 1 || !(d.pooling_factor > 0) ||
+            bad |= (d.dim < 4 || d.dim % 4 != 0 || d.dim > kMaxDim || d.hash_size < 1 || !(d.pooling_factor > 0) ||
                     !(d.skew >= 0) || d.reserved != 0);
             sum += d.dim;
         }

@@ -248,7 +248,7 @@ __global__ void k_expand(SearchBufs b, TaskView tv, int level) {
         }
         int m = 0;
         for (int k = 0; k < n; ++k)
-            if (tv.vdim[rows[cand[k]]] % 8 == 0) cand[m++] = cand[k];
+            if (tv.vdim[rows[cand[k]]] % 8 == 0 && rows[cand[k]] % kDepth < kDepth - 1) cand[m++] = cand[k];
         ncand = m;
     }
     __syncthreads();

@@ -468,11 +468,11 @@ ns_status ns_featurize_tables(ns_ctx* ctx, const ns_table_desc* tables, const in
         t->dims.resize(n);
         for (int g = 0; g < n; ++g) {
             const ns_table_desc& d = tables[g];
-            if (d.dim < 4 || d.dim % 4 != 0 || d.dim > (1 << 20) || d.hash_size < 1 || !(d.pooling_factor > 0) ||
+            if (d.dim < 4 || d.dim % 4 != 0 || d.dim > kMaxDim || d.hash_size < 1 || !(d.pooling_factor > 0) ||
                 !(d.skew >= 0) || d.reserved != 0) {
                 delete t;
                 return set_err(ctx, NS_ERR_ARG, "invalid table descriptor " + std::to_string(g) +
-                                                    " (need dim%4==0, dim>=4, hash>=1, pooling>0, skew>=0)");
+                                                    " (need dim%4==0, 4<=dim<=128, hash>=1, pooling>0, skew>=0)");
             }
             t->dims[g] = d.dim;
         }
@@ -679,12 +679,15 @@ ns_status ns_score_plans(ns_ctx* ctx, const ns_tables* t, int32_t task, int32_t 
     }
     std::vector<int32_t> dims;
     if (n_col > 0) dims.assign(t->dims.begin() + t->off[task], t->dims.begin() + t->off[task + 1]);
+    std::vector<int> depth(dims.size(), 0);   // variant row depth of each list entry (< kDepth)
     for (int i = 0; i < n_col; ++i) {
         int c = col_plan[i];
-        if (c < 0 || c >= (int)dims.size() || dims[c] % 8 != 0)
+        if (c < 0 || c >= (int)dims.size() || dims[c] % 8 != 0 || depth[c] >= kDepth - 1)
             return set_err(ctx, NS_ERR_ARG, "col_plan step " + std::to_string(i) + " is not a legal split");
         dims[c] /= 2;
         dims.push_back(dims[c]);
+        depth[c] += 1;
+        depth.push_back(depth[c]);
     }
     cudaSetDevice(ctx->device);
     if (n_col > 0 && !t->deep_done) {

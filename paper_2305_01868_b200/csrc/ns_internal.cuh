@@ -18,6 +18,10 @@ constexpr int kH = 128;      // encoder hidden width  ("128-32")
 constexpr int kE = 32;       // table representation width
 constexpr int kV = 64;       // head hidden width     ("32-64")
 constexpr int kDepth = 6;    // variant slots per table: dim, dim/2, ..., dim/32 (128 -> 4)
+// Largest accepted table dim: a split needs dim % 8 == 0 and leaves dim/2, so a
+// table of dim <= 4 << (kDepth - 1) = 128 (the paper's maximum) never
+// needs more than kDepth variant rows; larger dims are rejected at validation.
+constexpr int kMaxDim = 4 << (kDepth - 1);
 constexpr int kMaxD = 128;   // int8 device ids
 constexpr int kCommW[6] = {0, 128, 64, 32, 16, 0};   // comm widths "128-64-32-16"
 

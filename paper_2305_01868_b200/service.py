@@ -50,6 +50,10 @@ class ShardingService:
         self._q: "queue.SimpleQueue[Optional[Tuple[Any, Future]]]" = queue.SimpleQueue()
         self._ready = threading.Event()
         self._err: Optional[BaseException] = None
+        # submit/close/worker-exit serialise on this lock: once _closed is set
+        # no task can be queued behind the stop sentinel or after the drain
+        self._lock = threading.Lock()
+        self._closed = False
         self._worker = threading.Thread(target=self._run, args=(weights,), daemon=True)
         self._worker.start()
         self._ready.wait()
@@ -60,10 +64,11 @@ class ShardingService:
     def submit(self, task) -> Future:
         """Queue one task (fields dims, hash, pooling, skew, cap, T); returns
         a Future resolving to the task's plan dict."""
-        if not self._worker.is_alive():
-            raise RuntimeError("ShardingService is closed")
         f: Future = Future()
-        self._q.put((task, f))
+        with self._lock:
+            if self._closed:
+                raise RuntimeError("ShardingService is closed")
+            self._q.put((task, f))
         return f
 
     def shard(self, tasks: List) -> List[dict]:
@@ -72,9 +77,11 @@ class ShardingService:
         return [f.result() for f in fs]
 
     def close(self) -> None:
-        if self._worker.is_alive():
-            self._q.put(None)
-            self._worker.join()
+        with self._lock:
+            if not self._closed:
+                self._closed = True
+                self._q.put(None)
+        self._worker.join()
 
     def __enter__(self):
         return self
@@ -89,6 +96,8 @@ class ShardingService:
             ns.ns_load_cost_models(ctx, weights)
         except BaseException as e:   # pragma: no cover - reported to the constructor
             self._err = e
+            with self._lock:
+                self._closed = True
             self._ready.set()
             return
         self._ready.set()
@@ -114,6 +123,9 @@ class ShardingService:
                     batch.append(nxt)
                 self._search(ctx, batch)
         finally:
+            # no submit can pass the lock after this, so the drain below is final
+            with self._lock:
+                self._closed = True
             # fail whatever is still queued, then release the ctx
             while True:
                 try:

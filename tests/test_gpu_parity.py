@@ -486,6 +486,37 @@ def test_invalid_descriptor_device_and_pinned(ns, ctx):
         tabs.free()
 
 
+def test_dim_above_128_rejected(ns, ctx):
+    """the library caches kDepth = 6 variants per table
+    (dim ... dim/32), enough for every split chain of a dim <= 128 table (the
+    paper's maximum).  A dim-256 table would need a 7th variant, so it
+    is rejected at featurise (pageable: immediately; device: at the next
+    synchronising call) instead of letting a 6th split read the next table's
+    rows."""
+    import torch
+    w = gen_weights(4, "mono")
+    ns.ns_load_cost_models(ctx, w)
+    tasks = gen_tasks("C2", 2)
+    desc, off, caps = ns.table_descs(tasks)
+    desc["dim"][3] = 256
+    with pytest.raises(ns.NSError):
+        ns.ns_featurize_tables(ctx, desc, off, caps)
+    tabs = ns.ns_featurize_tables(ctx, torch.from_numpy(desc.view(np.uint8)).cuda(), off, caps)
+    with pytest.raises(ns.NSError):
+        ns.ns_shard_columnwise(ctx, tabs, 4, N=4, K=2, L=6, M=3)
+    tabs.free()
+    # dim 128 splits five times (128 -> 4) and no further: a 6-split column
+    # plan of one table is illegal for ns_score_plans
+    desc["dim"][3] = 128
+    tabs = ns.ns_featurize_tables(ctx, desc, off, caps)
+    T0 = int(off[1])
+    A = np.zeros((4, T0 + 5), np.int8)
+    ns.ns_score_plans(ctx, tabs, 0, 4, [3, 3, 3, 3, 3], A)
+    with pytest.raises(ns.NSError):
+        ns.ns_score_plans(ctx, tabs, 0, 4, [3, 3, 3, 3, 3, 3], np.zeros((4, T0 + 6), np.int8))
+    tabs.free()
+
+
 @pytest.mark.parametrize("D", [2, 4, 8, 16])
 def test_score_plans_tf32x3_tcgen05(ns, ctx, D):
     """Bulk mode: comm MLPs on tcgen05 in split-TF32 x3 (FP32 accumulation).

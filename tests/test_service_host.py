@@ -132,3 +132,36 @@ def test_closed_service_rejects_submits(fake):
     svc.close()
     with pytest.raises(RuntimeError, match="closed"):
         svc.submit(_tasks(1)[0])
+
+
+def test_submit_racing_close_never_strands_a_future(fake):
+    # a submit landing between the liveness check and the
+    # queue put, or after the worker's final drain, must not leave a Future
+    # that never resolves.  Every accepted submit resolves (result or
+    # "closed" error); every rejected one raises at submit.
+    tasks = _tasks(8)
+    for rep in range(20):
+        svc = S.ShardingService(None, 4, max_batch=4, max_wait_ms=0.5)
+        accepted, stop = [], threading.Event()
+
+        def sub():
+            k = 0
+            while not stop.is_set():
+                try:
+                    accepted.append(svc.submit(tasks[k % len(tasks)]))
+                except RuntimeError:
+                    return
+                k += 1
+
+        th = [threading.Thread(target=sub) for _ in range(3)]
+        for t in th:
+            t.start()
+        svc.close()
+        stop.set()
+        for t in th:
+            t.join()
+        for f in accepted:
+            try:
+                f.result(timeout=10)
+            except RuntimeError as e:
+                assert "closed" in str(e)
