@@ -244,7 +244,8 @@ class BeamResult:
 
 
 def beam_search(weights, emb, task, N: int, K: int, L: int, M: int, hi: float = 1.5,
-                cache=None, log: Optional[DecisionLog] = None) -> BeamResult:
+                cache=None, log: Optional[DecisionLog] = None,
+                trace: Optional[list] = None) -> BeamResult:
     """O9 = Alg. 1 BeamSearch.
 
     The empty column plan is evaluated first and is the initial global best
@@ -255,16 +256,21 @@ def beam_search(weights, emb, task, N: int, K: int, L: int, M: int, hi: float = 
     beam is the K lowest (cost, generation index) plans of the level (line 20;
     generation index = (beam rank, candidate rank), reading R13), infeasible
     plans having cost +inf (reading R16); duplicates are kept (reading R17).
+    ``trace`` (optional list) receives one record per level: the candidates
+    of every beam plan, the children as (cost, generation index, column
+    plan) in evaluation order, and the next beam -- introspection only.
     """
     r0 = greedy_grid_search(weights, emb, task, [], M, hi, cache, log)
     best = BeamResult(r0.cost, [], r0.assign, r0.grid_index, r0.work, 1, [])
     beam: List[List[int]] = [[]]
     for _level in range(L):
         children = []
+        cands = []
         for b, cp in enumerate(beam):
             tables = apply_col_plan(task, cp)
             singles = single_costs(weights, emb, tables, cache)
-            for j, t in enumerate(beam_candidates(task, tables, singles, N)):
+            cands.append(beam_candidates(task, tables, singles, N))
+            for j, t in enumerate(cands[-1]):
                 col = cp + [t]
                 r = greedy_grid_search(weights, emb, task, col, M, hi, cache, log)
                 best.work += r.work
@@ -275,11 +281,15 @@ def beam_search(weights, emb, task, N: int, K: int, L: int, M: int, hi: float = 
                         log.record("global", r.cost, best.cost)
                     best.cost, best.col_plan = r.cost, col
                     best.assign, best.grid_index = r.assign, r.grid_index
+        evaluated = list(children)
         children.sort(key=lambda x: (x[0], x[1]))
         if log is not None and len(children) > K:
             log.record("topk", children[K - 1][0], children[K][0])
         best.level_best.append(children[0][0] if children else INF)
         beam = [col for _, _, col in children[:K]]
+        if trace is not None:
+            trace.append({"candidates": cands, "children": evaluated, "beam": [list(c) for c in beam],
+                          "global_best": (best.cost, list(best.col_plan))})
         if not beam:
             break
     return best

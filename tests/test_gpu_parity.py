@@ -98,6 +98,26 @@ def test_hand_example(ns, ctx, golden_hand):
 
 
 @pytest.mark.parametrize("greedy", GREEDY)
+def test_beam_example(ns, ctx, greedy):
+    """The hand-derived beam example (tests/golden/beam_example.json: split
+    appended at the end P:237, candidate order P:270, top-K by (cost,
+    generation) with +inf children, strict-< global best P:275-281) through
+    the CUDA path."""
+    from conftest import load_golden
+    g = load_golden("beam_example.json")
+    w, task = hand_weights(g), hand_task(g)
+    tabs = _setup(ns, ctx, [task], w)
+    out = ns.ns_shard_columnwise(ctx, tabs, g["D"], N=g["N"], K=g["K"], L=g["L"], M=g["M"], greedy=greedy)
+    e = g["expected"]
+    nc = int(out["n_col"][0])
+    assert out["cost"][0] == e["cost"]
+    assert out["col_plan"][0, :nc].tolist() == e["col_plan"]
+    assert out["assign"][0, :task.T + nc].tolist() == e["assign"]
+    assert out["grid_index"][0] == e["grid_index"]
+    assert int(out["n_scores"][0]) == e["work"]
+
+
+@pytest.mark.parametrize("greedy", GREEDY)
 @pytest.mark.parametrize("kind", ["mono", "signed"])
 def test_tablewise_C1(ns, ctx, kind, greedy):
     w = gen_weights(2, kind)

@@ -200,3 +200,59 @@ def test_determinism():
     a = osr.beam_search(w, emb, task, N=4, K=2, L=2, M=5)
     b = osr.beam_search(w, emb, task, N=4, K=2, L=2, M=5)
     assert (a.cost, a.col_plan, a.assign, a.work) == (b.cost, b.col_plan, b.assign, b.work)
+
+
+# ------------------------------------------- worked beam example (hand-derived)
+def _f(x):
+    return math.inf if x == "inf" else float(x)
+
+
+@pytest.fixture
+def golden_beam():
+    from conftest import load_golden
+    return load_golden("beam_example.json")
+
+
+def test_beam_example_split_appends_to_end(golden_beam):
+    # the second half goes to the END of the table list
+    g = golden_beam
+    task = hand_task(g)
+    for c, lst in g["expected"]["split_lists"].items():
+        assert osr.apply_col_plan(task, eval(c)) == [tuple(e) for e in lst], c
+
+
+def test_beam_example_candidates(golden_beam):
+    # Alg. 1 line 8: costly list first, then the largest not yet listed
+    g = golden_beam
+    w, task = hand_weights(g), hand_task(g)
+    emb = om.TableEmbeddings(w, task)
+    for c, exp in g["expected"]["candidates"].items():
+        tables = osr.apply_col_plan(task, eval(c))
+        singles = osr.single_costs(w, emb, tables)
+        assert osr.beam_candidates(task, tables, singles, g["N"]) == exp, c
+    assert osr.single_costs(w, emb, osr.apply_col_plan(task, [])) == g["expected"]["single_costs"]
+
+
+def test_beam_example_levels_and_result(golden_beam):
+    # Alg. 1 lines 13-20: generation order, top-K by
+    # (cost, generation) with +inf children, strict-< global best
+    g = golden_beam
+    w, task = hand_weights(g), hand_task(g)
+    emb = om.TableEmbeddings(w, task)
+    e = g["expected"]
+    trace = []
+    r = osr.beam_search(w, emb, task, N=g["N"], K=g["K"], L=g["L"], M=g["M"], trace=trace)
+    assert len(trace) == g["L"]
+    for lvl, exp in enumerate(e["level_children"]):
+        got = [(c, col) for c, _, col in trace[lvl]["children"]]
+        assert got == [(_f(c), col) for c, col in exp], lvl
+        assert trace[lvl]["beam"] == e["beams"][lvl], lvl
+    assert r.cost == e["cost"]
+    assert r.col_plan == e["col_plan"]
+    assert r.assign == e["assign"]
+    assert r.grid_index == e["grid_index"]
+    assert r.work == e["work"]
+    assert r.n_plans == e["n_plans"]
+    assert r.level_best == [_f(x) for x in e["level_best"]]
+    for c, a in e["children_assign"].items():
+        assert osr.greedy_grid_search(w, emb, task, eval(c), g["M"]).assign == a, c
