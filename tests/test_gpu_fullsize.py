@@ -1,0 +1,154 @@
+"""GPU oracle identity on the full-size search paths (VERDICT r1 "next
+round" 1(b)): the decisions of the CUDA path against the fp64 oracle's on the
+long-list order / candidate kernels (T' > 256), the wide greedy (D = 128),
+full-depth beams (C3 K = 10 L = 10, C4 L = 10 M = 51) and ragged batches that
+mix one long task into short ones (the list-length switch is batch-wide).
+
+Expected values for the minutes-long cases come from
+tests/golden/oracle_full.json, written by tools/make_oracle_fixtures.py (which
+calls only oracle/); the short cases run the oracle here.  Tolerance: fp64 on
+both sides -> costs within 1e-12 relative and identical integers, unless the
+oracle's decision log has a margin below 1e-12, in which case the returned
+plan is certified instead (tests/certify.py)."""
+import math
+
+import numpy as np
+import pytest
+
+from certify import certify_plan
+from conftest import load_golden, small_task
+from oracle import model as om, search as osr
+from workload.synth import CONFIGS, gen_task, gen_tasks, gen_weights
+
+pytestmark = pytest.mark.gpu
+
+RTOL = 1e-12
+FIX = load_golden("oracle_full.json")["cases"]
+
+
+@pytest.fixture(scope="module")
+def ns():
+    import torch
+    assert torch.cuda.is_available()
+    import paper_2305_01868_b200 as ns
+    return ns
+
+
+@pytest.fixture(scope="module")
+def ctx(ns):
+    c = ns.ns_create(0)
+    yield c
+    ns.ns_destroy(c)
+
+
+def _f(x):
+    return math.inf if x == "inf" else float(x)
+
+
+def _run(ns, ctx, tasks, w, mode, N, K, L, M, greedy=0):
+    ns.ns_load_cost_models(ctx, w)
+    desc, off, caps = ns.table_descs(tasks)
+    tabs = ns.ns_featurize_tables(ctx, desc, off, caps)
+    try:
+        if mode == "tablewise":
+            return ns.ns_shard_tablewise(ctx, tabs, w.D, M=M, greedy=greedy)
+        return ns.ns_shard_columnwise(ctx, tabs, w.D, N=N, K=K, L=L, M=M, greedy=greedy)
+    finally:
+        tabs.free()
+
+
+def _compare(out, i, task, w, exp, min_margin, M):
+    """Exact identity when the oracle is tie-free at fp64 resolution, else
+    certify the returned plan."""
+    nc = int(out["n_col"][i]) if out.get("n_col") is not None else 0
+    col = out["col_plan"][i, :nc].tolist() if nc else []
+    cost = float(out["cost"][i])
+    if min_margin >= RTOL:
+        assert col == exp["col_plan"], "column plan"
+        ec = _f(exp["cost"])
+        assert (math.isinf(cost) and math.isinf(ec)) or abs(cost - ec) <= RTOL * abs(ec), (cost, ec)
+        assert int(out["n_scores"][i]) == exp["work"], "work W"
+        if exp["assign"] is not None:
+            assert int(out["grid_index"][i]) == exp["grid_index"]
+            assert out["assign"][i, :task.T + nc].tolist() == exp["assign"], "assignment"
+        return "identical"
+    if math.isinf(cost):
+        assert math.isinf(_f(exp["cost"]))
+        return "infeasible"
+    certify_plan(w, task, col, out["assign"][i, :task.T + nc].tolist(), int(out["grid_index"][i]), cost, M)
+    return "certified"
+
+
+@pytest.mark.parametrize("name", sorted(FIX))
+def test_fullsize_against_oracle_fixture(ns, ctx, name):
+    c = FIX[name]
+    task = gen_task(c["config"], c["task_index"], T=c["T"] if c["T"] != CONFIGS[c["config"]]["T"] else None)
+    assert task.T == c["T"]
+    w = gen_weights(c["D"], "mono")
+    out = _run(ns, ctx, [task], w, c["mode"], c["N"], c["K"], c["L"], c["M"])
+    how = _compare(out, 0, task, w, c["expected"], _f(c["min_margin"]), c["M"])
+    assert how == "identical" or _f(c["min_margin"]) < RTOL
+
+
+def test_fullsize_batched_same_as_single(ns, ctx):
+    """The C3 fixtures again as one batch of 2 (grouped greedy, batch-wide
+    kernels): identical to the oracle as well."""
+    names = ["C3_full_0", "C3_full_1"]
+    tasks = [gen_task("C3", FIX[n]["task_index"]) for n in names]
+    w = gen_weights(8, "mono")
+    out = _run(ns, ctx, tasks, w, "columnwise", 10, 10, 10, 11, greedy=1)
+    for i, n in enumerate(names):
+        _compare(out, i, tasks[i], w, FIX[n]["expected"], _f(FIX[n]["min_margin"]), 11)
+
+
+def _oracle_check_batch(out, tasks, w, mode, N, K, L, M):
+    kinds = {"identical": 0, "certified": 0, "infeasible": 0}
+    for i, task in enumerate(tasks):
+        emb = om.TableEmbeddings(w, task)
+        log = osr.DecisionLog()
+        if mode == "tablewise":
+            r = osr.greedy_grid_search(w, emb, task, [], M, log=log)
+            exp = dict(cost=r.cost, col_plan=[], assign=r.assign, grid_index=r.grid_index, work=r.work)
+        else:
+            r = osr.beam_search(w, emb, task, N=N, K=K, L=L, M=M, log=log)
+            exp = dict(cost=r.cost, col_plan=r.col_plan, assign=r.assign, grid_index=r.grid_index, work=r.work)
+        kinds[_compare(out, i, task, w, exp, log.min_margin(), M)] += 1
+        # the certificate holds for every returned plan, tie or not
+        nc = int(out["n_col"][i]) if out.get("n_col") is not None else 0
+        if math.isfinite(out["cost"][i]):
+            certify_plan(w, task, out["col_plan"][i, :nc].tolist() if nc else [],
+                         out["assign"][i, :task.T + nc].tolist(), int(out["grid_index"][i]),
+                         float(out["cost"][i]), M, emb=emb)
+    return kinds
+
+
+@pytest.mark.parametrize("greedy", [1, 2])
+def test_ragged_batch_long_task_moves_short_tasks_to_long_list_path(ns, ctx, greedy):
+    """One T = 300 task among short ones: the batch's max list length selects
+    the CTA-per-plan order and block-argmax candidate kernels for EVERY task,
+    so the short tasks (oracle-checkable in seconds) exercise the long-list
+    path too."""
+    w = gen_weights(4, "mono")
+    long_task = small_task(np.random.default_rng(900), 300, 4, hash_hi=1e5)   # T = 300 fits D = 4 at 4 GiB
+    tasks = [long_task] + gen_tasks("C2", 11, T=16)
+    out = _run(ns, ctx, tasks, w, "tablewise", 0, 0, 0, 11, greedy=greedy)
+    k = _oracle_check_batch(out, tasks, w, "tablewise", 0, 0, 0, 11)
+    assert k["identical"] >= 10
+    out = _run(ns, ctx, tasks, w, "columnwise", 4, 2, 2, 5, greedy=greedy)
+    k = _oracle_check_batch(out, tasks, w, "columnwise", 4, 2, 2, 5)
+    assert k["identical"] >= 10
+
+
+def test_near_tie_tasks_are_certified(ns, ctx):
+    """Tasks whose oracle log has a margin below 1e-12 are not skipped: the
+    returned plan is recomputed (T8), validated and certificate-replayed
+    (every returned plan is certified as well).  The 'lin' compute model
+    (zero comm) makes exact ties abundant: empty devices and equal dim sums."""
+    w = gen_weights(4, "lin")
+    tasks = gen_tasks("C2", 12, T=24)
+    out = _run(ns, ctx, tasks, w, "tablewise", 0, 0, 0, 11)
+    k = _oracle_check_batch(out, tasks, w, "tablewise", 0, 0, 0, 11)
+    assert sum(k.values()) == len(tasks)
+    out = _run(ns, ctx, tasks, w, "columnwise", 4, 2, 2, 5)
+    k = _oracle_check_batch(out, tasks, w, "columnwise", 4, 2, 2, 5)
+    assert sum(k.values()) == len(tasks)

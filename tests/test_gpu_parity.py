@@ -9,6 +9,7 @@ import math
 import numpy as np
 import pytest
 
+from certify import certify_plan
 from conftest import hand_task, hand_weights, small_task
 from oracle import brute, model as om, search as osr
 from workload.synth import gen_task, gen_tasks, gen_weights, gen_plans
@@ -56,9 +57,14 @@ def _check_tablewise(ns, ctx, tasks, w, M, greedy=0):
         emb = om.TableEmbeddings(w, task)
         log = osr.DecisionLog()
         r = osr.greedy_grid_search(w, emb, task, [], M, log=log)
-        assert int(out["n_scores"][i]) == r.work, f"task {i}: work"
+        assert int(out["n_scores"][i]) == r.work or log.min_margin() < RTOL, f"task {i}: work"
         if log.min_margin() < RTOL:
-            continue   # near-tie below fp64 resolution: decisions may legitimately differ
+            # near-tie below fp64 resolution: decisions may legitimately
+            # differ -- certify the returned plan instead (tests/certify.py)
+            if math.isfinite(out["cost"][i]):
+                certify_plan(w, task, [], out["assign"][i, :task.T].tolist(), int(out["grid_index"][i]),
+                             float(out["cost"][i]), M, emb=emb)
+            continue
         n_exact += 1
         assert _rel(out["cost"][i], r.cost) <= RTOL, f"task {i}: cost {out['cost'][i]} vs {r.cost}"
         if r.assign is None:
@@ -209,6 +215,10 @@ def _check_columnwise(ns, ctx, tasks, w, N, K, L, M, greedy=0):
         r = osr.beam_search(w, emb, task, N=N, K=K, L=L, M=M, log=log)
         assert int(out["n_scores"][i]) == r.work or log.min_margin() < RTOL, f"task {i}: work"
         if log.min_margin() < RTOL:
+            nc = int(out["n_col"][i])
+            if math.isfinite(out["cost"][i]):
+                certify_plan(w, task, out["col_plan"][i, :nc].tolist(), out["assign"][i, :task.T + nc].tolist(),
+                             int(out["grid_index"][i]), float(out["cost"][i]), M, emb=emb)
             continue
         n_exact += 1
         nc = int(out["n_col"][i])
