@@ -247,13 +247,43 @@ ns_status ns_shard_columnwise(ns_ctx* ctx, const ns_tables* tables, int32_t D,
 /* 128-byte NCCL unique id (call on rank 0, broadcast by any means). */
 ns_status ns_comm_unique_id(unsigned char id_out[128]);
 /* Make subsequent ns_score_plans / ns_shard_* calls collective over nranks
- * processes (one GPU each): each level's column plans are split into equal
- * contiguous blocks per rank and the per-trajectory results are allgathered
- * (NCCL) so every rank selects identically.  nranks == 1 is allowed (no-op).
+ * processes (one GPU each): each level's column plans are split
+ * into equal contiguous blocks per rank; the per-trajectory keys (cost,
+ * feasibility, work, duplicate link) are allgathered so every rank runs the
+ * same grid argmin / top-K / global-best selection; the winning assignment
+ * lives only on the rank that computed it and reaches the others through an
+ * int8 allreduce-max (the others contribute -128); finally an allreduce-min
+ * over the packed per-task keys (order-preserving cost bits, plan hash) and
+ * their complements certifies that every rank selected the same plan
+ * (NS_ERR_INTERNAL otherwise).  nranks == 1 with an id creates a real
+ * one-rank NCCL communicator (the collectives then run through NCCL);
+ * nranks == 1 with id == NULL is a no-op (plain single-GPU calls).
  * id == NULL with nranks > 1 is a test hook ("emulated ranks"): this process
  * computes every rank's block itself, exercising the partitioning without
  * NCCL. */
 ns_status ns_comm_init(ns_ctx* ctx, int32_t nranks, int32_t rank, const unsigned char id[128]);
+
+/* Caller-provided transport for the collectives (e.g. MPI or a
+ * torch.distributed gloo group): the library stages the data in host memory
+ * and calls these from the calling thread, in the same order on every rank.
+ * Both return 0 on success (anything else -> NS_ERR_NCCL).
+ *   allgather: send = this rank's bytes_per_rank bytes; recv = nranks blocks in
+ *              rank order (recv + rank * bytes_per_rank may alias send).
+ *   allreduce: element-wise over count elements in place; op NS_COMM_MIN_U64
+ *              (uint64 minimum) or NS_COMM_MAX_I8 (int8 maximum). */
+#define NS_COMM_MIN_U64 0
+#define NS_COMM_MAX_I8 1
+typedef struct {
+    void* user;
+    int (*allgather)(void* user, const void* send, void* recv, size_t bytes_per_rank);
+    int (*allreduce)(void* user, void* buf, size_t count, int op);
+} ns_host_comm;
+/* Like ns_comm_init, with the collectives going through `comm` (copied; the
+ * function pointers and user data must stay valid until the ctx is destroyed
+ * or re-initialised).  Several processes may share one GPU this way (NCCL
+ * refuses two ranks on one device), which is how the multi-process path is
+ * tested on a one-GPU box. */
+ns_status ns_comm_init_host(ns_ctx* ctx, int32_t nranks, int32_t rank, const ns_host_comm* comm);
 
 #ifdef __cplusplus
 }

@@ -17,6 +17,8 @@ from ._native import (  # noqa: F401
     TABLE_DESC,
     Tables,
     ns_comm_init,
+    ns_comm_init_host,
+    torch_host_comm,
     ns_comm_unique_id,
     ns_create,
     ns_destroy,

@@ -39,6 +39,14 @@ class ns_compute_model(C.Structure):
     _fields_ = [("enc", ns_linear * 2), ("head", ns_linear * 2)]
 
 
+_ALLGATHER_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_size_t)
+_ALLREDUCE_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_size_t, C.c_int)
+
+
+class ns_host_comm(C.Structure):
+    _fields_ = [("user", C.c_void_p), ("allgather", _ALLGATHER_FN), ("allreduce", _ALLREDUCE_FN)]
+
+
 class ns_comm_model(C.Structure):
     _fields_ = [("D", C.c_int32), ("layer", ns_linear * 5), ("start_scale", C.c_double), ("dim_scale", C.c_double)]
 
@@ -79,6 +87,7 @@ def _load():
         "ns_shard_columnwise": ([vp, vp, i32, C.POINTER(ns_search_params), C.POINTER(ns_plan_batch)], C.c_int),
         "ns_comm_unique_id": ([vp], C.c_int),
         "ns_comm_init": ([vp, i32, i32, vp], C.c_int),
+        "ns_comm_init_host": ([vp, i32, i32, C.POINTER(ns_host_comm)], C.c_int),
     }
     for name, (args, res) in sig.items():
         f = getattr(lib, name)
@@ -91,7 +100,8 @@ LIB = _load()
 EXPORTED = ["ns_create", "ns_destroy", "ns_last_error", "ns_set_stream", "ns_synchronize", "ns_kernel_launches",
             "ns_profile", "ns_profile_query",
             "ns_load_cost_models", "ns_featurize_tables", "ns_tables_free", "ns_tables_single_costs",
-            "ns_score_plans", "ns_shard_tablewise", "ns_shard_columnwise", "ns_comm_unique_id", "ns_comm_init"]
+            "ns_score_plans", "ns_shard_tablewise", "ns_shard_columnwise", "ns_comm_unique_id", "ns_comm_init",
+            "ns_comm_init_host"]
 
 
 def _check(ctx, status: int, allow_infeasible: bool = True) -> int:
@@ -322,3 +332,67 @@ def ns_comm_init(ctx: int, nranks: int, rank: int, uid: Optional[bytes]) -> None
     """uid None with nranks > 1: emulated ranks (test hook, no NCCL)."""
     buf = (C.c_ubyte * 128).from_buffer_copy(uid) if uid else None
     _check(ctx, LIB.ns_comm_init(ctx, nranks, rank, buf))
+
+
+NS_COMM_MIN_U64 = 0
+NS_COMM_MAX_I8 = 1
+_HOST_COMMS = {}   # ctx -> (struct, callbacks): kept alive while the ctx uses them
+
+
+def ns_comm_init_host(ctx: int, nranks: int, rank: int, allgather, allreduce) -> None:
+    """Collectives through Python callbacks on host buffers (header:
+    ns_host_comm).  ``allgather(send: np.ndarray[uint8], recv: np.ndarray[uint8])``
+    fills recv (nranks blocks); ``allreduce(buf: np.ndarray, op)`` reduces in
+    place (uint64 min or int8 max).  Marshalling only."""
+    def ag(user, send, recv, nbytes):
+        try:
+            s_ = np.ctypeslib.as_array((C.c_uint8 * nbytes).from_address(send))
+            r_ = np.ctypeslib.as_array((C.c_uint8 * (nbytes * nranks)).from_address(recv))
+            allgather(s_.copy(), r_)
+            return 0
+        except BaseException:   # reported to the caller as NS_ERR_NCCL
+            import traceback
+            traceback.print_exc()
+            return 1
+
+    def ar(user, buf, count, op):
+        try:
+            ct = C.c_uint64 if op == NS_COMM_MIN_U64 else C.c_int8
+            b_ = np.ctypeslib.as_array((ct * count).from_address(buf))
+            allreduce(b_, op)
+            return 0
+        except BaseException:
+            import traceback
+            traceback.print_exc()
+            return 1
+
+    cb = ns_host_comm(None, _ALLGATHER_FN(ag), _ALLREDUCE_FN(ar))
+    _HOST_COMMS[ctx] = cb
+    _check(ctx, LIB.ns_comm_init_host(ctx, nranks, rank, C.byref(cb)))
+
+
+def torch_host_comm(group=None):
+    """(allgather, allreduce) callbacks over a torch.distributed process group
+    (e.g. gloo) for ns_comm_init_host."""
+    import torch
+    import torch.distributed as dist
+
+    def allgather(send, recv):
+        world = dist.get_world_size(group)
+        t = torch.from_numpy(send)
+        outs = [torch.empty_like(t) for _ in range(world)]
+        dist.all_gather(outs, t, group=group)
+        recv[:] = torch.cat(outs).numpy()
+
+    def allreduce(buf, op):
+        if op == NS_COMM_MIN_U64:
+            # uint64 order == int64 order after flipping the sign bit
+            v = torch.from_numpy(buf.view(np.int64) ^ np.int64(-0x8000000000000000))
+            dist.all_reduce(v, op=dist.ReduceOp.MIN, group=group)
+            buf[:] = (v.numpy() ^ np.int64(-0x8000000000000000)).view(np.uint64)
+        else:
+            v = torch.from_numpy(buf.astype(np.int32))   # int8 max via int32 (gloo-safe)
+            dist.all_reduce(v, op=dist.ReduceOp.MAX, group=group)
+            buf[:] = v.numpy().astype(np.int8)
+
+    return allgather, allreduce

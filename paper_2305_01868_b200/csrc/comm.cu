@@ -67,25 +67,82 @@ void comm_destroy(ns_ctx* ctx) {
         ctx->nranks = 1;
         ctx->rank = 0;
         ctx->emulated = false;
+        ctx->host_comm_on = false;
+        ctx->host_comm = ns_host_comm{};
     }
 }
 
+bool comm_collective(const ns_ctx* ctx) {
+    return ctx->nranks > 1 || ctx->nccl != nullptr || ctx->host_comm_on || ctx->emulated;
+}
+
+namespace {
+// host-callback backend: stage through pinned memory on the ctx stream
+char* host_stage(ns_ctx* ctx, size_t bytes) {
+    if (ctx->comm_stage_bytes < bytes) {
+        if (ctx->comm_stage) cudaFreeHost(ctx->comm_stage);
+        ctx->comm_stage = nullptr;
+        ctx->comm_stage_bytes = 0;
+        if (cudaMallocHost(&ctx->comm_stage, bytes) != cudaSuccess) return nullptr;
+        ctx->comm_stage_bytes = bytes;
+    }
+    return (char*)ctx->comm_stage;
+}
+}  // namespace
+
 ns_status comm_allgather(ns_ctx* ctx, const void* send, void* recv, size_t bytes_per_rank) {
-    if (ctx->nranks == 1 || ctx->emulated) {
+    if (ctx->emulated || (!ctx->nccl && !ctx->host_comm_on)) {
         if (send != recv)
             NS_CUDA(ctx, cudaMemcpyAsync(recv, send, bytes_per_rank, cudaMemcpyDeviceToDevice, ctx->stream));
         return NS_OK;
     }
-    ncclResult_t r = api().AllGather(send, recv, bytes_per_rank, ncclUint8, (ncclComm_t)ctx->nccl, ctx->stream);
-    if (r != ncclSuccess) return nccl_err(ctx, r, "ncclAllGather");
+    if (ctx->nccl) {
+        ncclResult_t r = api().AllGather(send, recv, bytes_per_rank, ncclUint8, (ncclComm_t)ctx->nccl, ctx->stream);
+        if (r != ncclSuccess) return nccl_err(ctx, r, "ncclAllGather");
+        return NS_OK;
+    }
+    const size_t total = bytes_per_rank * (size_t)ctx->nranks;
+    char* h = host_stage(ctx, total);
+    if (!h) return set_err(ctx, NS_ERR_NOMEM, "pinned comm staging");
+    char* mine = h + (size_t)ctx->rank * bytes_per_rank;
+    NS_CUDA(ctx, cudaMemcpyAsync(mine, send, bytes_per_rank, cudaMemcpyDeviceToHost, ctx->stream));
+    NS_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+    if (ctx->host_comm.allgather(ctx->host_comm.user, mine, h, bytes_per_rank) != 0)
+        return set_err(ctx, NS_ERR_NCCL, "host allgather callback failed");
+    NS_CUDA(ctx, cudaMemcpyAsync(recv, h, total, cudaMemcpyHostToDevice, ctx->stream));
+    NS_CUDA(ctx, cudaStreamSynchronize(ctx->stream));   // the staging is reused by the next collective
     return NS_OK;
 }
 
-ns_status comm_allreduce_min_u64(ns_ctx* ctx, uint64_t* buf, size_t count) {
-    if (ctx->nranks == 1 || ctx->emulated) return NS_OK;
-    ncclResult_t r = api().AllReduce(buf, buf, count, ncclUint64, ncclMin, (ncclComm_t)ctx->nccl, ctx->stream);
-    if (r != ncclSuccess) return nccl_err(ctx, r, "ncclAllReduce(min)");
+namespace {
+ns_status allreduce(ns_ctx* ctx, void* buf, size_t count, int op) {
+    if (ctx->emulated || (!ctx->nccl && !ctx->host_comm_on)) return NS_OK;
+    if (ctx->nccl) {
+        ncclResult_t r = op == NS_COMM_MIN_U64
+                             ? api().AllReduce(buf, buf, count, ncclUint64, ncclMin, (ncclComm_t)ctx->nccl, ctx->stream)
+                             : api().AllReduce(buf, buf, count, ncclInt8, ncclMax, (ncclComm_t)ctx->nccl, ctx->stream);
+        if (r != ncclSuccess) return nccl_err(ctx, r, op == NS_COMM_MIN_U64 ? "ncclAllReduce(min)" : "ncclAllReduce(max)");
+        return NS_OK;
+    }
+    const size_t bytes = count * (op == NS_COMM_MIN_U64 ? 8 : 1);
+    char* h = host_stage(ctx, bytes);
+    if (!h) return set_err(ctx, NS_ERR_NOMEM, "pinned comm staging");
+    NS_CUDA(ctx, cudaMemcpyAsync(h, buf, bytes, cudaMemcpyDeviceToHost, ctx->stream));
+    NS_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+    if (ctx->host_comm.allreduce(ctx->host_comm.user, h, count, op) != 0)
+        return set_err(ctx, NS_ERR_NCCL, "host allreduce callback failed");
+    NS_CUDA(ctx, cudaMemcpyAsync(buf, h, bytes, cudaMemcpyHostToDevice, ctx->stream));
+    NS_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
     return NS_OK;
+}
+}  // namespace
+
+ns_status comm_allreduce_min_u64(ns_ctx* ctx, uint64_t* buf, size_t count) {
+    return allreduce(ctx, buf, count, NS_COMM_MIN_U64);
+}
+
+ns_status comm_allreduce_max_i8(ns_ctx* ctx, int8_t* buf, size_t count) {
+    return allreduce(ctx, buf, count, NS_COMM_MAX_I8);
 }
 
 }  // namespace ns
@@ -106,7 +163,7 @@ ns_status ns_comm_init(ns_ctx* ctx, int32_t nranks, int32_t rank, const unsigned
     if (!ctx) return NS_ERR_ARG;
     if (nranks < 1 || rank < 0 || rank >= nranks) return ns::set_err(ctx, NS_ERR_ARG, "ns_comm_init: bad nranks/rank");
     ns::comm_destroy(ctx);
-    if (nranks == 1) return NS_OK;
+    if (nranks == 1 && !id) return NS_OK;
     if (!id) {   // emulated ranks: partitioning exercised in one process, no NCCL
         ctx->nranks = nranks;
         ctx->rank = 0;
@@ -121,6 +178,18 @@ ns_status ns_comm_init(ns_ctx* ctx, int32_t nranks, int32_t rank, const unsigned
     ncclResult_t r = api().CommInitRank(&comm, nranks, uid, rank);
     if (r != ncclSuccess) return nccl_err(ctx, r, "ncclCommInitRank");
     ctx->nccl = comm;
+    ctx->nranks = nranks;
+    ctx->rank = rank;
+    return NS_OK;
+}
+
+ns_status ns_comm_init_host(ns_ctx* ctx, int32_t nranks, int32_t rank, const ns_host_comm* comm) {
+    if (!ctx) return NS_ERR_ARG;
+    if (nranks < 1 || rank < 0 || rank >= nranks || !comm || !comm->allgather || !comm->allreduce)
+        return ns::set_err(ctx, NS_ERR_ARG, "ns_comm_init_host: bad nranks/rank or missing callbacks");
+    ns::comm_destroy(ctx);
+    ctx->host_comm = *comm;
+    ctx->host_comm_on = true;
     ctx->nranks = nranks;
     ctx->rank = rank;
     return NS_OK;

@@ -402,7 +402,7 @@ ns_status run_score_plans(ns_ctx* ctx, const ns_tables* t, int task, int D, cons
     k_argmin_final<<<1, 32, 0, ctx->stream>>>(d_part, nblk_arg, d_best);
     prof_end(ctx);
     NS_LAUNCHED(ctx);
-    if (ctx->nranks > 1) {   // (emulated ranks run the key stages with a no-op reduction)
+    if (comm_collective(ctx)) {   // (emulated ranks run the key stages with a no-op reduction)
         // global argmin over ranks: exact two-key NCCL allreduce-min -- first
         // the order-preserving 64-bit image of the best cost, then the lowest
         // plan index among the ranks holding that cost (lowest index on ties)

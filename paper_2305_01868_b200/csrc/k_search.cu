@@ -59,6 +59,11 @@ struct SearchBufs {
     int32_t* best_plan;  // [n_tasks][Lcap]
     int8_t* best_assign; // [n_tasks][Tpm]
     uint64_t* n_scores;  // [n_tasks]
+    uint64_t* rank_keys; // [n_tasks][4] multi-rank consistency keys
+    // column plans [own_cb, own_ce) of the current level were computed by this
+    // rank (all of them with one rank or emulated ranks): only their
+    // assignment rows are valid here (multi-rank: the others are not exchanged)
+    int own_cb, own_ce;
 };
 
 struct TaskView {   // read-only table arrays of the batch
@@ -1586,13 +1591,17 @@ __global__ void __launch_bounds__(256) k_select0(SearchBufs b, OutStage o, int f
             const long long tau = (long long)q * b.M + bm;
             src = b.dup_of[tau] >= 0 ? (long long)b.dup_of[tau] : tau;
         }
+        // multi-rank: another rank owns the row -> -128 here, the int8
+        // allreduce-max after the search fills in the owner's values
+        const bool own = q >= b.own_cb && q < b.own_ce;
         if (final_out) {
             for (int i = lane; i < o.astride; i += 32)
                 o.assign[(size_t)q * o.astride + i] =
-                    (src >= 0 && i < Tp && i < b.Tpm) ? b.assign[src * b.Tpm + i] : (int8_t)-1;
+                    (src >= 0 && i < Tp && i < b.Tpm) ? (own ? b.assign[src * b.Tpm + i] : (int8_t)-128) : (int8_t)-1;
         } else {
             for (int i = lane; i < b.Tpm; i += 32)
-                b.best_assign[(size_t)q * b.Tpm + i] = (src >= 0 && i < Tp) ? b.assign[src * b.Tpm + i] : (int8_t)-1;
+                b.best_assign[(size_t)q * b.Tpm + i] =
+                    (src >= 0 && i < Tp) ? (own ? b.assign[src * b.Tpm + i] : (int8_t)-128) : (int8_t)-1;
         }
     }
 }
@@ -1721,8 +1730,10 @@ __global__ void __launch_bounds__(256) k_select(SearchBufs b, int C, int level, 
             const long long tau = (long long)g * b.M + mm;
             src = b.dup_of[tau] >= 0 ? (long long)b.dup_of[tau] : tau;
         }
+        const bool own = g >= b.own_cb && g < b.own_ce;
         for (int i = threadIdx.x; i < b.Tpm; i += blockDim.x)
-            b.best_assign[(size_t)q * b.Tpm + i] = (src >= 0 && i < Tp) ? b.assign[src * b.Tpm + i] : (int8_t)-1;
+            b.best_assign[(size_t)q * b.Tpm + i] =
+                (src >= 0 && i < Tp) ? (own ? b.assign[src * b.Tpm + i] : (int8_t)-128) : (int8_t)-1;
     }
     if (level > 0) {
         // next beam: rank among valid children by (cost, gen); one warp per child
@@ -1764,6 +1775,42 @@ __global__ void k_grid_caps(const int64_t* sumdim, int n_tasks, int D, int M, do
     capdim[i] = f > 2.0e9 ? 2000000000 : (int32_t)f;
 }
 
+
+// Multi-rank consistency check: per task the packed key
+// (order-preserving bits of the best cost, FNV-1a hash of (column plan, grid
+// index)) and its complement; after an allreduce-min over the ranks, key ==
+// min and ~key == min(~key) (i.e. key == max) on every rank iff all ranks
+// selected the same plan.  mode 0 builds the keys, mode 1 checks them.
+__device__ __forceinline__ unsigned long long order_key64(double c) {
+    const long long sb = __double_as_longlong(c + 0.0);
+    return (unsigned long long)(sb ^ ((sb >> 63) | (long long)0x8000000000000000ULL));
+}
+
+__global__ void k_rank_check(SearchBufs b, int mode, int32_t* flag) {
+    const int q = blockIdx.x * blockDim.x + threadIdx.x;
+    if (q >= b.n_tasks) return;
+    const unsigned long long k0 = order_key64(b.best_cost[q]);
+    unsigned long long h = 1469598103934665603ULL;
+    auto mix = [&](unsigned long long v) {
+        for (int i = 0; i < 4; ++i) {
+            h ^= (v >> (16 * i)) & 0xffffULL;
+            h *= 1099511628211ULL;
+        }
+    };
+    const int nc = b.best_ncol[q];
+    mix((unsigned long long)(unsigned)nc);
+    mix((unsigned long long)(unsigned)b.best_m[q]);
+    for (int k = 0; k < nc; ++k) mix((unsigned long long)(unsigned)b.best_plan[(size_t)q * b.Lcap + k]);
+    uint64_t* key = b.rank_keys + 4 * (size_t)q;
+    if (mode == 0) {
+        key[0] = k0;
+        key[1] = h;
+        key[2] = ~k0;
+        key[3] = ~h;
+    } else if (key[0] != k0 || key[1] != h || key[2] != ~k0 || key[3] != ~h) {
+        atomicOr(flag, 2);
+    }
+}
 
 __global__ void __launch_bounds__(256) k_write_out(SearchBufs b, OutStage o, int Lout) {
     const int lane = threadIdx.x & 31;
@@ -1835,6 +1882,7 @@ void carve(Carver& c, SearchBufs& b, OutStage& o, int Lout) {
     b.best_plan = c.take<int32_t>((size_t)b.n_tasks * b.Lcap);
     b.best_assign = c.take<int8_t>((size_t)b.n_tasks * b.Tpm);
     b.n_scores = c.take<uint64_t>(b.n_tasks);
+    b.rank_keys = c.take<uint64_t>((size_t)b.n_tasks * 4);
     o.cost = c.take<double>(b.n_tasks);
     o.n_col = c.take<int32_t>(b.n_tasks);
     o.col_plan = c.take<int32_t>((size_t)b.n_tasks * Lout);
@@ -2029,10 +2077,12 @@ ns_status launch_finalize(ns_ctx* ctx, const SearchBufs& b, long long tb, long l
 // per-trajectory results (cost, feasibility, work, duplicate link, assignment)
 // are allgathered in place so every rank runs the identical N6 selection
 // (SURVEY §8(e)).  Single rank: plain launches.
-ns_status run_level_trajectories(ns_ctx* ctx, const SearchBufs& b, const ns_tables* t, long long n_cp) {
+ns_status run_level_trajectories(ns_ctx* ctx, SearchBufs& b, const ns_tables* t, long long n_cp) {
     const long long R = ctx->nranks;
     const long long per = (n_cp + R - 1) / R;
     ns_status s;
+    b.own_cb = ctx->emulated ? 0 : (int)std::min(n_cp, ctx->rank * per);
+    b.own_ce = ctx->emulated ? (int)n_cp : (int)std::min(n_cp, (long long)b.own_cb + per);
     // emulated ranks (test hook, ns_comm_init with id == NULL): this process
     // computes every rank's block into the shared buffers, the allgather is
     // the identity
@@ -2044,14 +2094,15 @@ ns_status run_level_trajectories(ns_ctx* ctx, const SearchBufs& b, const ns_tabl
             if ((s = launch_finalize(ctx, b, cb * b.M, ce * b.M)) != NS_OK) return s;
         }
     }
-    if (R == 1 || ctx->emulated) return NS_OK;
+    if (!comm_collective(ctx) || ctx->emulated) return NS_OK;
     const long long rk = ctx->rank;
     const size_t blk = (size_t)per * b.M;   // trajectories per rank block
+    // the per-trajectory keys selection needs; assignment rows stay on their
+    // rank (the winner's reaches the others by the int8 allreduce-max)
     struct {
         void* base;
         size_t elem;
-    } arrs[] = {{b.tcost, sizeof(double)}, {b.feas, 1}, {b.work, sizeof(uint32_t)}, {b.dup_of, sizeof(int32_t)},
-                {b.assign, (size_t)b.Tpm}};
+    } arrs[] = {{b.tcost, sizeof(double)}, {b.feas, 1}, {b.work, sizeof(uint32_t)}, {b.dup_of, sizeof(int32_t)}};
     for (auto& ar : arrs) {
         char* recv = (char*)ar.base;
         const size_t bytes = blk * ar.elem;
@@ -2237,6 +2288,20 @@ ns_status run_search(ns_ctx* ctx, const ns_tables* t, int D, const ns_search_par
         if (ssel > 40 * 1024) cudaFuncSetAttribute(k_select, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ssel);
         k_select<<<b.n_tasks, 256, ssel, ctx->stream>>>(b, C, level, b.K, staged);
         prof_end(ctx);
+        NS_LAUNCHED(ctx);
+    }
+    if (comm_collective(ctx) && !ctx->emulated) {
+        // the winning assignment from its owner rank, then the consistency keys
+        if (final0) {
+            if ((s = comm_allreduce_max_i8(ctx, o.assign, (size_t)b.n_tasks * o.astride)) != NS_OK) return s;
+        } else if ((s = comm_allreduce_max_i8(ctx, b.best_assign, (size_t)b.n_tasks * b.Tpm)) != NS_OK) {
+            return s;
+        }
+        const unsigned kb = (unsigned)((b.n_tasks + 127) / 128);
+        k_rank_check<<<kb, 128, 0, ctx->stream>>>(b, 0, t->d_flag);
+        NS_LAUNCHED(ctx);
+        if ((s = comm_allreduce_min_u64(ctx, b.rank_keys, (size_t)b.n_tasks * 4)) != NS_OK) return s;
+        k_rank_check<<<kb, 128, 0, ctx->stream>>>(b, 1, t->d_flag);
         NS_LAUNCHED(ctx);
     }
     if (!final0) {

@@ -281,6 +281,7 @@ ns_status ns_destroy(ns_ctx* ctx) {
     if (ctx->arena) cudaFree(ctx->arena);
     if (ctx->pinned) cudaFreeHost(ctx->pinned);
     if (ctx->pinned_in) cudaFreeHost(ctx->pinned_in);
+    if (ctx->comm_stage) cudaFreeHost(ctx->comm_stage);
     if (ctx->pinned_in_done) cudaEventDestroy(ctx->pinned_in_done);
     if (ctx->d_async_flags) cudaFree(ctx->d_async_flags);
     if (ctx->copy_stream) {
@@ -595,6 +596,8 @@ ns_status check_async_flags(ns_ctx* ctx) {
 // Device-side validation flag of the descriptors (set by k_tables_validate).
 ns_status check_tables_flag(ns_ctx* ctx, const ns_tables* t, const int32_t* host_flag) {
     (void)t;
+    if (*host_flag & 2)   // set by the multi-rank consistency check (k_search.cu, k_rank_check)
+        return set_err(ctx, NS_ERR_INTERNAL, "ranks selected different plans (multi-rank consistency check)");
     if (*host_flag != 0)
         return set_err(ctx, NS_ERR_ARG,
                        "invalid table descriptor in device-resident input (need dim%4==0, dim>=4, hash>=1, "

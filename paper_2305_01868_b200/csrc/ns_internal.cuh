@@ -117,9 +117,13 @@ struct ns_ctx {
     std::vector<ns::ProfPending> prof_pending;
     std::vector<cudaEvent_t> prof_free;
     // multi-GPU
-    void* nccl = nullptr;    // ncclComm_t
+    void* nccl = nullptr;    // ncclComm_t (also with nranks == 1: ns_comm_init with an id)
     int nranks = 1, rank = 0;
     bool emulated = false;   // ns_comm_init(id == NULL): all ranks' blocks computed in-process (test hook)
+    bool host_comm_on = false;    // ns_comm_init_host: collectives through caller callbacks on host buffers
+    ns_host_comm host_comm{};
+    void* comm_stage = nullptr;   // pinned staging of the host-callback collectives
+    size_t comm_stage_bytes = 0;
     std::set<ns_tables*> tables;   // live ns_tables of this ctx (freed by ns_destroy)
     // validation flags of NS_SEARCH_ASYNC searches, checked by ns_synchronize
     static constexpr int kAsyncFlags = 256;
@@ -204,6 +208,10 @@ cudaError_t ensure_copy_stream(ns_ctx* ctx);          // lazily created copy str
 CommParams comm_params(const ns_ctx* ctx);
 ns_status comm_allgather(ns_ctx* ctx, const void* send, void* recv, size_t bytes_per_rank);
 ns_status comm_allreduce_min_u64(ns_ctx* ctx, uint64_t* dev_buf, size_t count);
+ns_status comm_allreduce_max_i8(ns_ctx* ctx, int8_t* dev_buf, size_t count);
+// true when search / score calls are collective over ranks (any backend,
+// including a 1-rank NCCL communicator and emulated ranks)
+bool comm_collective(const ns_ctx* ctx);
 void comm_destroy(ns_ctx* ctx);
 
 

@@ -47,3 +47,44 @@ def test_two_rank_aggregation_gloo():
     assert all(r[2] == 300.0 for r in res)         # sum over ranks
     seeds = [set(r[3]) for r in res]
     assert not (seeds[0] & seeds[1])               # disjoint tasks per rank
+
+
+def _comm_worker(rank, world, port, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    import numpy as np
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2305_01868_b200._native import NS_COMM_MAX_I8, NS_COMM_MIN_U64, torch_host_comm
+    ag, ar = torch_host_comm()
+    send = np.arange(5, dtype=np.uint8) + 10 * rank
+    recv = np.zeros(5 * world, np.uint8)
+    ag(send, recv)
+    # uint64 minimum across the sign bit (order-preserving cost keys live there)
+    keys = np.array([0xFFFF000000000000 - rank, 5 + rank, 0x8000000000000000 + rank], dtype=np.uint64)
+    ar(keys, NS_COMM_MIN_U64)
+    # int8 maximum: the owner's row wins over the others' -128 filler
+    row = np.array([-128, -128, -1], np.int8) if rank else np.array([3, 0, -1], np.int8)
+    ar(row, NS_COMM_MAX_I8)
+    q.put((rank, recv.tolist(), keys.tolist(), row.tolist()))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_host_comm_callbacks_world2():
+    """The torch.distributed (gloo) callbacks behind ns_comm_init_host: the
+    allgather concatenates in rank order, the uint64 min is unsigned (keys
+    above 2^63 are the common case), the int8 max fills in the owner's row."""
+    world, port = 2, _free_port()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    ps = [ctx.Process(target=_comm_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in ps:
+        p.start()
+    res = dict((r, rest) for r, *rest in (q.get(timeout=120) for _ in range(world)))
+    for p in ps:
+        p.join(timeout=60)
+    for r in range(world):
+        recv, keys, row = res[r]
+        assert recv == [0, 1, 2, 3, 4, 10, 11, 12, 13, 14]
+        assert keys == [0xFFFF000000000000 - 1, 5, 0x8000000000000000]
+        assert row == [3, 0, -1]
