@@ -1,17 +1,24 @@
 #!/usr/bin/env python
-"""bench.py -- NeuroShard B200 hot-path benchmark (contract: DESIGN.md §Measurement).
+"""bench.py -- NeuroShard B200 hot-path benchmark (contract: DESIGN.md §8).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 
-Workload (BASELINE.json configs[1], "C2"): DLRM-style synthetic sharding tasks
-of 40 tables on 4 GPUs, table-wise greedy grid search (Alg. 2, M = 11) with a
-4 GiB memory cap.  One step = the whole hot path over one batch of tasks:
-featurise + per-table precompute (N1), cost order, greedy placement (N4),
-plan cost (N5), grid argmin (N6) -- ns_featurize_tables + ns_shard_tablewise.
+Headline workload (BASELINE.json configs[4], "C5", the largest single-GPU
+configuration; BASELINE.json quotes its metric on no particular config):
+production-scale synthetic sharding tasks of 1000 tables on 128 simulated
+GPUs, column-wise beam search (Alg. 1, N=10 K=3 L=10) around the greedy grid
+search (Alg. 2, M=11), 4 GiB cap.  One step = the whole hot path over one
+batch of tasks: featurise + per-table precompute (N1), level candidates (N3),
+cost order, greedy placement (N4), plan cost (N5), grid argmin / top-K /
+global best (N6) -- ns_featurize_tables + ns_shard_columnwise.  With N ranks
+the batch is N x --tasks tasks and every beam level's column plans are
+partitioned over the ranks (ns_comm_init: NCCL allgather of the
+per-trajectory keys, int8 allreduce-max of the winner's row, packed-key
+allreduce-min check) -- weak scaling with the collective on the data path.
 Metric: candidate-plan scores per second (one score = one evaluation of
-C(S_d + {t}) for a feasible device, Alg. 2's innermost unit, O(LKNMTD) of
-PAPER.md:291), whole job over all ranks; tasks are partitioned over ranks
-(weak scaling, no collective on the data path).
+C(S_d + {t}) for a feasible device, Alg. 2's innermost unit, the O(LKNMTD)
+count of PAPER.md:291, W as the oracle counts it), whole job; and sharding
+search time per task.
 
 Rank 0 prints ONE JSON line.
 """
@@ -35,20 +42,20 @@ sys.path.insert(0, ROOT)
 from workload.synth import CONFIGS, gen_tasks, gen_weights  # noqa: E402
 
 METRIC = "candidate plans scored/s"
-CFG = "C2"
-WORKLOAD = "C2: DLRM-style 40 synthetic tables on 4 GPUs, table-wise greedy grid search (M=11), 4 GiB cap"
+CFG = "C5"
+WORKLOAD = ("C5: production-scale synthetic, 1000 tables on 128 simulated GPUs, column-wise beam search "
+            "(N=10, K=3, L=10) + greedy grid search (M=11), 4 GiB cap")
+C2_WORKLOAD = "C2: DLRM-style 40 synthetic tables on 4 GPUs, table-wise greedy grid search (M=11), 4 GiB cap"
 
 
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=30)
-    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    # 65536 tasks per step: the grouped greedy pulls column plans from a queue
-    # (~22 per resident warp), so the partially filled last round is a small
-    # share of the step (per-task cost 14% lower than at 16384 tasks)
-    ap.add_argument("--tasks", type=int, default=65536, help="tasks per GPU per step")
+    ap.add_argument("--tasks", type=int, default=32, help="C5 tasks per GPU per step")
+    ap.add_argument("--c2-tasks", type=int, default=65536, help="C2 tasks per step (secondary)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-secondary", action="store_true")
@@ -66,7 +73,7 @@ def dist_setup(n_gpus):
         import torch.distributed as dist
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
         n_dev = torch.cuda.device_count()
-        if n_dev >= world:
+        if n_dev >= world:   # one GPU per rank: NCCL process group
             torch.cuda.set_device(local)
             dist.init_process_group("nccl", device_id=torch.device("cuda", local))
         else:
@@ -75,7 +82,7 @@ def dist_setup(n_gpus):
             local = local % max(n_dev, 1)
             torch.cuda.set_device(local)
             dist.init_process_group("gloo")
-    return world, rank, local
+    return world, rank, local, world > 1 and torch.cuda.device_count() < world
 
 
 def barrier(world):
@@ -109,6 +116,24 @@ def allreduce_sum(world, x: float) -> float:
 def rank_tasks(cfg: str, n: int, rank: int):
     """Weak scaling: rank r owns tasks [r*n, (r+1)*n) of the config (disjoint seeds)."""
     return gen_tasks(cfg, n, start=rank * n)
+
+
+def comm_setup(ns, ctx, world, rank, shared_gpu):
+    """Make the library's calls collective over the ranks: NCCL (unique id
+    from rank 0, broadcast over torch.distributed); ranks sharing one GPU
+    (a functional run on a one-GPU box; NCCL refuses duplicate devices) use
+    the host-callback transport over the gloo group instead."""
+    if world == 1:
+        return "single rank"
+    import torch.distributed as dist
+    if shared_gpu:
+        ag, ar = ns.torch_host_comm()
+        ns.ns_comm_init_host(ctx, world, rank, ag, ar)
+        return "host callbacks (gloo), ranks share a GPU"
+    obj = [ns.ns_comm_unique_id() if rank == 0 else None]
+    dist.broadcast_object_list(obj, src=0)
+    ns.ns_comm_init(ctx, world, rank, obj[0])
+    return "NCCL"
 
 
 # --------------------------------------------------------------------------- clocks
@@ -179,54 +204,120 @@ class ClockSampler:
 
 
 # --------------------------------------------------------------------------- oracle timing
-def oracle_rate(tasks, w, M, budget_s):
-    """Oracle GreedyGridSearch (fp64, literal head, cache off) on tasks until
-    budget_s elapses; returns (scores/s, scores, seconds, tasks done)."""
+def feasible_c5_tasks(n):
+    """Indices of C5 tasks whose tables all fit the cap (level 0 of the search
+    is feasible, so a greedy trajectory runs through all 1000 tables)."""
+    out, i = [], 0
+    while len(out) < n:
+        t = gen_tasks("C5", 1, start=i)[0]
+        if int((t.hash * t.dims.astype(np.int64) * 4).max()) <= t.cap:
+            out.append(i)
+        i += 1
+    return out
+
+
+def _oracle_traj(args):
+    """One grid trajectory of GreedyGridSearch (Alg. 2) of C5 task i with the
+    empty column plan, by the oracle: greedy placement at grid point m and the
+    plan cost of the completed plan.  Returns the work W (candidate scores)."""
+    i, m = args
+    import math
     from oracle import model as om, search as osr
+    c = CONFIGS["C5"]
+    task = gen_tasks("C5", 1, start=i)[0]
+    w = gen_weights(c["D"], "mono")
+    emb = _EMB_CACHE.get(i)
+    if emb is None:
+        emb = _EMB_CACHE.setdefault(i, om.TableEmbeddings(w, task))
+    tables = osr.apply_col_plan(task, [])
+    order = osr.cost_order(osr.single_costs(w, emb, tables))
+    md = osr.grid_max_dims(int(task.dims.sum()), c["D"], c["M"])[m]
+    g = osr.greedy_place(w, emb, task, tables, order, c["D"], int(math.floor(md)))
+    if g.assign is not None:
+        om.plan_cost(w, emb, tables, g.assign, c["D"])
+    return g.work
+
+
+_EMB_CACHE = {}
+
+
+def oracle_rate(budget_s, cores, tasks_idx):
+    """The oracle's candidate scores/s on C5 trajectories: single thread in
+    this process (cores == 1) or a process pool over the (task, grid point)
+    trajectories (cores > 1, the independent trajectories of a beam level,
+    SURVEY §8(d)); stops after the first batch of trajectories that passes
+    budget_s.  Returns (scores/s, scores, seconds, trajectories)."""
+    M = CONFIGS["C5"]["M"]
+    jobs = [(i, m) for i in tasks_idx for m in range(M)]
     t0 = time.perf_counter()
     W, done = 0, 0
-    for task in tasks:
-        emb = om.TableEmbeddings(w, task)
-        W += osr.greedy_grid_search(w, emb, task, [], M).work
-        done += 1
-        if time.perf_counter() - t0 > budget_s:
-            break
+    if cores == 1:
+        for j in jobs:
+            W += _oracle_traj(j)
+            done += 1
+            if time.perf_counter() - t0 > budget_s:
+                break
+    else:
+        import multiprocessing as mp
+        with mp.get_context("fork").Pool(cores) as pool:
+            for k in range(0, len(jobs), cores):
+                W += sum(pool.map(_oracle_traj, jobs[k:k + cores]))
+                done += len(jobs[k:k + cores])
+                if time.perf_counter() - t0 > budget_s:
+                    break
     dt = time.perf_counter() - t0
     return W / dt, W, dt, done
 
 
+def host_cores():
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count() or 1
+
+
 def run_reference(args, world, rank):
-    """--impl reference: the oracle as it stands, timed on the host cores."""
+    """--impl reference: the fp64 oracle as it stands, timed on the host's
+    cores.  One step = the M = 11 grid trajectories of one C5 column plan
+    (GreedyGridSearch of a feasible C5 task's level-0 plan) over a process
+    pool of all cores -- a bounded sample of the headline workload."""
     if rank != 0:
         return
-    c = CONFIGS[CFG]
-    w = gen_weights(c["D"], "mono")
-    per_step = 16
-    tasks = gen_tasks(CFG, per_step * (args.steps + args.warmup))
+    cores = host_cores()
+    idx = feasible_c5_tasks(args.steps + args.warmup)
     for s in range(args.warmup):
-        oracle_rate(tasks[s * per_step:(s + 1) * per_step], w, c["M"], 1e9)
+        oracle_rate(1e9, cores, [idx[s]])
     t0 = time.perf_counter()
     W = 0
     for s in range(args.warmup, args.warmup + args.steps):
-        W += oracle_rate(tasks[s * per_step:(s + 1) * per_step], w, c["M"], 1e9)[1]
+        W += oracle_rate(1e9, cores, [idx[s]])[1]
     dt = time.perf_counter() - t0
     v = W / dt
-    cores = 1
     line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "scores/s", "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * dt / args.steps,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": WORKLOAD, "tasks_per_step": per_step, "parallelism": "host, 1 core"},
+            "config": {"workload": WORKLOAD, "sample": "per step: the 11 grid trajectories of one C5 task's "
+                       "level-0 column plan", "parallelism": f"host, {cores} cores (process pool over trajectories)"},
             "cpu_baseline": {"value": v, "unit": "scores/s", "cores": cores, "kind": "oracle",
-                             "sample": f"{per_step} C2 tasks per step x {args.steps} steps (numpy fp64 oracle)"},
+                             "sample": f"{args.steps} steps x 11 C5 greedy trajectories (1000 tables, D = 128), "
+                                       f"{W} scores in {dt:.1f} s, numpy fp64 oracle"},
             "e2e": {"value": v, "unit": "scores/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
 
 # --------------------------------------------------------------------------- ours
+def alloc_out(torch, n, T, L, dev, pinned=False):
+    def z(shape, dt):
+        t = torch.zeros(shape, dtype=dt, device=None if pinned else dev)
+        return t.pin_memory() if pinned else t
+    return dict(cost=z(n, torch.float64), n_col=z(n, torch.int32), col_plan=z((n, max(L, 1)), torch.int32),
+                assign=z((n, T + L), torch.int8), grid_index=z(n, torch.int32), n_scores=z(n, torch.int64))
+
+
 def main():
     args = parse()
     import torch
-    world, rank, local = dist_setup(args.gpus)
+    world, rank, local, shared_gpu = dist_setup(args.gpus)
     if args.impl == "reference":
         run_reference(args, world, rank)
         return
@@ -236,41 +327,35 @@ def main():
     torch.cuda.set_device(dev)
     stream = torch.cuda.current_stream()
     ctx = ns.ns_create(dev, stream.cuda_stream)
+    comm = comm_setup(ns, ctx, world, rank, shared_gpu)
     c = CONFIGS[CFG]
-    D, M = c["D"], c["M"]
+    D, N, K, L, M = c["D"], c["N"], c["K"], c["L"], c["M"]
     w = gen_weights(D, "mono")
     ns.ns_load_cost_models(ctx, w)
-    n = args.tasks
-    tasks = rank_tasks(CFG, n, rank)          # weak scaling: own tasks per rank
+    n = args.tasks * world                    # the job's batch: every rank holds it, computes 1/world of it
+    tasks = gen_tasks(CFG, n)
     desc, off, caps = ns.table_descs(tasks)
     T = int(np.max(np.diff(off)))
-    # device-resident inputs and outputs for the `value` measurement
     d_desc = torch.from_numpy(desc.view(np.uint8)).to(f"cuda:{dev}")
-    dout = dict(cost=torch.zeros(n, dtype=torch.float64, device=dev), n_col=torch.zeros(n, dtype=torch.int32, device=dev),
-                col_plan=None, assign=torch.zeros((n, T), dtype=torch.int8, device=dev),
-                grid_index=torch.zeros(n, dtype=torch.int32, device=dev),
-                n_scores=torch.zeros(n, dtype=torch.int64, device=dev))
+    dout = alloc_out(torch, n, T, L, dev)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)   # > 126 MB L2
 
     def step(desc_in, out):
-        # NS_SEARCH_ASYNC: the call returns once the step is enqueued, so the
-        # host prepares step k+1 while the GPU runs step k (results are read
-        # after the synchronize that closes the timed region / the e2e step)
+        # NS_SEARCH_ASYNC: the call returns once the step is enqueued (with the
+        # NCCL backend the collectives are enqueued on the ctx stream too)
         tabs = ns.ns_featurize_tables(ctx, desc_in, off, caps)
-        ns.ns_shard_tablewise(ctx, tabs, D, M=M, out=out, async_=True)
+        ns.ns_shard_columnwise(ctx, tabs, D, N=N, K=K, L=L, M=M, out=out, async_=True)
         tabs.free()
 
     for _ in range(args.warmup):
         step(d_desc, dout)
     ns.ns_synchronize(ctx)
-    scores_per_step = int(dout["n_scores"].sum().item())
+    scores_per_step = int(dout["n_scores"].sum().item())     # W of the whole batch (replicated outputs)
     n_infeasible = int(torch.isinf(dout["cost"]).sum().item())
 
     # ---- timed region: K steps, L2 flushed between steps (outside the events)
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
-    # only the roofline kernel (greedy) is bracketed by events inside the timed
-    # region; the per-kernel breakdown comes from a separate profiled pass
-    ns.ns_profile(ctx, True, kinds=("greedy",))
+    ns.ns_profile(ctx, True, kinds=("greedy",))   # events around the roofline kernel only
     launches0 = ns.ns_kernel_launches(ctx)
     sampler = ClockSampler(dev) if not args.profile_run else None
     barrier(world)
@@ -282,18 +367,16 @@ def main():
         ev[k][0].record(stream)
         step(d_desc, dout)
         ev[k][1].record(stream)
-    ns.ns_synchronize(ctx)   # also reports a deferred descriptor-validation error
+    ns.ns_synchronize(ctx)
     if sampler:
         sampler.__exit__()
     barrier(world)
     launches = ns.ns_kernel_launches(ctx) - launches0
-    ms_steps = [a.elapsed_time(b) for a, b in ev]
-    ms_local = float(np.sum(ms_steps))
+    ms_local = float(np.sum([a.elapsed_time(b) for a, b in ev]))
     prof = {kd: ns.ns_profile_query(ctx, kd) for kd in ns.PROFILE_KINDS}
+    stats = ns.ns_last_stats(ctx) if hasattr(ns, "ns_last_stats") else None
     ns.ns_profile(ctx, False)
-    # per-kernel-class breakdown: the same K steps again with every class timed
-    # (events around every launch; not part of the measurement)
-    ns.ns_profile(ctx, True)
+    ns.ns_profile(ctx, True)   # per-kernel-class breakdown: a second, fully profiled pass
     for k in range(args.steps):
         flush.fill_(k & 0xff)
         step(d_desc, dout)
@@ -301,37 +384,25 @@ def main():
     prof_all = {kd: ns.ns_profile_query(ctx, kd) for kd in ns.PROFILE_KINDS}
     ns.ns_profile(ctx, False)
     ms_total = allreduce_max(world, ms_local)
-    total_scores = allreduce_sum(world, float(scores_per_step)) * args.steps
+    total_scores = float(scores_per_step) * args.steps
     value = total_scores / (ms_total * 1e-3)
 
-    # ---- e2e: the same step through the public API with HOST buffers
+    # ---- e2e: the same steps through the public API with HOST buffers
     e2e = None
     if not args.no_e2e:
         pin_desc = torch.from_numpy(desc.view(np.uint8)).pin_memory()
-        hout = dict(cost=torch.zeros(n, dtype=torch.float64).pin_memory(),
-                    n_col=torch.zeros(n, dtype=torch.int32).pin_memory(), col_plan=None,
-                    assign=torch.zeros((n, T), dtype=torch.int8).pin_memory(),
-                    grid_index=torch.zeros(n, dtype=torch.int32).pin_memory(),
-                    n_scores=torch.zeros(n, dtype=torch.int64).pin_memory())
+        hout = alloc_out(torch, n, T, L, dev, pinned=True)
         h2d = desc.nbytes + off.nbytes + caps.nbytes
-        d2h = sum(int(v.numel() * v.element_size()) for v in hout.values() if v is not None)
+        d2h = sum(int(v.numel() * v.element_size()) for v in hout.values())
         for _ in range(2):
             step(pin_desc, hout)
         ns.ns_synchronize(ctx)
         barrier(world)
         torch.cuda.synchronize()
-        # K steps back to back as a user pipelining batches would run them:
-        # every step copies its descriptors in from pinned host memory (on the
-        # library's copy stream, overlapping the previous step's kernels) and
-        # its results out to pinned host memory; one event pair on the ctx
-        # stream spans all K steps (no L2 flush inside: a step's working set,
-        # 335 MB of cached v rows, exceeds the 126 MB L2)
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a.record(stream)
         for k in range(args.steps):
             step(pin_desc, hout)
-        # the last step's result copies run on the library's copy stream:
-        # close the timed region only after ns_synchronize has drained both
         ns.ns_synchronize(ctx)
         b.record(stream)
         torch.cuda.synchronize()
@@ -340,56 +411,60 @@ def main():
         assert int(hout["n_scores"].sum()) == scores_per_step
         e2e = {"value": total_scores / (e_total * 1e-3), "unit": "scores/s", "h2d_bytes_per_step": int(h2d),
                "d2h_bytes_per_step": int(d2h), "ms_per_step": e_total / args.steps,
-               "mode": "K steps pipelined through the public API (NS_SEARCH_ASYNC), one event pair, "
-                       "pinned host descriptors in / results out every step, no L2 flush (working set > L2)"}
+               "mode": "K steps pipelined through the public API (NS_SEARCH_ASYNC), one event pair, pinned host "
+                       "descriptors in / results (cost, column plan, assignment, grid index, W) out every step"}
 
     # ---- roofline of the dominant kernel (greedy, N4): FP64-pipe bound
     g_ms, g_n = prof["greedy"]
-    g_avg_ms = g_ms / max(g_n, 1)
-    flops_per_score = 256          # 64 x (add, max, mul, add) in fp64: DADD + DFMA on the FP64 pipe
-    achieved = scores_per_step * flops_per_score / (g_avg_ms * 1e-3) / 1e12   # per launch: 1 launch / step
     clocks = sampler.summary() if sampler else {}
-    sm_max = clocks.get("sm_max_mhz") or 1965
-    peak = 148 * 64 * 2 * sm_max * 1e6 / 1e12     # 64 DFMA/clk/SM (tools/fp64_peak.cu measures ~59-64)
-    roof = {"bound": "alu", "kernel": "k_greedy_dedup<8> (N4, grouped greedy)", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
-            "frac": achieved / peak, "traffic": None, "peak_basis": "FP64 pipe: 148 SM x 64 DFMA/clk x 2 flop at "
-            f"sm_max {sm_max} MHz; flops/score = 256 (64 x add, max, mul, add)",
-            "greedy_ms_per_launch": g_avg_ms, "step_share": g_ms / max(ms_local, 1e-9)}
-    traffic = os.path.join(ROOT, "profiles", "greedy_traffic.json")
-    if os.path.exists(traffic):
-        try:
-            roof["traffic"] = json.load(open(traffic)).get("bytes_per_launch")
-        except Exception:
-            pass
+    roof = greedy_roofline(clocks, scores_per_step * args.steps, g_ms, g_n, ms_local, stats,
+                           "k_greedy_wide* (N4, D = 128 greedy)")
 
     # ---- CPU baseline: the oracle on a bounded sample (rank 0, N=1 only)
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline and not args.profile_run:
-        rate, W, dt, done = oracle_rate(gen_tasks(CFG, 2000), w, M, 12.0)
-        cpu = {"value": rate, "unit": "scores/s", "cores": 1, "kind": "oracle",
-               "sample": f"{done} C2 tasks ({W} scores) in {dt:.1f} s, numpy fp64, single thread"}
+        idx = feasible_c5_tasks(3)
+        r1, W1, dt1, n1 = oracle_rate(12.0, 1, idx[:1])
+        cores = host_cores()
+        rN, WN, dtN, nN = oracle_rate(15.0, cores, idx) if cores > 1 else (r1, W1, dt1, n1)
+        cpu = {"value": rN, "unit": "scores/s", "cores": cores, "kind": "oracle",
+               "sample": f"C5 greedy grid-search trajectories (1000 tables, D = 128, level-0 column plans of "
+                         f"feasible tasks): {nN} trajectories, {WN} scores in {dtN:.1f} s on {cores} cores "
+                         f"(process pool over trajectories)",
+               "single_core": {"value": r1, "unit": "scores/s", "cores": 1,
+                               "sample": f"{n1} trajectories, {W1} scores in {dt1:.1f} s"}}
 
-    # ---- secondary: single-task search latency (sharding search time per task)
-    secondary = None
+    # ---- secondaries
+    secondary = {}
+    lat = search_time_per_task_c5(ns, ctx, torch, world)   # collective: every rank takes part
     if rank == 0 and not args.no_secondary and not args.profile_run:
-        secondary = search_latency(ns, ctx, torch)
-        secondary["score_plans"] = score_plans_rate(ns, ctx, torch)
-        secondary["service"] = service_rate(ns)
+        ctx1 = ns.ns_create(dev, stream.cuda_stream)        # rank-0-only measurements: a non-collective ctx
+        secondary["C2_batched"] = c2_batched(ns, ctx1, torch, args)
+        secondary["latency"] = search_latency(ns, ctx1, torch)
+        secondary["score_plans"] = score_plans_rate(ns, ctx1, torch)
+        ns.ns_destroy(ctx1)
+        if world == 1:
+            secondary["service"] = service_rate(ns)
 
     if rank == 0:
+        ms_step = ms_total / args.steps
         line = {"metric": METRIC, "value": value, "unit": "scores/s", "n_gpus": world, "steps": args.steps,
-                "warmup": args.warmup, "ms_per_step": ms_total / args.steps, "higher_is_better": True,
+                "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
                 "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-                "config": {"workload": WORKLOAD, "tasks_per_gpu": n, "tables_per_task": c["T"], "devices": D, "M": M,
-                           "scores_per_step_per_gpu": scores_per_step, "infeasible_tasks": n_infeasible,
-                           "weights": "random-init W-mono (paper architecture)", "parallelism": f"tasks/{world} ranks",
+                "config": {"workload": WORKLOAD, "tasks_per_step": n, "tasks_per_gpu": args.tasks,
+                           "tables_per_task": c["T"], "devices": D, "N": N, "K": K, "L": L, "M": M,
+                           "scores_per_step": scores_per_step, "infeasible_tasks": n_infeasible,
+                           "search_ms_per_task": ms_step / n,
+                           "weights": "random-init W-mono (paper architecture)",
+                           "parallelism": f"column plans of every beam level partitioned over {world} rank(s) ({comm})",
                            "l2": "flushed between steps (256 MiB write)"},
+                "search_time_per_task": lat,
                 "gpu_launches": int(launches), "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
                 "clocks": clocks, "kernels_ms_per_step": {k: v[0] / args.steps for k, v in prof_all.items() if v[1]},
                 "kernels_ms_note": "kernels_ms_per_step: a separate pass of the same K steps with CUDA events "
-                                   "around every launch; roofline.greedy_ms_per_launch: events around the "
-                                   "greedy only, inside the timed region",
-                "secondary": secondary}
+                                   "around every launch; roofline times: events around the greedy launches only, "
+                                   "inside the timed region",
+                "secondary": secondary or None}
         print(json.dumps(line), flush=True)
     ns.ns_destroy(ctx)
     if world > 1:
@@ -397,12 +472,105 @@ def main():
         dist.destroy_process_group()
 
 
+def greedy_roofline(clocks, W, g_ms, g_n, ms_region, stats, kernel):
+    """FP64-pipe roofline of the greedy (N4): algorithmic flops = 256 per
+    candidate score (64 x add, max, mul, add; SURVEY §8(d) unit x W) over the
+    greedy's event-timed duration; the executed fraction counts the scores the
+    kernels actually computed (grouped kernels share identical trajectories'
+    scores) when the library reports them."""
+    sm_max = clocks.get("sm_max_mhz") or 1965
+    peak = 148 * 64 * 2 * sm_max * 1e6 / 1e12
+    flops_per_score = 256
+    achieved = W * flops_per_score / (g_ms * 1e-3) / 1e12 if g_ms else 0.0
+    roof = {"bound": "alu", "kernel": kernel, "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+            "frac": achieved / peak, "traffic": None,
+            "peak_basis": f"FP64 pipe: 148 SM x 64 DFMA/clk x 2 flop at sm_max {sm_max} MHz (derived from unit "
+                          "counts; tools/fp64_peak.cu measures 34.2 TFLOP/s DFMA); flops/score = 256",
+            "frac_basis": "algorithmic: W (the oracle's candidate-score count) x 256 flop / greedy time",
+            "greedy_ms_per_launch": g_ms / max(g_n, 1), "greedy_launches": g_n,
+            "step_share": g_ms / max(ms_region, 1e-9)}
+    if stats and stats.get("scores_computed"):
+        ex = stats["scores_computed"] * flops_per_score / (g_ms * 1e-3) / 1e12 * (W / max(stats["scores"], 1))
+        roof["executed_achieved"] = ex
+        roof["executed_frac"] = ex / peak
+        roof["executed_basis"] = ("scores the greedy kernels computed (ns_last_stats.scores_computed; identical "
+                                  "trajectories share scores) x 256 flop / greedy time")
+    return roof
+
+
+def search_time_per_task_c5(ns, ctx, torch, world):
+    """Sharding search time per task: wall time of featurise +
+    ns_shard_columnwise for ONE C5 task, its column plans partitioned over the
+    ranks (strong scaling of a single search), median of 5 after 1 warm-up."""
+    c = CONFIGS["C5"]
+    task = gen_tasks("C5", 1, start=feasible_c5_tasks(1)[0])   # a task whose level 0 is feasible (W > 0)
+    desc, off, caps = ns.table_descs(task)
+    times, scores = [], 0
+    for it in range(6):
+        barrier(world)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        tabs = ns.ns_featurize_tables(ctx, desc, off, caps)
+        out = ns.ns_shard_columnwise(ctx, tabs, c["D"], N=c["N"], K=c["K"], L=c["L"], M=c["M"])
+        tabs.free()
+        torch.cuda.synchronize()
+        times.append(time.perf_counter() - t0)
+        scores = int(out["n_scores"][0])
+    t = allreduce_max(world, float(np.median(times[1:])))
+    return {"config": "C5, one task", "ranks": world, "search_ms_per_task": 1e3 * t, "scores": scores,
+            "scores_per_s": scores / t}
+
+
+def c2_batched(ns, ctx, torch, args):
+    """The round-1 headline as a secondary: 65536 C2 tasks (BASELINE configs[1])
+    per step, table-wise greedy grid search, device-resident, L2 flushed."""
+    c = CONFIGS["C2"]
+    D, M = c["D"], c["M"]
+    w = gen_weights(D, "mono")
+    ns.ns_load_cost_models(ctx, w)
+    n = args.c2_tasks
+    tasks = gen_tasks("C2", n)
+    desc, off, caps = ns.table_descs(tasks)
+    T = int(np.max(np.diff(off)))
+    dev = torch.cuda.current_device()
+    d_desc = torch.from_numpy(desc.view(np.uint8)).to(f"cuda:{dev}")
+    dout = alloc_out(torch, n, T, 0, dev)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    stream = torch.cuda.current_stream()
+    ns.ns_set_stream(ctx, stream.cuda_stream)
+
+    def step():
+        tabs = ns.ns_featurize_tables(ctx, d_desc, off, caps)
+        ns.ns_shard_tablewise(ctx, tabs, D, M=M, out=dout, async_=True)
+        tabs.free()
+
+    for _ in range(3):
+        step()
+    ns.ns_synchronize(ctx)
+    W = int(dout["n_scores"].sum().item())
+    steps = 10
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
+    ns.ns_profile(ctx, True, kinds=("greedy",))
+    for k in range(steps):
+        flush.fill_(k & 0xff)
+        ev[k][0].record(stream)
+        step()
+        ev[k][1].record(stream)
+    ns.ns_synchronize(ctx)
+    ms = float(np.sum([a.elapsed_time(b) for a, b in ev]))
+    g_ms, g_n = ns.ns_profile_query(ctx, "greedy")
+    stats = ns.ns_last_stats(ctx) if hasattr(ns, "ns_last_stats") else None
+    ns.ns_profile(ctx, False)
+    roof = greedy_roofline({}, W * steps, g_ms, g_n, ms, stats, "k_greedy_dedup<8,16> (N4, grouped greedy)")
+    return {"workload": C2_WORKLOAD, "tasks_per_step": n, "scores_per_step": W, "ms_per_step": ms / steps,
+            "scores_per_s": W * steps / (ms * 1e-3), "roofline": roof}
+
+
 def search_latency(ns, ctx, torch):
     """Wall time of one ns_shard_* call for ONE task (featurise included,
     model load excluded), C2 table-wise and C3 column-wise."""
     res = {}
-    for cfg, mode in (("C1", "tablewise"), ("C2", "tablewise"), ("C3", "columnwise"), ("C4", "columnwise"),
-                      ("C5", "columnwise")):
+    for cfg, mode in (("C1", "tablewise"), ("C2", "tablewise"), ("C3", "columnwise"), ("C4", "columnwise")):
         c = CONFIGS[cfg]
         w = gen_weights(c["D"], "mono")
         ns.ns_load_cost_models(ctx, w)
@@ -456,9 +624,9 @@ def service_rate(ns):
     import gc
     import threading
     from paper_2305_01868_b200.service import ShardingService
-    c = CONFIGS[CFG]
+    c = CONFIGS["C2"]
     w = gen_weights(c["D"], "mono")
-    tasks = gen_tasks(CFG, 16384, start=1 << 20)
+    tasks = gen_tasks("C2", 16384, start=1 << 20)
     runs = []
     with ShardingService(w, c["D"], M=c["M"], max_batch=8192, max_wait_ms=5.0) as svc:
         svc.shard(tasks[:256])   # warm-up
