@@ -76,6 +76,16 @@ uint64_t ns_kernel_launches(const ns_ctx* ctx);
  * "finalize" (N5), "select" (N6), "score" (N2), "other".  Both synchronise
  * the ctx stream. */
 ns_status ns_profile(ns_ctx* ctx, int32_t enable);
+/* Work counters since the last ns_profile call (synchronises the ctx
+ * stream): scores_computed = candidate scores the greedy kernels evaluated
+ * (the grouped kernels evaluate a score once for all identical trajectories,
+ * so this is <= the algorithmic count W the plans report); trajectories =
+ * greedy trajectories launched (column plans x grid points). */
+typedef struct {
+    uint64_t scores_computed;
+    uint64_t trajectories;
+} ns_stats;
+ns_status ns_stats_query(ns_ctx* ctx, ns_stats* out);
 ns_status ns_profile_query(ns_ctx* ctx, const char* kernel, double* total_ms, uint64_t* launches);
 
 /* ------------------------------------------------------------- cost models */

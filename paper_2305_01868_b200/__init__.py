@@ -24,6 +24,7 @@ from ._native import (  # noqa: F401
     ns_destroy,
     ns_featurize_tables,
     ns_kernel_launches,
+    ns_last_stats,
     ns_load_cost_models,
     ns_profile,
     ns_profile_query,

@@ -47,6 +47,10 @@ class ns_host_comm(C.Structure):
     _fields_ = [("user", C.c_void_p), ("allgather", _ALLGATHER_FN), ("allreduce", _ALLREDUCE_FN)]
 
 
+class ns_stats(C.Structure):
+    _fields_ = [("scores_computed", C.c_uint64), ("trajectories", C.c_uint64)]
+
+
 class ns_comm_model(C.Structure):
     _fields_ = [("D", C.c_int32), ("layer", ns_linear * 5), ("start_scale", C.c_double), ("dim_scale", C.c_double)]
 
@@ -88,6 +92,7 @@ def _load():
         "ns_comm_unique_id": ([vp], C.c_int),
         "ns_comm_init": ([vp, i32, i32, vp], C.c_int),
         "ns_comm_init_host": ([vp, i32, i32, C.POINTER(ns_host_comm)], C.c_int),
+        "ns_stats_query": ([vp, C.POINTER(ns_stats)], C.c_int),
     }
     for name, (args, res) in sig.items():
         f = getattr(lib, name)
@@ -101,7 +106,7 @@ EXPORTED = ["ns_create", "ns_destroy", "ns_last_error", "ns_set_stream", "ns_syn
             "ns_profile", "ns_profile_query",
             "ns_load_cost_models", "ns_featurize_tables", "ns_tables_free", "ns_tables_single_costs",
             "ns_score_plans", "ns_shard_tablewise", "ns_shard_columnwise", "ns_comm_unique_id", "ns_comm_init",
-            "ns_comm_init_host"]
+            "ns_comm_init_host", "ns_stats_query"]
 
 
 def _check(ctx, status: int, allow_infeasible: bool = True) -> int:
@@ -164,6 +169,13 @@ def ns_profile(ctx: int, enable: bool, kinds=None) -> None:
         for k in kinds:
             mode |= 1 << (PROFILE_KINDS.index(k) + 1)
     _check(ctx, LIB.ns_profile(ctx, mode))
+
+
+def ns_last_stats(ctx: int) -> dict:
+    """Work counters since the last ns_profile call (ns_stats_query)."""
+    st = ns_stats()
+    _check(ctx, LIB.ns_stats_query(ctx, C.byref(st)))
+    return {"scores_computed": int(st.scores_computed), "trajectories": int(st.trajectories)}
 
 
 PROFILE_KINDS = ("precompute", "validate", "order", "expand", "greedy", "finalize", "select", "score", "other")

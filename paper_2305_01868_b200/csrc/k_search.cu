@@ -17,7 +17,16 @@
 #include "ns_device.cuh"
 #include "ns_internal.cuh"
 
+#ifndef NS_WIDE_TPD
+#define NS_WIDE_TPD 2   // threads per device of the large-D greedy kernels
+#endif
+#ifndef NS_WGRP_MIN_CP
+#define NS_WGRP_MIN_CP 148   // column plans per launch from which large D uses the grouped kernel
+#endif
+
 namespace ns {
+
+struct WgrpQueue;   // k_greedy_wgrp work queue counters
 
 // ======================================================================
 // Device buffers of one search call (carved from the ctx arena).
@@ -46,6 +55,15 @@ struct SearchBufs {
     int32_t* uniq;       // [n_traj] compacted list of trajectories carrying a distinct feasible plan
     int32_t* n_uniq;     // [1]
     unsigned int* next_cp;   // [1] grouped-greedy work queue
+    double* wsnap;       // large-D grouped greedy (k_greedy_wgrp): fork snapshots [S * M][wsnap_doubles]
+    bool wgrp;           // k_greedy_wgrp buffers carved
+    size_t wsnap_doubles;   // per slot
+    WgrpQueue* wq;
+    int wgrp_cp_cap;     // column plans per launch the item buffers hold (a rank's block)
+    int32_t* witem_cp;   // [S * M] fork items
+    int32_t* witem_step;
+    unsigned long long* witem_mask;
+    int32_t* witem_ready;
     double* gscratch;    // grouped greedy group states
     int8_t* ghist;       // grouped greedy group histories [gscratch_warps][M][Tpm]
     int gscratch_warps;
@@ -476,6 +494,7 @@ struct GreedyArgs {
     int32_t* devdim;
     uint8_t* feas;
     uint32_t* work;
+    unsigned long long* computed;   // ctx stats counter: scores the kernel evaluated
     HeadParams head;
 };
 
@@ -1516,7 +1535,406 @@ __global__ void __launch_bounds__(128 * TPD, TPD >= 4 ? 1 : (TPD == 2 ? 2 : 3)) 
     if (threadIdx.x == 0) {
         a.feas[tau] = alive ? 1 : 0;
         a.work[tau] = work;
+        if (work) atomicAdd(a.computed, (unsigned long long)work);   // every trajectory scores its own devices
     }
+}
+
+// Large D, throughput mode: k_greedy_wgrp -- the M grid trajectories of a
+// column plan share their scores while they make identical decisions (the
+// paper's life-long cache, as data parallelism; on C5 26-33% of the
+// algorithmic scores are distinct).  A work item is a GROUP of
+// identical trajectories of one column plan from some step on; a CTA runs it
+// with the k_greedy_wide lane layout (TPD threads per device, u_d in
+// registers, rows through the same cp.async ring), so its scores are
+// bit-identical to k_greedy_wide's:
+//  * a step scores every device that passes the memory cap and the group's
+//    largest dim cap; one CTA argmin gives (d*, x* = dim_d* + dim_t);
+//  * fast path: x* <= the group's smallest cap -> every member picks d*
+//    (each member's feasible set is nested in the largest one and holds d*);
+//  * otherwise the members split: repeatedly, the argmin under the largest
+//    remaining member cap c is taken by every remaining member whose cap
+//    admits it (nested sets again); members with no feasible device strand
+//    (R9).  The subgroup holding the largest cap continues; every other one
+//    becomes a new work item (FORK): its state (u, dim and byte sums with its
+//    own choice applied) goes to the item's snapshot slot and any CTA picks it
+//    up from the global queue (persistent CTAs; the queue also balances
+//    column plans of different lengths);
+//  * the work count W of every member (|F_m| per step, O12) comes from the
+//    group's count when every device fits the smallest cap, else from one
+//    ballot per member; it travels with the members through forks;
+//  * at the end the group's lowest member is the representative (comp,
+//    devdim) and the others point to it (dup_of), as in k_greedy_dedup.
+// Caps are non-decreasing in m (R8), so a member set's extreme caps are its
+// lowest / highest member.
+struct WgrpQueue {
+    unsigned int next;        // items claimed
+    unsigned int forks;       // items published beyond the n_cp initial ones
+    unsigned int completed;   // items finished
+    unsigned int pad;
+};
+
+struct WgrpArgs {
+    int n_cp;                  // column plans of this launch (local slots 0 .. n_cp-1) = initial items
+    int n_items;               // item capacity n_cp * M (forks <= n_cp * (M - 1))
+    WgrpQueue* q;              // zeroed before the launch
+    int32_t* item_cp;          // fork items i >= n_cp: [n_cp * M] column plan, start step, member mask
+    int32_t* item_step;
+    unsigned long long* item_mask;
+    int32_t* item_ready;       // publication flags (zeroed before the launch)
+    double* snap;              // fork snapshots, slot i - n_cp of fork item i
+    int32_t* dup_of;           // local trajectory indexing, global tau values
+    long long tau_base;        // global tau of local trajectory 0
+};
+
+template <int TPD>
+__global__ void __launch_bounds__(128 * TPD, 2) k_greedy_wgrp(const GreedyArgs a, const WgrpArgs x) {
+    constexpr int FPL = kV / TPD;
+    constexpr int SS = FPL + 2;
+    constexpr int kLook = kStages - 2;
+    constexpr int kRingW = kStages;
+    constexpr int NWM = 4 * TPD;
+    constexpr int MMAX = 64;
+    __shared__ __align__(16) double s_w[TPD][SS];
+    __shared__ __align__(16) double s_hb1[kV];
+    __shared__ __align__(16) double ring[kRingW][TPD * SS];
+    __shared__ int4 smeta[kRingW];
+    __shared__ unsigned long long s_key[2][NWM];
+    __shared__ int s_dv[2][NWM], s_cnt[2][NWM], s_xw[2][NWM];
+    __shared__ unsigned s_xmax[2][NWM];
+    __shared__ unsigned long long r_key[NWM];   // slow-path rounds
+    __shared__ int r_dv[NWM], r_xw[NWM];
+    __shared__ int s_cap[MMAX];
+    __shared__ unsigned s_work[MMAX];
+    __shared__ unsigned long long s_sub_mask[MMAX];
+    __shared__ int s_sub_dev[MMAX], s_sub_item[MMAX];
+    __shared__ int s_nsub;
+    __shared__ unsigned long long s_dead, s_remain;
+    __shared__ int s_item;
+    const int lane = threadIdx.x & 31, wi = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    const int nth = blockDim.x;
+    for (int k = threadIdx.x; k < kV; k += blockDim.x) {
+        s_w[k / FPL][k % FPL] = a.head.H2[k];
+        s_hb1[k] = a.head.hb1[k];
+    }
+    const int d = threadIdx.x / TPD, part = threadIdx.x % TPD;
+    const bool dev = d < a.D;
+    const int M = a.M;
+    const int my_slice = (2 * lane) / FPL, my_off = (2 * lane) % FPL;
+    const double2* w2 = reinterpret_cast<const double2*>(&s_w[part][0]);
+    // snapshot layout: u as [FPL][nth] doubles, then dsum, bsum [nth] --
+    // coalesced per thread index
+    const size_t snap_doubles = (size_t)nth * (FPL + 2);
+    unsigned long long computed = 0;
+    volatile unsigned int* vq = reinterpret_cast<volatile unsigned int*>(x.q);
+    volatile int32_t* vready = x.item_ready;
+    for (;;) {
+        // ---- claim the next item (waits for a fork to be published, or for the end)
+        if (threadIdx.x == 0) {
+            const int i = (int)atomicAdd(&x.q->next, 1u);
+            int got = -1;
+            if (i < x.n_cp) {
+                got = i;
+            } else if (i < x.n_items) {   // beyond n_items nothing can ever be published
+                for (;;) {
+                    if (vready[i]) {
+                        got = i;
+                        break;
+                    }
+                    // all published items finished -> nothing can be published any more
+                    const unsigned pub = (unsigned)x.n_cp + vq[1];
+                    if (vq[2] == pub && (unsigned)i >= pub) break;
+                    __nanosleep(200);
+                }
+                __threadfence();
+            }
+            s_item = got;
+        }
+        __syncthreads();
+        const int item = s_item;
+        if (item < 0) break;
+        int g, p0;
+        unsigned long long mask;
+        if (item < x.n_cp) {
+            g = item;
+            p0 = 0;
+            mask = a.cp_valid[g] ? (M >= 64 ? ~0ULL : ((1ULL << M) - 1)) : 0ULL;
+        } else {
+            // written by another CTA during this launch: read past L1
+            g = __ldcg(x.item_cp + item);
+            p0 = __ldcg(x.item_step + item);
+            mask = __ldcg(x.item_mask + item);
+        }
+        const long long tau0 = (long long)g * M;   // local trajectory index of member 0
+        const int q = a.cp_task[g];
+        const int Tp = mask ? a.cp_Tp[g] : 0;
+        const long long cap = mask ? a.cap[q] : 0;
+        for (int m = threadIdx.x; m < M; m += blockDim.x) {
+            s_cap[m] = mask ? a.capdim[q * M + m] : 0;
+            if (item < x.n_cp) {   // a column plan starts: every member unplaced, no work yet
+                s_work[m] = 0;
+                a.feas[tau0 + m] = 0;
+                x.dup_of[tau0 + m] = -1;
+                if (!mask) a.work[tau0 + m] = 0;
+            } else {
+                s_work[m] = ((mask >> m) & 1ULL) ? __ldcg(a.work + tau0 + m) : 0u;
+            }
+        }
+        double u[FPL];
+        int dsum = 0;
+        long long bsum = 0;
+        if (item < x.n_cp) {
+#pragma unroll
+            for (int k = 0; k < FPL; ++k) u[k] = s_hb1[part * FPL + k];
+        } else {
+            const double* sp = x.snap + (size_t)(item - x.n_cp) * snap_doubles;
+#pragma unroll
+            for (int k = 0; k < FPL; ++k) u[k] = __ldcg(sp + (size_t)k * nth + threadIdx.x);
+            dsum = __double2loint(__ldcg(sp + (size_t)FPL * nth + threadIdx.x));
+            bsum = __double_as_longlong(__ldcg(sp + (size_t)(FPL + 1) * nth + threadIdx.x));
+        }
+        __syncthreads();
+        const int32_t* orow = a.ord_row + (size_t)g * a.Tpm;
+        const int4* ometa = a.ord_meta + (size_t)g * a.Tpm;
+        auto stage = [&](int pp) {
+            if (pp < Tp) {
+                const int r = __ldg(orow + pp);
+                const int sl = pp % kRingW;
+                cp_async16(&ring[sl][my_slice * SS + my_off], a.V + (size_t)r * kV + 2 * lane);
+                if (lane == 0) cp_async16(smeta + sl, ometa + pp);
+            }
+        };
+        if (wi == 0)
+            for (int pp = p0; pp < p0 + kLook; ++pp) {
+                stage(pp);
+                cp_async_commit();
+            }
+        bool alive = mask != 0;
+#pragma unroll 1
+        for (int p = p0; p < Tp && alive; ++p) {
+            const int par = p & 1;
+            if (wi == 0) {
+                stage(p + kLook);
+                cp_async_commit();
+                cp_async_wait<kLook>();
+            }
+            __syncthreads();
+            const int sl = p % kRingW;
+            const int4 mt = smeta[sl];
+            const int dt = mt.x;
+            const long long bt = (long long)(((unsigned long long)(unsigned)mt.w << 32) | (unsigned)mt.z);
+            const int cmin = s_cap[__ffsll((long long)mask) - 1], cmax = s_cap[63 - __clzll((long long)mask)];
+            const bool memok = dev && (bsum + bt <= cap);
+            const int xv = dsum + dt;
+            const bool f = memok && xv <= cmax;
+            const double2* v2 = reinterpret_cast<const double2*>(&ring[sl][part * SS]);
+            double ps = 0.0;
+            if (f) {
+                double acc[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+                for (int k2 = 0; k2 < FPL / 2; ++k2) {
+                    const double2 vv = v2[k2], ww = w2[k2];
+                    acc[(2 * k2) & 3] = fma(ww.x, relu_hi(u[2 * k2] + vv.x), acc[(2 * k2) & 3]);
+                    acc[(2 * k2 + 1) & 3] = fma(ww.y, relu_hi(u[2 * k2 + 1] + vv.y), acc[(2 * k2 + 1) & 3]);
+                }
+                ps = (acc[0] + acc[1]) + (acc[2] + acc[3]);
+            }
+            const double sco = a.head.hb2 + lane_group_sum<TPD>(ps);
+            const long long sb = __double_as_longlong(sco + 0.0);
+            const unsigned long long key =
+                f ? (unsigned long long)(sb ^ ((sb >> 63) | (long long)0x8000000000000000ULL)) : ~0ULL;
+            // warp: min key (two REDUX), lowest device holding it, its x,
+            // feasible count, max x over memory-feasible devices
+            {
+                const unsigned khi = (unsigned)(key >> 32), klo = (unsigned)key;
+                const unsigned mh = __reduce_min_sync(kFull, khi);
+                const unsigned ml = __reduce_min_sync(kFull, khi == mh ? klo : 0xFFFFFFFFu);
+                const unsigned hit = __ballot_sync(kFull, f && part == 0 && khi == mh && klo == ml);
+                const unsigned bal = __ballot_sync(kFull, f && part == 0);
+                const unsigned xm = __reduce_max_sync(kFull, memok && part == 0 ? (unsigned)xv : 0u);
+                const int hl = hit ? __ffs(hit) - 1 : 0;
+                const int xw = __shfl_sync(kFull, xv, hl);
+                if (lane == 0) {
+                    s_key[par][wi] = ((unsigned long long)mh << 32) | ml;
+                    s_dv[par][wi] = wi * (32 / TPD) + hl / TPD;
+                    s_xw[par][wi] = xw;
+                    s_cnt[par][wi] = __popc(bal);
+                    s_xmax[par][wi] = xm;
+                }
+            }
+            __syncthreads();
+            int bd, xstar, cnt;
+            unsigned xmax;
+            bool none;
+            {
+                const unsigned long long k2 = lane < nw ? s_key[par][lane] : ~0ULL;
+                const unsigned khi = (unsigned)(k2 >> 32), klo = (unsigned)k2;
+                const unsigned mh = __reduce_min_sync(kFull, khi);
+                const unsigned ml = __reduce_min_sync(kFull, khi == mh ? klo : 0xFFFFFFFFu);
+                const unsigned hit = __ballot_sync(kFull, lane < nw && khi == mh && klo == ml);
+                cnt = __reduce_add_sync(kFull, lane < nw ? s_cnt[par][lane] : 0);
+                xmax = __reduce_max_sync(kFull, lane < nw ? s_xmax[par][lane] : 0u);
+                none = (mh & ml) == 0xFFFFFFFFu;
+                const int ww = hit ? __ffs(hit) - 1 : 0;
+                bd = s_dv[par][ww];
+                xstar = s_xw[par][ww];
+            }
+            if (threadIdx.x == 0) computed += (unsigned long long)cnt;
+            // ---- work W per member (O12): |F_m| = #{memory-feasible d : x_d <= cap_m}
+            if (none || xmax <= (unsigned)cmin) {
+                // every memory-feasible device fits every member's cap (or none
+                // fits even the largest): |F_m| = cnt for all members
+                for (int m = threadIdx.x; m < M; m += blockDim.x)
+                    if ((mask >> m) & 1ULL) s_work[m] += (unsigned)cnt;
+            } else {
+                for (unsigned long long mm = mask; mm; mm &= mm - 1) {
+                    const int m = __ffsll((long long)mm) - 1;
+                    const unsigned b = __ballot_sync(kFull, memok && part == 0 && xv <= s_cap[m]);
+                    if (lane == 0 && b) atomicAdd(&s_work[m], (unsigned)__popc(b));
+                }
+            }
+            if (none) {   // nothing feasible even under the largest cap: the group strands
+                alive = false;
+                break;
+            }
+            if (xstar > cmin) {
+                // ---- slow path: members split by the caps that admit the winners
+                if (threadIdx.x == 0) {
+                    unsigned long long take = 0;
+                    for (unsigned long long mm = mask; mm; mm &= mm - 1) {
+                        const int m = __ffsll((long long)mm) - 1;
+                        if (s_cap[m] >= xstar) take |= 1ULL << m;
+                    }
+                    s_nsub = 1;
+                    s_sub_mask[0] = take;
+                    s_sub_dev[0] = bd;
+                    s_remain = mask & ~take;
+                    s_dead = 0;
+                }
+                __syncthreads();
+                while (s_remain) {
+                    const unsigned long long rem = s_remain;
+                    const int c = s_cap[63 - __clzll((long long)rem)];
+                    const bool fc = f && xv <= c;
+                    const unsigned long long kc = fc ? key : ~0ULL;
+                    const unsigned khi = (unsigned)(kc >> 32), klo = (unsigned)kc;
+                    const unsigned mh = __reduce_min_sync(kFull, khi);
+                    const unsigned ml = __reduce_min_sync(kFull, khi == mh ? klo : 0xFFFFFFFFu);
+                    const unsigned hit = __ballot_sync(kFull, fc && part == 0 && khi == mh && klo == ml);
+                    const int hl = hit ? __ffs(hit) - 1 : 0;
+                    const int xw = __shfl_sync(kFull, xv, hl);
+                    if (lane == 0) {
+                        r_key[wi] = ((unsigned long long)mh << 32) | ml;
+                        r_dv[wi] = wi * (32 / TPD) + hl / TPD;
+                        r_xw[wi] = xw;
+                    }
+                    __syncthreads();
+                    if (threadIdx.x == 0) {
+                        unsigned long long bk = ~0ULL;
+                        int bdv = 0, bx = 0;
+                        for (int k = 0; k < nw; ++k)
+                            if (r_key[k] < bk) {   // strict: the lowest warp (device) keeps ties
+                                bk = r_key[k];
+                                bdv = r_dv[k];
+                                bx = r_xw[k];
+                            }
+                        if (bk == ~0ULL) {
+                            s_dead = rem;   // no feasible device under these members' caps
+                            s_remain = 0;
+                        } else {
+                            unsigned long long take = 0;
+                            for (unsigned long long mm = rem; mm; mm &= mm - 1) {
+                                const int m = __ffsll((long long)mm) - 1;
+                                if (s_cap[m] >= bx) take |= 1ULL << m;
+                            }
+                            s_sub_mask[s_nsub] = take;
+                            s_sub_dev[s_nsub] = bdv;
+                            s_nsub++;
+                            s_remain = rem & ~take;
+                        }
+                    }
+                    __syncthreads();
+                }
+                // ---- fork every subgroup but the first into a new work item
+                const int nsub = s_nsub;
+                if (threadIdx.x == 0)
+                    for (int k = 1; k < nsub; ++k) s_sub_item[k] = x.n_cp + (int)atomicAdd(&x.q->forks, 1u);
+                __syncthreads();
+                for (int k = 1; k < nsub; ++k) {
+                    const int dk = s_sub_dev[k];
+                    const int it = s_sub_item[k];
+                    double* sp = x.snap + (size_t)(it - x.n_cp) * snap_doubles;
+                    const bool mine = d == dk;
+#pragma unroll
+                    for (int k2 = 0; k2 < FPL / 2; ++k2) {
+                        const double2 vv = v2[k2];
+                        sp[(size_t)(2 * k2) * nth + threadIdx.x] = mine ? u[2 * k2] + vv.x : u[2 * k2];
+                        sp[(size_t)(2 * k2 + 1) * nth + threadIdx.x] = mine ? u[2 * k2 + 1] + vv.y : u[2 * k2 + 1];
+                    }
+                    sp[(size_t)FPL * nth + threadIdx.x] = __hiloint2double(0, mine ? dsum + dt : dsum);
+                    sp[(size_t)(FPL + 1) * nth + threadIdx.x] = __longlong_as_double(mine ? bsum + bt : bsum);
+                    const unsigned long long km = s_sub_mask[k];
+                    for (int m = threadIdx.x; m < M; m += blockDim.x)
+                        if ((km >> m) & 1ULL) {
+                            a.assign[(size_t)(tau0 + m) * a.Tpm + mt.y] = (int8_t)dk;
+                            a.work[tau0 + m] = s_work[m];   // the members' work travels with them
+                        }
+                }
+                const unsigned long long dead = s_dead;
+                for (int m = threadIdx.x; m < M; m += blockDim.x)
+                    if ((dead >> m) & 1ULL) a.work[tau0 + m] = s_work[m];   // stranded (feas stays 0)
+                __threadfence();
+                __syncthreads();
+                if (threadIdx.x == 0)
+                    for (int k = 1; k < nsub; ++k) {
+                        const int it = s_sub_item[k];
+                        x.item_cp[it] = g;
+                        x.item_step[it] = p + 1;
+                        x.item_mask[it] = s_sub_mask[k];
+                        __threadfence();
+                        atomicExch(&x.item_ready[it], 1);   // publish
+                    }
+                mask = s_sub_mask[0];
+                bd = s_sub_dev[0];
+            }
+            // ---- the group's choice
+            if (d == bd) {
+#pragma unroll
+                for (int k2 = 0; k2 < FPL / 2; ++k2) {
+                    const double2 vv = v2[k2];
+                    u[2 * k2] += vv.x;
+                    u[2 * k2 + 1] += vv.y;
+                }
+                dsum += dt;
+                bsum += bt;
+            }
+            for (int m = threadIdx.x; m < M; m += blockDim.x)
+                if ((mask >> m) & 1ULL) a.assign[(size_t)(tau0 + m) * a.Tpm + mt.y] = (int8_t)bd;
+        }
+        if (wi == 0) cp_async_wait<0>();
+        // ---- item end: members' work; representative's per-device costs, links of the others
+        for (int m = threadIdx.x; m < M; m += blockDim.x)
+            if ((mask >> m) & 1ULL) a.work[tau0 + m] = s_work[m];
+        if (alive) {
+            double acc[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+            for (int k = 0; k < FPL; ++k) acc[k & 3] = fma(s_w[part][k], relu_exact(u[k]), acc[k & 3]);
+            const double hc = a.head.hb2 + lane_group_sum<TPD>((acc[0] + acc[1]) + (acc[2] + acc[3]));
+            const int rep = __ffsll((long long)mask) - 1;
+            if (dev && part == 0) {
+                a.comp[(tau0 + rep) * a.D + d] = dsum > 0 ? hc : 0.0;   // reading R4
+                a.devdim[(tau0 + rep) * a.D + d] = dsum;
+            }
+            for (int m = threadIdx.x; m < M; m += blockDim.x)
+                if ((mask >> m) & 1ULL) {
+                    a.feas[tau0 + m] = 1;
+                    x.dup_of[tau0 + m] = m == rep ? -1 : (int32_t)(x.tau_base + tau0 + rep);
+                }
+        }
+        __threadfence();
+        __syncthreads();   // ring and shared state are reused by the next item
+        if (threadIdx.x == 0) atomicAdd(&x.q->completed, 1u);
+    }
+    if (threadIdx.x == 0 && computed) atomicAdd(a.computed, computed);
 }
 
 // ======================================================================
@@ -1872,6 +2290,15 @@ void carve(Carver& c, SearchBufs& b, OutStage& o, int Lout) {
         b.next_cp = base_counter(ctr);
     }
     b.gscratch = c.take<double>((size_t)b.gscratch_warps * b.M * b.D * kV);
+    {
+        const size_t items = b.wgrp ? (size_t)b.wgrp_cp_cap * b.M : 0;
+        b.wsnap = c.take<double>(items * b.wsnap_doubles);
+        b.wq = reinterpret_cast<WgrpQueue*>(c.take<unsigned int>(4));
+        b.witem_cp = c.take<int32_t>(items);
+        b.witem_step = c.take<int32_t>(items);
+        b.witem_mask = c.take<unsigned long long>(items);
+        b.witem_ready = c.take<int32_t>(items);
+    }
     b.ghist = c.take<int8_t>((size_t)b.gscratch_warps * b.M * b.Tpm);
     b.capdim = c.take<int32_t>((size_t)b.n_tasks * b.M);
     b.beam_plan = c.take<int32_t>((size_t)b.n_tasks * b.K * b.Lcap);
@@ -1932,7 +2359,9 @@ ns_status launch_greedy(ns_ctx* ctx, const SearchBufs& b, const ns_tables* t, lo
     a.devdim = b.devdim;
     a.feas = b.feas;
     a.work = b.work;
+    a.computed = ctx->d_stats;
     a.head = ctx->model.head;
+    ctx->trajectories += (uint64_t)(te - tb);
     const long long n = te - tb;
     int dp = 1;
     while (dp < b.D) dp <<= 1;
@@ -2032,10 +2461,42 @@ ns_status launch_greedy(ns_ctx* ctx, const SearchBufs& b, const ns_tables* t, lo
             default: return set_err(ctx, NS_ERR_INTERNAL, "bad greedy lane split");
         }
         prof_end(ctx);
+    } else if (b.wgrp &&
+               (b.greedy_mode == NS_GREEDY_GROUPED || n_cp_launch >= NS_WGRP_MIN_CP)) {
+        // large D, many column plans: grouped trajectories (k_greedy_wgrp)
+        constexpr int TPD = NS_WIDE_TPD;
+        const int threads = ((b.D * TPD + 31) / 32) * 32;
+        const long long g0 = tb / b.M, g1 = te / b.M;
+        GreedyArgs a2 = a;
+        a2.ord_row = b.ord_row + (size_t)g0 * b.Tpm;
+        a2.ord_meta = b.ord_meta + (size_t)g0 * b.Tpm;
+        a2.cp_valid = b.cp_valid + g0;
+        a2.cp_task = b.cp_task + g0;
+        a2.cp_Tp = b.cp_Tp + g0;
+        a2.assign = b.assign + (size_t)g0 * b.M * b.Tpm;
+        a2.comp = b.comp + (size_t)g0 * b.M * b.D;
+        a2.devdim = b.devdim + (size_t)g0 * b.M * b.D;
+        a2.feas = b.feas + (size_t)g0 * b.M;
+        a2.work = b.work + (size_t)g0 * b.M;
+        WgrpArgs x;
+        x.n_cp = (int)(g1 - g0);
+        x.q = b.wq;
+        x.item_cp = b.witem_cp;
+        x.item_step = b.witem_step;
+        x.item_mask = b.witem_mask;
+        x.item_ready = b.witem_ready;
+        x.snap = b.wsnap;
+        x.dup_of = b.dup_of + (size_t)g0 * b.M;
+        x.tau_base = g0 * b.M;
+        const size_t n_items = (size_t)x.n_cp * b.M;
+        x.n_items = (int)n_items;
+        NS_CUDA(ctx, cudaMemsetAsync(b.wq, 0, sizeof(WgrpQueue), ctx->stream));
+        NS_CUDA(ctx, cudaMemsetAsync(b.witem_ready, 0, n_items * sizeof(int32_t), ctx->stream));
+        const int ctas = (int)std::min<long long>((long long)n_items, (long long)ctx->sm_count * 2);
+        prof_begin(ctx, PK_GREEDY);
+        k_greedy_wgrp<TPD><<<(unsigned)ctas, threads, 0, ctx->stream>>>(a2, x);
+        prof_end(ctx);
     } else {
-#ifndef NS_WIDE_TPD
-#define NS_WIDE_TPD 2
-#endif
         constexpr int TPD = NS_WIDE_TPD;
         const int threads = ((b.D * TPD + 31) / 32) * 32;
         prof_begin(ctx, PK_GREEDY);
@@ -2223,6 +2684,14 @@ ns_status run_search(ns_ctx* ctx, const ns_tables* t, int D, const ns_search_par
         long long warps = std::min<long long>(max_cp, (long long)ctx->sm_count * W * NS_DEDUP_BLOCKS8);
         warps = std::max<long long>(W, std::min<long long>(warps, (long long)((512ull << 20) / per)));
         b.gscratch_warps = dp <= 16 ? (int)(((warps + W - 1) / W) * W) : 0;
+        // large D: fork snapshots of k_greedy_wgrp (one set of M - 1 slots per resident CTA)
+        b.wgrp = dp > 16 && b.M <= 64 && b.greedy_mode != NS_GREEDY_LANES;
+        {   // a launch covers one rank's block of column plans (level 0: tasks; beam levels: S)
+            const long long R = ctx->nranks;
+            b.wgrp_cp_cap = (int)std::max<long long>((b.n_tasks + R - 1) / R, ((long long)b.S + R - 1) / R);
+        }
+        const int nth = ((D * NS_WIDE_TPD + 31) / 32) * 32;
+        b.wsnap_doubles = (size_t)nth * (kV / NS_WIDE_TPD + 2);
     }
     OutStage o{};
     Carver probe{nullptr};

@@ -260,6 +260,11 @@ ns_status ns_create(ns_ctx** out, int cuda_device, void* cuda_stream) {
         return NS_ERR_CUDA;
     }
     cudaDeviceGetAttribute(&c->sm_count, cudaDevAttrMultiProcessorCount, cuda_device);
+    if (cudaMalloc((void**)&c->d_stats, ns::kStats * sizeof(unsigned long long)) != cudaSuccess ||
+        cudaMemset(c->d_stats, 0, ns::kStats * sizeof(unsigned long long)) != cudaSuccess) {
+        delete c;
+        return NS_ERR_NOMEM;
+    }
     // keep stream-ordered allocations (ns_tables buffers) cached in the pool
     cudaMemPool_t pool;
     if (cudaDeviceGetDefaultMemPool(&pool, cuda_device) == cudaSuccess) {
@@ -282,6 +287,7 @@ ns_status ns_destroy(ns_ctx* ctx) {
     if (ctx->pinned) cudaFreeHost(ctx->pinned);
     if (ctx->pinned_in) cudaFreeHost(ctx->pinned_in);
     if (ctx->comm_stage) cudaFreeHost(ctx->comm_stage);
+    if (ctx->d_stats) cudaFree(ctx->d_stats);
     if (ctx->pinned_in_done) cudaEventDestroy(ctx->pinned_in_done);
     if (ctx->d_async_flags) cudaFree(ctx->d_async_flags);
     if (ctx->copy_stream) {
@@ -326,6 +332,17 @@ ns_status ns_synchronize(ns_ctx* ctx) {
 
 uint64_t ns_kernel_launches(const ns_ctx* ctx) { return ctx ? ctx->launches : 0; }
 
+ns_status ns_stats_query(ns_ctx* ctx, ns_stats* out) {
+    if (!ctx || !out) return NS_ERR_ARG;
+    cudaSetDevice(ctx->device);
+    unsigned long long h[kStats];
+    NS_CUDA(ctx, cudaMemcpyAsync(h, ctx->d_stats, sizeof(h), cudaMemcpyDeviceToHost, ctx->stream));
+    NS_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+    out->scores_computed = h[0];
+    out->trajectories = ctx->trajectories;
+    return NS_OK;
+}
+
 static const char* kProfNames[PK_COUNT] = {"precompute", "validate", "order", "expand", "greedy",
                                             "finalize", "select", "score", "other"};
 
@@ -335,6 +352,8 @@ ns_status ns_profile(ns_ctx* ctx, int32_t enable) {
     NS_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
     prof_collect(ctx);
     for (int k = 0; k < PK_COUNT; ++k) ctx->prof_acc[k] = ProfEntry();
+    NS_CUDA(ctx, cudaMemsetAsync(ctx->d_stats, 0, kStats * sizeof(unsigned long long), ctx->stream));
+    ctx->trajectories = 0;
     // 1: every kernel class; > 1: bit (k + 1) times class k only (fewer
     // events inside a timed region)
     ctx->prof = enable != 0;

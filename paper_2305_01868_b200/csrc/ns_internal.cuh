@@ -23,6 +23,7 @@ constexpr int kDepth = 6;    // variant slots per table: dim, dim/2, ..., dim/32
 // needs more than kDepth variant rows; larger dims are rejected at validation.
 constexpr int kMaxDim = 4 << (kDepth - 1);
 constexpr int kMaxD = 128;   // int8 device ids
+constexpr int kStats = 4;    // device counters of ns_stats ([0] scores computed by the greedy kernels)
 constexpr int kCommW[6] = {0, 128, 64, 32, 16, 0};   // comm widths "128-64-32-16"
 
 // Head weights passed by value as a kernel parameter (lands in the constant
@@ -120,6 +121,8 @@ struct ns_ctx {
     void* nccl = nullptr;    // ncclComm_t (also with nranks == 1: ns_comm_init with an id)
     int nranks = 1, rank = 0;
     bool emulated = false;   // ns_comm_init(id == NULL): all ranks' blocks computed in-process (test hook)
+    unsigned long long* d_stats = nullptr;   // [kStats] device counters (reset by ns_profile)
+    uint64_t trajectories = 0;               // greedy trajectories launched (host count)
     bool host_comm_on = false;    // ns_comm_init_host: collectives through caller callbacks on host buffers
     ns_host_comm host_comm{};
     void* comm_stage = nullptr;   // pinned staging of the host-callback collectives

@@ -79,13 +79,16 @@ def _compare(out, i, task, w, exp, min_margin, M):
     return "certified"
 
 
+@pytest.mark.parametrize("greedy", [0, 1])
 @pytest.mark.parametrize("name", sorted(FIX))
-def test_fullsize_against_oracle_fixture(ns, ctx, name):
+def test_fullsize_against_oracle_fixture(ns, ctx, name, greedy):
+    """greedy 0 = auto (a single task: the latency kernels), 1 = the grouped
+    kernels (k_greedy_dedup for D <= 16, k_greedy_wgrp for D = 128)."""
     c = FIX[name]
     task = gen_task(c["config"], c["task_index"], T=c["T"] if c["T"] != CONFIGS[c["config"]]["T"] else None)
     assert task.T == c["T"]
     w = gen_weights(c["D"], "mono")
-    out = _run(ns, ctx, [task], w, c["mode"], c["N"], c["K"], c["L"], c["M"])
+    out = _run(ns, ctx, [task], w, c["mode"], c["N"], c["K"], c["L"], c["M"], greedy=greedy)
     how = _compare(out, 0, task, w, c["expected"], _f(c["min_margin"]), c["M"])
     assert how == "identical" or _f(c["min_margin"]) < RTOL
 
@@ -152,3 +155,27 @@ def test_near_tie_tasks_are_certified(ns, ctx):
     out = _run(ns, ctx, tasks, w, "columnwise", 4, 2, 2, 5)
     k = _oracle_check_batch(out, tasks, w, "columnwise", 4, 2, 2, 5)
     assert sum(k.values()) == len(tasks)
+
+
+@pytest.mark.parametrize("D", [40, 128])
+def test_wide_grouped_kernel_bit_identical_to_per_trajectory(ns, ctx, D):
+    """k_greedy_wgrp (identical trajectories share scores, forks on
+    divergence) against k_greedy_wide (every trajectory alone): same lane
+    layout and summation order, so every output is bit-identical -- costs,
+    assignments, grid indices, W -- on C5-shaped batches, table- and
+    column-wise, and the executed-score counter is below W."""
+    w = gen_weights(D, "mono")
+    tasks = gen_tasks("C5", 6, start=20, T=400 if D == 128 else 150, D=D)
+    for mode, kw in (("tablewise", {}), ("columnwise", dict(N=4, K=2, L=3))):
+        outs = {}
+        comp = {}
+        for g in (1, 2):
+            ns.ns_profile(ctx, True)
+            outs[g] = _run(ns, ctx, tasks, w, mode, kw.get("N", 0), kw.get("K", 0), kw.get("L", 0), 11, greedy=g)
+            comp[g] = ns.ns_last_stats(ctx)["scores_computed"]
+            ns.ns_profile(ctx, False)
+        for k in ("cost", "assign", "grid_index", "n_scores") + (("n_col", "col_plan") if mode == "columnwise" else ()):
+            assert np.array_equal(outs[1][k], outs[2][k]), (mode, k)
+        W = int(np.sum(outs[1]["n_scores"]))
+        assert comp[2] == W                    # per-trajectory kernel: executed == algorithmic
+        assert 0 < comp[1] < W                 # grouped: identical trajectories share scores
