@@ -20,6 +20,9 @@
 #ifndef NS_WIDE_TPD
 #define NS_WIDE_TPD 2   // threads per device of the large-D greedy kernels
 #endif
+#ifndef NS_WGRP_TPD
+#define NS_WGRP_TPD 2   // threads per device of k_greedy_wgrp (same scores as any TPD: block_score)
+#endif
 #ifndef NS_WGRP_MIN_CP
 #define NS_WGRP_MIN_CP 148   // column plans per launch from which large D uses the grouped kernel
 #endif
@@ -582,6 +585,56 @@ __device__ __forceinline__ void load_lane_head(const HeadParams& hp, int part, d
         w[k] = hw;
         asm volatile("" : "+d"(w[k]));
     }
+}
+
+
+// Large-D score in a lane-split-INDEPENDENT order, so k_greedy_wide (TPD = 2,
+// latency) and k_greedy_wgrp (TPD = 4, throughput) give bit-identical
+// scores: the 64 features form 4 blocks of 16; a block is summed with 4
+// accumulators (feature k of the block into accumulator k & 3) as
+// (a0 + a1) + (a2 + a3); the blocks combine as (B0 + B1) + (B2 + B3) -- one
+// local add (TPD = 2: a thread holds blocks 2p, 2p + 1) or the xor-1 shuffle
+// (TPD = 4), then the xor-2 level (block_group_sum).
+template <int FPL>
+__device__ __forceinline__ double block_score(const double (&u)[FPL], const double2* __restrict__ v2,
+                                              const double2* __restrict__ w2) {
+    double bs = 0.0;
+#pragma unroll
+    for (int b = 0; b < FPL / 16; ++b) {
+        double acc[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+        for (int k2 = 0; k2 < 8; ++k2) {
+            const double2 vv = v2[b * 8 + k2], ww = w2[b * 8 + k2];
+            acc[(2 * k2) & 3] = fma(ww.x, relu_hi(u[b * 16 + 2 * k2] + vv.x), acc[(2 * k2) & 3]);
+            acc[(2 * k2 + 1) & 3] = fma(ww.y, relu_hi(u[b * 16 + 2 * k2 + 1] + vv.y), acc[(2 * k2 + 1) & 3]);
+        }
+        const double blk = (acc[0] + acc[1]) + (acc[2] + acc[3]);
+        bs = b == 0 ? blk : bs + blk;
+    }
+    return bs;
+}
+
+// Final per-device head sum_k H2_k ReLU(u_k) in the same block order.
+template <int FPL>
+__device__ __forceinline__ double block_head(const double (&u)[FPL], const double* __restrict__ w) {
+    double bs = 0.0;
+#pragma unroll
+    for (int b = 0; b < FPL / 16; ++b) {
+        double acc[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+        for (int k = 0; k < 16; ++k) acc[k & 3] = fma(w[b * 16 + k], relu_exact(u[b * 16 + k]), acc[k & 3]);
+        const double blk = (acc[0] + acc[1]) + (acc[2] + acc[3]);
+        bs = b == 0 ? blk : bs + blk;
+    }
+    return bs;
+}
+
+// Join the TPD partial block sums of a device: xor 1 first, then xor 2.
+template <int TPD>
+__device__ __forceinline__ double block_group_sum(double x) {
+#pragma unroll
+    for (int o = 1; o < TPD; o <<= 1) x += __shfl_xor_sync(kFull, x, o);
+    return x;
 }
 
 // Staged greedy: one CTA per (column plan, chunk of grid points).  All
@@ -1446,18 +1499,8 @@ __global__ void __launch_bounds__(128 * TPD, TPD >= 4 ? 1 : (TPD == 2 ? 2 : 3)) 
         const long long bt = (long long)(((unsigned long long)(unsigned)mt.w << 32) | (unsigned)mt.z);
         const bool f = dev && (bsum + bt <= cap) && (dsum + dt <= capd);
         const double2* v2 = reinterpret_cast<const double2*>(&ring[sl][part * SS]);
-        double ps = 0.0;
-        if (f) {
-            double acc[4] = {0.0, 0.0, 0.0, 0.0};
-#pragma unroll
-            for (int k2 = 0; k2 < FPL / 2; ++k2) {
-                const double2 vv = v2[k2], ww = w2[k2];
-                acc[(2 * k2) & 3] = fma(ww.x, relu_hi(u[2 * k2] + vv.x), acc[(2 * k2) & 3]);
-                acc[(2 * k2 + 1) & 3] = fma(ww.y, relu_hi(u[2 * k2 + 1] + vv.y), acc[(2 * k2 + 1) & 3]);
-            }
-            ps = (acc[0] + acc[1]) + (acc[2] + acc[3]);
-        }
-        const double sco = a.head.hb2 + lane_group_sum<TPD>(ps);
+        const double ps = f ? block_score<FPL>(u, v2, w2) : 0.0;
+        const double sco = a.head.hb2 + block_group_sum<TPD>(ps);
 #if NS_REDUX_ARGMIN
         // order keys (see k_greedy_dedup): warp minimum by two REDUX, the
         // lowest device holding it from one ballot; then lane k takes warp
@@ -1524,10 +1567,7 @@ __global__ void __launch_bounds__(128 * TPD, TPD >= 4 ? 1 : (TPD == 2 ? 2 : 3)) 
     }
     if (wi == 0) cp_async_wait<0>();
     // final per-device cost (every lane takes part in the lane-group sum)
-    double acc[4] = {0.0, 0.0, 0.0, 0.0};
-#pragma unroll
-    for (int k = 0; k < FPL; ++k) acc[k & 3] = fma(s_w[part][k], relu_exact(u[k]), acc[k & 3]);
-    const double hc = a.head.hb2 + lane_group_sum<TPD>((acc[0] + acc[1]) + (acc[2] + acc[3]));
+    const double hc = a.head.hb2 + block_group_sum<TPD>(block_head<FPL>(u, &s_w[part][0]));
     if (dev && part == 0) {
         a.comp[tau * a.D + d] = dsum > 0 ? hc : 0.0;   // reading R4
         a.devdim[tau * a.D + d] = dsum;
@@ -1544,9 +1584,8 @@ __global__ void __launch_bounds__(128 * TPD, TPD >= 4 ? 1 : (TPD == 2 ? 2 : 3)) 
 // paper's life-long cache, as data parallelism; on C5 26-33% of the
 // algorithmic scores are distinct).  A work item is a GROUP of
 // identical trajectories of one column plan from some step on; a CTA runs it
-// with the k_greedy_wide lane layout (TPD threads per device, u_d in
-// registers, rows through the same cp.async ring), so its scores are
-// bit-identical to k_greedy_wide's:
+// with TPD threads per device (u_d in registers) and scores in the block
+// order of block_score, so its scores are bit-identical to k_greedy_wide's:
 //  * a step scores every device that passes the memory cap and the group's
 //    largest dim cap; one CTA argmin gives (d*, x* = dim_d* + dim_t);
 //  * fast path: x* <= the group's smallest cap -> every member picks d*
@@ -1559,13 +1598,17 @@ __global__ void __launch_bounds__(128 * TPD, TPD >= 4 ? 1 : (TPD == 2 ? 2 : 3)) 
 //    own choice applied) goes to the item's snapshot slot and any CTA picks it
 //    up from the global queue (persistent CTAs; the queue also balances
 //    column plans of different lengths);
-//  * the work count W of every member (|F_m| per step, O12) comes from the
-//    group's count when every device fits the smallest cap, else from one
+//  * W of every member (|F_m| per step, O12) is the group's count when every
+//    device fits the smallest cap (one register for the whole group), else one
 //    ballot per member; it travels with the members through forks;
-//  * at the end the group's lowest member is the representative (comp,
-//    devdim) and the others point to it (dup_of), as in k_greedy_dedup.
-// Caps are non-decreasing in m (R8), so a member set's extreme caps are its
-// lowest / highest member.
+//  * the assignment is written to ONE row per group (its lowest member's) and
+//    copied to the other members' rows when they leave (fork) or finish;
+//  * at the end the lowest member is the representative (comp, devdim) and
+//    the others point to it (dup_of), as in k_greedy_dedup.
+// One barrier per step: warp 0 waits for the NEXT row before the barrier that
+// publishes the warps' argmin keys (double-buffered by step parity).  Caps are
+// non-decreasing in m (R8), so a member set's extreme caps are its lowest /
+// highest member.
 struct WgrpQueue {
     unsigned int next;        // items claimed
     unsigned int forks;       // items published beyond the n_cp initial ones
@@ -1577,7 +1620,7 @@ struct WgrpArgs {
     int n_cp;                  // column plans of this launch (local slots 0 .. n_cp-1) = initial items
     int n_items;               // item capacity n_cp * M (forks <= n_cp * (M - 1))
     WgrpQueue* q;              // zeroed before the launch
-    int32_t* item_cp;          // fork items i >= n_cp: [n_cp * M] column plan, start step, member mask
+    int32_t* item_cp;          // fork items i >= n_cp: column plan, start step, member mask
     int32_t* item_step;
     unsigned long long* item_mask;
     int32_t* item_ready;       // publication flags (zeroed before the launch)
@@ -1627,6 +1670,13 @@ __global__ void __launch_bounds__(128 * TPD, 2) k_greedy_wgrp(const GreedyArgs a
     unsigned long long computed = 0;
     volatile unsigned int* vq = reinterpret_cast<volatile unsigned int*>(x.q);
     volatile int32_t* vready = x.item_ready;
+    // copy assignment row src -> dst (list positions [0, n)); rows written by
+    // other CTAs are read past L1
+    auto copy_row = [&](long long src, long long dst, int n) {
+        const int8_t* sp = a.assign + (size_t)src * a.Tpm;
+        int8_t* dp = a.assign + (size_t)dst * a.Tpm;
+        for (int i = threadIdx.x; i < n; i += nth) dp[i] = __ldcg(sp + i);
+    };
     for (;;) {
         // ---- claim the next item (waits for a fork to be published, or for the end)
         if (threadIdx.x == 0) {
@@ -1692,7 +1742,6 @@ __global__ void __launch_bounds__(128 * TPD, 2) k_greedy_wgrp(const GreedyArgs a
             dsum = __double2loint(__ldcg(sp + (size_t)FPL * nth + threadIdx.x));
             bsum = __double_as_longlong(__ldcg(sp + (size_t)(FPL + 1) * nth + threadIdx.x));
         }
-        __syncthreads();
         const int32_t* orow = a.ord_row + (size_t)g * a.Tpm;
         const int4* ometa = a.ord_meta + (size_t)g * a.Tpm;
         auto stage = [&](int pp) {
@@ -1703,21 +1752,20 @@ __global__ void __launch_bounds__(128 * TPD, 2) k_greedy_wgrp(const GreedyArgs a
                 if (lane == 0) cp_async16(smeta + sl, ometa + pp);
             }
         };
-        if (wi == 0)
+        if (wi == 0) {
             for (int pp = p0; pp < p0 + kLook; ++pp) {
                 stage(pp);
                 cp_async_commit();
             }
+            cp_async_wait<kLook - 1>();   // row p0 landed
+        }
+        __syncthreads();
+        unsigned gw = 0;                  // work common to every member of the group (this item)
+        int rep = mask ? __ffsll((long long)mask) - 1 : 0;   // the row holding the group's history
         bool alive = mask != 0;
 #pragma unroll 1
-        for (int p = p0; p < Tp && alive; ++p) {
+        for (int p = p0; p < Tp; ++p) {
             const int par = p & 1;
-            if (wi == 0) {
-                stage(p + kLook);
-                cp_async_commit();
-                cp_async_wait<kLook>();
-            }
-            __syncthreads();
             const int sl = p % kRingW;
             const int4 mt = smeta[sl];
             const int dt = mt.x;
@@ -1727,18 +1775,8 @@ __global__ void __launch_bounds__(128 * TPD, 2) k_greedy_wgrp(const GreedyArgs a
             const int xv = dsum + dt;
             const bool f = memok && xv <= cmax;
             const double2* v2 = reinterpret_cast<const double2*>(&ring[sl][part * SS]);
-            double ps = 0.0;
-            if (f) {
-                double acc[4] = {0.0, 0.0, 0.0, 0.0};
-#pragma unroll
-                for (int k2 = 0; k2 < FPL / 2; ++k2) {
-                    const double2 vv = v2[k2], ww = w2[k2];
-                    acc[(2 * k2) & 3] = fma(ww.x, relu_hi(u[2 * k2] + vv.x), acc[(2 * k2) & 3]);
-                    acc[(2 * k2 + 1) & 3] = fma(ww.y, relu_hi(u[2 * k2 + 1] + vv.y), acc[(2 * k2 + 1) & 3]);
-                }
-                ps = (acc[0] + acc[1]) + (acc[2] + acc[3]);
-            }
-            const double sco = a.head.hb2 + lane_group_sum<TPD>(ps);
+            const double ps = f ? block_score<FPL>(u, v2, w2) : 0.0;
+            const double sco = a.head.hb2 + block_group_sum<TPD>(ps);
             const long long sb = __double_as_longlong(sco + 0.0);
             const unsigned long long key =
                 f ? (unsigned long long)(sb ^ ((sb >> 63) | (long long)0x8000000000000000ULL)) : ~0ULL;
@@ -1761,6 +1799,11 @@ __global__ void __launch_bounds__(128 * TPD, 2) k_greedy_wgrp(const GreedyArgs a
                     s_xmax[par][wi] = xm;
                 }
             }
+            if (wi == 0) {   // the next row lands before the barrier (its slot was last read at p - 2)
+                stage(p + kLook);
+                cp_async_commit();
+                cp_async_wait<kLook - 1>();
+            }
             __syncthreads();
             int bd, xstar, cnt;
             unsigned xmax;
@@ -1778,13 +1821,10 @@ __global__ void __launch_bounds__(128 * TPD, 2) k_greedy_wgrp(const GreedyArgs a
                 bd = s_dv[par][ww];
                 xstar = s_xw[par][ww];
             }
-            if (threadIdx.x == 0) computed += (unsigned long long)cnt;
+            computed += (unsigned long long)cnt;
             // ---- work W per member (O12): |F_m| = #{memory-feasible d : x_d <= cap_m}
             if (none || xmax <= (unsigned)cmin) {
-                // every memory-feasible device fits every member's cap (or none
-                // fits even the largest): |F_m| = cnt for all members
-                for (int m = threadIdx.x; m < M; m += blockDim.x)
-                    if ((mask >> m) & 1ULL) s_work[m] += (unsigned)cnt;
+                gw += (unsigned)cnt;   // every member: |F_m| = cnt
             } else {
                 for (unsigned long long mm = mask; mm; mm &= mm - 1) {
                     const int m = __ffsll((long long)mm) - 1;
@@ -1798,6 +1838,7 @@ __global__ void __launch_bounds__(128 * TPD, 2) k_greedy_wgrp(const GreedyArgs a
             }
             if (xstar > cmin) {
                 // ---- slow path: members split by the caps that admit the winners
+                __syncthreads();   // per-member work atomics done
                 if (threadIdx.x == 0) {
                     unsigned long long take = 0;
                     for (unsigned long long mm = mask; mm; mm &= mm - 1) {
@@ -1872,16 +1913,28 @@ __global__ void __launch_bounds__(128 * TPD, 2) k_greedy_wgrp(const GreedyArgs a
                     }
                     sp[(size_t)FPL * nth + threadIdx.x] = __hiloint2double(0, mine ? dsum + dt : dsum);
                     sp[(size_t)(FPL + 1) * nth + threadIdx.x] = __longlong_as_double(mine ? bsum + bt : bsum);
+                    // the subgroup's history row: the group's history so far + its choice
                     const unsigned long long km = s_sub_mask[k];
+                    const int krep = __ffsll((long long)km) - 1;
+                    copy_row(tau0 + rep, tau0 + krep, Tp);
                     for (int m = threadIdx.x; m < M; m += blockDim.x)
-                        if ((km >> m) & 1ULL) {
-                            a.assign[(size_t)(tau0 + m) * a.Tpm + mt.y] = (int8_t)dk;
-                            a.work[tau0 + m] = s_work[m];   // the members' work travels with them
-                        }
+                        if ((km >> m) & 1ULL) a.work[tau0 + m] = s_work[m] + gw;   // work travels with the members
                 }
                 const unsigned long long dead = s_dead;
                 for (int m = threadIdx.x; m < M; m += blockDim.x)
-                    if ((dead >> m) & 1ULL) a.work[tau0 + m] = s_work[m];   // stranded (feas stays 0)
+                    if ((dead >> m) & 1ULL) a.work[tau0 + m] = s_work[m] + gw;   // stranded (feas stays 0)
+                __syncthreads();   // row copies done before the choices below land in them
+                if (threadIdx.x < nsub && threadIdx.x > 0) {
+                    const unsigned long long km = s_sub_mask[threadIdx.x];
+                    a.assign[(size_t)(tau0 + __ffsll((long long)km) - 1) * a.Tpm + mt.y] = (int8_t)s_sub_dev[threadIdx.x];
+                }
+                mask = s_sub_mask[0];
+                bd = s_sub_dev[0];
+                const int nrep = __ffsll((long long)mask) - 1;
+                if (nrep != rep) {
+                    copy_row(tau0 + rep, tau0 + nrep, Tp);
+                    rep = nrep;
+                }
                 __threadfence();
                 __syncthreads();
                 if (threadIdx.x == 0)
@@ -1893,8 +1946,6 @@ __global__ void __launch_bounds__(128 * TPD, 2) k_greedy_wgrp(const GreedyArgs a
                         __threadfence();
                         atomicExch(&x.item_ready[it], 1);   // publish
                     }
-                mask = s_sub_mask[0];
-                bd = s_sub_dev[0];
             }
             // ---- the group's choice
             if (d == bd) {
@@ -1907,19 +1958,15 @@ __global__ void __launch_bounds__(128 * TPD, 2) k_greedy_wgrp(const GreedyArgs a
                 dsum += dt;
                 bsum += bt;
             }
-            for (int m = threadIdx.x; m < M; m += blockDim.x)
-                if ((mask >> m) & 1ULL) a.assign[(size_t)(tau0 + m) * a.Tpm + mt.y] = (int8_t)bd;
+            if (threadIdx.x == 0) a.assign[(size_t)(tau0 + rep) * a.Tpm + mt.y] = (int8_t)bd;
         }
         if (wi == 0) cp_async_wait<0>();
-        // ---- item end: members' work; representative's per-device costs, links of the others
+        __syncthreads();   // the representative row is complete
+        // ---- item end: members' work and rows; representative's per-device costs, links of the others
         for (int m = threadIdx.x; m < M; m += blockDim.x)
-            if ((mask >> m) & 1ULL) a.work[tau0 + m] = s_work[m];
+            if ((mask >> m) & 1ULL) a.work[tau0 + m] = s_work[m] + gw;
         if (alive) {
-            double acc[4] = {0.0, 0.0, 0.0, 0.0};
-#pragma unroll
-            for (int k = 0; k < FPL; ++k) acc[k & 3] = fma(s_w[part][k], relu_exact(u[k]), acc[k & 3]);
-            const double hc = a.head.hb2 + lane_group_sum<TPD>((acc[0] + acc[1]) + (acc[2] + acc[3]));
-            const int rep = __ffsll((long long)mask) - 1;
+            const double hc = a.head.hb2 + block_group_sum<TPD>(block_head<FPL>(u, &s_w[part][0]));
             if (dev && part == 0) {
                 a.comp[(tau0 + rep) * a.D + d] = dsum > 0 ? hc : 0.0;   // reading R4
                 a.devdim[(tau0 + rep) * a.D + d] = dsum;
@@ -1929,6 +1976,8 @@ __global__ void __launch_bounds__(128 * TPD, 2) k_greedy_wgrp(const GreedyArgs a
                     a.feas[tau0 + m] = 1;
                     x.dup_of[tau0 + m] = m == rep ? -1 : (int32_t)(x.tau_base + tau0 + rep);
                 }
+            for (unsigned long long mm = mask & ~(1ULL << rep); mm; mm &= mm - 1)
+                copy_row(tau0 + rep, tau0 + __ffsll((long long)mm) - 1, Tp);
         }
         __threadfence();
         __syncthreads();   // ring and shared state are reused by the next item
@@ -2464,7 +2513,7 @@ ns_status launch_greedy(ns_ctx* ctx, const SearchBufs& b, const ns_tables* t, lo
     } else if (b.wgrp &&
                (b.greedy_mode == NS_GREEDY_GROUPED || n_cp_launch >= NS_WGRP_MIN_CP)) {
         // large D, many column plans: grouped trajectories (k_greedy_wgrp)
-        constexpr int TPD = NS_WIDE_TPD;
+        constexpr int TPD = NS_WGRP_TPD;
         const int threads = ((b.D * TPD + 31) / 32) * 32;
         const long long g0 = tb / b.M, g1 = te / b.M;
         GreedyArgs a2 = a;
@@ -2690,8 +2739,8 @@ ns_status run_search(ns_ctx* ctx, const ns_tables* t, int D, const ns_search_par
             const long long R = ctx->nranks;
             b.wgrp_cp_cap = (int)std::max<long long>((b.n_tasks + R - 1) / R, ((long long)b.S + R - 1) / R);
         }
-        const int nth = ((D * NS_WIDE_TPD + 31) / 32) * 32;
-        b.wsnap_doubles = (size_t)nth * (kV / NS_WIDE_TPD + 2);
+        const int nth = ((D * NS_WGRP_TPD + 31) / 32) * 32;
+        b.wsnap_doubles = (size_t)nth * (kV / NS_WGRP_TPD + 2);
     }
     OutStage o{};
     Carver probe{nullptr};

@@ -27,7 +27,8 @@ for n in [int(a) for a in sys.argv[1:]] or [1, 4, 16]:
             ns.ns_profile(ctx, True)
         torch.cuda.synchronize()
         t0 = time.perf_counter()
-        out = ns.ns_shard_columnwise(ctx, tabs, c["D"], N=c["N"], K=c["K"], L=c["L"], M=c["M"])
+        out = ns.ns_shard_columnwise(ctx, tabs, c["D"], N=c["N"], K=c["K"], L=c["L"], M=c["M"],
+                                     greedy=int(os.environ.get("GREEDY", "0")))
         torch.cuda.synchronize()
         dt = time.perf_counter() - t0
         tabs.free()
