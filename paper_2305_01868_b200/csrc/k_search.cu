@@ -23,6 +23,9 @@
 #ifndef NS_WGRP_TPD
 #define NS_WGRP_TPD 2   // threads per device of k_greedy_wgrp (same scores as any TPD: block_score)
 #endif
+#ifndef NS_WGRP_CTAS
+#define NS_WGRP_CTAS 2   // resident CTAs per SM of k_greedy_wgrp (launch bounds and persistent grid)
+#endif
 #ifndef NS_WGRP_MIN_CP
 #define NS_WGRP_MIN_CP 148   // column plans per launch from which large D uses the grouped kernel
 #endif
@@ -1630,7 +1633,7 @@ struct WgrpArgs {
 };
 
 template <int TPD>
-__global__ void __launch_bounds__(128 * TPD, 2) k_greedy_wgrp(const GreedyArgs a, const WgrpArgs x) {
+__global__ void __launch_bounds__(128 * TPD, NS_WGRP_CTAS) k_greedy_wgrp(const GreedyArgs a, const WgrpArgs x) {
     constexpr int FPL = kV / TPD;
     constexpr int SS = FPL + 2;
     constexpr int kLook = kStages - 2;
@@ -1642,7 +1645,7 @@ __global__ void __launch_bounds__(128 * TPD, 2) k_greedy_wgrp(const GreedyArgs a
     __shared__ __align__(16) double ring[kRingW][TPD * SS];
     __shared__ int4 smeta[kRingW];
     __shared__ unsigned long long s_key[2][NWM];
-    __shared__ int s_dv[2][NWM], s_cnt[2][NWM], s_xw[2][NWM];
+    __shared__ int s_dv[2][NWM], s_xw[2][NWM];
     __shared__ unsigned s_xmax[2][NWM];
     __shared__ unsigned long long r_key[NWM];   // slow-path rounds
     __shared__ int r_dv[NWM], r_xw[NWM];
@@ -1676,6 +1679,15 @@ __global__ void __launch_bounds__(128 * TPD, 2) k_greedy_wgrp(const GreedyArgs a
         const int8_t* sp = a.assign + (size_t)src * a.Tpm;
         int8_t* dp = a.assign + (size_t)dst * a.Tpm;
         for (int i = threadIdx.x; i < n; i += nth) dp[i] = __ldcg(sp + i);
+    };
+    // sum of cf over the CTA (every member's common work |F_max| summed over the steps so far)
+    auto block_sum = [&](unsigned v) -> unsigned {
+        v = __reduce_add_sync(kFull, v);
+        if (lane == 0) r_xw[wi] = (int)v;
+        __syncthreads();
+        unsigned t = __reduce_add_sync(kFull, lane < nw ? (unsigned)r_xw[lane] : 0u);
+        __syncthreads();
+        return t;
     };
     for (;;) {
         // ---- claim the next item (waits for a fork to be published, or for the end)
@@ -1760,7 +1772,7 @@ __global__ void __launch_bounds__(128 * TPD, 2) k_greedy_wgrp(const GreedyArgs a
             cp_async_wait<kLook - 1>();   // row p0 landed
         }
         __syncthreads();
-        unsigned gw = 0;                  // work common to every member of the group (this item)
+        unsigned cf = 0;                  // steps this thread's device was scored (part 0 threads)
         int rep = mask ? __ffsll((long long)mask) - 1 : 0;   // the row holding the group's history
         bool alive = mask != 0;
 #pragma unroll 1
@@ -1787,15 +1799,13 @@ __global__ void __launch_bounds__(128 * TPD, 2) k_greedy_wgrp(const GreedyArgs a
                 const unsigned mh = __reduce_min_sync(kFull, khi);
                 const unsigned ml = __reduce_min_sync(kFull, khi == mh ? klo : 0xFFFFFFFFu);
                 const unsigned hit = __ballot_sync(kFull, f && part == 0 && khi == mh && klo == ml);
-                const unsigned bal = __ballot_sync(kFull, f && part == 0);
-                const unsigned xm = __reduce_max_sync(kFull, memok && part == 0 ? (unsigned)xv : 0u);
+                const unsigned xm = __reduce_max_sync(kFull, f && part == 0 ? (unsigned)xv : 0u);
                 const int hl = hit ? __ffs(hit) - 1 : 0;
                 const int xw = __shfl_sync(kFull, xv, hl);
                 if (lane == 0) {
                     s_key[par][wi] = ((unsigned long long)mh << 32) | ml;
                     s_dv[par][wi] = wi * (32 / TPD) + hl / TPD;
                     s_xw[par][wi] = xw;
-                    s_cnt[par][wi] = __popc(bal);
                     s_xmax[par][wi] = xm;
                 }
             }
@@ -1805,7 +1815,7 @@ __global__ void __launch_bounds__(128 * TPD, 2) k_greedy_wgrp(const GreedyArgs a
                 cp_async_wait<kLook - 1>();
             }
             __syncthreads();
-            int bd, xstar, cnt;
+            int bd, xstar;
             unsigned xmax;
             bool none;
             {
@@ -1814,22 +1824,23 @@ __global__ void __launch_bounds__(128 * TPD, 2) k_greedy_wgrp(const GreedyArgs a
                 const unsigned mh = __reduce_min_sync(kFull, khi);
                 const unsigned ml = __reduce_min_sync(kFull, khi == mh ? klo : 0xFFFFFFFFu);
                 const unsigned hit = __ballot_sync(kFull, lane < nw && khi == mh && klo == ml);
-                cnt = __reduce_add_sync(kFull, lane < nw ? s_cnt[par][lane] : 0);
                 xmax = __reduce_max_sync(kFull, lane < nw ? s_xmax[par][lane] : 0u);
                 none = (mh & ml) == 0xFFFFFFFFu;
                 const int ww = hit ? __ffs(hit) - 1 : 0;
                 bd = s_dv[par][ww];
                 xstar = s_xw[par][ww];
             }
-            computed += (unsigned long long)cnt;
             // ---- work W per member (O12): |F_m| = #{memory-feasible d : x_d <= cap_m}
-            if (none || xmax <= (unsigned)cmin) {
-                gw += (unsigned)cnt;   // every member: |F_m| = cnt
-            } else {
+            // = |F_max| (this thread's device counts in cf) minus the devices
+            // with cap_m < x_d <= cap_max, counted only for the members whose
+            // cap is below the largest feasible x (xmax)
+            cf += (f && part == 0) ? 1u : 0u;
+            if (xmax > (unsigned)cmin) {
                 for (unsigned long long mm = mask; mm; mm &= mm - 1) {
                     const int m = __ffsll((long long)mm) - 1;
-                    const unsigned b = __ballot_sync(kFull, memok && part == 0 && xv <= s_cap[m]);
-                    if (lane == 0 && b) atomicAdd(&s_work[m], (unsigned)__popc(b));
+                    if ((unsigned)s_cap[m] >= xmax) break;   // caps non-decreasing in m
+                    const unsigned b = __ballot_sync(kFull, f && part == 0 && xv > s_cap[m]);
+                    if (lane == 0 && b) atomicSub(&s_work[m], (unsigned)__popc(b));
                 }
             }
             if (none) {   // nothing feasible even under the largest cap: the group strands
@@ -1897,6 +1908,7 @@ __global__ void __launch_bounds__(128 * TPD, 2) k_greedy_wgrp(const GreedyArgs a
                 }
                 // ---- fork every subgroup but the first into a new work item
                 const int nsub = s_nsub;
+                const unsigned gw = block_sum(cf);
                 if (threadIdx.x == 0)
                     for (int k = 1; k < nsub; ++k) s_sub_item[k] = x.n_cp + (int)atomicAdd(&x.q->forks, 1u);
                 __syncthreads();
@@ -1962,6 +1974,8 @@ __global__ void __launch_bounds__(128 * TPD, 2) k_greedy_wgrp(const GreedyArgs a
         }
         if (wi == 0) cp_async_wait<0>();
         __syncthreads();   // the representative row is complete
+        const unsigned gw = block_sum(cf);
+        computed += gw;
         // ---- item end: members' work and rows; representative's per-device costs, links of the others
         for (int m = threadIdx.x; m < M; m += blockDim.x)
             if ((mask >> m) & 1ULL) a.work[tau0 + m] = s_work[m] + gw;
@@ -2541,7 +2555,7 @@ ns_status launch_greedy(ns_ctx* ctx, const SearchBufs& b, const ns_tables* t, lo
         x.n_items = (int)n_items;
         NS_CUDA(ctx, cudaMemsetAsync(b.wq, 0, sizeof(WgrpQueue), ctx->stream));
         NS_CUDA(ctx, cudaMemsetAsync(b.witem_ready, 0, n_items * sizeof(int32_t), ctx->stream));
-        const int ctas = (int)std::min<long long>((long long)n_items, (long long)ctx->sm_count * 2);
+        const int ctas = (int)std::min<long long>((long long)n_items, (long long)ctx->sm_count * NS_WGRP_CTAS);
         prof_begin(ctx, PK_GREEDY);
         k_greedy_wgrp<TPD><<<(unsigned)ctas, threads, 0, ctx->stream>>>(a2, x);
         prof_end(ctx);
