@@ -442,6 +442,7 @@ def main():
         secondary["C2_batched"] = c2_batched(ns, ctx1, torch, args)
         secondary["latency"] = search_latency(ns, ctx1, torch)
         secondary["score_plans"] = score_plans_rate(ns, ctx1, torch)
+        secondary["pretrain"] = pretrain_rate(ns, ctx1, torch)
         ns.ns_destroy(ctx1)
         if world == 1:
             secondary["service"] = service_rate(ns)
@@ -718,3 +719,89 @@ def score_plans_rate(ns, ctx, torch):
 
 if __name__ == "__main__":
     main()
+
+
+def pretrain_rate(ns, ctx, torch):
+    """pre-training throughput on the GPU.  App. F's recipe
+    (PAPER.md:788-789): 100K samples per model, batch 512, Adam lr 1e-3;
+    compute-model combinations of 1-15 tables from the 856-table pool
+    augmented with {4..128} (Alg. 3-4), comm samples of 20-120 tables on 8
+    GPUs (Alg. 5).  Reports sample generation (features + labels) and Adam
+    steps per second (fused forward/backward + reduce/Adam kernels, fp64),
+    with the executed FP64 rate against the FP64 pipe peak."""
+    from workload.pretrain_synth import AUG_DIMS, gen_combinations, gen_placement_draws, gen_pool, init_params
+    from oracle.pretrain import COMPUTE_WIDTHS, comm_widths  # shapes only (layer widths)
+    pool = gen_pool(856)
+    desc = np.zeros(pool.n, dtype=ns.TABLE_DESC)
+    desc["dim"], desc["hash_size"], desc["pooling_factor"], desc["skew"] = pool.dims, pool.hash, pool.pooling, pool.skew
+    pd = torch.from_numpy(desc.view(np.uint8)).cuda()
+    ad = torch.tensor(AUG_DIMS, dtype=torch.int32, device="cuda")
+    n = 100_000
+    off, idx = gen_combinations(pool.n * len(AUG_DIMS), n, 1, 15)
+    off_d, idx_d = torch.from_numpy(off).cuda(), torch.from_numpy(idx).cuda()
+    feats = torch.zeros((len(idx), 5), dtype=torch.float64, device="cuda")
+    labels = torch.zeros(n, dtype=torch.float64, device="cuda")
+    ev = lambda: torch.cuda.Event(enable_timing=True)   # noqa: E731
+    a, b = ev(), ev()
+    ns.ns_pretrain_compute_samples(ctx, pd, ad, off_d, idx_d, feats, labels)
+    a.record()
+    ns.ns_pretrain_compute_samples(ctx, pd, ad, off_d, idx_d, feats, labels)
+    b.record()
+    torch.cuda.synchronize()
+    gen_ms = a.elapsed_time(b)
+    res = {"samples": n, "compute_samples_gen_ms": gen_ms}
+    B, steps = 512, 200
+    rng = np.random.default_rng(0)
+    perm = torch.from_numpy(np.concatenate([rng.permutation(n) for _ in range(2)]).astype(np.int32)).cuda()
+    th = torch.from_numpy(init_params(COMPUTE_WIDTHS, seed=1)).cuda()
+    m, v = torch.zeros_like(th), torch.zeros_like(th)
+    loss = torch.zeros(1, dtype=torch.float64, device="cuda")
+    maxrows = int(np.max(np.diff(off)))
+    rows_per_sample = float(len(idx)) / n
+    for t in range(1, 11):
+        ns.ns_pretrain_compute_step(ctx, th, m, v, t, 1e-3, feats, off_d, labels, perm[t * B:(t + 1) * B], maxrows, loss)
+    a.record()
+    for t in range(11, 11 + steps):
+        ns.ns_pretrain_compute_step(ctx, th, m, v, t, 1e-3, feats, off_d, labels, perm[t * B:(t + 1) * B], maxrows, loss)
+    b.record()
+    torch.cuda.synchronize()
+    ms = a.elapsed_time(b) / steps
+    # MACs per sample: encoder row forward 5*128 + 128*32, backward dW2 + dh1 + dW1 = 4096 + 4096 + 640;
+    # head forward 32*64 + 64, backward dH1 + dS + dH2 = 2048 + 2048 + 64
+    mac = rows_per_sample * (640 + 4096 + 4096 + 4096 + 640) + (2048 + 64 + 2048 + 2048 + 64)
+    fp64_peak = 148 * 64 * 2 * 1965e6
+    res["compute_model"] = {"batch": B, "ms_per_step": ms, "samples_per_s": B / (ms * 1e-3),
+                            "tflops_fp64": B * mac * 2 / (ms * 1e-3) / 1e12,
+                            "frac_fp64_pipe": B * mac * 2 / (ms * 1e-3) / fp64_peak,
+                            "epoch_s_100k": n / B * ms * 1e-3, "loss_after": float(loss.item())}
+    D = 8
+    dr = gen_placement_draws(pool.n * len(AUG_DIMS), n, D, 20, 120)
+    tt = lambda q: torch.from_numpy(np.ascontiguousarray(q)).cuda()   # noqa: E731
+    x = torch.zeros((n, 2 * D), dtype=torch.float64, device="cuda")
+    yf, yb = torch.zeros((n, D), dtype=torch.float64, device="cuda"), torch.zeros((n, D), dtype=torch.float64,
+                                                                                   device="cuda")
+    asg = torch.full((int(dr.off[-1]),), -1, dtype=torch.int8, device="cuda")
+    valid = torch.zeros(n, dtype=torch.uint8, device="cuda")
+    args = [tt(dr.off), tt(dr.idx), tt(dr.p), tt(dr.u), tt(dr.r), tt(dr.starts)]
+    ns.ns_pretrain_comm_samples(ctx, pd, ad, D, 4 << 30, *args, x, yf, yb, asg, valid)
+    a.record()
+    ns.ns_pretrain_comm_samples(ctx, pd, ad, D, 4 << 30, *args, x, yf, yb, asg, valid)
+    b.record()
+    torch.cuda.synchronize()
+    res["comm_samples_gen_ms"] = a.elapsed_time(b)
+    res["comm_valid_frac"] = float(valid.float().mean().item())
+    th = torch.from_numpy(init_params(comm_widths(D), seed=2)).cuda()
+    m, v = torch.zeros_like(th), torch.zeros_like(th)
+    for t in range(1, 11):
+        ns.ns_pretrain_comm_step(ctx, D, th, m, v, t, 1e-3, x, yf, perm[t * B:(t + 1) * B], loss)
+    a.record()
+    for t in range(11, 11 + steps):
+        ns.ns_pretrain_comm_step(ctx, D, th, m, v, t, 1e-3, x, yf, perm[t * B:(t + 1) * B], loss)
+    b.record()
+    torch.cuda.synchronize()
+    ms = a.elapsed_time(b) / steps
+    cmac = sum(i * o for i, o in comm_widths(D)) * 3
+    res["comm_model_fwd_D8"] = {"batch": B, "ms_per_step": ms, "samples_per_s": B / (ms * 1e-3),
+                                "tflops_fp64": B * cmac * 2 / (ms * 1e-3) / 1e12,
+                                "frac_fp64_pipe": B * cmac * 2 / (ms * 1e-3) / fp64_peak}
+    return res

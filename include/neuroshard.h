@@ -253,6 +253,56 @@ ns_status ns_shard_tablewise(ns_ctx* ctx, const ns_tables* tables, int32_t D,
 ns_status ns_shard_columnwise(ns_ctx* ctx, const ns_tables* tables, int32_t D,
                               const ns_search_params* params, ns_plan_batch* out);
 
+/* ------------------------------------------------------------ pre-training */
+/* generate cost samples and train the cost models on
+ * the GPU (§3.1-3.2, App. B Alg. 3-5, App. C, App. F).  Every
+ * pointer is DEVICE memory (the datasets live in HBM; NS_ERR_ARG otherwise);
+ * work is enqueued on the ctx stream.  Random numbers are inputs: the caller
+ * draws Alg. 4's combinations, Alg. 5's subsets and its uniforms.
+ *
+ * Augmented tables (Alg. 3): augmented table a is pool table
+ * a / n_dims with dimension aug_dims[a % n_dims] (App. F: {4,...,128}).
+ * Labels: SPEC.md's analytic cost model stands in for the
+ * paper's GPU micro-benchmarks (reading F2-L in DESIGN.md).
+ *
+ * ns_pretrain_compute_samples: combination s (Alg. 4) = augmented tables
+ *   comb_idx[comb_off[s] .. comb_off[s+1]); writes the R1 features of every
+ *   table ([rows][5]) and the label launch + sum_t(gamma*overhead + work(t))
+ *   (one table: launch + overhead + work) ([n]).
+ * ns_pretrain_comm_samples: placement s (Alg. 5) of the augmented tables
+ *   idx[off[s] .. off[s+1]) (at most 256) on D devices with per-device memory
+ *   cap mem_cap: tables sorted by descending dimension (stable); table k of
+ *   that order goes, if u[off[s]+k] <= p[s], to the memory-feasible device with
+ *   the lowest device dimension (lowest index on ties), else to the
+ *   floor(r[off[s]+k] * |feasible|)-th feasible device; no feasible device ->
+ *   valid_out[s] = 0 (reading F2-P).  assign_out [rows] (per sampled table),
+ *   x_out [n][2D] = [starts/20, devdim/1024] (reading R10 scaling), yf_out /
+ *   yb_out [n][D] = per-device forward / backward comm labels from the
+ *   starts [n][D] (ms) and device dims.
+ * ns_pretrain_compute_step / ns_pretrain_comm_step: one Adam step (torch
+ *   defaults, lr as given: P:789) of the MSE loss (mean over the batch; comm:
+ *   over batch x D) of the computation model (theta: 7073 fp64, per layer W
+ *   [out][in] then b: enc 5->128, 128->32, head 32->64, 64->1) or a comm model
+ *   (2D->128->64->32->16->D) on the samples batch[0..B) (indices into the
+ *   sample arrays; max_rows = the largest combination, <= 64).  t is the
+ *   1-based Adam step (bias correction).  theta, adam_m, adam_v are updated in
+ *   place; *loss_out (device, may be NULL) receives the batch loss before the
+ *   update.  Deterministic (fixed reduction order, no atomics). */
+ns_status ns_pretrain_compute_samples(ns_ctx* ctx, const ns_table_desc* pool, int32_t n_pool,
+                                      const int32_t* aug_dims, int32_t n_dims, const int32_t* comb_off,
+                                      const int32_t* comb_idx, int32_t n, double* feats_out, double* labels_out);
+ns_status ns_pretrain_comm_samples(ns_ctx* ctx, const ns_table_desc* pool, int32_t n_pool, const int32_t* aug_dims,
+                                   int32_t n_dims, int32_t D, int64_t mem_cap, const int32_t* off, const int32_t* idx,
+                                   const double* p, const double* u, const double* r, const double* starts,
+                                   int32_t n, double* x_out, double* yf_out, double* yb_out, int8_t* assign_out,
+                                   uint8_t* valid_out);
+ns_status ns_pretrain_compute_step(ns_ctx* ctx, double* theta, double* adam_m, double* adam_v, int64_t t, double lr,
+                                   const double* feats, const int32_t* off, const double* labels,
+                                   const int32_t* batch, int32_t B, int32_t max_rows, double* loss_out);
+ns_status ns_pretrain_comm_step(ns_ctx* ctx, int32_t D, double* theta, double* adam_m, double* adam_v, int64_t t,
+                                double lr, const double* x, const double* y, const int32_t* batch, int32_t B,
+                                double* loss_out);
+
 /* ------------------------------------------------------------ multi-GPU */
 /* 128-byte NCCL unique id (call on rank 0, broadcast by any means). */
 ns_status ns_comm_unique_id(unsigned char id_out[128]);

@@ -27,6 +27,10 @@ from ._native import (  # noqa: F401
     ns_last_stats,
     ns_load_cost_models,
     ns_profile,
+    ns_pretrain_comm_samples,
+    ns_pretrain_comm_step,
+    ns_pretrain_compute_samples,
+    ns_pretrain_compute_step,
     ns_profile_query,
     PROFILE_KINDS,
     ns_score_plans,

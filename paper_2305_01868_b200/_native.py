@@ -93,6 +93,11 @@ def _load():
         "ns_comm_init": ([vp, i32, i32, vp], C.c_int),
         "ns_comm_init_host": ([vp, i32, i32, C.POINTER(ns_host_comm)], C.c_int),
         "ns_stats_query": ([vp, C.POINTER(ns_stats)], C.c_int),
+        "ns_pretrain_compute_samples": ([vp, vp, i32, vp, i32, vp, vp, i32, vp, vp], C.c_int),
+        "ns_pretrain_comm_samples": ([vp, vp, i32, vp, i32, i32, i64, vp, vp, vp, vp, vp, vp, i32, vp, vp, vp, vp,
+                                      vp], C.c_int),
+        "ns_pretrain_compute_step": ([vp, vp, vp, vp, i64, C.c_double, vp, vp, vp, vp, i32, i32, vp], C.c_int),
+        "ns_pretrain_comm_step": ([vp, i32, vp, vp, vp, i64, C.c_double, vp, vp, vp, i32, vp], C.c_int),
     }
     for name, (args, res) in sig.items():
         f = getattr(lib, name)
@@ -106,7 +111,8 @@ EXPORTED = ["ns_create", "ns_destroy", "ns_last_error", "ns_set_stream", "ns_syn
             "ns_profile", "ns_profile_query",
             "ns_load_cost_models", "ns_featurize_tables", "ns_tables_free", "ns_tables_single_costs",
             "ns_score_plans", "ns_shard_tablewise", "ns_shard_columnwise", "ns_comm_unique_id", "ns_comm_init",
-            "ns_comm_init_host", "ns_stats_query"]
+            "ns_comm_init_host", "ns_stats_query", "ns_pretrain_compute_samples", "ns_pretrain_comm_samples",
+            "ns_pretrain_compute_step", "ns_pretrain_comm_step"]
 
 
 def _check(ctx, status: int, allow_infeasible: bool = True) -> int:
@@ -408,3 +414,41 @@ def torch_host_comm(group=None):
             buf[:] = v.numpy().astype(np.int8)
 
     return allgather, allreduce
+
+
+# ----------------------------------------------------------------- pre-training (F2)
+def _dp(t):
+    """Device pointer of a CUDA torch tensor (marshalling only)."""
+    if t is None:
+        return None
+    if not t.is_cuda:
+        raise ValueError("pre-training buffers must be CUDA tensors")
+    return t.data_ptr()
+
+
+def ns_pretrain_compute_samples(ctx: int, pool_desc, aug_dims, comb_off, comb_idx, feats_out, labels_out) -> None:
+    """Alg. 4 samples: features [rows][5] and labels [n] (device tensors)."""
+    n_pool = pool_desc.numel() // TABLE_DESC.itemsize
+    _check(ctx, LIB.ns_pretrain_compute_samples(ctx, _dp(pool_desc), n_pool, _dp(aug_dims), aug_dims.numel(),
+                                                _dp(comb_off), _dp(comb_idx), comb_off.numel() - 1, _dp(feats_out),
+                                                _dp(labels_out)))
+
+
+def ns_pretrain_comm_samples(ctx: int, pool_desc, aug_dims, D: int, mem_cap: int, off, idx, p, u, r, starts,
+                             x_out, yf_out, yb_out, assign_out, valid_out) -> None:
+    """Alg. 5 placements and their comm labels (device tensors)."""
+    n_pool = pool_desc.numel() // TABLE_DESC.itemsize
+    _check(ctx, LIB.ns_pretrain_comm_samples(ctx, _dp(pool_desc), n_pool, _dp(aug_dims), aug_dims.numel(), D, mem_cap,
+                                             _dp(off), _dp(idx), _dp(p), _dp(u), _dp(r), _dp(starts), off.numel() - 1,
+                                             _dp(x_out), _dp(yf_out), _dp(yb_out), _dp(assign_out), _dp(valid_out)))
+
+
+def ns_pretrain_compute_step(ctx: int, theta, m, v, t: int, lr: float, feats, off, labels, batch, max_rows: int,
+                             loss_out=None) -> None:
+    _check(ctx, LIB.ns_pretrain_compute_step(ctx, _dp(theta), _dp(m), _dp(v), t, lr, _dp(feats), _dp(off),
+                                             _dp(labels), _dp(batch), batch.numel(), max_rows, _dp(loss_out)))
+
+
+def ns_pretrain_comm_step(ctx: int, D: int, theta, m, v, t: int, lr: float, x, y, batch, loss_out=None) -> None:
+    _check(ctx, LIB.ns_pretrain_comm_step(ctx, D, _dp(theta), _dp(m), _dp(v), t, lr, _dp(x), _dp(y), _dp(batch),
+                                          batch.numel(), _dp(loss_out)))
