@@ -443,6 +443,7 @@ def main():
         secondary["latency"] = search_latency(ns, ctx1, torch)
         secondary["score_plans"] = score_plans_rate(ns, ctx1, torch)
         secondary["pretrain"] = pretrain_rate(ns, ctx1, torch)
+        secondary["embedding_bag"] = embag_rate(ns, ctx1, torch)
         ns.ns_destroy(ctx1)
         if world == 1:
             secondary["service"] = service_rate(ns)
@@ -805,3 +806,70 @@ def pretrain_rate(ns, ctx, torch):
                                 "tflops_fp64": B * cmac * 2 / (ms * 1e-3) / 1e12,
                                 "frac_fp64_pipe": B * cmac * 2 / (ms * 1e-3) / fp64_peak}
     return res
+
+
+def embag_rate(ns, ctx, torch):
+    """SURVEY §8(f) F3 (single-GPU half): the computation cost of one
+    device's shard measured the paper's way (App. A.2, PAPER.md:594-600:
+    10 warm-ups, median of 100) with the fused embedding-bag kernels.  The
+    shard is the device-0 tables of the best plan the search returns for a C2
+    task (batch 65536 as the paper's dataset; bag lengths
+    ~ Poisson(pooling factor), Zipf-like indices with the table's skew).
+    HBM roofline: algorithmic bytes = gathered / scattered rows + indices +
+    offsets + output (forward) or output gradient (backward), against
+    MEASURED_PEAKS hbm_gbs; rows repeated across bags (Zipf-hot) are served
+    from L2, so this can exceed the DRAM traffic."""
+    from workload.pretrain_synth import gen_bag_indices
+    c = CONFIGS["C2"]
+    w = gen_weights(c["D"], "mono")
+    ns.ns_load_cost_models(ctx, w)
+    task = gen_tasks("C2", 1, start=7)[0]
+    desc, off, caps = ns.table_descs([task])
+    tabs = ns.ns_featurize_tables(ctx, desc, off, caps)
+    plan = ns.ns_shard_tablewise(ctx, tabs, c["D"], M=c["M"])
+    tabs.free()
+    mine = [k for k in range(task.T) if plan["assign"][0, k] == 0]
+    B = 65536
+    rng = np.random.default_rng(1)
+    shard, algo_f, algo_b = [], 0, 0
+    gen = torch.Generator("cuda").manual_seed(0)
+    for k in mine:
+        rows, dim = int(task.hash[k]), int(task.dims[k])
+        W = torch.randn((rows, dim), device="cuda", generator=gen, dtype=torch.float32).mul_(0.01)
+        o, i = gen_bag_indices(rows, float(task.pooling[k]), float(task.skew[k]), B, rng)
+        shard.append((W, torch.from_numpy(i).cuda(), torch.from_numpy(o).cuda()))
+        algo_f += len(i) * (dim * 4 + 8) + (B + 1) * 4 + B * dim * 4
+        algo_b += len(i) * (dim * 4 * 2 + 8) + (B + 1) * 4 + B * dim * 4
+    C = sum(int(task.dims[k]) for k in mine)
+    out = torch.zeros((B, C), dtype=torch.float32, device="cuda")
+    gout = torch.randn((B, C), device="cuda", generator=gen).mul_(1e-3)
+
+    def med(fn):
+        for _ in range(10):
+            fn()
+        ts = []
+        for _ in range(100):
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record()
+            fn()
+            b.record()
+            torch.cuda.synchronize()
+            ts.append(a.elapsed_time(b))
+        return float(np.median(ts))
+
+    fwd = med(lambda: ns.ns_embedding_bag_forward(ctx, shard, B, out))
+    bwd = med(lambda: ns.ns_embedding_bag_backward_sgd(ctx, shard, B, gout, 1e-4))
+    peaks = {}
+    try:
+        peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        pass
+    hbm = peaks.get("hbm_gbs", 6650.0)
+    return {"shard": f"device 0 of the C2 task's plan: {len(mine)} tables, dims {[int(task.dims[k]) for k in mine]}, "
+                     f"{sum(int(task.hash[k]) * int(task.dims[k]) * 4 for k in mine) / 2**30:.2f} GiB of fp32 rows",
+            "batch": B, "forward_ms_median": fwd, "backward_sgd_ms_median": bwd,
+            "cost_ms": fwd + bwd,
+            "forward_gbs": algo_f / (fwd * 1e-3) / 1e9, "backward_gbs": algo_b / (bwd * 1e-3) / 1e9,
+            "forward_frac_hbm": algo_f / (fwd * 1e-3) / 1e9 / hbm,
+            "backward_frac_hbm": algo_b / (bwd * 1e-3) / 1e9 / hbm,
+            "hbm_peak_gbs": hbm, "protocol": "10 warm-ups, median of 100 (PAPER.md:596)"}

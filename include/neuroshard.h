@@ -303,6 +303,36 @@ ns_status ns_pretrain_comm_step(ns_ctx* ctx, int32_t D, double* theta, double* a
                                 double lr, const double* x, const double* y, const int32_t* batch, int32_t B,
                                 double* loss_out);
 
+/* ------------------------------------------------------------ real-cost evaluator */
+/* SURVEY §8(f) row F3, single-GPU half: the computation cost of a device's
+ * shard measured by running its fused embedding-bag operation (PAPER.md:391
+ * "real costs", App. A.2: forward + backward, FBGEMM
+ * table-batched embeddings).  One launch covers all n_tables tables of the
+ * shard (table-batched).  Every buffer is DEVICE memory:
+ *   weights  [rows][dim] fp32 (4 bytes per element, reading R7), dim % 4 == 0, <= 128
+ *   offsets  [batch + 1] int32: bag b of this table = indices[offsets[b] .. offsets[b+1])
+ *   indices  int64 row ids in [0, rows) (not checked on the device); may be NULL
+ *            when every bag of the table is empty
+ * ns_embedding_bag_forward: out[b][col_t + j] = sum_{i in bag(b, t)} W_t[i][j]
+ *   (sum pooling, fp32 accumulation in index order), out [batch][sum_t dim_t],
+ *   tables' columns in argument order.
+ * ns_embedding_bag_backward_sgd: the SGD update fused into the backward
+ *   (as FBGEMM fuses the optimizer): W_t[i] -= lr * grad_out[b][col_t ...] for
+ *   every occurrence of row i in bag (b, t).  Repeated rows accumulate with
+ *   fp32 atomics (order not fixed: last-bit nondeterminism). */
+typedef struct {
+    int32_t dim;
+    int32_t reserved;
+    int64_t rows;
+    float* weights;
+    const int64_t* indices;
+    const int32_t* offsets;
+} ns_bag_table;
+ns_status ns_embedding_bag_forward(ns_ctx* ctx, const ns_bag_table* tables, int32_t n_tables, int32_t batch,
+                                   float* out);
+ns_status ns_embedding_bag_backward_sgd(ns_ctx* ctx, const ns_bag_table* tables, int32_t n_tables, int32_t batch,
+                                        const float* grad_out, float lr);
+
 /* ------------------------------------------------------------ multi-GPU */
 /* 128-byte NCCL unique id (call on rank 0, broadcast by any means). */
 ns_status ns_comm_unique_id(unsigned char id_out[128]);

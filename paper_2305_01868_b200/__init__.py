@@ -22,6 +22,8 @@ from ._native import (  # noqa: F401
     ns_comm_unique_id,
     ns_create,
     ns_destroy,
+    ns_embedding_bag_backward_sgd,
+    ns_embedding_bag_forward,
     ns_featurize_tables,
     ns_kernel_launches,
     ns_last_stats,

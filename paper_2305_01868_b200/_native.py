@@ -51,6 +51,11 @@ class ns_stats(C.Structure):
     _fields_ = [("scores_computed", C.c_uint64), ("trajectories", C.c_uint64)]
 
 
+class ns_bag_table(C.Structure):
+    _fields_ = [("dim", C.c_int32), ("reserved", C.c_int32), ("rows", C.c_int64), ("weights", C.c_void_p),
+                ("indices", C.c_void_p), ("offsets", C.c_void_p)]
+
+
 class ns_comm_model(C.Structure):
     _fields_ = [("D", C.c_int32), ("layer", ns_linear * 5), ("start_scale", C.c_double), ("dim_scale", C.c_double)]
 
@@ -98,6 +103,8 @@ def _load():
                                       vp], C.c_int),
         "ns_pretrain_compute_step": ([vp, vp, vp, vp, i64, C.c_double, vp, vp, vp, vp, i32, i32, vp], C.c_int),
         "ns_pretrain_comm_step": ([vp, i32, vp, vp, vp, i64, C.c_double, vp, vp, vp, i32, vp], C.c_int),
+        "ns_embedding_bag_forward": ([vp, C.POINTER(ns_bag_table), i32, i32, vp], C.c_int),
+        "ns_embedding_bag_backward_sgd": ([vp, C.POINTER(ns_bag_table), i32, i32, vp, C.c_float], C.c_int),
     }
     for name, (args, res) in sig.items():
         f = getattr(lib, name)
@@ -112,7 +119,8 @@ EXPORTED = ["ns_create", "ns_destroy", "ns_last_error", "ns_set_stream", "ns_syn
             "ns_load_cost_models", "ns_featurize_tables", "ns_tables_free", "ns_tables_single_costs",
             "ns_score_plans", "ns_shard_tablewise", "ns_shard_columnwise", "ns_comm_unique_id", "ns_comm_init",
             "ns_comm_init_host", "ns_stats_query", "ns_pretrain_compute_samples", "ns_pretrain_comm_samples",
-            "ns_pretrain_compute_step", "ns_pretrain_comm_step"]
+            "ns_pretrain_compute_step", "ns_pretrain_comm_step", "ns_embedding_bag_forward",
+            "ns_embedding_bag_backward_sgd"]
 
 
 def _check(ctx, status: int, allow_infeasible: bool = True) -> int:
@@ -452,3 +460,23 @@ def ns_pretrain_compute_step(ctx: int, theta, m, v, t: int, lr: float, feats, of
 def ns_pretrain_comm_step(ctx: int, D: int, theta, m, v, t: int, lr: float, x, y, batch, loss_out=None) -> None:
     _check(ctx, LIB.ns_pretrain_comm_step(ctx, D, _dp(theta), _dp(m), _dp(v), t, lr, _dp(x), _dp(y), _dp(batch),
                                           batch.numel(), _dp(loss_out)))
+
+
+# ----------------------------------------------------------------- real-cost evaluator (F3)
+def _bag_tables(tables):
+    """tables: sequence of (weights [rows][dim] f32, indices i64, offsets i32) CUDA tensors."""
+    arr = (ns_bag_table * len(tables))()
+    for k, (W, idx, off) in enumerate(tables):
+        arr[k] = ns_bag_table(int(W.shape[1]), 0, int(W.shape[0]), _dp(W), _dp(idx) if idx.numel() else None,
+                              _dp(off))
+    return arr
+
+
+def ns_embedding_bag_forward(ctx: int, tables, batch: int, out) -> None:
+    arr = _bag_tables(tables)
+    _check(ctx, LIB.ns_embedding_bag_forward(ctx, arr, len(tables), batch, _dp(out)))
+
+
+def ns_embedding_bag_backward_sgd(ctx: int, tables, batch: int, grad_out, lr: float) -> None:
+    arr = _bag_tables(tables)
+    _check(ctx, LIB.ns_embedding_bag_backward_sgd(ctx, arr, len(tables), batch, _dp(grad_out), lr))

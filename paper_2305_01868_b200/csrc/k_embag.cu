@@ -1,0 +1,200 @@
+// k_embag.cu -- SURVEY §8(f) row F3 (single-GPU half): the real-cost
+// evaluator's computation side.  The paper measures a device's computation
+// cost by running the fused embedding-bag operation of the tables placed on
+// it, forward and backward, 10 warm-ups then the median of 100 runs
+// (App. A.2; FBGEMM table-batched embeddings).
+//
+// B200 design (HBM-bound gathers):
+//  * table-batched: one launch covers every table of the shard; a device-side
+//    descriptor array gives each table's weights (fp32 [rows][dim], reading
+//    R7's 4 bytes per element), bag offsets and indices;
+//  * forward (sum pooling): a "bag group" of dim/4 lanes owns one bag
+//    (sample b, table t) and streams its rows as 16-byte vectors (one 128-bit
+//    load per lane per row: a 512-byte row of a dim-128 table is one
+//    coalesced warp access), 4 rows in flight per lane; 32 / (dim/4) bags per
+//    warp; the pooled vector goes straight to out[b][col_t ...];
+//  * backward + SGD (the optimizer fused into the backward, as FBGEMM does):
+//    each bag's output gradient is loaded once and -lr * grad is added to
+//    every row the bag gathered with one 16-byte vector atomic
+//    (red.global.add.v4.f32, sm_90+) per lane and row -- no sort, no
+//    gradient buffer; rows repeated across bags (Zipf-hot rows) accumulate
+//    in L2.  The summation order of repeated rows is not fixed (fp32
+//    atomics), so parity is checked against an error bound, not bit-exactly.
+//  * work items: a persistent grid strides over (table, bag-group) items, the
+//    tables' items concatenated (per-table item offsets).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <vector>
+
+#include "ns_internal.cuh"
+
+namespace ns {
+namespace {
+
+struct BagTab {
+    float* W;              // [rows][dim]
+    const int64_t* idx;    // [offsets[B]]
+    const int32_t* off;    // [B + 1]
+    long long rows;
+    int dim, col;          // dimension, first output column
+    int lanes, bpw;        // lanes per bag (dim / 4), bags per warp (32 / lanes)
+    long long item0;       // first warp item of this table
+};
+
+__device__ __forceinline__ int find_table(const BagTab* tabs, int n, long long item) {
+    int lo = 0, hi = n - 1;
+    while (lo < hi) {   // last table with item0 <= item
+        const int mid = (lo + hi + 1) >> 1;
+        if (tabs[mid].item0 <= item) lo = mid;
+        else hi = mid - 1;
+    }
+    return lo;
+}
+
+__global__ void __launch_bounds__(256) k_bag_forward(const BagTab* __restrict__ tabs, int n_tabs, long long n_items,
+                                                     int B, int out_ld, float* __restrict__ out) {
+    const int lane = threadIdx.x & 31;
+    const long long warps = ((long long)gridDim.x * blockDim.x) >> 5;
+    for (long long it = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5; it < n_items; it += warps) {
+        const int t = find_table(tabs, n_tabs, it);
+        const BagTab tb = tabs[t];
+        const int g = lane / tb.lanes, l = lane % tb.lanes;
+        const long long b = (it - tb.item0) * tb.bpw + g;
+        if (g >= tb.bpw || b >= B) continue;
+        const int i0 = tb.off[b], i1 = tb.off[b + 1];
+        float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+        int i = i0;
+        for (; i + 4 <= i1; i += 4) {   // 4 rows in flight
+            const long long r0 = __ldg(tb.idx + i), r1 = __ldg(tb.idx + i + 1), r2 = __ldg(tb.idx + i + 2),
+                            r3 = __ldg(tb.idx + i + 3);
+            const float4 a0 = __ldg(reinterpret_cast<const float4*>(tb.W + r0 * tb.dim) + l);
+            const float4 a1 = __ldg(reinterpret_cast<const float4*>(tb.W + r1 * tb.dim) + l);
+            const float4 a2 = __ldg(reinterpret_cast<const float4*>(tb.W + r2 * tb.dim) + l);
+            const float4 a3 = __ldg(reinterpret_cast<const float4*>(tb.W + r3 * tb.dim) + l);
+            acc.x += a0.x; acc.y += a0.y; acc.z += a0.z; acc.w += a0.w;
+            acc.x += a1.x; acc.y += a1.y; acc.z += a1.z; acc.w += a1.w;
+            acc.x += a2.x; acc.y += a2.y; acc.z += a2.z; acc.w += a2.w;
+            acc.x += a3.x; acc.y += a3.y; acc.z += a3.z; acc.w += a3.w;
+        }
+        for (; i < i1; ++i) {
+            const long long r = __ldg(tb.idx + i);
+            const float4 a = __ldg(reinterpret_cast<const float4*>(tb.W + r * tb.dim) + l);
+            acc.x += a.x; acc.y += a.y; acc.z += a.z; acc.w += a.w;
+        }
+        reinterpret_cast<float4*>(out + (size_t)b * out_ld + tb.col)[l] = acc;
+    }
+}
+
+__global__ void __launch_bounds__(256) k_bag_backward_sgd(const BagTab* __restrict__ tabs, int n_tabs,
+                                                          long long n_items, int B, int out_ld,
+                                                          const float* __restrict__ gout, float lr) {
+    const int lane = threadIdx.x & 31;
+    const long long warps = ((long long)gridDim.x * blockDim.x) >> 5;
+    for (long long it = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5; it < n_items; it += warps) {
+        const int t = find_table(tabs, n_tabs, it);
+        const BagTab tb = tabs[t];
+        const int g = lane / tb.lanes, l = lane % tb.lanes;
+        const long long b = (it - tb.item0) * tb.bpw + g;
+        if (g >= tb.bpw || b >= B) continue;
+        float4 gv = __ldg(reinterpret_cast<const float4*>(gout + (size_t)b * out_ld + tb.col) + l);
+        gv.x *= -lr; gv.y *= -lr; gv.z *= -lr; gv.w *= -lr;
+        const int i0 = tb.off[b], i1 = tb.off[b + 1];
+        for (int i = i0; i < i1; ++i) {
+            const long long r = __ldg(tb.idx + i);
+            atomicAdd(reinterpret_cast<float4*>(tb.W + r * tb.dim) + l, gv);   // red.global.add.v4.f32
+        }
+    }
+}
+
+struct BagPlan {
+    std::vector<BagTab> tabs;
+    long long items = 0;
+    int out_ld = 0;
+};
+
+ns_status plan_bags(ns_ctx* ctx, const ns_bag_table* t, int n, int B, BagPlan& p) {
+    p.tabs.resize(n);
+    int col = 0;
+    for (int k = 0; k < n; ++k) {
+        const ns_bag_table& s = t[k];
+        if (!s.weights || !s.offsets || s.rows < 1 || s.dim < 4 || s.dim > kMaxDim || s.dim % 4 != 0)
+            return set_err(ctx, NS_ERR_ARG, "ns_embedding_bag: table " + std::to_string(k) +
+                                                " needs weights, offsets, rows >= 1, dim % 4 == 0 <= 128");
+        // indices may be NULL when every bag of the table is empty
+        if (!is_device_ptr(s.weights) || (s.indices && !is_device_ptr(s.indices)) || !is_device_ptr(s.offsets))
+            return set_err(ctx, NS_ERR_ARG, "ns_embedding_bag: table buffers must be device memory");
+        BagTab& b = p.tabs[k];
+        b.W = s.weights;
+        b.idx = s.indices;
+        b.off = s.offsets;
+        b.rows = s.rows;
+        b.dim = s.dim;
+        b.col = col;
+        b.lanes = s.dim / 4;
+        b.bpw = 32 / b.lanes;
+        b.item0 = p.items;
+        p.items += (B + b.bpw - 1) / b.bpw;
+        col += s.dim;
+    }
+    p.out_ld = col;
+    return NS_OK;
+}
+
+// descriptor array -> device (pageable source: the copy is staged before the call returns)
+ns_status upload(ns_ctx* ctx, const BagPlan& p, BagTab** d) {
+    const size_t bytes = p.tabs.size() * sizeof(BagTab);
+    char* a = (char*)arena_get(ctx, bytes + 256);
+    if (!a) return set_err(ctx, NS_ERR_NOMEM, "ns_embedding_bag descriptors");
+    NS_CUDA(ctx, cudaMemcpyAsync(a, p.tabs.data(), bytes, cudaMemcpyHostToDevice, ctx->stream));
+    *d = (BagTab*)a;
+    return NS_OK;
+}
+
+}  // namespace
+}  // namespace ns
+
+using namespace ns;
+
+extern "C" {
+
+ns_status ns_embedding_bag_forward(ns_ctx* ctx, const ns_bag_table* tables, int32_t n_tables, int32_t batch,
+                                   float* out) {
+    if (!ctx) return NS_ERR_ARG;
+    if (!tables || n_tables < 1 || batch < 1 || !out) return set_err(ctx, NS_ERR_ARG, "ns_embedding_bag_forward");
+    if (!is_device_ptr(out)) return set_err(ctx, NS_ERR_ARG, "ns_embedding_bag_forward: out must be device memory");
+    cudaSetDevice(ctx->device);
+    BagPlan p;
+    ns_status s = plan_bags(ctx, tables, n_tables, batch, p);
+    if (s != NS_OK) return s;
+    BagTab* d = nullptr;
+    if ((s = upload(ctx, p, &d)) != NS_OK) return s;
+    const unsigned blocks = (unsigned)std::min<long long>((p.items + 7) / 8, (long long)ctx->sm_count * 8);
+    prof_begin(ctx, PK_OTHER);
+    k_bag_forward<<<blocks, 256, 0, ctx->stream>>>(d, n_tables, p.items, batch, p.out_ld, out);
+    prof_end(ctx);
+    NS_LAUNCHED(ctx);
+    return NS_OK;
+}
+
+ns_status ns_embedding_bag_backward_sgd(ns_ctx* ctx, const ns_bag_table* tables, int32_t n_tables, int32_t batch,
+                                        const float* grad_out, float lr) {
+    if (!ctx) return NS_ERR_ARG;
+    if (!tables || n_tables < 1 || batch < 1 || !grad_out)
+        return set_err(ctx, NS_ERR_ARG, "ns_embedding_bag_backward_sgd");
+    if (!is_device_ptr(grad_out)) return set_err(ctx, NS_ERR_ARG, "ns_embedding_bag_backward_sgd: grad_out device");
+    cudaSetDevice(ctx->device);
+    BagPlan p;
+    ns_status s = plan_bags(ctx, tables, n_tables, batch, p);
+    if (s != NS_OK) return s;
+    BagTab* d = nullptr;
+    if ((s = upload(ctx, p, &d)) != NS_OK) return s;
+    const unsigned blocks = (unsigned)std::min<long long>((p.items + 7) / 8, (long long)ctx->sm_count * 8);
+    prof_begin(ctx, PK_OTHER);
+    k_bag_backward_sgd<<<blocks, 256, 0, ctx->stream>>>(d, n_tables, p.items, batch, p.out_ld, grad_out, lr);
+    prof_end(ctx);
+    NS_LAUNCHED(ctx);
+    return NS_OK;
+}
+
+}  // extern "C"

@@ -82,3 +82,26 @@ def init_params(widths, seed: int) -> np.ndarray:
         parts.append(rng.uniform(-bound, bound, size=i * o))
         parts.append(rng.uniform(-bound, bound, size=o))
     return np.concatenate(parts)
+
+
+def gen_bag_indices(rows: int, pooling: float, skew: float, B: int, rng: np.random.Generator):
+    """Embedding-bag inputs of one table: bag lengths
+    ~ Poisson(pooling factor) (empty bags possible), row ids Zipf-like with
+    exponent = the table's skew (0 = uniform) over the table's rows: rank
+    k = floor of the inverse CDF of the continuous power law on [1, rows+1),
+    mapped to a row by a fixed multiplicative hash so the hot rows are spread
+    over the table.  Returns (offsets [B+1] int32, indices int64)."""
+    lens = rng.poisson(pooling, size=B)
+    off = np.zeros(B + 1, np.int64)
+    np.cumsum(lens, out=off[1:])
+    n = int(off[-1])
+    u = rng.uniform(0.0, 1.0, size=n)
+    H = float(rows)
+    if abs(skew - 1.0) < 1e-9:
+        k = np.floor(np.exp(u * np.log(H + 1.0)))
+    else:
+        a = 1.0 - skew
+        k = np.floor((((H + 1.0) ** a - 1.0) * u + 1.0) ** (1.0 / a))
+    k = np.clip(k.astype(np.int64), 1, rows) - 1
+    idx = (k * 2654435761) % rows
+    return off.astype(np.int32), idx.astype(np.int64)
