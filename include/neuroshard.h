@@ -215,6 +215,12 @@ ns_status ns_score_plans(ns_ctx* ctx, const ns_tables* tables, int32_t task, int
  * ns_synchronize.  Output pointers should be device or pinned host memory
  * (pageable host outputs make the copy, and so the call, blocking). */
 #define NS_SEARCH_ASYNC 4u
+/* "w/o greedy grid search" (Table 3: "not grid-searching the
+ * table dimension threshold"; reading R8b): the greedy runs once per column
+ * plan with NO dimension threshold -- only the memory cap constrains.  Needs
+ * M == 1.  (M = 1 without this flag is the single tightest threshold M_s,
+ * reading R8.) */
+#define NS_NO_DIM_CAP 8u
 
 typedef struct {
     int32_t N;               /* candidate tables per kind, default 10 */
@@ -222,7 +228,7 @@ typedef struct {
     int32_t L;               /* split steps, default 10; ignored by tablewise */
     int32_t M;               /* grid points, default 11 */
     double  grid_hi_factor;  /* M_e = factor * M_s, default 1.5 */
-    uint32_t flags;          /* NS_GREEDY_* (0 = auto) | NS_SEARCH_ASYNC; other bits must be 0 */
+    uint32_t flags;          /* NS_GREEDY_* (0 = auto) | NS_SEARCH_ASYNC | NS_NO_DIM_CAP; other bits 0 */
 } ns_search_params;
 
 /* Per-task results.  Every pointer is host or device; only `cost` is

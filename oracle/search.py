@@ -175,7 +175,7 @@ class GGSResult:
 
 
 def greedy_grid_search(weights, emb, task, c: List[int], M: int, hi: float = 1.5,
-                       cache=None, log: Optional[DecisionLog] = None) -> GGSResult:
+                       cache=None, log: Optional[DecisionLog] = None, dim_cap: bool = True) -> GGSResult:
     """O8 = Alg. 2 GreedyGridSearch.
 
     Line 2: build the T' = T + |c| column-sharded tables; line 3: sort them in
@@ -184,7 +184,13 @@ def greedy_grid_search(weights, emb, task, c: List[int], M: int, hi: float = 1.5
     models (PAPER.md:289 step 4).  Lines 316-318 are mis-nested in the paper;
     read as "best completed plan over the grid points, lowest grid index on
     ties" (reading R12).
+
+    ``dim_cap=False`` is Table 3's "w/o greedy grid search" ("not
+    grid-searching the table dimension threshold"; reading
+    R8b): one greedy placement with no dimension threshold (M must be 1).
     """
+    if not dim_cap and M != 1:
+        raise ValueError("dim_cap=False needs M == 1")
     tables = apply_col_plan(task, c)
     singles = single_costs(weights, emb, tables, cache)
     order = cost_order(singles)
@@ -195,8 +201,8 @@ def greedy_grid_search(weights, emb, task, c: List[int], M: int, hi: float = 1.5
     best = GGSResult(INF, None, -1, 0, tables, [])
     finite = []
     for m, md in enumerate(grid_max_dims(sum_dim, task.D, M, hi)):
-        g = greedy_place(weights, emb, task, tables, order, task.D, int(math.floor(md)),
-                         cache, log)
+        cap = int(math.floor(md)) if dim_cap else 10 ** 18
+        g = greedy_place(weights, emb, task, tables, order, task.D, cap, cache, log)
         best.work += g.work
         if g.assign is None:
             cost = INF
@@ -245,7 +251,7 @@ class BeamResult:
 
 def beam_search(weights, emb, task, N: int, K: int, L: int, M: int, hi: float = 1.5,
                 cache=None, log: Optional[DecisionLog] = None,
-                trace: Optional[list] = None) -> BeamResult:
+                trace: Optional[list] = None, dim_cap: bool = True) -> BeamResult:
     """O9 = Alg. 1 BeamSearch.
 
     The empty column plan is evaluated first and is the initial global best
@@ -260,7 +266,7 @@ def beam_search(weights, emb, task, N: int, K: int, L: int, M: int, hi: float = 
     of every beam plan, the children as (cost, generation index, column
     plan) in evaluation order, and the next beam -- introspection only.
     """
-    r0 = greedy_grid_search(weights, emb, task, [], M, hi, cache, log)
+    r0 = greedy_grid_search(weights, emb, task, [], M, hi, cache, log, dim_cap)
     best = BeamResult(r0.cost, [], r0.assign, r0.grid_index, r0.work, 1, [])
     beam: List[List[int]] = [[]]
     for _level in range(L):
@@ -272,7 +278,7 @@ def beam_search(weights, emb, task, N: int, K: int, L: int, M: int, hi: float = 
             cands.append(beam_candidates(task, tables, singles, N))
             for j, t in enumerate(cands[-1]):
                 col = cp + [t]
-                r = greedy_grid_search(weights, emb, task, col, M, hi, cache, log)
+                r = greedy_grid_search(weights, emb, task, col, M, hi, cache, log, dim_cap)
                 best.work += r.work
                 best.n_plans += 1
                 children.append((r.cost, (b, j), col))

@@ -310,8 +310,12 @@ NS_GREEDY_AUTO, NS_GREEDY_GROUPED, NS_GREEDY_LANES = 0, 1, 2
 NS_SEARCH_ASYNC = 4
 
 
-def _params(N, K, L, M, hi, greedy=NS_GREEDY_AUTO, async_=False):
-    return ns_search_params(N, K, L, M, hi, greedy | (NS_SEARCH_ASYNC if async_ else 0))
+NS_NO_DIM_CAP = 8
+
+
+def _params(N, K, L, M, hi, greedy=NS_GREEDY_AUTO, async_=False, no_dim_cap=False):
+    return ns_search_params(N, K, L, M, hi, greedy | (NS_SEARCH_ASYNC if async_ else 0) |
+                            (NS_NO_DIM_CAP if no_dim_cap else 0))
 
 
 def _alloc_out(n: int, stride: int, L: int, out: Optional[dict]):
@@ -326,10 +330,11 @@ def _alloc_out(n: int, stride: int, L: int, out: Optional[dict]):
 
 
 def ns_shard_tablewise(ctx: int, tables: Tables, D: int, M: int = 11, hi: float = 1.5, out: Optional[dict] = None,
-                       greedy: int = NS_GREEDY_AUTO, async_: bool = False):
-    """async_=True: NS_SEARCH_ASYNC (returns after enqueueing; sync before reading out)."""
+                       greedy: int = NS_GREEDY_AUTO, async_: bool = False, no_dim_cap: bool = False):
+    """async_=True: NS_SEARCH_ASYNC (returns after enqueueing; sync before reading out);
+    no_dim_cap=True: NS_NO_DIM_CAP (Table 3 "w/o greedy grid search", M must be 1)."""
     out, pb = _alloc_out(tables.n_tasks, tables.T_max, 0, out)
-    p = _params(10, 3, 0, M, hi, greedy, async_)
+    p = _params(10, 3, 0, M, hi, greedy, async_, no_dim_cap)
     st = _check(ctx, LIB.ns_shard_tablewise(ctx, tables.handle, D, C.byref(p), C.byref(pb)))
     out["status"] = st
     return out
@@ -337,9 +342,9 @@ def ns_shard_tablewise(ctx: int, tables: Tables, D: int, M: int = 11, hi: float 
 
 def ns_shard_columnwise(ctx: int, tables: Tables, D: int, N: int = 10, K: int = 3, L: int = 10, M: int = 11,
                         hi: float = 1.5, out: Optional[dict] = None, greedy: int = NS_GREEDY_AUTO,
-                        async_: bool = False):
+                        async_: bool = False, no_dim_cap: bool = False):
     out, pb = _alloc_out(tables.n_tasks, tables.T_max + L, L, out)
-    p = _params(N, K, L, M, hi, greedy, async_)
+    p = _params(N, K, L, M, hi, greedy, async_, no_dim_cap)
     st = _check(ctx, LIB.ns_shard_columnwise(ctx, tables.handle, D, C.byref(p), C.byref(pb)))
     out["status"] = st
     return out

@@ -375,7 +375,10 @@ __global__ void k_build_order(SearchBufs b, TaskView tv) {
 // per-task search state (column plan [] of task q in slot q) and the task's
 // M grid caps floor(max_dim_m) (Alg. 2 line 4; operation order of
 // reading R8 with explicit IEEE roundings).
+// hi < 0: NS_NO_DIM_CAP ("w/o greedy grid search", Table 3, reading
+// R8b): no dimension threshold at all, only the memory cap constrains.
 __device__ __forceinline__ int32_t grid_cap(long long sumdim, int D, int M, int m, double hi) {
+    if (hi < 0.0) return 2000000000;
     const double Ms = __ddiv_rn((double)sumdim, (double)D);
     double md = Ms;
     if (M > 1) {
@@ -2245,6 +2248,10 @@ __global__ void k_grid_caps(const int64_t* sumdim, int n_tasks, int D, int M, do
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n_tasks * M) return;
     const int q = i / M, m = i % M;
+    if (hi < 0.0) {   // NS_NO_DIM_CAP
+        capdim[i] = 2000000000;
+        return;
+    }
     const double Ms = __ddiv_rn((double)sumdim[q], (double)D);
     double md = Ms;
     if (M > 1) {
@@ -2717,6 +2724,7 @@ ns_status deliver(ns_ctx* ctx, const ns_tables* t, const OutStage& o, int Lout, 
 
 ns_status run_search(ns_ctx* ctx, const ns_tables* t, int D, const ns_search_params* p, ns_plan_batch* out,
                      bool columnwise) {
+    const double grid_hi = (p->flags & NS_NO_DIM_CAP) ? -1.0 : p->grid_hi_factor;
     SearchBufs b{};
     b.n_tasks = t->n_tasks;
     b.greedy_mode = p->flags & 3u;
@@ -2775,7 +2783,7 @@ ns_status run_search(ns_ctx* ctx, const ns_tables* t, int D, const ns_search_par
         prof_begin(ctx, PK_ORDER);
         if (warp_order) {
             const unsigned blocks = (unsigned)std::max(1, std::min((n_cp + 7) / 8, ctx->sm_count * 8));
-            k_order_warp<<<blocks, 256, wsm, ctx->stream>>>(b, tv, n_cp, level0, t->d_sumdim, p->grid_hi_factor);
+            k_order_warp<<<blocks, 256, wsm, ctx->stream>>>(b, tv, n_cp, level0, t->d_sumdim, grid_hi);
         } else {
             k_build_order<<<n_cp, 512, bsm, ctx->stream>>>(b, tv);
         }
@@ -2786,7 +2794,7 @@ ns_status run_search(ns_ctx* ctx, const ns_tables* t, int D, const ns_search_par
     if (!warp_order) {
         prof_begin(ctx, PK_OTHER);
         k_grid_caps<<<(b.n_tasks * b.M + 255) / 256, 256, 0, ctx->stream>>>(t->d_sumdim, b.n_tasks, b.D, b.M,
-                                                                            p->grid_hi_factor, b.capdim);
+                                                                            grid_hi, b.capdim);
         k_setup_level0<<<(b.n_tasks + 255) / 256, 256, 0, ctx->stream>>>(b);
         prof_end(ctx);
         NS_LAUNCHED(ctx);

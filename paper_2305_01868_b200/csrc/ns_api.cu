@@ -648,8 +648,9 @@ static ns_status check_search(ns_ctx* ctx, const ns_tables* t, int D, const ns_s
     if (!ctx->model.loaded) return set_err(ctx, NS_ERR_STATE, "no cost models loaded");
     if (D != ctx->model.D) return set_err(ctx, NS_ERR_ARG, "D differs from the loaded comm models' D");
     if (p->M < 1 || p->M > 4096) return set_err(ctx, NS_ERR_ARG, "need 1 <= M <= 4096");
-    if (!(p->grid_hi_factor >= 1.0) || (p->flags & ~NS_SEARCH_ASYNC) > NS_GREEDY_LANES)
+    if (!(p->grid_hi_factor >= 1.0) || (p->flags & ~(NS_SEARCH_ASYNC | NS_NO_DIM_CAP)) > NS_GREEDY_LANES)
         return set_err(ctx, NS_ERR_ARG, "bad grid_hi_factor/flags");
+    if ((p->flags & NS_NO_DIM_CAP) && p->M != 1) return set_err(ctx, NS_ERR_ARG, "NS_NO_DIM_CAP needs M == 1");
     if (columnwise) {
         if (p->N < 1 || p->K < 1 || p->L < 0 || p->L > 64 || p->N > 512 || p->K > 512)
             return set_err(ctx, NS_ERR_ARG, "need N,K in [1,512], L in [0,64]");

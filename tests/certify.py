@@ -20,7 +20,7 @@ import math
 from oracle import model as om, search as osr
 
 
-def certify_plan(w, task, col_plan, assign, grid_index, cost, M, hi=1.5, tol=1e-11, emb=None):
+def certify_plan(w, task, col_plan, assign, grid_index, cost, M, hi=1.5, tol=1e-11, emb=None, dim_cap=True):
     emb = emb or om.TableEmbeddings(w, task)
     D = task.D
     tables = osr.apply_col_plan(task, list(col_plan))      # raises on an illegal split
@@ -31,7 +31,7 @@ def certify_plan(w, task, col_plan, assign, grid_index, cost, M, hi=1.5, tol=1e-
     assert abs(cost - f) <= 1e-12 * abs(f), (cost, f)
     # validity
     sum_dim = sum(d for _, d in tables)
-    cap_dim = int(math.floor(osr.grid_max_dims(sum_dim, D, M, hi)[grid_index]))
+    cap_dim = int(math.floor(osr.grid_max_dims(sum_dim, D, M, hi)[grid_index])) if dim_cap else 10 ** 18
     load, dd = [0] * D, [0] * D
     for i, a in enumerate(assign):
         load[a] += osr.table_bytes(task, tables[i])

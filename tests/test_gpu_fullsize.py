@@ -45,19 +45,19 @@ def _f(x):
     return math.inf if x == "inf" else float(x)
 
 
-def _run(ns, ctx, tasks, w, mode, N, K, L, M, greedy=0):
+def _run(ns, ctx, tasks, w, mode, N, K, L, M, greedy=0, dim_cap=True):
     ns.ns_load_cost_models(ctx, w)
     desc, off, caps = ns.table_descs(tasks)
     tabs = ns.ns_featurize_tables(ctx, desc, off, caps)
     try:
         if mode == "tablewise":
-            return ns.ns_shard_tablewise(ctx, tabs, w.D, M=M, greedy=greedy)
-        return ns.ns_shard_columnwise(ctx, tabs, w.D, N=N, K=K, L=L, M=M, greedy=greedy)
+            return ns.ns_shard_tablewise(ctx, tabs, w.D, M=M, greedy=greedy, no_dim_cap=not dim_cap)
+        return ns.ns_shard_columnwise(ctx, tabs, w.D, N=N, K=K, L=L, M=M, greedy=greedy, no_dim_cap=not dim_cap)
     finally:
         tabs.free()
 
 
-def _compare(out, i, task, w, exp, min_margin, M):
+def _compare(out, i, task, w, exp, min_margin, M, dim_cap=True):
     """Exact identity when the oracle is tie-free at fp64 resolution, else
     certify the returned plan."""
     nc = int(out["n_col"][i]) if out.get("n_col") is not None else 0
@@ -75,7 +75,8 @@ def _compare(out, i, task, w, exp, min_margin, M):
     if math.isinf(cost):
         assert math.isinf(_f(exp["cost"]))
         return "infeasible"
-    certify_plan(w, task, col, out["assign"][i, :task.T + nc].tolist(), int(out["grid_index"][i]), cost, M)
+    certify_plan(w, task, col, out["assign"][i, :task.T + nc].tolist(), int(out["grid_index"][i]), cost, M,
+                 dim_cap=dim_cap)
     return "certified"
 
 
@@ -104,24 +105,24 @@ def test_fullsize_batched_same_as_single(ns, ctx):
         _compare(out, i, tasks[i], w, FIX[n]["expected"], _f(FIX[n]["min_margin"]), 11)
 
 
-def _oracle_check_batch(out, tasks, w, mode, N, K, L, M):
+def _oracle_check_batch(out, tasks, w, mode, N, K, L, M, dim_cap=True):
     kinds = {"identical": 0, "certified": 0, "infeasible": 0}
     for i, task in enumerate(tasks):
         emb = om.TableEmbeddings(w, task)
         log = osr.DecisionLog()
         if mode == "tablewise":
-            r = osr.greedy_grid_search(w, emb, task, [], M, log=log)
+            r = osr.greedy_grid_search(w, emb, task, [], M, log=log, dim_cap=dim_cap)
             exp = dict(cost=r.cost, col_plan=[], assign=r.assign, grid_index=r.grid_index, work=r.work)
         else:
-            r = osr.beam_search(w, emb, task, N=N, K=K, L=L, M=M, log=log)
+            r = osr.beam_search(w, emb, task, N=N, K=K, L=L, M=M, log=log, dim_cap=dim_cap)
             exp = dict(cost=r.cost, col_plan=r.col_plan, assign=r.assign, grid_index=r.grid_index, work=r.work)
-        kinds[_compare(out, i, task, w, exp, log.min_margin(), M)] += 1
+        kinds[_compare(out, i, task, w, exp, log.min_margin(), M, dim_cap)] += 1
         # the certificate holds for every returned plan, tie or not
         nc = int(out["n_col"][i]) if out.get("n_col") is not None else 0
         if math.isfinite(out["cost"][i]):
             certify_plan(w, task, out["col_plan"][i, :nc].tolist() if nc else [],
                          out["assign"][i, :task.T + nc].tolist(), int(out["grid_index"][i]),
-                         float(out["cost"][i]), M, emb=emb)
+                         float(out["cost"][i]), M, emb=emb, dim_cap=dim_cap)
     return kinds
 
 
@@ -179,3 +180,29 @@ def test_wide_grouped_kernel_bit_identical_to_per_trajectory(ns, ctx, D):
         W = int(np.sum(outs[1]["n_scores"]))
         assert comp[2] == W                    # per-trajectory kernel: executed == algorithmic
         assert 0 < comp[1] < W                 # grouped: identical trajectories share scores
+
+
+# every ablation / sweep variant of tools/ablation.py on
+# oracle-checkable tasks (T = 16, D = 4, tables that may exceed the cap):
+# identical to the oracle's Alg. 1 / Alg. 2 (or certified at near-ties).
+ABLATIONS = [
+    ("full", "columnwise", dict(N=4, K=2, L=3, M=5), True),
+    ("w/o beam search (L = 0)", "columnwise", dict(N=4, K=2, L=0, M=5), True),
+    ("w/o greedy grid search (no dim threshold, R8b)", "columnwise", dict(N=4, K=2, L=3, M=1), False),
+    ("w/o greedy grid search, table-wise", "tablewise", dict(N=0, K=0, L=0, M=1), False),
+    ("single tightest threshold (M = 1, R8)", "columnwise", dict(N=4, K=2, L=3, M=1), True),
+    ("sweep N = 1", "columnwise", dict(N=1, K=2, L=3, M=5), True),
+    ("sweep K = 1", "columnwise", dict(N=4, K=1, L=3, M=5), True),
+    ("sweep K = 3", "columnwise", dict(N=4, K=3, L=3, M=5), True),
+    ("sweep L = 1", "columnwise", dict(N=4, K=2, L=1, M=5), True),
+    ("sweep M = 9", "columnwise", dict(N=4, K=2, L=2, M=9), True),
+]
+
+
+@pytest.mark.parametrize("name,mode,hp,dim_cap", ABLATIONS, ids=[a[0] for a in ABLATIONS])
+def test_ablation_variants_match_oracle(ns, ctx, name, mode, hp, dim_cap):
+    w = gen_weights(4, "mono")
+    tasks = [gen_task("C3", 500 + i, T=16, D=4) for i in range(10)]
+    out = _run(ns, ctx, tasks, w, mode, hp["N"], hp["K"], hp["L"], hp["M"], dim_cap=dim_cap)
+    k = _oracle_check_batch(out, tasks, w, mode, hp["N"], hp["K"], hp["L"], hp["M"], dim_cap=dim_cap)
+    assert k["identical"] + k["infeasible"] >= 8, k

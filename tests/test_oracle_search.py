@@ -256,3 +256,27 @@ def test_beam_example_levels_and_result(golden_beam):
     assert r.level_best == [_f(x) for x in e["level_best"]]
     for c, a in e["children_assign"].items():
         assert osr.greedy_grid_search(w, emb, task, eval(c), g["M"]).assign == a, c
+
+
+def test_no_dim_cap_reading():
+    # Table 3 "w/o greedy grid search", reading R8b: no
+    # dimension threshold.  With the textbook linear cost it is plain LPT on
+    # all tables; with the threshold (M = 1, R8) the tight cap can strand.
+    rng = np.random.default_rng(9)
+    task = small_task(rng, 18, 3, hash_hi=1e5)
+    w = gen_weights(3, "lin")
+    emb = om.TableEmbeddings(w, task)
+    r = osr.greedy_grid_search(w, emb, task, [], 1, dim_cap=False)
+    a_ref, _ = _lpt(task.dims.tolist(), 3)
+    assert r.assign == a_ref and r.work == 3 * task.T
+    with pytest.raises(ValueError):
+        osr.greedy_grid_search(w, emb, task, [], 3, dim_cap=False)
+    # never fewer feasible tasks than the tightest threshold (a superset of placements is allowed)
+    w = gen_weights(4, "mono")
+    n_cap = n_free = 0
+    for i in range(12):
+        t = gen_task("C2", 40 + i, T=14)
+        e = om.TableEmbeddings(w, t)
+        n_cap += math.isfinite(osr.greedy_grid_search(w, e, t, [], 1).cost)
+        n_free += math.isfinite(osr.greedy_grid_search(w, e, t, [], 1, dim_cap=False).cost)
+    assert n_free >= n_cap and n_free == 12

@@ -5,7 +5,7 @@ w/o greedy grid search, w/o caching) and Fig. 8
 cost models (no trained weights exist here, so absolute costs are the
 random models' units, not milliseconds on real GPUs).
 
-    python tools/ablation.py [--tasks 100] [--T 40] [--D 4] > profiles/r1_ablation.json
+    python tools/ablation.py [--tasks 100] [--T 40] [--D 4] > profiles/r2_ablation.json
 
 Tasks: the paper's protocol draws 100 random sharding tasks per setting
 (PAPER.md:391); here T tables with dims up to 128 and hash sizes that make
@@ -36,35 +36,35 @@ from workload.synth import gen_task, gen_weights  # noqa: E402
 DEFAULT = dict(N=10, K=3, L=10, M=11)
 
 
-def run(ctx, tabs, tasks, D, N, K, L, M):
+def run(ctx, tabs, tasks, D, N, K, L, M, no_dim_cap=False):
     # one untimed call first: a larger configuration grows the library's
     # device arena once (cudaMalloc), which is not search time
     if L == 0:
-        ns.ns_shard_tablewise(ctx, tabs, D, M=M)
+        ns.ns_shard_tablewise(ctx, tabs, D, M=M, no_dim_cap=no_dim_cap)
     else:
-        ns.ns_shard_columnwise(ctx, tabs, D, N=N, K=K, L=L, M=M)
+        ns.ns_shard_columnwise(ctx, tabs, D, N=N, K=K, L=L, M=M, no_dim_cap=no_dim_cap)
     torch.cuda.synchronize()
     t0 = time.perf_counter()
     if L == 0:
-        out = ns.ns_shard_tablewise(ctx, tabs, D, M=M)
+        out = ns.ns_shard_tablewise(ctx, tabs, D, M=M, no_dim_cap=no_dim_cap)
     else:
-        out = ns.ns_shard_columnwise(ctx, tabs, D, N=N, K=K, L=L, M=M)
+        out = ns.ns_shard_columnwise(ctx, tabs, D, N=N, K=K, L=L, M=M, no_dim_cap=no_dim_cap)
     torch.cuda.synchronize()
     dt = time.perf_counter() - t0
     cost = np.asarray(out["cost"], dtype=np.float64).copy()
     return cost, dt, int(np.sum(out["n_scores"]))
 
 
-def latency(ctx, task, w, D, N, K, L, M, reps=3):
+def latency(ctx, task, w, D, N, K, L, M, reps=3, no_dim_cap=False):
     d, o, c = ns.table_descs([task])
     ts = []
     for _ in range(reps + 1):
         t0 = time.perf_counter()
         tabs = ns.ns_featurize_tables(ctx, d, o, c)
         if L == 0:
-            ns.ns_shard_tablewise(ctx, tabs, D, M=M)
+            ns.ns_shard_tablewise(ctx, tabs, D, M=M, no_dim_cap=no_dim_cap)
         else:
-            ns.ns_shard_columnwise(ctx, tabs, D, N=N, K=K, L=L, M=M)
+            ns.ns_shard_columnwise(ctx, tabs, D, N=N, K=K, L=L, M=M, no_dim_cap=no_dim_cap)
         tabs.free()
         torch.cuda.synchronize()
         ts.append(time.perf_counter() - t0)
@@ -111,10 +111,14 @@ def main():
     c0, dt0, sc0 = run(ctx, tabs, tasks, D, **p)
     rows.append(summary("w/o beam search (L=0)", c0, dt0, sc0, n, latency(ctx, tasks[0], w, D, **p), ok_full))
     p = dict(DEFAULT, M=1)
+    c2, dt2, sc2 = run(ctx, tabs, tasks, D, **p, no_dim_cap=True)
+    rows.append(summary("w/o greedy grid search (no dim threshold, reading R8b = Table 3)", c2, dt2, sc2, n,
+                        latency(ctx, tasks[0], w, D, **p, no_dim_cap=True), ok_full))
     c1, dt1, sc1 = run(ctx, tabs, tasks, D, **p)
-    rows.append(summary("w/o greedy grid search (M=1)", c1, dt1, sc1, n, latency(ctx, tasks[0], w, D, **p), ok_full))
+    rows.append(summary("single tightest threshold M_s (M=1, reading R8)", c1, dt1, sc1, n,
+                        latency(ctx, tasks[0], w, D, **p), ok_full))
     # relative cost of each variant vs full on tasks both solve
-    for r, c in zip(rows, (full, c0, c1)):
+    for r, c in zip(rows, (full, c0, c2, c1)):
         both = np.isfinite(c) & ok_full
         r["cost_vs_full_common"] = float(np.mean(c[both] / full[both])) if both.any() else None
     # oracle-side cache row: hit rate of the literal
