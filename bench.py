@@ -418,13 +418,13 @@ def main():
     g_ms, g_n = prof["greedy"]
     clocks = sampler.summary() if sampler else {}
     roof = greedy_roofline(clocks, scores_per_step * args.steps, g_ms, g_n, ms_local, stats,
-                           "k_greedy_wide* (N4, D = 128 greedy)")
+                           "k_greedy_wgrp (N4, D = 128 grouped greedy; level 0 k_greedy_wide)")
 
     # ---- CPU baseline: the oracle on a bounded sample (rank 0, N=1 only)
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline and not args.profile_run:
-        idx = feasible_c5_tasks(3)
-        r1, W1, dt1, n1 = oracle_rate(12.0, 1, idx[:1])
+        idx = feasible_c5_tasks(16)
+        r1, W1, dt1, n1 = oracle_rate(12.0, 1, idx[:2])
         cores = host_cores()
         rN, WN, dtN, nN = oracle_rate(15.0, cores, idx) if cores > 1 else (r1, W1, dt1, n1)
         cpu = {"value": rN, "unit": "scores/s", "cores": cores, "kind": "oracle",
@@ -491,8 +491,19 @@ def greedy_roofline(clocks, W, g_ms, g_n, ms_region, stats, kernel):
             "frac_basis": "algorithmic: W (the oracle's candidate-score count) x 256 flop / greedy time",
             "greedy_ms_per_launch": g_ms / max(g_n, 1), "greedy_launches": g_n,
             "step_share": g_ms / max(ms_region, 1e-9)}
+    traffic = os.path.join(ROOT, "profiles", "greedy_traffic.json")
+    if os.path.exists(traffic):
+        try:
+            tj = json.load(open(traffic))
+            if tj.get("kernel", "").split("<")[0].split()[-1] in kernel:
+                roof["traffic"] = tj.get("bytes_per_launch")
+                roof["traffic_source"] = tj.get("source")
+        except Exception:
+            pass
     if stats and stats.get("scores_computed"):
-        ex = stats["scores_computed"] * flops_per_score / (g_ms * 1e-3) / 1e12 * (W / max(stats["scores"], 1))
+        ex = stats["scores_computed"] * flops_per_score / (g_ms * 1e-3) / 1e12
+        roof["scores_computed"] = stats["scores_computed"]
+        roof["executed_share_of_W"] = stats["scores_computed"] / max(W, 1)
         roof["executed_achieved"] = ex
         roof["executed_frac"] = ex / peak
         roof["executed_basis"] = ("scores the greedy kernels computed (ns_last_stats.scores_computed; identical "
@@ -718,9 +729,6 @@ def score_plans_rate(ns, ctx, torch):
     return res
 
 
-if __name__ == "__main__":
-    main()
-
 
 def pretrain_rate(ns, ctx, torch):
     """pre-training throughput on the GPU.  App. F's recipe
@@ -873,3 +881,7 @@ def embag_rate(ns, ctx, torch):
             "forward_frac_hbm": algo_f / (fwd * 1e-3) / 1e9 / hbm,
             "backward_frac_hbm": algo_b / (bwd * 1e-3) / 1e9 / hbm,
             "hbm_peak_gbs": hbm, "protocol": "10 warm-ups, median of 100 (PAPER.md:596)"}
+
+
+if __name__ == "__main__":
+    main()

@@ -87,10 +87,11 @@ def main():
               f"fp64 {float(d['sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active']):.1f}%, "
               f"dmma {float(d.get('sm__pipe_tensor_subpipe_dmma_cycles_active.avg.pct_of_peak_sustained_active', 0)):.1f}%, "
               f"DRAM {dram / 1e6:.0f} MB")
-        if "k_greedy_dedup" in d["Kernel Name"]:
+        if "k_greedy_dedup" in d["Kernel Name"] or "k_greedy_wgrp" in d["Kernel Name"]:
             json.dump({"kernel": d["Kernel Name"], "bytes_per_launch": dram,
                        "source": f"ncu --set full, profiles/{out_tag}_ncu_full_metrics.json "
-                                 "(dram__bytes_read.sum + dram__bytes_write.sum, bench default batch of C2 tasks)"},
+                                 "(dram__bytes_read.sum + dram__bytes_write.sum of one launch of the bench's "
+                                 "headline step)"},
                       open("profiles/greedy_traffic.json", "w"), indent=1)
 
 
