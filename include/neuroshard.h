@@ -80,10 +80,12 @@ ns_status ns_profile(ns_ctx* ctx, int32_t enable);
  * stream): scores_computed = candidate scores the greedy kernels evaluated
  * (the grouped kernels evaluate a score once for all identical trajectories,
  * so this is <= the algorithmic count W the plans report); trajectories =
- * greedy trajectories launched (column plans x grid points). */
+ * greedy trajectories launched (column plans x grid points); group_steps =
+ * steps run by k_greedy_wgrp (D > 16, grouped). */
 typedef struct {
     uint64_t scores_computed;
     uint64_t trajectories;
+    uint64_t group_steps;   /* steps the large-D grouped greedy ran (one per group and table) */
 } ns_stats;
 ns_status ns_stats_query(ns_ctx* ctx, ns_stats* out);
 ns_status ns_profile_query(ns_ctx* ctx, const char* kernel, double* total_ms, uint64_t* launches);

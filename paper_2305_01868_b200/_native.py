@@ -48,7 +48,7 @@ class ns_host_comm(C.Structure):
 
 
 class ns_stats(C.Structure):
-    _fields_ = [("scores_computed", C.c_uint64), ("trajectories", C.c_uint64)]
+    _fields_ = [("scores_computed", C.c_uint64), ("trajectories", C.c_uint64), ("group_steps", C.c_uint64)]
 
 
 class ns_bag_table(C.Structure):
@@ -189,7 +189,8 @@ def ns_last_stats(ctx: int) -> dict:
     """Work counters since the last ns_profile call (ns_stats_query)."""
     st = ns_stats()
     _check(ctx, LIB.ns_stats_query(ctx, C.byref(st)))
-    return {"scores_computed": int(st.scores_computed), "trajectories": int(st.trajectories)}
+    return {"scores_computed": int(st.scores_computed), "trajectories": int(st.trajectories),
+            "group_steps": int(st.group_steps)}
 
 
 PROFILE_KINDS = ("precompute", "validate", "order", "expand", "greedy", "finalize", "select", "score", "other")

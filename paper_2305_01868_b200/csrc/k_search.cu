@@ -1673,7 +1673,7 @@ __global__ void __launch_bounds__(128 * TPD, NS_WGRP_CTAS) k_greedy_wgrp(const G
     // snapshot layout: u as [FPL][nth] doubles, then dsum, bsum [nth] --
     // coalesced per thread index
     const size_t snap_doubles = (size_t)nth * (FPL + 2);
-    unsigned long long computed = 0;
+    unsigned long long computed = 0, steps = 0;   // executed scores / group-steps (ns_stats)
     volatile unsigned int* vq = reinterpret_cast<volatile unsigned int*>(x.q);
     volatile int32_t* vready = x.item_ready;
     // copy assignment row src -> dst (list positions [0, n)); rows written by
@@ -1700,6 +1700,7 @@ __global__ void __launch_bounds__(128 * TPD, NS_WGRP_CTAS) k_greedy_wgrp(const G
             if (i < x.n_cp) {
                 got = i;
             } else if (i < x.n_items) {   // beyond n_items nothing can ever be published
+                unsigned ns_sleep = 128;   // exponential backoff: a waiting CTA shares its SM with a working one
                 for (;;) {
                     if (vready[i]) {
                         got = i;
@@ -1708,7 +1709,8 @@ __global__ void __launch_bounds__(128 * TPD, NS_WGRP_CTAS) k_greedy_wgrp(const G
                     // all published items finished -> nothing can be published any more
                     const unsigned pub = (unsigned)x.n_cp + vq[1];
                     if (vq[2] == pub && (unsigned)i >= pub) break;
-                    __nanosleep(200);
+                    __nanosleep(ns_sleep);
+                    if (ns_sleep < 4096) ns_sleep <<= 1;
                 }
                 __threadfence();
             }
@@ -1778,14 +1780,18 @@ __global__ void __launch_bounds__(128 * TPD, NS_WGRP_CTAS) k_greedy_wgrp(const G
         unsigned cf = 0;                  // steps this thread's device was scored (part 0 threads)
         int rep = mask ? __ffsll((long long)mask) - 1 : 0;   // the row holding the group's history
         bool alive = mask != 0;
+        int steps_done = 0;
+        // the group's extreme caps (members ordered by cap, R8); they change only at forks
+        int cmin = mask ? s_cap[__ffsll((long long)mask) - 1] : 0;
+        int cmax = mask ? s_cap[63 - __clzll((long long)mask)] : 0;
 #pragma unroll 1
         for (int p = p0; p < Tp; ++p) {
+            ++steps_done;
             const int par = p & 1;
             const int sl = p % kRingW;
             const int4 mt = smeta[sl];
             const int dt = mt.x;
             const long long bt = (long long)(((unsigned long long)(unsigned)mt.w << 32) | (unsigned)mt.z);
-            const int cmin = s_cap[__ffsll((long long)mask) - 1], cmax = s_cap[63 - __clzll((long long)mask)];
             const bool memok = dev && (bsum + bt <= cap);
             const int xv = dsum + dt;
             const bool f = memok && xv <= cmax;
@@ -1945,6 +1951,8 @@ __global__ void __launch_bounds__(128 * TPD, NS_WGRP_CTAS) k_greedy_wgrp(const G
                 }
                 mask = s_sub_mask[0];
                 bd = s_sub_dev[0];
+                cmin = s_cap[__ffsll((long long)mask) - 1];
+                cmax = s_cap[63 - __clzll((long long)mask)];
                 const int nrep = __ffsll((long long)mask) - 1;
                 if (nrep != rep) {
                     copy_row(tau0 + rep, tau0 + nrep, Tp);
@@ -1979,6 +1987,7 @@ __global__ void __launch_bounds__(128 * TPD, NS_WGRP_CTAS) k_greedy_wgrp(const G
         __syncthreads();   // the representative row is complete
         const unsigned gw = block_sum(cf);
         computed += gw;
+        steps += (unsigned long long)(steps_done);
         // ---- item end: members' work and rows; representative's per-device costs, links of the others
         for (int m = threadIdx.x; m < M; m += blockDim.x)
             if ((mask >> m) & 1ULL) a.work[tau0 + m] = s_work[m] + gw;
@@ -2001,6 +2010,7 @@ __global__ void __launch_bounds__(128 * TPD, NS_WGRP_CTAS) k_greedy_wgrp(const G
         if (threadIdx.x == 0) atomicAdd(&x.q->completed, 1u);
     }
     if (threadIdx.x == 0 && computed) atomicAdd(a.computed, computed);
+    if (threadIdx.x == 0 && steps) atomicAdd(a.computed + 1, steps);
 }
 
 // ======================================================================

@@ -340,6 +340,7 @@ ns_status ns_stats_query(ns_ctx* ctx, ns_stats* out) {
     NS_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
     out->scores_computed = h[0];
     out->trajectories = ctx->trajectories;
+    out->group_steps = h[1];
     return NS_OK;
 }
 

@@ -33,8 +33,13 @@ for n in [int(a) for a in sys.argv[1:]] or [1, 4, 16]:
         dt = time.perf_counter() - t0
         tabs.free()
     prof = {k: ns.ns_profile_query(ctx, k) for k in ns.PROFILE_KINDS}
+    st = ns.ns_last_stats(ctx)
     ns.ns_profile(ctx, False)
     W = int(np.sum(out["n_scores"]))
     print(f"{cfg} n={n}: {1e3*dt:.2f} ms ({1e3*dt/n:.2f} ms/task) W={W} {W/dt:.3e} scores/s  "
-          + " ".join(f"{k}={v[0]:.2f}ms/{v[1]}" for k, v in prof.items() if v[1]), flush=True)
+          + " ".join(f"{k}={v[0]:.2f}ms/{v[1]}" for k, v in prof.items() if v[1])
+          + f" | computed={st['scores_computed'] / max(W, 1):.3f}W group_steps={st['group_steps']}"
+          + (f" ({st['scores_computed'] / max(st['group_steps'], 1):.1f} scores/step,"
+             f" {prof['greedy'][0] * 1e-3 * 1.965e9 * 148 * 2 / max(st['group_steps'], 1):.0f} CTA-cycles/step)"
+             if st['group_steps'] else ""), flush=True)
 ns.ns_destroy(ctx)
