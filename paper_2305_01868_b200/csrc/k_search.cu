@@ -1647,9 +1647,9 @@ __global__ void __launch_bounds__(128 * TPD, NS_WGRP_CTAS) k_greedy_wgrp(const G
     __shared__ __align__(16) double s_hb1[kV];
     __shared__ __align__(16) double ring[kRingW][TPD * SS];
     __shared__ int4 smeta[kRingW];
-    __shared__ unsigned long long s_key[2][NWM];
-    __shared__ int s_dv[2][NWM], s_xw[2][NWM];
-    __shared__ unsigned s_xmax[2][NWM];
+    // per warp and step parity: {key lo, key hi, device | x_winner << 7, max x} -- one 16-byte record
+    // (dim sums < 2^25: T' * 128 < 2^24 is checked on the host)
+    __shared__ uint4 s_rec[2][NWM];
     __shared__ unsigned long long r_key[NWM];   // slow-path rounds
     __shared__ int r_dv[NWM], r_xw[NWM];
     __shared__ int s_cap[MMAX];
@@ -1670,7 +1670,7 @@ __global__ void __launch_bounds__(128 * TPD, NS_WGRP_CTAS) k_greedy_wgrp(const G
     const int M = a.M;
     const int my_slice = (2 * lane) / FPL, my_off = (2 * lane) % FPL;
     const double2* w2 = reinterpret_cast<const double2*>(&s_w[part][0]);
-    // snapshot layout: u as [FPL][nth] doubles, then dsum, bsum [nth] --
+    // snapshot layout: u as [FPL][nth] doubles, then dsum, memory headroom [nth] --
     // coalesced per thread index
     const size_t snap_doubles = (size_t)nth * (FPL + 2);
     unsigned long long computed = 0, steps = 0;   // executed scores / group-steps (ns_stats)
@@ -1734,7 +1734,7 @@ __global__ void __launch_bounds__(128 * TPD, NS_WGRP_CTAS) k_greedy_wgrp(const G
         const long long tau0 = (long long)g * M;   // local trajectory index of member 0
         const int q = a.cp_task[g];
         const int Tp = mask ? a.cp_Tp[g] : 0;
-        const long long cap = mask ? a.cap[q] : 0;
+        const long long cap = mask ? a.cap[q] : 0;   // (fresh items start with room = cap)
         for (int m = threadIdx.x; m < M; m += blockDim.x) {
             s_cap[m] = mask ? a.capdim[q * M + m] : 0;
             if (item < x.n_cp) {   // a column plan starts: every member unplaced, no work yet
@@ -1748,16 +1748,17 @@ __global__ void __launch_bounds__(128 * TPD, NS_WGRP_CTAS) k_greedy_wgrp(const G
         }
         double u[FPL];
         int dsum = 0;
-        long long bsum = 0;
+        long long room = 0;   // memory headroom cap - bytes on this device (R7)
         if (item < x.n_cp) {
 #pragma unroll
             for (int k = 0; k < FPL; ++k) u[k] = s_hb1[part * FPL + k];
+            room = cap;
         } else {
             const double* sp = x.snap + (size_t)(item - x.n_cp) * snap_doubles;
 #pragma unroll
             for (int k = 0; k < FPL; ++k) u[k] = __ldcg(sp + (size_t)k * nth + threadIdx.x);
             dsum = __double2loint(__ldcg(sp + (size_t)FPL * nth + threadIdx.x));
-            bsum = __double_as_longlong(__ldcg(sp + (size_t)(FPL + 1) * nth + threadIdx.x));
+            room = __double_as_longlong(__ldcg(sp + (size_t)(FPL + 1) * nth + threadIdx.x));
         }
         const int32_t* orow = a.ord_row + (size_t)g * a.Tpm;
         const int4* ometa = a.ord_meta + (size_t)g * a.Tpm;
@@ -1780,19 +1781,19 @@ __global__ void __launch_bounds__(128 * TPD, NS_WGRP_CTAS) k_greedy_wgrp(const G
         unsigned cf = 0;                  // steps this thread's device was scored (part 0 threads)
         int rep = mask ? __ffsll((long long)mask) - 1 : 0;   // the row holding the group's history
         bool alive = mask != 0;
-        int steps_done = 0;
+        int pend = p0;   // steps run = pend - p0
         // the group's extreme caps (members ordered by cap, R8); they change only at forks
         int cmin = mask ? s_cap[__ffsll((long long)mask) - 1] : 0;
         int cmax = mask ? s_cap[63 - __clzll((long long)mask)] : 0;
 #pragma unroll 1
         for (int p = p0; p < Tp; ++p) {
-            ++steps_done;
+            pend = p + 1;
             const int par = p & 1;
             const int sl = p % kRingW;
             const int4 mt = smeta[sl];
             const int dt = mt.x;
             const long long bt = (long long)(((unsigned long long)(unsigned)mt.w << 32) | (unsigned)mt.z);
-            const bool memok = dev && (bsum + bt <= cap);
+            const bool memok = dev && (bt <= room);
             const int xv = dsum + dt;
             const bool f = memok && xv <= cmax;
             const double2* v2 = reinterpret_cast<const double2*>(&ring[sl][part * SS]);
@@ -1811,12 +1812,8 @@ __global__ void __launch_bounds__(128 * TPD, NS_WGRP_CTAS) k_greedy_wgrp(const G
                 const unsigned xm = __reduce_max_sync(kFull, f && part == 0 ? (unsigned)xv : 0u);
                 const int hl = hit ? __ffs(hit) - 1 : 0;
                 const int xw = __shfl_sync(kFull, xv, hl);
-                if (lane == 0) {
-                    s_key[par][wi] = ((unsigned long long)mh << 32) | ml;
-                    s_dv[par][wi] = wi * (32 / TPD) + hl / TPD;
-                    s_xw[par][wi] = xw;
-                    s_xmax[par][wi] = xm;
-                }
+                if (lane == 0)
+                    s_rec[par][wi] = make_uint4(ml, mh, (unsigned)(wi * (32 / TPD) + hl / TPD) | ((unsigned)xw << 7), xm);
             }
             if (wi == 0) {   // the next row lands before the barrier (its slot was last read at p - 2)
                 stage(p + kLook);
@@ -1828,16 +1825,15 @@ __global__ void __launch_bounds__(128 * TPD, NS_WGRP_CTAS) k_greedy_wgrp(const G
             unsigned xmax;
             bool none;
             {
-                const unsigned long long k2 = lane < nw ? s_key[par][lane] : ~0ULL;
-                const unsigned khi = (unsigned)(k2 >> 32), klo = (unsigned)k2;
-                const unsigned mh = __reduce_min_sync(kFull, khi);
-                const unsigned ml = __reduce_min_sync(kFull, khi == mh ? klo : 0xFFFFFFFFu);
-                const unsigned hit = __ballot_sync(kFull, lane < nw && khi == mh && klo == ml);
-                xmax = __reduce_max_sync(kFull, lane < nw ? s_xmax[par][lane] : 0u);
+                const uint4 rc = lane < nw ? s_rec[par][lane] : make_uint4(~0u, ~0u, 0u, 0u);
+                const unsigned mh = __reduce_min_sync(kFull, rc.y);
+                const unsigned ml = __reduce_min_sync(kFull, rc.y == mh ? rc.x : 0xFFFFFFFFu);
+                const unsigned hit = __ballot_sync(kFull, lane < nw && rc.y == mh && rc.x == ml);
+                xmax = __reduce_max_sync(kFull, rc.w);
                 none = (mh & ml) == 0xFFFFFFFFu;
-                const int ww = hit ? __ffs(hit) - 1 : 0;
-                bd = s_dv[par][ww];
-                xstar = s_xw[par][ww];
+                const unsigned dx = __shfl_sync(kFull, rc.z, hit ? __ffs(hit) - 1 : 0);
+                bd = (int)(dx & 127u);
+                xstar = (int)(dx >> 7);
             }
             // ---- work W per member (O12): |F_m| = #{memory-feasible d : x_d <= cap_m}
             // = |F_max| (this thread's device counts in cf) minus the devices
@@ -1933,7 +1929,7 @@ __global__ void __launch_bounds__(128 * TPD, NS_WGRP_CTAS) k_greedy_wgrp(const G
                         sp[(size_t)(2 * k2 + 1) * nth + threadIdx.x] = mine ? u[2 * k2 + 1] + vv.y : u[2 * k2 + 1];
                     }
                     sp[(size_t)FPL * nth + threadIdx.x] = __hiloint2double(0, mine ? dsum + dt : dsum);
-                    sp[(size_t)(FPL + 1) * nth + threadIdx.x] = __longlong_as_double(mine ? bsum + bt : bsum);
+                    sp[(size_t)(FPL + 1) * nth + threadIdx.x] = __longlong_as_double(mine ? room - bt : room);
                     // the subgroup's history row: the group's history so far + its choice
                     const unsigned long long km = s_sub_mask[k];
                     const int krep = __ffsll((long long)km) - 1;
@@ -1979,7 +1975,7 @@ __global__ void __launch_bounds__(128 * TPD, NS_WGRP_CTAS) k_greedy_wgrp(const G
                     u[2 * k2 + 1] += vv.y;
                 }
                 dsum += dt;
-                bsum += bt;
+                room -= bt;
             }
             if (threadIdx.x == 0) a.assign[(size_t)(tau0 + rep) * a.Tpm + mt.y] = (int8_t)bd;
         }
@@ -1987,7 +1983,7 @@ __global__ void __launch_bounds__(128 * TPD, NS_WGRP_CTAS) k_greedy_wgrp(const G
         __syncthreads();   // the representative row is complete
         const unsigned gw = block_sum(cf);
         computed += gw;
-        steps += (unsigned long long)(steps_done);
+        steps += (unsigned long long)(pend - p0);
         // ---- item end: members' work and rows; representative's per-device costs, links of the others
         for (int m = threadIdx.x; m < M; m += blockDim.x)
             if ((mask >> m) & 1ULL) a.work[tau0 + m] = s_work[m] + gw;
@@ -2766,7 +2762,8 @@ ns_status run_search(ns_ctx* ctx, const ns_tables* t, int D, const ns_search_par
         warps = std::max<long long>(W, std::min<long long>(warps, (long long)((512ull << 20) / per)));
         b.gscratch_warps = dp <= 16 ? (int)(((warps + W - 1) / W) * W) : 0;
         // large D: fork snapshots of k_greedy_wgrp (one set of M - 1 slots per resident CTA)
-        b.wgrp = dp > 16 && b.M <= 64 && b.greedy_mode != NS_GREEDY_LANES;
+        // (k_greedy_wgrp packs dim sums in 25 bits: T' * 128 < 2^24)
+        b.wgrp = dp > 16 && b.M <= 64 && b.greedy_mode != NS_GREEDY_LANES && (long long)b.Tpm * kMaxDim < (1 << 24);
         {   // a launch covers one rank's block of column plans (level 0: tasks; beam levels: S)
             const long long R = ctx->nranks;
             b.wgrp_cp_cap = (int)std::max<long long>((b.n_tasks + R - 1) / R, ((long long)b.S + R - 1) / R);
