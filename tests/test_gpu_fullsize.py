@@ -206,3 +206,31 @@ def test_ablation_variants_match_oracle(ns, ctx, name, mode, hp, dim_cap):
     out = _run(ns, ctx, tasks, w, mode, hp["N"], hp["K"], hp["L"], hp["M"], dim_cap=dim_cap)
     k = _oracle_check_batch(out, tasks, w, mode, hp["N"], hp["K"], hp["L"], hp["M"], dim_cap=dim_cap)
     assert k["identical"] + k["infeasible"] >= 8, k
+
+
+@pytest.mark.parametrize("D,M", [(17, 64), (33, 1), (128, 2)])
+def test_wide_grouped_edges_against_oracle(ns, ctx, D, M):
+    """Edges of the large-D kernels: D = 17 (the first D on the wide path)
+    with M = 64 (the grouped kernel's member limit), M = 1 (single-member
+    groups), M = 2; grouped and per-trajectory kernels bit-identical and
+    equal to the oracle's beam search."""
+    w = gen_weights(D, "mono", seed=D)
+    rng = np.random.default_rng(D)
+    tasks = [small_task(rng, 3 * D, D, hash_hi=2e5) for _ in range(2)]
+    outs = [_run(ns, ctx, tasks, w, "columnwise", 3, 2, 2, M, greedy=g) for g in (1, 2)]
+    for k in ("cost", "assign", "grid_index", "n_scores", "n_col", "col_plan"):
+        assert np.array_equal(outs[0][k], outs[1][k]), k
+    kinds = _oracle_check_batch(outs[0], tasks, w, "columnwise", 3, 2, 2, M)
+    assert kinds["identical"] + kinds["infeasible"] >= 1, kinds
+
+
+@pytest.mark.parametrize("T", [256, 257])
+def test_order_kernel_switch_boundary(ns, ctx, T):
+    """T' = 256 is the last list length on the warp-per-plan order kernel,
+    257 the first on the CTA bitonic sort (k_build_order): both equal the
+    oracle's GreedyGridSearch (order, assignment, W)."""
+    w = gen_weights(16, "mono", seed=3)
+    task = small_task(np.random.default_rng(T), T, 16, hash_hi=1e5)
+    out = _run(ns, ctx, [task], w, "tablewise", 0, 0, 0, 5)
+    kinds = _oracle_check_batch(out, [task], w, "tablewise", 0, 0, 0, 5)
+    assert kinds["identical"] + kinds["certified"] == 1
