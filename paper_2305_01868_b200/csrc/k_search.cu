@@ -1706,9 +1706,14 @@ __global__ void __launch_bounds__(128 * TPD, NS_WGRP_CTAS) k_greedy_wgrp(const G
                         got = i;
                         break;
                     }
-                    // all published items finished -> nothing can be published any more
+                    // all published items finished -> nothing can be published any more.
+                    // Read `completed` BEFORE `forks`: an item publishes its forks
+                    // before it completes, so completed == n_cp + forks (in this order)
+                    // means no item was running when `completed` was read.
+                    const unsigned done = vq[2];
+                    __threadfence();
                     const unsigned pub = (unsigned)x.n_cp + vq[1];
-                    if (vq[2] == pub && (unsigned)i >= pub) break;
+                    if (done == pub && (unsigned)i >= pub) break;
                     __nanosleep(ns_sleep);
                     if (ns_sleep < 4096) ns_sleep <<= 1;
                 }
