@@ -183,9 +183,36 @@ __global__ void __launch_bounds__(256) k_pt_compute_grad(const double* __restric
     double* dA = A + 16 * 64;                 // [spb][64]
     double* dS = dA + 16 * 64;                // [spb][32]
     double* err = dS + 16 * 32;               // [spb]
-    int* rs = (int*)(err + 16);               // [kPtRows] sample (local) of each row
+    double* sW1 = err + 16;                   // weights staged in shared memory (conflict-free layouts):
+    double* sb1 = sW1 + 640;                  //   W1 [128][5], b1
+    double* sW2 = sb1 + 128;                  //   W2 [32][128] (dh1 = W2^T de: lanes over inputs)
+    double* sW2T = sW2 + 4096;                //   W2^T [128][32] (z2 = W2 h1: lanes over outputs)
+    double* sb2 = sW2T + 4096;
+    double* sH1 = sb2 + 32;                   //   H1 [64][32] (dS = H1^T dA)
+    double* sH1T = sH1 + 2048;                //   H1^T [32][64] (za = H1 s)
+    double* shb1 = sH1T + 2048;
+    double* sH2 = shb1 + 64;                  //   H2 [64], hb2
+    int* rs = (int*)(sH2 + 64 + 2);           // [kPtRows] sample (local) of each row
     __shared__ int s_r0[17];
     const int tid = threadIdx.x, nt = blockDim.x;
+    for (int i = tid; i < 640; i += nt) sW1[i] = __ldg(th + o1 + i);
+    for (int i = tid; i < 128; i += nt) sb1[i] = __ldg(th + ob1 + i);
+    for (int i = tid; i < 4096; i += nt) {
+        const double wv = __ldg(th + o2 + i);
+        sW2[i] = wv;
+        sW2T[(i & 127) * 32 + (i >> 7)] = wv;
+    }
+    for (int i = tid; i < 32; i += nt) sb2[i] = __ldg(th + ob2 + i);
+    for (int i = tid; i < 2048; i += nt) {
+        const double wv = __ldg(th + o3 + i);
+        sH1[i] = wv;
+        sH1T[(i & 31) * 64 + (i >> 5)] = wv;
+    }
+    for (int i = tid; i < 64; i += nt) {
+        shb1[i] = __ldg(th + ob3 + i);
+        sH2[i] = __ldg(th + o4 + i);
+    }
+    if (tid == 0) sH2[64] = __ldg(th + ob4);
     const int s0 = blockIdx.x * spb, ns_ = min(spb, B - s0);
     if (tid == 0) {
         int acc = 0;
@@ -211,16 +238,16 @@ __global__ void __launch_bounds__(256) k_pt_compute_grad(const double* __restric
     for (int e = tid; e < R * 128; e += nt) {
         const int rr = e >> 7, o = e & 127;
         double z = 0.0;
-        for (int i = 0; i < 5; ++i) z = fma(__ldg(th + o1 + o * 5 + i), X[rr * 5 + i], z);
-        H[e] = relu_exact(z + __ldg(th + ob1 + o));
+        for (int i = 0; i < 5; ++i) z = fma(sW1[o * 5 + i], X[rr * 5 + i], z);
+        H[e] = relu_exact(z + sb1[o]);
     }
     __syncthreads();
     // e = ReLU(W2 h1 + b2)
     for (int e = tid; e < R * 32; e += nt) {
         const int rr = e >> 5, o = e & 31;
         double z = 0.0;
-        for (int i = 0; i < 128; ++i) z = fma(__ldg(th + o2 + o * 128 + i), H[rr * 128 + i], z);
-        E[e] = relu_exact(z + __ldg(th + ob2 + o));
+        for (int i = 0; i < 128; ++i) z = fma(sW2T[i * 32 + o], H[rr * 128 + i], z);
+        E[e] = relu_exact(z + sb2[o]);
     }
     __syncthreads();
     // per-sample sum (row order)
@@ -235,31 +262,31 @@ __global__ void __launch_bounds__(256) k_pt_compute_grad(const double* __restric
     for (int e = tid; e < ns_ * 64; e += nt) {
         const int k = e >> 6, o = e & 63;
         double z = 0.0;
-        for (int i = 0; i < 32; ++i) z = fma(__ldg(th + o3 + o * 32 + i), S[k * 32 + i], z);
-        A[e] = relu_exact(z + __ldg(th + ob3 + o));
+        for (int i = 0; i < 32; ++i) z = fma(sH1T[i * 64 + o], S[k * 32 + i], z);
+        A[e] = relu_exact(z + shb1[o]);
     }
     __syncthreads();
     // y = H2 a + hb2; err; dA
     for (int k = tid >> 5; k < ns_; k += nt >> 5) {   // one warp per sample
         const int l = tid & 31;
-        double z = fma(__ldg(th + o4 + l), A[k * 64 + l], 0.0);
-        z = fma(__ldg(th + o4 + 32 + l), A[k * 64 + 32 + l], z);
+        double z = fma(sH2[l], A[k * 64 + l], 0.0);
+        z = fma(sH2[32 + l], A[k * 64 + 32 + l], z);
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) z += __shfl_xor_sync(kFull, z, o);
-        if (l == 0) err[k] = (z + __ldg(th + ob4)) - labels[list[s0 + k]];
+        if (l == 0) err[k] = (z + sH2[64]) - labels[list[s0 + k]];
     }
     __syncthreads();
     for (int e = tid; e < ns_ * 64; e += nt) {
         const int k = e >> 6, o = e & 63;
         const double dy = 2.0 * err[k] / (double)B;
-        dA[e] = A[e] > 0.0 ? dy * __ldg(th + o4 + o) : 0.0;
+        dA[e] = A[e] > 0.0 ? dy * sH2[o] : 0.0;
     }
     __syncthreads();
     // dS = H1^T dA
     for (int e = tid; e < ns_ * 32; e += nt) {
         const int k = e >> 5, j = e & 31;
         double z = 0.0;
-        for (int o = 0; o < 64; ++o) z = fma(__ldg(th + o3 + o * 32 + j), dA[k * 64 + o], z);
+        for (int o = 0; o < 64; ++o) z = fma(sH1[o * 32 + j], dA[k * 64 + o], z);
         dS[e] = z;
     }
     __syncthreads();
@@ -308,7 +335,7 @@ __global__ void __launch_bounds__(256) k_pt_compute_grad(const double* __restric
     for (int e = tid; e < R * 128; e += nt) {
         const int rr = e >> 7, i = e & 127;
         double z = 0.0;
-        for (int o = 0; o < 32; ++o) z = fma(__ldg(th + o2 + o * 128 + i), E[rr * 32 + o], z);
+        for (int o = 0; o < 32; ++o) z = fma(sW2[o * 128 + i], E[rr * 32 + o], z);
         H[e] = H[e] > 0.0 ? z : 0.0;
     }
     __syncthreads();
@@ -521,8 +548,8 @@ ns_status ns_pretrain_compute_step(ns_ctx* ctx, double* theta, double* adam_m, d
     double* part = (double*)arena_get(ctx, ((size_t)nblk * P + nblk + 64) * sizeof(double));
     if (!part) return set_err(ctx, NS_ERR_NOMEM, "device arena (pretrain)");
     double* loss_part = part + (size_t)nblk * P;
-    const size_t smem = ((size_t)kPtRows * (5 + 128 + 32) + 16 * (32 + 64 + 64 + 32) + 16) * sizeof(double) +
-                        kPtRows * sizeof(int);
+    const size_t smem = ((size_t)kPtRows * (5 + 128 + 32) + 16 * (32 + 64 + 64 + 32) + 16 + 640 + 128 + 2 * 4096 + 32 +
+                         2 * 2048 + 64 + 64 + 2) * sizeof(double) + kPtRows * sizeof(int);
     static bool attr = false;
     if (!attr) {
         cudaFuncSetAttribute(k_pt_compute_grad, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
