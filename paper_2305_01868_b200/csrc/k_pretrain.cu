@@ -550,11 +550,8 @@ ns_status ns_pretrain_compute_step(ns_ctx* ctx, double* theta, double* adam_m, d
     double* loss_part = part + (size_t)nblk * P;
     const size_t smem = ((size_t)kPtRows * (5 + 128 + 32) + 16 * (32 + 64 + 64 + 32) + 16 + 640 + 128 + 2 * 4096 + 32 +
                          2 * 2048 + 64 + 64 + 2) * sizeof(double) + kPtRows * sizeof(int);
-    static bool attr = false;
-    if (!attr) {
-        cudaFuncSetAttribute(k_pt_compute_grad, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        attr = true;
-    }
+    // (per call: the attribute is per device, a process may drive several)
+    cudaFuncSetAttribute(k_pt_compute_grad, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     prof_begin(ctx, PK_OTHER);
     k_pt_compute_grad<<<nblk, 256, smem, ctx->stream>>>(theta, feats, off, batch, labels, B, spb, part, loss_part);
     prof_end(ctx);
