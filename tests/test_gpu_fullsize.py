@@ -234,3 +234,31 @@ def test_order_kernel_switch_boundary(ns, ctx, T):
     out = _run(ns, ctx, [task], w, "tablewise", 0, 0, 0, 5)
     kinds = _oracle_check_batch(out, [task], w, "tablewise", 0, 0, 0, 5)
     assert kinds["identical"] + kinds["certified"] == 1
+
+
+def test_bench_launch_C5_batch(ns, ctx):
+    """The bench's headline launch (128 C5 tasks per call: the grouped large-D
+    greedy with forks on the work queue) against single-task calls of the
+    same tasks (the per-trajectory latency kernels): bit-identical plans,
+    costs, grid indices and W for a sample of tasks; two of them certified
+    by the oracle (T8, validity, certificate replay)."""
+    import bench
+    c = CONFIGS["C5"]
+    w = gen_weights(128, "mono")
+    n = 128
+    tasks = gen_tasks("C5", n)
+    out = _run(ns, ctx, tasks, w, "columnwise", c["N"], c["K"], c["L"], c["M"])
+    assert bench.CFG == "C5"
+    certified = 0
+    for i in (0, 3, 37, 101):
+        one = _run(ns, ctx, [tasks[i]], w, "columnwise", c["N"], c["K"], c["L"], c["M"])
+        for k in ("cost", "n_col", "grid_index", "n_scores"):
+            assert one[k][0] == out[k][i], (i, k)
+        nc = int(out["n_col"][i])
+        assert np.array_equal(one["col_plan"][0, :nc], out["col_plan"][i, :nc])
+        assert np.array_equal(one["assign"][0, :1000 + nc], out["assign"][i, :1000 + nc])
+        if math.isfinite(out["cost"][i]) and certified < 2:
+            certify_plan(w, tasks[i], out["col_plan"][i, :nc].tolist(), out["assign"][i, :1000 + nc].tolist(),
+                         int(out["grid_index"][i]), float(out["cost"][i]), c["M"])
+            certified += 1
+    assert certified == 2
