@@ -2827,6 +2827,9 @@ ns_status run_search(ns_ctx* ctx, const ns_tables* t, int D, const ns_search_par
     NS_LAUNCHED(ctx);
     // ---- beam levels (Alg. 1 lines 6-22)
     for (int level = 1; level <= L; ++level) {
+        static const char* kLevelNames[] = {"level 1", "level 2", "level 3", "level 4", "level 5", "level 6",
+                                            "level 7", "level 8", "level 9", "level 10", "level > 10"};
+        NvtxRange nvtx_level(kLevelNames[level <= 10 ? level - 1 : 10]);
         const size_t esm = (size_t)b.Tpm * 20 + (size_t)b.N2 * 4 * 2 + (size_t)b.N2 * 4 + 64;
         if (esm > 48 * 1024)
             cudaFuncSetAttribute(k_expand, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)esm);

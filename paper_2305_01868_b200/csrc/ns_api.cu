@@ -454,6 +454,7 @@ ns_status ns_load_cost_models(ns_ctx* ctx, const ns_compute_model* cm, const ns_
 
 ns_status ns_featurize_tables(ns_ctx* ctx, const ns_table_desc* tables, const int32_t* task_offsets,
                               const int64_t* mem_cap, int32_t n_tasks, ns_tables** out) {
+    NvtxRange nvtx_("ns_featurize_tables");
     if (!ctx) return NS_ERR_ARG;
     if (!out || !tables || !task_offsets || !mem_cap || n_tasks < 1)
         return set_err(ctx, NS_ERR_ARG, "ns_featurize_tables: null argument or n_tasks < 1");
@@ -665,6 +666,7 @@ static ns_status check_search(ns_ctx* ctx, const ns_tables* t, int D, const ns_s
 
 ns_status ns_shard_tablewise(ns_ctx* ctx, const ns_tables* t, int32_t D, const ns_search_params* p,
                              ns_plan_batch* out) {
+    NvtxRange nvtx_("ns_shard_tablewise");
     ns_status s = check_search(ctx, t, D, p, out, false);
     if (s != NS_OK) return s;
     cudaSetDevice(ctx->device);
@@ -673,6 +675,7 @@ ns_status ns_shard_tablewise(ns_ctx* ctx, const ns_tables* t, int32_t D, const n
 
 ns_status ns_shard_columnwise(ns_ctx* ctx, const ns_tables* t, int32_t D, const ns_search_params* p,
                               ns_plan_batch* out) {
+    NvtxRange nvtx_("ns_shard_columnwise");
     ns_status s = check_search(ctx, t, D, p, out, true);
     if (s != NS_OK) return s;
     cudaSetDevice(ctx->device);
@@ -687,6 +690,7 @@ ns_status ns_shard_columnwise(ns_ctx* ctx, const ns_tables* t, int32_t D, const 
 ns_status ns_score_plans(ns_ctx* ctx, const ns_tables* t, int32_t task, int32_t D, const int32_t* col_plan,
                          int32_t n_col, const int8_t* assign, int64_t P, int32_t mode, double* cost_out,
                          int64_t* best_index_out, double* best_cost_out) {
+    NvtxRange nvtx_("ns_score_plans");
     if (!ctx) return NS_ERR_ARG;
     if (!t || !assign || P < 1 || (n_col > 0 && !col_plan) || n_col < 0)
         return set_err(ctx, NS_ERR_ARG, "ns_score_plans: null argument or P < 1");

@@ -10,8 +10,17 @@
 #include <vector>
 
 #include "../../include/neuroshard.h"
+#include <nvtx3/nvToolsExt.h>   // header-only NVTX v3 (ranges show up in Nsight Systems; no-ops otherwise)
 
 namespace ns {
+
+// NVTX range for the lifetime of a scope (public entry points, beam levels)
+struct NvtxRange {
+    explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+    ~NvtxRange() { nvtxRangePop(); }
+    NvtxRange(const NvtxRange&) = delete;
+    NvtxRange& operator=(const NvtxRange&) = delete;
+};
 
 constexpr int kF = 5;        // table features (reading R1)
 constexpr int kH = 128;      // encoder hidden width  ("128-32")
