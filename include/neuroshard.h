@@ -188,6 +188,7 @@ typedef enum {
  * f = max_d(comp_d + fwd_d + bwd_d) with comp_d = C(S_d) (0 if empty),
  * fwd starts = comp - min(comp), bwd starts = 0 (readings R4, R10, R11).
  * Memory and max_dim constraints are NOT applied (any plan can be scored).
+ * mode may carry NS_R10_ABS_STARTS / NS_R11_SUM_OF_MAX (alternative readings).
  * After ns_comm_init the P plans are split over the ranks and the argmin is
  * an allreduce-min over packed (cost, index) keys; cost_out then holds only
  * this rank's slice [P_begin, P_end) at its global positions. */
@@ -223,6 +224,18 @@ ns_status ns_score_plans(ns_ctx* ctx, const ns_tables* tables, int32_t task, int
  * M == 1.  (M = 1 without this flag is the single tightest threshold M_s,
  * reading R8.) */
 #define NS_NO_DIM_CAP 8u
+/* Alternative readings of ambiguous passages, OR-ed into
+ * ns_search_params.flags (all three) or into ns_score_plans' mode (R10, R11);
+ * the oracle implements the same alternatives:
+ *  NS_R10_ABS_STARTS  forward comm starts = the absolute compute costs, not
+ *                     comp - min comp (reading R10)
+ *  NS_R11_SUM_OF_MAX  f = max comp + max fwd + max bwd ("summing up")
+ *                     instead of the maximum per-device sum (R11)
+ *  NS_R14_SPLITTABLE  beam candidates: top N among the splittable tables only,
+ *                     not top N of all then unsplittable dropped (R14) */
+#define NS_R10_ABS_STARTS 16u
+#define NS_R11_SUM_OF_MAX 32u
+#define NS_R14_SPLITTABLE 64u
 
 typedef struct {
     int32_t N;               /* candidate tables per kind, default 10 */
@@ -230,7 +243,7 @@ typedef struct {
     int32_t L;               /* split steps, default 10; ignored by tablewise */
     int32_t M;               /* grid points, default 11 */
     double  grid_hi_factor;  /* M_e = factor * M_s, default 1.5 */
-    uint32_t flags;          /* NS_GREEDY_* (0 = auto) | NS_SEARCH_ASYNC | NS_NO_DIM_CAP; other bits 0 */
+    uint32_t flags;          /* NS_GREEDY_* (0 = auto) | NS_SEARCH_ASYNC | NS_NO_DIM_CAP | NS_R1x_*; other bits 0 */
 } ns_search_params;
 
 /* Per-task results.  Every pointer is host or device; only `cost` is

@@ -107,13 +107,26 @@ def comm_costs(layers, starts: np.ndarray, devdims: np.ndarray,
     return mlp(layers, x, relu_last=False)
 
 
+def reduce_plan(comp: np.ndarray, fwd: np.ndarray, bwd: np.ndarray, sum_of_max: bool = False) -> float:
+    """The reduction of O6 over devices.  Reading R11 (default): the maximum
+    over devices of the per-device sum comp + fwd + bwd ("the
+    maximum cost across devices").  Alternative (``sum_of_max``, flag
+    NS_R11_SUM_OF_MAX): "summing up the predicted computation,
+    forward communication, and backward communication costs" read as the sum
+    of the three per-term maxima."""
+    if sum_of_max:
+        return float(comp.max() + fwd.max() + bwd.max())
+    return float((comp + fwd + bwd).max())
+
+
 def plan_cost(weights, emb: TableEmbeddings, tables: List[Tuple[int, int]],
-              assign: Sequence[int], D: int):
+              assign: Sequence[int], D: int, abs_starts: bool = False, sum_of_max: bool = False):
     """O6.  Simulated embedding cost f(c, t): "summing up the
     predicted computation, forward communication, and backward communication
-    costs", reduced by the maximum over devices (reading R11).
-    Forward starts are the relative compute delays comp - min(comp) (reading
-    R10), backward starts are zero.
+    costs", reduced by the maximum over devices (reading R11,
+    ``reduce_plan``).  Forward starts are the relative compute delays
+    comp - min(comp) (reading R10; ``abs_starts``: the absolute compute costs,
+    flag NS_R10_ABS_STARTS), backward starts are zero.
 
     ``tables`` is the post-split table list [(source, dim)], ``assign[i]`` the
     device of table i.  Returns (cost, comp[D], fwd[D], bwd[D], devdim[D]).
@@ -124,8 +137,7 @@ def plan_cost(weights, emb: TableEmbeddings, tables: List[Tuple[int, int]],
         members[int(d)].append(tables[i])
         devdim[int(d)] += tables[i][1]
     comp = np.array([compute_cost(weights, emb, members[d]) for d in range(D)])
-    starts = comp - comp.min()
+    starts = comp if abs_starts else comp - comp.min()
     fwd = comm_costs(weights.comm_fwd, starts, devdim, weights.start_scale, weights.dim_scale)
     bwd = comm_costs(weights.comm_bwd, np.zeros(D), devdim, weights.start_scale, weights.dim_scale)
-    total = comp + fwd + bwd
-    return float(total.max()), comp, fwd, bwd, devdim
+    return reduce_plan(comp, fwd, bwd, sum_of_max), comp, fwd, bwd, devdim

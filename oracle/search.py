@@ -175,7 +175,8 @@ class GGSResult:
 
 
 def greedy_grid_search(weights, emb, task, c: List[int], M: int, hi: float = 1.5,
-                       cache=None, log: Optional[DecisionLog] = None, dim_cap: bool = True) -> GGSResult:
+                       cache=None, log: Optional[DecisionLog] = None, dim_cap: bool = True,
+                       abs_starts: bool = False, sum_of_max: bool = False) -> GGSResult:
     """O8 = Alg. 2 GreedyGridSearch.
 
     Line 2: build the T' = T + |c| column-sharded tables; line 3: sort them in
@@ -212,7 +213,7 @@ def greedy_grid_search(weights, emb, task, c: List[int], M: int, hi: float = 1.5
                     mem = [tables[i] for i in range(len(tables)) if g.assign[i] == d]
                     if mem:
                         cache.cost(weights, emb, mem)
-            cost = plan_cost(weights, emb, tables, g.assign, task.D)[0]
+            cost = plan_cost(weights, emb, tables, g.assign, task.D, abs_starts, sum_of_max)[0]
             finite.append((cost, tuple(g.assign)))
         best.grid_costs.append(cost)
         if cost < best.cost:
@@ -225,15 +226,17 @@ def greedy_grid_search(weights, emb, task, c: List[int], M: int, hi: float = 1.5
 
 
 # --------------------------------------------------------------------------- O9
-def beam_candidates(task, tables, singles, N: int) -> List[int]:
+def beam_candidates(task, tables, singles, N: int, splittable_only: bool = False) -> List[int]:
     """Alg. 1 line 8: "merging the top N costly tables and the
     top N tables with the largest sizes with duplicates removed".  Costly =
     single-table predicted cost, order (-cost, index); largest = (-bytes,
     index); then tables that cannot be halved (dim % 8 != 0) are dropped
-    (reading R14)."""
+    (reading R14).  ``splittable_only`` (flag NS_R14_SPLITTABLE): rank only
+    the splittable tables, so up to N of each kind survive."""
     n = len(tables)
-    by_cost = sorted(range(n), key=lambda i: (-singles[i], i))[:N]
-    by_size = sorted(range(n), key=lambda i: (-table_bytes(task, tables[i]), i))[:N]
+    pool = [i for i in range(n) if tables[i][1] % 8 == 0] if splittable_only else list(range(n))
+    by_cost = sorted(pool, key=lambda i: (-singles[i], i))[:N]
+    by_size = sorted(pool, key=lambda i: (-table_bytes(task, tables[i]), i))[:N]
     cand = list(by_cost) + [i for i in by_size if i not in by_cost]
     return [i for i in cand if tables[i][1] % 8 == 0]
 
@@ -251,7 +254,8 @@ class BeamResult:
 
 def beam_search(weights, emb, task, N: int, K: int, L: int, M: int, hi: float = 1.5,
                 cache=None, log: Optional[DecisionLog] = None,
-                trace: Optional[list] = None, dim_cap: bool = True) -> BeamResult:
+                trace: Optional[list] = None, dim_cap: bool = True, abs_starts: bool = False,
+                sum_of_max: bool = False, splittable_only: bool = False) -> BeamResult:
     """O9 = Alg. 1 BeamSearch.
 
     The empty column plan is evaluated first and is the initial global best
@@ -266,7 +270,7 @@ def beam_search(weights, emb, task, N: int, K: int, L: int, M: int, hi: float = 
     of every beam plan, the children as (cost, generation index, column
     plan) in evaluation order, and the next beam -- introspection only.
     """
-    r0 = greedy_grid_search(weights, emb, task, [], M, hi, cache, log, dim_cap)
+    r0 = greedy_grid_search(weights, emb, task, [], M, hi, cache, log, dim_cap, abs_starts, sum_of_max)
     best = BeamResult(r0.cost, [], r0.assign, r0.grid_index, r0.work, 1, [])
     beam: List[List[int]] = [[]]
     for _level in range(L):
@@ -275,10 +279,10 @@ def beam_search(weights, emb, task, N: int, K: int, L: int, M: int, hi: float = 
         for b, cp in enumerate(beam):
             tables = apply_col_plan(task, cp)
             singles = single_costs(weights, emb, tables, cache)
-            cands.append(beam_candidates(task, tables, singles, N))
+            cands.append(beam_candidates(task, tables, singles, N, splittable_only))
             for j, t in enumerate(cands[-1]):
                 col = cp + [t]
-                r = greedy_grid_search(weights, emb, task, col, M, hi, cache, log, dim_cap)
+                r = greedy_grid_search(weights, emb, task, col, M, hi, cache, log, dim_cap, abs_starts, sum_of_max)
                 best.work += r.work
                 best.n_plans += 1
                 children.append((r.cost, (b, j), col))

@@ -13,6 +13,9 @@ from ._native import (  # noqa: F401
     NS_GREEDY_AUTO,
     NS_GREEDY_GROUPED,
     NS_GREEDY_LANES,
+    NS_R10_ABS_STARTS,
+    NS_R11_SUM_OF_MAX,
+    NS_R14_SPLITTABLE,
     NSError,
     TABLE_DESC,
     Tables,

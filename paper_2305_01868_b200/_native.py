@@ -312,11 +312,12 @@ NS_SEARCH_ASYNC = 4
 
 
 NS_NO_DIM_CAP = 8
+NS_R10_ABS_STARTS, NS_R11_SUM_OF_MAX, NS_R14_SPLITTABLE = 16, 32, 64   # alternative readings
 
 
-def _params(N, K, L, M, hi, greedy=NS_GREEDY_AUTO, async_=False, no_dim_cap=False):
+def _params(N, K, L, M, hi, greedy=NS_GREEDY_AUTO, async_=False, no_dim_cap=False, readings=0):
     return ns_search_params(N, K, L, M, hi, greedy | (NS_SEARCH_ASYNC if async_ else 0) |
-                            (NS_NO_DIM_CAP if no_dim_cap else 0))
+                            (NS_NO_DIM_CAP if no_dim_cap else 0) | readings)
 
 
 def _alloc_out(n: int, stride: int, L: int, out: Optional[dict]):
@@ -331,11 +332,12 @@ def _alloc_out(n: int, stride: int, L: int, out: Optional[dict]):
 
 
 def ns_shard_tablewise(ctx: int, tables: Tables, D: int, M: int = 11, hi: float = 1.5, out: Optional[dict] = None,
-                       greedy: int = NS_GREEDY_AUTO, async_: bool = False, no_dim_cap: bool = False):
+                       greedy: int = NS_GREEDY_AUTO, async_: bool = False, no_dim_cap: bool = False,
+                       readings: int = 0):
     """async_=True: NS_SEARCH_ASYNC (returns after enqueueing; sync before reading out);
     no_dim_cap=True: NS_NO_DIM_CAP (Table 3 "w/o greedy grid search", M must be 1)."""
     out, pb = _alloc_out(tables.n_tasks, tables.T_max, 0, out)
-    p = _params(10, 3, 0, M, hi, greedy, async_, no_dim_cap)
+    p = _params(10, 3, 0, M, hi, greedy, async_, no_dim_cap, readings)
     st = _check(ctx, LIB.ns_shard_tablewise(ctx, tables.handle, D, C.byref(p), C.byref(pb)))
     out["status"] = st
     return out
@@ -343,9 +345,9 @@ def ns_shard_tablewise(ctx: int, tables: Tables, D: int, M: int = 11, hi: float 
 
 def ns_shard_columnwise(ctx: int, tables: Tables, D: int, N: int = 10, K: int = 3, L: int = 10, M: int = 11,
                         hi: float = 1.5, out: Optional[dict] = None, greedy: int = NS_GREEDY_AUTO,
-                        async_: bool = False, no_dim_cap: bool = False):
+                        async_: bool = False, no_dim_cap: bool = False, readings: int = 0):
     out, pb = _alloc_out(tables.n_tasks, tables.T_max + L, L, out)
-    p = _params(N, K, L, M, hi, greedy, async_, no_dim_cap)
+    p = _params(N, K, L, M, hi, greedy, async_, no_dim_cap, readings)
     st = _check(ctx, LIB.ns_shard_columnwise(ctx, tables.handle, D, C.byref(p), C.byref(pb)))
     out["status"] = st
     return out

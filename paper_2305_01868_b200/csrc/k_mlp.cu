@@ -32,6 +32,7 @@ struct PlanCostArgs {
     CommParams cp;
     double start_scale, dim_scale;
     int ldx, ldy;                   // smem row strides (doubles)
+    uint32_t rflags;                // NS_R10_ABS_STARTS / NS_R11_SUM_OF_MAX
     const int32_t* list;            // optional: rows = list[i], i < *list_n (then row_begin = 0, row_end = capacity)
     const int32_t* list_n;
 };
@@ -142,7 +143,7 @@ __global__ void __launch_bounds__(128, BIG ? 3 : NS_PC_BLOCKS) k_plan_cost_dmma(
             m = CUDART_INF;
             for (int d = 0; d < D; ++d) m = fmin(m, a.comp[r * D + d]);
         }
-        mn[lane] = m;
+        mn[lane] = (a.rflags & NS_R10_ABS_STARTS) ? 0.0 : m;   // R10: relative (default) or absolute starts
     }
     __syncthreads();
     if (rows) {
@@ -249,7 +250,18 @@ __global__ void __launch_bounds__(128, BIG ? 3 : NS_PC_BLOCKS) k_plan_cost_dmma(
             double c = CUDART_INF;
             if (!a.feas || a.feas[row]) {
                 c = -CUDART_INF;
-                for (int d = 0; d < D; ++d) c = fmax(c, (a.comp[row * D + d] + O[lane * 2 * D + d]) + O[lane * 2 * D + D + d]);
+                if (a.rflags & NS_R11_SUM_OF_MAX) {   // alternative R11: sum of the per-term maxima
+                    double mc = -CUDART_INF, mf = -CUDART_INF, mb = -CUDART_INF;
+                    for (int d = 0; d < D; ++d) {
+                        mc = fmax(mc, a.comp[row * D + d]);
+                        mf = fmax(mf, O[lane * 2 * D + d]);
+                        mb = fmax(mb, O[lane * 2 * D + D + d]);
+                    }
+                    c = (mc + mf) + mb;
+                } else {
+                    for (int d = 0; d < D; ++d)
+                        c = fmax(c, (a.comp[row * D + d] + O[lane * 2 * D + d]) + O[lane * 2 * D + D + d]);
+                }
             }
             a.cost[row] = c;
         }
@@ -520,6 +532,7 @@ ns_status launch_plan_cost(ns_ctx* ctx, long long rb, long long re, const uint8_
     a.row_begin = rb;
     a.row_end = re;
     a.D = ctx->model.D;
+    a.rflags = ctx->rflags;
     a.feas = feas;
     a.comp = comp;
     a.devdim = devdim;

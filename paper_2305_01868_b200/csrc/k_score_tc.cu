@@ -118,6 +118,7 @@ struct TcArgs {
     const double* b[5];
     double start_scale, dim_scale;
     int n_tiles;
+    uint32_t rflags;
 };
 
 // weight smem layout: per layer hi block then lo block, each K-major [Np x Kp]
@@ -289,8 +290,9 @@ __global__ void __launch_bounds__(128 * kGroups, 1) k_plan_mlp_tc(const TcArgs a
         const bool rv = row < a.row_end;
         // ---- layer-1 input row: [starts / start_scale, devdim / dim_scale]
         double mn = CUDART_INF;
-        if (rv && a.dir == 0)
+        if (rv && a.dir == 0 && !(a.rflags & NS_R10_ABS_STARTS))
             for (int d = 0; d < a.D; ++d) mn = fmin(mn, a.comp[row * a.D + d]);
+        if (a.rflags & NS_R10_ABS_STARTS) mn = 0.0;   // R10 alternative: absolute starts
         layer(0, a.K0p, 0, [&](int c0, float (&v)[kKc]) {
             for (int j = 0; j < kKc; ++j) {
                 const int k = c0 + j;
@@ -323,12 +325,22 @@ __global__ void __launch_bounds__(128 * kGroups, 1) k_plan_mlp_tc(const TcArgs a
 }
 
 __global__ void k_plan_cost_combine(const double* comp, const float* fwd, const float* bwd, const uint8_t* ok,
-                                    long long pb, long long pe, int D, double* cost) {
+                                    long long pb, long long pe, int D, double* cost, int sum_of_max) {
     for (long long p = pb + (long long)blockIdx.x * blockDim.x + threadIdx.x; p < pe;
          p += (long long)gridDim.x * blockDim.x) {
         double c = -CUDART_INF;
-        for (int d = 0; d < D; ++d)
-            c = fmax(c, (comp[p * D + d] + (double)fwd[p * D + d]) + (double)bwd[p * D + d]);
+        if (sum_of_max) {   // R11 alternative: sum of the per-term maxima
+            double mc = -CUDART_INF, mf = -CUDART_INF, mb = -CUDART_INF;
+            for (int d = 0; d < D; ++d) {
+                mc = fmax(mc, comp[p * D + d]);
+                mf = fmax(mf, (double)fwd[p * D + d]);
+                mb = fmax(mb, (double)bwd[p * D + d]);
+            }
+            c = (mc + mf) + mb;
+        } else {
+            for (int d = 0; d < D; ++d)
+                c = fmax(c, (comp[p * D + d] + (double)fwd[p * D + d]) + (double)bwd[p * D + d]);
+        }
         cost[p] = ok[p] ? c : CUDART_NAN;
     }
 }
@@ -353,6 +365,7 @@ ns_status launch_plan_cost_tc(ns_ctx* ctx, long long pb, long long pe, const dou
     a.start_scale = ctx->model.start_scale;
     a.dim_scale = ctx->model.dim_scale;
     a.n_tiles = (int)((pe - pb + kTile - 1) / kTile);
+    a.rflags = ctx->rflags;
     // weight floats: 2 * sum(Kp * Np)
     const int wfl = 2 * (a.K0p * 128 + 128 * 64 + 64 * 32 + 32 * 16 + 16 * 16);
     const size_t smem = (size_t)(wfl + kGroups * 2 * kABuf) * sizeof(float) + 128;
@@ -372,7 +385,7 @@ ns_status launch_plan_cost_tc(ns_ctx* ctx, long long pb, long long pe, const dou
     }
     const long long n = pe - pb;
     k_plan_cost_combine<<<(unsigned)std::min<long long>((n + 255) / 256, 4096), 256, 0, ctx->stream>>>(
-        comp, fbuf, bbuf, ok, pb, pe, D, cost);
+        comp, fbuf, bbuf, ok, pb, pe, D, cost, (ctx->rflags & NS_R11_SUM_OF_MAX) ? 1 : 0);
     NS_LAUNCHED(ctx);
     return NS_OK;
 }

@@ -88,6 +88,7 @@ struct SearchBufs {
     // rank (all of them with one rank or emulated ranks): only their
     // assignment rows are valid here (multi-rank: the others are not exchanged)
     int own_cb, own_ce;
+    int r14;             // NS_R14_SPLITTABLE: rank only splittable tables as candidates
 };
 
 struct TaskView {   // read-only table arrays of the batch
@@ -161,6 +162,10 @@ __global__ void k_expand(SearchBufs b, TaskView tv, int level) {
     for (int i = threadIdx.x; i < Tp; i += blockDim.x) {
         keyc[i] = tv.C[rows[i]];
         keyb[i] = tv.vbytes[rows[i]];
+        if (b.r14 && (tv.vdim[rows[i]] % 8 != 0 || rows[i] % kDepth >= kDepth - 1)) {
+            keyc[i] = -CUDART_INF;   // R14 alternative: unsplittable tables rank last
+            keyb[i] = LLONG_MIN;     // (and are dropped by the filter below)
+        }
     }
     __syncthreads();
     if (Tp <= 256) {
@@ -2739,7 +2744,9 @@ ns_status deliver(ns_ctx* ctx, const ns_tables* t, const OutStage& o, int Lout, 
 ns_status run_search(ns_ctx* ctx, const ns_tables* t, int D, const ns_search_params* p, ns_plan_batch* out,
                      bool columnwise) {
     const double grid_hi = (p->flags & NS_NO_DIM_CAP) ? -1.0 : p->grid_hi_factor;
+    ctx->rflags = p->flags & (NS_R10_ABS_STARTS | NS_R11_SUM_OF_MAX);
     SearchBufs b{};
+    b.r14 = (p->flags & NS_R14_SPLITTABLE) ? 1 : 0;
     b.n_tasks = t->n_tasks;
     b.greedy_mode = p->flags & 3u;
     b.D = D;

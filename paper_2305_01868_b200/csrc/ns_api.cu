@@ -650,7 +650,9 @@ static ns_status check_search(ns_ctx* ctx, const ns_tables* t, int D, const ns_s
     if (!ctx->model.loaded) return set_err(ctx, NS_ERR_STATE, "no cost models loaded");
     if (D != ctx->model.D) return set_err(ctx, NS_ERR_ARG, "D differs from the loaded comm models' D");
     if (p->M < 1 || p->M > 4096) return set_err(ctx, NS_ERR_ARG, "need 1 <= M <= 4096");
-    if (!(p->grid_hi_factor >= 1.0) || (p->flags & ~(NS_SEARCH_ASYNC | NS_NO_DIM_CAP)) > NS_GREEDY_LANES)
+    if (!(p->grid_hi_factor >= 1.0) ||
+        (p->flags & ~(NS_SEARCH_ASYNC | NS_NO_DIM_CAP | NS_R10_ABS_STARTS | NS_R11_SUM_OF_MAX | NS_R14_SPLITTABLE)) >
+            NS_GREEDY_LANES)
         return set_err(ctx, NS_ERR_ARG, "bad grid_hi_factor/flags");
     if ((p->flags & NS_NO_DIM_CAP) && p->M != 1) return set_err(ctx, NS_ERR_ARG, "NS_NO_DIM_CAP needs M == 1");
     if (columnwise) {
@@ -698,7 +700,10 @@ ns_status ns_score_plans(ns_ctx* ctx, const ns_tables* t, int32_t task, int32_t 
     if (!ctx->model.loaded) return set_err(ctx, NS_ERR_STATE, "no cost models loaded");
     if (D != ctx->model.D) return set_err(ctx, NS_ERR_ARG, "D differs from the loaded comm models' D");
     if (task < 0 || task >= t->n_tasks) return set_err(ctx, NS_ERR_ARG, "task out of range");
+    const uint32_t readings = (uint32_t)mode & (NS_R10_ABS_STARTS | NS_R11_SUM_OF_MAX);
+    mode &= ~(int32_t)(NS_R10_ABS_STARTS | NS_R11_SUM_OF_MAX);
     if (mode != NS_SCORE_FP64 && mode != NS_SCORE_TF32X3) return set_err(ctx, NS_ERR_ARG, "bad mode");
+    ctx->rflags = readings;
     if (mode == NS_SCORE_TF32X3 && D > 16) return set_err(ctx, NS_ERR_ARG, "NS_SCORE_TF32X3 needs D <= 16");
     // validate the column plan against the evolving dims
     if (n_col > 0) {

@@ -130,6 +130,7 @@ struct ns_ctx {
     void* nccl = nullptr;    // ncclComm_t (also with nranks == 1: ns_comm_init with an id)
     int nranks = 1, rank = 0;
     bool emulated = false;   // ns_comm_init(id == NULL): all ranks' blocks computed in-process (test hook)
+    uint32_t rflags = 0;                     // NS_R10/R11 readings of the current search / score call
     unsigned long long* d_stats = nullptr;   // [kStats] device counters (reset by ns_profile)
     uint64_t trajectories = 0;               // greedy trajectories launched (host count)
     bool host_comm_on = false;    // ns_comm_init_host: collectives through caller callbacks on host buffers

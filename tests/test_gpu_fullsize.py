@@ -262,3 +262,46 @@ def test_bench_launch_C5_batch(ns, ctx):
                          int(out["grid_index"][i]), float(out["cost"][i]), c["M"])
             certified += 1
     assert certified == 2
+
+
+READINGS = [("R10 absolute starts", 16, dict(abs_starts=True)),
+            ("R11 sum of maxima", 32, dict(sum_of_max=True)),
+            ("R14 splittable only", 64, dict(splittable_only=True)),
+            ("R10 + R11 + R14", 112, dict(abs_starts=True, sum_of_max=True, splittable_only=True))]
+
+
+@pytest.mark.parametrize("name,bits,kw", READINGS, ids=[r[0] for r in READINGS])
+def test_alternative_readings_match_oracle(ns, ctx, name, bits, kw):
+    """The alternative readings (flags NS_R10_ABS_STARTS, NS_R11_SUM_OF_MAX,
+    NS_R14_SPLITTABLE) on both sides: column-wise searches
+    identical to the oracle's beam search under the same reading, and
+    ns_score_plans (fp64 and TF32x3) against the oracle's plan cost."""
+    w = gen_weights(4, "mono", seed=5)
+    rng = np.random.default_rng(bits)
+    tasks = [small_task(rng, 14, 4) for _ in range(6)]
+    for t in tasks:   # some unsplittable dims so R14 matters
+        t.dims[::3] = 12
+    ns.ns_load_cost_models(ctx, w)
+    desc, off, caps = ns.table_descs(tasks)
+    tabs = ns.ns_featurize_tables(ctx, desc, off, caps)
+    out = ns.ns_shard_columnwise(ctx, tabs, 4, N=2, K=2, L=2, M=5, readings=bits)
+    for i, task in enumerate(tasks):
+        emb = om.TableEmbeddings(w, task)
+        log = osr.DecisionLog()
+        r = osr.beam_search(w, emb, task, N=2, K=2, L=2, M=5, log=log, **kw)
+        exp = dict(cost=r.cost, col_plan=r.col_plan, assign=r.assign, grid_index=r.grid_index, work=r.work)
+        if log.min_margin() >= RTOL:
+            _compare(out, i, task, w, exp, log.min_margin(), 5)
+    base = ns.ns_shard_columnwise(ctx, tabs, 4, N=2, K=2, L=2, M=5)
+    # the reading changes something (the test is not vacuous)
+    assert not (np.array_equal(base["cost"], out["cost"]) and np.array_equal(base["n_scores"], out["n_scores"]))
+    if bits & 48:
+        A = np.random.default_rng(7).integers(0, 4, size=(300, tasks[0].T)).astype(np.int8)
+        emb = om.TableEmbeddings(w, tasks[0])
+        tables = osr.apply_col_plan(tasks[0], [])
+        ref = np.array([om.plan_cost(w, emb, tables, a.tolist(), 4, bool(bits & 16), bool(bits & 32))[0] for a in A])
+        c64, _, _ = ns.ns_score_plans(ctx, tabs, 0, 4, [], A, mode=ns.NS_SCORE_FP64 | (bits & 48))
+        np.testing.assert_allclose(c64, ref, rtol=1e-12)
+        c32, _, _ = ns.ns_score_plans(ctx, tabs, 0, 4, [], A, mode=ns.NS_SCORE_TF32X3 | (bits & 48))
+        np.testing.assert_allclose(c32, ref, rtol=1e-5)
+    tabs.free()

@@ -181,3 +181,36 @@ def test_split_conserves_dims_and_bytes():
     if four:
         with pytest.raises(ValueError):
             osr.apply_col_plan(task, [four[0]])
+
+
+# ---------------------------------------------------- alternative readings
+def test_reduce_plan_readings():
+    # R11 max of per-device sums vs the alternative sum of the
+    # per-term maxima: hand values
+    comp, fwd, bwd = np.array([1.0, 3.0]), np.array([5.0, 0.0]), np.array([0.0, 0.5])
+    assert om.reduce_plan(comp, fwd, bwd) == 6.0
+    assert om.reduce_plan(comp, fwd, bwd, sum_of_max=True) == 8.5
+    # the alternative is never below the default; equal when one device dominates every term
+    rng = np.random.default_rng(0)
+    for _ in range(50):
+        c, f, b = rng.uniform(0, 5, (3, 4))
+        assert om.reduce_plan(c, f, b, True) >= om.reduce_plan(c, f, b)
+    c = np.array([3.0, 1.0]); f = np.array([2.0, 1.0]); b = np.array([4.0, 0.0])
+    assert om.reduce_plan(c, f, b, True) == om.reduce_plan(c, f, b) == 9.0
+
+
+def test_hand_example_absolute_starts(golden_hand):
+    # R10 alternative on the hand example (tests/golden/hand_example.json):
+    # forward starts = comp = [3.12, 1.35] -> fwd = 0.5*start + 0.01*devdim + 1
+    # = [1.56 + 0.72 + 1, 0.675 + 0.60 + 1] = [3.28, 2.275]; bwd unchanged
+    # [1.864, 1.720]; cost = max(3.12 + 3.28 + 1.864, 1.35 + 2.275 + 1.72) = 8.264
+    g = golden_hand
+    w, task = hand_weights(g), hand_task(g)
+    emb = om.TableEmbeddings(w, task)
+    tables = [(s, int(task.dims[s])) for s in range(task.T)]
+    cost, comp, fwd, bwd, _ = om.plan_cost(w, emb, tables, g["expected"]["assign"], 2, abs_starts=True)
+    np.testing.assert_allclose(fwd, [3.28, 2.275], rtol=1e-12)
+    np.testing.assert_allclose(bwd, [1.864, 1.720], rtol=1e-12)
+    assert cost == pytest.approx(8.264, rel=1e-12)
+    # and the sum-of-maxima reduction: 3.12 + 3.28 + 1.864 (device 0 dominates)
+    assert om.plan_cost(w, emb, tables, g["expected"]["assign"], 2, True, True)[0] == pytest.approx(8.264, rel=1e-12)

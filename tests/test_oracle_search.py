@@ -280,3 +280,22 @@ def test_no_dim_cap_reading():
         n_cap += math.isfinite(osr.greedy_grid_search(w, e, t, [], 1).cost)
         n_free += math.isfinite(osr.greedy_grid_search(w, e, t, [], 1, dim_cap=False).cost)
     assert n_free >= n_cap and n_free == 12
+
+
+def test_candidates_splittable_only_reading(golden_hand):
+    # R14 alternative (flag NS_R14_SPLITTABLE): rank only splittable tables.
+    # Hand example tables a (dim 60, unsplittable: 60 % 8 = 4), b (40), t (32),
+    # single costs 1.35 / 1.90 / 1.32, bytes proportional to dim (equal hash).
+    # N = 1, literal: by cost [b], by size [a] -> [b, a] -> a dropped -> [b];
+    # N = 1, splittable only: by cost [b], by size [b] -> [b].
+    # N = 2, literal: by cost [b, a], by size [a, b] -> [b, a] -> [b];
+    # N = 2, splittable only: by cost [b, t], by size [b, t] -> [b, t].
+    g = golden_hand
+    w, task = hand_weights(g), hand_task(g)
+    emb = om.TableEmbeddings(w, task)
+    tables = osr.apply_col_plan(task, [])
+    singles = osr.single_costs(w, emb, tables)
+    assert osr.beam_candidates(task, tables, singles, 1) == [1]
+    assert osr.beam_candidates(task, tables, singles, 1, splittable_only=True) == [1]
+    assert osr.beam_candidates(task, tables, singles, 2) == [1]
+    assert osr.beam_candidates(task, tables, singles, 2, splittable_only=True) == [1, 2]
