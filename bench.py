@@ -867,6 +867,16 @@ def embag_rate(ns, ctx, torch):
 
     fwd = med(lambda: ns.ns_embedding_bag_forward(ctx, shard, B, out))
     bwd = med(lambda: ns.ns_embedding_bag_backward_sgd(ctx, shard, B, gout, 1e-4))
+    # the whole model-parallel step through the exchange calls (one rank: the
+    # all-to-alls are the self blocks)
+    recv = torch.empty_like(out)
+    gbuf = torch.empty_like(out)
+
+    def xstep():
+        ns.ns_embedding_bag_forward_exchange(ctx, shard, B, [C], out, recv)
+        ns.ns_embedding_bag_backward_exchange_sgd(ctx, shard, B, [C], gout.view(-1), gbuf, 1e-4)
+
+    step_x = med(xstep)
     peaks = {}
     try:
         peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
@@ -877,6 +887,9 @@ def embag_rate(ns, ctx, torch):
                      f"{sum(int(task.hash[k]) * int(task.dims[k]) * 4 for k in mine) / 2**30:.2f} GiB of fp32 rows",
             "batch": B, "forward_ms_median": fwd, "backward_sgd_ms_median": bwd,
             "cost_ms": fwd + bwd,
+            "exchange_step_ms_median": step_x,
+            "exchange_step": "forward + all-to-all + all-to-all + backward/SGD through "
+                             "ns_embedding_bag_*_exchange at one rank (self blocks)",
             "forward_gbs": algo_f / (fwd * 1e-3) / 1e9, "backward_gbs": algo_b / (bwd * 1e-3) / 1e9,
             "forward_frac_hbm": algo_f / (fwd * 1e-3) / 1e9 / hbm,
             "backward_frac_hbm": algo_b / (bwd * 1e-3) / 1e9 / hbm,

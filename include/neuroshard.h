@@ -354,6 +354,33 @@ ns_status ns_embedding_bag_forward(ns_ctx* ctx, const ns_bag_table* tables, int3
 ns_status ns_embedding_bag_backward_sgd(ns_ctx* ctx, const ns_bag_table* tables, int32_t n_tables, int32_t batch,
                                         const float* grad_out, float lr);
 
+/* SURVEY §8(f) row F3, multi-GPU half: the model-parallel embedding step of
+ * DLRM training with its two all-to-alls (forward computation,
+ * forward all-to-all, backward all-to-all, backward computation; the paper
+ * times each and takes the max over GPUs, App. A.3).  Collective after
+ * ns_comm_init / ns_comm_init_host (host transport: needs the alltoallv
+ * callback); without a communicator it is the one-rank case (the exchange is
+ * a copy).  R = nranks, batch % R == 0, Bl = batch / R; cols [R] HOST int32,
+ * cols[r] = sum of the dims of rank r's tables (cols[rank] must equal this
+ * shard's sum).  Rank q's samples are rows q*Bl .. (q+1)*Bl - 1 of the global
+ * batch.  Every buffer is DEVICE memory.
+ * forward_exchange: out [batch][cols[rank]] = ns_embedding_bag_forward of this
+ *   shard for the whole batch (written, and it is the send buffer: sample
+ *   block q is the contiguous block sent to rank q); recv [sum_r Bl*cols[r]]
+ *   rank-blocked: block r (at float offset Bl * sum_{r'<r} cols[r']) is
+ *   [Bl][cols[r]], the pooled rows of rank r's tables for this rank's samples.
+ * backward_exchange_sgd: grad_recv has recv's layout (the gradient w.r.t. this
+ *   rank's samples' pooled rows of every rank's tables); block r goes back to
+ *   rank r, the blocks from all ranks land in grad_out [batch][cols[rank]]
+ *   (device scratch, written), then ns_embedding_bag_backward_sgd(grad_out).
+ * Errors: NS_ERR_ARG (layout), NS_ERR_STATE (emulated ranks or a host
+ * transport without alltoallv), NS_ERR_NCCL; outputs undefined on error. */
+ns_status ns_embedding_bag_forward_exchange(ns_ctx* ctx, const ns_bag_table* tables, int32_t n_tables, int32_t batch,
+                                            const int32_t* cols, float* out, float* recv);
+ns_status ns_embedding_bag_backward_exchange_sgd(ns_ctx* ctx, const ns_bag_table* tables, int32_t n_tables,
+                                                 int32_t batch, const int32_t* cols, const float* grad_recv,
+                                                 float* grad_out, float lr);
+
 /* ------------------------------------------------------------ multi-GPU */
 /* 128-byte NCCL unique id (call on rank 0, broadcast by any means). */
 ns_status ns_comm_unique_id(unsigned char id_out[128]);
@@ -377,7 +404,7 @@ ns_status ns_comm_init(ns_ctx* ctx, int32_t nranks, int32_t rank, const unsigned
 /* Caller-provided transport for the collectives (e.g. MPI or a
  * torch.distributed gloo group): the library stages the data in host memory
  * and calls these from the calling thread, in the same order on every rank.
- * Both return 0 on success (anything else -> NS_ERR_NCCL).
+ * Each returns 0 on success (anything else -> NS_ERR_NCCL).
  *   allgather: send = this rank's bytes_per_rank bytes; recv = nranks blocks in
  *              rank order (recv + rank * bytes_per_rank may alias send).
  *   allreduce: element-wise over count elements in place; op NS_COMM_MIN_U64
@@ -388,6 +415,11 @@ typedef struct {
     void* user;
     int (*allgather)(void* user, const void* send, void* recv, size_t bytes_per_rank);
     int (*allreduce)(void* user, void* buf, size_t count, int op);
+    /* all-to-all (ns_embedding_bag_*_exchange only; may be NULL otherwise):
+     * send = nranks blocks in peer order, block q (send_bytes[q] bytes) goes to
+     * rank q; recv = nranks blocks in peer order, block r (recv_bytes[r] bytes)
+     * comes from rank r. */
+    int (*alltoallv)(void* user, const void* send, const size_t* send_bytes, void* recv, const size_t* recv_bytes);
 } ns_host_comm;
 /* Like ns_comm_init, with the collectives going through `comm` (copied; the
  * function pointers and user data must stay valid until the ctx is destroyed

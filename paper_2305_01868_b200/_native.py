@@ -41,10 +41,13 @@ class ns_compute_model(C.Structure):
 
 _ALLGATHER_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_size_t)
 _ALLREDUCE_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_size_t, C.c_int)
+_ALLTOALLV_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.POINTER(C.c_size_t), C.c_void_p,
+                            C.POINTER(C.c_size_t))
 
 
 class ns_host_comm(C.Structure):
-    _fields_ = [("user", C.c_void_p), ("allgather", _ALLGATHER_FN), ("allreduce", _ALLREDUCE_FN)]
+    _fields_ = [("user", C.c_void_p), ("allgather", _ALLGATHER_FN), ("allreduce", _ALLREDUCE_FN),
+                ("alltoallv", _ALLTOALLV_FN)]
 
 
 class ns_stats(C.Structure):
@@ -105,6 +108,9 @@ def _load():
         "ns_pretrain_comm_step": ([vp, i32, vp, vp, vp, i64, C.c_double, vp, vp, vp, i32, vp], C.c_int),
         "ns_embedding_bag_forward": ([vp, C.POINTER(ns_bag_table), i32, i32, vp], C.c_int),
         "ns_embedding_bag_backward_sgd": ([vp, C.POINTER(ns_bag_table), i32, i32, vp, C.c_float], C.c_int),
+        "ns_embedding_bag_forward_exchange": ([vp, C.POINTER(ns_bag_table), i32, i32, vp, vp, vp], C.c_int),
+        "ns_embedding_bag_backward_exchange_sgd": ([vp, C.POINTER(ns_bag_table), i32, i32, vp, vp, vp, C.c_float],
+                                                   C.c_int),
     }
     for name, (args, res) in sig.items():
         f = getattr(lib, name)
@@ -120,7 +126,8 @@ EXPORTED = ["ns_create", "ns_destroy", "ns_last_error", "ns_set_stream", "ns_syn
             "ns_score_plans", "ns_shard_tablewise", "ns_shard_columnwise", "ns_comm_unique_id", "ns_comm_init",
             "ns_comm_init_host", "ns_stats_query", "ns_pretrain_compute_samples", "ns_pretrain_comm_samples",
             "ns_pretrain_compute_step", "ns_pretrain_comm_step", "ns_embedding_bag_forward",
-            "ns_embedding_bag_backward_sgd"]
+            "ns_embedding_bag_backward_sgd", "ns_embedding_bag_forward_exchange",
+            "ns_embedding_bag_backward_exchange_sgd"]
 
 
 def _check(ctx, status: int, allow_infeasible: bool = True) -> int:
@@ -373,21 +380,26 @@ NS_COMM_MAX_I8 = 1
 _HOST_COMMS = {}   # ctx -> (struct, callbacks): kept alive while the ctx uses them
 
 
-def ns_comm_init_host(ctx: int, nranks: int, rank: int, allgather, allreduce) -> None:
+def ns_comm_init_host(ctx: int, nranks: int, rank: int, allgather, allreduce, alltoallv=None) -> None:
     """Collectives through Python callbacks on host buffers (header:
     ns_host_comm).  ``allgather(send: np.ndarray[uint8], recv: np.ndarray[uint8])``
     fills recv (nranks blocks); ``allreduce(buf: np.ndarray, op)`` reduces in
-    place (uint64 min or int8 max).  Marshalling only."""
+    place (uint64 min or int8 max); ``alltoallv(send, send_bytes, recv,
+    recv_bytes)`` (uint8 arrays, per-peer byte counts; optional, needed by the
+    embedding-bag exchange).  Marshalling only."""
+    def _report():   # a failing callback is reported to the caller as NS_ERR_NCCL
+        import traceback
+        traceback.print_exc()
+        return 1
+
     def ag(user, send, recv, nbytes):
         try:
             s_ = np.ctypeslib.as_array((C.c_uint8 * nbytes).from_address(send))
             r_ = np.ctypeslib.as_array((C.c_uint8 * (nbytes * nranks)).from_address(recv))
             allgather(s_.copy(), r_)
             return 0
-        except BaseException:   # reported to the caller as NS_ERR_NCCL
-            import traceback
-            traceback.print_exc()
-            return 1
+        except BaseException:
+            return _report()
 
     def ar(user, buf, count, op):
         try:
@@ -396,13 +408,53 @@ def ns_comm_init_host(ctx: int, nranks: int, rank: int, allgather, allreduce) ->
             allreduce(b_, op)
             return 0
         except BaseException:
-            import traceback
-            traceback.print_exc()
-            return 1
+            return _report()
 
-    cb = ns_host_comm(None, _ALLGATHER_FN(ag), _ALLREDUCE_FN(ar))
+    def a2a(user, send, send_bytes, recv, recv_bytes):
+        try:
+            sb = [int(send_bytes[q]) for q in range(nranks)]
+            rb = [int(recv_bytes[q]) for q in range(nranks)]
+            s_ = np.ctypeslib.as_array((C.c_uint8 * max(sum(sb), 1)).from_address(send))[:sum(sb)]
+            r_ = np.ctypeslib.as_array((C.c_uint8 * max(sum(rb), 1)).from_address(recv))[:sum(rb)]
+            alltoallv(s_.copy(), sb, r_, rb)
+            return 0
+        except BaseException:
+            return _report()
+
+    cb = ns_host_comm(None, _ALLGATHER_FN(ag), _ALLREDUCE_FN(ar),
+                      _ALLTOALLV_FN(a2a) if alltoallv is not None else _ALLTOALLV_FN())
     _HOST_COMMS[ctx] = cb
     _check(ctx, LIB.ns_comm_init_host(ctx, nranks, rank, C.byref(cb)))
+
+
+def torch_host_alltoallv(group=None):
+    """alltoallv callback over a torch.distributed process group (gloo:
+    point-to-point send/recv of each peer's block, the self block copied)."""
+    import torch
+    import torch.distributed as dist
+
+    def alltoallv(send, send_bytes, recv, recv_bytes):
+        me = dist.get_rank(group)
+        so = np.concatenate([[0], np.cumsum(send_bytes)]).astype(np.int64)
+        ro = np.concatenate([[0], np.cumsum(recv_bytes)]).astype(np.int64)
+        reqs = []
+        for q in range(len(send_bytes)):
+            if q == me:
+                recv[ro[q]:ro[q + 1]] = send[so[q]:so[q + 1]]
+                continue
+            if send_bytes[q]:
+                reqs.append(dist.isend(torch.from_numpy(send[so[q]:so[q + 1]].copy()), q, group=group))
+        bufs = {}
+        for r in range(len(recv_bytes)):
+            if r != me and recv_bytes[r]:
+                bufs[r] = torch.empty(int(recv_bytes[r]), dtype=torch.uint8)
+                reqs.append(dist.irecv(bufs[r], r, group=group))
+        for rq in reqs:
+            rq.wait()
+        for r, t in bufs.items():
+            recv[ro[r]:ro[r + 1]] = t.numpy()
+
+    return alltoallv
 
 
 def torch_host_comm(group=None):
@@ -488,3 +540,23 @@ def ns_embedding_bag_forward(ctx: int, tables, batch: int, out) -> None:
 def ns_embedding_bag_backward_sgd(ctx: int, tables, batch: int, grad_out, lr: float) -> None:
     arr = _bag_tables(tables)
     _check(ctx, LIB.ns_embedding_bag_backward_sgd(ctx, arr, len(tables), batch, _dp(grad_out), lr))
+
+
+def _cols_arg(cols):
+    a = (C.c_int32 * len(cols))(*[int(c) for c in cols])
+    return a
+
+
+def ns_embedding_bag_forward_exchange(ctx: int, tables, batch: int, cols, out, recv) -> None:
+    """Forward + all-to-all (header: ns_embedding_bag_forward_exchange); cols
+    = per-rank sums of table dims (host list)."""
+    arr = _bag_tables(tables)
+    _check(ctx, LIB.ns_embedding_bag_forward_exchange(ctx, arr, len(tables), batch, _cols_arg(cols), _dp(out),
+                                                      _dp(recv)))
+
+
+def ns_embedding_bag_backward_exchange_sgd(ctx: int, tables, batch: int, cols, grad_recv, grad_out,
+                                           lr: float) -> None:
+    arr = _bag_tables(tables)
+    _check(ctx, LIB.ns_embedding_bag_backward_exchange_sgd(ctx, arr, len(tables), batch, _cols_arg(cols),
+                                                           _dp(grad_recv), _dp(grad_out), lr))

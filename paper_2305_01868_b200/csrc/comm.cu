@@ -10,6 +10,7 @@
 
 #include <cstring>
 #include <string>
+#include <vector>
 
 #include "ns_internal.cuh"
 
@@ -24,6 +25,10 @@ struct NcclApi {
     ncclResult_t (*AllGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
     ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
                               cudaStream_t) = nullptr;
+    ncclResult_t (*GroupStart)() = nullptr;
+    ncclResult_t (*GroupEnd)() = nullptr;
+    ncclResult_t (*Send)(const void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*Recv)(void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
     const char* (*GetErrorString)(ncclResult_t) = nullptr;
 };
 
@@ -48,7 +53,12 @@ NcclApi& api() {
     a.AllGather = (decltype(a.AllGather))dlsym(h, "ncclAllGather");
     a.AllReduce = (decltype(a.AllReduce))dlsym(h, "ncclAllReduce");
     a.GetErrorString = (decltype(a.GetErrorString))dlsym(h, "ncclGetErrorString");
-    a.ok = a.GetUniqueId && a.CommInitRank && a.CommDestroy && a.AllGather && a.AllReduce && a.GetErrorString;
+    a.GroupStart = (decltype(a.GroupStart))dlsym(h, "ncclGroupStart");
+    a.GroupEnd = (decltype(a.GroupEnd))dlsym(h, "ncclGroupEnd");
+    a.Send = (decltype(a.Send))dlsym(h, "ncclSend");
+    a.Recv = (decltype(a.Recv))dlsym(h, "ncclRecv");
+    a.ok = a.GetUniqueId && a.CommInitRank && a.CommDestroy && a.AllGather && a.AllReduce && a.GetErrorString &&
+           a.GroupStart && a.GroupEnd && a.Send && a.Recv;
     if (!a.ok) a.why = "libnccl.so.2 lacks required symbols";
     return a;
 }
@@ -143,6 +153,49 @@ ns_status comm_allreduce_min_u64(ns_ctx* ctx, uint64_t* buf, size_t count) {
 
 ns_status comm_allreduce_max_i8(ns_ctx* ctx, int8_t* buf, size_t count) {
     return allreduce(ctx, buf, count, NS_COMM_MAX_I8);
+}
+
+// All-to-all with per-peer sizes: send block q (send_bytes[q] bytes, blocks
+// contiguous in peer order) goes to rank q; the block from rank r lands at
+// recv + sum_{r' < r} recv_bytes[r'].  NCCL: one group of ncclSend/ncclRecv
+// pairs (the self pair included), so every transfer is in flight at once.
+ns_status comm_alltoallv(ns_ctx* ctx, const void* send, const size_t* send_bytes, void* recv,
+                         const size_t* recv_bytes) {
+    const int R = ctx->nranks;
+    if (ctx->emulated) return set_err(ctx, NS_ERR_STATE, "all-to-all needs real ranks (not emulated)");
+    std::vector<size_t> so(R + 1, 0), ro(R + 1, 0);
+    for (int q = 0; q < R; ++q) {
+        so[q + 1] = so[q] + send_bytes[q];
+        ro[q + 1] = ro[q] + recv_bytes[q];
+    }
+    if (!ctx->nccl && !ctx->host_comm_on) {   // one rank: the block to self
+        if (send_bytes[0] != recv_bytes[0]) return set_err(ctx, NS_ERR_ARG, "all-to-all: self block sizes differ");
+        if (send_bytes[0])
+            NS_CUDA(ctx, cudaMemcpyAsync(recv, send, send_bytes[0], cudaMemcpyDeviceToDevice, ctx->stream));
+        return NS_OK;
+    }
+    if (ctx->nccl) {
+        ncclResult_t r = api().GroupStart();
+        for (int q = 0; q < R && r == ncclSuccess; ++q) {
+            if (send_bytes[q]) r = api().Send((const char*)send + so[q], send_bytes[q], ncclUint8, q, (ncclComm_t)ctx->nccl, ctx->stream);
+            if (r == ncclSuccess && recv_bytes[q])
+                r = api().Recv((char*)recv + ro[q], recv_bytes[q], ncclUint8, q, (ncclComm_t)ctx->nccl, ctx->stream);
+        }
+        const ncclResult_t e = api().GroupEnd();
+        if (r != ncclSuccess) return nccl_err(ctx, r, "ncclSend/ncclRecv");
+        if (e != ncclSuccess) return nccl_err(ctx, e, "ncclGroupEnd");
+        return NS_OK;
+    }
+    if (!ctx->host_comm.alltoallv) return set_err(ctx, NS_ERR_STATE, "host transport without an alltoallv callback");
+    char* h = host_stage(ctx, so[R] + ro[R]);
+    if (!h) return set_err(ctx, NS_ERR_NOMEM, "pinned comm staging");
+    if (so[R]) NS_CUDA(ctx, cudaMemcpyAsync(h, send, so[R], cudaMemcpyDeviceToHost, ctx->stream));
+    NS_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+    if (ctx->host_comm.alltoallv(ctx->host_comm.user, h, send_bytes, h + so[R], recv_bytes) != 0)
+        return set_err(ctx, NS_ERR_NCCL, "host alltoallv callback failed");
+    if (ro[R]) NS_CUDA(ctx, cudaMemcpyAsync(recv, h + so[R], ro[R], cudaMemcpyHostToDevice, ctx->stream));
+    NS_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+    return NS_OK;
 }
 
 }  // namespace ns

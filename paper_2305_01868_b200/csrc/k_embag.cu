@@ -198,3 +198,69 @@ ns_status ns_embedding_bag_backward_sgd(ns_ctx* ctx, const ns_bag_table* tables,
 }
 
 }  // extern "C"
+
+// ---------------------------------------------------------------- exchange
+// The model-parallel embedding step of DLRM training: "each GPU
+// queries the other GPUs with its sparse features to look up the embeddings
+// from their tables (forward computation) and obtain the embeddings through an
+// all-to-all communication (forward communication). In the backward pass, the
+// gradients are sent back to the GPUs with another all-to-all communication
+// (backward communication) and applied to the embeddings (backward
+// computation)".  Layouts are chosen so that neither all-to-all needs a pack
+// or unpack kernel: this shard's pooled rows [batch][cols[rank]] are already
+// nranks contiguous per-destination blocks (sample block q goes to rank q),
+// and the receive side is rank-blocked (block r = [Bl][cols[r]], Bl = batch /
+// nranks), which is also the layout the backward sends from.
+namespace {
+ns_status exchange_sizes(ns_ctx* ctx, int batch, const int32_t* cols, int local_cols, std::vector<size_t>& mine,
+                         std::vector<size_t>& theirs) {
+    const int R = ctx->nranks;
+    if (!cols) return set_err(ctx, NS_ERR_ARG, "exchange: cols[nranks] needed");
+    if (batch % R != 0) return set_err(ctx, NS_ERR_ARG, "exchange: batch must be a multiple of nranks");
+    if (cols[ctx->rank] != local_cols)
+        return set_err(ctx, NS_ERR_ARG, "exchange: cols[rank] must equal the sum of this shard's dims");
+    const size_t Bl = (size_t)(batch / R);
+    mine.assign(R, Bl * (size_t)local_cols * sizeof(float));
+    theirs.resize(R);
+    for (int r = 0; r < R; ++r) {
+        if (cols[r] < 0) return set_err(ctx, NS_ERR_ARG, "exchange: cols[r] < 0");
+        theirs[r] = Bl * (size_t)cols[r] * sizeof(float);
+    }
+    return NS_OK;
+}
+}  // namespace
+
+extern "C" {
+
+ns_status ns_embedding_bag_forward_exchange(ns_ctx* ctx, const ns_bag_table* tables, int32_t n_tables, int32_t batch,
+                                            const int32_t* cols, float* out, float* recv) {
+    if (!ctx) return NS_ERR_ARG;
+    if (!recv || !is_device_ptr(recv)) return set_err(ctx, NS_ERR_ARG, "ns_embedding_bag_forward_exchange: recv device");
+    ns_status s = ns_embedding_bag_forward(ctx, tables, n_tables, batch, out);
+    if (s != NS_OK) return s;
+    int local = 0;
+    for (int k = 0; k < n_tables; ++k) local += tables[k].dim;
+    std::vector<size_t> send_b, recv_b;
+    if ((s = exchange_sizes(ctx, batch, cols, local, send_b, recv_b)) != NS_OK) return s;
+    return comm_alltoallv(ctx, out, send_b.data(), recv, recv_b.data());
+}
+
+ns_status ns_embedding_bag_backward_exchange_sgd(ns_ctx* ctx, const ns_bag_table* tables, int32_t n_tables,
+                                                 int32_t batch, const int32_t* cols, const float* grad_recv,
+                                                 float* grad_out, float lr) {
+    if (!ctx) return NS_ERR_ARG;
+    if (!tables || n_tables < 1 || !grad_recv || !grad_out || !is_device_ptr(grad_recv) || !is_device_ptr(grad_out))
+        return set_err(ctx, NS_ERR_ARG, "ns_embedding_bag_backward_exchange_sgd: device grad_recv, grad_out");
+    cudaSetDevice(ctx->device);
+    int local = 0;
+    for (int k = 0; k < n_tables; ++k) local += tables[k].dim;
+    std::vector<size_t> mine, theirs;
+    ns_status s = exchange_sizes(ctx, batch, cols, local, mine, theirs);
+    if (s != NS_OK) return s;
+    // the reverse exchange: block r of grad_recv goes back to rank r; rank q's
+    // block lands at sample rows q * Bl ... of grad_out
+    if ((s = comm_alltoallv(ctx, grad_recv, theirs.data(), grad_out, mine.data())) != NS_OK) return s;
+    return ns_embedding_bag_backward_sgd(ctx, tables, n_tables, batch, grad_out, lr);
+}
+
+}  // extern "C"

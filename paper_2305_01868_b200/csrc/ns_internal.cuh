@@ -222,6 +222,7 @@ CommParams comm_params(const ns_ctx* ctx);
 ns_status comm_allgather(ns_ctx* ctx, const void* send, void* recv, size_t bytes_per_rank);
 ns_status comm_allreduce_min_u64(ns_ctx* ctx, uint64_t* dev_buf, size_t count);
 ns_status comm_allreduce_max_i8(ns_ctx* ctx, int8_t* dev_buf, size_t count);
+ns_status comm_alltoallv(ns_ctx* ctx, const void* send, const size_t* send_bytes, void* recv, const size_t* recv_bytes);
 // true when search / score calls are collective over ranks (any backend,
 // including a 1-rank NCCL communicator and emulated ranks)
 bool comm_collective(const ns_ctx* ctx);

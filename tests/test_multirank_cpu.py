@@ -88,3 +88,46 @@ def test_host_comm_callbacks_world2():
         assert recv == [0, 1, 2, 3, 4, 10, 11, 12, 13, 14]
         assert keys == [0xFFFF000000000000 - 1, 5, 0x8000000000000000]
         assert row == [3, 0, -1]
+
+
+def _a2a_worker(rank, world, port, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    import numpy as np
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from oracle import embag as oe
+    from paper_2305_01868_b200._native import torch_host_alltoallv
+    # the embedding exchange's host transport on the layouts the library
+    # uses: this rank's [B][cols[rank]] pooled rows as nranks sample blocks
+    cols, B = [3, 1, 2][:world], 6
+    X = np.arange(B * sum(cols), dtype=np.float32).reshape(B, sum(cols))   # the global pooled matrix
+    c0 = sum(cols[:rank])
+    mine = np.ascontiguousarray(X[:, c0:c0 + cols[rank]])
+    Bl = B // world
+    send_b = [Bl * cols[rank] * 4] * world
+    recv_b = [Bl * c * 4 for c in cols]
+    recv = np.zeros(sum(recv_b), np.uint8)
+    torch_host_alltoallv()(mine.view(np.uint8).reshape(-1), send_b, recv, recv_b)
+    got = recv.view(np.float32)
+    ok = np.array_equal(got, oe.exchange_forward(X.astype(np.float64), cols)[rank])
+    q.put((rank, bool(ok)))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_host_alltoallv_callback_gloo(world):
+    """The torch.distributed (gloo) all-to-all callback behind the embedding
+    exchange (ns_host_comm.alltoallv): per-peer block sizes differ, the self
+    block is copied, and every rank ends with the oracle's rank-blocked
+    receive buffer (oracle/embag.exchange_forward)."""
+    port = _free_port()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    ps = [ctx.Process(target=_a2a_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in ps:
+        p.start()
+    res = dict(q.get(timeout=120) for _ in range(world))
+    for p in ps:
+        p.join(timeout=60)
+    assert all(res[r] for r in range(world)), res

@@ -67,3 +67,44 @@ def test_zipf_indices_in_range_and_skewed():
     o, i = gen_bag_indices(10_000, 20.0, 0.0, 2000, rng)
     _, counts = np.unique(i, return_counts=True)
     assert counts.max() < 30                            # skew 0: near uniform
+
+
+# ------------------------------------------------------------- the exchanges
+def test_exchange_hand_example():
+    """B = 4 samples, R = 2 ranks, rank 0 owns 1 column, rank 1 two
+    (PAPER.md:49): rank 0 receives rows 0-1 of every rank's columns, rank 1
+    rows 2-3, each rank-blocked.  Expected values written out by hand."""
+    pooled = np.arange(12, dtype=np.float64).reshape(4, 3)
+    r0, r1 = oe.exchange_forward(pooled, [1, 2])
+    assert r0.tolist() == [0, 3, 1, 2, 4, 5]
+    assert r1.tolist() == [6, 9, 7, 8, 10, 11]
+    g0, g1 = oe.exchange_backward([r0, r1], [1, 2])
+    assert g0.tolist() == [[0], [3], [6], [9]]
+    assert g1.tolist() == [[1, 2], [4, 5], [7, 8], [10, 11]]
+
+
+def test_exchange_elementwise_and_round_trip():
+    """Every received element is the pooled element its (rank, block, row,
+    column) names (an index loop written independently of the slicing), and
+    the backward exchange inverts the forward one (zero-width ranks too)."""
+    rng = np.random.default_rng(5)
+    for cols, B in (([5, 0, 7], 9), ([3], 4), ([2, 2, 2, 2], 8)):
+        R = len(cols)
+        X = rng.normal(size=(B, sum(cols)))
+        recv = oe.exchange_forward(X, cols)
+        Bl = B // R
+        for q in range(R):
+            pos = 0
+            for r in range(R):
+                c0 = sum(cols[:r])
+                for i in range(Bl):
+                    for j in range(cols[r]):
+                        assert recv[q][pos] == X[q * Bl + i, c0 + j]
+                        pos += 1
+            assert pos == len(recv[q])
+        back = oe.exchange_backward(recv, cols)
+        for r in range(R):
+            np.testing.assert_array_equal(back[r], X[:, sum(cols[:r]):sum(cols[:r]) + cols[r]])
+    # one rank: the exchange is the identity
+    X = rng.normal(size=(6, 4))
+    np.testing.assert_array_equal(oe.exchange_forward(X, [4])[0], X.reshape(-1))
