@@ -274,6 +274,29 @@ ns_status ns_shard_tablewise(ns_ctx* ctx, const ns_tables* tables, int32_t D,
 ns_status ns_shard_columnwise(ns_ctx* ctx, const ns_tables* tables, int32_t D,
                               const ns_search_params* params, ns_plan_batch* out);
 
+/* ------------------------------------------------------------- workspace */
+/* Caller-owned device scratch (e.g. a torch.uint8 CUDA tensor).
+ * By default each ctx keeps a grow-only arena of its own (cudaMalloc).  After
+ * ns_set_workspace(ctx, ptr, bytes) every call carves its scratch from
+ * [ptr, ptr + bytes) instead and never allocates device memory: a call whose
+ * scratch does not fit returns NS_ERR_NOMEM, ns_last_error naming the bytes
+ * needed.  ptr must be 256-byte aligned device memory of the ctx's device;
+ * the caller keeps it alive and unchanged while the ctx may use it (until
+ * ns_set_workspace(ctx, NULL, 0), which returns to the internal arena, or
+ * ns_destroy).  The call synchronises the ctx stream and frees the internal
+ * arena.  Sizes: ns_search_workspace_bytes for ns_shard_* on a batch of
+ * n_tasks tasks whose longest table list has T_max tables (columnwise = 0
+ * for ns_shard_tablewise, 1 for ns_shard_columnwise; depends on the ctx's
+ * ranks), ns_score_workspace_bytes for ns_score_plans with P plans of
+ * T_prime = T + n_col tables (assign_on_device: the assignments are device
+ * memory).  Other calls (pre-training, embedding bag) need a few KB to MB;
+ * their error message names the size. */
+ns_status ns_set_workspace(ns_ctx* ctx, void* device_ptr, size_t bytes);
+ns_status ns_search_workspace_bytes(ns_ctx* ctx, int32_t n_tasks, int32_t T_max, int32_t D,
+                                    const ns_search_params* params, int32_t columnwise, size_t* bytes_out);
+ns_status ns_score_workspace_bytes(ns_ctx* ctx, int32_t T_prime, int32_t D, int64_t P, int32_t assign_on_device,
+                                   size_t* bytes_out);
+
 /* ------------------------------------------------------------ pre-training */
 /* generate cost samples and train the cost models on
  * the GPU (§3.1-3.2, App. B Alg. 3-5, App. C, App. F).  Every

@@ -108,6 +108,10 @@ def _load():
         "ns_pretrain_comm_step": ([vp, i32, vp, vp, vp, i64, C.c_double, vp, vp, vp, i32, vp], C.c_int),
         "ns_embedding_bag_forward": ([vp, C.POINTER(ns_bag_table), i32, i32, vp], C.c_int),
         "ns_embedding_bag_backward_sgd": ([vp, C.POINTER(ns_bag_table), i32, i32, vp, C.c_float], C.c_int),
+        "ns_set_workspace": ([vp, vp, C.c_size_t], C.c_int),
+        "ns_search_workspace_bytes": ([vp, i32, i32, i32, C.POINTER(ns_search_params), i32,
+                                       C.POINTER(C.c_size_t)], C.c_int),
+        "ns_score_workspace_bytes": ([vp, i32, i32, i64, i32, C.POINTER(C.c_size_t)], C.c_int),
         "ns_embedding_bag_forward_exchange": ([vp, C.POINTER(ns_bag_table), i32, i32, vp, vp, vp], C.c_int),
         "ns_embedding_bag_backward_exchange_sgd": ([vp, C.POINTER(ns_bag_table), i32, i32, vp, vp, vp, C.c_float],
                                                    C.c_int),
@@ -127,7 +131,8 @@ EXPORTED = ["ns_create", "ns_destroy", "ns_last_error", "ns_set_stream", "ns_syn
             "ns_comm_init_host", "ns_stats_query", "ns_pretrain_compute_samples", "ns_pretrain_comm_samples",
             "ns_pretrain_compute_step", "ns_pretrain_comm_step", "ns_embedding_bag_forward",
             "ns_embedding_bag_backward_sgd", "ns_embedding_bag_forward_exchange",
-            "ns_embedding_bag_backward_exchange_sgd"]
+            "ns_embedding_bag_backward_exchange_sgd", "ns_set_workspace", "ns_search_workspace_bytes",
+            "ns_score_workspace_bytes"]
 
 
 def _check(ctx, status: int, allow_infeasible: bool = True) -> int:
@@ -358,6 +363,37 @@ def ns_shard_columnwise(ctx: int, tables: Tables, D: int, N: int = 10, K: int = 
     st = _check(ctx, LIB.ns_shard_columnwise(ctx, tables.handle, D, C.byref(p), C.byref(pb)))
     out["status"] = st
     return out
+
+
+# ----------------------------------------------------------------- workspace
+_WORKSPACES = {}   # ctx -> the caller's tensor (kept alive while the ctx may use it)
+
+
+def ns_set_workspace(ctx: int, buf) -> None:
+    """Caller-owned device scratch (header: ns_set_workspace): ``buf`` is a
+    CUDA tensor (e.g. torch.empty(n, dtype=torch.uint8, device="cuda")) or None
+    to return to the library's own arena.  Marshalling only."""
+    if buf is None:
+        _check(ctx, LIB.ns_set_workspace(ctx, None, 0))
+        _WORKSPACES.pop(ctx, None)
+        return
+    _check(ctx, LIB.ns_set_workspace(ctx, _dp(buf), buf.numel() * buf.element_size()))
+    _WORKSPACES[ctx] = buf
+
+
+def ns_search_workspace_bytes(ctx: int, n_tasks: int, T_max: int, D: int, columnwise: bool, N: int = 10,
+                              K: int = 3, L: int = 10, M: int = 11, hi: float = 1.5, greedy: int = NS_GREEDY_AUTO) -> int:
+    n = C.c_size_t(0)
+    p = _params(N, K, L if columnwise else 0, M, hi, greedy)
+    _check(ctx, LIB.ns_search_workspace_bytes(ctx, n_tasks, T_max, D, C.byref(p), 1 if columnwise else 0,
+                                              C.byref(n)))
+    return int(n.value)
+
+
+def ns_score_workspace_bytes(ctx: int, T_prime: int, D: int, P: int, assign_on_device: bool) -> int:
+    n = C.c_size_t(0)
+    _check(ctx, LIB.ns_score_workspace_bytes(ctx, T_prime, D, P, 1 if assign_on_device else 0, C.byref(n)))
+    return int(n.value)
 
 
 # ----------------------------------------------------------------- comm

@@ -145,7 +145,7 @@ ns_status plan_bags(ns_ctx* ctx, const ns_bag_table* t, int n, int B, BagPlan& p
 ns_status upload(ns_ctx* ctx, const BagPlan& p, BagTab** d) {
     const size_t bytes = p.tabs.size() * sizeof(BagTab);
     char* a = (char*)arena_get(ctx, bytes + 256);
-    if (!a) return set_err(ctx, NS_ERR_NOMEM, "ns_embedding_bag descriptors");
+    if (!a) return arena_error(ctx, "ns_embedding_bag descriptors", bytes + 256);
     NS_CUDA(ctx, cudaMemcpyAsync(a, p.tabs.data(), bytes, cudaMemcpyHostToDevice, ctx->stream));
     *d = (BagTab*)a;
     return NS_OK;

@@ -519,8 +519,9 @@ ns_status ns_pretrain_comm_samples(ns_ctx* ctx, const ns_table_desc* pool, int32
                           (const void*)yf_out, (const void*)yb_out, (const void*)assign_out, (const void*)valid_out})
         if (!is_device_ptr(q)) return set_err(ctx, NS_ERR_ARG, "ns_pretrain_*: pointers must be device memory");
     cudaSetDevice(ctx->device);
-    long long* scratch = (long long*)arena_get(ctx, (size_t)n * 2 * D * sizeof(long long) + 256);
-    if (!scratch) return set_err(ctx, NS_ERR_NOMEM, "device arena (placements)");
+    const size_t need = (size_t)n * 2 * D * sizeof(long long) + 256;
+    long long* scratch = (long long*)arena_get(ctx, need);
+    if (!scratch) return arena_error(ctx, "placements", need);
     AugView av{pool, aug_dims, n_dims};
     prof_begin(ctx, PK_OTHER);
     k_pt_place<<<(n + 127) / 128, 128, 0, ctx->stream>>>(av, D, mem_cap, off, idx, p, u, r, starts, n, x_out, yf_out,
@@ -545,8 +546,9 @@ ns_status ns_pretrain_compute_step(ns_ctx* ctx, double* theta, double* adam_m, d
     constexpr int P = 7073;
     const int spb = std::max(1, std::min(16, kPtRows / max_rows));
     const int nblk = (B + spb - 1) / spb;
-    double* part = (double*)arena_get(ctx, ((size_t)nblk * P + nblk + 64) * sizeof(double));
-    if (!part) return set_err(ctx, NS_ERR_NOMEM, "device arena (pretrain)");
+    const size_t need = ((size_t)nblk * P + nblk + 64) * sizeof(double);
+    double* part = (double*)arena_get(ctx, need);
+    if (!part) return arena_error(ctx, "pretrain", need);
     double* loss_part = part + (size_t)nblk * P;
     const size_t smem = ((size_t)kPtRows * (5 + 128 + 32) + 16 * (32 + 64 + 64 + 32) + 16 + 640 + 128 + 2 * 4096 + 32 +
                          2 * 2048 + 64 + 64 + 2) * sizeof(double) + kPtRows * sizeof(int);
@@ -574,8 +576,9 @@ ns_status ns_pretrain_comm_step(ns_ctx* ctx, int32_t D, double* theta, double* a
     int P = 0;
     for (int l = 0; l < 5; ++l) P += w[l] * w[l + 1] + w[l + 1];
     const int nblk = (B + kPtCommSpb - 1) / kPtCommSpb;
-    double* part = (double*)arena_get(ctx, ((size_t)nblk * P + nblk + 64) * sizeof(double));
-    if (!part) return set_err(ctx, NS_ERR_NOMEM, "device arena (pretrain)");
+    const size_t need = ((size_t)nblk * P + nblk + 64) * sizeof(double);
+    double* part = (double*)arena_get(ctx, need);
+    if (!part) return arena_error(ctx, "pretrain", need);
     double* loss_part = part + (size_t)nblk * P;
     const size_t smem = comm_smem(D);
     if (smem > 48 * 1024) cudaFuncSetAttribute(k_pt_comm_grad, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);

@@ -277,6 +277,19 @@ __global__ void k_rank_key(BestRec* best, uint64_t* key, int stage) {
     }
 }
 
+// Scratch of one ns_score_plans call (this rank's slice of the P plans).
+size_t score_workspace(const ns_ctx* ctx, int Tp, int D, long long P, bool dev_assign) {
+    const int R = ctx->emulated ? 1 : ctx->nranks;
+    const long long per = (P + R - 1) / R;
+    const long long pb = std::min<long long>(P, per * (ctx->emulated ? 0 : ctx->rank));
+    const long long np_ = std::min<long long>(P, pb + per) - pb;
+    const int nblk_arg = 296;
+    size_t need = 256 + (size_t)Tp * 4 + (size_t)P * 8 + (size_t)(nblk_arg + 2 + ctx->nranks) * sizeof(BestRec) +
+                  (size_t)np_ * D * 20 + (size_t)np_ + 4096;
+    if (!dev_assign) need += (size_t)np_ * Tp + 256;
+    return need;
+}
+
 ns_status run_score_plans(ns_ctx* ctx, const ns_tables* t, int task, int D, const int32_t* col_plan, int n_col,
                           const int8_t* assign, int64_t P, int mode, double* cost_out, int64_t* best_index_out,
                           double* best_cost_out) {
@@ -297,11 +310,9 @@ ns_status run_score_plans(ns_ctx* ctx, const ns_tables* t, int task, int D, cons
     const bool dev_assign = is_device_ptr(assign);
     const int nblk_arg = 296;
     const long long np_ = pe - pb;
-    size_t need = 256 + (size_t)Tp * 4 + (size_t)P * 8 + (size_t)(nblk_arg + 2 + ctx->nranks) * sizeof(BestRec) +
-                  (size_t)np_ * D * 20 + (size_t)np_ + 4096;
-    if (!dev_assign) need += (size_t)np_ * Tp + 256;
+    const size_t need = score_workspace(ctx, Tp, D, P, dev_assign);
     char* base = (char*)arena_get(ctx, need);
-    if (!base) return set_err(ctx, NS_ERR_NOMEM, "device arena (score)");
+    if (!base) return arena_error(ctx, "score", need);
     size_t off = 0;
     auto take = [&](size_t bytes) {
         off = (off + 255) & ~size_t(255);

@@ -2741,13 +2741,14 @@ ns_status deliver(ns_ctx* ctx, const ns_tables* t, const OutStage& o, int Lout, 
     return NS_OK;
 }
 
-ns_status run_search(ns_ctx* ctx, const ns_tables* t, int D, const ns_search_params* p, ns_plan_batch* out,
-                     bool columnwise) {
-    const double grid_hi = (p->flags & NS_NO_DIM_CAP) ? -1.0 : p->grid_hi_factor;
-    ctx->rflags = p->flags & (NS_R10_ABS_STARTS | NS_R11_SUM_OF_MAX);
-    SearchBufs b{};
+// Buffer shapes of one search call (everything but the pointers): a function
+// of the batch shape (tasks, longest table list), D, the search parameters
+// and the ctx (ranks, SM count) only -- ns_search_workspace_bytes uses it too.
+static void search_layout(const ns_ctx* ctx, int n_tasks, int T_max, int D, const ns_search_params* p,
+                          bool columnwise, SearchBufs& b) {
+    b = SearchBufs{};
     b.r14 = (p->flags & NS_R14_SPLITTABLE) ? 1 : 0;
-    b.n_tasks = t->n_tasks;
+    b.n_tasks = n_tasks;
     b.greedy_mode = p->flags & 3u;
     b.D = D;
     b.M = p->M;
@@ -2755,7 +2756,7 @@ ns_status run_search(ns_ctx* ctx, const ns_tables* t, int D, const ns_search_par
     b.K = columnwise ? p->K : 1;
     b.N2 = columnwise ? 2 * p->N : 1;
     b.Lcap = L > 0 ? L : 1;
-    b.Tpm = t->T_max + L;
+    b.Tpm = T_max + L;
     const int C = (columnwise && L > 0) ? b.K * b.N2 : 1;
     b.S = b.n_tasks * C;
     {
@@ -2765,7 +2766,6 @@ ns_status run_search(ns_ctx* ctx, const ns_tables* t, int D, const ns_search_par
         const long long per0 = (b.n_tasks + R - 1) / R, per = ((long long)b.S + R - 1) / R;
         b.n_traj = (int)(std::max(per0, per) * R * b.M);
     }
-    const int Lout = L;
     {
         int dp = 1;
         while (dp < D) dp <<= 1;
@@ -2786,11 +2786,22 @@ ns_status run_search(ns_ctx* ctx, const ns_tables* t, int D, const ns_search_par
         const int nth = ((D * NS_WGRP_TPD + 31) / 32) * 32;
         b.wsnap_doubles = (size_t)nth * (kV / NS_WGRP_TPD + 2);
     }
+}
+
+ns_status run_search(ns_ctx* ctx, const ns_tables* t, int D, const ns_search_params* p, ns_plan_batch* out,
+                     bool columnwise) {
+    const double grid_hi = (p->flags & NS_NO_DIM_CAP) ? -1.0 : p->grid_hi_factor;
+    ctx->rflags = p->flags & (NS_R10_ABS_STARTS | NS_R11_SUM_OF_MAX);
+    SearchBufs b;
+    search_layout(ctx, t->n_tasks, t->T_max, D, p, columnwise, b);
+    const int L = columnwise ? p->L : 0;
+    const int Lout = L;
+    const int C = (columnwise && L > 0) ? b.K * b.N2 : 1;
     OutStage o{};
     Carver probe{nullptr};
     carve(probe, b, o, Lout > 0 ? Lout : 1);
     char* base = (char*)arena_get(ctx, probe.off + 256);
-    if (!base) return set_err(ctx, NS_ERR_NOMEM, "device arena (search)");
+    if (!base) return arena_error(ctx, "search", probe.off + 256);
     Carver cv{base};
     carve(cv, b, o, Lout > 0 ? Lout : 1);
     ns_status s;
@@ -2881,6 +2892,17 @@ ns_status run_search(ns_ctx* ctx, const ns_tables* t, int D, const ns_search_par
 }
 
 }  // namespace
+
+size_t search_workspace(const ns_ctx* ctx, int n_tasks, int T_max, int D, const ns_search_params* p,
+                        bool columnwise) {
+    SearchBufs b;
+    search_layout(ctx, n_tasks, T_max, D, p, columnwise, b);
+    OutStage o{};
+    Carver probe{nullptr};
+    const int L = columnwise ? p->L : 0;
+    carve(probe, b, o, L > 0 ? L : 1);
+    return probe.off + 256;
+}
 
 ns_status run_tablewise(ns_ctx* ctx, const ns_tables* t, int D, const ns_search_params* p, ns_plan_batch* out) {
     return run_search(ctx, t, D, p, out, false);

@@ -54,6 +54,7 @@ void* arena_get(ns_ctx* ctx, size_t bytes) {
         ctx->out_pending = false;
     }
     if (bytes <= ctx->arena_bytes) return ctx->arena;
+    if (ctx->arena_external) return nullptr;   // the caller's workspace is too small (arena_error)
     if (ctx->arena) {
         cudaStreamSynchronize(ctx->stream);
         if (ctx->out_stream) cudaStreamSynchronize(ctx->out_stream);   // result copies read the arena
@@ -69,6 +70,13 @@ void* arena_get(ns_ctx* ctx, size_t bytes) {
     }
     ctx->arena_bytes = want;
     return ctx->arena;
+}
+
+ns_status arena_error(ns_ctx* ctx, const char* what, size_t bytes) {
+    std::string m = std::string("device arena (") + what + "): need " + std::to_string(bytes) + " bytes";
+    if (ctx->arena_external)
+        m += ", the caller workspace (ns_set_workspace) holds " + std::to_string(ctx->arena_bytes);
+    return set_err(ctx, NS_ERR_NOMEM, m);
 }
 
 void* pinned_get(ns_ctx* ctx, size_t bytes) {
@@ -283,7 +291,7 @@ ns_status ns_destroy(ns_ctx* ctx) {
     while (!ctx->tables.empty()) ns_tables_free(*ctx->tables.begin());
     cudaStreamSynchronize(ctx->stream);
     free_model(ctx->model);
-    if (ctx->arena) cudaFree(ctx->arena);
+    if (ctx->arena && !ctx->arena_external) cudaFree(ctx->arena);
     if (ctx->pinned) cudaFreeHost(ctx->pinned);
     if (ctx->pinned_in) cudaFreeHost(ctx->pinned_in);
     if (ctx->comm_stage) cudaFreeHost(ctx->comm_stage);
@@ -730,6 +738,41 @@ ns_status ns_score_plans(ns_ctx* ctx, const ns_tables* t, int32_t task, int32_t 
     }
     return run_score_plans(ctx, t, task, D, col_plan, n_col, assign, P, mode, cost_out, best_index_out,
                            best_cost_out);
+}
+
+ns_status ns_set_workspace(ns_ctx* ctx, void* device_ptr, size_t bytes) {
+    if (!ctx) return NS_ERR_ARG;
+    if (device_ptr && (!is_device_ptr(device_ptr) || ((uintptr_t)device_ptr & 255) != 0))
+        return set_err(ctx, NS_ERR_ARG, "ns_set_workspace: need 256-byte aligned device memory");
+    cudaSetDevice(ctx->device);
+    // work in flight (and async result copies) may still use the current arena
+    NS_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+    if (ctx->out_stream) NS_CUDA(ctx, cudaStreamSynchronize(ctx->out_stream));
+    ctx->out_pending = false;
+    if (ctx->arena && !ctx->arena_external) cudaFree(ctx->arena);
+    ctx->arena = device_ptr;
+    ctx->arena_bytes = device_ptr ? bytes : 0;
+    ctx->arena_external = device_ptr != nullptr;
+    return NS_OK;
+}
+
+ns_status ns_search_workspace_bytes(ns_ctx* ctx, int32_t n_tasks, int32_t T_max, int32_t D,
+                                    const ns_search_params* p, int32_t columnwise, size_t* bytes_out) {
+    if (!ctx) return NS_ERR_ARG;
+    if (!p || !bytes_out || n_tasks < 1 || T_max < 1 || D < 1 || D > kMaxD || p->M < 1 ||
+        (columnwise && (p->N < 1 || p->K < 1 || p->L < 0 || p->L > 64)))
+        return set_err(ctx, NS_ERR_ARG, "ns_search_workspace_bytes: bad shape or parameters");
+    *bytes_out = search_workspace(ctx, n_tasks, T_max, D, p, columnwise != 0);
+    return NS_OK;
+}
+
+ns_status ns_score_workspace_bytes(ns_ctx* ctx, int32_t T_prime, int32_t D, int64_t P, int32_t assign_on_device,
+                                   size_t* bytes_out) {
+    if (!ctx) return NS_ERR_ARG;
+    if (!bytes_out || T_prime < 1 || D < 1 || D > kMaxD || P < 1)
+        return set_err(ctx, NS_ERR_ARG, "ns_score_workspace_bytes: bad shape");
+    *bytes_out = score_workspace(ctx, T_prime, D, P, assign_on_device != 0);
+    return NS_OK;
 }
 
 }  // extern "C"

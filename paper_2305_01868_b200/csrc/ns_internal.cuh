@@ -96,6 +96,7 @@ struct ns_ctx {
     // grow-only device arena for per-call scratch
     void* arena = nullptr;
     size_t arena_bytes = 0;
+    bool arena_external = false;   // ns_set_workspace: caller-owned (never grown or freed here)
     // pinned host staging (results), and a second buffer for featurise inputs
     // guarded by an event so a new featurise call never waits for the stream
     void* pinned = nullptr;
@@ -214,6 +215,10 @@ ns_status set_err(ns_ctx* ctx, ns_status s, const std::string& msg);
 ns_status cuda_check(ns_ctx* ctx, cudaError_t e, const char* what);
 bool is_device_ptr(const void* p);
 void* arena_get(ns_ctx* ctx, size_t bytes);   // nullptr on failure
+ns_status arena_error(ns_ctx* ctx, const char* what, size_t bytes);   // NS_ERR_NOMEM with the size needed
+// arena bytes a search / a score call of this shape needs (ns_*_workspace_bytes)
+size_t search_workspace(const ns_ctx* ctx, int n_tasks, int T_max, int D, const ns_search_params* p, bool columnwise);
+size_t score_workspace(const ns_ctx* ctx, int Tp, int D, long long P, bool dev_assign);
 void* pinned_get(ns_ctx* ctx, size_t bytes);
 void* pinned_in_get(ns_ctx* ctx, size_t bytes);      // waits only for the previous input copy
 void pinned_in_release(ns_ctx* ctx);                  // record: copies out of it are enqueued

@@ -38,6 +38,10 @@ CASES = {
     "C3_full_0": ("C3", 0, None, "columnwise", 10, 10, 10, 11, "full C3 (K = 10, L = 10)"),
     "C3_full_1": ("C3", 1, None, "columnwise", 10, 10, 10, 11, "full C3, second task"),
     "C4_full_0": ("C4", 0, None, "columnwise", 10, 3, 10, 51, "full C4 (L = 10, M = 51 wide grid, 8 GiB cap)"),
+    "C6_tw_0": ("C6", 0, None, "tablewise", 10, 3, 0, 5,
+                "F4 stress: 4000 tables on 128 devices, table-wise, M = 5 (T' = 4000: k_build_order, wide greedy)"),
+    "C6_L1_0": ("C6", 1, None, "columnwise", 2, 1, 1, 3,
+                "F4 stress: 4000 tables on 128 devices, column-wise level 1 (N = 2, K = 1, M = 3)"),
 }
 
 

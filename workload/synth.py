@@ -54,6 +54,12 @@ CONFIGS: Dict[str, dict] = {
                N=10, K=3, L=10, M=51, reject_single=False),
     "C5": dict(cfg_id=5, T=1000, D=128, cap=4 * GiB, max_dim=128, mode="columnwise",
                N=10, K=3, L=10, M=11, reject_single=False),
+    # SURVEY §8(f) F4 stress shape beyond the paper's production model (nearly a
+    # thousand tables on 128 GPUs): 4000 tables on 128 devices,
+    # the cap raised to 16 GiB so the same table recipe fits (2 TiB in total,
+    # "multi-terabyte memory").  Not a BASELINE.json config.
+    "C6": dict(cfg_id=6, T=4000, D=128, cap=16 * GiB, max_dim=128, mode="columnwise",
+               N=10, K=3, L=10, M=11, reject_single=False),
 }
 
 
