@@ -21,7 +21,8 @@
 #define NS_WIDE_TPD 2   // threads per device of the large-D greedy kernels
 #endif
 #ifndef NS_WGRP_TPD
-#define NS_WGRP_TPD 2   // threads per device of k_greedy_wgrp (same scores as any TPD: block_score)
+#define NS_WGRP_TPD 1   // threads per device of k_greedy_wgrp (same scores as any TPD: block_score);
+                        // 1: the head weights are constant-bank operands (block_score_c)
 #endif
 #ifndef NS_WGRP_CTAS
 #define NS_WGRP_CTAS 2   // resident CTAs per SM of k_greedy_wgrp (launch bounds and persistent grid)
@@ -599,6 +600,16 @@ __device__ __forceinline__ void load_lane_head(const HeadParams& hp, int part, d
 }
 
 
+// Blocks of one thread combined pairwise -- ((B0 + B1) + (B2 + B3)) for 4,
+// B0 + B1 for 2 -- the same association as TPD = 2 (a thread adds its two
+// blocks, the xor-1 shuffle joins the halves) and TPD = 4 (two shuffle levels).
+template <int NB>
+__device__ __forceinline__ double combine_blocks(const double (&blk)[NB]) {
+    if constexpr (NB == 1) return blk[0];
+    else if constexpr (NB == 2) return blk[0] + blk[1];
+    else return (blk[0] + blk[1]) + (blk[2] + blk[3]);
+}
+
 // Large-D score in a lane-split-INDEPENDENT order, so k_greedy_wide (TPD = 2,
 // latency) and k_greedy_wgrp (TPD = 4, throughput) give bit-identical
 // scores: the 64 features form 4 blocks of 16; a block is summed with 4
@@ -609,7 +620,7 @@ __device__ __forceinline__ void load_lane_head(const HeadParams& hp, int part, d
 template <int FPL>
 __device__ __forceinline__ double block_score(const double (&u)[FPL], const double2* __restrict__ v2,
                                               const double2* __restrict__ w2) {
-    double bs = 0.0;
+    double blk[FPL / 16];
 #pragma unroll
     for (int b = 0; b < FPL / 16; ++b) {
         double acc[4] = {0.0, 0.0, 0.0, 0.0};
@@ -619,25 +630,46 @@ __device__ __forceinline__ double block_score(const double (&u)[FPL], const doub
             acc[(2 * k2) & 3] = fma(ww.x, relu_hi(u[b * 16 + 2 * k2] + vv.x), acc[(2 * k2) & 3]);
             acc[(2 * k2 + 1) & 3] = fma(ww.y, relu_hi(u[b * 16 + 2 * k2 + 1] + vv.y), acc[(2 * k2 + 1) & 3]);
         }
-        const double blk = (acc[0] + acc[1]) + (acc[2] + acc[3]);
-        bs = b == 0 ? blk : bs + blk;
+        blk[b] = (acc[0] + acc[1]) + (acc[2] + acc[3]);
     }
-    return bs;
+    return combine_blocks<FPL / 16>(blk);
+}
+
+// block_score for TPD = 1 (a thread holds all 64 features of its device):
+// the head weights are read from the kernel-parameter bank (HeadParams is
+// passed by value; every lane of the warp uses the same H2[k], so each DFMA
+// takes it as a constant operand) instead of 16 shared-memory loads per step
+// -- identical operations in identical order, so identical scores.
+__device__ __forceinline__ double block_score_c(const double (&u)[kV], const double2* __restrict__ v2,
+                                                const HeadParams& hp) {
+    double blk[kV / 16];
+#pragma unroll
+    for (int b = 0; b < kV / 16; ++b) {
+        double acc[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+        for (int k2 = 0; k2 < 8; ++k2) {
+            const double2 vv = v2[b * 8 + k2];
+            acc[(2 * k2) & 3] = fma(hp.H2[b * 16 + 2 * k2], relu_hi(u[b * 16 + 2 * k2] + vv.x), acc[(2 * k2) & 3]);
+            acc[(2 * k2 + 1) & 3] =
+                fma(hp.H2[b * 16 + 2 * k2 + 1], relu_hi(u[b * 16 + 2 * k2 + 1] + vv.y), acc[(2 * k2 + 1) & 3]);
+        }
+        blk[b] = (acc[0] + acc[1]) + (acc[2] + acc[3]);
+    }
+    return combine_blocks<kV / 16>(blk);
 }
 
 // Final per-device head sum_k H2_k ReLU(u_k) in the same block order.
 template <int FPL>
 __device__ __forceinline__ double block_head(const double (&u)[FPL], const double* __restrict__ w) {
-    double bs = 0.0;
+    double blk[FPL / 16];
 #pragma unroll
     for (int b = 0; b < FPL / 16; ++b) {
         double acc[4] = {0.0, 0.0, 0.0, 0.0};
 #pragma unroll
         for (int k = 0; k < 16; ++k) acc[k & 3] = fma(w[b * 16 + k], relu_exact(u[b * 16 + k]), acc[k & 3]);
-        const double blk = (acc[0] + acc[1]) + (acc[2] + acc[3]);
-        bs = b == 0 ? blk : bs + blk;
+        blk[b] = (acc[0] + acc[1]) + (acc[2] + acc[3]);
     }
-    return bs;
+    return combine_blocks<FPL / 16>(blk);
 }
 
 // Join the TPD partial block sums of a device: xor 1 first, then xor 2.
@@ -1810,7 +1842,9 @@ __global__ void __launch_bounds__(128 * TPD, NS_WGRP_CTAS) k_greedy_wgrp(const G
             // every device scores (no divergent branch: 3% faster than skipping
             // the infeasible ones); an infeasible device's finite score is
             // masked by its key ~0
-            const double ps = block_score<FPL>(u, v2, w2);
+            double ps;
+            if constexpr (TPD == 1) ps = block_score_c(u, v2, a.head);
+            else ps = block_score<FPL>(u, v2, w2);
             const double sco = a.head.hb2 + block_group_sum<TPD>(ps);
             const long long sb = __double_as_longlong(sco + 0.0);
             const unsigned long long key =
