@@ -1711,6 +1711,18 @@ __global__ void __launch_bounds__(128 * TPD, NS_WGRP_CTAS) k_greedy_wgrp(const G
     // coalesced per thread index
     const size_t snap_doubles = (size_t)nth * (FPL + 2);
     unsigned long long computed = 0, steps = 0;   // executed scores / group-steps (ns_stats)
+#ifdef NS_WGRP_TIMING   // debug build: clock64 per step phase of thread 0, printed by CTAs 0-3
+    unsigned long long tph[7] = {0, 0, 0, 0, 0, 0, 0};
+    long long tlast = clock64();
+#define NS_TMARK(k)                                  \
+    {                                                \
+        const long long tn = clock64();              \
+        tph[k] += (unsigned long long)(tn - tlast);  \
+        tlast = tn;                                  \
+    }
+#else
+#define NS_TMARK(k)
+#endif
     volatile unsigned int* vq = reinterpret_cast<volatile unsigned int*>(x.q);
     volatile int32_t* vready = x.item_ready;
     // copy assignment row src -> dst (list positions [0, n)); rows written by
@@ -1829,6 +1841,7 @@ __global__ void __launch_bounds__(128 * TPD, NS_WGRP_CTAS) k_greedy_wgrp(const G
         int cmax = mask ? s_cap[63 - __clzll((long long)mask)] : 0;
 #pragma unroll 1
         for (int p = p0; p < Tp; ++p) {
+            NS_TMARK(5)
             pend = p + 1;
             const int par = p & 1;
             const int sl = p % kRingW;
@@ -1846,6 +1859,7 @@ __global__ void __launch_bounds__(128 * TPD, NS_WGRP_CTAS) k_greedy_wgrp(const G
             if constexpr (TPD == 1) ps = block_score_c(u, v2, a.head);
             else ps = block_score<FPL>(u, v2, w2);
             const double sco = a.head.hb2 + block_group_sum<TPD>(ps);
+            NS_TMARK(0)
             const long long sb = __double_as_longlong(sco + 0.0);
             const unsigned long long key =
                 f ? (unsigned long long)(sb ^ ((sb >> 63) | (long long)0x8000000000000000ULL)) : ~0ULL;
@@ -1862,12 +1876,14 @@ __global__ void __launch_bounds__(128 * TPD, NS_WGRP_CTAS) k_greedy_wgrp(const G
                 if (lane == 0)
                     s_rec[par][wi] = make_uint4(ml, mh, (unsigned)(wi * (32 / TPD) + hl / TPD) | ((unsigned)xw << 7), xm);
             }
+            NS_TMARK(1)
             if (wi == 0) {   // the next row lands before the barrier (its slot was last read at p - 2)
                 stage(p + kLook);
                 cp_async_commit();
                 cp_async_wait<kLook - 1>();
             }
             __syncthreads();
+            NS_TMARK(2)
             int bd, xstar;
             unsigned xmax;
             bool none;
@@ -1882,6 +1898,7 @@ __global__ void __launch_bounds__(128 * TPD, NS_WGRP_CTAS) k_greedy_wgrp(const G
                 bd = (int)(dx & 127u);
                 xstar = (int)(dx >> 7);
             }
+            NS_TMARK(3)
             // ---- work W per member (O12): |F_m| = #{memory-feasible d : x_d <= cap_m}
             // = |F_max| (this thread's device counts in cf) minus the devices
             // with cap_m < x_d <= cap_max, counted only for the members whose
@@ -1899,6 +1916,7 @@ __global__ void __launch_bounds__(128 * TPD, NS_WGRP_CTAS) k_greedy_wgrp(const G
                 alive = false;
                 break;
             }
+            NS_TMARK(4)
             if (xstar > cmin) {
                 // ---- slow path: members split by the caps that admit the winners
                 __syncthreads();   // per-member work atomics done
@@ -2013,6 +2031,7 @@ __global__ void __launch_bounds__(128 * TPD, NS_WGRP_CTAS) k_greedy_wgrp(const G
                         atomicExch(&x.item_ready[it], 1);   // publish
                     }
             }
+            NS_TMARK(6)
             // ---- the group's choice
             if (d == bd) {
 #pragma unroll
@@ -2052,6 +2071,14 @@ __global__ void __launch_bounds__(128 * TPD, NS_WGRP_CTAS) k_greedy_wgrp(const G
         __syncthreads();   // ring and shared state are reused by the next item
         if (threadIdx.x == 0) atomicAdd(&x.q->completed, 1u);
     }
+#ifdef NS_WGRP_TIMING
+    if (threadIdx.x == 0 && blockIdx.x < 4 && steps)
+        printf("wgrp cta %d steps %llu cycles/step: score %.0f key+warp %.0f stage+bar %.0f xwarp %.0f W %.0f "
+               "slow %.0f update+loop %.0f\n",
+               blockIdx.x, steps, (double)tph[0] / steps, (double)tph[1] / steps, (double)tph[2] / steps,
+               (double)tph[3] / steps, (double)tph[4] / steps, (double)tph[6] / steps, (double)tph[5] / steps);
+#endif
+#undef NS_TMARK
     if (threadIdx.x == 0 && computed) atomicAdd(a.computed, computed);
     if (threadIdx.x == 0 && steps) atomicAdd(a.computed + 1, steps);
 }
