@@ -41,7 +41,7 @@ struct BagTab {
     int dim, col;          // dimension, first output column
     int lanes, bpw;        // lanes per bag (dim / 4), bags per warp (32 / lanes)
     long long item0;       // first warp item of this table
-    int hoff;              // backward: first float of this table's hot-row accumulators in shared memory
+    int cta0;              // hot backward: first CTA of this table
 };
 
 // Hot rows (backward): Zipf-like indices send a large share of a table's
@@ -144,10 +144,20 @@ __global__ void __launch_bounds__(256) k_bag_hot_detect(const BagTab* __restrict
     if (threadIdx.x < kHot) best[threadIdx.x] = 0;
     __syncthreads();
     const long long n = tb.idx ? (long long)tb.off[B] : 0;
-    const int S = (int)std::min<long long>(n, 8192);
+    const int S = (int)std::min<long long>(n, 8192);   // (blockDim.x == 256: at most 32 samples per thread)
     const long long stride = S ? n / S : 1;
-    for (int j = threadIdx.x; j < S; j += blockDim.x) {
-        const unsigned long long r = (unsigned long long)__ldg(tb.idx + (long long)j * stride);
+    // the sampled loads are independent: issue a thread's (<= 32) loads before any insertion
+    constexpr int kPer = 8192 / 256;
+    unsigned long long rs[kPer];
+#pragma unroll
+    for (int q = 0; q < kPer; ++q) {
+        const int j = threadIdx.x + q * (int)blockDim.x;
+        rs[q] = j < S ? (unsigned long long)__ldg(tb.idx + (long long)j * stride) : ~0ull;
+    }
+#pragma unroll
+    for (int q = 0; q < kPer; ++q) {
+        const unsigned long long r = rs[q];
+        if (r == ~0ull) continue;
         int sl = (int)((r * 0x9E3779B97F4A7C15ull) >> 53);   // 11 bits
         for (int probe = 0; probe < 32; ++probe, sl = (sl + 1) & (HS - 1)) {
             const unsigned long long prev = atomicCAS(&key[sl], ~0ull, r);
@@ -168,57 +178,70 @@ __global__ void __launch_bounds__(256) k_bag_hot_detect(const BagTab* __restrict
     }
 }
 
-// Backward + SGD with the hot rows aggregated per CTA (dynamic shared memory:
-// the accumulators [sum_t kHot * dim_t] floats, then the hot keys
-// [n_tabs * kHot]).
-__global__ void __launch_bounds__(256) k_bag_backward_sgd_hot(const BagTab* __restrict__ tabs, int n_tabs,
-                                                              long long n_items, int B, int out_ld,
-                                                              const float* __restrict__ gout, float lr,
-                                                              const long long* __restrict__ hot_keys, int n_acc) {
-    extern __shared__ __align__(16) float hacc[];
-    long long* hkey = reinterpret_cast<long long*>(hacc + n_acc);
-    for (int i = threadIdx.x; i < n_acc; i += blockDim.x) hacc[i] = 0.f;
-    for (int i = threadIdx.x; i < n_tabs * kHot; i += blockDim.x) hkey[i] = __ldg(hot_keys + i);
+// One update of row r by lane l of a bag group: into the CTA's hot-row copy if
+// r is the table's hot row of its slot, else straight to the row (vector atomic).
+__device__ __forceinline__ void hot_update(const long long* hk, float* hacc, float* W, int dim, int l, long long r,
+                                           float4 gv) {
+    const int h = hot_slot(r);
+    if (hk[h] == r) {
+        float* a = hacc + h * dim + 4 * l;
+        atomicAdd(a, gv.x);
+        atomicAdd(a + 1, gv.y);
+        atomicAdd(a + 2, gv.z);
+        atomicAdd(a + 3, gv.w);
+    } else {
+        atomicAdd(reinterpret_cast<float4*>(W + r * dim) + l, gv);   // red.global.add.v4.f32
+    }
+}
+
+// Backward + SGD with the hot rows aggregated per CTA.  Each CTA works on a
+// contiguous range of ONE table's warp items (table t owns CTAs
+// [cta0_t, cta0_t + n_cta_t)), so its shared-memory accumulators hold only
+// that table's kHot rows (kHot * dim floats <= 8 KB): occupancy stays at 8
+// CTAs per SM, and no per-item table search.
+__global__ void __launch_bounds__(256) k_bag_backward_sgd_hot(const BagTab* __restrict__ tabs, int n_tabs, int B,
+                                                              int out_ld, const float* __restrict__ gout, float lr,
+                                                              const long long* __restrict__ hot_keys,
+                                                              int items_per_cta) {
+    __shared__ __align__(16) float hacc[kHot * kMaxDim];
+    __shared__ long long hk[kHot];
+    int t = 0;
+    while (t + 1 < n_tabs && tabs[t + 1].cta0 <= (int)blockIdx.x) ++t;   // few tables: linear scan
+    const BagTab tb = tabs[t];
+    for (int i = threadIdx.x; i < kHot * tb.dim; i += blockDim.x) hacc[i] = 0.f;
+    if (threadIdx.x < kHot) hk[threadIdx.x] = __ldg(hot_keys + t * kHot + threadIdx.x);
     __syncthreads();
-    const int lane = threadIdx.x & 31;
-    const long long warps = ((long long)gridDim.x * blockDim.x) >> 5;
-    for (long long it = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5; it < n_items; it += warps) {
-        const int t = find_table(tabs, n_tabs, it);
-        const BagTab tb = tabs[t];
-        const int g = lane / tb.lanes, l = lane % tb.lanes;
-        const long long b = (it - tb.item0) * tb.bpw + g;
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    const int g = lane / tb.lanes, l = lane % tb.lanes;
+    const long long it0 = (long long)((int)blockIdx.x - tb.cta0) * items_per_cta;
+    const long long it1 = std::min<long long>(it0 + items_per_cta, (B + tb.bpw - 1) / tb.bpw);
+    for (long long it = it0 + w; it < it1; it += nw) {
+        const long long b = it * tb.bpw + g;
         if (g >= tb.bpw || b >= B) continue;
         float4 gv = __ldg(reinterpret_cast<const float4*>(gout + (size_t)b * out_ld + tb.col) + l);
         gv.x *= -lr; gv.y *= -lr; gv.z *= -lr; gv.w *= -lr;
-        const long long* hk = hkey + t * kHot;
         const int i0 = tb.off[b], i1 = tb.off[b + 1];
-        for (int i = i0; i < i1; ++i) {
-            const long long r = __ldg(tb.idx + i);
-            const int h = hot_slot(r);
-            if (hk[h] == r) {
-                float* a = hacc + tb.hoff + h * tb.dim + 4 * l;
-                atomicAdd(a, gv.x);
-                atomicAdd(a + 1, gv.y);
-                atomicAdd(a + 2, gv.z);
-                atomicAdd(a + 3, gv.w);
-            } else {
-                atomicAdd(reinterpret_cast<float4*>(tb.W + r * tb.dim) + l, gv);   // red.global.add.v4.f32
-            }
+        int i = i0;
+        for (; i + 4 <= i1; i += 4) {   // 4 index loads in flight
+            const long long r0 = __ldg(tb.idx + i), r1 = __ldg(tb.idx + i + 1), r2 = __ldg(tb.idx + i + 2),
+                            r3 = __ldg(tb.idx + i + 3);
+            hot_update(hk, hacc, tb.W, tb.dim, l, r0, gv);
+            hot_update(hk, hacc, tb.W, tb.dim, l, r1, gv);
+            hot_update(hk, hacc, tb.W, tb.dim, l, r2, gv);
+            hot_update(hk, hacc, tb.W, tb.dim, l, r3, gv);
         }
+        for (; i < i1; ++i) hot_update(hk, hacc, tb.W, tb.dim, l, __ldg(tb.idx + i), gv);
     }
     __syncthreads();
     // flush this CTA's hot-row sums: one vector atomic per non-zero 16-byte chunk
-    for (int t = 0; t < n_tabs; ++t) {
-        const BagTab tb = tabs[t];
-        const int q = tb.dim / 4;
-        for (int i = threadIdx.x; i < kHot * q; i += blockDim.x) {
-            const int h = i / q, c = i % q;
-            const long long r = hkey[t * kHot + h];
-            if (r < 0) continue;
-            const float4 v = *reinterpret_cast<const float4*>(hacc + tb.hoff + h * tb.dim + 4 * c);
-            if (v.x != 0.f || v.y != 0.f || v.z != 0.f || v.w != 0.f)
-                atomicAdd(reinterpret_cast<float4*>(tb.W + r * tb.dim) + c, v);
-        }
+    const int q = tb.dim / 4;
+    for (int i = threadIdx.x; i < kHot * q; i += blockDim.x) {
+        const int h = i / q, c = i % q;
+        const long long r = hk[h];
+        if (r < 0) continue;
+        const float4 v = *reinterpret_cast<const float4*>(hacc + h * tb.dim + 4 * c);
+        if (v.x != 0.f || v.y != 0.f || v.z != 0.f || v.w != 0.f)
+            atomicAdd(reinterpret_cast<float4*>(tb.W + r * tb.dim) + c, v);
     }
 }
 
@@ -226,7 +249,6 @@ struct BagPlan {
     std::vector<BagTab> tabs;
     long long items = 0;
     int out_ld = 0;
-    int n_acc = 0;   // hot-row accumulator floats (kHot * sum of dims)
 };
 
 ns_status plan_bags(ns_ctx* ctx, const ns_bag_table* t, int n, int B, BagPlan& p) {
@@ -250,8 +272,6 @@ ns_status plan_bags(ns_ctx* ctx, const ns_bag_table* t, int n, int B, BagPlan& p
         b.lanes = s.dim / 4;
         b.bpw = 32 / b.lanes;
         b.item0 = p.items;
-        b.hoff = p.n_acc;
-        p.n_acc += kHot * s.dim;
         p.items += (B + b.bpw - 1) / b.bpw;
         col += s.dim;
     }
@@ -308,9 +328,19 @@ ns_status ns_embedding_bag_backward_sgd(ns_ctx* ctx, const ns_bag_table* tables,
     BagPlan p;
     ns_status s = plan_bags(ctx, tables, n_tables, batch, p);
     if (s != NS_OK) return s;
-    // hot-row aggregation when the accumulators leave room for >= 2 CTAs per SM
-    const size_t hsm = (size_t)p.n_acc * sizeof(float) + (size_t)n_tables * kHot * sizeof(long long);
-    const bool hot = hsm <= 96 * 1024 && !getenv("NS_BAG_NO_HOT");
+    // hot-row aggregation: CTAs are assigned to tables in proportion to their
+    // warp items (one table per CTA), items_per_cta chosen for ~4 waves of 8
+    // CTAs per SM
+    const bool hot = !getenv("NS_BAG_NO_HOT");
+    int items_per_cta = 0, n_cta = 0;
+    if (hot) {
+        items_per_cta = (int)std::max<long long>(8, p.items / ((long long)ctx->sm_count * 8 * 4));
+        for (int k = 0; k < n_tables; ++k) {
+            const long long it_k = (batch + p.tabs[k].bpw - 1) / p.tabs[k].bpw;
+            p.tabs[k].cta0 = n_cta;
+            n_cta += (int)((it_k + items_per_cta - 1) / items_per_cta);
+        }
+    }
     BagTab* d = nullptr;
     void* kx = nullptr;
     if ((s = upload(ctx, p, &d, hot ? (size_t)n_tables * kHot * sizeof(long long) : 0, &kx)) != NS_OK) return s;
@@ -319,13 +349,8 @@ ns_status ns_embedding_bag_backward_sgd(ns_ctx* ctx, const ns_bag_table* tables,
         long long* keys = reinterpret_cast<long long*>(kx);
         k_bag_hot_detect<<<n_tables, 256, 0, ctx->stream>>>(d, batch, keys);
         NS_LAUNCHED(ctx);
-        if (hsm > 48 * 1024)
-            NS_CUDA(ctx, cudaFuncSetAttribute(k_bag_backward_sgd_hot, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)hsm));
-        int per_sm = 0;
-        NS_CUDA(ctx, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_bag_backward_sgd_hot, 256, hsm));
-        const unsigned blocks = (unsigned)std::min<long long>((p.items + 7) / 8, (long long)ctx->sm_count * std::max(1, per_sm));
-        k_bag_backward_sgd_hot<<<blocks, 256, hsm, ctx->stream>>>(d, n_tables, p.items, batch, p.out_ld, grad_out, lr,
-                                                                  keys, p.n_acc);
+        k_bag_backward_sgd_hot<<<n_cta, 256, 0, ctx->stream>>>(d, n_tables, batch, p.out_ld, grad_out, lr, keys,
+                                                               items_per_cta);
     } else {
         const unsigned blocks = (unsigned)std::min<long long>((p.items + 7) / 8, (long long)ctx->sm_count * 8);
         k_bag_backward_sgd<<<blocks, 256, 0, ctx->stream>>>(d, n_tables, p.items, batch, p.out_ld, grad_out, lr);

@@ -1463,7 +1463,7 @@ __global__ void __launch_bounds__(NS_DEDUP_WPB * 32, (LPD >= 8 ? NS_DEDUP_BLOCKS
 // parity); lane k of every warp loads warp k's entry and one warp butterfly
 // picks the lowest (score, device) (R13).
 template <int TPD>
-__global__ void __launch_bounds__(128 * TPD, TPD >= 4 ? 1 : (TPD == 2 ? 2 : 3)) k_greedy_wide(const GreedyArgs a) {
+__global__ void __launch_bounds__(128 * TPD, TPD >= 4 ? 1 : 2) k_greedy_wide(const GreedyArgs a) {
     constexpr int FPL = kV / TPD;            // features per thread
     constexpr int SS = FPL + 2;              // padded slice stride (doubles)
     constexpr int kLook = kStages - 2;       // the slot being overwritten was last read two steps ago
@@ -1542,7 +1542,11 @@ __global__ void __launch_bounds__(128 * TPD, TPD >= 4 ? 1 : (TPD == 2 ? 2 : 3)) 
         const long long bt = (long long)(((unsigned long long)(unsigned)mt.w << 32) | (unsigned)mt.z);
         const bool f = dev && (bsum + bt <= cap) && (dsum + dt <= capd);
         const double2* v2 = reinterpret_cast<const double2*>(&ring[sl][part * SS]);
-        const double ps = f ? block_score<FPL>(u, v2, w2) : 0.0;
+        double ps = 0.0;
+        if (f) {
+            if constexpr (TPD == 1) ps = block_score_c(u, v2, a.head);
+            else ps = block_score<FPL>(u, v2, w2);
+        }
         const double sco = a.head.hb2 + block_group_sum<TPD>(ps);
 #if NS_REDUX_ARGMIN
         // order keys (see k_greedy_dedup): warp minimum by two REDUX, the
