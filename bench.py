@@ -418,7 +418,7 @@ def main():
     g_ms, g_n = prof["greedy"]
     clocks = sampler.summary() if sampler else {}
     roof = greedy_roofline(clocks, scores_per_step * args.steps, g_ms, g_n, ms_local, stats,
-                           "k_greedy_wgrp (N4, D = 128 grouped greedy; level 0 k_greedy_wide)")
+                           "k_greedy_wgrp88 (N4, D = 128 grouped greedy; level 0 k_greedy_wide88)")
 
     # ---- CPU baseline: the oracle on a bounded sample (rank 0, N=1 only)
     cpu = None

@@ -81,7 +81,7 @@ ns_status ns_profile(ns_ctx* ctx, int32_t enable);
  * (the grouped kernels evaluate a score once for all identical trajectories,
  * so this is <= the algorithmic count W the plans report); trajectories =
  * greedy trajectories launched (column plans x grid points); group_steps =
- * steps run by k_greedy_wgrp (D > 16, grouped). */
+ * steps run by k_greedy_wgrp88 (D > 16, grouped). */
 typedef struct {
     uint64_t scores_computed;
     uint64_t trajectories;

@@ -17,15 +17,8 @@
 #include "ns_device.cuh"
 #include "ns_internal.cuh"
 
-#ifndef NS_WIDE_TPD
-#define NS_WIDE_TPD 2   // threads per device of the large-D greedy kernels
-#endif
-#ifndef NS_WGRP_TPD
-#define NS_WGRP_TPD 1   // threads per device of k_greedy_wgrp (same scores as any TPD: block_score);
-                        // 1: the head weights are constant-bank operands (block_score_c)
-#endif
 #ifndef NS_WGRP_CTAS
-#define NS_WGRP_CTAS 2   // resident CTAs per SM of k_greedy_wgrp (launch bounds and persistent grid)
+#define NS_WGRP_CTAS 2   // resident CTAs per SM of k_greedy_wgrp88 (launch bounds and persistent grid)
 #endif
 #ifndef NS_WGRP_MIN_CP
 #define NS_WGRP_MIN_CP 148   // column plans per launch from which large D uses the grouped kernel
@@ -33,7 +26,7 @@
 
 namespace ns {
 
-struct WgrpQueue;   // k_greedy_wgrp work queue counters
+struct WgrpQueue;   // k_greedy_wgrp88 work queue counters
 
 // ======================================================================
 // Device buffers of one search call (carved from the ctx arena).
@@ -62,8 +55,8 @@ struct SearchBufs {
     int32_t* uniq;       // [n_traj] compacted list of trajectories carrying a distinct feasible plan
     int32_t* n_uniq;     // [1]
     unsigned int* next_cp;   // [1] grouped-greedy work queue
-    double* wsnap;       // large-D grouped greedy (k_greedy_wgrp): fork snapshots [S * M][wsnap_doubles]
-    bool wgrp;           // k_greedy_wgrp buffers carved
+    double* wsnap;       // large-D grouped greedy (k_greedy_wgrp88): fork snapshots [S * M][wsnap_doubles]
+    bool wgrp;           // k_greedy_wgrp88 buffers carved
     size_t wsnap_doubles;   // per slot
     WgrpQueue* wq;
     int wgrp_cp_cap;     // column plans per launch the item buffers hold (a rank's block)
@@ -488,7 +481,7 @@ __global__ void __launch_bounds__(256) k_order_warp(SearchBufs b, TaskView tv, i
 // 64 head weights exceed the register budget and the compiler spills the
 // weights.  Three kernels share this scheme: k_greedy_cta (latency mode,
 // every trajectory in its own lane segment), k_greedy_dedup (throughput mode,
-// one warp per column plan, identical trajectories grouped) and k_greedy_wide
+// one warp per column plan, identical trajectories grouped) and k_greedy_wide88
 // (D > 16: one trajectory per CTA, one thread per device).
 // ======================================================================
 struct GreedyArgs {
@@ -599,86 +592,6 @@ __device__ __forceinline__ void load_lane_head(const HeadParams& hp, int part, d
     }
 }
 
-
-// Blocks of one thread combined pairwise -- ((B0 + B1) + (B2 + B3)) for 4,
-// B0 + B1 for 2 -- the same association as TPD = 2 (a thread adds its two
-// blocks, the xor-1 shuffle joins the halves) and TPD = 4 (two shuffle levels).
-template <int NB>
-__device__ __forceinline__ double combine_blocks(const double (&blk)[NB]) {
-    if constexpr (NB == 1) return blk[0];
-    else if constexpr (NB == 2) return blk[0] + blk[1];
-    else return (blk[0] + blk[1]) + (blk[2] + blk[3]);
-}
-
-// Large-D score in a lane-split-INDEPENDENT order, so k_greedy_wide (TPD = 2,
-// latency) and k_greedy_wgrp (TPD = 4, throughput) give bit-identical
-// scores: the 64 features form 4 blocks of 16; a block is summed with 4
-// accumulators (feature k of the block into accumulator k & 3) as
-// (a0 + a1) + (a2 + a3); the blocks combine as (B0 + B1) + (B2 + B3) -- one
-// local add (TPD = 2: a thread holds blocks 2p, 2p + 1) or the xor-1 shuffle
-// (TPD = 4), then the xor-2 level (block_group_sum).
-template <int FPL>
-__device__ __forceinline__ double block_score(const double (&u)[FPL], const double2* __restrict__ v2,
-                                              const double2* __restrict__ w2) {
-    double blk[FPL / 16];
-#pragma unroll
-    for (int b = 0; b < FPL / 16; ++b) {
-        double acc[4] = {0.0, 0.0, 0.0, 0.0};
-#pragma unroll
-        for (int k2 = 0; k2 < 8; ++k2) {
-            const double2 vv = v2[b * 8 + k2], ww = w2[b * 8 + k2];
-            acc[(2 * k2) & 3] = fma(ww.x, relu_hi(u[b * 16 + 2 * k2] + vv.x), acc[(2 * k2) & 3]);
-            acc[(2 * k2 + 1) & 3] = fma(ww.y, relu_hi(u[b * 16 + 2 * k2 + 1] + vv.y), acc[(2 * k2 + 1) & 3]);
-        }
-        blk[b] = (acc[0] + acc[1]) + (acc[2] + acc[3]);
-    }
-    return combine_blocks<FPL / 16>(blk);
-}
-
-// block_score for TPD = 1 (a thread holds all 64 features of its device):
-// the head weights are read from the kernel-parameter bank (HeadParams is
-// passed by value; every lane of the warp uses the same H2[k], so each DFMA
-// takes it as a constant operand) instead of 16 shared-memory loads per step
-// -- identical operations in identical order, so identical scores.
-__device__ __forceinline__ double block_score_c(const double (&u)[kV], const double2* __restrict__ v2,
-                                                const HeadParams& hp) {
-    double blk[kV / 16];
-#pragma unroll
-    for (int b = 0; b < kV / 16; ++b) {
-        double acc[4] = {0.0, 0.0, 0.0, 0.0};
-#pragma unroll
-        for (int k2 = 0; k2 < 8; ++k2) {
-            const double2 vv = v2[b * 8 + k2];
-            acc[(2 * k2) & 3] = fma(hp.H2[b * 16 + 2 * k2], relu_hi(u[b * 16 + 2 * k2] + vv.x), acc[(2 * k2) & 3]);
-            acc[(2 * k2 + 1) & 3] =
-                fma(hp.H2[b * 16 + 2 * k2 + 1], relu_hi(u[b * 16 + 2 * k2 + 1] + vv.y), acc[(2 * k2 + 1) & 3]);
-        }
-        blk[b] = (acc[0] + acc[1]) + (acc[2] + acc[3]);
-    }
-    return combine_blocks<kV / 16>(blk);
-}
-
-// Final per-device head sum_k H2_k ReLU(u_k) in the same block order.
-template <int FPL>
-__device__ __forceinline__ double block_head(const double (&u)[FPL], const double* __restrict__ w) {
-    double blk[FPL / 16];
-#pragma unroll
-    for (int b = 0; b < FPL / 16; ++b) {
-        double acc[4] = {0.0, 0.0, 0.0, 0.0};
-#pragma unroll
-        for (int k = 0; k < 16; ++k) acc[k & 3] = fma(w[b * 16 + k], relu_exact(u[b * 16 + k]), acc[k & 3]);
-        blk[b] = (acc[0] + acc[1]) + (acc[2] + acc[3]);
-    }
-    return combine_blocks<FPL / 16>(blk);
-}
-
-// Join the TPD partial block sums of a device: xor 1 first, then xor 2.
-template <int TPD>
-__device__ __forceinline__ double block_group_sum(double x) {
-#pragma unroll
-    for (int o = 1; o < TPD; o <<= 1) x += __shfl_xor_sync(kFull, x, o);
-    return x;
-}
 
 // Staged greedy: one CTA per (column plan, chunk of grid points).  All
 // trajectories of a column plan consume the same cost-ordered table stream,
@@ -1451,44 +1364,146 @@ __global__ void __launch_bounds__(NS_DEDUP_WPB * 32, (LPD >= 8 ? NS_DEDUP_BLOCKS
 
 #undef GW
 
-// Large D (D > 16, e.g. C5's 128 simulated GPUs): one trajectory per CTA,
-// TPD threads per device, each holding FPL = 64 / TPD features of u_d in
-// registers; the head weights and the staged v row are read from shared memory
-// (per-slice rows padded 16 B apart: the TPD slices of one load fall on
-// distinct banks).  A single-task search is latency-bound -- its longest
-// trajectories (~T' steps) run nearly alone once the short ones have
-// stranded -- so the per-step chain matters most: TPD = 4 cuts the per-thread
-// score to 16 features plus a 2-level lane butterfly.  Cross-warp argmin: each
-// warp's (score, device) goes through shared memory (double-buffered by step
-// parity); lane k of every warp loads warp k's entry and one warp butterfly
-// picks the lowest (score, device) (R13).
-template <int TPD>
-__global__ void __launch_bounds__(128 * TPD, TPD >= 4 ? 1 : 2) k_greedy_wide(const GreedyArgs a) {
-    constexpr int FPL = kV / TPD;            // features per thread
-    constexpr int SS = FPL + 2;              // padded slice stride (doubles)
-    constexpr int kLook = kStages - 2;       // the slot being overwritten was last read two steps ago
+struct WgrpQueue {
+    unsigned int next;        // items claimed
+    unsigned int forks;       // items published beyond the n_cp initial ones
+    unsigned int completed;   // items finished
+    unsigned int pad;
+};
+
+struct WgrpArgs {
+    int n_cp;                  // column plans of this launch (local slots 0 .. n_cp-1) = initial items
+    int n_items;               // item capacity n_cp * M (forks <= n_cp * (M - 1))
+    WgrpQueue* q;              // zeroed before the launch
+    int32_t* item_cp;          // fork items i >= n_cp: column plan, start step, member mask
+    int32_t* item_step;
+    unsigned long long* item_mask;
+    int32_t* item_ready;       // publication flags (zeroed before the launch)
+    double* snap;              // fork snapshots, slot i - n_cp of fork item i
+    int32_t* dup_of;           // local trajectory indexing, global tau values
+    long long tau_base;        // global tau of local trajectory 0
+};
+
+// ----------------------------------------------------------------------
+// 8 x 8 lane layout of the large-D greedy (k_greedy_wide88 / k_greedy_wgrp88).
+// A warp owns 32 devices.  Lane l holds feature group fg = l & 7 (features
+// 8 fg .. 8 fg + 7) of the 8 devices of device group dg = l >> 3 (devices
+// 32 w + 8 dg + j, j = 0..7): u is 64 doubles per lane as with one thread per
+// device, but
+//  * a lane reads only its 8 features of the staged v row (4 LDS.128, the
+//    8 groups padded 16 B apart: one wavefront each) instead of all 64
+//    (32 broadcast LDS.128 -- shared-memory wavefronts were the step's
+//    bottleneck); the winner's update re-reads them on the 8
+//    lanes that hold the winner (4 LDS.128 instead of 32);
+//  * the head weights of its 8 features live in registers;
+//  * a transposed butterfly over the 8 feature-group lanes (xor 4, 2, 1)
+//    leaves lane l with the full score of device 32 w + l, so the argmin,
+//    feasibility and work counts stay one device per lane.
+// Score order (identical in both kernels): per (device, feature group) one
+// accumulator over the 8 features in order, then the butterfly tree over the
+// feature groups, then + hb2.
+constexpr int kG8 = 8;                  // features per lane
+constexpr int kSlot88 = 8 * (kG8 + 2);  // staged row: 8 groups of 8 doubles, padded by 2
+
+// per-lane partials of the 8 devices: sum_{k<8} w_k ReLU(u_jk + v_k), one
+// accumulator per device (features in order k = 0..7; the 8 devices are the
+// independent chains), v streamed pairwise from the staged slot (register
+// pressure: u alone is 128 registers)
+template <typename W>
+__device__ __forceinline__ void part88(const double (&u)[8][kG8], const double* slot, int fg, const W& w,
+                                       double (&p)[8]) {
+    const double2* s2 = reinterpret_cast<const double2*>(slot + fg * (kG8 + 2));
+#pragma unroll
+    for (int j = 0; j < 8; ++j) p[j] = 0.0;
+#pragma unroll
+    for (int q = 0; q < kG8 / 2; ++q) {
+        const double2 vv = s2[q];
+        const double w0 = w[2 * q], w1 = w[2 * q + 1];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            p[j] = fma(w0, relu_hi(u[j][2 * q] + vv.x), p[j]);
+            p[j] = fma(w1, relu_hi(u[j][2 * q + 1] + vv.y), p[j]);
+        }
+    }
+}
+
+// the final per-device head partials sum_k w_k ReLU(u_jk) (exact ReLU), same order
+template <typename W>
+__device__ __forceinline__ void head88(const double (&u)[8][kG8], const W& w, double (&p)[8]) {
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+        double a = 0.0;
+#pragma unroll
+        for (int k = 0; k < kG8; ++k) a = fma(w[k], relu_exact(u[j][k]), a);
+        p[j] = a;
+    }
+}
+
+// Transposed butterfly over the 8 feature-group lanes: at each level a lane
+// keeps the half of its device values whose index bit matches its own fg bit
+// and adds the partner's copy (IEEE addition commutes, so the lane pair
+// computes one well-defined sum).  Returns the sum over the 8 groups of p[fg].
+__device__ __forceinline__ double bfly88(double (&p)[8], int fg) {
+    {
+        const bool hi = fg & 4;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            const double send = hi ? p[i] : p[i + 4], keep = hi ? p[i + 4] : p[i];
+            p[i] = keep + __shfl_xor_sync(kFull, send, 4);
+        }
+    }
+    {
+        const bool hi = fg & 2;
+#pragma unroll
+        for (int i = 0; i < 2; ++i) {
+            const double send = hi ? p[i] : p[i + 2], keep = hi ? p[i + 2] : p[i];
+            p[i] = keep + __shfl_xor_sync(kFull, send, 2);
+        }
+    }
+    const bool hi = fg & 1;
+    const double send = hi ? p[0] : p[1], keep = hi ? p[1] : p[0];
+    return keep + __shfl_xor_sync(kFull, send, 1);
+}
+
+// warp 0 lane l copies features 2l, 2l + 1 of a row into the padded slot
+__device__ __forceinline__ double* stage_dst88(double* slot, int lane) {
+    return slot + (lane >> 2) * (kG8 + 2) + 2 * (lane & 3);
+}
+
+// the winner's update u_j += v on the 8 lanes holding device (dg*, j*): the
+// lane's 8 features of the row re-read from the staged slot
+__device__ __forceinline__ void add88(double (&u)[8][kG8], const double* slot, int fg, int j) {
+    const double2* s2 = reinterpret_cast<const double2*>(slot + fg * (kG8 + 2));
+#pragma unroll
+    for (int jj = 0; jj < 8; ++jj)
+        if (jj == j) {
+#pragma unroll
+            for (int q = 0; q < kG8 / 2; ++q) {
+                const double2 vv = s2[q];
+                u[jj][2 * q] += vv.x;
+                u[jj][2 * q + 1] += vv.y;
+            }
+        }
+}
+
+// Large D, latency mode (one trajectory per CTA) in the 8 x 8 layout; the
+// step is as in k_greedy_wide88: one CTA argmin per table (warp REDUX argmin,
+// then the warps' records through shared memory, double-buffered by step
+// parity), cp.async ring of the cost-ordered v rows.
+__global__ void __launch_bounds__(128, 2) k_greedy_wide88(const GreedyArgs a) {
+    constexpr int kLook = kStages - 2;
     constexpr int kRingW = kStages;
-    constexpr int NWM = 4 * TPD;             // warps of a D = 128 CTA
-    __shared__ __align__(16) double s_w[TPD][SS];
-    __shared__ __align__(16) double s_hb1[kV];
-    __shared__ __align__(16) double ring[kRingW][TPD * SS];
-#if NS_REDUX_ARGMIN
-    __shared__ unsigned long long s_key[2][NWM];
-#else
-    __shared__ double s_sc[2][NWM];
-#endif
-    __shared__ int s_dv[2][NWM];
-    __shared__ int s_cnt[2][NWM];
-    __shared__ int4 smeta[kRingW];    // {dim, list index, bytes lo, bytes hi}
+    __shared__ __align__(16) double ring[kRingW][kSlot88];
+    __shared__ unsigned long long s_key[2][4];
+    __shared__ int s_dv[2][4];
+    __shared__ int s_cnt[2][4];
+    __shared__ int4 smeta[kRingW];
     const int lane = threadIdx.x & 31, wi = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    const int fg = lane & 7, dg = lane >> 3;
     const long long tau = a.traj_begin + blockIdx.x;
     if (tau >= a.traj_end) return;
-    for (int k = threadIdx.x; k < kV; k += blockDim.x) {
-        s_w[k / FPL][k % FPL] = a.head.H2[k];
-        s_hb1[k] = a.head.hb1[k];
-    }
     const int g = (int)(tau / a.M), m = (int)(tau % a.M);
-    const int d = threadIdx.x / TPD, part = threadIdx.x % TPD;
+    const int d = threadIdx.x;   // this lane's device after the butterfly
     bool alive = a.cp_valid[g] != 0;
     int Tp = 0, capd = 0;
     long long cap = 0;
@@ -1499,10 +1514,14 @@ __global__ void __launch_bounds__(128 * TPD, TPD >= 4 ? 1 : 2) k_greedy_wide(con
         capd = a.capdim[q * a.M + m];
     }
     const bool dev = d < a.D;
-    __syncthreads();
-    double u[FPL];
+    double u[8][kG8], w[kG8];
 #pragma unroll
-    for (int k = 0; k < FPL; ++k) u[k] = s_hb1[part * FPL + k];
+    for (int k = 0; k < kG8; ++k) {
+        w[k] = a.head.H2[kG8 * fg + k];
+        const double h = a.head.hb1[kG8 * fg + k];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) u[j][k] = h;
+    }
     int dsum = 0;
     long long bsum = 0;
     uint32_t work = 0;
@@ -1510,24 +1529,17 @@ __global__ void __launch_bounds__(128 * TPD, TPD >= 4 ? 1 : 2) k_greedy_wide(con
     const int4* ometa = a.ord_meta + (size_t)g * a.Tpm;
     int8_t* asg = a.assign + (size_t)tau * a.Tpm;
     const int T = alive ? Tp : 0;
-    // warp 0 streams the cost-ordered v rows through a cp.async ring; lane l
-    // copies features (2l, 2l + 1) into slice 2l / FPL
-    const int my_slice = (2 * lane) / FPL, my_off = (2 * lane) % FPL;
-    auto stage = [&](int pp) {
+    auto issue = [&](int pp) {
         if (pp < T) {
             const int r = __ldg(orow + pp);
             const int slot = pp % kRingW;
-            cp_async16(&ring[slot][my_slice * SS + my_off], a.V + (size_t)r * kV + 2 * lane);
+            cp_async16(stage_dst88(ring[slot], lane), a.V + (size_t)r * kV + 2 * lane);
             if (lane == 0) cp_async16(smeta + slot, ometa + pp);
         }
-    };
-    auto issue = [&](int pp) {
-        stage(pp);
         cp_async_commit();
     };
     if (wi == 0)
         for (int pp = 0; pp < kLook; ++pp) issue(pp);
-    const double2* w2 = reinterpret_cast<const double2*>(&s_w[part][0]);
 #pragma unroll 1
     for (int p = 0; p < T; ++p) {
         const int par = p & 1;
@@ -1541,28 +1553,19 @@ __global__ void __launch_bounds__(128 * TPD, TPD >= 4 ? 1 : 2) k_greedy_wide(con
         const int dt = mt.x;
         const long long bt = (long long)(((unsigned long long)(unsigned)mt.w << 32) | (unsigned)mt.z);
         const bool f = dev && (bsum + bt <= cap) && (dsum + dt <= capd);
-        const double2* v2 = reinterpret_cast<const double2*>(&ring[sl][part * SS]);
-        double ps = 0.0;
-        if (f) {
-            if constexpr (TPD == 1) ps = block_score_c(u, v2, a.head);
-            else ps = block_score<FPL>(u, v2, w2);
-        }
-        const double sco = a.head.hb2 + block_group_sum<TPD>(ps);
-#if NS_REDUX_ARGMIN
-        // order keys (see k_greedy_dedup): warp minimum by two REDUX, the
-        // lowest device holding it from one ballot; then lane k takes warp
-        // k's key and the same two REDUX + ballot give the CTA's lowest
-        // (score, device) -- warps hold increasing device ranges
+        double pp8[8];
+        part88(u, ring[sl], fg, w, pp8);
+        const double sco = a.head.hb2 + bfly88(pp8, fg);
         const long long sb = __double_as_longlong(sco + 0.0);
         unsigned long long key = f ? (unsigned long long)(sb ^ ((sb >> 63) | (long long)0x8000000000000000ULL)) : ~0ULL;
         unsigned khi = (unsigned)(key >> 32), klo = (unsigned)key;
         unsigned mhi = __reduce_min_sync(kFull, khi);
         unsigned mlo = __reduce_min_sync(kFull, khi == mhi ? klo : 0xFFFFFFFFu);
-        unsigned hit = __ballot_sync(kFull, f && part == 0 && khi == mhi && klo == mlo);
-        const unsigned bal = __ballot_sync(kFull, f && part == 0);
+        unsigned hit = __ballot_sync(kFull, f && khi == mhi && klo == mlo);
+        const unsigned bal = __ballot_sync(kFull, f);
         if (lane == 0) {
             s_key[par][wi] = ((unsigned long long)mhi << 32) | mlo;
-            s_dv[par][wi] = wi * (32 / TPD) + (hit ? (__ffs(hit) - 1) / TPD : 0);
+            s_dv[par][wi] = wi * 32 + (hit ? __ffs(hit) - 1 : 0);
             s_cnt[par][wi] = __popc(bal);
         }
         __syncthreads();
@@ -1573,66 +1576,41 @@ __global__ void __launch_bounds__(128 * TPD, TPD >= 4 ? 1 : 2) k_greedy_wide(con
         mlo = __reduce_min_sync(kFull, khi == mhi ? klo : 0xFFFFFFFFu);
         hit = __ballot_sync(kFull, lane < nw && khi == mhi && klo == mlo);
         const int cnt = __reduce_add_sync(kFull, lane < nw ? s_cnt[par][lane] : 0);
-        const double bs = (mhi & mlo) == 0xFFFFFFFFu ? CUDART_INF : 0.0;   // INF: nothing feasible
         const int bd = s_dv[par][hit ? __ffs(hit) - 1 : 0];
-#else
-        double bs = f ? sco : CUDART_INF;
-        int bd = d;
-#pragma unroll
-        for (int o = 16; o >= TPD; o >>= 1) argmin_step(bs, bd, o);
-        const unsigned bal = __ballot_sync(kFull, f && part == 0);
-        if (lane == 0) {
-            s_sc[par][wi] = bs;
-            s_dv[par][wi] = bd;
-            s_cnt[par][wi] = __popc(bal);
-        }
-        __syncthreads();
-        // lane k holds warp k's candidate; one butterfly gives every lane the
-        // lowest (score, device) of the CTA
-        bs = lane < nw ? s_sc[par][lane] : CUDART_INF;
-        bd = lane < nw ? s_dv[par][lane] : INT_MAX;
-        const int cnt = __reduce_add_sync(kFull, lane < nw ? s_cnt[par][lane] : 0);
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) argmin_step(bs, bd, o);
-#endif
         work += cnt;
-        if (bs == CUDART_INF) {
+        if ((mhi & mlo) == 0xFFFFFFFFu) {   // nothing feasible (uniform across the CTA)
             alive = false;
-            break;   // uniform across the CTA
+            break;
         }
+        if (wi == (bd >> 5) && dg == ((bd >> 3) & 3)) add88(u, ring[sl], fg, bd & 7);
         if (d == bd) {
-#pragma unroll
-            for (int k2 = 0; k2 < FPL / 2; ++k2) {
-                const double2 vv = v2[k2];
-                u[2 * k2] += vv.x;
-                u[2 * k2 + 1] += vv.y;
-            }
             dsum += dt;
             bsum += bt;
         }
         if (threadIdx.x == 0) asg[mt.y] = (int8_t)bd;
     }
     if (wi == 0) cp_async_wait<0>();
-    // final per-device cost (every lane takes part in the lane-group sum)
-    const double hc = a.head.hb2 + block_group_sum<TPD>(block_head<FPL>(u, &s_w[part][0]));
-    if (dev && part == 0) {
+    double hp[8];
+    head88(u, w, hp);
+    const double hc = a.head.hb2 + bfly88(hp, fg);
+    if (dev) {
         a.comp[tau * a.D + d] = dsum > 0 ? hc : 0.0;   // reading R4
         a.devdim[tau * a.D + d] = dsum;
     }
     if (threadIdx.x == 0) {
         a.feas[tau] = alive ? 1 : 0;
         a.work[tau] = work;
-        if (work) atomicAdd(a.computed, (unsigned long long)work);   // every trajectory scores its own devices
+        if (work) atomicAdd(a.computed, (unsigned long long)work);
     }
 }
 
-// Large D, throughput mode: k_greedy_wgrp -- the M grid trajectories of a
+// Large D, throughput mode: k_greedy_wgrp88 -- the M grid trajectories of a
 // column plan share their scores while they make identical decisions (the
 // paper's life-long cache, as data parallelism; on C5 26-33% of the
 // algorithmic scores are distinct).  A work item is a GROUP of
 // identical trajectories of one column plan from some step on; a CTA runs it
-// with TPD threads per device (u_d in registers) and scores in the block
-// order of block_score, so its scores are bit-identical to k_greedy_wide's:
+// in the 8 x 8 lane layout (part88 / bfly88), so its scores are bit-identical
+// to k_greedy_wide88's:
 //  * a step scores every device that passes the memory cap and the group's
 //    largest dim cap; one CTA argmin gives (d*, x* = dim_d* + dim_t);
 //  * fast path: x* <= the group's smallest cap -> every member picks d*
@@ -1656,37 +1634,13 @@ __global__ void __launch_bounds__(128 * TPD, TPD >= 4 ? 1 : 2) k_greedy_wide(con
 // publishes the warps' argmin keys (double-buffered by step parity).  Caps are
 // non-decreasing in m (R8), so a member set's extreme caps are its lowest /
 // highest member.
-struct WgrpQueue {
-    unsigned int next;        // items claimed
-    unsigned int forks;       // items published beyond the n_cp initial ones
-    unsigned int completed;   // items finished
-    unsigned int pad;
-};
-
-struct WgrpArgs {
-    int n_cp;                  // column plans of this launch (local slots 0 .. n_cp-1) = initial items
-    int n_items;               // item capacity n_cp * M (forks <= n_cp * (M - 1))
-    WgrpQueue* q;              // zeroed before the launch
-    int32_t* item_cp;          // fork items i >= n_cp: column plan, start step, member mask
-    int32_t* item_step;
-    unsigned long long* item_mask;
-    int32_t* item_ready;       // publication flags (zeroed before the launch)
-    double* snap;              // fork snapshots, slot i - n_cp of fork item i
-    int32_t* dup_of;           // local trajectory indexing, global tau values
-    long long tau_base;        // global tau of local trajectory 0
-};
-
-template <int TPD>
-__global__ void __launch_bounds__(128 * TPD, NS_WGRP_CTAS) k_greedy_wgrp(const GreedyArgs a, const WgrpArgs x) {
-    constexpr int FPL = kV / TPD;
-    constexpr int SS = FPL + 2;
+__global__ void __launch_bounds__(128, NS_WGRP_CTAS) k_greedy_wgrp88(const GreedyArgs a, const WgrpArgs x) {
     constexpr int kLook = kStages - 2;
     constexpr int kRingW = kStages;
-    constexpr int NWM = 4 * TPD;
+    constexpr int NWM = 4;
     constexpr int MMAX = 64;
-    __shared__ __align__(16) double s_w[TPD][SS];
-    __shared__ __align__(16) double s_hb1[kV];
-    __shared__ __align__(16) double ring[kRingW][TPD * SS];
+    __shared__ __align__(16) double ring[kRingW][kSlot88];
+    __shared__ __align__(16) double s_w88[kSlot88];
     __shared__ int4 smeta[kRingW];
     // per warp and step parity: {key lo, key hi, device | x_winner << 7, max x} -- one 16-byte record
     // (dim sums < 2^25: T' * 128 < 2^24 is checked on the host)
@@ -1702,18 +1656,17 @@ __global__ void __launch_bounds__(128 * TPD, NS_WGRP_CTAS) k_greedy_wgrp(const G
     __shared__ int s_item;
     const int lane = threadIdx.x & 31, wi = threadIdx.x >> 5, nw = blockDim.x >> 5;
     const int nth = blockDim.x;
-    for (int k = threadIdx.x; k < kV; k += blockDim.x) {
-        s_w[k / FPL][k % FPL] = a.head.H2[k];
-        s_hb1[k] = a.head.hb1[k];
-    }
-    const int d = threadIdx.x / TPD, part = threadIdx.x % TPD;
+    const int fg = lane & 7, dg = lane >> 3;
+    const int d = threadIdx.x;   // this lane's device after the butterfly (bfly88)
     const bool dev = d < a.D;
+    // head weights of the lane's feature group from shared memory (padded like
+    // the row slots: conflict-free), registers are the scarce resource here
+    for (int q = threadIdx.x; q < kV; q += blockDim.x) s_w88[(q / kG8) * (kG8 + 2) + q % kG8] = a.head.H2[q];
+    const double* w = s_w88 + fg * (kG8 + 2);
     const int M = a.M;
-    const int my_slice = (2 * lane) / FPL, my_off = (2 * lane) % FPL;
-    const double2* w2 = reinterpret_cast<const double2*>(&s_w[part][0]);
-    // snapshot layout: u as [FPL][nth] doubles, then dsum, memory headroom [nth] --
+    // snapshot layout: u as [8 devices x 8 features][nth] doubles, then dsum, memory headroom [nth] --
     // coalesced per thread index
-    const size_t snap_doubles = (size_t)nth * (FPL + 2);
+    const size_t snap_doubles = (size_t)nth * (kV + 2);
     unsigned long long computed = 0, steps = 0;   // executed scores / group-steps (ns_stats)
 #ifdef NS_WGRP_TIMING   // debug build: clock64 per step phase of thread 0, printed by CTAs 0-3
     unsigned long long tph[7] = {0, 0, 0, 0, 0, 0, 0};
@@ -1804,19 +1757,25 @@ __global__ void __launch_bounds__(128 * TPD, NS_WGRP_CTAS) k_greedy_wgrp(const G
                 s_work[m] = ((mask >> m) & 1ULL) ? __ldcg(a.work + tau0 + m) : 0u;
             }
         }
-        double u[FPL];
+        double u[8][kG8];
         int dsum = 0;
         long long room = 0;   // memory headroom cap - bytes on this device (R7)
         if (item < x.n_cp) {
 #pragma unroll
-            for (int k = 0; k < FPL; ++k) u[k] = s_hb1[part * FPL + k];
+            for (int q = 0; q < kG8; ++q) {
+                const double h = a.head.hb1[kG8 * fg + q];
+#pragma unroll
+                for (int jj = 0; jj < 8; ++jj) u[jj][q] = h;
+            }
             room = cap;
         } else {
             const double* sp = x.snap + (size_t)(item - x.n_cp) * snap_doubles;
 #pragma unroll
-            for (int k = 0; k < FPL; ++k) u[k] = __ldcg(sp + (size_t)k * nth + threadIdx.x);
-            dsum = __double2loint(__ldcg(sp + (size_t)FPL * nth + threadIdx.x));
-            room = __double_as_longlong(__ldcg(sp + (size_t)(FPL + 1) * nth + threadIdx.x));
+            for (int jj = 0; jj < 8; ++jj)
+#pragma unroll
+                for (int q = 0; q < kG8; ++q) u[jj][q] = __ldcg(sp + (size_t)(jj * kG8 + q) * nth + threadIdx.x);
+            dsum = __double2loint(__ldcg(sp + (size_t)kV * nth + threadIdx.x));
+            room = __double_as_longlong(__ldcg(sp + (size_t)(kV + 1) * nth + threadIdx.x));
         }
         const int32_t* orow = a.ord_row + (size_t)g * a.Tpm;
         const int4* ometa = a.ord_meta + (size_t)g * a.Tpm;
@@ -1824,7 +1783,7 @@ __global__ void __launch_bounds__(128 * TPD, NS_WGRP_CTAS) k_greedy_wgrp(const G
             if (pp < Tp) {
                 const int r = __ldg(orow + pp);
                 const int sl = pp % kRingW;
-                cp_async16(&ring[sl][my_slice * SS + my_off], a.V + (size_t)r * kV + 2 * lane);
+                cp_async16(stage_dst88(ring[sl], lane), a.V + (size_t)r * kV + 2 * lane);
                 if (lane == 0) cp_async16(smeta + sl, ometa + pp);
             }
         };
@@ -1836,7 +1795,7 @@ __global__ void __launch_bounds__(128 * TPD, NS_WGRP_CTAS) k_greedy_wgrp(const G
             cp_async_wait<kLook - 1>();   // row p0 landed
         }
         __syncthreads();
-        unsigned cf = 0;                  // steps this thread's device was scored (part 0 threads)
+        unsigned cf = 0;                  // steps this lane's device was scored
         int rep = mask ? __ffsll((long long)mask) - 1 : 0;   // the row holding the group's history
         bool alive = mask != 0;
         int pend = p0;   // steps run = pend - p0
@@ -1855,14 +1814,11 @@ __global__ void __launch_bounds__(128 * TPD, NS_WGRP_CTAS) k_greedy_wgrp(const G
             const bool memok = dev && (bt <= room);
             const int xv = dsum + dt;
             const bool f = memok && xv <= cmax;
-            const double2* v2 = reinterpret_cast<const double2*>(&ring[sl][part * SS]);
-            // every device scores (no divergent branch: 3% faster than skipping
-            // the infeasible ones); an infeasible device's finite score is
-            // masked by its key ~0
-            double ps;
-            if constexpr (TPD == 1) ps = block_score_c(u, v2, a.head);
-            else ps = block_score<FPL>(u, v2, w2);
-            const double sco = a.head.hb2 + block_group_sum<TPD>(ps);
+            // every device scores (no divergent branch); an infeasible
+            // device's finite score is masked by its key ~0
+            double pp8[8];
+            part88(u, ring[sl], fg, w, pp8);
+            const double sco = a.head.hb2 + bfly88(pp8, fg);
             NS_TMARK(0)
             const long long sb = __double_as_longlong(sco + 0.0);
             const unsigned long long key =
@@ -1873,12 +1829,12 @@ __global__ void __launch_bounds__(128 * TPD, NS_WGRP_CTAS) k_greedy_wgrp(const G
                 const unsigned khi = (unsigned)(key >> 32), klo = (unsigned)key;
                 const unsigned mh = __reduce_min_sync(kFull, khi);
                 const unsigned ml = __reduce_min_sync(kFull, khi == mh ? klo : 0xFFFFFFFFu);
-                const unsigned hit = __ballot_sync(kFull, f && part == 0 && khi == mh && klo == ml);
-                const unsigned xm = __reduce_max_sync(kFull, f && part == 0 ? (unsigned)xv : 0u);
+                const unsigned hit = __ballot_sync(kFull, f && khi == mh && klo == ml);
+                const unsigned xm = __reduce_max_sync(kFull, f ? (unsigned)xv : 0u);
                 const int hl = hit ? __ffs(hit) - 1 : 0;
                 const int xw = __shfl_sync(kFull, xv, hl);
                 if (lane == 0)
-                    s_rec[par][wi] = make_uint4(ml, mh, (unsigned)(wi * (32 / TPD) + hl / TPD) | ((unsigned)xw << 7), xm);
+                    s_rec[par][wi] = make_uint4(ml, mh, (unsigned)(wi * 32 + hl) | ((unsigned)xw << 7), xm);
             }
             NS_TMARK(1)
             if (wi == 0) {   // the next row lands before the barrier (its slot was last read at p - 2)
@@ -1907,12 +1863,12 @@ __global__ void __launch_bounds__(128 * TPD, NS_WGRP_CTAS) k_greedy_wgrp(const G
             // = |F_max| (this thread's device counts in cf) minus the devices
             // with cap_m < x_d <= cap_max, counted only for the members whose
             // cap is below the largest feasible x (xmax)
-            cf += (f && part == 0) ? 1u : 0u;
+            cf += (f) ? 1u : 0u;
             if (xmax > (unsigned)cmin) {
                 for (unsigned long long mm = mask; mm; mm &= mm - 1) {
                     const int m = __ffsll((long long)mm) - 1;
                     if ((unsigned)s_cap[m] >= xmax) break;   // caps non-decreasing in m
-                    const unsigned b = __ballot_sync(kFull, f && part == 0 && xv > s_cap[m]);
+                    const unsigned b = __ballot_sync(kFull, f && xv > s_cap[m]);
                     if (lane == 0 && b) atomicSub(&s_work[m], (unsigned)__popc(b));
                 }
             }
@@ -1945,12 +1901,12 @@ __global__ void __launch_bounds__(128 * TPD, NS_WGRP_CTAS) k_greedy_wgrp(const G
                     const unsigned khi = (unsigned)(kc >> 32), klo = (unsigned)kc;
                     const unsigned mh = __reduce_min_sync(kFull, khi);
                     const unsigned ml = __reduce_min_sync(kFull, khi == mh ? klo : 0xFFFFFFFFu);
-                    const unsigned hit = __ballot_sync(kFull, fc && part == 0 && khi == mh && klo == ml);
+                    const unsigned hit = __ballot_sync(kFull, fc && khi == mh && klo == ml);
                     const int hl = hit ? __ffs(hit) - 1 : 0;
                     const int xw = __shfl_sync(kFull, xv, hl);
                     if (lane == 0) {
                         r_key[wi] = ((unsigned long long)mh << 32) | ml;
-                        r_dv[wi] = wi * (32 / TPD) + hl / TPD;
+                        r_dv[wi] = wi * 32 + hl;
                         r_xw[wi] = xw;
                     }
                     __syncthreads();
@@ -1991,14 +1947,18 @@ __global__ void __launch_bounds__(128 * TPD, NS_WGRP_CTAS) k_greedy_wgrp(const G
                     const int it = s_sub_item[k];
                     double* sp = x.snap + (size_t)(it - x.n_cp) * snap_doubles;
                     const bool mine = d == dk;
+                    const bool owner = wi == (dk >> 5) && dg == ((dk >> 3) & 3);
+                    const double* vs = ring[sl] + fg * (kG8 + 2);
 #pragma unroll
-                    for (int k2 = 0; k2 < FPL / 2; ++k2) {
-                        const double2 vv = v2[k2];
-                        sp[(size_t)(2 * k2) * nth + threadIdx.x] = mine ? u[2 * k2] + vv.x : u[2 * k2];
-                        sp[(size_t)(2 * k2 + 1) * nth + threadIdx.x] = mine ? u[2 * k2 + 1] + vv.y : u[2 * k2 + 1];
-                    }
-                    sp[(size_t)FPL * nth + threadIdx.x] = __hiloint2double(0, mine ? dsum + dt : dsum);
-                    sp[(size_t)(FPL + 1) * nth + threadIdx.x] = __longlong_as_double(mine ? room - bt : room);
+                    for (int jj = 0; jj < 8; ++jj)
+#pragma unroll
+                        for (int q = 0; q < kG8; ++q) {
+                            double val = u[jj][q];
+                            if (owner && jj == (dk & 7)) val += vs[q];
+                            __stcg(sp + (size_t)(jj * kG8 + q) * nth + threadIdx.x, val);
+                        }
+                    sp[(size_t)kV * nth + threadIdx.x] = __hiloint2double(0, mine ? dsum + dt : dsum);
+                    sp[(size_t)(kV + 1) * nth + threadIdx.x] = __longlong_as_double(mine ? room - bt : room);
                     // the subgroup's history row: the group's history so far + its choice
                     const unsigned long long km = s_sub_mask[k];
                     const int krep = __ffsll((long long)km) - 1;
@@ -2037,13 +1997,8 @@ __global__ void __launch_bounds__(128 * TPD, NS_WGRP_CTAS) k_greedy_wgrp(const G
             }
             NS_TMARK(6)
             // ---- the group's choice
+            if (wi == (bd >> 5) && dg == ((bd >> 3) & 3)) add88(u, ring[sl], fg, bd & 7);
             if (d == bd) {
-#pragma unroll
-                for (int k2 = 0; k2 < FPL / 2; ++k2) {
-                    const double2 vv = v2[k2];
-                    u[2 * k2] += vv.x;
-                    u[2 * k2 + 1] += vv.y;
-                }
                 dsum += dt;
                 room -= bt;
             }
@@ -2058,8 +2013,10 @@ __global__ void __launch_bounds__(128 * TPD, NS_WGRP_CTAS) k_greedy_wgrp(const G
         for (int m = threadIdx.x; m < M; m += blockDim.x)
             if ((mask >> m) & 1ULL) a.work[tau0 + m] = s_work[m] + gw;
         if (alive) {
-            const double hc = a.head.hb2 + block_group_sum<TPD>(block_head<FPL>(u, &s_w[part][0]));
-            if (dev && part == 0) {
+            double hp[8];
+            head88(u, w, hp);
+            const double hc = a.head.hb2 + bfly88(hp, fg);
+            if (dev) {
                 a.comp[(tau0 + rep) * a.D + d] = dsum > 0 ? hc : 0.0;   // reading R4
                 a.devdim[(tau0 + rep) * a.D + d] = dsum;
             }
@@ -2617,9 +2574,8 @@ ns_status launch_greedy(ns_ctx* ctx, const SearchBufs& b, const ns_tables* t, lo
         prof_end(ctx);
     } else if (b.wgrp &&
                (b.greedy_mode == NS_GREEDY_GROUPED || n_cp_launch >= NS_WGRP_MIN_CP)) {
-        // large D, many column plans: grouped trajectories (k_greedy_wgrp)
-        constexpr int TPD = NS_WGRP_TPD;
-        const int threads = ((b.D * TPD + 31) / 32) * 32;
+        // large D, many column plans: grouped trajectories (k_greedy_wgrp88)
+        const int threads = ((b.D + 31) / 32) * 32;   // one warp per 32 devices (8 x 8 layout)
         const long long g0 = tb / b.M, g1 = te / b.M;
         GreedyArgs a2 = a;
         a2.ord_row = b.ord_row + (size_t)g0 * b.Tpm;
@@ -2648,13 +2604,12 @@ ns_status launch_greedy(ns_ctx* ctx, const SearchBufs& b, const ns_tables* t, lo
         NS_CUDA(ctx, cudaMemsetAsync(b.witem_ready, 0, n_items * sizeof(int32_t), ctx->stream));
         const int ctas = (int)std::min<long long>((long long)n_items, (long long)ctx->sm_count * NS_WGRP_CTAS);
         prof_begin(ctx, PK_GREEDY);
-        k_greedy_wgrp<TPD><<<(unsigned)ctas, threads, 0, ctx->stream>>>(a2, x);
+        k_greedy_wgrp88<<<(unsigned)ctas, threads, 0, ctx->stream>>>(a2, x);
         prof_end(ctx);
     } else {
-        constexpr int TPD = NS_WIDE_TPD;
-        const int threads = ((b.D * TPD + 31) / 32) * 32;
+        const int threads = ((b.D + 31) / 32) * 32;
         prof_begin(ctx, PK_GREEDY);
-        k_greedy_wide<TPD><<<(unsigned)n, threads, 0, ctx->stream>>>(a);
+        k_greedy_wide88<<<(unsigned)n, threads, 0, ctx->stream>>>(a);
         prof_end(ctx);
         // no grouping: every trajectory carries its own plan
         NS_CUDA(ctx, cudaMemsetAsync(b.dup_of + tb, 0xff, (size_t)n * sizeof(int32_t), ctx->stream));
@@ -2841,15 +2796,15 @@ static void search_layout(const ns_ctx* ctx, int n_tasks, int T_max, int D, cons
         long long warps = std::min<long long>(max_cp, (long long)ctx->sm_count * W * NS_DEDUP_BLOCKS8);
         warps = std::max<long long>(W, std::min<long long>(warps, (long long)((512ull << 20) / per)));
         b.gscratch_warps = dp <= 16 ? (int)(((warps + W - 1) / W) * W) : 0;
-        // large D: fork snapshots of k_greedy_wgrp (one set of M - 1 slots per resident CTA)
-        // (k_greedy_wgrp packs dim sums in 25 bits: T' * 128 < 2^24)
+        // large D: fork snapshots of k_greedy_wgrp88 (one set of M - 1 slots per resident CTA)
+        // (k_greedy_wgrp88 packs dim sums in 25 bits: T' * 128 < 2^24)
         b.wgrp = dp > 16 && b.M <= 64 && b.greedy_mode != NS_GREEDY_LANES && (long long)b.Tpm * kMaxDim < (1 << 24);
         {   // a launch covers one rank's block of column plans (level 0: tasks; beam levels: S)
             const long long R = ctx->nranks;
             b.wgrp_cp_cap = (int)std::max<long long>((b.n_tasks + R - 1) / R, ((long long)b.S + R - 1) / R);
         }
-        const int nth = ((D * NS_WGRP_TPD + 31) / 32) * 32;
-        b.wsnap_doubles = (size_t)nth * (kV / NS_WGRP_TPD + 2);
+        const int nth = ((D + 31) / 32) * 32;   // 8 x 8 layout: 64 doubles of u per lane
+        b.wsnap_doubles = (size_t)nth * (kV + 2);
     }
 }
 

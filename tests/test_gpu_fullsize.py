@@ -84,7 +84,7 @@ def _compare(out, i, task, w, exp, min_margin, M, dim_cap=True):
 @pytest.mark.parametrize("name", sorted(FIX))
 def test_fullsize_against_oracle_fixture(ns, ctx, name, greedy):
     """greedy 0 = auto (a single task: the latency kernels), 1 = the grouped
-    kernels (k_greedy_dedup for D <= 16, k_greedy_wgrp for D = 128)."""
+    kernels (k_greedy_dedup for D <= 16, k_greedy_wgrp88 for D = 128)."""
     c = FIX[name]
     task = gen_task(c["config"], c["task_index"], T=c["T"] if c["T"] != CONFIGS[c["config"]]["T"] else None)
     assert task.T == c["T"]
@@ -160,8 +160,8 @@ def test_near_tie_tasks_are_certified(ns, ctx):
 
 @pytest.mark.parametrize("D", [40, 128])
 def test_wide_grouped_kernel_bit_identical_to_per_trajectory(ns, ctx, D):
-    """k_greedy_wgrp (identical trajectories share scores, forks on
-    divergence) against k_greedy_wide (every trajectory alone): same lane
+    """k_greedy_wgrp88 (identical trajectories share scores, forks on
+    divergence) against k_greedy_wide88 (every trajectory alone): same lane
     layout and summation order, so every output is bit-identical -- costs,
     assignments, grid indices, W -- on C5-shaped batches, table- and
     column-wise, and the executed-score counter is below W."""

@@ -1,5 +1,5 @@
 #!/bin/bash
-# A/B of k_greedy_wgrp build variants on the GPU box (run under gpurun):
+# A/B of k_greedy_wgrp88 build variants on the GPU box (run under gpurun):
 #   tools/ab_wgrp.sh name1 "-DFOO=1" name2 "-DBAR=1" ...
 # each variant: rebuild, the large-D bit-identity/oracle tests, C5 probe (128 tasks)
 while [ $# -gt 1 ]; do

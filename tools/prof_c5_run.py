@@ -1,4 +1,4 @@
-"""One C5 single-task column-wise search (for an ncu capture of k_greedy_wide)."""
+"""One C5 single-task column-wise search (for an ncu capture of k_greedy_wide88)."""
 import sys
 sys.path.insert(0, '/root/repo')
 import torch

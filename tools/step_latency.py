@@ -1,7 +1,7 @@
 """Per-step latency of the large-D greedy kernels on an otherwise idle GPU:
 one C5 task, table-wise (one column plan, 11 grid trajectories, ~1000
-steps each), grouped (k_greedy_wgrp: one chain + forks) vs per-trajectory
-(k_greedy_wide: 11 CTAs).  python tools/step_latency.py"""
+steps each), grouped (k_greedy_wgrp88: one chain + forks) vs per-trajectory
+(k_greedy_wide88: 11 CTAs).  python tools/step_latency.py"""
 import os
 import sys
 
