@@ -42,6 +42,7 @@ struct SearchBufs {
     int32_t* cp_len;
     int32_t* cp_plan;    // [S][Lcap]
     int32_t* cp_Tp;
+    int ord_b, ord_e;    // column plans whose cost order this rank builds (its greedy block; others get cp_Tp only)
     int32_t* ord_row;    // [S][Tpm]  variant row of the p-th table in cost order
     int4* ord_meta;      // [S][Tpm]  {dim, list index, bytes lo, bytes hi} of the p-th table (grouped greedy stream)
     // per traj
@@ -338,6 +339,7 @@ __global__ void k_build_order(SearchBufs b, TaskView tv) {
         b.cp_Tp[g] = Tp;
     }
     __syncthreads();
+    if (g < b.ord_b || g >= b.ord_e) return;   // another rank's greedy block (multi-rank)
     for (int i = threadIdx.x; i < n; i += blockDim.x) {
         key[i] = i < Tp ? -tv.C[rows[i]] : CUDART_INF;
         id[i] = i < Tp ? i : INT_MAX;
@@ -427,6 +429,7 @@ __global__ void __launch_bounds__(256) k_order_warp(SearchBufs b, TaskView tv, i
             b.cp_Tp[g] = Tp;
         }
         __syncwarp();
+        if (g < b.ord_b || g >= b.ord_e) continue;   // another rank's greedy block (multi-rank)
         for (int i = lane; i < Tp; i += 32) key[i] = tv.C[rows[i]];
         __syncwarp();
         if (Tp <= 64) {
@@ -2833,6 +2836,12 @@ ns_status run_search(ns_ctx* ctx, const ns_tables* t, int D, const ns_search_par
     const bool warp_order = b.Tpm <= 256;
     const size_t wsm = 8 * osm;
     auto launch_order = [&](int n_cp, int level0) {
+        // only this rank's greedy block needs the cost order (the same
+        // contiguous blocks as run_level_trajectories)
+        const long long R = ctx->emulated ? 1 : ctx->nranks;
+        const long long per = ((long long)n_cp + R - 1) / R;
+        b.ord_b = ctx->emulated ? 0 : (int)std::min<long long>(n_cp, ctx->rank * per);
+        b.ord_e = ctx->emulated ? n_cp : (int)std::min<long long>(n_cp, (long long)b.ord_b + per);
         prof_begin(ctx, PK_ORDER);
         if (warp_order) {
             const unsigned blocks = (unsigned)std::max(1, std::min((n_cp + 7) / 8, ctx->sm_count * 8));
