@@ -1,6 +1,9 @@
-"""Small runs of every hot kernel for compute-sanitizer (memcheck / racecheck):
-grouped greedy (pair-staged rows), per-lane greedy, large-D greedy, plan cost,
-precompute (both shapes), score_plans in both modes (tcgen05 two tile groups)."""
+"""Small runs of every hot kernel for compute-sanitizer (memcheck / racecheck /
+synccheck): grouped greedy (pair-staged rows), per-lane greedy, the large-D
+greedy in the 8x8 layout (k_greedy_wgrp88 with forks, k_greedy_wide88), plan
+cost, precompute (both shapes), score_plans in both modes (tcgen05 two tile
+groups), pre-training steps, the embedding-bag kernels (hot-row backward,
+exchange at one rank)."""
 import sys
 sys.path.insert(0, '/root/repo')
 import numpy as np
@@ -31,6 +34,34 @@ t40 = [gen_task("C3", 7, T=60, D=40)]
 d, o, c = ns.table_descs(t40)
 tabs = ns.ns_featurize_tables(ctx, d, o, c)
 ns.ns_shard_tablewise(ctx, tabs, 40, M=3)                         # large-D greedy + BIG plan cost
+g1 = ns.ns_shard_columnwise(ctx, tabs, 40, N=3, K=2, L=2, M=7, greedy=1)   # k_greedy_wgrp88 (forks)
+g2 = ns.ns_shard_columnwise(ctx, tabs, 40, N=3, K=2, L=2, M=7, greedy=2)   # k_greedy_wide88
+assert np.array_equal(g1["cost"], g2["cost"]) and np.array_equal(g1["assign"], g2["assign"])
 tabs.free()
+# F2: one Adam step of each cost model
+import torch
+from oracle import pretrain as opt
+from workload.pretrain_synth import gen_bag_indices, init_params
+rng = np.random.default_rng(0)
+feats = torch.from_numpy(rng.uniform(0, 1, (40, 5))).cuda()
+off = torch.from_numpy(np.arange(0, 41, 4, dtype=np.int32)).cuda()
+lab = torch.from_numpy(rng.uniform(1, 3, 10)).cuda()
+th = torch.from_numpy(init_params(opt.COMPUTE_WIDTHS, seed=1)).cuda()
+ns.ns_pretrain_compute_step(ctx, th, torch.zeros_like(th), torch.zeros_like(th), 1, 1e-3, feats, off, lab,
+                            torch.arange(10, dtype=torch.int32, device="cuda"), 4)
+# F3: embedding bag forward / hot-row backward / exchange (one rank)
+B = 512
+tabs3 = []
+for rows, dim, pool, skew in ((3000, 16, 4.0, 1.5), (800, 64, 6.0, 1.8), (500, 4, 2.0, 0.0)):
+    o_, i_ = gen_bag_indices(rows, pool, skew, B, rng)
+    tabs3.append((torch.randn(rows, dim, device="cuda"), torch.from_numpy(i_).cuda(), torch.from_numpy(o_).cuda()))
+C = 16 + 64 + 4
+out = torch.zeros(B, C, device="cuda")
+ns.ns_embedding_bag_forward(ctx, tabs3, B, out)
+ns.ns_embedding_bag_backward_sgd(ctx, tabs3, B, torch.randn(B, C, device="cuda"), 0.01)
+recv = torch.zeros(B * C, device="cuda")
+ns.ns_embedding_bag_forward_exchange(ctx, tabs3, B, [C], out, recv)
+ns.ns_embedding_bag_backward_exchange_sgd(ctx, tabs3, B, [C], recv, torch.zeros(B, C, device="cuda"), 0.01)
+torch.cuda.synchronize()
 ns.ns_destroy(ctx)
 print("sanitize run ok")
