@@ -35,6 +35,7 @@ struct WgrpQueue;   // k_greedy_wgrp88 work queue counters
 // ======================================================================
 struct SearchBufs {
     int n_tasks, D, M, K, N2, Lcap, Tpm, S, n_traj;
+    long long n_rows_lin;   // variant rows bound (n_tasks * T_max * kDepth): Brow capacity
     uint32_t greedy_mode;   // NS_GREEDY_*
     // per cp
     int32_t* cp_task;
@@ -42,6 +43,8 @@ struct SearchBufs {
     int32_t* cp_len;
     int32_t* cp_plan;    // [S][Lcap]
     int32_t* cp_Tp;
+    double* vmin;        // [n_tasks][64] smallest v_k over the task's variant rows (linear-regime certificate)
+    double* Brow;        // [rows] sum_k H2_k v_rk (k_task_lin)
     int ord_b, ord_e;    // column plans whose cost order this rank builds (its greedy block; others get cp_Tp only)
     int32_t* ord_row;    // [S][Tpm]  variant row of the p-th table in cost order
     int4* ord_meta;      // [S][Tpm]  {dim, list index, bytes lo, bytes hi} of the p-th table (grouped greedy stream)
@@ -500,6 +503,8 @@ struct GreedyArgs {
     const double* V;
     const int32_t* vdim;
     const int64_t* vbytes;
+    const double* vmin;   // [n_tasks][64] (k_task_lin)
+    const double* Brow;   // [rows] (k_task_lin)
     int8_t* assign;
     double* comp;
     int32_t* devdim;
@@ -739,7 +744,10 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 
-constexpr int kStages = 8;   // row-stream ring depth (large-D greedy)
+#ifndef NS_KSTAGES
+#define NS_KSTAGES 8
+#endif
+constexpr int kStages = NS_KSTAGES;   // row-stream ring depth (large-D greedy)
 #ifndef NS_DSTAGES
 #define NS_DSTAGES 3
 #endif
@@ -1489,6 +1497,125 @@ __device__ __forceinline__ void add88(double (&u)[8][kG8], const double* slot, i
         }
 }
 
+// Linear-regime certificate (exact).  vmin_k is the smallest v_tk over every
+// variant row the search can stream for the task (k_task_vmin).  If
+// u_dk + vmin_k >= 0 for all 64 features then every pre-activation
+// fl(u_dk + v_tk) of any later table is >= 0 (rounding is monotone), ReLU is
+// the identity, and C(S_d + {t}) = hb2 + sum_k H2_k (u_dk + v_tk) =
+// hb2 + (A_d + B_t), A_d = sum_k H2_k u_dk, B_t = sum_k H2_k v_tk -- the same
+// real number the literal form computes, evaluated in another order (as the
+// hoisting of H1 already is).  A warp whose 32 devices all hold the
+// certificate skips part88 / bfly88 and scores its devices as hb2 + (A_d +
+// B_t); otherwise it runs the literal form for all of them.  With monotone
+// cost models (non-negative v) a device holds it from its first table on
+// (92% of the C5 warp steps); with signed weights it never
+// triggers.  A_d starts from lin_init88 (a fresh trajectory, u = hb1) and
+// grows by B_t with every table the device takes (A_d + B_t is the real sum
+// of the new u); the flag is re-checked on the winner's updated u.  Fork
+// snapshots carry A_d and the flag, so the grouped and the per-trajectory
+// kernels stay bit-identical.
+
+// A_d and the certificate of the lane's own device (32 w + lane) for every
+// device of the warp at once: per device j of the lane's group the 8-feature
+// partial, the transposed butterfly (bfly88), one ballot per j for the flags
+template <typename W>
+__device__ __forceinline__ void lin_init88(const double (&u)[8][kG8], const W& w, const double* vm, int fg, int dg,
+                                           bool dev, double& A, bool& lin) {
+    double pa[8];
+    unsigned okm = 0;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+        double x = 0.0;
+        bool ok = true;
+#pragma unroll
+        for (int k = 0; k < kG8; ++k) {
+            x = fma(w[k], u[j][k], x);
+            ok &= (u[j][k] + vm[k] >= 0.0);
+        }
+        pa[j] = x;
+        okm |= (ok ? 1u : 0u) << j;
+    }
+    A = bfly88(pa, fg);
+    bool mine = true;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+        const unsigned bal = __ballot_sync(kFull, (okm >> j) & 1u);
+        if (j == fg) mine = ((bal >> (8 * dg)) & 0xFFu) == 0xFFu;
+    }
+    lin = mine || !dev;
+}
+
+// the winner's update u_j += v (as add88) and its certificate check on the 8
+// lanes holding it: returns whether this lane's 8 features of u_j now satisfy
+// u + vmin >= 0 (true on every other lane)
+__device__ __forceinline__ bool add88_lin(double (&u)[8][kG8], const double* slot, int fg, int j, const double* vm) {
+    const double2* s2 = reinterpret_cast<const double2*>(slot + fg * (kG8 + 2));
+    bool ok = true;
+#pragma unroll
+    for (int jj = 0; jj < 8; ++jj)
+        if (jj == j) {
+#pragma unroll
+            for (int q = 0; q < kG8 / 2; ++q) {
+                const double2 vv = s2[q];
+                u[jj][2 * q] += vv.x;
+                u[jj][2 * q + 1] += vv.y;
+                ok &= (u[jj][2 * q] + vm[2 * q] >= 0.0) & (u[jj][2 * q + 1] + vm[2 * q + 1] >= 0.0);
+            }
+        }
+    return ok;
+}
+
+// the certificate check of add88_lin without the update (a fork's device):
+// whether this lane's 8 features of u_j + v satisfy u_j + v + vmin >= 0,
+// the sums rounded as the update rounds them
+__device__ __forceinline__ bool chk88(const double (&u)[8][kG8], const double* slot, int fg, int j, const double* vm) {
+    const double2* s2 = reinterpret_cast<const double2*>(slot + fg * (kG8 + 2));
+    bool ok = true;
+#pragma unroll
+    for (int jj = 0; jj < 8; ++jj)
+        if (jj == j) {
+#pragma unroll
+            for (int q = 0; q < kG8 / 2; ++q) {
+                const double2 vv = s2[q];
+                const double x0 = u[jj][2 * q] + vv.x, x1 = u[jj][2 * q + 1] + vv.y;
+                ok &= (x0 + vm[2 * q] >= 0.0) & (x1 + vm[2 * q + 1] >= 0.0);
+            }
+        }
+    return ok;
+}
+
+// Per task: vmin_k over the variant rows a search can stream (depth <
+// depths; invalid variants, vdim 0, skipped), and per such row
+// B_r = sum_k H2_k v_rk (the linear-regime table term; lane l adds features
+// 2l, 2l + 1, then a xor butterfly).  One CTA of 8 warps per task, a warp per
+// row at a time.
+__global__ void __launch_bounds__(256) k_task_lin(TaskView tv, int depths, HeadParams hp, double* vmin,
+                                                  double* Brow) {
+    __shared__ double s_min[8][kV];
+    const int q = blockIdx.x, lane = threadIdx.x & 31, wi = threadIdx.x >> 5;
+    const double w0 = hp.H2[2 * lane], w1 = hp.H2[2 * lane + 1];
+    double m0 = CUDART_INF, m1 = CUDART_INF;
+    const int r0 = tv.off[q] * kDepth, r1 = tv.off[q + 1] * kDepth;
+    for (int r = r0 + wi; r < r1; r += 8) {
+        if (r % kDepth >= depths || __ldg(tv.vdim + r) == 0) continue;
+        const double2 v = __ldg(reinterpret_cast<const double2*>(tv.V + (size_t)r * kV) + lane);
+        m0 = fmin(m0, v.x);
+        m1 = fmin(m1, v.y);
+        double b = fma(w1, v.y, w0 * v.x);
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) b += __shfl_xor_sync(kFull, b, o);
+        if (lane == 0) Brow[r] = b;
+    }
+    s_min[wi][2 * lane] = m0;
+    s_min[wi][2 * lane + 1] = m1;
+    __syncthreads();
+    if (threadIdx.x < kV) {
+        double m = s_min[0][threadIdx.x];
+        for (int k = 1; k < 8; ++k) m = fmin(m, s_min[k][threadIdx.x]);
+        vmin[(size_t)q * kV + threadIdx.x] = m;
+    }
+}
+
 // Large D, latency mode (one trajectory per CTA) in the 8 x 8 layout; the
 // step is as in k_greedy_wide88: one CTA argmin per table (warp REDUX argmin,
 // then the warps' records through shared memory, double-buffered by step
@@ -1501,6 +1628,8 @@ __global__ void __launch_bounds__(128, 2) k_greedy_wide88(const GreedyArgs a) {
     __shared__ int s_dv[2][4];
     __shared__ int s_cnt[2][4];
     __shared__ int4 smeta[kRingW];
+    __shared__ __align__(16) double ringB[kRingW];   // B_t of the staged rows (k_task_lin)
+    __shared__ __align__(16) double s_vmin[kV];
     const int lane = threadIdx.x & 31, wi = threadIdx.x >> 5, nw = blockDim.x >> 5;
     const int fg = lane & 7, dg = lane >> 3;
     const long long tau = a.traj_begin + blockIdx.x;
@@ -1508,10 +1637,10 @@ __global__ void __launch_bounds__(128, 2) k_greedy_wide88(const GreedyArgs a) {
     const int g = (int)(tau / a.M), m = (int)(tau % a.M);
     const int d = threadIdx.x;   // this lane's device after the butterfly
     bool alive = a.cp_valid[g] != 0;
-    int Tp = 0, capd = 0;
+    int Tp = 0, capd = 0, q = 0;
     long long cap = 0;
     if (alive) {
-        const int q = a.cp_task[g];
+        q = a.cp_task[g];
         Tp = a.cp_Tp[g];
         cap = a.cap[q];
         capd = a.capdim[q * a.M + m];
@@ -1525,6 +1654,12 @@ __global__ void __launch_bounds__(128, 2) k_greedy_wide88(const GreedyArgs a) {
 #pragma unroll
         for (int j = 0; j < 8; ++j) u[j][k] = h;
     }
+    for (int k2 = threadIdx.x; k2 < kV; k2 += blockDim.x) s_vmin[k2] = a.vmin[(size_t)q * kV + k2];
+    __syncthreads();
+    const double* vmq = s_vmin + kG8 * fg;   // this lane's 8 features of vmin
+    double A = 0.0;   // linear-regime certificate of the lane's device (lin_init88)
+    bool lin = false;
+    lin_init88(u, w, vmq, fg, dg, dev, A, lin);
     int dsum = 0;
     long long bsum = 0;
     uint32_t work = 0;
@@ -1538,6 +1673,7 @@ __global__ void __launch_bounds__(128, 2) k_greedy_wide88(const GreedyArgs a) {
             const int slot = pp % kRingW;
             cp_async16(stage_dst88(ring[slot], lane), a.V + (size_t)r * kV + 2 * lane);
             if (lane == 0) cp_async16(smeta + slot, ometa + pp);
+            if (lane == 1) cp_async8(ringB + slot, a.Brow + r);
         }
         cp_async_commit();
     };
@@ -1556,9 +1692,15 @@ __global__ void __launch_bounds__(128, 2) k_greedy_wide88(const GreedyArgs a) {
         const int dt = mt.x;
         const long long bt = (long long)(((unsigned long long)(unsigned)mt.w << 32) | (unsigned)mt.z);
         const bool f = dev && (bsum + bt <= cap) && (dsum + dt <= capd);
-        double pp8[8];
-        part88(u, ring[sl], fg, w, pp8);
-        const double sco = a.head.hb2 + bfly88(pp8, fg);
+        const double Bt = ringB[sl];
+        double sco;
+        if (__all_sync(kFull, lin)) {   // every device of the warp holds the certificate
+            sco = a.head.hb2 + (A + Bt);
+        } else {
+            double pp8[8];
+            part88(u, ring[sl], fg, w, pp8);
+            sco = a.head.hb2 + bfly88(pp8, fg);
+        }
         const long long sb = __double_as_longlong(sco + 0.0);
         unsigned long long key = f ? (unsigned long long)(sb ^ ((sb >> 63) | (long long)0x8000000000000000ULL)) : ~0ULL;
         unsigned khi = (unsigned)(key >> 32), klo = (unsigned)key;
@@ -1585,7 +1727,15 @@ __global__ void __launch_bounds__(128, 2) k_greedy_wide88(const GreedyArgs a) {
             alive = false;
             break;
         }
-        if (wi == (bd >> 5) && dg == ((bd >> 3) & 3)) add88(u, ring[sl], fg, bd & 7);
+        if (wi == (bd >> 5)) {   // the winner's update and certificate (whole warp: ballot)
+            const bool mine = dg == ((bd >> 3) & 3);
+            const bool ok = mine ? add88_lin(u, ring[sl], fg, bd & 7, vmq) : true;
+            const unsigned okm = __ballot_sync(kFull, ok);
+            if (d == bd) {
+                A += Bt;
+                lin = ((okm >> (8 * dg)) & 0xFFu) == 0xFFu;
+            }
+        }
         if (d == bd) {
             dsum += dt;
             bsum += bt;
@@ -1644,6 +1794,8 @@ __global__ void __launch_bounds__(128, NS_WGRP_CTAS) k_greedy_wgrp88(const Greed
     constexpr int MMAX = 64;
     __shared__ __align__(16) double ring[kRingW][kSlot88];
     __shared__ __align__(16) double s_w88[kSlot88];
+    __shared__ __align__(16) double s_vmin[kV];
+    __shared__ __align__(16) double ringB[kRingW];   // B_t of the staged rows (k_task_lin)
     __shared__ int4 smeta[kRingW];
     // per warp and step parity: {key lo, key hi, device | x_winner << 7, max x} -- one 16-byte record
     // (dim sums < 2^25: T' * 128 < 2^24 is checked on the host)
@@ -1667,12 +1819,13 @@ __global__ void __launch_bounds__(128, NS_WGRP_CTAS) k_greedy_wgrp88(const Greed
     for (int q = threadIdx.x; q < kV; q += blockDim.x) s_w88[(q / kG8) * (kG8 + 2) + q % kG8] = a.head.H2[q];
     const double* w = s_w88 + fg * (kG8 + 2);
     const int M = a.M;
-    // snapshot layout: u as [8 devices x 8 features][nth] doubles, then dsum, memory headroom [nth] --
+    // snapshot layout: u as [8 devices x 8 features][nth] doubles, then dsum, memory headroom,
+    // A_d, certificate flag [nth] --
     // coalesced per thread index
-    const size_t snap_doubles = (size_t)nth * (kV + 2);
+    const size_t snap_doubles = (size_t)nth * (kV + 4);
     unsigned long long computed = 0, steps = 0;   // executed scores / group-steps (ns_stats)
 #ifdef NS_WGRP_TIMING   // debug build: clock64 per step phase of thread 0, printed by CTAs 0-3
-    unsigned long long tph[7] = {0, 0, 0, 0, 0, 0, 0};
+    unsigned long long tph[7] = {0, 0, 0, 0, 0, 0, 0}, nlin = 0;
     long long tlast = clock64();
 #define NS_TMARK(k)                                  \
     {                                                \
@@ -1780,21 +1933,36 @@ __global__ void __launch_bounds__(128, NS_WGRP_CTAS) k_greedy_wgrp88(const Greed
             dsum = __double2loint(__ldcg(sp + (size_t)kV * nth + threadIdx.x));
             room = __double_as_longlong(__ldcg(sp + (size_t)(kV + 1) * nth + threadIdx.x));
         }
+        for (int k2 = threadIdx.x; k2 < kV; k2 += blockDim.x) s_vmin[k2] = a.vmin[(size_t)q * kV + k2];
+        __syncthreads();
+        const double* vmq = s_vmin + kG8 * fg;   // this lane's 8 features of vmin
+        double A = 0.0;   // linear-regime certificate of the lane's device
+        bool lin = false;
+        if (item < x.n_cp) {
+            lin_init88(u, w, vmq, fg, dg, dev, A, lin);
+        } else {
+            const double* sp = x.snap + (size_t)(item - x.n_cp) * snap_doubles;
+            A = __ldcg(sp + (size_t)(kV + 2) * nth + threadIdx.x);
+            lin = __double2loint(__ldcg(sp + (size_t)(kV + 3) * nth + threadIdx.x)) != 0;
+        }
         const int32_t* orow = a.ord_row + (size_t)g * a.Tpm;
         const int4* ometa = a.ord_meta + (size_t)g * a.Tpm;
-        auto stage = [&](int pp) {
+        // warp 0 stages row pp with its index r (loaded a step ahead: rnext)
+        auto stage_r = [&](int pp, int r) {
             if (pp < Tp) {
-                const int r = __ldg(orow + pp);
                 const int sl = pp % kRingW;
                 cp_async16(stage_dst88(ring[sl], lane), a.V + (size_t)r * kV + 2 * lane);
                 if (lane == 0) cp_async16(smeta + sl, ometa + pp);
+                if (lane == 1) cp_async8(ringB + sl, a.Brow + r);
             }
         };
+        int rnext = 0;
         if (wi == 0) {
             for (int pp = p0; pp < p0 + kLook; ++pp) {
-                stage(pp);
+                stage_r(pp, pp < Tp ? __ldg(orow + pp) : 0);
                 cp_async_commit();
             }
+            rnext = p0 + kLook < Tp ? __ldg(orow + p0 + kLook) : 0;
             cp_async_wait<kLook - 1>();   // row p0 landed
         }
         __syncthreads();
@@ -1819,9 +1987,18 @@ __global__ void __launch_bounds__(128, NS_WGRP_CTAS) k_greedy_wgrp88(const Greed
             const bool f = memok && xv <= cmax;
             // every device scores (no divergent branch); an infeasible
             // device's finite score is masked by its key ~0
-            double pp8[8];
-            part88(u, ring[sl], fg, w, pp8);
-            const double sco = a.head.hb2 + bfly88(pp8, fg);
+            const double Bt = ringB[sl];
+            double sco;
+            if (__all_sync(kFull, lin)) {   // every device of the warp holds the certificate
+#ifdef NS_WGRP_TIMING
+                ++nlin;
+#endif
+                sco = a.head.hb2 + (A + Bt);
+            } else {
+                double pp8[8];
+                part88(u, ring[sl], fg, w, pp8);
+                sco = a.head.hb2 + bfly88(pp8, fg);
+            }
             NS_TMARK(0)
             const long long sb = __double_as_longlong(sco + 0.0);
             const unsigned long long key =
@@ -1840,12 +2017,16 @@ __global__ void __launch_bounds__(128, NS_WGRP_CTAS) k_greedy_wgrp88(const Greed
                     s_rec[par][wi] = make_uint4(ml, mh, (unsigned)(wi * 32 + hl) | ((unsigned)xw << 7), xm);
             }
             NS_TMARK(1)
-            if (wi == 0) {   // the next row lands before the barrier (its slot was last read at p - 2)
-                stage(p + kLook);
-                cp_async_commit();
-                cp_async_wait<kLook - 1>();
-            }
+            // warp 0: row p + 1 lands before the barrier that publishes it (rows
+            // up to p + kLook - 1 are in flight); row p + kLook is issued after
+            // the barrier, off the warps' critical path
+            if (wi == 0) cp_async_wait<kLook - 2>();
             __syncthreads();
+            if (wi == 0) {   // slot (p + kLook) % kRingW held row p - 2, read at step p - 2 at the latest
+                stage_r(p + kLook, rnext);
+                rnext = p + kLook + 1 < Tp ? __ldg(orow + p + kLook + 1) : 0;   // consumed next step
+                cp_async_commit();
+            }
             NS_TMARK(2)
             int bd, xstar;
             unsigned xmax;
@@ -1962,6 +2143,13 @@ __global__ void __launch_bounds__(128, NS_WGRP_CTAS) k_greedy_wgrp88(const Greed
                         }
                     sp[(size_t)kV * nth + threadIdx.x] = __hiloint2double(0, mine ? dsum + dt : dsum);
                     sp[(size_t)(kV + 1) * nth + threadIdx.x] = __longlong_as_double(mine ? room - bt : room);
+                    {   // A_d and the certificate with dk's choice applied (as the update below does)
+                        const bool ok = owner ? chk88(u, ring[sl], fg, dk & 7, vmq) : true;
+                        const unsigned okm = __ballot_sync(kFull, ok);
+                        const bool kl = ((okm >> (8 * dg)) & 0xFFu) == 0xFFu;
+                        sp[(size_t)(kV + 2) * nth + threadIdx.x] = mine ? A + Bt : A;
+                        sp[(size_t)(kV + 3) * nth + threadIdx.x] = __hiloint2double(0, mine ? (kl ? 1 : 0) : (lin ? 1 : 0));
+                    }
                     // the subgroup's history row: the group's history so far + its choice
                     const unsigned long long km = s_sub_mask[k];
                     const int krep = __ffsll((long long)km) - 1;
@@ -2000,7 +2188,15 @@ __global__ void __launch_bounds__(128, NS_WGRP_CTAS) k_greedy_wgrp88(const Greed
             }
             NS_TMARK(6)
             // ---- the group's choice
-            if (wi == (bd >> 5) && dg == ((bd >> 3) & 3)) add88(u, ring[sl], fg, bd & 7);
+            if (wi == (bd >> 5)) {   // the winner's update and certificate (whole warp: ballot)
+                const bool mine = dg == ((bd >> 3) & 3);
+                const bool ok = mine ? add88_lin(u, ring[sl], fg, bd & 7, vmq) : true;
+                const unsigned okm = __ballot_sync(kFull, ok);
+                if (d == bd) {
+                    A += Bt;
+                    lin = ((okm >> (8 * dg)) & 0xFFu) == 0xFFu;
+                }
+            }
             if (d == bd) {
                 dsum += dt;
                 room -= bt;
@@ -2036,11 +2232,11 @@ __global__ void __launch_bounds__(128, NS_WGRP_CTAS) k_greedy_wgrp88(const Greed
         if (threadIdx.x == 0) atomicAdd(&x.q->completed, 1u);
     }
 #ifdef NS_WGRP_TIMING
-    if (threadIdx.x == 0 && blockIdx.x < 4 && steps)
-        printf("wgrp cta %d steps %llu cycles/step: score %.0f key+warp %.0f stage+bar %.0f xwarp %.0f W %.0f "
-               "slow %.0f update+loop %.0f\n",
-               blockIdx.x, steps, (double)tph[0] / steps, (double)tph[1] / steps, (double)tph[2] / steps,
-               (double)tph[3] / steps, (double)tph[4] / steps, (double)tph[6] / steps, (double)tph[5] / steps);
+    if ((threadIdx.x & 31) == 0 && blockIdx.x < 2 && steps)
+        printf("wgrp cta %d warp %d steps %llu cycles/step: score %.0f key+warp %.0f stage+bar %.0f xwarp %.0f W %.0f "
+               "slow %.0f update+loop %.0f linear %.3f\n",
+               blockIdx.x, threadIdx.x >> 5, steps, (double)tph[0] / steps, (double)tph[1] / steps, (double)tph[2] / steps,
+               (double)tph[3] / steps, (double)tph[4] / steps, (double)tph[6] / steps, (double)tph[5] / steps, (double)nlin / steps);
 #endif
 #undef NS_TMARK
     if (threadIdx.x == 0 && computed) atomicAdd(a.computed, computed);
@@ -2415,6 +2611,8 @@ void carve(Carver& c, SearchBufs& b, OutStage& o, int Lout) {
     }
     b.ghist = c.take<int8_t>((size_t)b.gscratch_warps * b.M * b.Tpm);
     b.capdim = c.take<int32_t>((size_t)b.n_tasks * b.M);
+    b.vmin = c.take<double>((size_t)b.n_tasks * kV);
+    b.Brow = c.take<double>((size_t)b.n_rows_lin);
     b.beam_plan = c.take<int32_t>((size_t)b.n_tasks * b.K * b.Lcap);
     b.beam_cnt = c.take<int32_t>(b.n_tasks);
     b.best_cost = c.take<double>(b.n_tasks);
@@ -2468,6 +2666,8 @@ ns_status launch_greedy(ns_ctx* ctx, const SearchBufs& b, const ns_tables* t, lo
     a.V = t->d_V;
     a.vdim = t->d_vdim;
     a.vbytes = t->d_vbytes;
+    a.vmin = b.vmin;
+    a.Brow = b.Brow;
     a.assign = b.assign;
     a.comp = b.comp;
     a.devdim = b.devdim;
@@ -2772,6 +2972,7 @@ static void search_layout(const ns_ctx* ctx, int n_tasks, int T_max, int D, cons
     b = SearchBufs{};
     b.r14 = (p->flags & NS_R14_SPLITTABLE) ? 1 : 0;
     b.n_tasks = n_tasks;
+    b.n_rows_lin = (long long)n_tasks * T_max * kDepth;
     b.greedy_mode = p->flags & 3u;
     b.D = D;
     b.M = p->M;
@@ -2807,7 +3008,7 @@ static void search_layout(const ns_ctx* ctx, int n_tasks, int T_max, int D, cons
             b.wgrp_cp_cap = (int)std::max<long long>((b.n_tasks + R - 1) / R, ((long long)b.S + R - 1) / R);
         }
         const int nth = ((D + 31) / 32) * 32;   // 8 x 8 layout: 64 doubles of u per lane
-        b.wsnap_doubles = (size_t)nth * (kV + 2);
+        b.wsnap_doubles = (size_t)nth * (kV + 4);   // + dsum, headroom, A_d, certificate
     }
 }
 
@@ -2829,6 +3030,13 @@ ns_status run_search(ns_ctx* ctx, const ns_tables* t, int D, const ns_search_par
     carve(cv, b, o, Lout > 0 ? Lout : 1);
     ns_status s;
     const TaskView tv = task_view(t);
+    // linear-regime bound of the large-D greedy: rows a table-wise search
+    // streams are depth 0, a column-wise one any depth
+    if (D > 16) {
+        k_task_lin<<<b.n_tasks, 256, 0, ctx->stream>>>(tv, columnwise ? kDepth : 1, ctx->model.head, b.vmin,
+                                                       b.Brow);
+        NS_LAUNCHED(ctx);
+    }
     const size_t osm = order_smem(b.Tpm);                                        // per warp (k_order_warp)
     const size_t bsm = (size_t)pow2_ceil(b.Tpm) * 12 + (size_t)b.Tpm * 4 + 16;   // k_build_order
     if (bsm > 48 * 1024) cudaFuncSetAttribute(k_build_order, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bsm);
