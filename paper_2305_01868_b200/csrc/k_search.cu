@@ -1825,7 +1825,7 @@ __global__ void __launch_bounds__(128, NS_WGRP_CTAS) k_greedy_wgrp88(const Greed
     const size_t snap_doubles = (size_t)nth * (kV + 4);
     unsigned long long computed = 0, steps = 0;   // executed scores / group-steps (ns_stats)
 #ifdef NS_WGRP_TIMING   // debug build: clock64 per step phase of thread 0, printed by CTAs 0-3
-    unsigned long long tph[7] = {0, 0, 0, 0, 0, 0, 0}, nlin = 0;
+    unsigned long long tph[7] = {0, 0, 0, 0, 0, 0, 0}, nlin = 0, town = 0, nown = 0;
     long long tlast = clock64();
 #define NS_TMARK(k)                                  \
     {                                                \
@@ -1933,9 +1933,18 @@ __global__ void __launch_bounds__(128, NS_WGRP_CTAS) k_greedy_wgrp88(const Greed
             dsum = __double2loint(__ldcg(sp + (size_t)kV * nth + threadIdx.x));
             room = __double_as_longlong(__ldcg(sp + (size_t)(kV + 1) * nth + threadIdx.x));
         }
-        for (int k2 = threadIdx.x; k2 < kV; k2 += blockDim.x) s_vmin[k2] = a.vmin[(size_t)q * kV + k2];
-        __syncthreads();
+        bool vpos = true;
+        for (int k2 = threadIdx.x; k2 < kV; k2 += blockDim.x) {
+            s_vmin[k2] = a.vmin[(size_t)q * kV + k2];
+            vpos = vpos && s_vmin[k2] >= 0.0;
+        }
+        // vmin >= 0 (monotone cost models): a device's certificate, once
+        // held, holds for good (u only grows), so a linear warp never needs
+        // u again before the item ends -- the winner's u update is deferred
+        // past the next record publication (off the step's critical path)
+        const bool vmin_ok = __syncthreads_and(vpos) != 0;
         const double* vmq = s_vmin + kG8 * fg;   // this lane's 8 features of vmin
+        int pend_j = -1, pend_sl = 0;            // deferred u update (owner lanes)
         double A = 0.0;   // linear-regime certificate of the lane's device
         bool lin = false;
         if (item < x.n_cp) {
@@ -2020,6 +2029,10 @@ __global__ void __launch_bounds__(128, NS_WGRP_CTAS) k_greedy_wgrp88(const Greed
             // warp 0: row p + 1 lands before the barrier that publishes it (rows
             // up to p + kLook - 1 are in flight); row p + kLook is issued after
             // the barrier, off the warps' critical path
+            if (pend_j >= 0) {   // last step's deferred winner update (the ring slot is still intact)
+                add88(u, ring[pend_sl], fg, pend_j);
+                pend_j = -1;
+            }
             if (wi == 0) cp_async_wait<kLook - 2>();
             __syncthreads();
             if (wi == 0) {   // slot (p + kLook) % kRingW held row p - 2, read at step p - 2 at the latest
@@ -2189,19 +2202,39 @@ __global__ void __launch_bounds__(128, NS_WGRP_CTAS) k_greedy_wgrp88(const Greed
             NS_TMARK(6)
             // ---- the group's choice
             if (wi == (bd >> 5)) {   // the winner's update and certificate (whole warp: ballot)
+#ifdef NS_WGRP_TIMING
+                const long long to0 = clock64();
+#endif
                 const bool mine = dg == ((bd >> 3) & 3);
-                const bool ok = mine ? add88_lin(u, ring[sl], fg, bd & 7, vmq) : true;
-                const unsigned okm = __ballot_sync(kFull, ok);
-                if (d == bd) {
-                    A += Bt;
-                    lin = ((okm >> (8 * dg)) & 0xFFu) == 0xFFu;
+                if (vmin_ok && __all_sync(kFull, lin)) {
+                    // linear warp: the certificate persists; u's update waits
+                    if (mine) {
+                        pend_j = bd & 7;
+                        pend_sl = sl;
+                    }
+                    if (d == bd) A += Bt;
+                } else {
+                    const bool ok = mine ? add88_lin(u, ring[sl], fg, bd & 7, vmq) : true;
+                    const unsigned okm = __ballot_sync(kFull, ok);
+                    if (d == bd) {
+                        A += Bt;
+                        lin = ((okm >> (8 * dg)) & 0xFFu) == 0xFFu;
+                    }
                 }
+#ifdef NS_WGRP_TIMING
+                town += (unsigned long long)(clock64() - to0);
+                ++nown;
+#endif
             }
             if (d == bd) {
                 dsum += dt;
                 room -= bt;
             }
             if (threadIdx.x == 0) a.assign[(size_t)(tau0 + rep) * a.Tpm + mt.y] = (int8_t)bd;
+        }
+        if (pend_j >= 0) {   // the last step's deferred winner update
+            add88(u, ring[pend_sl], fg, pend_j);
+            pend_j = -1;
         }
         if (wi == 0) cp_async_wait<0>();
         __syncthreads();   // the representative row is complete
@@ -2234,9 +2267,10 @@ __global__ void __launch_bounds__(128, NS_WGRP_CTAS) k_greedy_wgrp88(const Greed
 #ifdef NS_WGRP_TIMING
     if ((threadIdx.x & 31) == 0 && blockIdx.x < 2 && steps)
         printf("wgrp cta %d warp %d steps %llu cycles/step: score %.0f key+warp %.0f stage+bar %.0f xwarp %.0f W %.0f "
-               "slow %.0f update+loop %.0f linear %.3f\n",
+               "slow %.0f update+loop %.0f linear %.3f owner-update %.0f (%.2f of steps)\n",
                blockIdx.x, threadIdx.x >> 5, steps, (double)tph[0] / steps, (double)tph[1] / steps, (double)tph[2] / steps,
-               (double)tph[3] / steps, (double)tph[4] / steps, (double)tph[6] / steps, (double)tph[5] / steps, (double)nlin / steps);
+               (double)tph[3] / steps, (double)tph[4] / steps, (double)tph[6] / steps, (double)tph[5] / steps, (double)nlin / steps,
+               nown ? (double)town / nown : 0.0, (double)nown / steps);
 #endif
 #undef NS_TMARK
     if (threadIdx.x == 0 && computed) atomicAdd(a.computed, computed);
