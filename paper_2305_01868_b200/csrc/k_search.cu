@@ -27,6 +27,7 @@
 namespace ns {
 
 struct WgrpQueue;   // k_greedy_wgrp88 work queue counters
+struct P2Hdr;       // phase-2 item header (k_greedy_p2)
 
 // ======================================================================
 // Device buffers of one search call (carved from the ctx arena).
@@ -68,6 +69,22 @@ struct SearchBufs {
     int32_t* witem_step;
     unsigned long long* witem_mask;
     int32_t* witem_ready;
+    // phase 2 of the large-D grouped greedy (k_greedy_p2):
+    // items handed over by k_greedy_wgrp88 once every device holds the
+    // linear certificate, plus the forks phase 2 makes; frozen u of the
+    // hand-offs; representatives whose u is replayed (k_greedy_replay)
+    int p2_cap, uf_cap, rp_cap;
+    P2Hdr* p2_hdr;       // [p2_cap]
+    uint32_t* p2_work;   // [p2_cap][64] work of each member so far
+    double* p2_A;        // [p2_cap][128] per-device A_d
+    long long* p2_room;  // [p2_cap][128] per-device memory headroom
+    int32_t* p2_dsum;    // [p2_cap][128] per-device dim sum
+    int32_t* p2_ready;   // [p2_cap] publication flags of phase-2 forks
+    unsigned int* p2_q;  // [8] counters: next, forks, completed, n_init, uf used, replay entries
+    double* uf_buf;      // [uf_cap][64][128] frozen u of the hand-offs
+    int32_t* rp_tau;     // [rp_cap] local tau of a representative to replay
+    int32_t* rp_uf;      // [rp_cap]
+    int32_t* rp_psw;     // [rp_cap] first step whose placement the frozen u lacks
     double* gscratch;    // grouped greedy group states
     int8_t* ghist;       // grouped greedy group histories [gscratch_warps][M][Tpm]
     int gscratch_warps;
@@ -1393,6 +1410,25 @@ struct WgrpArgs {
     double* snap;              // fork snapshots, slot i - n_cp of fork item i
     int32_t* dup_of;           // local trajectory indexing, global tau values
     long long tau_base;        // global tau of local trajectory 0
+    // phase-2 hand-off (see SearchBufs)
+    int p2_cap, uf_cap, rp_cap;
+    P2Hdr* p2_hdr;
+    uint32_t* p2_work;
+    double* p2_A;
+    long long* p2_room;
+    int32_t* p2_dsum;
+    int32_t* p2_ready;
+    unsigned int* p2_q;
+    double* uf_buf;
+    int32_t* rp_tau;
+    int32_t* rp_uf;
+    int32_t* rp_psw;
+};
+
+struct P2Hdr {   // 32 bytes
+    int g, p, rep, uf;
+    int p_sw, pad;
+    unsigned long long mask;
 };
 
 // ----------------------------------------------------------------------
@@ -1809,6 +1845,7 @@ __global__ void __launch_bounds__(128, NS_WGRP_CTAS) k_greedy_wgrp88(const Greed
     __shared__ int s_nsub;
     __shared__ unsigned long long s_dead, s_remain;
     __shared__ int s_item;
+    __shared__ int s_h, s_h2;   // phase-2 hand-off slots
     const int lane = threadIdx.x & 31, wi = threadIdx.x >> 5, nw = blockDim.x >> 5;
     const int nth = blockDim.x;
     const int fg = lane & 7, dg = lane >> 3;
@@ -1862,7 +1899,7 @@ __global__ void __launch_bounds__(128, NS_WGRP_CTAS) k_greedy_wgrp88(const Greed
             if (i < x.n_cp) {
                 got = i;
             } else if (i < x.n_items) {   // beyond n_items nothing can ever be published
-                unsigned ns_sleep = 128;   // exponential backoff: a waiting CTA shares its SM with a working one
+                unsigned ns_sleep = 128, it = 0;   // exponential backoff: a waiting CTA shares its SM with a working one
                 for (;;) {
                     if (vready[i]) {
                         got = i;
@@ -1871,13 +1908,16 @@ __global__ void __launch_bounds__(128, NS_WGRP_CTAS) k_greedy_wgrp88(const Greed
                     // all published items finished -> nothing can be published any more.
                     // Read `completed` BEFORE `forks`: an item publishes its forks
                     // before it completes, so completed == n_cp + forks (in this order)
-                    // means no item was running when `completed` was read.
-                    const unsigned done = vq[2];
-                    __threadfence();
-                    const unsigned pub = (unsigned)x.n_cp + vq[1];
-                    if (done == pub && (unsigned)i >= pub) break;
+                    // means no item was running when `completed` was read.  (Rarely:
+                    // the fence invalidates the L1 the SM's working CTA uses.)
+                    if ((++it & 7u) == 0) {
+                        const unsigned done = vq[2];
+                        __threadfence();
+                        const unsigned pub = (unsigned)x.n_cp + vq[1];
+                        if (done == pub && (unsigned)i >= pub) break;
+                    }
                     __nanosleep(ns_sleep);
-                    if (ns_sleep < 4096) ns_sleep <<= 1;
+                    if (ns_sleep < 8192) ns_sleep <<= 1;
                 }
                 __threadfence();
             }
@@ -1976,6 +2016,7 @@ __global__ void __launch_bounds__(128, NS_WGRP_CTAS) k_greedy_wgrp88(const Greed
         }
         __syncthreads();
         unsigned cf = 0;                  // steps this lane's device was scored
+        bool handed = false;              // the item went on to phase 2
         int rep = mask ? __ffsll((long long)mask) - 1 : 0;   // the row holding the group's history
         bool alive = mask != 0;
         int pend = p0;   // steps run = pend - p0
@@ -1998,7 +2039,8 @@ __global__ void __launch_bounds__(128, NS_WGRP_CTAS) k_greedy_wgrp88(const Greed
             // device's finite score is masked by its key ~0
             const double Bt = ringB[sl];
             double sco;
-            if (__all_sync(kFull, lin)) {   // every device of the warp holds the certificate
+            const bool wlin = __all_sync(kFull, lin);
+            if (wlin) {   // every device of the warp holds the certificate
 #ifdef NS_WGRP_TIMING
                 ++nlin;
 #endif
@@ -2022,8 +2064,11 @@ __global__ void __launch_bounds__(128, NS_WGRP_CTAS) k_greedy_wgrp88(const Greed
                 const unsigned xm = __reduce_max_sync(kFull, f ? (unsigned)xv : 0u);
                 const int hl = hit ? __ffs(hit) - 1 : 0;
                 const int xw = __shfl_sync(kFull, xv, hl);
-                if (lane == 0)
-                    s_rec[par][wi] = make_uint4(ml, mh, (unsigned)(wi * 32 + hl) | ((unsigned)xw << 7), xm);
+                if (lane == 0)   // bit 31: every device of the warp held the certificate
+                    s_rec[par][wi] = make_uint4(ml, mh,
+                                                (unsigned)(wi * 32 + hl) | ((unsigned)xw << 7) |
+                                                    (wlin ? 0x80000000u : 0u),
+                                                xm);
             }
             NS_TMARK(1)
             // warp 0: row p + 1 lands before the barrier that publishes it (rows
@@ -2043,17 +2088,18 @@ __global__ void __launch_bounds__(128, NS_WGRP_CTAS) k_greedy_wgrp88(const Greed
             NS_TMARK(2)
             int bd, xstar;
             unsigned xmax;
-            bool none;
+            bool none, alllin;
             {
-                const uint4 rc = lane < nw ? s_rec[par][lane] : make_uint4(~0u, ~0u, 0u, 0u);
+                const uint4 rc = lane < nw ? s_rec[par][lane] : make_uint4(~0u, ~0u, 0x80000000u, 0u);
                 const unsigned mh = __reduce_min_sync(kFull, rc.y);
                 const unsigned ml = __reduce_min_sync(kFull, rc.y == mh ? rc.x : 0xFFFFFFFFu);
                 const unsigned hit = __ballot_sync(kFull, lane < nw && rc.y == mh && rc.x == ml);
                 xmax = __reduce_max_sync(kFull, rc.w);
                 none = (mh & ml) == 0xFFFFFFFFu;
+                alllin = __all_sync(kFull, (rc.z >> 31) != 0u);
                 const unsigned dx = __shfl_sync(kFull, rc.z, hit ? __ffs(hit) - 1 : 0);
                 bd = (int)(dx & 127u);
-                xstar = (int)(dx >> 7);
+                xstar = (int)((dx >> 7) & 0xFFFFFFu);
             }
             NS_TMARK(3)
             // ---- work W per member (O12): |F_m| = #{memory-feasible d : x_d <= cap_m}
@@ -2231,6 +2277,54 @@ __global__ void __launch_bounds__(128, NS_WGRP_CTAS) k_greedy_wgrp88(const Greed
                 room -= bt;
             }
             if (threadIdx.x == 0) a.assign[(size_t)(tau0 + rep) * a.Tpm + mt.y] = (int8_t)bd;
+            // ---- hand-off to phase 2 (k_greedy_p2): every device held the
+            // certificate at this step (so it holds for good, vmin >= 0); the
+            // rest of the trajectory needs only (A_d, dim sum, headroom) per
+            // device -- phase 2 runs it with one warp per group, the frozen u
+            // is kept for the representative's final replay
+            if (alllin && vmin_ok && p + 2 < Tp) {
+                if (threadIdx.x == 0) {
+                    const unsigned ufs = atomicAdd(x.p2_q + 4, 1u);
+                    s_h = ufs < (unsigned)x.uf_cap ? (int)ufs : -1;
+                    s_h2 = s_h >= 0 ? (int)atomicAdd(x.p2_q + 3, 1u) : -1;
+                }
+                __syncthreads();
+                const int uf = s_h, slot = s_h2;
+                if (uf >= 0) {
+                    if (pend_j >= 0) {
+                        add88(u, ring[pend_sl], fg, pend_j);
+                        pend_j = -1;
+                    }
+                    double* up = x.uf_buf + (size_t)uf * kV * 128;
+#pragma unroll
+                    for (int jj = 0; jj < 8; ++jj)
+#pragma unroll
+                        for (int q2 = 0; q2 < kG8; ++q2) __stcg(up + (size_t)(jj * kG8 + q2) * 128 + threadIdx.x, u[jj][q2]);
+                    if (dev) {
+                        x.p2_A[(size_t)slot * 128 + d] = A;
+                        x.p2_room[(size_t)slot * 128 + d] = room;
+                        x.p2_dsum[(size_t)slot * 128 + d] = dsum;
+                    }
+                    const unsigned gwh = block_sum(cf);
+                    for (int m = threadIdx.x; m < M; m += blockDim.x)
+                        if ((mask >> m) & 1ULL) x.p2_work[(size_t)slot * 64 + m] = s_work[m] + gwh;
+                    if (threadIdx.x == 0) {
+                        P2Hdr h;
+                        h.g = g;
+                        h.p = p + 1;
+                        h.rep = rep;
+                        h.uf = uf;
+                        h.p_sw = p + 1;
+                        h.pad = 0;
+                        h.mask = mask;
+                        x.p2_hdr[slot] = h;
+                    }
+                    computed += gwh;
+                    steps += (unsigned long long)(p + 1 - p0);
+                    handed = true;
+                    break;
+                }
+            }
         }
         if (pend_j >= 0) {   // the last step's deferred winner update
             add88(u, ring[pend_sl], fg, pend_j);
@@ -2238,6 +2332,7 @@ __global__ void __launch_bounds__(128, NS_WGRP_CTAS) k_greedy_wgrp88(const Greed
         }
         if (wi == 0) cp_async_wait<0>();
         __syncthreads();   // the representative row is complete
+        if (!handed) {
         const unsigned gw = block_sum(cf);
         computed += gw;
         steps += (unsigned long long)(pend - p0);
@@ -2260,6 +2355,7 @@ __global__ void __launch_bounds__(128, NS_WGRP_CTAS) k_greedy_wgrp88(const Greed
             for (unsigned long long mm = mask & ~(1ULL << rep); mm; mm &= mm - 1)
                 copy_row(tau0 + rep, tau0 + __ffsll((long long)mm) - 1, Tp);
         }
+        }   // !handed
         __threadfence();
         __syncthreads();   // ring and shared state are reused by the next item
         if (threadIdx.x == 0) atomicAdd(&x.q->completed, 1u);
@@ -2275,6 +2371,463 @@ __global__ void __launch_bounds__(128, NS_WGRP_CTAS) k_greedy_wgrp88(const Greed
 #undef NS_TMARK
     if (threadIdx.x == 0 && computed) atomicAdd(a.computed, computed);
     if (threadIdx.x == 0 && steps) atomicAdd(a.computed + 1, steps);
+}
+
+
+// u_j += v from registers (phase-2 replay)
+__device__ __forceinline__ void addv88(double (&u)[8][kG8], const double (&v)[kG8], int j) {
+#pragma unroll
+    for (int jj = 0; jj < 8; ++jj)
+        if (jj == j) {
+#pragma unroll
+            for (int k = 0; k < kG8; ++k) u[jj][k] += v[k];
+        }
+}
+
+// ----------------------------------------------------------------------
+// Phase 2 of the large-D grouped greedy (k_greedy_p2).  Once every device
+// of a group holds the linear certificate (and vmin >= 0, so it holds for
+// good), a step needs only (A_d, dim sum, headroom) per device: the score is
+// hb2 + (A_d + B_t), the winner's update A += B_t (the same operations
+// k_greedy_wgrp88 and k_greedy_wide88 perform).  k_greedy_wgrp88 hands such
+// a group over (frozen u, per-device states, member work so far); here ONE
+// warp runs it -- each lane holds devices lane + 32 j (j < 4), every argmin is
+// a warp reduction, no barrier, ~40 registers, so many groups are resident
+// per SM.  The member splits (slow path) run inside the warp: the subgroup
+// holding the largest cap continues, every other one becomes a phase-2 fork
+// (tiny record) published on this kernel's queue.  Work counts, history rows
+// and links are written as k_greedy_wgrp88 writes them; the representative's
+// final per-device cost needs u, so it is queued for k_greedy_replay.
+__device__ __forceinline__ int p2_cap_of(int cap0, int cap1, int m) {
+    const int c0 = __shfl_sync(kFull, cap0, m & 31), c1 = __shfl_sync(kFull, cap1, m & 31);
+    return m < 32 ? c0 : c1;
+}
+
+#ifndef NS_P2_CTAS
+#define NS_P2_CTAS 2   // resident 8-warp CTAs per SM of k_greedy_p2
+#endif
+__global__ void __launch_bounds__(256, NS_P2_CTAS) k_greedy_p2(const GreedyArgs a, const WgrpArgs x) {
+    const int lane = threadIdx.x & 31;
+    const int M = a.M, D = a.D;
+    volatile unsigned int* vq = x.p2_q;   // [0] claimed [1] forks [2] completed [3] hand-offs [4] frozen u [5] replays
+    volatile int32_t* vready = x.p2_ready;
+    const unsigned n_init = __ldcg(x.p2_q + 3);
+    unsigned long long computed = 0, nsteps = 0;
+#ifdef NS_WGRP_TIMING
+    unsigned long long t_loop = 0, t_claim = 0, n_items = 0, t_key = 0, t_w = 0;
+    long long tc0 = clock64();
+#endif
+    for (;;) {
+        // ---- claim an item (a hand-off, or a fork once published)
+        int item = -1;
+        if (lane == 0) {
+            const unsigned i = atomicAdd(x.p2_q + 0, 1u);
+            if (i < n_init) {
+                item = (int)i;
+            } else if (i < (unsigned)x.p2_cap) {
+                // a waiting warp polls its slot's flag (L2) and sleeps; the
+                // fenced termination test runs rarely -- a fence invalidates the
+                // SM's L1, which the working warps on the SM depend on
+                unsigned ns = 256, it = 0;
+                for (;;) {
+                    if (vready[i]) {
+                        item = (int)i;
+                        break;
+                    }
+                    if ((++it & 7u) == 0) {
+                        const unsigned done = vq[2];   // completed before published (see k_greedy_wgrp88)
+                        __threadfence();
+                        const unsigned pub = n_init + vq[1];
+                        if (done == pub && i >= pub) break;
+                    }
+                    __nanosleep(ns);
+                    if (ns < 16384) ns <<= 1;
+                }
+                __threadfence();
+            }
+        }
+        item = __shfl_sync(kFull, item, 0);
+#ifdef NS_WGRP_TIMING
+        const long long tc1 = clock64();
+        t_claim += (unsigned long long)(tc1 - tc0);
+        ++n_items;
+#endif
+        if (item < 0) break;
+        const long long* hp = reinterpret_cast<const long long*>(x.p2_hdr + item);
+        P2Hdr h;
+        {
+            long long hv[4];
+#pragma unroll
+            for (int k = 0; k < 4; ++k) hv[k] = __ldcg(hp + k);
+            h = *reinterpret_cast<P2Hdr*>(hv);
+        }
+        const int g = h.g, uf = h.uf, p_sw = h.p_sw;
+        int rep = h.rep;
+        unsigned long long mask = h.mask;
+        const long long tau0 = (long long)g * M;
+        const int q = a.cp_task[g];
+        const int Tp = a.cp_Tp[g];
+        const int cap0 = lane < M ? a.capdim[q * M + lane] : INT_MAX;
+        const int cap1 = lane + 32 < M ? a.capdim[q * M + lane + 32] : INT_MAX;
+        unsigned wk0 = (lane < M && ((mask >> lane) & 1ULL)) ? __ldcg(x.p2_work + (size_t)item * 64 + lane) : 0u;
+        unsigned wk1 = (lane + 32 < M && ((mask >> (lane + 32)) & 1ULL))
+                           ? __ldcg(x.p2_work + (size_t)item * 64 + lane + 32) : 0u;
+        double A4[4];
+        int ds4[4];
+        long long rm4[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const int dd = lane + 32 * j;
+            const bool v = dd < D;
+            A4[j] = v ? __ldcg(x.p2_A + (size_t)item * 128 + dd) : 0.0;
+            ds4[j] = v ? __ldcg(x.p2_dsum + (size_t)item * 128 + dd) : 0;
+            rm4[j] = v ? __ldcg(x.p2_room + (size_t)item * 128 + dd) : 0;
+        }
+        int cmin = p2_cap_of(cap0, cap1, __ffsll((long long)mask) - 1);
+        int cmax = p2_cap_of(cap0, cap1, 63 - __clzll((long long)mask));
+        const int32_t* orow = a.ord_row + (size_t)g * a.Tpm;
+        const int4* ometa = a.ord_meta + (size_t)g * a.Tpm;
+        auto copy_row = [&](long long src, long long dst, int n) {
+            const int8_t* sp = a.assign + (size_t)src * a.Tpm;
+            int8_t* dp = a.assign + (size_t)dst * a.Tpm;
+            for (int i = lane; i < n; i += 32) dp[i] = __ldcg(sp + i);
+            __syncwarp();
+        };
+        bool alive = true;
+        // the step stream in chunks of 32 steps, lane l holding step c + l:
+        // chunk c in (cm, cB), chunk c + 32 in flight (nm, nB), the row indices
+        // of chunk c + 64 in flight (nr) -- one load latency per 32 steps
+        const int c0 = h.p;
+        auto ld_m = [&](int pp) { return pp < Tp ? __ldg(ometa + pp) : make_int4(0, 0, 0, 0); };
+        auto ld_r = [&](int pp) { return pp < Tp ? __ldg(orow + pp) : 0; };
+        int4 cm = ld_m(c0 + lane);
+        double cB = __ldg(a.Brow + ld_r(c0 + lane));
+        int nr0 = ld_r(c0 + 32 + lane);
+        int4 nm = ld_m(c0 + 32 + lane);
+        double nB = __ldg(a.Brow + nr0);
+        int nr = ld_r(c0 + 64 + lane);
+#pragma unroll 1
+        for (int p = h.p; p < Tp; ++p) {
+            const int k32 = (p - c0) & 31;
+            if (k32 == 0 && p > c0) {   // next chunk
+                cm = nm;
+                cB = nB;
+                nm = ld_m(p + 32 + lane);
+                nB = __ldg(a.Brow + nr);
+                nr = ld_r(p + 64 + lane);
+            }
+            int4 mt;
+            mt.x = __shfl_sync(kFull, cm.x, k32);
+            mt.y = __shfl_sync(kFull, cm.y, k32);
+            mt.z = __shfl_sync(kFull, cm.z, k32);
+            mt.w = __shfl_sync(kFull, cm.w, k32);
+            const double Bt = __shfl_sync(kFull, cB, k32);
+            const int dt = mt.x, li = mt.y;
+#ifdef NS_WGRP_TIMING
+            const long long tk0 = clock64();
+#endif
+            const long long bt = (long long)(((unsigned long long)(unsigned)mt.w << 32) | (unsigned)mt.z);
+            int xj[4];
+            bool fj[4];
+            unsigned long long best = ~0ULL;
+            int bj = 0, cfl = 0;
+            unsigned xm = 0;
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                xj[j] = ds4[j] + dt;
+                fj[j] = lane + 32 * j < D && bt <= rm4[j] && xj[j] <= cmax;
+                const long long sb = __double_as_longlong(a.head.hb2 + (A4[j] + Bt) + 0.0);
+                const unsigned long long kj =
+                    fj[j] ? (unsigned long long)(sb ^ ((sb >> 63) | (long long)0x8000000000000000ULL)) : ~0ULL;
+                if (kj < best) {   // strict: the lane's lowest device keeps ties
+                    best = kj;
+                    bj = j;
+                }
+                if (fj[j]) {
+                    xm = max(xm, (unsigned)xj[j]);
+                    ++cfl;
+                }
+            }
+            const unsigned khi = (unsigned)(best >> 32), klo = (unsigned)best;
+            const unsigned mh = __reduce_min_sync(kFull, khi);
+            const unsigned ml = __reduce_min_sync(kFull, khi == mh ? klo : 0xFFFFFFFFu);
+            const bool none = (mh & ml) == 0xFFFFFFFFu;
+            const unsigned dmin =
+                __reduce_min_sync(kFull, (khi == mh && klo == ml) ? (unsigned)(32 * bj + lane) : 0xFFFFFFFFu);
+            const unsigned xmax = __reduce_max_sync(kFull, xm);
+            const unsigned cfc = __reduce_add_sync(kFull, (unsigned)cfl);
+            int bd = none ? 0 : (int)dmin;
+            const int xb = bj == 0 ? xj[0] : bj == 1 ? xj[1] : bj == 2 ? xj[2] : xj[3];
+            const int xstar = __shfl_sync(kFull, xb, bd & 31);
+            computed += cfc;
+            ++nsteps;
+#ifdef NS_WGRP_TIMING
+            const long long tk1 = clock64();
+            t_key += (unsigned long long)(tk1 - tk0);
+#endif
+            // ---- work W per member (O12): |F_max| minus the devices with cap_m < x_d
+            if (lane < M && ((mask >> lane) & 1ULL)) wk0 += cfc;
+            if (lane + 32 < M && ((mask >> (lane + 32)) & 1ULL)) wk1 += cfc;
+            if (xmax > (unsigned)cmin) {
+                for (unsigned long long mm = mask; mm; mm &= mm - 1) {
+                    const int m = __ffsll((long long)mm) - 1;
+                    const int cm = p2_cap_of(cap0, cap1, m);
+                    if ((unsigned)cm >= xmax) break;   // caps non-decreasing in m
+                    int c = 0;
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) c += (fj[j] && xj[j] > cm) ? 1 : 0;
+                    const unsigned cnt = __reduce_add_sync(kFull, (unsigned)c);
+                    if (lane == (m & 31)) {
+                        if (m < 32) wk0 -= cnt;
+                        else wk1 -= cnt;
+                    }
+                }
+            }
+#ifdef NS_WGRP_TIMING
+            t_w += (unsigned long long)(clock64() - tk1);
+#endif
+            if (none) {   // nothing feasible even under the largest cap: the group strands
+                alive = false;
+                break;
+            }
+            if (xstar > cmin) {
+                // ---- slow path: members split by the caps that admit the winners
+                unsigned long long take0 = 0;
+                for (unsigned long long mm = mask; mm; mm &= mm - 1) {
+                    const int m = __ffsll((long long)mm) - 1;
+                    if (p2_cap_of(cap0, cap1, m) >= xstar) take0 |= 1ULL << m;
+                }
+                unsigned long long rem = mask & ~take0, dead = 0;
+                while (rem) {
+                    const int c = p2_cap_of(cap0, cap1, 63 - __clzll((long long)rem));
+                    unsigned long long b2 = ~0ULL;
+                    int bj2 = 0;
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) {
+                        const long long sb = __double_as_longlong(a.head.hb2 + (A4[j] + Bt) + 0.0);
+                        const unsigned long long kj = (fj[j] && xj[j] <= c)
+                                                          ? (unsigned long long)(sb ^ ((sb >> 63) | (long long)0x8000000000000000ULL))
+                                                          : ~0ULL;
+                        if (kj < b2) {
+                            b2 = kj;
+                            bj2 = j;
+                        }
+                    }
+                    const unsigned h2 = (unsigned)(b2 >> 32), l2 = (unsigned)b2;
+                    const unsigned mh2 = __reduce_min_sync(kFull, h2);
+                    const unsigned ml2 = __reduce_min_sync(kFull, h2 == mh2 ? l2 : 0xFFFFFFFFu);
+                    if ((mh2 & ml2) == 0xFFFFFFFFu) {   // no feasible device under these members' caps
+                        dead = rem;
+                        break;
+                    }
+                    const int dk = (int)__reduce_min_sync(kFull, (h2 == mh2 && l2 == ml2) ? (unsigned)(32 * bj2 + lane)
+                                                                                         : 0xFFFFFFFFu);
+                    const int xb2 = bj2 == 0 ? xj[0] : bj2 == 1 ? xj[1] : bj2 == 2 ? xj[2] : xj[3];
+                    const int xk = __shfl_sync(kFull, xb2, dk & 31);
+                    unsigned long long take = 0;
+                    for (unsigned long long mm = rem; mm; mm &= mm - 1) {
+                        const int m = __ffsll((long long)mm) - 1;
+                        if (p2_cap_of(cap0, cap1, m) >= xk) take |= 1ULL << m;
+                    }
+                    rem &= ~take;
+                    // fork: the subgroup with its own choice, as a phase-2 item
+                    int slot = 0;
+                    if (lane == 0) slot = (int)(n_init + atomicAdd(x.p2_q + 1, 1u));
+                    slot = __shfl_sync(kFull, slot, 0);
+                    const int krep = __ffsll((long long)take) - 1;
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) {
+                        const int dd = lane + 32 * j;
+                        if (dd < D) {
+                            const bool mine = dd == dk;
+                            x.p2_A[(size_t)slot * 128 + dd] = mine ? A4[j] + Bt : A4[j];
+                            x.p2_dsum[(size_t)slot * 128 + dd] = mine ? ds4[j] + dt : ds4[j];
+                            x.p2_room[(size_t)slot * 128 + dd] = mine ? rm4[j] - bt : rm4[j];
+                        }
+                    }
+                    if (lane < M && ((take >> lane) & 1ULL)) x.p2_work[(size_t)slot * 64 + lane] = wk0;
+                    if (lane + 32 < M && ((take >> (lane + 32)) & 1ULL)) x.p2_work[(size_t)slot * 64 + lane + 32] = wk1;
+                    copy_row(tau0 + rep, tau0 + krep, Tp);   // the group's history so far
+                    if (lane == 0) {
+                        a.assign[(size_t)(tau0 + krep) * a.Tpm + li] = (int8_t)dk;   // + its choice
+                        P2Hdr fh;
+                        fh.g = g;
+                        fh.p = p + 1;
+                        fh.rep = krep;
+                        fh.uf = uf;
+                        fh.p_sw = p_sw;
+                        fh.pad = 0;
+                        fh.mask = take;
+                        x.p2_hdr[slot] = fh;
+                        __threadfence();
+                        atomicExch(x.p2_ready + slot, 1);   // publish
+                    }
+                    __syncwarp();
+                }
+                // stranded members (feas stays 0): their work
+                if (lane < M && ((dead >> lane) & 1ULL)) a.work[tau0 + lane] = wk0;
+                if (lane + 32 < M && ((dead >> (lane + 32)) & 1ULL)) a.work[tau0 + lane + 32] = wk1;
+                mask = take0;
+                cmin = p2_cap_of(cap0, cap1, __ffsll((long long)mask) - 1);
+                cmax = p2_cap_of(cap0, cap1, 63 - __clzll((long long)mask));
+                const int nrep = __ffsll((long long)mask) - 1;
+                if (nrep != rep) {
+                    copy_row(tau0 + rep, tau0 + nrep, Tp);
+                    rep = nrep;
+                }
+            }
+            // ---- the group's choice
+#pragma unroll
+            for (int j = 0; j < 4; ++j)
+                if (lane + 32 * j == bd) {
+                    A4[j] += Bt;
+                    ds4[j] += dt;
+                    rm4[j] -= bt;
+                }
+            if (lane == 0) a.assign[(size_t)(tau0 + rep) * a.Tpm + li] = (int8_t)bd;
+            __syncwarp();
+        }
+#ifdef NS_WGRP_TIMING
+        tc0 = clock64();
+        t_loop += (unsigned long long)(tc0 - tc1);
+#endif
+        // ---- item end: members' work; representative's dims, links of the others, replay entry
+        if (lane < M && ((mask >> lane) & 1ULL)) a.work[tau0 + lane] = wk0;
+        if (lane + 32 < M && ((mask >> (lane + 32)) & 1ULL)) a.work[tau0 + lane + 32] = wk1;
+        if (alive) {
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                const int dd = lane + 32 * j;
+                if (dd < D) a.devdim[(tau0 + rep) * D + dd] = ds4[j];
+            }
+            for (int m = lane; m < M; m += 32)
+                if ((mask >> m) & 1ULL) {
+                    a.feas[tau0 + m] = 1;
+                    x.dup_of[tau0 + m] = m == rep ? -1 : (int32_t)(x.tau_base + tau0 + rep);
+                }
+            __syncwarp();
+            for (unsigned long long mm = mask & ~(1ULL << rep); mm; mm &= mm - 1)
+                copy_row(tau0 + rep, tau0 + __ffsll((long long)mm) - 1, Tp);
+            if (lane == 0) {
+                const unsigned e = atomicAdd(x.p2_q + 5, 1u);
+                x.rp_tau[e] = (int32_t)(tau0 + rep);
+                x.rp_uf[e] = uf;
+                x.rp_psw[e] = p_sw;
+            }
+        }
+        __threadfence();
+        __syncwarp();
+        if (lane == 0) atomicAdd(x.p2_q + 2, 1u);   // completed
+    }
+#ifdef NS_WGRP_TIMING
+    if (lane == 0 && (blockIdx.x < 2) && (threadIdx.x >> 5) < 2)
+        printf("p2 cta %d warp %d: items %llu steps %llu cycles/step %.0f (keys %.0f W %.0f) claim-wait cycles %llu (n_init %u)\n",
+               blockIdx.x, threadIdx.x >> 5, n_items, nsteps, nsteps ? (double)t_loop / nsteps : 0.0,
+               nsteps ? (double)t_key / nsteps : 0.0, nsteps ? (double)t_w / nsteps : 0.0, t_claim, n_init);
+#endif
+    if (lane == 0 && computed) atomicAdd(a.computed, computed);
+    if (lane == 0 && nsteps) atomicAdd(a.computed + 1, nsteps);
+}
+
+// The representatives of phase-2 groups: u = the frozen u of the hand-off +
+// every later placement replayed in step order (the same additions, in the
+// same order, the per-trajectory kernel makes), then the head in the order
+// of k_greedy_wide88 / k_greedy_wgrp88.  One CTA per representative, ONE
+// thread per device holding all 64 features: the steps' (device, row) go to
+// shared memory, each thread scans them for its own device (a device takes
+// ~T' / D rows) and adds those rows in step order; the head is the 8 x 8
+// order written out -- per feature group fg an FMA chain over its 8 features
+// (head88), then the tree bfly88 builds for device index j = d & 7:
+// ((P_j + P_j^4) + (P_j^2 + P_j^6)) + ((P_j^1 + P_j^5) + (P_j^3 + P_j^7)).
+__global__ void __launch_bounds__(128, 2) k_greedy_replay(const GreedyArgs a, const WgrpArgs x) {
+    extern __shared__ __align__(16) int s_rp[];   // [Tpm] rows, [Tpm] per-device lists, [Tpm] devices (int8)
+    __shared__ int s_cnt[128], s_off[128];
+    const int d = threadIdx.x;
+    const bool dev = d < a.D;
+    const unsigned n = __ldcg(x.p2_q + 5);
+    int* srow = s_rp;
+    int* s_lst = s_rp + a.Tpm;
+    int8_t* sdev = reinterpret_cast<int8_t*>(s_rp + 2 * a.Tpm);
+    const int wgi = d >> 5, dgi = (d >> 3) & 3, jd = d & 7;   // this device's place in the 8 x 8 layout
+    for (unsigned e = blockIdx.x; e < n; e += gridDim.x) {
+        const long long tau = x.rp_tau[e];
+        const int uf = x.rp_uf[e], p_sw = x.rp_psw[e];
+        const int g = (int)(tau / a.M);
+        const int Tp = a.cp_Tp[g];
+        const int ns = Tp - p_sw;
+        const int8_t* hist = a.assign + (size_t)tau * a.Tpm;
+        const int32_t* orow = a.ord_row + (size_t)g * a.Tpm;
+        const int4* ometa = a.ord_meta + (size_t)g * a.Tpm;
+        __syncthreads();   // the previous representative's steps are consumed
+        for (int i = threadIdx.x; i < ns; i += blockDim.x) {
+            srow[i] = __ldg(orow + p_sw + i);
+            sdev[i] = __ldcg(hist + __ldg(ometa + p_sw + i).y);
+        }
+        __syncthreads();
+        // frozen u of this device: 8 x 8 layout, lane (wgi, dgi, fg) held features 8 fg .. of device jd
+        const double* up = x.uf_buf + (size_t)uf * kV * 128;
+        double u[kV];
+#pragma unroll
+        for (int fg = 0; fg < 8; ++fg)
+#pragma unroll
+            for (int q2 = 0; q2 < kG8; ++q2)
+                u[kG8 * fg + q2] = __ldcg(up + (size_t)(jd * kG8 + q2) * 128 + (32 * wgi + 8 * dgi + fg));
+        // this device's rows in step order: one pass counting, one pass
+        // copying the row indices into this thread's region of the list,
+        // then the additions with every thread of the warp active at once
+        int cnt = 0;
+        for (int i = 0; i < ns; ++i) cnt += sdev[i] == d ? 1 : 0;
+        s_cnt[d] = cnt;
+        __syncthreads();
+        if (threadIdx.x < 32) {   // exclusive prefix of the counts
+            int v0 = s_cnt[4 * threadIdx.x], v1 = s_cnt[4 * threadIdx.x + 1], v2 = s_cnt[4 * threadIdx.x + 2],
+                v3 = s_cnt[4 * threadIdx.x + 3];
+            int tot = v0 + v1 + v2 + v3, incl = tot;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int y = __shfl_up_sync(kFull, incl, o);
+                if ((int)threadIdx.x >= o) incl += y;
+            }
+            int ex = incl - tot;
+            s_off[4 * threadIdx.x] = ex;
+            s_off[4 * threadIdx.x + 1] = ex + v0;
+            s_off[4 * threadIdx.x + 2] = ex + v0 + v1;
+            s_off[4 * threadIdx.x + 3] = ex + v0 + v1 + v2;
+        }
+        __syncthreads();
+        int* mylist = s_lst + s_off[d];
+        {
+            int c = 0;
+            for (int i = 0; i < ns; ++i)
+                if (sdev[i] == d) mylist[c++] = srow[i];
+        }
+        for (int c = 0; c < cnt; ++c) {
+            const double2* r2 = reinterpret_cast<const double2*>(a.V + (size_t)mylist[c] * kV);
+#pragma unroll
+            for (int k2 = 0; k2 < kV / 2; ++k2) {
+                const double2 t2 = __ldg(r2 + k2);
+                u[2 * k2] += t2.x;
+                u[2 * k2 + 1] += t2.y;
+            }
+        }
+        double P[8];
+#pragma unroll
+        for (int fg = 0; fg < 8; ++fg) {
+            double acc = 0.0;
+#pragma unroll
+            for (int q2 = 0; q2 < kG8; ++q2) acc = fma(a.head.H2[kG8 * fg + q2], relu_exact(u[kG8 * fg + q2]), acc);
+            P[fg] = acc;
+        }
+        double t[8];
+#pragma unroll
+        for (int b = 0; b < 8; ++b) t[b] = P[jd ^ b];   // t[b] = P_{j ^ b}
+        const double s3 = ((t[0] + t[4]) + (t[2] + t[6])) + ((t[1] + t[5]) + (t[3] + t[7]));
+        const double hc = a.head.hb2 + s3;
+        if (dev) {
+            const int ds = a.devdim[tau * a.D + d];
+            a.comp[tau * a.D + d] = ds > 0 ? hc : 0.0;   // reading R4
+        }
+    }
 }
 
 // ======================================================================
@@ -2642,6 +3195,20 @@ void carve(Carver& c, SearchBufs& b, OutStage& o, int Lout) {
         b.witem_step = c.take<int32_t>(items);
         b.witem_mask = c.take<unsigned long long>(items);
         b.witem_ready = c.take<int32_t>(items);
+        b.p2_cap = (int)items;
+        b.uf_cap = b.wgrp ? 2 * b.wgrp_cp_cap : 0;
+        b.rp_cap = (int)items;
+        b.p2_hdr = reinterpret_cast<P2Hdr*>(c.take<long long>((size_t)b.p2_cap * 4));
+        b.p2_work = c.take<uint32_t>((size_t)b.p2_cap * 64);
+        b.p2_A = c.take<double>((size_t)b.p2_cap * 128);
+        b.p2_room = c.take<long long>((size_t)b.p2_cap * 128);
+        b.p2_dsum = c.take<int32_t>((size_t)b.p2_cap * 128);
+        b.p2_ready = c.take<int32_t>((size_t)b.p2_cap);
+        b.p2_q = c.take<unsigned int>(8);
+        b.uf_buf = c.take<double>((size_t)b.uf_cap * kV * 128);
+        b.rp_tau = c.take<int32_t>((size_t)b.rp_cap);
+        b.rp_uf = c.take<int32_t>((size_t)b.rp_cap);
+        b.rp_psw = c.take<int32_t>((size_t)b.rp_cap);
     }
     b.ghist = c.take<int8_t>((size_t)b.gscratch_warps * b.M * b.Tpm);
     b.capdim = c.take<int32_t>((size_t)b.n_tasks * b.M);
@@ -2837,11 +3404,45 @@ ns_status launch_greedy(ns_ctx* ctx, const SearchBufs& b, const ns_tables* t, lo
         x.tau_base = g0 * b.M;
         const size_t n_items = (size_t)x.n_cp * b.M;
         x.n_items = (int)n_items;
+        x.p2_cap = b.p2_cap;
+        x.uf_cap = b.uf_cap;
+        x.rp_cap = b.rp_cap;
+        x.p2_hdr = b.p2_hdr;
+        x.p2_work = b.p2_work;
+        x.p2_A = b.p2_A;
+        x.p2_room = b.p2_room;
+        x.p2_dsum = b.p2_dsum;
+        x.p2_ready = b.p2_ready;
+        x.p2_q = b.p2_q;
+        x.uf_buf = b.uf_buf;
+        x.rp_tau = b.rp_tau;
+        x.rp_uf = b.rp_uf;
+        x.rp_psw = b.rp_psw;
         NS_CUDA(ctx, cudaMemsetAsync(b.wq, 0, sizeof(WgrpQueue), ctx->stream));
         NS_CUDA(ctx, cudaMemsetAsync(b.witem_ready, 0, n_items * sizeof(int32_t), ctx->stream));
+        NS_CUDA(ctx, cudaMemsetAsync(b.p2_q, 0, 8 * sizeof(unsigned int), ctx->stream));
+        NS_CUDA(ctx, cudaMemsetAsync(b.p2_ready, 0, (size_t)b.p2_cap * sizeof(int32_t), ctx->stream));
         const int ctas = (int)std::min<long long>((long long)n_items, (long long)ctx->sm_count * NS_WGRP_CTAS);
         prof_begin(ctx, PK_GREEDY);
         k_greedy_wgrp88<<<(unsigned)ctas, threads, 0, ctx->stream>>>(a2, x);
+#ifdef NS_SPLIT_PROF   // diagnosis: phase 2 and the replays timed as "other"
+        prof_end(ctx);
+        prof_begin(ctx, PK_OTHER);
+#endif
+        // phase 2 (one warp per group, 3 CTAs of 8 warps per SM) and the representatives' replays
+        k_greedy_p2<<<(unsigned)(ctx->sm_count * NS_P2_CTAS), 256, 0, ctx->stream>>>(a2, x);
+#ifdef NS_SPLIT_PROF   // diagnosis: the replays timed as "score"
+        prof_end(ctx);
+        prof_begin(ctx, PK_SCORE);
+#endif
+        {
+            const size_t rsm = (size_t)b.Tpm * (2 * sizeof(int) + 1) + 16;
+            if (rsm > 48 * 1024)
+                NS_CUDA(ctx, cudaFuncSetAttribute(k_greedy_replay, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rsm));
+            k_greedy_replay<<<(unsigned)(ctx->sm_count * 2), 128, rsm, ctx->stream>>>(a2, x);
+        }
+        NS_LAUNCHED(ctx);
+        NS_LAUNCHED(ctx);
         prof_end(ctx);
     } else {
         const int threads = ((b.D + 31) / 32) * 32;
