@@ -418,7 +418,7 @@ def main():
     g_ms, g_n = prof["greedy"]
     clocks = sampler.summary() if sampler else {}
     roof = greedy_roofline(clocks, scores_per_step * args.steps, g_ms, g_n, ms_local, stats,
-                           "k_greedy_wgrp88 (N4, D = 128 grouped greedy; level 0 k_greedy_wide88)")
+                           "N4 greedy, D = 128: k_greedy_wgrp88 (phase 1) + k_greedy_p2 (phase 2) + k_rp_sort + k_greedy_replay; level 0 k_greedy_wide88")
 
     # ---- CPU baseline: the oracle on a bounded sample (rank 0, N=1 only)
     cpu = None
@@ -501,13 +501,25 @@ def greedy_roofline(clocks, W, g_ms, g_n, ms_region, stats, kernel):
         except Exception:
             pass
     if stats and stats.get("scores_computed"):
-        ex = stats["scores_computed"] * flops_per_score / (g_ms * 1e-3) / 1e12
+        # executed FP64 work: scores with feature arithmetic (256 flop), scores in
+        # the closed linear form hb2 + (A_d + B_t) (2 flop), phase-2 replays
+        # (64 adds per replayed row, 2 x 64 + 8 flop per device head)
+        lin = stats.get("scores_linear", 0)
+        full = stats["scores_computed"] - lin
+        rp_flops = 64 * stats.get("replay_rows", 0) + 136 * 128 * stats.get("replay_reps", 0)
+        ex_flops = full * flops_per_score + 2 * lin + rp_flops
+        ex = ex_flops / (g_ms * 1e-3) / 1e12
         roof["scores_computed"] = stats["scores_computed"]
+        roof["scores_linear"] = lin
+        roof["replay_rows"] = stats.get("replay_rows", 0)
+        roof["replay_reps"] = stats.get("replay_reps", 0)
         roof["executed_share_of_W"] = stats["scores_computed"] / max(W, 1)
+        roof["full_score_share_of_W"] = full / max(W, 1)
         roof["executed_achieved"] = ex
         roof["executed_frac"] = ex / peak
-        roof["executed_basis"] = ("scores the greedy kernels computed (ns_last_stats.scores_computed; identical "
-                                  "trajectories share scores) x 256 flop / greedy time")
+        roof["executed_basis"] = ("FP64 flops the greedy kernels executed: scores with feature arithmetic x 256 + "
+                                  "closed-linear-form scores x 2 + replay (64 per row, 136 per device head); "
+                                  "identical trajectories share scores; / greedy time")
     return roof
 
 

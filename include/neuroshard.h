@@ -81,11 +81,18 @@ ns_status ns_profile(ns_ctx* ctx, int32_t enable);
  * (the grouped kernels evaluate a score once for all identical trajectories,
  * so this is <= the algorithmic count W the plans report); trajectories =
  * greedy trajectories launched (column plans x grid points); group_steps =
- * steps run by k_greedy_wgrp88 (D > 16, grouped). */
+ * steps run by k_greedy_wgrp88 and k_greedy_p2 (D > 16, grouped);
+ * scores_linear = the part of scores_computed taken in the closed linear form
+ * hb2 + (A_d + B_t) (2 flops instead of 256; DESIGN.md "linear-regime
+ * certificate"); replay_rows / replay_reps = rows added and representatives
+ * rebuilt by k_greedy_replay (phase 2). */
 typedef struct {
     uint64_t scores_computed;
     uint64_t trajectories;
     uint64_t group_steps;   /* steps the large-D grouped greedy ran (one per group and table) */
+    uint64_t scores_linear;
+    uint64_t replay_rows;
+    uint64_t replay_reps;
 } ns_stats;
 ns_status ns_stats_query(ns_ctx* ctx, ns_stats* out);
 ns_status ns_profile_query(ns_ctx* ctx, const char* kernel, double* total_ms, uint64_t* launches);

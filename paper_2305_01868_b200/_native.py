@@ -51,7 +51,8 @@ class ns_host_comm(C.Structure):
 
 
 class ns_stats(C.Structure):
-    _fields_ = [("scores_computed", C.c_uint64), ("trajectories", C.c_uint64), ("group_steps", C.c_uint64)]
+    _fields_ = [("scores_computed", C.c_uint64), ("trajectories", C.c_uint64), ("group_steps", C.c_uint64),
+                ("scores_linear", C.c_uint64), ("replay_rows", C.c_uint64), ("replay_reps", C.c_uint64)]
 
 
 class ns_bag_table(C.Structure):
@@ -202,7 +203,8 @@ def ns_last_stats(ctx: int) -> dict:
     st = ns_stats()
     _check(ctx, LIB.ns_stats_query(ctx, C.byref(st)))
     return {"scores_computed": int(st.scores_computed), "trajectories": int(st.trajectories),
-            "group_steps": int(st.group_steps)}
+            "group_steps": int(st.group_steps), "scores_linear": int(st.scores_linear),
+            "replay_rows": int(st.replay_rows), "replay_reps": int(st.replay_reps)}
 
 
 PROFILE_KINDS = ("precompute", "validate", "order", "expand", "greedy", "finalize", "select", "score", "other")

@@ -85,6 +85,7 @@ struct SearchBufs {
     int32_t* rp_tau;     // [rp_cap] local tau of a representative to replay
     int32_t* rp_uf;      // [rp_cap]
     int32_t* rp_psw;     // [rp_cap] first step whose placement the frozen u lacks
+    int32_t* rp_ord;     // [rp_cap] replay order: entries bucketed by column plan (k_rp_sort)
     double* gscratch;    // grouped greedy group states
     int8_t* ghist;       // grouped greedy group histories [gscratch_warps][M][Tpm]
     int gscratch_warps;
@@ -1423,6 +1424,7 @@ struct WgrpArgs {
     int32_t* rp_tau;
     int32_t* rp_uf;
     int32_t* rp_psw;
+    int32_t* rp_ord;
 };
 
 struct P2Hdr {   // 32 bytes
@@ -1861,6 +1863,7 @@ __global__ void __launch_bounds__(128, NS_WGRP_CTAS) k_greedy_wgrp88(const Greed
     // coalesced per thread index
     const size_t snap_doubles = (size_t)nth * (kV + 4);
     unsigned long long computed = 0, steps = 0;   // executed scores / group-steps (ns_stats)
+    unsigned lin_sc = 0;                          // this thread's scores taken in the closed linear form
 #ifdef NS_WGRP_TIMING   // debug build: clock64 per step phase of thread 0, printed by CTAs 0-3
     unsigned long long tph[7] = {0, 0, 0, 0, 0, 0, 0}, nlin = 0, town = 0, nown = 0;
     long long tlast = clock64();
@@ -2107,6 +2110,7 @@ __global__ void __launch_bounds__(128, NS_WGRP_CTAS) k_greedy_wgrp88(const Greed
             // with cap_m < x_d <= cap_max, counted only for the members whose
             // cap is below the largest feasible x (xmax)
             cf += (f) ? 1u : 0u;
+            lin_sc += (f && wlin) ? 1u : 0u;
             if (xmax > (unsigned)cmin) {
                 for (unsigned long long mm = mask; mm; mm &= mm - 1) {
                     const int m = __ffsll((long long)mm) - 1;
@@ -2371,6 +2375,8 @@ __global__ void __launch_bounds__(128, NS_WGRP_CTAS) k_greedy_wgrp88(const Greed
 #undef NS_TMARK
     if (threadIdx.x == 0 && computed) atomicAdd(a.computed, computed);
     if (threadIdx.x == 0 && steps) atomicAdd(a.computed + 1, steps);
+    const unsigned lsum = __reduce_add_sync(kFull, lin_sc);
+    if ((threadIdx.x & 31) == 0 && lsum) atomicAdd(a.computed + 2, (unsigned long long)lsum);
 }
 
 
@@ -2481,7 +2487,7 @@ __global__ void __launch_bounds__(256, NS_P2_CTAS) k_greedy_p2(const GreedyArgs 
             const bool v = dd < D;
             A4[j] = v ? __ldcg(x.p2_A + (size_t)item * 128 + dd) : 0.0;
             ds4[j] = v ? __ldcg(x.p2_dsum + (size_t)item * 128 + dd) : 0;
-            rm4[j] = v ? __ldcg(x.p2_room + (size_t)item * 128 + dd) : 0;
+            rm4[j] = v ? __ldcg(x.p2_room + (size_t)item * 128 + dd) : -1;   // no device: no room
         }
         int cmin = p2_cap_of(cap0, cap1, __ffsll((long long)mask) - 1);
         int cmax = p2_cap_of(cap0, cap1, 63 - __clzll((long long)mask));
@@ -2506,47 +2512,62 @@ __global__ void __launch_bounds__(256, NS_P2_CTAS) k_greedy_p2(const GreedyArgs 
         int4 nm = ld_m(c0 + 32 + lane);
         double nB = __ldg(a.Brow + nr0);
         int nr = ld_r(c0 + 64 + lane);
+        // the group's choices of the chunk's steps: lane l keeps step c + l's and
+        // writes it when the chunk ends (one store per 32 steps); the members'
+        // work gains |F_max| per step, summed in csum until a split or the end
+        int mybd = -1;
+        int8_t* hrow = a.assign + (size_t)(tau0 + rep) * a.Tpm;
+        unsigned csum = 0;
+        auto flush_hist = [&]() {
+            if (mybd >= 0) hrow[cm.y] = (int8_t)mybd;
+            mybd = -1;
+            __syncwarp();
+        };
+        auto flush_work = [&]() {
+            if (lane < M && ((mask >> lane) & 1ULL)) wk0 += csum;
+            if (lane + 32 < M && ((mask >> (lane + 32)) & 1ULL)) wk1 += csum;
+            csum = 0;
+        };
 #pragma unroll 1
         for (int p = h.p; p < Tp; ++p) {
             const int k32 = (p - c0) & 31;
             if (k32 == 0 && p > c0) {   // next chunk
+                flush_hist();
                 cm = nm;
                 cB = nB;
                 nm = ld_m(p + 32 + lane);
                 nB = __ldg(a.Brow + nr);
                 nr = ld_r(p + 64 + lane);
             }
-            int4 mt;
-            mt.x = __shfl_sync(kFull, cm.x, k32);
-            mt.y = __shfl_sync(kFull, cm.y, k32);
-            mt.z = __shfl_sync(kFull, cm.z, k32);
-            mt.w = __shfl_sync(kFull, cm.w, k32);
+            const int dt = __shfl_sync(kFull, cm.x, k32);
+            const unsigned btl = (unsigned)__shfl_sync(kFull, cm.z, k32), bth = (unsigned)__shfl_sync(kFull, cm.w, k32);
             const double Bt = __shfl_sync(kFull, cB, k32);
-            const int dt = mt.x, li = mt.y;
 #ifdef NS_WGRP_TIMING
             const long long tk0 = clock64();
 #endif
-            const long long bt = (long long)(((unsigned long long)(unsigned)mt.w << 32) | (unsigned)mt.z);
+            const long long bt = (long long)(((unsigned long long)bth << 32) | btl);
+            // scores hb2 + (A_d + B_t) of the lane's 4 devices; devices >= D have room -1
             int xj[4];
             bool fj[4];
-            unsigned long long best = ~0ULL;
+            double bs = CUDART_INF;
             int bj = 0, cfl = 0;
             unsigned xm = 0;
 #pragma unroll
             for (int j = 0; j < 4; ++j) {
                 xj[j] = ds4[j] + dt;
-                fj[j] = lane + 32 * j < D && bt <= rm4[j] && xj[j] <= cmax;
-                const long long sb = __double_as_longlong(a.head.hb2 + (A4[j] + Bt) + 0.0);
-                const unsigned long long kj =
-                    fj[j] ? (unsigned long long)(sb ^ ((sb >> 63) | (long long)0x8000000000000000ULL)) : ~0ULL;
-                if (kj < best) {   // strict: the lane's lowest device keeps ties
-                    best = kj;
+                fj[j] = (bt <= rm4[j]) & (xj[j] <= cmax);
+                const double s = a.head.hb2 + (A4[j] + Bt);
+                if (fj[j] & (s < bs)) {   // strict: the lane's lowest device keeps ties (-0 == +0)
+                    bs = s;
                     bj = j;
                 }
-                if (fj[j]) {
-                    xm = max(xm, (unsigned)xj[j]);
-                    ++cfl;
-                }
+                xm = fj[j] ? max(xm, (unsigned)xj[j]) : xm;
+                cfl += fj[j] ? 1 : 0;
+            }
+            unsigned long long best = ~0ULL;
+            if (bs < CUDART_INF) {   // order-preserving key of the lane's best (+0.0: -0 and +0 alike)
+                const long long sb = __double_as_longlong(bs + 0.0);
+                best = (unsigned long long)(sb ^ ((sb >> 63) | (long long)0x8000000000000000ULL));
             }
             const unsigned khi = (unsigned)(best >> 32), klo = (unsigned)best;
             const unsigned mh = __reduce_min_sync(kFull, khi);
@@ -2556,26 +2577,26 @@ __global__ void __launch_bounds__(256, NS_P2_CTAS) k_greedy_p2(const GreedyArgs 
                 __reduce_min_sync(kFull, (khi == mh && klo == ml) ? (unsigned)(32 * bj + lane) : 0xFFFFFFFFu);
             const unsigned xmax = __reduce_max_sync(kFull, xm);
             const unsigned cfc = __reduce_add_sync(kFull, (unsigned)cfl);
-            int bd = none ? 0 : (int)dmin;
-            const int xb = bj == 0 ? xj[0] : bj == 1 ? xj[1] : bj == 2 ? xj[2] : xj[3];
-            const int xstar = __shfl_sync(kFull, xb, bd & 31);
+            const int bd = none ? 0 : (int)dmin;
+            const int jb = bd >> 5, ob = bd & 31;   // the winner's slot and owner lane (warp-uniform)
+            const int dsb = jb == 0 ? ds4[0] : jb == 1 ? ds4[1] : jb == 2 ? ds4[2] : ds4[3];
+            const int xstar = __shfl_sync(kFull, dsb, ob) + dt;
             computed += cfc;
+            csum += cfc;
             ++nsteps;
 #ifdef NS_WGRP_TIMING
             const long long tk1 = clock64();
             t_key += (unsigned long long)(tk1 - tk0);
 #endif
-            // ---- work W per member (O12): |F_max| minus the devices with cap_m < x_d
-            if (lane < M && ((mask >> lane) & 1ULL)) wk0 += cfc;
-            if (lane + 32 < M && ((mask >> (lane + 32)) & 1ULL)) wk1 += cfc;
+            // ---- work W per member (O12): |F_max| (csum) minus the devices with cap_m < x_d
             if (xmax > (unsigned)cmin) {
                 for (unsigned long long mm = mask; mm; mm &= mm - 1) {
                     const int m = __ffsll((long long)mm) - 1;
-                    const int cm = p2_cap_of(cap0, cap1, m);
-                    if ((unsigned)cm >= xmax) break;   // caps non-decreasing in m
+                    const int cmm = p2_cap_of(cap0, cap1, m);
+                    if ((unsigned)cmm >= xmax) break;   // caps non-decreasing in m
                     int c = 0;
 #pragma unroll
-                    for (int j = 0; j < 4; ++j) c += (fj[j] && xj[j] > cm) ? 1 : 0;
+                    for (int j = 0; j < 4; ++j) c += (fj[j] & (xj[j] > cmm)) ? 1 : 0;
                     const unsigned cnt = __reduce_add_sync(kFull, (unsigned)c);
                     if (lane == (m & 31)) {
                         if (m < 32) wk0 -= cnt;
@@ -2592,6 +2613,9 @@ __global__ void __launch_bounds__(256, NS_P2_CTAS) k_greedy_p2(const GreedyArgs 
             }
             if (xstar > cmin) {
                 // ---- slow path: members split by the caps that admit the winners
+                flush_work();
+                flush_hist();
+                const int li = __shfl_sync(kFull, cm.y, k32);
                 unsigned long long take0 = 0;
                 for (unsigned long long mm = mask; mm; mm &= mm - 1) {
                     const int m = __ffsll((long long)mm) - 1;
@@ -2674,19 +2698,23 @@ __global__ void __launch_bounds__(256, NS_P2_CTAS) k_greedy_p2(const GreedyArgs 
                 if (nrep != rep) {
                     copy_row(tau0 + rep, tau0 + nrep, Tp);
                     rep = nrep;
+                    hrow = a.assign + (size_t)(tau0 + rep) * a.Tpm;
                 }
             }
-            // ---- the group's choice
-#pragma unroll
-            for (int j = 0; j < 4; ++j)
-                if (lane + 32 * j == bd) {
-                    A4[j] += Bt;
-                    ds4[j] += dt;
-                    rm4[j] -= bt;
+            // ---- the group's choice: the owner lane updates its slot jb; this
+            // lane records it if step p is its slot of the chunk
+            if (lane == ob) {
+                switch (jb) {
+                    case 0: A4[0] += Bt; ds4[0] += dt; rm4[0] -= bt; break;
+                    case 1: A4[1] += Bt; ds4[1] += dt; rm4[1] -= bt; break;
+                    case 2: A4[2] += Bt; ds4[2] += dt; rm4[2] -= bt; break;
+                    default: A4[3] += Bt; ds4[3] += dt; rm4[3] -= bt; break;
                 }
-            if (lane == 0) a.assign[(size_t)(tau0 + rep) * a.Tpm + li] = (int8_t)bd;
-            __syncwarp();
+            }
+            mybd = lane == k32 ? bd : mybd;
         }
+        flush_hist();
+        flush_work();
 #ifdef NS_WGRP_TIMING
         tc0 = clock64();
         t_loop += (unsigned long long)(tc0 - tc1);
@@ -2726,30 +2754,111 @@ __global__ void __launch_bounds__(256, NS_P2_CTAS) k_greedy_p2(const GreedyArgs 
                nsteps ? (double)t_key / nsteps : 0.0, nsteps ? (double)t_w / nsteps : 0.0, t_claim, n_init);
 #endif
     if (lane == 0 && computed) atomicAdd(a.computed, computed);
+    if (lane == 0 && computed) atomicAdd(a.computed + 2, computed);   // every phase-2 score is linear
     if (lane == 0 && nsteps) atomicAdd(a.computed + 1, nsteps);
+}
+
+// Replay order: the queue's entries bucketed by column plan (counting sort,
+// one CTA), so the CTAs replaying at the same time read the same tasks' V rows
+// and those stay in L2.  The order within a bucket is immaterial: every
+// representative is replayed independently.
+constexpr int kRpBuckets = 8192;
+__global__ void __launch_bounds__(1024) k_rp_sort(const GreedyArgs a, const WgrpArgs x) {
+    __shared__ int cnt[kRpBuckets];
+    const unsigned n = __ldcg(x.p2_q + 5);
+    const long long ncp = x.n_cp > 0 ? x.n_cp : 1;
+    for (int i = threadIdx.x; i < kRpBuckets; i += blockDim.x) cnt[i] = 0;
+    __syncthreads();
+    auto bucket = [&](unsigned e) {
+        const long long g = x.rp_tau[e] / a.M;
+        return (int)(ncp <= kRpBuckets ? g : g * kRpBuckets / ncp);
+    };
+    for (unsigned e = threadIdx.x; e < n; e += blockDim.x) atomicAdd(&cnt[bucket(e)], 1);
+    __syncthreads();
+    // exclusive scan: each thread owns kRpBuckets / 1024 consecutive buckets
+    constexpr int per = kRpBuckets / 1024;
+    int loc[per], tot = 0;
+#pragma unroll
+    for (int k = 0; k < per; ++k) {
+        loc[k] = cnt[threadIdx.x * per + k];
+        tot += loc[k];
+    }
+    __shared__ int wsum[32];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    int incl = tot;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(kFull, incl, o);
+        if (lane >= o) incl += y;
+    }
+    if (lane == 31) wsum[wid] = incl;
+    __syncthreads();
+    if (wid == 0) {
+        int v = wsum[lane], iv = v;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int y = __shfl_up_sync(kFull, iv, o);
+            if (lane >= o) iv += y;
+        }
+        wsum[lane] = iv - v;
+    }
+    __syncthreads();
+    int run = wsum[wid] + incl - tot;
+#pragma unroll
+    for (int k = 0; k < per; ++k) {
+        cnt[threadIdx.x * per + k] = run;
+        run += loc[k];
+    }
+    __syncthreads();
+    for (unsigned e = threadIdx.x; e < n; e += blockDim.x) x.rp_ord[atomicAdd(&cnt[bucket(e)], 1)] = (int)e;
 }
 
 // The representatives of phase-2 groups: u = the frozen u of the hand-off +
 // every later placement replayed in step order (the same additions, in the
 // same order, the per-trajectory kernel makes), then the head in the order
-// of k_greedy_wide88 / k_greedy_wgrp88.  One CTA per representative, ONE
-// thread per device holding all 64 features: the steps' (device, row) go to
-// shared memory, each thread scans them for its own device (a device takes
-// ~T' / D rows) and adds those rows in step order; the head is the 8 x 8
-// order written out -- per feature group fg an FMA chain over its 8 features
-// (head88), then the tree bfly88 builds for device index j = d & 7:
-// ((P_j + P_j^4) + (P_j^2 + P_j^6)) + ((P_j^1 + P_j^5) + (P_j^3 + P_j^7)).
+// of k_greedy_wide88 / k_greedy_wgrp88.  One CTA (4 warps) per
+// representative, its u for all devices in shared memory, device-major with
+// a 16-byte aligned row stride (kUS):
+//  1. the steps' (row, device) go to shared memory, the frozen u is copied
+//     from the 8 x 8 layout (coalesced reads, conflict-free writes);
+//  2. warp w owns the devices d = w (mod 4) and lists its steps in order
+//     (ballots over the device bytes); it adds each row to u_d with the 32
+//     lanes on 2 features each (one coalesced 512-byte row per instruction),
+//     the next 8 rows' loads in flight while the current 8 are added -- a
+//     device's rows stay in step order, so every feature sums in the same
+//     order as the sequential greedy;
+//  3. one thread per device: the head written out in the 8 x 8 order -- per
+//     feature group fg an FMA chain over its 8 features (head88), then the
+//     tree bfly88 builds for device index j = d & 7:
+//     ((P_j + P_j^4) + (P_j^2 + P_j^6)) + ((P_j^1 + P_j^5) + (P_j^3 + P_j^7)).
+constexpr int kUS = kV + 2;
+#ifndef NS_RP_BATCH
+#define NS_RP_BATCH 16
+#endif
+constexpr int kRpBatch = NS_RP_BATCH;
+// dynamic shared memory of k_greedy_replay; phase 2 is off (no hand-offs)
+// when it exceeds the opt-in maximum (Tpm above ~12k column tables)
+inline size_t replay_smem(int Tpm) {
+    return (size_t)128 * kUS * sizeof(double) + (size_t)(3 * Tpm + 4) * sizeof(int) + (size_t)Tpm + 32;
+}
+constexpr size_t kSmemOptin = 232448;
 __global__ void __launch_bounds__(128, 2) k_greedy_replay(const GreedyArgs a, const WgrpArgs x) {
-    extern __shared__ __align__(16) int s_rp[];   // [Tpm] rows, [Tpm] per-device lists, [Tpm] devices (int8)
-    __shared__ int s_cnt[128], s_off[128];
-    const int d = threadIdx.x;
-    const bool dev = d < a.D;
+    extern __shared__ __align__(16) double s_u[];   // [128][kUS] u, then [Tpm] rows, [4][Tpm] step lists, [Tpm + 32] devices
+    const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
     const unsigned n = __ldcg(x.p2_q + 5);
-    int* srow = s_rp;
-    int* s_lst = s_rp + a.Tpm;
-    int8_t* sdev = reinterpret_cast<int8_t*>(s_rp + 2 * a.Tpm);
-    const int wgi = d >> 5, dgi = (d >> 3) & 3, jd = d & 7;   // this device's place in the 8 x 8 layout
-    for (unsigned e = blockIdx.x; e < n; e += gridDim.x) {
+    unsigned long long rows = 0, reps = 0;   // ns_stats: rows replayed, representatives
+    int* srow = reinterpret_cast<int*>(s_u + 128 * kUS);
+    uint16_t* slst = reinterpret_cast<uint16_t*>(srow + a.Tpm) + (size_t)w * a.Tpm;
+    uint8_t* sdev = reinterpret_cast<uint8_t*>(srow + a.Tpm + 2 * a.Tpm + 4);   // after 4 uint16 lists (+ pad)
+#ifdef NS_WGRP_TIMING
+    long long tph[6] = {0, 0, 0, 0, 0, 0}, nsum = 0, csum = 0;
+    long long c0 = clock64(), c1;
+#define RP_T(k) do { c1 = clock64(); tph[k] += c1 - c0; c0 = c1; } while (0)
+#else
+#define RP_T(k) do { } while (0)
+#endif
+    for (unsigned e0 = blockIdx.x; e0 < n; e0 += gridDim.x) {
+        const int e = __ldcg(x.rp_ord + e0);
         const long long tau = x.rp_tau[e];
         const int uf = x.rp_uf[e], p_sw = x.rp_psw[e];
         const int g = (int)(tau / a.M);
@@ -2758,76 +2867,133 @@ __global__ void __launch_bounds__(128, 2) k_greedy_replay(const GreedyArgs a, co
         const int8_t* hist = a.assign + (size_t)tau * a.Tpm;
         const int32_t* orow = a.ord_row + (size_t)g * a.Tpm;
         const int4* ometa = a.ord_meta + (size_t)g * a.Tpm;
-        __syncthreads();   // the previous representative's steps are consumed
-        for (int i = threadIdx.x; i < ns; i += blockDim.x) {
-            srow[i] = __ldg(orow + p_sw + i);
-            sdev[i] = __ldcg(hist + __ldg(ometa + p_sw + i).y);
-        }
-        __syncthreads();
-        // frozen u of this device: 8 x 8 layout, lane (wgi, dgi, fg) held features 8 fg .. of device jd
-        const double* up = x.uf_buf + (size_t)uf * kV * 128;
-        double u[kV];
+        __syncthreads();   // the previous representative's head has read s_u
+        // 1. steps and frozen u
+        for (int i0 = tid; i0 < ns; i0 += 4 * blockDim.x) {
+            int r[4], m[4];
 #pragma unroll
-        for (int fg = 0; fg < 8; ++fg)
-#pragma unroll
-            for (int q2 = 0; q2 < kG8; ++q2)
-                u[kG8 * fg + q2] = __ldcg(up + (size_t)(jd * kG8 + q2) * 128 + (32 * wgi + 8 * dgi + fg));
-        // this device's rows in step order: one pass counting, one pass
-        // copying the row indices into this thread's region of the list,
-        // then the additions with every thread of the warp active at once
-        int cnt = 0;
-        for (int i = 0; i < ns; ++i) cnt += sdev[i] == d ? 1 : 0;
-        s_cnt[d] = cnt;
-        __syncthreads();
-        if (threadIdx.x < 32) {   // exclusive prefix of the counts
-            int v0 = s_cnt[4 * threadIdx.x], v1 = s_cnt[4 * threadIdx.x + 1], v2 = s_cnt[4 * threadIdx.x + 2],
-                v3 = s_cnt[4 * threadIdx.x + 3];
-            int tot = v0 + v1 + v2 + v3, incl = tot;
-#pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                const int y = __shfl_up_sync(kFull, incl, o);
-                if ((int)threadIdx.x >= o) incl += y;
+            for (int k = 0; k < 4; ++k) {
+                const int i = i0 + k * blockDim.x;
+                r[k] = i < ns ? __ldg(orow + p_sw + i) : 0;
+                m[k] = i < ns ? __ldg(ometa + p_sw + i).y : -1;
             }
-            int ex = incl - tot;
-            s_off[4 * threadIdx.x] = ex;
-            s_off[4 * threadIdx.x + 1] = ex + v0;
-            s_off[4 * threadIdx.x + 2] = ex + v0 + v1;
-            s_off[4 * threadIdx.x + 3] = ex + v0 + v1 + v2;
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                const int i = i0 + k * blockDim.x;
+                if (i < ns) {
+                    srow[i] = r[k];
+                    sdev[i] = (uint8_t)__ldcg(hist + m[k]);
+                }
+            }
         }
-        __syncthreads();
-        int* mylist = s_lst + s_off[d];
         {
-            int c = 0;
-            for (int i = 0; i < ns; ++i)
-                if (sdev[i] == d) mylist[c++] = srow[i];
-        }
-        for (int c = 0; c < cnt; ++c) {
-            const double2* r2 = reinterpret_cast<const double2*>(a.V + (size_t)mylist[c] * kV);
+            // uf_buf element (j = jd * 8 + q, c = 32 wgi + 8 dgi + fg) is feature 8 fg + q of
+            // device 32 wgi + 8 dgi + jd; a warp instruction covers one device's 32 features
+            const double* up = x.uf_buf + (size_t)uf * kV * 128;
+            const int q = lane & 7, fgl = lane >> 3;
+            for (int it0 = w; it0 < 256; it0 += 4 * 32) {   // 32 loads in flight per thread
+                double vv[32];
 #pragma unroll
-            for (int k2 = 0; k2 < kV / 2; ++k2) {
-                const double2 t2 = __ldg(r2 + k2);
-                u[2 * k2] += t2.x;
-                u[2 * k2 + 1] += t2.y;
+                for (int k = 0; k < 32; ++k) {
+                    const int it = it0 + 4 * k, d = it >> 1, fg = 4 * (it & 1) + fgl;
+                    vv[k] = __ldcg(up + (size_t)((d & 7) * 8 + q) * 128 + (d & ~7) + fg);
+                }
+#pragma unroll
+                for (int k = 0; k < 32; ++k) {
+                    const int it = it0 + 4 * k, d = it >> 1, fg = 4 * (it & 1) + fgl;
+                    s_u[d * kUS + 8 * fg + q] = vv[k];
+                }
             }
         }
-        double P[8];
-#pragma unroll
-        for (int fg = 0; fg < 8; ++fg) {
-            double acc = 0.0;
-#pragma unroll
-            for (int q2 = 0; q2 < kG8; ++q2) acc = fma(a.head.H2[kG8 * fg + q2], relu_exact(u[kG8 * fg + q2]), acc);
-            P[fg] = acc;
+        __syncthreads();
+        RP_T(0);
+        // 2. this warp's steps (devices d = w mod 4) in step order
+        int cnt = 0;
+        for (int i0 = 0; i0 < ns; i0 += 32) {
+            const int i = i0 + lane;
+            const bool mine = i < ns && (sdev[i] & 3) == w;
+            const unsigned bm = __ballot_sync(kFull, mine);
+            if (mine) slst[cnt + __popc(bm & ((1u << lane) - 1u))] = (uint16_t)i;
+            cnt += __popc(bm);
         }
-        double t[8];
+        __syncwarp();
+        RP_T(1);
+        {
+            double2 cur[kRpBatch];
 #pragma unroll
-        for (int b = 0; b < 8; ++b) t[b] = P[jd ^ b];   // t[b] = P_{j ^ b}
-        const double s3 = ((t[0] + t[4]) + (t[2] + t[6])) + ((t[1] + t[5]) + (t[3] + t[7]));
-        const double hc = a.head.hb2 + s3;
-        if (dev) {
+            for (int k = 0; k < kRpBatch; ++k)
+                if (k < cnt) cur[k] = __ldg(reinterpret_cast<const double2*>(a.V + (size_t)srow[slst[k]] * kV) + lane);
+            for (int b0 = 0; b0 < cnt; b0 += kRpBatch) {
+                double2 nxt[kRpBatch];
+#pragma unroll
+                for (int k = 0; k < kRpBatch; ++k)
+                    if (b0 + kRpBatch + k < cnt)
+                        nxt[k] = __ldg(reinterpret_cast<const double2*>(a.V + (size_t)srow[slst[b0 + kRpBatch + k]] * kV) +
+                                       lane);
+#pragma unroll
+                for (int k = 0; k < kRpBatch; ++k)
+                    if (b0 + k < cnt) {
+                        double2* p = reinterpret_cast<double2*>(s_u + sdev[slst[b0 + k]] * kUS) + lane;
+                        double2 t = *p;
+                        t.x += cur[k].x;
+                        t.y += cur[k].y;
+                        *p = t;
+                    }
+#pragma unroll
+                for (int k = 0; k < kRpBatch; ++k) cur[k] = nxt[k];
+            }
+        }
+#ifdef NS_WGRP_TIMING
+        nsum += ns;
+        csum += cnt;
+#endif
+        __syncthreads();
+        RP_T(3);
+        // 3. head, one thread per device
+        const int d = tid;
+        if (d < a.D) {
+            const double* ud = s_u + d * kUS;
+            double P[8];
+#pragma unroll
+            for (int fg = 0; fg < 8; ++fg) {
+                double acc = 0.0;
+#pragma unroll
+                for (int q2 = 0; q2 < kG8; ++q2) acc = fma(a.head.H2[kG8 * fg + q2], relu_exact(ud[kG8 * fg + q2]), acc);
+                P[fg] = acc;
+            }
+            const int jd = d & 7;
+            double t[8];   // t[b] = P_{j ^ b}: three rounds of register swaps (no local memory)
+#pragma unroll
+            for (int b = 0; b < 8; ++b) t[b] = P[b];
+#pragma unroll
+            for (int bit = 1; bit < 8; bit <<= 1) {
+                const bool sw = (jd & bit) != 0;
+#pragma unroll
+                for (int b = 0; b < 8; ++b)
+                    if (!(b & bit)) {
+                        const double lo = t[b], hi = t[b | bit];
+                        t[b] = sw ? hi : lo;
+                        t[b | bit] = sw ? lo : hi;
+                    }
+            }
+            const double s3 = ((t[0] + t[4]) + (t[2] + t[6])) + ((t[1] + t[5]) + (t[3] + t[7]));
             const int ds = a.devdim[tau * a.D + d];
-            a.comp[tau * a.D + d] = ds > 0 ? hc : 0.0;   // reading R4
+            a.comp[tau * a.D + d] = ds > 0 ? a.head.hb2 + s3 : 0.0;   // reading R4
         }
+        RP_T(4);
+        rows += (unsigned long long)ns;
+        ++reps;
     }
+    if (tid == 0 && reps) {
+        atomicAdd(a.computed + 3, rows);
+        atomicAdd(a.computed + 4, reps);
+    }
+#ifdef NS_WGRP_TIMING
+    if (blockIdx.x < 4 && threadIdx.x == 0)
+        printf("replay cta %d n=%u uf=%u: fill %lld lists %lld scan %lld adds %lld head %lld | ns %lld cnt %lld\n", blockIdx.x, n,
+               __ldcg(x.p2_q + 4), tph[0], tph[1], tph[2], tph[3], tph[4], nsum, csum);
+#endif
+#undef RP_T
 }
 
 // ======================================================================
@@ -3196,7 +3362,7 @@ void carve(Carver& c, SearchBufs& b, OutStage& o, int Lout) {
         b.witem_mask = c.take<unsigned long long>(items);
         b.witem_ready = c.take<int32_t>(items);
         b.p2_cap = (int)items;
-        b.uf_cap = b.wgrp ? 2 * b.wgrp_cp_cap : 0;
+        b.uf_cap = b.wgrp && replay_smem(b.Tpm) <= kSmemOptin ? 2 * b.wgrp_cp_cap : 0;
         b.rp_cap = (int)items;
         b.p2_hdr = reinterpret_cast<P2Hdr*>(c.take<long long>((size_t)b.p2_cap * 4));
         b.p2_work = c.take<uint32_t>((size_t)b.p2_cap * 64);
@@ -3209,6 +3375,7 @@ void carve(Carver& c, SearchBufs& b, OutStage& o, int Lout) {
         b.rp_tau = c.take<int32_t>((size_t)b.rp_cap);
         b.rp_uf = c.take<int32_t>((size_t)b.rp_cap);
         b.rp_psw = c.take<int32_t>((size_t)b.rp_cap);
+        b.rp_ord = c.take<int32_t>((size_t)b.rp_cap);
     }
     b.ghist = c.take<int8_t>((size_t)b.gscratch_warps * b.M * b.Tpm);
     b.capdim = c.take<int32_t>((size_t)b.n_tasks * b.M);
@@ -3418,6 +3585,7 @@ ns_status launch_greedy(ns_ctx* ctx, const SearchBufs& b, const ns_tables* t, lo
         x.rp_tau = b.rp_tau;
         x.rp_uf = b.rp_uf;
         x.rp_psw = b.rp_psw;
+        x.rp_ord = b.rp_ord;
         NS_CUDA(ctx, cudaMemsetAsync(b.wq, 0, sizeof(WgrpQueue), ctx->stream));
         NS_CUDA(ctx, cudaMemsetAsync(b.witem_ready, 0, n_items * sizeof(int32_t), ctx->stream));
         NS_CUDA(ctx, cudaMemsetAsync(b.p2_q, 0, 8 * sizeof(unsigned int), ctx->stream));
@@ -3436,11 +3604,13 @@ ns_status launch_greedy(ns_ctx* ctx, const SearchBufs& b, const ns_tables* t, lo
         prof_begin(ctx, PK_SCORE);
 #endif
         {
-            const size_t rsm = (size_t)b.Tpm * (2 * sizeof(int) + 1) + 16;
+            const size_t rsm = replay_smem(b.Tpm);
             if (rsm > 48 * 1024)
                 NS_CUDA(ctx, cudaFuncSetAttribute(k_greedy_replay, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rsm));
+            k_rp_sort<<<1, 1024, 0, ctx->stream>>>(a2, x);
             k_greedy_replay<<<(unsigned)(ctx->sm_count * 2), 128, rsm, ctx->stream>>>(a2, x);
         }
+        NS_LAUNCHED(ctx);   // p2, sort, replay (the caller counts wgrp88)
         NS_LAUNCHED(ctx);
         NS_LAUNCHED(ctx);
         prof_end(ctx);

@@ -349,6 +349,9 @@ ns_status ns_stats_query(ns_ctx* ctx, ns_stats* out) {
     out->scores_computed = h[0];
     out->trajectories = ctx->trajectories;
     out->group_steps = h[1];
+    out->scores_linear = h[2];
+    out->replay_rows = h[3];
+    out->replay_reps = h[4];
     return NS_OK;
 }
 

@@ -32,7 +32,7 @@ constexpr int kDepth = 6;    // variant slots per table: dim, dim/2, ..., dim/32
 // needs more than kDepth variant rows; larger dims are rejected at validation.
 constexpr int kMaxDim = 4 << (kDepth - 1);
 constexpr int kMaxD = 128;   // int8 device ids
-constexpr int kStats = 4;    // device counters of ns_stats ([0] scores computed by the greedy kernels)
+constexpr int kStats = 6;    // device counters of ns_stats ([0] scores computed by the greedy kernels)
 constexpr int kCommW[6] = {0, 128, 64, 32, 16, 0};   // comm widths "128-64-32-16"
 
 // Head weights passed by value as a kernel parameter (lands in the constant
