@@ -73,7 +73,7 @@ struct SearchBufs {
     // items handed over by k_greedy_wgrp88 once every device holds the
     // linear certificate, plus the forks phase 2 makes; frozen u of the
     // hand-offs; representatives whose u is replayed (k_greedy_replay)
-    int p2_cap, uf_cap, rp_cap;
+    int p2_cap, uf_cap, rp_ctas;
     P2Hdr* p2_hdr;       // [p2_cap]
     uint32_t* p2_work;   // [p2_cap][64] work of each member so far
     double* p2_A;        // [p2_cap][128] per-device A_d
@@ -82,10 +82,12 @@ struct SearchBufs {
     int32_t* p2_ready;   // [p2_cap] publication flags of phase-2 forks
     unsigned int* p2_q;  // [8] counters: next, forks, completed, n_init, uf used, replay entries
     double* uf_buf;      // [uf_cap][64][128] frozen u of the hand-offs
-    int32_t* rp_tau;     // [rp_cap] local tau of a representative to replay
-    int32_t* rp_uf;      // [rp_cap]
-    int32_t* rp_psw;     // [rp_cap] first step whose placement the frozen u lacks
-    int32_t* rp_ord;     // [rp_cap] replay order: entries bucketed by column plan (k_rp_sort)
+    int32_t* rp_ord;     // [p2_cap] replay order of the families (roots bucketed by column plan, k_rp_sort)
+    int32_t* p2_first;   // [p2_cap] first fork of an item (-1: none), forks in step order
+    int32_t* p2_next;    // [p2_cap] next fork of the same parent (-1: last)
+    int32_t* p2_rtau;    // [p2_cap] an item's final representative (local tau)
+    uint8_t* p2_alive;   // [p2_cap] 1: the item ended feasible (its representative needs comp)
+    double* rp_snap;     // [replay CTAs][M][128][64] DFS snapshots of u at fork steps
     double* gscratch;    // grouped greedy group states
     int8_t* ghist;       // grouped greedy group histories [gscratch_warps][M][Tpm]
     int gscratch_warps;
@@ -1412,7 +1414,7 @@ struct WgrpArgs {
     int32_t* dup_of;           // local trajectory indexing, global tau values
     long long tau_base;        // global tau of local trajectory 0
     // phase-2 hand-off (see SearchBufs)
-    int p2_cap, uf_cap, rp_cap;
+    int p2_cap, uf_cap, rp_ctas;
     P2Hdr* p2_hdr;
     uint32_t* p2_work;
     double* p2_A;
@@ -1421,10 +1423,12 @@ struct WgrpArgs {
     int32_t* p2_ready;
     unsigned int* p2_q;
     double* uf_buf;
-    int32_t* rp_tau;
-    int32_t* rp_uf;
-    int32_t* rp_psw;
     int32_t* rp_ord;
+    int32_t* p2_first;
+    int32_t* p2_next;
+    int32_t* p2_rtau;
+    uint8_t* p2_alive;
+    double* rp_snap;
 };
 
 struct P2Hdr {   // 32 bytes
@@ -2420,7 +2424,8 @@ __global__ void __launch_bounds__(256, NS_P2_CTAS) k_greedy_p2(const GreedyArgs 
     const unsigned n_init = __ldcg(x.p2_q + 3);
     unsigned long long computed = 0, nsteps = 0;
 #ifdef NS_WGRP_TIMING
-    unsigned long long t_loop = 0, t_claim = 0, n_items = 0, t_key = 0, t_w = 0;
+    unsigned long long t_loop = 0, t_claim = 0, n_items = 0, t_key = 0, t_w = 0, n_fk = 0;
+    double fk_pos = 0.0, fk_rem = 0.0;
     long long tc0 = clock64();
 #endif
     for (;;) {
@@ -2491,6 +2496,7 @@ __global__ void __launch_bounds__(256, NS_P2_CTAS) k_greedy_p2(const GreedyArgs 
         }
         int cmin = p2_cap_of(cap0, cap1, __ffsll((long long)mask) - 1);
         int cmax = p2_cap_of(cap0, cap1, 63 - __clzll((long long)mask));
+        int last_fork = -1;   // this item's latest fork (the replay walks forks in step order)
         const int32_t* orow = a.ord_row + (size_t)g * a.Tpm;
         const int4* ometa = a.ord_meta + (size_t)g * a.Tpm;
         auto copy_row = [&](long long src, long long dst, int n) {
@@ -2654,6 +2660,11 @@ __global__ void __launch_bounds__(256, NS_P2_CTAS) k_greedy_p2(const GreedyArgs 
                         if (p2_cap_of(cap0, cap1, m) >= xk) take |= 1ULL << m;
                     }
                     rem &= ~take;
+#ifdef NS_WGRP_TIMING
+                    ++n_fk;
+                    fk_pos += (double)(p - p_sw) / (double)(Tp - p_sw);
+                    fk_rem += (double)(Tp - p);
+#endif
                     // fork: the subgroup with its own choice, as a phase-2 item
                     int slot = 0;
                     if (lane == 0) slot = (int)(n_init + atomicAdd(x.p2_q + 1, 1u));
@@ -2673,6 +2684,8 @@ __global__ void __launch_bounds__(256, NS_P2_CTAS) k_greedy_p2(const GreedyArgs 
                     if (lane + 32 < M && ((take >> (lane + 32)) & 1ULL)) x.p2_work[(size_t)slot * 64 + lane + 32] = wk1;
                     copy_row(tau0 + rep, tau0 + krep, Tp);   // the group's history so far
                     if (lane == 0) {
+                        if (last_fork < 0) x.p2_first[item] = slot;
+                        else x.p2_next[last_fork] = slot;
                         a.assign[(size_t)(tau0 + krep) * a.Tpm + li] = (int8_t)dk;   // + its choice
                         P2Hdr fh;
                         fh.g = g;
@@ -2686,6 +2699,7 @@ __global__ void __launch_bounds__(256, NS_P2_CTAS) k_greedy_p2(const GreedyArgs 
                         __threadfence();
                         atomicExch(x.p2_ready + slot, 1);   // publish
                     }
+                    last_fork = slot;
                     __syncwarp();
                 }
                 // stranded members (feas stays 0): their work
@@ -2736,22 +2750,22 @@ __global__ void __launch_bounds__(256, NS_P2_CTAS) k_greedy_p2(const GreedyArgs 
             __syncwarp();
             for (unsigned long long mm = mask & ~(1ULL << rep); mm; mm &= mm - 1)
                 copy_row(tau0 + rep, tau0 + __ffsll((long long)mm) - 1, Tp);
-            if (lane == 0) {
-                const unsigned e = atomicAdd(x.p2_q + 5, 1u);
-                x.rp_tau[e] = (int32_t)(tau0 + rep);
-                x.rp_uf[e] = uf;
-                x.rp_psw[e] = p_sw;
-            }
+        }
+        if (lane == 0) {   // for the replay: the item's representative row and whether it needs comp
+            x.p2_rtau[item] = (int32_t)(tau0 + rep);
+            x.p2_alive[item] = alive ? 1 : 0;
         }
         __threadfence();
         __syncwarp();
         if (lane == 0) atomicAdd(x.p2_q + 2, 1u);   // completed
     }
 #ifdef NS_WGRP_TIMING
-    if (lane == 0 && (blockIdx.x < 2) && (threadIdx.x >> 5) < 2)
-        printf("p2 cta %d warp %d: items %llu steps %llu cycles/step %.0f (keys %.0f W %.0f) claim-wait cycles %llu (n_init %u)\n",
+    if (lane == 0 && (blockIdx.x < 8))
+        printf("p2 cta %d warp %d: items %llu steps %llu cycles/step %.0f (keys %.0f W %.0f) claim-wait cycles %llu (n_init %u) "
+               "forks %llu at %.2f of the phase-2 span, %.0f steps left\n",
                blockIdx.x, threadIdx.x >> 5, n_items, nsteps, nsteps ? (double)t_loop / nsteps : 0.0,
-               nsteps ? (double)t_key / nsteps : 0.0, nsteps ? (double)t_w / nsteps : 0.0, t_claim, n_init);
+               nsteps ? (double)t_key / nsteps : 0.0, nsteps ? (double)t_w / nsteps : 0.0, t_claim, n_init, n_fk,
+               n_fk ? fk_pos / n_fk : 0.0, n_fk ? fk_rem / n_fk : 0.0);
 #endif
     if (lane == 0 && computed) atomicAdd(a.computed, computed);
     if (lane == 0 && computed) atomicAdd(a.computed + 2, computed);   // every phase-2 score is linear
@@ -2765,12 +2779,12 @@ __global__ void __launch_bounds__(256, NS_P2_CTAS) k_greedy_p2(const GreedyArgs 
 constexpr int kRpBuckets = 8192;
 __global__ void __launch_bounds__(1024) k_rp_sort(const GreedyArgs a, const WgrpArgs x) {
     __shared__ int cnt[kRpBuckets];
-    const unsigned n = __ldcg(x.p2_q + 5);
+    const unsigned n = __ldcg(x.p2_q + 3);   // families: one per hand-off
     const long long ncp = x.n_cp > 0 ? x.n_cp : 1;
     for (int i = threadIdx.x; i < kRpBuckets; i += blockDim.x) cnt[i] = 0;
     __syncthreads();
     auto bucket = [&](unsigned e) {
-        const long long g = x.rp_tau[e] / a.M;
+        const long long g = x.p2_hdr[e].g;
         return (int)(ncp <= kRpBuckets ? g : g * kRpBuckets / ncp);
     };
     for (unsigned e = threadIdx.x; e < n; e += blockDim.x) atomicAdd(&cnt[bucket(e)], 1);
@@ -2816,80 +2830,189 @@ __global__ void __launch_bounds__(1024) k_rp_sort(const GreedyArgs a, const Wgrp
 // The representatives of phase-2 groups: u = the frozen u of the hand-off +
 // every later placement replayed in step order (the same additions, in the
 // same order, the per-trajectory kernel makes), then the head in the order
-// of k_greedy_wide88 / k_greedy_wgrp88.  One CTA (4 warps) per
-// representative, its u for all devices in shared memory, device-major with
-// a 16-byte aligned row stride (kUS):
-//  1. the steps' (row, device) go to shared memory, the frozen u is copied
-//     from the 8 x 8 layout (coalesced reads, conflict-free writes);
+// of k_greedy_wide88 / k_greedy_wgrp88.  One CTA (4 warps) per family -- a
+// hand-off and the items forked from it, which share the history before
+// their fork step -- walked depth-first: an item's rows are added up to its
+// next fork step f, u is saved (snapshot slot of the depth), the fork's
+// subtree is walked from f with its own history, u is restored and the item
+// continues; an item that ended feasible gets its comp at Tp.  Every
+// representative's u is therefore the frozen u plus its own history's rows
+// in step order, bit for bit, while the shared prefixes are added once.
+// u for all devices lives in shared memory, device-major with a 16-byte
+// aligned row stride (kUS); a walk over steps [s0, s1):
+//  1. the steps' (row, device) go to shared memory;
 //  2. warp w owns the devices d = w (mod 4) and lists its steps in order
 //     (ballots over the device bytes); it adds each row to u_d with the 32
 //     lanes on 2 features each (one coalesced 512-byte row per instruction),
-//     the next 8 rows' loads in flight while the current 8 are added -- a
+//     the next rows' loads in flight while the current ones are added -- a
 //     device's rows stay in step order, so every feature sums in the same
-//     order as the sequential greedy;
-//  3. one thread per device: the head written out in the 8 x 8 order -- per
-//     feature group fg an FMA chain over its 8 features (head88), then the
-//     tree bfly88 builds for device index j = d & 7:
-//     ((P_j + P_j^4) + (P_j^2 + P_j^6)) + ((P_j^1 + P_j^5) + (P_j^3 + P_j^7)).
+//     order as the sequential greedy.
+// The head, one thread per device, is the 8 x 8 order written out -- per
+// feature group fg an FMA chain over its 8 features (head88), then the tree
+// bfly88 builds for device index j = d & 7:
+// ((P_j + P_j^4) + (P_j^2 + P_j^6)) + ((P_j^1 + P_j^5) + (P_j^3 + P_j^7)).
 constexpr int kUS = kV + 2;
 #ifndef NS_RP_BATCH
-#define NS_RP_BATCH 16
+#define NS_RP_BATCH 12
 #endif
 constexpr int kRpBatch = NS_RP_BATCH;
 // dynamic shared memory of k_greedy_replay; phase 2 is off (no hand-offs)
 // when it exceeds the opt-in maximum (Tpm above ~12k column tables)
 inline size_t replay_smem(int Tpm) {
-    return (size_t)128 * kUS * sizeof(double) + (size_t)(3 * Tpm + 4) * sizeof(int) + (size_t)Tpm + 32;
+    return (size_t)128 * kUS * sizeof(double) + (size_t)Tpm * (sizeof(int2) + 2 * sizeof(int) + 1);
 }
 constexpr size_t kSmemOptin = 232448;
-__global__ void __launch_bounds__(128, 2) k_greedy_replay(const GreedyArgs a, const WgrpArgs x) {
-    extern __shared__ __align__(16) double s_u[];   // [128][kUS] u, then [Tpm] rows, [4][Tpm] step lists, [Tpm + 32] devices
-    const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
-    const unsigned n = __ldcg(x.p2_q + 5);
-    unsigned long long rows = 0, reps = 0;   // ns_stats: rows replayed, representatives
-    int* srow = reinterpret_cast<int*>(s_u + 128 * kUS);
-    uint16_t* slst = reinterpret_cast<uint16_t*>(srow + a.Tpm) + (size_t)w * a.Tpm;
-    uint8_t* sdev = reinterpret_cast<uint8_t*>(srow + a.Tpm + 2 * a.Tpm + 4);   // after 4 uint16 lists (+ pad)
+
 #ifdef NS_WGRP_TIMING
-    long long tph[6] = {0, 0, 0, 0, 0, 0}, nsum = 0, csum = 0;
-    long long c0 = clock64(), c1;
-#define RP_T(k) do { c1 = clock64(); tph[k] += c1 - c0; c0 = c1; } while (0)
+__device__ unsigned long long g_rp_t[8];   // replay phase cycles summed over CTAs (thread 0)
+#define RP_CLK(k, t0) do { if (threadIdx.x == 0) { const long long t1_ = clock64(); atomicAdd(&g_rp_t[k], (unsigned long long)(t1_ - t0)); t0 = t1_; } } while (0)
 #else
-#define RP_T(k) do { } while (0)
+#define RP_CLK(k, t0) do { } while (0)
 #endif
-    for (unsigned e0 = blockIdx.x; e0 < n; e0 += gridDim.x) {
-        const int e = __ldcg(x.rp_ord + e0);
-        const long long tau = x.rp_tau[e];
-        const int uf = x.rp_uf[e], p_sw = x.rp_psw[e];
-        const int g = (int)(tau / a.M);
+// rows of steps [s0, s1) of one history (hist) added to s_u (CTA-wide); the
+// family's row and table index of every step are in srow / stab (indexed by
+// step).  Warp w takes the steps whose device is w (mod 4): it counts them,
+// then (offsets from the four counts) lists them in step order as (row,
+// device offset in s_u) pairs; the devices are gathered from hist twice
+// (the second time from L1).
+__device__ __forceinline__ void rp_walk(const GreedyArgs& a, double* s_u, const int* srow, const int* stab, int2* slst,
+                                        uint8_t* sdev, int* s_wcnt, const int8_t* hist, int s0, int s1) {
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+#ifdef NS_WGRP_TIMING
+    long long tq = clock64();
+#endif
+    __syncthreads();   // the previous walk's lists are consumed
+    for (int i0 = s0 + (int)threadIdx.x; i0 < s1; i0 += 4 * blockDim.x) {   // the walk's devices (4 loads in flight)
+        int8_t v[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const int i = i0 + k * blockDim.x;
+            v[k] = i < s1 ? __ldcg(hist + stab[i]) : (int8_t)0;
+        }
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const int i = i0 + k * blockDim.x;
+            if (i < s1) sdev[i] = (uint8_t)v[k];
+        }
+    }
+    __syncthreads();
+    int cnt = 0;
+    for (int i = s0 + lane; i - lane < s1; i += 32)
+        cnt += __popc(__ballot_sync(kFull, i < s1 && (sdev[i] & 3) == w));
+    if (lane == 0) s_wcnt[w] = cnt;
+    __syncthreads();
+    RP_CLK(1, tq);
+    int2* lst = slst;
+    for (int v = 0; v < w; ++v) lst += s_wcnt[v];
+    {
+        int c = 0;
+        for (int i = s0 + lane; i - lane < s1; i += 32) {
+            const int dv = i < s1 ? (int)sdev[i] : -1;
+            const bool mine = i < s1 && (dv & 3) == w;
+            const unsigned bm = __ballot_sync(kFull, mine);
+            if (mine) lst[c + __popc(bm & ((1u << lane) - 1u))] = make_int2(srow[i], dv * kUS);
+            c += __popc(bm);
+        }
+    }
+    __syncwarp();
+    RP_CLK(2, tq);
+    double2 cur[kRpBatch];
+#pragma unroll
+    for (int k = 0; k < kRpBatch; ++k)
+        if (k < cnt) cur[k] = __ldg(reinterpret_cast<const double2*>(a.V + (size_t)lst[k].x * kV) + lane);
+    for (int b0 = 0; b0 < cnt; b0 += kRpBatch) {
+        double2 nxt[kRpBatch];
+#pragma unroll
+        for (int k = 0; k < kRpBatch; ++k)
+            if (b0 + kRpBatch + k < cnt)
+                nxt[k] = __ldg(reinterpret_cast<const double2*>(a.V + (size_t)lst[b0 + kRpBatch + k].x * kV) + lane);
+#pragma unroll
+        for (int k = 0; k < kRpBatch; ++k)
+            if (b0 + k < cnt) {
+                double2* p = reinterpret_cast<double2*>(s_u + lst[b0 + k].y) + lane;
+                double2 t = *p;
+                t.x += cur[k].x;
+                t.y += cur[k].y;
+                *p = t;
+            }
+#pragma unroll
+        for (int k = 0; k < kRpBatch; ++k) cur[k] = nxt[k];
+    }
+    RP_CLK(3, tq);
+    __syncthreads();
+    RP_CLK(4, tq);
+}
+
+// u (s_u rows) <-> a snapshot slot [128][64] in global memory (CTA-wide, coalesced)
+__device__ __forceinline__ void rp_save(const double* s_u, double* snap) {
+    __syncthreads();
+    for (int i = threadIdx.x; i < 128 * kV / 2; i += blockDim.x) {
+        const int d = i / (kV / 2), k2 = i % (kV / 2);
+        __stcg(reinterpret_cast<double2*>(snap) + i, reinterpret_cast<const double2*>(s_u + d * kUS)[k2]);
+    }
+}
+__device__ __forceinline__ void rp_load(double* s_u, const double* snap) {
+    __syncthreads();
+    for (int i0 = threadIdx.x; i0 < 128 * kV / 2; i0 += 16 * blockDim.x) {   // 16 loads in flight per thread
+        double2 v[16];
+#pragma unroll
+        for (int k = 0; k < 16; ++k) {
+            const int i = i0 + k * blockDim.x;
+            if (i < 128 * kV / 2) v[k] = __ldcg(reinterpret_cast<const double2*>(snap) + i);
+        }
+#pragma unroll
+        for (int k = 0; k < 16; ++k) {
+            const int i = i0 + k * blockDim.x;
+            if (i < 128 * kV / 2) reinterpret_cast<double2*>(s_u + (i / (kV / 2)) * kUS)[i % (kV / 2)] = v[k];
+        }
+    }
+    __syncthreads();
+}
+
+__global__ void __launch_bounds__(128, 2) k_greedy_replay(const GreedyArgs a, const WgrpArgs x) {
+    // [128][kUS] u, then [Tpm] (row, device offset) step lists, [Tpm] rows and [Tpm] table indices of the steps
+    extern __shared__ __align__(16) double s_u[];
+    __shared__ int stk_item[64], stk_pos[64], stk_fork[64];   // DFS stack: item, step reached, its next fork
+    __shared__ int s_wcnt[4];
+    const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+    const unsigned n = __ldcg(x.p2_q + 3);   // families (hand-offs)
+    unsigned long long rows = 0, reps = 0;   // ns_stats: rows replayed, representatives
+    int2* slst = reinterpret_cast<int2*>(s_u + 128 * kUS);
+    int* srow = reinterpret_cast<int*>(slst + a.Tpm);
+    int* stab = srow + a.Tpm;
+    uint8_t* sdev = reinterpret_cast<uint8_t*>(stab + a.Tpm);   // indexed by step
+    double* snap = x.rp_snap + (size_t)blockIdx.x * a.M * 128 * kV;
+    __shared__ unsigned s_claim;
+#ifdef NS_WGRP_TIMING
+    long long t_start = clock64(), t_busy = 0;
+    unsigned n_fam = 0;
+#endif
+    for (;;) {
+        __syncthreads();   // the previous family's head has read s_u, s_claim consumed
+        if (tid == 0) s_claim = atomicAdd(x.p2_q + 6, 1u);   // families claimed in order (dynamic balance)
+        __syncthreads();
+        const unsigned e0 = s_claim;
+        if (e0 >= n) break;
+        const int root = __ldcg(x.rp_ord + e0);
+        if (!__ldcg(x.p2_alive + root) && __ldcg(x.p2_first + root) < 0) continue;   // stranded, no forks
+        const P2Hdr h = x.p2_hdr[root];
+        const int g = h.g;
         const int Tp = a.cp_Tp[g];
-        const int ns = Tp - p_sw;
-        const int8_t* hist = a.assign + (size_t)tau * a.Tpm;
         const int32_t* orow = a.ord_row + (size_t)g * a.Tpm;
         const int4* ometa = a.ord_meta + (size_t)g * a.Tpm;
-        __syncthreads();   // the previous representative's head has read s_u
-        // 1. steps and frozen u
-        for (int i0 = tid; i0 < ns; i0 += 4 * blockDim.x) {
-            int r[4], m[4];
-#pragma unroll
-            for (int k = 0; k < 4; ++k) {
-                const int i = i0 + k * blockDim.x;
-                r[k] = i < ns ? __ldg(orow + p_sw + i) : 0;
-                m[k] = i < ns ? __ldg(ometa + p_sw + i).y : -1;
-            }
-#pragma unroll
-            for (int k = 0; k < 4; ++k) {
-                const int i = i0 + k * blockDim.x;
-                if (i < ns) {
-                    srow[i] = r[k];
-                    sdev[i] = (uint8_t)__ldcg(hist + m[k]);
-                }
-            }
+#ifdef NS_WGRP_TIMING
+        const long long tf0 = clock64();
+        ++n_fam;
+#endif
+        // the family's steps (shared by all its items): V row and table index
+        for (int i = h.p_sw + tid; i < Tp; i += blockDim.x) {
+            srow[i] = __ldg(orow + i);
+            stab[i] = __ldg(ometa + i).y;
         }
         {
-            // uf_buf element (j = jd * 8 + q, c = 32 wgi + 8 dgi + fg) is feature 8 fg + q of
-            // device 32 wgi + 8 dgi + jd; a warp instruction covers one device's 32 features
-            const double* up = x.uf_buf + (size_t)uf * kV * 128;
+            // frozen u: uf_buf element (j = jd * 8 + q, c = 32 wgi + 8 dgi + fg) is feature
+            // 8 fg + q of device 32 wgi + 8 dgi + jd; a warp instruction covers one device's 32 features
+            const double* up = x.uf_buf + (size_t)h.uf * kV * 128;
             const int q = lane & 7, fgl = lane >> 3;
             for (int it0 = w; it0 < 256; it0 += 4 * 32) {   // 32 loads in flight per thread
                 double vv[32];
@@ -2905,95 +3028,96 @@ __global__ void __launch_bounds__(128, 2) k_greedy_replay(const GreedyArgs a, co
                 }
             }
         }
-        __syncthreads();
-        RP_T(0);
-        // 2. this warp's steps (devices d = w mod 4) in step order
-        int cnt = 0;
-        for (int i0 = 0; i0 < ns; i0 += 32) {
-            const int i = i0 + lane;
-            const bool mine = i < ns && (sdev[i] & 3) == w;
-            const unsigned bm = __ballot_sync(kFull, mine);
-            if (mine) slst[cnt + __popc(bm & ((1u << lane) - 1u))] = (uint16_t)i;
-            cnt += __popc(bm);
-        }
-        __syncwarp();
-        RP_T(1);
-        {
-            double2 cur[kRpBatch];
-#pragma unroll
-            for (int k = 0; k < kRpBatch; ++k)
-                if (k < cnt) cur[k] = __ldg(reinterpret_cast<const double2*>(a.V + (size_t)srow[slst[k]] * kV) + lane);
-            for (int b0 = 0; b0 < cnt; b0 += kRpBatch) {
-                double2 nxt[kRpBatch];
-#pragma unroll
-                for (int k = 0; k < kRpBatch; ++k)
-                    if (b0 + kRpBatch + k < cnt)
-                        nxt[k] = __ldg(reinterpret_cast<const double2*>(a.V + (size_t)srow[slst[b0 + kRpBatch + k]] * kV) +
-                                       lane);
-#pragma unroll
-                for (int k = 0; k < kRpBatch; ++k)
-                    if (b0 + k < cnt) {
-                        double2* p = reinterpret_cast<double2*>(s_u + sdev[slst[b0 + k]] * kUS) + lane;
-                        double2 t = *p;
-                        t.x += cur[k].x;
-                        t.y += cur[k].y;
-                        *p = t;
-                    }
-#pragma unroll
-                for (int k = 0; k < kRpBatch; ++k) cur[k] = nxt[k];
+        int item = root, pos = h.p_sw, fork = __ldcg(x.p2_first + root), depth = 0;
+        for (;;) {
+            const bool alive = __ldcg(x.p2_alive + item) != 0;
+            const int target = fork >= 0 ? x.p2_hdr[fork].p - 1 : (alive ? Tp : pos);
+            const long long rtau = __ldcg(x.p2_rtau + item);
+            if (target > pos) {
+                rp_walk(a, s_u, srow, stab, slst, sdev, s_wcnt, a.assign + (size_t)rtau * a.Tpm, pos, target);
+                rows += (unsigned long long)(target - pos);
+                pos = target;
             }
+            if (fork >= 0) {   // descend: save u at the fork step, walk the fork from there
+#ifdef NS_WGRP_TIMING
+                long long tq = clock64();
+#endif
+                rp_save(s_u, snap + (size_t)depth * 128 * kV);
+                RP_CLK(5, tq);
+                if (tid == 0) {
+                    stk_item[depth] = item;
+                    stk_pos[depth] = pos;
+                    stk_fork[depth] = __ldcg(x.p2_next + fork);
+                }
+                ++depth;
+                item = fork;
+                fork = __ldcg(x.p2_first + item);
+                continue;
+            }
+            if (alive) {   // head, one thread per device
+                __syncthreads();
+                const int d = tid;
+                if (d < a.D) {
+                    const double* ud = s_u + d * kUS;
+                    double P[8];
+#pragma unroll
+                    for (int fg = 0; fg < 8; ++fg) {
+                        double acc = 0.0;
+#pragma unroll
+                        for (int q2 = 0; q2 < kG8; ++q2) acc = fma(a.head.H2[kG8 * fg + q2], relu_exact(ud[kG8 * fg + q2]), acc);
+                        P[fg] = acc;
+                    }
+                    const int jd = d & 7;
+                    double t[8];   // t[b] = P_{j ^ b}: three rounds of register swaps (no local memory)
+#pragma unroll
+                    for (int b = 0; b < 8; ++b) t[b] = P[b];
+#pragma unroll
+                    for (int bit = 1; bit < 8; bit <<= 1) {
+                        const bool sw = (jd & bit) != 0;
+#pragma unroll
+                        for (int b = 0; b < 8; ++b)
+                            if (!(b & bit)) {
+                                const double lo = t[b], hi = t[b | bit];
+                                t[b] = sw ? hi : lo;
+                                t[b | bit] = sw ? lo : hi;
+                            }
+                    }
+                    const double s3 = ((t[0] + t[4]) + (t[2] + t[6])) + ((t[1] + t[5]) + (t[3] + t[7]));
+                    const int ds = a.devdim[rtau * a.D + d];
+                    a.comp[rtau * a.D + d] = ds > 0 ? a.head.hb2 + s3 : 0.0;   // reading R4
+                }
+                ++reps;
+            }
+            if (depth == 0) break;
+            // ascend: the parent's u at the fork step, its next fork
+            --depth;
+            __syncthreads();   // stack entries written by thread 0 are visible
+            item = stk_item[depth];
+            pos = stk_pos[depth];
+            fork = stk_fork[depth];
+#ifdef NS_WGRP_TIMING
+            long long tq = clock64();
+#endif
+            rp_load(s_u, snap + (size_t)depth * 128 * kV);
+            RP_CLK(6, tq);
         }
 #ifdef NS_WGRP_TIMING
-        nsum += ns;
-        csum += cnt;
+        t_busy += clock64() - tf0;
 #endif
-        __syncthreads();
-        RP_T(3);
-        // 3. head, one thread per device
-        const int d = tid;
-        if (d < a.D) {
-            const double* ud = s_u + d * kUS;
-            double P[8];
-#pragma unroll
-            for (int fg = 0; fg < 8; ++fg) {
-                double acc = 0.0;
-#pragma unroll
-                for (int q2 = 0; q2 < kG8; ++q2) acc = fma(a.head.H2[kG8 * fg + q2], relu_exact(ud[kG8 * fg + q2]), acc);
-                P[fg] = acc;
-            }
-            const int jd = d & 7;
-            double t[8];   // t[b] = P_{j ^ b}: three rounds of register swaps (no local memory)
-#pragma unroll
-            for (int b = 0; b < 8; ++b) t[b] = P[b];
-#pragma unroll
-            for (int bit = 1; bit < 8; bit <<= 1) {
-                const bool sw = (jd & bit) != 0;
-#pragma unroll
-                for (int b = 0; b < 8; ++b)
-                    if (!(b & bit)) {
-                        const double lo = t[b], hi = t[b | bit];
-                        t[b] = sw ? hi : lo;
-                        t[b | bit] = sw ? lo : hi;
-                    }
-            }
-            const double s3 = ((t[0] + t[4]) + (t[2] + t[6])) + ((t[1] + t[5]) + (t[3] + t[7]));
-            const int ds = a.devdim[tau * a.D + d];
-            a.comp[tau * a.D + d] = ds > 0 ? a.head.hb2 + s3 : 0.0;   // reading R4
-        }
-        RP_T(4);
-        rows += (unsigned long long)ns;
-        ++reps;
     }
-    if (tid == 0 && reps) {
+#ifdef NS_WGRP_TIMING
+    if (tid == 0 && (blockIdx.x % 37) == 0)
+        printf("replay cta %d: families %u rows %llu reps %llu busy %lld of %lld cycles\n", blockIdx.x, n_fam, rows, reps,
+               t_busy, clock64() - t_start);
+    if (tid == 0 && blockIdx.x == 0) {   // sums of the previous launch (this one is still running)
+        printf("replay phases (all CTAs, prev launch): sync0 %llu fill %llu lists %llu adds %llu sync1 %llu save %llu load %llu\n",
+               g_rp_t[0], g_rp_t[1], g_rp_t[2], g_rp_t[3], g_rp_t[4], g_rp_t[5], g_rp_t[6]);
+    }
+#endif
+    if (tid == 0 && (reps || rows)) {
         atomicAdd(a.computed + 3, rows);
         atomicAdd(a.computed + 4, reps);
     }
-#ifdef NS_WGRP_TIMING
-    if (blockIdx.x < 4 && threadIdx.x == 0)
-        printf("replay cta %d n=%u uf=%u: fill %lld lists %lld scan %lld adds %lld head %lld | ns %lld cnt %lld\n", blockIdx.x, n,
-               __ldcg(x.p2_q + 4), tph[0], tph[1], tph[2], tph[3], tph[4], nsum, csum);
-#endif
-#undef RP_T
 }
 
 // ======================================================================
@@ -3363,7 +3487,6 @@ void carve(Carver& c, SearchBufs& b, OutStage& o, int Lout) {
         b.witem_ready = c.take<int32_t>(items);
         b.p2_cap = (int)items;
         b.uf_cap = b.wgrp && replay_smem(b.Tpm) <= kSmemOptin ? 2 * b.wgrp_cp_cap : 0;
-        b.rp_cap = (int)items;
         b.p2_hdr = reinterpret_cast<P2Hdr*>(c.take<long long>((size_t)b.p2_cap * 4));
         b.p2_work = c.take<uint32_t>((size_t)b.p2_cap * 64);
         b.p2_A = c.take<double>((size_t)b.p2_cap * 128);
@@ -3372,10 +3495,12 @@ void carve(Carver& c, SearchBufs& b, OutStage& o, int Lout) {
         b.p2_ready = c.take<int32_t>((size_t)b.p2_cap);
         b.p2_q = c.take<unsigned int>(8);
         b.uf_buf = c.take<double>((size_t)b.uf_cap * kV * 128);
-        b.rp_tau = c.take<int32_t>((size_t)b.rp_cap);
-        b.rp_uf = c.take<int32_t>((size_t)b.rp_cap);
-        b.rp_psw = c.take<int32_t>((size_t)b.rp_cap);
-        b.rp_ord = c.take<int32_t>((size_t)b.rp_cap);
+        b.rp_ord = c.take<int32_t>((size_t)b.p2_cap);
+        b.p2_first = c.take<int32_t>((size_t)b.p2_cap);
+        b.p2_next = c.take<int32_t>((size_t)b.p2_cap);
+        b.p2_rtau = c.take<int32_t>((size_t)b.p2_cap);
+        b.p2_alive = c.take<uint8_t>((size_t)b.p2_cap);
+        b.rp_snap = c.take<double>(b.uf_cap ? (size_t)b.rp_ctas * b.M * 128 * kV : 0);
     }
     b.ghist = c.take<int8_t>((size_t)b.gscratch_warps * b.M * b.Tpm);
     b.capdim = c.take<int32_t>((size_t)b.n_tasks * b.M);
@@ -3573,7 +3698,7 @@ ns_status launch_greedy(ns_ctx* ctx, const SearchBufs& b, const ns_tables* t, lo
         x.n_items = (int)n_items;
         x.p2_cap = b.p2_cap;
         x.uf_cap = b.uf_cap;
-        x.rp_cap = b.rp_cap;
+        x.rp_ctas = b.rp_ctas;
         x.p2_hdr = b.p2_hdr;
         x.p2_work = b.p2_work;
         x.p2_A = b.p2_A;
@@ -3582,14 +3707,18 @@ ns_status launch_greedy(ns_ctx* ctx, const SearchBufs& b, const ns_tables* t, lo
         x.p2_ready = b.p2_ready;
         x.p2_q = b.p2_q;
         x.uf_buf = b.uf_buf;
-        x.rp_tau = b.rp_tau;
-        x.rp_uf = b.rp_uf;
-        x.rp_psw = b.rp_psw;
         x.rp_ord = b.rp_ord;
+        x.p2_first = b.p2_first;
+        x.p2_next = b.p2_next;
+        x.p2_rtau = b.p2_rtau;
+        x.p2_alive = b.p2_alive;
+        x.rp_snap = b.rp_snap;
         NS_CUDA(ctx, cudaMemsetAsync(b.wq, 0, sizeof(WgrpQueue), ctx->stream));
         NS_CUDA(ctx, cudaMemsetAsync(b.witem_ready, 0, n_items * sizeof(int32_t), ctx->stream));
         NS_CUDA(ctx, cudaMemsetAsync(b.p2_q, 0, 8 * sizeof(unsigned int), ctx->stream));
         NS_CUDA(ctx, cudaMemsetAsync(b.p2_ready, 0, (size_t)b.p2_cap * sizeof(int32_t), ctx->stream));
+        NS_CUDA(ctx, cudaMemsetAsync(b.p2_first, 0xff, (size_t)b.p2_cap * sizeof(int32_t), ctx->stream));
+        NS_CUDA(ctx, cudaMemsetAsync(b.p2_next, 0xff, (size_t)b.p2_cap * sizeof(int32_t), ctx->stream));
         const int ctas = (int)std::min<long long>((long long)n_items, (long long)ctx->sm_count * NS_WGRP_CTAS);
         prof_begin(ctx, PK_GREEDY);
         k_greedy_wgrp88<<<(unsigned)ctas, threads, 0, ctx->stream>>>(a2, x);
@@ -3608,7 +3737,7 @@ ns_status launch_greedy(ns_ctx* ctx, const SearchBufs& b, const ns_tables* t, lo
             if (rsm > 48 * 1024)
                 NS_CUDA(ctx, cudaFuncSetAttribute(k_greedy_replay, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rsm));
             k_rp_sort<<<1, 1024, 0, ctx->stream>>>(a2, x);
-            k_greedy_replay<<<(unsigned)(ctx->sm_count * 2), 128, rsm, ctx->stream>>>(a2, x);
+            k_greedy_replay<<<(unsigned)b.rp_ctas, 128, rsm, ctx->stream>>>(a2, x);
         }
         NS_LAUNCHED(ctx);   // p2, sort, replay (the caller counts wgrp88)
         NS_LAUNCHED(ctx);
@@ -3814,6 +3943,9 @@ static void search_layout(const ns_ctx* ctx, int n_tasks, int T_max, int D, cons
         }
         const int nth = ((D + 31) / 32) * 32;   // 8 x 8 layout: 64 doubles of u per lane
         b.wsnap_doubles = (size_t)nth * (kV + 4);   // + dsum, headroom, A_d, certificate
+        // phase-2 replay: 2 CTAs per SM, M DFS snapshot slots (64 KiB) each, within 512 MiB
+        b.rp_ctas = (int)std::max<long long>(
+            ctx->sm_count, std::min<long long>(2LL * ctx->sm_count, (512LL << 20) / ((long long)b.M * 128 * kV * 8)));
     }
 }
 

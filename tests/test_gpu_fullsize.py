@@ -164,17 +164,24 @@ def test_wide_grouped_kernel_bit_identical_to_per_trajectory(ns, ctx, D):
     divergence) against k_greedy_wide88 (every trajectory alone): same lane
     layout and summation order, so every output is bit-identical -- costs,
     assignments, grid indices, W -- on C5-shaped batches, table- and
-    column-wise, and the executed-score counter is below W."""
+    column-wise, and the executed-score counter is below W.  At D = 128 the
+    grouped run takes phase 2 (k_greedy_p2 + k_greedy_replay: closed linear
+    form scores, replayed representatives) -- the counters prove it ran."""
     w = gen_weights(D, "mono")
     tasks = gen_tasks("C5", 6, start=20, T=400 if D == 128 else 150, D=D)
     for mode, kw in (("tablewise", {}), ("columnwise", dict(N=4, K=2, L=3))):
         outs = {}
-        comp = {}
+        comp, st = {}, {}
         for g in (1, 2):
             ns.ns_profile(ctx, True)
             outs[g] = _run(ns, ctx, tasks, w, mode, kw.get("N", 0), kw.get("K", 0), kw.get("L", 0), 11, greedy=g)
-            comp[g] = ns.ns_last_stats(ctx)["scores_computed"]
+            st[g] = ns.ns_last_stats(ctx)
+            comp[g] = st[g]["scores_computed"]
             ns.ns_profile(ctx, False)
+        if D == 128:
+            assert st[1]["replay_reps"] > 0 and st[1]["replay_rows"] > 0, (mode, st[1])
+            assert 0 < st[1]["scores_linear"] < comp[1], (mode, st[1])
+        assert st[2]["replay_reps"] == 0
         for k in ("cost", "assign", "grid_index", "n_scores") + (("n_col", "col_plan") if mode == "columnwise" else ()):
             assert np.array_equal(outs[1][k], outs[2][k]), (mode, k)
         W = int(np.sum(outs[1]["n_scores"]))
@@ -247,7 +254,11 @@ def test_bench_launch_C5_batch(ns, ctx):
     w = gen_weights(128, "mono")
     n = 128
     tasks = gen_tasks("C5", n)
+    ns.ns_profile(ctx, True)
     out = _run(ns, ctx, tasks, w, "columnwise", c["N"], c["K"], c["L"], c["M"])
+    st = ns.ns_last_stats(ctx)
+    ns.ns_profile(ctx, False)
+    assert st["replay_reps"] > 0 and st["scores_linear"] > 0, st   # phase 2 ran
     assert bench.CFG == "C5"
     certified = 0
     for i in (0, 3, 37, 101):

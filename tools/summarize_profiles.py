@@ -87,13 +87,25 @@ def main():
               f"fp64 {float(d['sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active']):.1f}%, "
               f"dmma {float(d.get('sm__pipe_tensor_subpipe_dmma_cycles_active.avg.pct_of_peak_sustained_active', 0)):.1f}%, "
               f"DRAM {dram / 1e6:.0f} MB")
-        if "k_greedy_dedup" in d["Kernel Name"] or "k_greedy_wgrp" in d["Kernel Name"]:
-            json.dump({"kernel": d["Kernel Name"], "bytes_per_launch": dram,
+    # the large-D greedy is three kernels per launch: phase 1, phase 2, replay --
+    # the first consecutive triple of the capture (one beam level)
+    names = [d["Kernel Name"] for d in fm]
+    parts = ("k_greedy_wgrp88", "k_greedy_p2", "k_greedy_replay")
+    for i in range(len(fm) - 2):
+        if all(parts[k] in names[i + k] for k in range(3)):
+            tot_b, per = 0.0, {}
+            for d in fm[i:i + 3]:
+                u = d["units"]
+                scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+                b = sum(float(d[m]) * scale[u[m]] for m in ("dram__bytes_read.sum", "dram__bytes_write.sum"))
+                per[d["Kernel Name"].split("(")[0]] = b
+                tot_b += b
+            json.dump({"kernel": " + ".join(parts), "bytes_per_launch": tot_b, "per_kernel": per,
                        "source": f"ncu --set full, profiles/{out_tag}_ncu_full_metrics.json "
-                                 "(dram__bytes_read.sum + dram__bytes_write.sum of one launch of the bench's "
-                                 "headline step)"},
+                                 "(dram__bytes_read.sum + dram__bytes_write.sum of one launch each of the three "
+                                 "kernels of one beam level of the bench's headline step)"},
                       open("profiles/greedy_traffic.json", "w"), indent=1)
-
+            break
 
 if __name__ == "__main__":
     main()
