@@ -515,11 +515,18 @@ def greedy_roofline(clocks, W, g_ms, g_n, ms_region, stats, kernel):
         roof["replay_reps"] = stats.get("replay_reps", 0)
         roof["executed_share_of_W"] = stats["scores_computed"] / max(W, 1)
         roof["full_score_share_of_W"] = full / max(W, 1)
-        roof["executed_achieved"] = ex
-        roof["executed_frac"] = ex / peak
-        roof["executed_basis"] = ("FP64 flops the greedy kernels executed: scores with feature arithmetic x 256 + "
-                                  "closed-linear-form scores x 2 + replay (64 per row, 136 per device head); "
-                                  "identical trajectories share scores; / greedy time")
+        # the headline fraction is the EXECUTED one: W-based flops count scores
+        # the kernels never compute (shared by identical trajectories, or
+        # decided in the closed linear form) and exceed the pipe's peak
+        roof["oracle_equivalent_achieved"] = achieved
+        roof["oracle_equivalent_frac"] = achieved / peak
+        roof["oracle_equivalent_basis"] = roof.pop("frac_basis")
+        roof["achieved"] = ex
+        roof["frac"] = ex / peak
+        roof["frac_basis"] = ("executed: FP64 flops the greedy kernels executed (scores with feature arithmetic x 256 "
+                              "+ closed-linear-form scores x 2 + replay: 64 per row, 136 per device head; identical "
+                              "trajectories share scores) / greedy time; the kernels are latency-bound (sequential "
+                              "per-table argmin chain): profiles/r2_summary.md")
     return roof
 
 
