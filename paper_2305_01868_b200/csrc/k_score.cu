@@ -10,6 +10,7 @@
 #include <math_constants.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <type_traits>
 #include <vector>
@@ -357,7 +358,11 @@ ns_status run_score_plans(ns_ctx* ctx, const ns_tables* t, int task, int D, cons
                                  8 * 16 * sizeof(int) + 16;
             const size_t uw = (size_t)D * kV * sizeof(double);
             (void)uw;
-            if (D <= 16 && stage <= 160 * 1024) {
+            if (f32 && pool_tc_smem(Tp, D) && !getenv("NS_POOL_SIMT")) {
+                // one-hot bf16 x3 contraction on tcgen05 (k_score_tc.cu)
+                ns_status s = launch_pool_tc(ctx, pb, pe, Tp, D, d_assign, d_rows, t, d_comp, d_dd, d_ok);
+                if (s != NS_OK) return s;
+            } else if (D <= 16 && stage <= 160 * 1024) {
                 // staged task rows, registers per device: 8 warps per CTA
                 const int wpb = 8;
                 const size_t smem = stage;

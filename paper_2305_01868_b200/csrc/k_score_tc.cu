@@ -91,6 +91,18 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, float (&v)[16]) {
     for (int j = 0; j < 16; ++j) v[j] = __uint_as_float(r[j]);
 }
 
+// 16 consecutive fp32 columns, no wait (caller issues tcgen05.wait::ld)
+__device__ __forceinline__ void tmem_ld16_nw(uint32_t taddr, float (&v)[16]) {
+    uint32_t r[16];
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+                   "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+                 : "r"(taddr)
+                 : "memory");
+#pragma unroll
+    for (int j = 0; j < 16; ++j) v[j] = __uint_as_float(r[j]);
+}
+
 // 32 consecutive fp32 columns of this thread's TMEM lane (one load, one wait)
 __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v)[32]) {
     uint32_t r[32];
@@ -345,6 +357,257 @@ __global__ void k_plan_cost_combine(const double* comp, const float* fwd, const 
     }
 }
 
+// ---------------------------------------------------------------------------
+// N2 on tcgen05 (NS_SCORE_TF32X3): per-device sum pooling of every plan as a
+// one-hot contraction.  Row r = (plan, device d) of a 128-row tile:
+//   U[r][n] = sum_t A[r][t] * B[n][t],  A[r][t] = [a_{p,t} == d] (exact in bf16),
+// B[n][t] = the task's cached head row v_t (n < 64), the variant dim (n = 64,
+// integers <= 128: exact) and 1 (n = 65: tables per device).  v is split in
+// three bf16 pieces (v = hi + mid + lo to ~2^-24 relative) and the three
+// pieces are accumulated into ONE fp32 TMEM accumulator by three MMAs per K
+// step; a ones column of A (t = Tp) times B[n][Tp] = hb1_n adds the head bias
+// on the tensor core, so u = hb1 + sum_{t on d} v_t comes out of TMEM ready.
+// The one-hot operand is 2 bytes per (row, table) -- 1/8 of the 64 fp32 of a
+// staged v row a SIMT warp reads per (plan, table).  Epilogue: ReLU and the
+// H2 dot in fp64; a plan holding an id outside 0..D-1 is caught by its table
+// count (sum over its D rows of column 65 != Tp).  Two tile groups of 8 warps
+// per CTA (threads r and r + 128 of a group share TMEM lane r and split the
+// K chunks of the build and the 64 features of the epilogue); each group has
+// its own 128 TMEM columns, one-hot buffer, double-buffered cp.async staging
+// of the assignment bytes (prefetched a tile ahead) and mbarrier.
+constexpr int kPoolN = 80;      // per piece: 64 features + dims + count, padded to 16
+
+struct PoolTcArgs {
+    long long p_begin, p_end;
+    int Tp, Kp, D, LG;          // Kp = Tp + 1 (ones column) rounded up to 16; rows per plan 1 << LG >= D
+    int SG;                     // bytes of one assignment staging buffer
+    const int8_t* assign;       // [P][Tp] (global plan index)
+    const int32_t* rows;        // [Tp] variant rows
+    const double* V;            // [rows][64]
+    const int32_t* vdim;
+    double* comp;               // [P][D]
+    int32_t* devdim;            // [P][D]
+    uint8_t* ok;                // [P]
+    HeadParams head;
+    float h2f[kV];              // H2 rounded to fp32 (epilogue partial dots)
+    long long n_tiles;
+};
+
+__device__ __forceinline__ uint32_t bf16_bits(float x) {   // round to nearest even
+    const uint32_t u = __float_as_uint(x);
+    return (u + 0x7FFFu + ((u >> 16) & 1u)) >> 16;
+}
+
+__device__ __forceinline__ void mma_bf16(uint32_t tmem, uint64_t ad, uint64_t bd, uint32_t idesc, uint32_t acc) {
+    asm volatile("{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
+                 " tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}" ::"r"(tmem),
+                 "l"(ad), "l"(bd), "r"(idesc), "r"(acc));
+}
+
+// piece k (0 hi, 1 mid, 2 lo) of x as bf16 bits: x = hi + mid + lo + O(2^-25 |x|)
+__device__ __forceinline__ uint32_t bf16_piece(double x, int k) {
+    const uint32_t hb = bf16_bits((float)x);
+    if (k == 0) return hb;
+    const double r1 = x - (double)__uint_as_float(hb << 16);
+    const uint32_t mb = bf16_bits((float)r1);
+    if (k == 1) return mb;
+    return bf16_bits((float)(r1 - (double)__uint_as_float(mb << 16)));
+}
+
+__global__ void __launch_bounds__(512, 1) k_pool_tc(const PoolTcArgs a) {
+    extern __shared__ __align__(128) uint8_t psm[];
+    __shared__ uint32_t s_tmem;
+    __shared__ __align__(8) uint64_t s_bar[2][2];   // per group, per accumulator buffer
+    __shared__ double s_part[2][128];     // the upper half's partial head dot per row
+    const int tid = threadIdx.x, warp = tid >> 5;
+    const int grp = tid >> 8, gtid = tid & 255, gwarp = warp & 3;
+    const int r = gtid & 127, hf = gtid >> 7;
+    const int Kp = a.Kp, Tp = a.Tp, D = a.D, LG = a.LG, PT = 128 >> LG;
+    const size_t bblk = (size_t)kPoolN * Kp * 2;                    // bytes of one piece block
+    uint8_t* sB = psm;                                              // 3 x [80 x Kp] bf16, K-major
+    uint8_t* sA = psm + 3 * bblk + (size_t)grp * 2 * 128 * Kp * 2;  // 2 x [128 x Kp] one-hot
+    uint8_t* sG = psm + 3 * bblk + (size_t)4 * 128 * Kp * 2 + (size_t)grp * 2 * a.SG;  // 2 x [SG] bytes
+    // ---- resident B (three piece blocks)
+    for (int i = tid; i < 3 * kPoolN * Kp; i += blockDim.x) {
+        const int k = i / (kPoolN * Kp), rem = i - k * (kPoolN * Kp);
+        const int n = rem / Kp, t = rem - n * Kp;
+        uint32_t bits = 0;
+        if (t < Tp) {
+            const int row = __ldg(a.rows + t);
+            if (n < 64)
+                bits = bf16_piece(__ldg(a.V + (size_t)row * kV + n), k);
+            else if (k == 0 && n == 64)
+                bits = bf16_bits((float)__ldg(a.vdim + row));
+            else if (k == 0 && n == 65)
+                bits = 0x3F80u;
+        } else if (t == Tp && n < 64) {
+            bits = bf16_piece(a.head.hb1[n], k);   // bias column (A's ones column)
+        }
+        *reinterpret_cast<uint16_t*>(sB + (size_t)k * bblk + (size_t)(t >> 3) * (kPoolN * 16) + (n >> 3) * 128 +
+                                     (n & 7) * 16 + (t & 7) * 2) = (uint16_t)bits;
+    }
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(su32(&s_tmem)), "r"(512));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    if (tid == 0) {
+        for (int g = 0; g < 4; ++g) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(su32(&s_bar[g >> 1][g & 1])));
+        asm volatile("fence.mbarrier_init.release.cluster;");
+    }
+    asm volatile("fence.proxy.async.shared::cta;");
+    asm volatile("tcgen05.fence::before_thread_sync;");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;");
+    const uint32_t tmem = s_tmem + (uint32_t)(grp * 256);   // two 128-column accumulators per group
+    const uint32_t lane_off = (uint32_t)(gwarp * 32) << 16;
+    uint32_t phbits = 0;   // mbarrier phase per accumulator buffer
+    const uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(kPoolN >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
+    const int pl = r >> LG, d = r & ((1 << LG) - 1);
+    const uint32_t d4 = (uint32_t)d * 0x01010101u;
+    auto gbar = [&]() { asm volatile("bar.sync %0, 256;" ::"r"(1 + grp)); };
+    // stage a tile's assignment bytes (contiguous in global: PT plans x Tp) as
+    // 16-byte cp.async chunks from the 16-byte aligned-down start
+    const uintptr_t abase = reinterpret_cast<uintptr_t>(a.assign);
+    auto stage = [&](long long tile, int buf) {
+        if (tile < a.n_tiles) {
+            const long long p0 = a.p_begin + tile * PT;
+            const long long np = a.p_end - p0 < PT ? a.p_end - p0 : PT;
+            const uintptr_t g0 = (abase + (uintptr_t)(p0 * Tp)) & ~(uintptr_t)15;
+            const uintptr_t g1 = abase + (uintptr_t)((p0 + np) * Tp);
+            const int nch = (int)((g1 - g0 + 15) >> 4);
+            const uint32_t dst = su32(sG + (size_t)buf * a.SG);
+            for (int c = gtid; c < nch; c += 256)
+                asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst + 16 * c), "l"(g0 + 16 * (uintptr_t)c));
+        }
+        asm volatile("cp.async.commit_group;");
+    };
+    const int kh = Kp >> 4;                   // K chunks (8 tables) per half
+    const int kc_last = (Tp - 1) >> 3;        // chunks from here on hold bytes past the row (masked)
+    // one-hot rows of `tile` (staged in sG[buf]) into A[buf], then the MMAs into accumulator buf
+    auto build_mma = [&](long long tile, int buf) {
+        const long long p0 = a.p_begin + tile * PT;
+        uint8_t* Ab = sA + (size_t)buf * 128 * Kp * 2;
+        {
+            const int o = (int)((abase + (uintptr_t)(p0 * Tp)) & 15) + pl * Tp;
+            const uint32_t* g = reinterpret_cast<const uint32_t*>(sG + (size_t)buf * a.SG) + (o >> 2);
+            const uint32_t sh = 8u * (uint32_t)(o & 3);
+            uint8_t* arow = Ab + (r >> 3) * 128 + (r & 7) * 16;
+            uint32_t w0 = g[2 * kh * hf];
+            for (int kc = kh * hf; kc < kh * (hf + 1); ++kc) {
+                const uint32_t w1 = g[2 * kc + 1], w2 = g[2 * kc + 2];
+                uint32_t x0 = __funnelshift_r(w0, w1, sh), x1 = __funnelshift_r(w1, w2, sh);
+                w0 = w2;
+                uint32_t one0 = 0, one1 = 0;
+                if (kc >= kc_last) {   // uniform: bytes past the row never match; the ones column
+                    const int t0 = 8 * kc;
+                    const int v0 = min(max(Tp - t0, 0), 4), v1 = min(max(Tp - t0 - 4, 0), 4);
+                    x0 |= v0 >= 4 ? 0u : (0xFFFFFFFFu << (8 * v0));
+                    x1 |= v1 >= 4 ? 0u : (0xFFFFFFFFu << (8 * v1));
+                    const int j = Tp - t0;   // ones column position in this chunk (0..7), if any
+                    if (j >= 0 && j < 4) one0 = 0xFFu << (8 * j);
+                    if (j >= 4 && j < 8) one1 = 0xFFu << (8 * (j - 4));
+                }
+                // 0xFF per matching byte; the ones column's byte forced to match
+                const uint32_t e0 = __vcmpeq4(x0, d4) | one0;
+                const uint32_t e1 = __vcmpeq4(x1, d4) | one1;
+                uint4 q;
+                q.x = __byte_perm(e0, 0, 0x1100) & 0x3F803F80u;
+                q.y = __byte_perm(e0, 0, 0x3322) & 0x3F803F80u;
+                q.z = __byte_perm(e1, 0, 0x1100) & 0x3F803F80u;
+                q.w = __byte_perm(e1, 0, 0x3322) & 0x3F803F80u;
+                *reinterpret_cast<uint4*>(arow + (size_t)kc * (128 * 16)) = q;
+            }
+        }
+        asm volatile("fence.proxy.async.shared::cta;");
+        asm volatile("tcgen05.fence::before_thread_sync;");
+        gbar();
+        asm volatile("tcgen05.fence::after_thread_sync;");
+        if (gtid == 0) {
+            for (int ks = 0; ks < (Kp >> 4); ++ks) {
+                const uint64_t ad = umma_desc(su32(Ab + (size_t)ks * 2 * (128 * 16)), 128 * 16, 128);
+#pragma unroll
+                for (int k = 0; k < 3; ++k) {
+                    const uint64_t bd = umma_desc(su32(sB + k * bblk + (size_t)ks * 2 * (kPoolN * 16)), kPoolN * 16, 128);
+                    mma_bf16(tmem + 128 * buf, ad, bd, idesc, (ks > 0 || k > 0) ? 1u : 0u);
+                }
+            }
+            commit(&s_bar[grp][buf]);
+        }
+    };
+    // head epilogue of `tile` from accumulator buf: comp = H2 . ReLU(u) + hb2 in
+    // fp64; half hf reads features [32 hf, 32 hf + 32)
+    auto epilogue = [&](long long tile, int buf) {
+        mbar_wait(&s_bar[grp][buf], (phbits >> buf) & 1u);
+        phbits ^= 1u << buf;
+        asm volatile("tcgen05.fence::after_thread_sync;");
+        const uint32_t lb = tmem + 128 * buf + lane_off;
+        const long long p0 = a.p_begin + tile * PT;
+        const int np = (int)(a.p_end - p0 < PT ? a.p_end - p0 : PT);
+        float u[32];
+        tmem_ld32(lb + 32 * hf, u);
+        // H2 . ReLU(u) as fp32 partial dots of 16 terms (their rounding is of
+        // the order of the fp32 pooling's own), summed in fp64: 2 f32->f64
+        // conversions per thread instead of 32 on the conversion pipe
+        float dp[8];
+        if (hf == 0) {
+#pragma unroll
+            for (int j = 0; j < 8; ++j) dp[j] = a.h2f[j] * fmaxf(u[j], 0.0f);
+#pragma unroll
+            for (int j = 8; j < 32; ++j) dp[j & 7] = fmaf(a.h2f[j], fmaxf(u[j], 0.0f), dp[j & 7]);
+        } else {
+#pragma unroll
+            for (int j = 0; j < 8; ++j) dp[j] = a.h2f[32 + j] * fmaxf(u[j], 0.0f);
+#pragma unroll
+            for (int j = 8; j < 32; ++j) dp[j & 7] = fmaf(a.h2f[32 + j], fmaxf(u[j], 0.0f), dp[j & 7]);
+        }
+        const double part = (double)((dp[0] + dp[1]) + (dp[2] + dp[3])) + (double)((dp[4] + dp[5]) + (dp[6] + dp[7]));
+        int ddim = 0;
+        bool bad = false;
+        if (hf == 0) {   // warp-uniform: dims and table count of the row
+            float dv[16];
+            tmem_ld16(lb + 64, dv);
+            ddim = (int)dv[0];
+            int cnt = d < D ? (int)dv[1] : 0;
+            for (int o = 1; o < (1 << LG); o <<= 1) cnt += __shfl_xor_sync(kFull, cnt, o);
+            bad = cnt != Tp;   // some id of the plan lies outside 0..D-1
+        }
+        asm volatile("tcgen05.fence::before_thread_sync;");
+        if (hf == 1) s_part[grp][r] = part;
+        gbar();
+        const long long p = p0 + pl;
+        if (hf == 0 && pl < np && d < D) {
+            a.comp[p * D + d] = ddim > 0 ? (part + s_part[grp][r]) + a.head.hb2 : 0.0;
+            a.devdim[p * D + d] = ddim;
+            if (d == 0) a.ok[p] = bad ? 0 : 1;
+        }
+    };
+    // software pipeline per group: stage two tiles ahead, build + MMA one tile
+    // ahead, so tile i+1's MMAs run under tile i's epilogue
+    const long long tstride = (long long)gridDim.x * 2;
+    long long tile = (long long)blockIdx.x * 2 + grp;
+    stage(tile, 0);
+    stage(tile + tstride, 1);
+    if (tile < a.n_tiles) {
+        asm volatile("cp.async.wait_group 1;");
+        gbar();
+        build_mma(tile, 0);
+    }
+    for (int it = 0; tile < a.n_tiles; tile += tstride, ++it) {
+        const int buf = it & 1;
+        if (tile + tstride < a.n_tiles) {
+            asm volatile("cp.async.wait_group 0;");   // tile + 1's bytes
+            gbar();
+            stage(tile + 2 * tstride, buf);          // sG[buf] was read by this tile's build
+            build_mma(tile + tstride, buf ^ 1);
+        }
+        epilogue(tile, buf);
+    }
+    asm volatile("cp.async.wait_group 0;");
+    asm volatile("tcgen05.fence::before_thread_sync;");
+    __syncthreads();
+    if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(s_tmem), "r"(512));
+}
+
 }  // namespace
 
 // Plan costs of rows [pb, pe) with the comm MLPs on tcgen05 (3xTF32).
@@ -386,6 +649,57 @@ ns_status launch_plan_cost_tc(ns_ctx* ctx, long long pb, long long pe, const dou
     const long long n = pe - pb;
     k_plan_cost_combine<<<(unsigned)std::min<long long>((n + 255) / 256, 4096), 256, 0, ctx->stream>>>(
         comp, fbuf, bbuf, ok, pb, pe, D, cost, (ctx->rflags & NS_R11_SUM_OF_MAX) ? 1 : 0);
+    NS_LAUNCHED(ctx);
+    return NS_OK;
+}
+
+
+// Shared-memory bytes of k_pool_tc for a post-split list of Tp tables
+// (0 when the tensor-core pooling does not apply).
+static int pool_tc_kp(int Tp) { return ((Tp + 1 + 15) / 16) * 16; }   // + the ones column
+
+static int pool_tc_sg(int Tp) {   // 16-byte lead-in + 64 plans + the last row's read-ahead
+    const int Kp = pool_tc_kp(Tp);
+    return ((16 + 64 * Tp + Kp + 16) + 15) / 16 * 16;
+}
+
+size_t pool_tc_smem(int Tp, int D) {
+    if (D > 16 || Tp <= 0) return 0;
+    const size_t Kp = (size_t)pool_tc_kp(Tp);
+    const size_t smem = 3 * Kp * kPoolN * 2 + 4 * 128 * Kp * 2 + 2 * 2 * (size_t)pool_tc_sg(Tp);
+    return smem <= 200 * 1024 ? smem : 0;
+}
+
+ns_status launch_pool_tc(ns_ctx* ctx, long long pb, long long pe, int Tp, int D, const int8_t* assign,
+                         const int32_t* rows, const ns_tables* t, double* comp, int32_t* devdim, uint8_t* ok) {
+    const size_t smem = pool_tc_smem(Tp, D);
+    if (!smem) return set_err(ctx, NS_ERR_INTERNAL, "k_pool_tc shape");
+    if (pe <= pb) return NS_OK;
+    PoolTcArgs a;
+    a.p_begin = pb;
+    a.p_end = pe;
+    a.Tp = Tp;
+    a.Kp = pool_tc_kp(Tp);
+    a.SG = pool_tc_sg(Tp);
+    a.D = D;
+    a.LG = 1;
+    while ((1 << a.LG) < D) ++a.LG;
+    a.assign = assign;
+    a.rows = rows;
+    a.V = t->d_V;
+    a.vdim = t->d_vdim;
+    a.comp = comp;
+    a.devdim = devdim;
+    a.ok = ok;
+    a.head = ctx->model.head;
+    for (int k = 0; k < kV; ++k) a.h2f[k] = (float)a.head.H2[k];
+    const int PT = 128 >> a.LG;
+    a.n_tiles = (pe - pb + PT - 1) / PT;
+    cudaFuncSetAttribute(k_pool_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    const long long grid = std::min<long long>((a.n_tiles + 1) / 2, ctx->sm_count);
+    prof_begin(ctx, PK_SCORE);
+    k_pool_tc<<<(unsigned)grid, 512, smem, ctx->stream>>>(a);
+    prof_end(ctx);
     NS_LAUNCHED(ctx);
     return NS_OK;
 }

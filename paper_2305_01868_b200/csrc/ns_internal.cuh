@@ -210,6 +210,12 @@ ns_status launch_plan_cost(ns_ctx* ctx, long long rb, long long re, const uint8_
 ns_status launch_plan_cost_tc(ns_ctx* ctx, long long pb, long long pe, const double* comp, const int32_t* devdim,
                               const uint8_t* ok, float* fbuf, float* bbuf, double* cost);
 
+// N2 on tcgen05 (k_score_tc.cu, NS_SCORE_TF32X3): per-device pooling as a
+// one-hot bf16 x3 contraction; writes comp / devdim / ok like k_pool_staged.
+size_t pool_tc_smem(int Tp, int D);
+ns_status launch_pool_tc(ns_ctx* ctx, long long pb, long long pe, int Tp, int D, const int8_t* assign,
+                         const int32_t* rows, const ns_tables* t, double* comp, int32_t* devdim, uint8_t* ok);
+
 // helpers (ns_api.cu)
 ns_status set_err(ns_ctx* ctx, ns_status s, const std::string& msg);
 ns_status cuda_check(ns_ctx* ctx, cudaError_t e, const char* what);

@@ -571,6 +571,45 @@ def test_score_plans_tf32x3_tcgen05(ns, ctx, D):
         assert b32 == b64
 
 
+@pytest.mark.parametrize("D,T,n_col", [(1, 12, 0), (3, 40, 2), (5, 17, 0), (8, 80, 0), (8, 61, 3), (16, 150, 4)])
+def test_score_plans_pool_tcgen05(ns, ctx, D, T, n_col, monkeypatch):
+    """NS_SCORE_TF32X3 pooling as a one-hot bf16 x3 contraction on tcgen05
+    (k_pool_tc): plan costs within 1e-5 relative of the oracle's plan_cost
+    (P:232 / P:391), within 1e-6 of the SIMT fp32 pooling (NS_POOL_SIMT), on
+    odd D (unused one-hot rows), Tp with and without a multiple of 4 (word and
+    byte staging), column plans, a ragged last tile, host and device
+    assignments; plans holding an invalid device id score NaN."""
+    import torch
+    rng = np.random.default_rng(500 + D * 7 + T)
+    task = small_task(rng, T, D)
+    w = gen_weights(D, "mono", seed=90 + D)
+    tabs = _setup(ns, ctx, [task], w)
+    col = [int(c) for c in rng.choice(np.flatnonzero(task.dims % 8 == 0), size=n_col, replace=False)]
+    Tp = T + n_col
+    P = 2 * 128 + 37
+    A = gen_plans(Tp, D, P, seed=D + T)
+    A[5, Tp - 1] = D            # invalid ids: out of range and negative
+    A[77, 0] = -1
+    c_tc, b_tc, _ = ns.ns_score_plans(ctx, tabs, 0, D, col, A, mode=ns.NS_SCORE_TF32X3)
+    c_dev, b_dev, _ = ns.ns_score_plans(ctx, tabs, 0, D, col, torch.from_numpy(A).cuda(), mode=ns.NS_SCORE_TF32X3)
+    monkeypatch.setenv("NS_POOL_SIMT", "1")
+    c_simt, b_simt, _ = ns.ns_score_plans(ctx, tabs, 0, D, col, A, mode=ns.NS_SCORE_TF32X3)
+    monkeypatch.delenv("NS_POOL_SIMT")
+    assert np.isnan(c_tc[5]) and np.isnan(c_tc[77]) and np.isnan(c_simt[5])
+    good = np.ones(P, bool)
+    good[[5, 77]] = False
+    np.testing.assert_array_equal(c_tc, c_dev)
+    assert b_tc == b_dev
+    rel = np.abs(c_tc[good] - c_simt[good]) / np.abs(c_simt[good])
+    assert rel.max() < 1e-6, rel.max()
+    emb = om.TableEmbeddings(w, task)
+    tables = osr.apply_col_plan(task, col)
+    for p in list(range(0, P, 17)) + [P - 1]:
+        if good[p]:
+            assert _rel(c_tc[p], om.plan_cost(w, emb, tables, A[p].tolist(), D)[0]) < 1e-5, p
+    tabs.free()
+
+
 def test_profile_class_mask(ns, ctx):
     """ns_profile with a class list times only those kernel classes (the bench
     brackets just the roofline kernel inside its timed region); the search

@@ -1,5 +1,5 @@
 """ns_score_plans throughput (plans/s) for FP64 (DMMA) and TF32X3 (tcgen05) modes."""
-import sys, time
+import os, sys, time
 sys.path.insert(0, '/root/repo')
 import numpy as np, torch
 import paper_2305_01868_b200 as ns
@@ -12,7 +12,12 @@ for cfg, D in (("C2", 4), ("C3", 8)):
     P = 1 << 20
     A = torch.from_numpy(gen_plans(task.T, D, P, seed=1)).cuda()
     cost = torch.zeros(P, dtype=torch.float64, device="cuda")
-    for mode, name in ((ns.NS_SCORE_FP64, "fp64-dmma"), (ns.NS_SCORE_TF32X3, "tf32x3-tcgen05")):
+    for mode, name, simt in ((ns.NS_SCORE_FP64, "fp64-dmma", 0), (ns.NS_SCORE_TF32X3, "tf32x3 (SIMT pooling)", 1),
+                             (ns.NS_SCORE_TF32X3, "tf32x3 (tcgen05 pooling)", 0)):
+        if simt:
+            os.environ["NS_POOL_SIMT"] = "1"
+        else:
+            os.environ.pop("NS_POOL_SIMT", None)
         ns.ns_score_plans(ctx, tabs, 0, D, [], A, mode=mode, cost_out=cost)
         ns.ns_profile(ctx, True)
         torch.cuda.synchronize(); t0 = time.perf_counter()
