@@ -710,6 +710,10 @@ def score_plans_rate(ns, ctx, torch):
     cost = torch.zeros(P, dtype=torch.float64, device="cuda")
     mlp_flop = 2.0 * 2 * (2 * D * 128 + 128 * 64 + 64 * 32 + 32 * 16 + 16 * D)
     pool_flop = T * 64 + D * 64 * 3
+    rows_per_plan = 2
+    while rows_per_plan < D:
+        rows_per_plan *= 2
+    pool_mma_flop = rows_per_plan * 240 * ((T + 1 + 15) // 16 * 16) * 2
     clock = 1965e6
     fp64_pipe = 148 * 64 * clock          # DADD/s
     peaks = {}
@@ -742,6 +746,14 @@ def score_plans_rate(ns, ctx, torch):
                      ("pool_frac_fp64_pipe" if name == "fp64" else "pool_frac_fp32_pipe"):
                          P * pool_flop / (pool_ms * 1e-3) / (fp64_pipe if name == "fp64" else 2 * fp64_pipe),
                      "mlp_tflops": P * mlp_work / (mlp_ms * 1e-3) / 1e12,
+                     # TF32X3 pooling runs on tcgen05 as a one-hot bf16 x3 contraction
+                     # (k_pool_tc): executed MMA flops per plan = rows per plan (D rounded
+                     # up to a power of two) x 240 columns x Kp (T + 1 rounded up to 16) x 2
+                     **({"pool_kernel": "k_pool_tc (one-hot bf16 x3 on tcgen05)",
+                         "pool_mma_tflops": P * pool_mma_flop / (pool_ms * 1e-3) / 1e12,
+                         "pool_mma_frac_bf16": P * pool_mma_flop / (pool_ms * 1e-3) / (peaks.get("bf16_tflops", 2250.0) * 1e12),
+                         "pool_useful_frac_of_mma": pool_flop / pool_mma_flop}
+                        if name == "tf32x3" else {"pool_kernel": "k_pool_staged (fp64 SIMT)"}),
                      "mlp_frac": P * mlp_work / (mlp_ms * 1e-3) / mlp_peak,
                      "hbm_gbs": (P * T + P * 8) / (ms * 1e-3) / 1e9}
     tabs.free()
