@@ -9,6 +9,7 @@
 #include <math_constants.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <climits>
 #include <cmath>
 #include <cstring>
@@ -47,6 +48,10 @@ struct SearchBufs {
     double* vmin;        // [n_tasks][64] smallest v_k over the task's variant rows (linear-regime certificate)
     double* Brow;        // [rows] sum_k H2_k v_rk (k_task_lin)
     int ord_b, ord_e;    // column plans whose cost order this rank builds (its greedy block; others get cp_Tp only)
+    int prev_b, prev_e;  // the previous level's ord_b / ord_e (k_merge_order: parents this rank ordered)
+    int32_t* ord_row2;   // the previous level's cost orders (swapped with ord_row / ord_meta per level)
+    int4* ord_meta2;
+    int32_t* beam_slot;  // [n_tasks][K] slot (previous level's numbering) of each beam
     int32_t* ord_row;    // [S][Tpm]  variant row of the p-th table in cost order
     int4* ord_meta;      // [S][Tpm]  {dim, list index, bytes lo, bytes hi} of the p-th table (grouped greedy stream)
     // per traj
@@ -338,13 +343,10 @@ __device__ __forceinline__ int4 pack_meta(const TaskView& tv, int row, int i) {
     return make_int4(tv.vdim[row], i, (int)(unsigned)(by & 0xffffffffull), (int)(unsigned)(by >> 32));
 }
 
-__global__ void k_build_order(SearchBufs b, TaskView tv) {
-    extern __shared__ __align__(16) unsigned char bsm[];
-    const int g = blockIdx.x;
-    if (!b.cp_valid[g]) return;
-    const int q = b.cp_task[g];
-    const int len = b.cp_len[g];
-    const int base = tv.off[q], T = tv.off[q + 1] - base;
+// The bitonic rank sort of column plan g (list of T + len entries) into
+// ord_row / ord_meta (one CTA, shared memory as k_build_order sizes it).
+__device__ void sort_order(const SearchBufs& b, const TaskView& tv, int g, int base, int T, int len,
+                           unsigned char* bsm) {
     const int Tp = T + len;
     const int n = pow2_ceil(b.Tpm);
     double* key = (double*)bsm;              // [n]  -C
@@ -359,10 +361,8 @@ __global__ void k_build_order(SearchBufs b, TaskView tv) {
             rows[c] += 1;
             rows[T + k] = rows[c];
         }
-        b.cp_Tp[g] = Tp;
     }
     __syncthreads();
-    if (g < b.ord_b || g >= b.ord_e) return;   // another rank's greedy block (multi-rank)
     for (int i = threadIdx.x; i < n; i += blockDim.x) {
         key[i] = i < Tp ? -tv.C[rows[i]] : CUDART_INF;
         id[i] = i < Tp ? i : INT_MAX;
@@ -391,6 +391,87 @@ __global__ void k_build_order(SearchBufs b, TaskView tv) {
         const int i = id[r];
         b.ord_row[(size_t)g * b.Tpm + r] = rows[i];
         b.ord_meta[(size_t)g * b.Tpm + r] = pack_meta(tv, rows[i], i);
+    }
+}
+
+__global__ void k_build_order(SearchBufs b, TaskView tv) {
+    extern __shared__ __align__(16) unsigned char bsm[];
+    const int g = blockIdx.x;
+    if (!b.cp_valid[g]) return;
+    const int q = b.cp_task[g];
+    const int len = b.cp_len[g];
+    const int base = tv.off[q], T = tv.off[q + 1] - base;
+    if (threadIdx.x == 0) b.cp_Tp[g] = T + len;
+    if (g < b.ord_b || g >= b.ord_e) return;   // another rank's greedy block (multi-rank)
+    sort_order(b, tv, g, base, T, len, bsm);
+}
+
+// Beam levels, long lists: a child column plan is its parent's (a beam of the
+// previous level, whose cost order that level built) plus one split c, so its
+// order is the parent's with entry c removed and the two halves (-C_h, c) and
+// (-C_h, T'_parent) merged in -- the same unique ascending order of the
+// distinct keys (-C_i, i) the rank sort produces (reading R13), in one pass:
+// parent entry r moves to r - [r > pos(c)] + [e1 < key_r] + [e2 < key_r], and
+// e1 / e2 land after the entries below them.  The previous level's orders sit
+// in ord_row2 / ord_meta2 (swapped per level); a parent another rank ordered
+// (multi-rank block boundary) falls back to the rank sort.
+__global__ void k_merge_order(SearchBufs b, TaskView tv, int level) {
+    extern __shared__ __align__(16) unsigned char bsm[];
+    __shared__ int s_pc, s_rowc, s_lt1, s_lt2;
+    const int g = blockIdx.x;
+    if (!b.cp_valid[g]) return;
+    const int q = b.cp_task[g];
+    const int len = b.cp_len[g];
+    const int base = tv.off[q], T = tv.off[q + 1] - base;
+    const int Tp = T + len, Tpp = Tp - 1;
+    if (threadIdx.x == 0) b.cp_Tp[g] = Tp;
+    if (g < b.ord_b || g >= b.ord_e) return;   // another rank's greedy block (multi-rank)
+    const int bb = (g / b.N2) % b.K;
+    const int gp = level == 1 ? q : b.beam_slot[q * b.K + bb];
+    if (gp < b.prev_b || gp >= b.prev_e) {   // the parent's order lives on another rank
+        sort_order(b, tv, g, base, T, len, bsm);
+        return;
+    }
+    const int c = b.cp_plan[(size_t)g * b.Lcap + len - 1];
+    const int32_t* prow = b.ord_row2 + (size_t)gp * b.Tpm;
+    const int4* pmeta = b.ord_meta2 + (size_t)gp * b.Tpm;
+    if (threadIdx.x == 0) {
+        s_lt1 = 0;
+        s_lt2 = 0;
+    }
+    for (int r = threadIdx.x; r < Tpp; r += blockDim.x)
+        if (__ldg(&pmeta[r].y) == c) {
+            s_pc = r;
+            s_rowc = __ldg(prow + r);
+        }
+    __syncthreads();
+    const int pc = s_pc, rowh = s_rowc + 1;   // both halves are the next variant row
+    const double kh = -tv.C[rowh];
+    int32_t* orow = b.ord_row + (size_t)g * b.Tpm;
+    int4* ometa = b.ord_meta + (size_t)g * b.Tpm;
+    int lt1 = 0, lt2 = 0;
+    for (int r = threadIdx.x; r < Tpp; r += blockDim.x) {
+        if (r == pc) continue;
+        const int row = __ldg(prow + r);
+        const int4 m = __ldg(pmeta + r);
+        const double kr = -tv.C[row];
+        const bool b1 = kh < kr || (kh == kr && c < m.y);   // e1 = (-C_h, c) sorts before entry r
+        const bool b2 = kh < kr;                            // e2 = (-C_h, Tpp): Tpp > every parent index
+        const int np = r - (r > pc ? 1 : 0) + (b1 ? 1 : 0) + (b2 ? 1 : 0);
+        orow[np] = row;
+        ometa[np] = m;
+        lt1 += b1 ? 0 : 1;
+        lt2 += b2 ? 0 : 1;
+    }
+    atomicAdd(&s_lt1, lt1);
+    atomicAdd(&s_lt2, lt2);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        const int p1 = s_lt1, p2 = s_lt2 + 1;
+        orow[p1] = rowh;
+        ometa[p1] = pack_meta(tv, rowh, c);
+        orow[p2] = rowh;
+        ometa[p2] = pack_meta(tv, rowh, Tpp);
     }
 }
 
@@ -3351,6 +3432,7 @@ __global__ void __launch_bounds__(256) k_select(SearchBufs b, int C, int level, 
                 const int g = q * C + j;
                 for (int k = lane; k < level; k += 32)
                     b.beam_plan[((size_t)q * b.K + r) * b.Lcap + k] = b.cp_plan[(size_t)g * b.Lcap + k];
+                if (lane == 0) b.beam_slot[q * b.K + r] = g;   // its cost order: the next level's parent
             }
         }
         if (threadIdx.x == 0) b.beam_cnt[q] = s_nvalid < Kbeam ? s_nvalid : Kbeam;
@@ -3463,6 +3545,11 @@ void carve(Carver& c, SearchBufs& b, OutStage& o, int Lout) {
     b.cp_Tp = c.take<int32_t>(b.S);
     b.ord_row = c.take<int32_t>((size_t)b.S * b.Tpm);
     b.ord_meta = c.take<int4>((size_t)b.S * b.Tpm);
+    // the second order buffer of the incremental (merge) orders: long lists, beam levels
+    const bool merge_orders = b.Tpm > 256 && b.Lcap > 0 && b.S > b.n_tasks;
+    b.ord_row2 = merge_orders ? c.take<int32_t>((size_t)b.S * b.Tpm) : nullptr;
+    b.ord_meta2 = merge_orders ? c.take<int4>((size_t)b.S * b.Tpm) : nullptr;
+    b.beam_slot = c.take<int32_t>((size_t)b.n_tasks * b.K);
     b.assign = c.take<int8_t>((size_t)b.n_traj * b.Tpm);
     b.comp = c.take<double>((size_t)b.n_traj * b.D);
     b.devdim = c.take<int32_t>((size_t)b.n_traj * b.D);
@@ -3980,17 +4067,25 @@ ns_status run_search(ns_ctx* ctx, const ns_tables* t, int D, const ns_search_par
     // short lists: one warp per column plan (8 per CTA); long lists: one CTA
     const bool warp_order = b.Tpm <= 256;
     const size_t wsm = 8 * osm;
-    auto launch_order = [&](int n_cp, int level0) {
+    if (bsm > 48 * 1024) cudaFuncSetAttribute(k_merge_order, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bsm);
+    const bool merge_orders = b.ord_row2 != nullptr && !getenv("NS_SORT_ORDERS");
+    auto launch_order = [&](int n_cp, int level0, int level) {
         // only this rank's greedy block needs the cost order (the same
         // contiguous blocks as run_level_trajectories)
         const long long R = ctx->emulated ? 1 : ctx->nranks;
         const long long per = ((long long)n_cp + R - 1) / R;
+        b.prev_b = b.ord_b;
+        b.prev_e = b.ord_e;
         b.ord_b = ctx->emulated ? 0 : (int)std::min<long long>(n_cp, ctx->rank * per);
         b.ord_e = ctx->emulated ? n_cp : (int)std::min<long long>(n_cp, (long long)b.ord_b + per);
         prof_begin(ctx, PK_ORDER);
         if (warp_order) {
             const unsigned blocks = (unsigned)std::max(1, std::min((n_cp + 7) / 8, ctx->sm_count * 8));
             k_order_warp<<<blocks, 256, wsm, ctx->stream>>>(b, tv, n_cp, level0, t->d_sumdim, grid_hi);
+        } else if (merge_orders && level > 0) {
+            std::swap(b.ord_row, b.ord_row2);   // the previous level's orders become the parents
+            std::swap(b.ord_meta, b.ord_meta2);
+            k_merge_order<<<n_cp, 512, bsm, ctx->stream>>>(b, tv, level);
         } else {
             k_build_order<<<n_cp, 512, bsm, ctx->stream>>>(b, tv);
         }
@@ -4007,7 +4102,7 @@ ns_status run_search(ns_ctx* ctx, const ns_tables* t, int D, const ns_search_par
         NS_LAUNCHED(ctx);
         NS_LAUNCHED(ctx);
     }
-    launch_order(b.n_tasks, warp_order ? 1 : 0);
+    launch_order(b.n_tasks, warp_order ? 1 : 0, 0);
     if ((s = run_level_trajectories(ctx, b, t, b.n_tasks)) != NS_OK) return s;
     // table-wise (L = 0): the level-0 selection also packs the outputs
     const bool final0 = L == 0;
@@ -4029,7 +4124,7 @@ ns_status run_search(ns_ctx* ctx, const ns_tables* t, int D, const ns_search_par
         k_expand<<<b.n_tasks * b.K, 256, esm, ctx->stream>>>(b, tv, level);
         prof_end(ctx);
         NS_LAUNCHED(ctx);
-        launch_order(b.S, 0);
+        launch_order(b.S, 0, level);
         if ((s = run_level_trajectories(ctx, b, t, b.S)) != NS_OK) return s;
         prof_begin(ctx, PK_SELECT);
         size_t ssel = (size_t)C * 16 + 8;

@@ -275,6 +275,30 @@ def test_bench_launch_C5_batch(ns, ctx):
     assert certified == 2
 
 
+def test_merge_orders_identical_to_rank_sort(ns, ctx, monkeypatch):
+    """Beam levels with long lists derive each child's cost order from its
+    parent's (k_merge_order: remove the split entry, merge the two halves);
+    the result must be the rank sort's (k_build_order, forced with
+    NS_SORT_ORDERS) bit for bit -- checked through every output of a
+    column-wise C5 batch (ragged: one task cut to 700 tables), plus a table
+    list with duplicated tables (equal single costs: ties broken by index)."""
+    c = CONFIGS["C5"]
+    w = gen_weights(128, "mono")
+    tasks = gen_tasks("C5", 12)
+    t0 = tasks[5]
+    tasks[5] = type(t0)(t0.dims[:700], t0.hash[:700], t0.pooling[:700], t0.skew[:700], t0.D, t0.cap, t0.seed)
+    t1 = tasks[7]
+    rep = np.concatenate([np.arange(400), np.arange(400)])   # every table twice
+    tasks[7] = type(t1)(t1.dims[rep], t1.hash[rep], t1.pooling[rep], t1.skew[rep], t1.D, t1.cap, t1.seed)
+    merged = _run(ns, ctx, tasks, w, "columnwise", c["N"], c["K"], c["L"], c["M"])
+    monkeypatch.setenv("NS_SORT_ORDERS", "1")
+    sorted_ = _run(ns, ctx, tasks, w, "columnwise", c["N"], c["K"], c["L"], c["M"])
+    monkeypatch.delenv("NS_SORT_ORDERS")
+    for k in ("cost", "n_col", "col_plan", "assign", "grid_index", "n_scores"):
+        np.testing.assert_array_equal(np.asarray(merged[k]), np.asarray(sorted_[k]), err_msg=k)
+    assert int(np.max(merged["n_col"])) >= 2   # beams deeper than level 1 were taken
+
+
 READINGS = [("R10 absolute starts", 16, dict(abs_starts=True)),
             ("R11 sum of maxima", 32, dict(sum_of_max=True)),
             ("R14 splittable only", 64, dict(splittable_only=True)),
