@@ -15,6 +15,8 @@
 // Forward starts are comp - min(comp) (reading R10), backward starts 0,
 // inputs scaled by division exactly like the oracle (R10).
 #include <cuda_runtime.h>
+
+#include <cmath>
 #include <math_constants.h>
 
 #include "ns_device.cuh"
@@ -31,11 +33,14 @@ struct PlanCostArgs {
     double* cost;                   // [rows]
     CommParams cp;
     double start_scale, dim_scale;
+    double inv_dim_scale;           // 1 / dim_scale when dim_scale is a power of two (exact), else 0
     int ldx, ldy;                   // smem row strides (doubles)
     uint32_t rflags;                // NS_R10_ABS_STARTS / NS_R11_SUM_OF_MAX
     const int32_t* list;            // optional: rows = list[i], i < *list_n (then row_begin = 0, row_end = capacity)
     const int32_t* list_n;
 };
+
+constexpr unsigned kFullMlp = 0xffffffffu;
 
 __device__ __forceinline__ void dmma(double (&c)[2], double a, double b) {
     asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
@@ -111,10 +116,13 @@ __device__ __forceinline__ void warp_layer(const double* __restrict__ W, const d
 #ifndef NS_PC_BLOCKS
 #define NS_PC_BLOCKS 4
 #endif
+#ifndef NS_PC_BIG_UNROLL
+#define NS_PC_BIG_UNROLL 16
+#endif
 // BIG (D > 16, e.g. C5's 128 devices): the wide layers' weights stream from L2;
 // their k-loops are unrolled so several B-fragment loads are in flight
 template <bool BIG>
-__global__ void __launch_bounds__(128, BIG ? 3 : NS_PC_BLOCKS) k_plan_cost_dmma(const PlanCostArgs a) {
+__global__ void __launch_bounds__(128, BIG ? 2 : NS_PC_BLOCKS) k_plan_cost_dmma(const PlanCostArgs a) {
     extern __shared__ double psm[];
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
     const int g = lane >> 2, t = lane & 3;
@@ -132,33 +140,59 @@ __global__ void __launch_bounds__(128, BIG ? 3 : NS_PC_BLOCKS) k_plan_cost_dmma(
     const long long base = a.row_begin + ((long long)blockIdx.x * nrb + rb) * 16;
     const long long end = a.list ? a.row_begin + *a.list_n : a.row_end;
     const bool rows = base < end;
-    // row ids and per-row min comp (lane r < 16 of the fwd warp owns row r)
-    if (rows && dir == 0 && lane < 16) {
-        const long long i = base + lane;
-        long long r = -1;
-        if (i < end) r = a.list ? (long long)a.list[i] : i;
-        rid[lane] = r;
-        double m = 0.0;
-        if (r >= 0) {
-            m = CUDART_INF;
-            for (int d = 0; d < D; ++d) m = fmin(m, a.comp[r * D + d]);
+    // row ids (lane r < 16 of the fwd warp owns row r) and the per-row min
+    // comp (min is exact in any order): small D one lane per row, large D
+    // the fwd warp's lanes over the devices
+    if (rows && dir == 0) {
+        if (lane < 16) {
+            const long long i = base + lane;
+            long long r = -1;
+            if (i < end) r = a.list ? (long long)a.list[i] : i;
+            rid[lane] = r;
+            if constexpr (!BIG) {
+                double m = 0.0;
+                if (r >= 0) {
+                    m = CUDART_INF;
+                    for (int d = 0; d < D; ++d) m = fmin(m, a.comp[r * D + d]);
+                }
+                mn[lane] = (a.rflags & NS_R10_ABS_STARTS) ? 0.0 : m;   // R10: relative (default) or absolute starts
+            }
         }
-        mn[lane] = (a.rflags & NS_R10_ABS_STARTS) ? 0.0 : m;   // R10: relative (default) or absolute starts
+        if constexpr (BIG) {
+            __syncwarp();
+            for (int r = 0; r < 16; ++r) {
+                const long long row = rid[r];
+                double m = CUDART_INF;
+                if (row >= 0)
+                    for (int d = lane; d < D; d += 32) m = fmin(m, a.comp[row * D + d]);
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) m = fmin(m, __shfl_xor_sync(kFullMlp, m, o));
+                if (lane == 0) mn[r] = (row < 0 || (a.rflags & NS_R10_ABS_STARTS)) ? 0.0 : m;
+            }
+        }
     }
     __syncthreads();
     if (rows) {
-        // input rows [starts / start_scale (D), devdim / dim_scale (D)], zero padded
-        for (int i = lane; i < 16 * K0p; i += 32) {
-            const int r = i / K0p, c = i % K0p;
+        // input rows [starts / start_scale (D), devdim / dim_scale (D)], zero
+        // padded; a power-of-two dim_scale divides exactly by its reciprocal
+        auto input = [&](int r, int c) {
             const long long row = rid[r];
             double v = 0.0;
             if (row >= 0 && c < K0) {
-                if (c < D)
+                if (c < D) {
                     v = dir == 0 ? (a.comp[row * D + c] - mn[r]) / a.start_scale : 0.0;
-                else
-                    v = (double)a.devdim[row * D + (c - D)] / a.dim_scale;
+                } else {
+                    const double dd = (double)a.devdim[row * D + (c - D)];
+                    v = a.inv_dim_scale != 0.0 ? dd * a.inv_dim_scale : dd / a.dim_scale;
+                }
             }
             X[r * ldx + c] = v;
+        };
+        if constexpr (BIG) {
+            for (int r = 0; r < 16; ++r)
+                for (int c = lane; c < K0p; c += 32) input(r, c);
+        } else {
+            for (int i = lane; i < 16 * K0p; i += 32) input(i / K0p, i % K0p);
         }
         __syncwarp();
         const double* W1 = a.cp.W[dir][0];
@@ -191,8 +225,8 @@ __global__ void __launch_bounds__(128, BIG ? 3 : NS_PC_BLOCKS) k_plan_cost_dmma(
                     dmma(acc1[1][q], a1, bv);
                 }
             };
-            if constexpr (BIG) {
-#pragma unroll 4
+            if constexpr (BIG) {   // (2 CTAs/SM by shared memory: registers for 16 steps of loads in flight)
+#pragma unroll 16
                 for (int kt = 0; kt < K0p / 4; ++kt) l1_step(kt);
             } else {
                 for (int kt = 0; kt < K0p / 4; ++kt) l1_step(kt);
@@ -540,6 +574,10 @@ ns_status launch_plan_cost(ns_ctx* ctx, long long rb, long long re, const uint8_
     a.cp = comm_params(ctx);
     a.start_scale = ctx->model.start_scale;
     a.dim_scale = ctx->model.dim_scale;
+    {
+        int e;
+        a.inv_dim_scale = (a.dim_scale > 0.0 && std::frexp(a.dim_scale, &e) == 0.5) ? 1.0 / a.dim_scale : 0.0;
+    }
     const int K0p = (2 * a.D + 3) & ~3;
     a.ldx = ld_pad(K0p > 64 ? K0p : 64);
     a.ldy = ld_pad(32);
