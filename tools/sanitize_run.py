@@ -1,8 +1,8 @@
 """Small runs of every hot kernel for compute-sanitizer (memcheck / racecheck /
 synccheck): grouped greedy (pair-staged rows), per-lane greedy, the large-D
 greedy in the 8x8 layout (k_greedy_wgrp88 with forks, k_greedy_wide88), plan
-cost, precompute (both shapes), score_plans in both modes (tcgen05 two tile
-groups), pre-training steps, the embedding-bag kernels (hot-row backward,
+cost, precompute (both shapes), long-list orders (rank sort, merge),
+score_plans in both modes (tcgen05 pooling and comm MLPs), pre-training steps, the embedding-bag kernels (hot-row backward,
 exchange at one rank)."""
 import sys
 sys.path.insert(0, '/root/repo')
@@ -37,6 +37,17 @@ ns.ns_shard_tablewise(ctx, tabs, 40, M=3)                         # large-D gree
 g1 = ns.ns_shard_columnwise(ctx, tabs, 40, N=3, K=2, L=2, M=7, greedy=1)   # k_greedy_wgrp88 (forks)
 g2 = ns.ns_shard_columnwise(ctx, tabs, 40, N=3, K=2, L=2, M=7, greedy=2)   # k_greedy_wide88
 assert np.array_equal(g1["cost"], g2["cost"]) and np.array_equal(g1["assign"], g2["assign"])
+tabs.free()
+# long lists (T' > 256): level-0 rank sort (k_build_order), beam levels by merge (k_merge_order)
+t300 = [gen_task("C3", 9, T=300, D=40), gen_task("C3", 10, T=280, D=40)]
+d, o, c = ns.table_descs(t300)
+tabs = ns.ns_featurize_tables(ctx, d, o, c)
+m1 = ns.ns_shard_columnwise(ctx, tabs, 40, N=3, K=2, L=3, M=3)
+import os
+os.environ["NS_SORT_ORDERS"] = "1"
+m2 = ns.ns_shard_columnwise(ctx, tabs, 40, N=3, K=2, L=3, M=3)
+del os.environ["NS_SORT_ORDERS"]
+assert np.array_equal(m1["cost"], m2["cost"]) and np.array_equal(m1["assign"], m2["assign"])
 tabs.free()
 # F2: one Adam step of each cost model
 import torch
