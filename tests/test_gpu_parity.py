@@ -571,14 +571,17 @@ def test_score_plans_tf32x3_tcgen05(ns, ctx, D):
         assert b32 == b64
 
 
-@pytest.mark.parametrize("D,T,n_col", [(1, 12, 0), (3, 40, 2), (5, 17, 0), (8, 80, 0), (8, 61, 3), (16, 150, 4)])
+@pytest.mark.parametrize("D,T,n_col", [(1, 12, 0), (3, 40, 2), (5, 17, 0), (8, 80, 0), (8, 61, 3), (16, 100, 4),
+                                         (8, 111, 0), (8, 112, 0), (16, 150, 4)])
 def test_score_plans_pool_tcgen05(ns, ctx, D, T, n_col, monkeypatch):
     """NS_SCORE_TF32X3 pooling as a one-hot bf16 x3 contraction on tcgen05
     (k_pool_tc): plan costs within 1e-5 relative of the oracle's plan_cost
     (P:232 / P:391), within 1e-6 of the SIMT fp32 pooling (NS_POOL_SIMT), on
     odd D (unused one-hot rows), Tp with and without a multiple of 4 (word and
     byte staging), column plans, a ragged last tile, host and device
-    assignments; plans holding an invalid device id score NaN."""
+    assignments, both sides of the shared-memory limit (T' = 111 is the last
+    list on k_pool_tc, 112 the first on the SIMT pooling); plans holding an
+    invalid device id score NaN."""
     import torch
     rng = np.random.default_rng(500 + D * 7 + T)
     task = small_task(rng, T, D)
@@ -602,6 +605,9 @@ def test_score_plans_pool_tcgen05(ns, ctx, D, T, n_col, monkeypatch):
     assert b_tc == b_dev
     rel = np.abs(c_tc[good] - c_simt[good]) / np.abs(c_simt[good])
     assert rel.max() < 1e-6, rel.max()
+    for n in (1, 17):   # a single, partially filled tile: the same per-plan values
+        c_n, _, _ = ns.ns_score_plans(ctx, tabs, 0, D, col, A[:n].copy(), mode=ns.NS_SCORE_TF32X3)
+        np.testing.assert_array_equal(c_n, c_tc[:n])
     emb = om.TableEmbeddings(w, task)
     tables = osr.apply_col_plan(task, col)
     for p in list(range(0, P, 17)) + [P - 1]:
