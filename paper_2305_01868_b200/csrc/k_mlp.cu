@@ -116,9 +116,6 @@ __device__ __forceinline__ void warp_layer(const double* __restrict__ W, const d
 #ifndef NS_PC_BLOCKS
 #define NS_PC_BLOCKS 4
 #endif
-#ifndef NS_PC_BIG_UNROLL
-#define NS_PC_BIG_UNROLL 16
-#endif
 // BIG (D > 16, e.g. C5's 128 devices): the wide layers' weights stream from L2;
 // their k-loops are unrolled so several B-fragment loads are in flight
 template <bool BIG>

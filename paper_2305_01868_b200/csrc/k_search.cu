@@ -19,7 +19,7 @@
 #include "ns_internal.cuh"
 
 #ifndef NS_WGRP_CTAS
-#define NS_WGRP_CTAS 2   // resident CTAs per SM of k_greedy_wgrp88 (launch bounds and persistent grid)
+#define NS_WGRP_CTAS 3   // resident CTAs per SM of k_greedy_wgrp88 (launch bounds and persistent grid; 168 registers with spills: +1% over 2 at 1024 C5 tasks)
 #endif
 #ifndef NS_WGRP_MIN_CP
 #define NS_WGRP_MIN_CP 148   // column plans per launch from which large D uses the grouped kernel
