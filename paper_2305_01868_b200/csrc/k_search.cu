@@ -21,6 +21,9 @@
 #ifndef NS_WGRP_CTAS
 #define NS_WGRP_CTAS 3   // resident CTAs per SM of k_greedy_wgrp88 (launch bounds and persistent grid; 168 registers with spills: +1% over 2 at 1024 C5 tasks)
 #endif
+#ifndef NS_MERGE_THREADS
+#define NS_MERGE_THREADS 256   // threads per column plan of k_merge_order (its rank-sort fallback included; 512: 2.04 vs 1.58 ms per step)
+#endif
 #ifndef NS_WGRP_MIN_CP
 #define NS_WGRP_MIN_CP 148   // column plans per launch from which large D uses the grouped kernel
 #endif
@@ -4085,7 +4088,7 @@ ns_status run_search(ns_ctx* ctx, const ns_tables* t, int D, const ns_search_par
         } else if (merge_orders && level > 0) {
             std::swap(b.ord_row, b.ord_row2);   // the previous level's orders become the parents
             std::swap(b.ord_meta, b.ord_meta2);
-            k_merge_order<<<n_cp, 512, bsm, ctx->stream>>>(b, tv, level);
+            k_merge_order<<<n_cp, NS_MERGE_THREADS, bsm, ctx->stream>>>(b, tv, level);
         } else {
             k_build_order<<<n_cp, 512, bsm, ctx->stream>>>(b, tv);
         }
