@@ -24,6 +24,9 @@
 #ifndef NS_MERGE_THREADS
 #define NS_MERGE_THREADS 256   // threads per column plan of k_merge_order (its rank-sort fallback included; 512: 2.04 vs 1.58 ms per step)
 #endif
+#ifndef NS_EXPAND_COUNT_MAX
+#define NS_EXPAND_COUNT_MAX 256   // k_expand: lists up to this length select candidates by rank counting
+#endif
 #ifndef NS_WGRP_MIN_CP
 #define NS_WGRP_MIN_CP 148   // column plans per launch from which large D uses the grouped kernel
 #endif
@@ -194,7 +197,7 @@ __global__ void k_expand(SearchBufs b, TaskView tv, int level) {
         }
     }
     __syncthreads();
-    if (Tp <= 256) {
+    if (Tp <= NS_EXPAND_COUNT_MAX) {
         // short lists: ranks by counting, stopped once both reach N
         for (int i = threadIdx.x; i < Tp; i += blockDim.x) {
             const double ci = keyc[i];
@@ -221,7 +224,7 @@ __global__ void k_expand(SearchBufs b, TaskView tv, int level) {
     long long pb = LLONG_MAX;
     int pic = -1, pib = -1;
     const int lane = threadIdx.x & 31, wi = threadIdx.x >> 5, nwarp = blockDim.x >> 5;
-    for (int r = 0; r < (Tp > 256 ? N : 0); ++r) {
+    for (int r = 0; r < (Tp > NS_EXPAND_COUNT_MAX ? N : 0); ++r) {
         double bc = -CUDART_INF;
         long long bbv = LLONG_MIN;
         int ic = -1, ib = -1;
