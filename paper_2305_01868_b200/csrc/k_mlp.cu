@@ -223,8 +223,10 @@ __global__ void __launch_bounds__(128, BIG ? 2 : NS_PC_BLOCKS) k_plan_cost_dmma(
                 }
             };
             if constexpr (BIG) {   // (2 CTAs/SM by shared memory: registers for 16 steps of loads in flight)
+                // bwd: the start inputs are 0, their products +-0 leave the
+                // accumulators (+0 from the start) unchanged -- skip them
 #pragma unroll 16
-                for (int kt = 0; kt < K0p / 4; ++kt) l1_step(kt);
+                for (int kt = dir == 1 ? D / 4 : 0; kt < K0p / 4; ++kt) l1_step(kt);
             } else {
                 for (int kt = 0; kt < K0p / 4; ++kt) l1_step(kt);
             }
