@@ -54,7 +54,7 @@ def parse():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--tasks", type=int, default=1024, help="C5 tasks per GPU per step")
+    ap.add_argument("--tasks", type=int, default=1536, help="C5 tasks per GPU per step")
     ap.add_argument("--c2-tasks", type=int, default=65536, help="C2 tasks per step (secondary)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
