@@ -54,7 +54,9 @@ def parse():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--tasks", type=int, default=1536, help="C5 tasks per GPU per step")
+    ap.add_argument("--tasks", type=int, default=None,
+                    help="C5 tasks per GPU per step (default 1536 on one GPU; 1024 per GPU with N > 1, whose ranks "
+                         "also hold every task's replicated featurisation: ~111 GB per GPU at N = 8)")
     ap.add_argument("--c2-tasks", type=int, default=65536, help="C2 tasks per step (secondary)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -332,6 +334,8 @@ def main():
     D, N, K, L, M = c["D"], c["N"], c["K"], c["L"], c["M"]
     w = gen_weights(D, "mono")
     ns.ns_load_cost_models(ctx, w)
+    if args.tasks is None:
+        args.tasks = 1536 if world == 1 else 1024
     n = args.tasks * world                    # the job's batch: every rank holds it, computes 1/world of it
     tasks = gen_tasks(CFG, n)
     desc, off, caps = ns.table_descs(tasks)
