@@ -504,6 +504,21 @@ def greedy_roofline(clocks, W, g_ms, g_n, ms_region, stats, kernel):
                 roof["traffic_source"] = tj.get("source")
         except Exception:
             pass
+    # issue-slot view of the same kernels from the committed ncu capture (the
+    # greedy is latency-bound: issue-active is the roof it is measured against)
+    full = os.path.join(ROOT, "profiles", "r2_ncu_full_metrics.json")
+    if os.path.exists(full):
+        try:
+            iss = {}
+            for rec in json.load(open(full)):
+                name = rec.get("Kernel Name", "").split("(")[0].split()[-1]
+                if name.startswith("k_greedy") and "smsp__issue_active.avg.pct_of_peak_sustained_active" in rec:
+                    iss.setdefault(name, []).append(float(rec["smsp__issue_active.avg.pct_of_peak_sustained_active"]))
+            if iss:
+                roof["ncu_issue_active_pct"] = iss
+                roof["ncu_issue_source"] = "profiles/r2_ncu_full_metrics.json (one launch per kernel per captured level)"
+        except Exception:
+            pass
     if stats and stats.get("scores_computed"):
         # executed FP64 work: scores with feature arithmetic (256 flop), scores in
         # the closed linear form hb2 + (A_d + B_t) (2 flop), phase-2 replays
