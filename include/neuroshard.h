@@ -180,9 +180,13 @@ ns_status ns_tables_single_costs(ns_ctx* ctx, const ns_tables* tables,
 typedef enum {
     NS_SCORE_FP64 = 0,    /* fp64: pooling on the FP64 pipe, comm MLPs on the FP64 tensor cores */
     NS_SCORE_TF32X3 = 1   /* bulk mode (D <= 16): comm MLPs on the tcgen05 tensor cores in
-                             split-TF32 (hi*hi + hi*lo + lo*hi), FP32 accumulation in TMEM,
-                             and the per-device pooling in fp32 (head epilogue in fp64);
-                             ~1e-6 relative plan costs (north star tolerance 1e-3) */
+                             split-TF32 (hi*hi + hi*lo + lo*hi), FP32 accumulation in TMEM;
+                             the per-device pooling on tcgen05 as a one-hot bf16 contraction
+                             (v split hi + mid + lo, FP32 accumulation; T' <= 111, else SIMT
+                             fp32 pooling), head epilogue in fp32 partial dots summed in fp64;
+                             ~1e-6 relative plan costs (north star tolerance 1e-3).  A device
+                             `assign` is read in 16-byte aligned chunks: up to 15 bytes before
+                             its first and after its last plan may be read (never written) */
 } ns_score_mode;
 
 /* Simulator f(c, t) as a service ("estimate the embedding cost of any
