@@ -2917,7 +2917,7 @@ __global__ void __launch_bounds__(1024) k_rp_sort(const GreedyArgs a, const Wgrp
 // The representatives of phase-2 groups: u = the frozen u of the hand-off +
 // every later placement replayed in step order (the same additions, in the
 // same order, the per-trajectory kernel makes), then the head in the order
-// of k_greedy_wide88 / k_greedy_wgrp88.  One CTA (4 warps) per family -- a
+// of k_greedy_wide88 / k_greedy_wgrp88.  One CTA (NS_RP_WARPS warps) per family -- a
 // hand-off and the items forked from it, which share the history before
 // their fork step -- walked depth-first: an item's rows are added up to its
 // next fork step f, u is saved (snapshot slot of the depth), the fork's
@@ -2928,7 +2928,7 @@ __global__ void __launch_bounds__(1024) k_rp_sort(const GreedyArgs a, const Wgrp
 // u for all devices lives in shared memory, device-major with a 16-byte
 // aligned row stride (kUS); a walk over steps [s0, s1):
 //  1. the steps' (row, device) go to shared memory;
-//  2. warp w owns the devices d = w (mod 4) and lists its steps in order
+//  2. warp w owns the devices d = w (mod NS_RP_WARPS) and lists its steps in order
 //     (ballots over the device bytes); it adds each row to u_d with the 32
 //     lanes on 2 features each (one coalesced 512-byte row per instruction),
 //     the next rows' loads in flight while the current ones are added -- a
@@ -2940,9 +2940,13 @@ __global__ void __launch_bounds__(1024) k_rp_sort(const GreedyArgs a, const Wgrp
 // ((P_j + P_j^4) + (P_j^2 + P_j^6)) + ((P_j^1 + P_j^5) + (P_j^3 + P_j^7)).
 constexpr int kUS = kV + 2;
 #ifndef NS_RP_BATCH
-#define NS_RP_BATCH 8   // rows in flight per warp of the replay (12 measured 1.5% slower at 1024 tasks)
+#define NS_RP_BATCH 4   // rows in flight per warp of the replay (sweep at 1536 tasks: 8 warps x 4 best; 4 warps x 8: -2%, 16 warps x 2: -1.4%)
 #endif
 constexpr int kRpBatch = NS_RP_BATCH;
+#ifndef NS_RP_WARPS
+#define NS_RP_WARPS 8   // warps per replay CTA (devices d = w mod NS_RP_WARPS per warp; 128 registers, small spills)
+#endif
+constexpr int kRpWarps = NS_RP_WARPS;
 // dynamic shared memory of k_greedy_replay; phase 2 is off (no hand-offs)
 // when it exceeds the opt-in maximum (Tpm above ~12k column tables)
 inline size_t replay_smem(int Tpm) {
@@ -2985,7 +2989,7 @@ __device__ __forceinline__ void rp_walk(const GreedyArgs& a, double* s_u, const 
     __syncthreads();
     int cnt = 0;
     for (int i = s0 + lane; i - lane < s1; i += 32)
-        cnt += __popc(__ballot_sync(kFull, i < s1 && (sdev[i] & 3) == w));
+        cnt += __popc(__ballot_sync(kFull, i < s1 && (sdev[i] & (kRpWarps - 1)) == w));
     if (lane == 0) s_wcnt[w] = cnt;
     __syncthreads();
     RP_CLK(1, tq);
@@ -2995,7 +2999,7 @@ __device__ __forceinline__ void rp_walk(const GreedyArgs& a, double* s_u, const 
         int c = 0;
         for (int i = s0 + lane; i - lane < s1; i += 32) {
             const int dv = i < s1 ? (int)sdev[i] : -1;
-            const bool mine = i < s1 && (dv & 3) == w;
+            const bool mine = i < s1 && (dv & (kRpWarps - 1)) == w;
             const unsigned bm = __ballot_sync(kFull, mine);
             if (mine) lst[c + __popc(bm & ((1u << lane) - 1u))] = make_int2(srow[i], dv * kUS);
             c += __popc(bm);
@@ -3040,15 +3044,16 @@ __device__ __forceinline__ void rp_save(const double* s_u, double* snap) {
 }
 __device__ __forceinline__ void rp_load(double* s_u, const double* snap) {
     __syncthreads();
-    for (int i0 = threadIdx.x; i0 < 128 * kV / 2; i0 += 16 * blockDim.x) {   // 16 loads in flight per thread
-        double2 v[16];
+    constexpr int KL = 64 / kRpWarps;   // loads in flight per thread (16 at 4 warps)
+    for (int i0 = threadIdx.x; i0 < 128 * kV / 2; i0 += KL * blockDim.x) {
+        double2 v[KL];
 #pragma unroll
-        for (int k = 0; k < 16; ++k) {
+        for (int k = 0; k < KL; ++k) {
             const int i = i0 + k * blockDim.x;
             if (i < 128 * kV / 2) v[k] = __ldcg(reinterpret_cast<const double2*>(snap) + i);
         }
 #pragma unroll
-        for (int k = 0; k < 16; ++k) {
+        for (int k = 0; k < KL; ++k) {
             const int i = i0 + k * blockDim.x;
             if (i < 128 * kV / 2) reinterpret_cast<double2*>(s_u + (i / (kV / 2)) * kUS)[i % (kV / 2)] = v[k];
         }
@@ -3056,11 +3061,11 @@ __device__ __forceinline__ void rp_load(double* s_u, const double* snap) {
     __syncthreads();
 }
 
-__global__ void __launch_bounds__(128, 2) k_greedy_replay(const GreedyArgs a, const WgrpArgs x) {
+__global__ void __launch_bounds__(32 * kRpWarps, 2) k_greedy_replay(const GreedyArgs a, const WgrpArgs x) {
     // [128][kUS] u, then [Tpm] (row, device offset) step lists, [Tpm] rows and [Tpm] table indices of the steps
     extern __shared__ __align__(16) double s_u[];
     __shared__ int stk_item[64], stk_pos[64], stk_fork[64];   // DFS stack: item, step reached, its next fork
-    __shared__ int s_wcnt[4];
+    __shared__ int s_wcnt[kRpWarps];
     const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
     const unsigned n = __ldcg(x.p2_q + 3);   // families (hand-offs)
     unsigned long long rows = 0, reps = 0;   // ns_stats: rows replayed, representatives
@@ -3101,16 +3106,17 @@ __global__ void __launch_bounds__(128, 2) k_greedy_replay(const GreedyArgs a, co
             // 8 fg + q of device 32 wgi + 8 dgi + jd; a warp instruction covers one device's 32 features
             const double* up = x.uf_buf + (size_t)h.uf * kV * 128;
             const int q = lane & 7, fgl = lane >> 3;
-            for (int it0 = w; it0 < 256; it0 += 4 * 32) {   // 32 loads in flight per thread
-                double vv[32];
+            constexpr int KK = 128 / kRpWarps;   // loads in flight per thread
+            for (int it0 = w; it0 < 256; it0 += kRpWarps * KK) {
+                double vv[KK];
 #pragma unroll
-                for (int k = 0; k < 32; ++k) {
-                    const int it = it0 + 4 * k, d = it >> 1, fg = 4 * (it & 1) + fgl;
+                for (int k = 0; k < KK; ++k) {
+                    const int it = it0 + kRpWarps * k, d = it >> 1, fg = 4 * (it & 1) + fgl;
                     vv[k] = __ldcg(up + (size_t)((d & 7) * 8 + q) * 128 + (d & ~7) + fg);
                 }
 #pragma unroll
-                for (int k = 0; k < 32; ++k) {
-                    const int it = it0 + 4 * k, d = it >> 1, fg = 4 * (it & 1) + fgl;
+                for (int k = 0; k < KK; ++k) {
+                    const int it = it0 + kRpWarps * k, d = it >> 1, fg = 4 * (it & 1) + fgl;
                     s_u[d * kUS + 8 * fg + q] = vv[k];
                 }
             }
@@ -3830,7 +3836,7 @@ ns_status launch_greedy(ns_ctx* ctx, const SearchBufs& b, const ns_tables* t, lo
             if (rsm > 48 * 1024)
                 NS_CUDA(ctx, cudaFuncSetAttribute(k_greedy_replay, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rsm));
             k_rp_sort<<<1, 1024, 0, ctx->stream>>>(a2, x);
-            k_greedy_replay<<<(unsigned)b.rp_ctas, 128, rsm, ctx->stream>>>(a2, x);
+            k_greedy_replay<<<(unsigned)b.rp_ctas, 32 * kRpWarps, rsm, ctx->stream>>>(a2, x);
         }
         NS_LAUNCHED(ctx);   // p2, sort, replay (the caller counts wgrp88)
         NS_LAUNCHED(ctx);
