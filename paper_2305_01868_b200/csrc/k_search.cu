@@ -19,10 +19,13 @@
 #include "ns_internal.cuh"
 
 #ifndef NS_WGRP_CTAS
-#define NS_WGRP_CTAS 3   // resident CTAs per SM of k_greedy_wgrp88 (launch bounds and persistent grid; 168 registers with spills: +1% over 2 at 1024 C5 tasks)
+#define NS_WGRP_CTAS 4   // resident CTAs per SM of k_greedy_wgrp88 (launch bounds and persistent grid; 128 registers with spills: 2 -> 3 -> 4 each +1-2% at 1024-1536 C5 tasks, 5 slower)
 #endif
 #ifndef NS_MERGE_THREADS
 #define NS_MERGE_THREADS 256   // threads per column plan of k_merge_order (its rank-sort fallback included; 512: 2.04 vs 1.58 ms per step)
+#endif
+#ifndef NS_EXPAND_THREADS
+#define NS_EXPAND_THREADS 128   // threads per (task, beam) of k_expand (256: 3.08 vs 2.00 ms per 1536-task step)
 #endif
 #ifndef NS_EXPAND_COUNT_MAX
 #define NS_EXPAND_COUNT_MAX 256   // k_expand: lists up to this length select candidates by rank counting
@@ -4133,7 +4136,7 @@ ns_status run_search(ns_ctx* ctx, const ns_tables* t, int D, const ns_search_par
         if (esm > 48 * 1024)
             cudaFuncSetAttribute(k_expand, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)esm);
         prof_begin(ctx, PK_EXPAND);
-        k_expand<<<b.n_tasks * b.K, 256, esm, ctx->stream>>>(b, tv, level);
+        k_expand<<<b.n_tasks * b.K, NS_EXPAND_THREADS, esm, ctx->stream>>>(b, tv, level);
         prof_end(ctx);
         NS_LAUNCHED(ctx);
         launch_order(b.S, 0, level);
