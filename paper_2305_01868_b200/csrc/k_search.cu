@@ -24,6 +24,9 @@
 #ifndef NS_MERGE_THREADS
 #define NS_MERGE_THREADS 256   // threads per column plan of k_merge_order (its rank-sort fallback included; 512: 2.04 vs 1.58 ms per step)
 #endif
+#ifndef NS_SELECT_THREADS
+#define NS_SELECT_THREADS 256   // threads per task of k_select
+#endif
 #ifndef NS_EXPAND_THREADS
 #define NS_EXPAND_THREADS 128   // threads per (task, beam) of k_expand (256: 3.08 vs 2.00 ms per 1536-task step)
 #endif
@@ -4146,7 +4149,7 @@ ns_status run_search(ns_ctx* ctx, const ns_tables* t, int D, const ns_search_par
         const int staged = ssel + (size_t)C * b.M * 8 <= 160 * 1024 ? 1 : 0;
         if (staged) ssel += (size_t)C * b.M * 8;
         if (ssel > 40 * 1024) cudaFuncSetAttribute(k_select, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ssel);
-        k_select<<<b.n_tasks, 256, ssel, ctx->stream>>>(b, C, level, b.K, staged);
+        k_select<<<b.n_tasks, NS_SELECT_THREADS, ssel, ctx->stream>>>(b, C, level, b.K, staged);
         prof_end(ctx);
         NS_LAUNCHED(ctx);
     }
