@@ -35,6 +35,7 @@ struct PlanCostArgs {
     double start_scale, dim_scale;
     double inv_dim_scale;           // 1 / dim_scale when dim_scale is a power of two (exact), else 0
     int ldx, ldy;                   // smem row strides (doubles)
+    int ldy2;                       // large D: row stride of the per-warp layer-2 / layer-4 outputs
     uint32_t rflags;                // NS_R10_ABS_STARTS / NS_R11_SUM_OF_MAX
     const int32_t* list;            // optional: rows = list[i], i < *list_n (then row_begin = 0, row_end = capacity)
     const int32_t* list_n;
@@ -129,11 +130,28 @@ __global__ void __launch_bounds__(128, BIG ? 2 : NS_PC_BLOCKS) k_plan_cost_dmma(
     const int nrb = nwarps >> 1;
     const int per_warp = 16 * (ldx + ldh);
     const int per_rb = 16 * 2 * D + 32;
-    double* X = psm + (size_t)w * per_warp;  // [16][ldx]: input, layer-2 out (64), layer-4 out (16)
-    double* Hc = X + 16 * ldx;               // [16][ldh]: layer-1 chunk (32), layer-3 out (32)
-    double* O = psm + (size_t)nwarps * per_warp + (size_t)rb * per_rb;   // [16][2D]: fwd, bwd
-    double* mn = O + 16 * 2 * D;             // [16] min comp per row
-    long long* rid = (long long*)(mn + 16);
+    double *X, *Hc, *O, *mn, *Y;
+    long long* rid;
+    if constexpr (BIG) {
+        // one input tile per row block, read by both models (the bwd model
+        // masks its start inputs); per warp Hc and Y; the outputs O overlay
+        // the input tile after layer 1 -- 60 KB per CTA, 3 CTAs per SM
+        const size_t rbw = (size_t)16 * ldx + 2 * 16 * (ldh + a.ldy2) + 64;
+        X = psm + (size_t)rb * rbw;          // [16][ldx]: input, then O [16][2D]
+        Hc = X + 16 * ldx + (size_t)dir * 16 * (ldh + a.ldy2);   // [16][ldh]: layer-1 chunk, layer-3 out
+        Y = Hc + 16 * ldh;                   // [16][ldy2]: layer-2 out (64), layer-4 out (16)
+        O = X;
+        mn = X + 16 * ldx + 2 * 16 * (ldh + a.ldy2);
+        rid = (long long*)(mn + 16);
+    } else {
+        X = psm + (size_t)w * per_warp;      // [16][ldx]: input, layer-2 out (64), layer-4 out (16)
+        Hc = X + 16 * ldx;                   // [16][ldh]: layer-1 chunk (32), layer-3 out (32)
+        Y = X;
+        O = psm + (size_t)nwarps * per_warp + (size_t)rb * per_rb;   // [16][2D]: fwd, bwd
+        mn = O + 16 * 2 * D;                 // [16] min comp per row
+        rid = (long long*)(mn + 16);
+    }
+    const int ldyy = BIG ? a.ldy2 : ldx;     // row stride of Y
     const long long base = a.row_begin + ((long long)blockIdx.x * nrb + rb) * 16;
     const long long end = a.list ? a.row_begin + *a.list_n : a.row_end;
     const bool rows = base < end;
@@ -177,7 +195,7 @@ __global__ void __launch_bounds__(128, BIG ? 2 : NS_PC_BLOCKS) k_plan_cost_dmma(
             double v = 0.0;
             if (row >= 0 && c < K0) {
                 if (c < D) {
-                    v = dir == 0 ? (a.comp[row * D + c] - mn[r]) / a.start_scale : 0.0;
+                    v = (dir == 0 || BIG) ? (a.comp[row * D + c] - mn[r]) / a.start_scale : 0.0;
                 } else {
                     const double dd = (double)a.devdim[row * D + (c - D)];
                     v = a.inv_dim_scale != 0.0 ? dd * a.inv_dim_scale : dd / a.dim_scale;
@@ -185,9 +203,10 @@ __global__ void __launch_bounds__(128, BIG ? 2 : NS_PC_BLOCKS) k_plan_cost_dmma(
             }
             X[r * ldx + c] = v;
         };
-        if constexpr (BIG) {
-            for (int r = 0; r < 16; ++r)
+        if constexpr (BIG) {   // the shared tile: each warp builds 8 of its rows
+            for (int r = 8 * dir; r < 8 * dir + 8; ++r)
                 for (int c = lane; c < K0p; c += 32) input(r, c);
+            __syncthreads();   // (BIG: one row block per CTA, rows is CTA-uniform)
         } else {
             for (int i = lane; i < 16 * K0p; i += 32) input(i / K0p, i % K0p);
         }
@@ -213,7 +232,8 @@ __global__ void __launch_bounds__(128, BIG ? 2 : NS_PC_BLOCKS) k_plan_cost_dmma(
             // stream from L2 and a one-step loop exposes its latency per step)
             auto l1_step = [&](int kt) {
                 const int k = 4 * kt + t;
-                const double a0 = X[g * ldx + k], a1 = X[(8 + g) * ldx + k];
+                const bool zs = BIG && dir == 1 && k < D;   // bwd: start inputs are 0
+                const double a0 = zs ? 0.0 : X[g * ldx + k], a1 = zs ? 0.0 : X[(8 + g) * ldx + k];
 #pragma unroll
                 for (int q = 0; q < 4; ++q) {
                     const int n = hc * 32 + 8 * q + g;
@@ -267,14 +287,15 @@ __global__ void __launch_bounds__(128, BIG ? 2 : NS_PC_BLOCKS) k_plan_cost_dmma(
                     double2 yv;
                     yv.x = relu_exact(acc2[m][q][0] + c0);
                     yv.y = relu_exact(acc2[m][q][1] + c1);
-                    *reinterpret_cast<double2*>(X + (8 * m + g) * ldx + col) = yv;
+                    *reinterpret_cast<double2*>(Y + (8 * m + g) * ldyy + col) = yv;
                 }
             }
         }
         __syncwarp();
-        warp_layer<true, BIG>(a.cp.W[dir][2], a.cp.b[dir][2], 64, 32, X, ldx, Hc, ldh, lane);
-        warp_layer<true, BIG>(a.cp.W[dir][3], a.cp.b[dir][3], 32, 16, Hc, ldh, X, ldx, lane);
-        warp_layer<false, BIG>(a.cp.W[dir][4], a.cp.b[dir][4], 16, D, X, ldx, O + dir * D, 2 * D, lane);
+        if constexpr (BIG) __syncthreads();   // both models are done with the input tile O overlays
+        warp_layer<true, BIG>(a.cp.W[dir][2], a.cp.b[dir][2], 64, 32, Y, ldyy, Hc, ldh, lane);
+        warp_layer<true, BIG>(a.cp.W[dir][3], a.cp.b[dir][3], 32, 16, Hc, ldh, Y, ldyy, lane);
+        warp_layer<false, BIG>(a.cp.W[dir][4], a.cp.b[dir][4], 16, D, Y, ldyy, O + dir * D, 2 * D, lane);
     }
     __syncthreads();
     if (rows && dir == 0 && lane < 16) {
@@ -580,11 +601,16 @@ ns_status launch_plan_cost(ns_ctx* ctx, long long rb, long long re, const uint8_
     const int K0p = (2 * a.D + 3) & ~3;
     a.ldx = ld_pad(K0p > 64 ? K0p : 64);
     a.ldy = ld_pad(32);
+    a.ldy2 = ld_pad(64);
     const size_t per_warp = (size_t)16 * (a.ldx + a.ldy) * sizeof(double);
     const size_t per_rb = (size_t)(16 * 2 * a.D + 32) * sizeof(double);
     int wpb = 4;   // warps per CTA: two per 16-row block (fwd, bwd)
     while (wpb > 2 && per_warp * wpb + per_rb * (wpb / 2) > 72 * 1024) wpb >>= 1;
-    const size_t smem = per_warp * wpb + per_rb * (wpb / 2);
+    size_t smem = per_warp * wpb + per_rb * (wpb / 2);
+    if (a.D > 16) {   // large D: one row block per CTA with a shared input tile (k_plan_cost_dmma<true>)
+        wpb = 2;
+        smem = ((size_t)16 * a.ldx + 2 * 16 * (a.ldy + a.ldy2) + 64) * sizeof(double);
+    }
     if (a.D > 16)
         cudaFuncSetAttribute(k_plan_cost_dmma<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     else
