@@ -17,6 +17,7 @@
 #include <cuda_runtime.h>
 
 #include <cmath>
+#include <cstdlib>
 #include <math_constants.h>
 
 #include "ns_device.cuh"
@@ -345,6 +346,7 @@ struct PreDmmaArgs {
     int32_t* vdim;
     int64_t* vbytes;
     int ldx, ldy;
+    const int32_t* list;     // optional: rows r = list[1 + i], i < list[0] (valid deep variants only)
 };
 
 // One warp owns 16 rows.  The 128-wide hidden layer is produced in four
@@ -412,14 +414,15 @@ __global__ void __launch_bounds__(WSM ? 32 * NS_PRE_WSM_WARPS : 128, WSM ? 1 : N
     double* Hc = X + 16 * ldx;
     double* E = WSM ? Hc : Hc + 16 * ldh;
     long long* rowid = (long long*)(E + 16 * ldh);
-    for (long long base = ((long long)blockIdx.x * nwarps + w) * 16; base < a.n_rows;
+    const long long n_rows = a.list ? (long long)__ldg(a.list) : a.n_rows;
+    for (long long base = ((long long)blockIdx.x * nwarps + w) * 16; base < n_rows;
          base += (long long)gridDim.x * nwarps * 16) {
         // ---- features of the 16 rows (lane r < 16 owns row r); invalid variants -> zeros
         if (lane < 16) {
-            const long long r = base + lane;
+            const long long r = (a.list && base + lane < n_rows) ? (long long)__ldg(a.list + 1 + base + lane) : base + lane;
             double x[kF] = {0, 0, 0, 0, 0};
             long long row = -1;
-            if (r < a.n_rows) {
+            if (base + lane < n_rows) {
                 const long long gtab = r / a.nj;
                 const int j = a.jlo + (int)(r % a.nj);
                 const ns_table_desc td = a.desc[gtab];
@@ -627,6 +630,31 @@ ns_status launch_plan_cost(ns_ctx* ctx, long long rb, long long re, const uint8_
     return NS_OK;
 }
 
+// Deep variants (depth >= 1): only a table whose dims stay divisible by 8
+// can be halved j times (the dim % 8 rule of the candidates), so the
+// rows that cannot exist get vdim = 0 here and the DMMA kernel runs over the
+// compacted list of the others (about 2/5 of them for dims uniform in
+// multiples of 4).  Row order in the list does not matter: every row's
+// arithmetic is independent of its 16-row block.
+__global__ void k_pre_compact(const ns_table_desc* desc, long long n_rows, int jlo, int nj, int32_t* vdim,
+                              int32_t* list) {
+    for (long long r = (long long)blockIdx.x * blockDim.x + threadIdx.x; r < n_rows;
+         r += (long long)gridDim.x * blockDim.x) {
+        const long long g = r / nj;
+        const int j = jlo + (int)(r % nj);
+        int dim = desc[g].dim;
+        bool ok = true;
+        for (int k = 0; k < j; ++k) {
+            if (dim % 8 != 0) ok = false;
+            dim >>= 1;
+        }
+        if (ok)
+            list[1 + atomicAdd(list, 1)] = (int32_t)r;
+        else
+            vdim[g * kDepth + j] = 0;
+    }
+}
+
 void launch_precompute(ns_ctx* ctx, const ns_tables* t, int jlo, int jhi) {
     PreDmmaArgs a;
     a.desc = t->d_desc;
@@ -646,6 +674,14 @@ void launch_precompute(ns_ctx* ctx, const ns_tables* t, int jlo, int jhi) {
     a.vbytes = t->d_vbytes;
     a.ldx = ld_pad(8);    // x (8 features, zero padded)
     a.ldy = ld_pad(32);   // hidden chunk and e (32)
+    a.list = nullptr;
+    if (jlo >= 1 && t->d_plist && a.n_rows >= 16LL * 16 * ctx->sm_count && !getenv("NS_PRE_ALL_ROWS")) {
+        cudaMemsetAsync(t->d_plist, 0, sizeof(int32_t), ctx->stream);
+        const long long cb = std::min<long long>((a.n_rows + 255) / 256, (long long)ctx->sm_count * 16);
+        k_pre_compact<<<(unsigned)cb, 256, 0, ctx->stream>>>(a.desc, a.n_rows, a.jlo, a.nj, a.vdim, t->d_plist);
+        ctx->launches++;
+        a.list = t->d_plist;
+    }
     // batches stage the weights once per SM; a few hundred rows (a single
     // task) read them through L1 instead of paying the staging latency
     const bool wsm = a.n_rows >= 16LL * 16 * ctx->sm_count;

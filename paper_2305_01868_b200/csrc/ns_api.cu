@@ -528,6 +528,7 @@ ns_status ns_featurize_tables(ns_ctx* ctx, const ns_table_desc* tables, const in
     NS_TALLOC(t->d_C, rows * sizeof(double));
     NS_TALLOC(t->d_vdim, rows * sizeof(int32_t));
     NS_TALLOC(t->d_vbytes, rows * sizeof(int64_t));
+    NS_TALLOC(t->d_plist, (rows + 1) * sizeof(int32_t));
     NS_TALLOC(t->d_flag, sizeof(int32_t));
 #undef NS_TALLOC
     // small host arrays go through pinned staging so the copies stay async
@@ -571,7 +572,7 @@ ns_status ns_tables_free(ns_tables* t) {
     cudaStream_t st = t->ctx ? t->ctx->stream : nullptr;
     if (t->ctx) cudaSetDevice(t->ctx->device);
     void* ps[] = {t->d_off, t->d_cap, t->d_sumdim, t->d_desc, t->d_feat, t->d_V, t->d_C, t->d_vdim, t->d_vbytes,
-                  t->d_flag};
+                  t->d_flag, t->d_plist};
     for (void* p : ps)
         if (p) cudaFreeAsync(p, st);
     delete t;

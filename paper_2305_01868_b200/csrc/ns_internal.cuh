@@ -165,6 +165,7 @@ struct ns_tables {
     double* d_C = nullptr;      // [rows]      single-table cost C({t})
     int32_t* d_vdim = nullptr;  // [rows]      0 = invalid variant
     int64_t* d_vbytes = nullptr;// [rows]
+    int32_t* d_plist = nullptr; // [rows + 1] deep-variant precompute: count, then the valid rows
     bool deep_done = false;     // variants of depth >= 1 computed
 };
 
